@@ -1,0 +1,411 @@
+#!/usr/bin/env python
+"""Benchmark of the FastFormers encoder forward on B200 (BASELINE.json metric:
+sequences/sec at seq 128, int8 & fp16, 1/2/4/8 GPUs; GEMM tensor-pipe % of peak).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one process per GPU)
+
+A step = one full encoder forward (every row of DESIGN.md's hot-path table:
+embedding+LN, 6 x {QKV GEMM, attention, requant, O GEMM, add+LN, FFN1 GEMM,
+requant, FFN2 GEMM, add+LN}, pooler+classifier) over one synthetic batch of
+BASELINE configs[2] (pruned distilroberta shape, int8, B=256, S=128), replayed
+as a CUDA graph through the C ABI.  Multi-GPU: weak scaling -- every rank owns
+its own request batches, logits are gathered to rank 0 over NCCL each step.
+Timing: W warm-up steps, then K steps each bracketed by CUDA events on the
+launching stream with the L2 flushed (256 MiB memset) between steps; barrier
++ synchronize on both sides; max over ranks.  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured (MEASURED_PEAKS.json)"
+    return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c3", help="synth config name (c1..c5)")
+    ap.add_argument("--dtype", choices=["i8", "f16"], default="i8")
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--seq", type=int, default=None)
+    ap.add_argument("--no-variants", action="store_true", help="skip the fp16 side measurement")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload(args):
+    from paper_2010_13382_b200 import synth
+    cfg = synth.config(args.config).with_dtype(1 if args.dtype == "i8" else 0)
+    cfg = cfg.with_batch(args.batch or cfg.batch, args.seq or cfg.seq)
+    return cfg
+
+
+def config_json(cfg, args, n):
+    idx = {"c1": 0, "c2": 1, "c3": 2, "c4": 3, "c5": 4}.get(cfg.name)
+    return {"workload": f"BASELINE configs[{idx}] {cfg.name}: {cfg.num_layers}L H{cfg.hidden} heads{sorted(set(cfg.heads))} "
+                        f"FFN{sorted(set(cfg.ffn_dim))} {args.dtype}, random-init weights",
+            "batch_per_gpu": cfg.batch, "global_batch": cfg.batch * n, "seq_len": cfg.seq,
+            "parallelism": f"dp{n} (batch sharding, NCCL gather of logits)",
+            "l2": "flushed between timed steps (256 MiB memset), per-step CUDA events",
+            "inputs": "synthetic ids U[5,V) + CLS, all-ones mask (fixed seq), 4 rotating batches per rank"}
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock / throttle reasons during the timed region."""
+
+    def __init__(self, index: int, period: float = 0.01):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            names = {
+                "hw_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
+                "hw_thermal_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+                "sw_thermal_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+                "sw_power_cap": getattr(pynvml, "nvmlClocksThrottleReasonSwPowerCap", 0x4),
+                "hw_power_brake_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonHwPowerBrakeSlowdown", 0x80),
+            }
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                        for k, bit in names.items():
+                            if r & bit:
+                                self.reasons.add(k)
+                    except Exception:
+                        pass
+                    time.sleep(self.period)
+
+            self._t = threading.Thread(target=run, daemon=True)
+            self._t.start()
+        except Exception as e:  # NVML missing: record why
+            self.reasons.add(f"nvml_unavailable:{type(e).__name__}")
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------- cpu baseline
+def cpu_baseline(cfg, weights, ids, mask, n_seq=None):
+    """The oracle as it stands, multi-instance on the host cores (one
+    single-threaded instance per core, whole sequences)."""
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    n = n_seq or cores
+    orc = oracle.Oracle(cfg, weights)
+    done = []
+
+    def work(i):
+        j = i % ids.shape[0]
+        orc.encode(ids[j:j + 1], mask[j:j + 1])
+        done.append(i)
+
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(n)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    wall = time.perf_counter() - t0
+    return {"value": n / wall, "unit": "sequences/s", "cores": min(cores, n), "kind": "oracle",
+            "sample": f"{n} sequences of {cfg.name} (S={ids.shape[1]}, {'int8' if cfg.dtype[0] else 'fp16'} emulation),"
+                      f" one oracle instance per core, wall {wall:.1f} s"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    from paper_2010_13382_b200 import synth
+    import oracle
+    cfg = workload(args)
+    w = synth.make_weights(cfg)
+    ids, mask = synth.make_inputs(cfg, seed=1000)
+    cores = len(os.sched_getaffinity(0))
+    orc = oracle.Oracle(cfg, w)
+    # one sequence per core per step; bound the run to ~3 minutes of wall time
+    t0 = time.perf_counter()
+    orc.encode(ids[:1], mask[:1])
+    t1 = time.perf_counter() - t0
+    warm = min(args.warmup, 1)
+    steps = max(1, min(args.steps, int(170.0 / max(t1, 1e-3)) - warm))
+
+    def one_step(k):
+        ths = []
+        for i in range(cores):
+            j = (k * cores + i) % cfg.batch
+            ths.append(threading.Thread(target=orc.encode, args=(ids[j:j + 1], mask[j:j + 1])))
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+
+    for k in range(warm):
+        one_step(k)
+    t0 = time.perf_counter()
+    for k in range(steps):
+        one_step(k + warm)
+    wall = time.perf_counter() - t0
+    value = steps * cores / wall
+    unit = "sequences/s"
+    line = {"metric": "sequences/sec at seq 128 (int8 encoder forward, pruned distilroberta shape)", "value": value,
+            "unit": unit, "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": wall / steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8" if args.dtype == "i8" else "f16", "data": "synthetic (random-init weights, random ids)",
+            "config": config_json(cfg, args, 1), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "oracle",
+                             "sample": f"{cores} sequences per step (one oracle instance per core), {steps} steps"
+                                       f" (capped from --steps {args.steps} to fit ~3 min)"},
+            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ ours
+def kernel_bytes(kind, cfg, B, S):
+    """Algorithmic HBM bytes of one launch of an HBM-bound kernel kind (mean
+    over the layer's launches of that kind), DESIGN.md 'Roofline'."""
+    M, H, d = B * S, cfg.hidden, cfg.head_dim
+    A = sum(cfg.heads) / len(cfg.heads)
+    F = sum(cfg.ffn_dim) / len(cfg.ffn_dim)
+    D = A * d
+    q = cfg.dtype[0] == 1
+    if kind == "attention":
+        return M * 3 * D * 2 + M * 4 + M * D * 2
+    if kind == "add_ln":
+        return M * H * 2 * 2 + M * H * 2 + (M * H + M * 4 if q else 0) + 2 * H * 4
+    if kind == "quant_rows":
+        K = (D + F) / 2
+        return M * K * 2 + M * K + M * 4
+    if kind == "embed_ln":
+        return M * 8 + M * H * 4 * 2 + M * H * 2 + (M * H + M * 4 if q else 0)
+    return None
+
+
+def gemm_flops(cfg, B, S):
+    return cfg.gemm_flops_per_seq(S) * B
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2010_13382_b200 import synth
+    from paper_2010_13382_b200.fastformers import Encoder
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = workload(args)
+    B, S = cfg.batch, cfg.seq
+    w = synth.make_weights(cfg)
+    enc = Encoder(cfg, w, max_tokens=B * S, device=local)
+    NB = 4
+    batches = [synth.make_inputs(cfg, seed=1000 + rank * 10 ** 6 + k) for k in range(NB)]
+    dids = [torch.from_numpy(i).cuda() for i, _ in batches]
+    dmask = [torch.from_numpy(m).cuda() for _, m in batches]
+    logits = torch.empty((B, cfg.num_classes), dtype=torch.float32, device="cuda")
+    gather_list = [torch.empty_like(logits) for _ in range(world)] if (world > 1 and rank == 0) else None
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step(k):
+        enc.encode(dids[k % NB], dmask[k % NB], logits)
+        if world > 1:
+            dist.gather(logits, gather_list, dst=0)
+
+    for k in range(max(args.warmup, 3)):
+        step(k)
+    enc.check_inputs()
+    torch.cuda.synchronize()
+
+    # ---- per-kernel device times (CUDA events around each launch on the stream)
+    prof_runs = [enc.profile(dids[0], dmask[0]) for _ in range(3)]
+    by_kind = {}
+    for run in prof_runs:
+        for kind, ms in run:
+            by_kind.setdefault(kind, []).append(ms)
+    n_prof = len(prof_runs)
+    launches_per_step = enc.launch_count(B, S)
+
+    # ---- timed region
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for k in range(args.steps):
+        flush.zero_()
+        evs[k][0].record(stream)
+        step(args.warmup + k)
+        evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    t_ms = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_ms = float(t.item())
+    value = world * B * args.steps / (t_ms / 1e3)
+
+    # ---- end to end through the public API with host buffers (pinned)
+    h_ids = [torch.from_numpy(i).pin_memory() for i, _ in batches]
+    h_mask = [torch.from_numpy(m).pin_memory() for _, m in batches]
+    h_logits = torch.empty((B, cfg.num_classes), dtype=torch.float32).pin_memory()
+    e2e_steps = min(args.steps, 50)
+    for k in range(3):
+        enc.encode_host(h_ids[k % NB], h_mask[k % NB], h_logits)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for k in range(e2e_steps):
+        enc.encode_host(h_ids[k % NB], h_mask[k % NB], h_logits)
+        if world > 1:
+            dist.gather(logits, gather_list, dst=0)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * B * e2e_steps / float(te.item())
+
+    # ---- fp16 side measurement of the same geometry (metric names fp16 & int8)
+    variants = {}
+    if not args.no_variants and world == 1:
+        cfg16 = cfg.with_dtype(0)
+        enc16 = Encoder(cfg16, w, max_tokens=B * S, device=local)
+        for k in range(5):
+            enc16.encode(dids[k % NB], dmask[k % NB], logits)
+        torch.cuda.synchronize()
+        ev16 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(50)]
+        for k in range(50):
+            flush.zero_()
+            ev16[k][0].record(stream)
+            enc16.encode(dids[k % NB], dmask[k % NB], logits)
+            ev16[k][1].record(stream)
+        torch.cuda.synchronize()
+        t16 = sum(a.elapsed_time(b) for a, b in ev16)
+        p16 = enc16.profile(dids[0], dmask[0])
+        g16 = sum(ms for kd, ms in p16 if kd.startswith("gemm"))
+        peaks, _ = load_peaks()
+        variants["fp16"] = {"value": B * 50 / (t16 / 1e3), "unit": "sequences/s", "ms_per_step": t16 / 50,
+                            "gemm_tflops": gemm_flops(cfg16, B, S) / (g16 / 1e3) / 1e12,
+                            "gemm_frac_of_peak": gemm_flops(cfg16, B, S) / (g16 / 1e3) / 1e12 /
+                                                 peaks["bf16_tflops_sustained"]}
+        del enc16
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel class
+    peaks, peak_src = load_peaks()
+    step_prof_ms = {k: sum(v) / n_prof for k, v in by_kind.items()}
+    total_prof = sum(step_prof_ms.values())
+    dom = max(step_prof_ms, key=step_prof_ms.get)
+    kernels = {}
+    for kind, per_step in sorted(step_prof_ms.items(), key=lambda kv: -kv[1]):
+        n_launch = len(by_kind[kind]) // n_prof
+        ent = {"ms_per_step": per_step, "share": per_step / total_prof, "launches_per_step": n_launch,
+               "avg_launch_us": per_step / n_launch * 1e3}
+        if kind.startswith("gemm"):
+            ach = gemm_flops(cfg, B, S) / (per_step / 1e3) / 1e12
+            pk = peaks["bf16_tflops_sustained"] * (2.0 if kind == "gemm_i8" else 1.0)
+            ent.update({"achieved": ach, "unit": "TFLOP/s", "peak": pk, "frac": ach / pk})
+        else:
+            by = kernel_bytes(kind, cfg, B, S)
+            if by is not None:
+                ach = by / (per_step / n_launch / 1e3) / 1e9
+                ent.update({"achieved": ach, "unit": "GB/s", "peak": peaks["hbm_gbs"], "frac": ach / peaks["hbm_gbs"]})
+        kernels[kind] = ent
+    d = kernels[dom]
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        tj = json.load(open(tp))
+        key = f"{cfg.name}_{args.dtype}_{dom}"
+        if key in tj:
+            traffic = tj[key]
+    if dom.startswith("gemm"):
+        roof = {"bound": "tensor", "achieved": d["achieved"], "peak": d["peak"], "unit": "TFLOP/s",
+                "frac": d["frac"], "traffic": traffic, "kernel": dom,
+                "peak_source": f"{peak_src}: bf16 sustained x {'2 (int8/bf16 nominal ratio)' if dom == 'gemm_i8' else '1'}",
+                "algorithmic": f"{gemm_flops(cfg, B, S) / 1e9:.1f} G{'OP' if dom == 'gemm_i8' else 'FLOP'} per step over "
+                               f"{d['launches_per_step']} launches (DESIGN.md Roofline)"}
+    else:
+        roof = {"bound": "hbm", "achieved": d.get("achieved"), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": d.get("frac"), "traffic": traffic, "kernel": dom, "peak_source": peak_src}
+
+    line = {"metric": "sequences/sec at seq 128 (int8 encoder forward, pruned distilroberta shape)",
+            "value": value, "unit": "sequences/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int8" if args.dtype == "i8" else "f16", "data": "synthetic (random-init weights, random ids)",
+            "config": config_json(cfg, args, world),
+            "e2e": {"value": e2e_value, "unit": "sequences/s", "h2d_bytes_per_step": 2 * B * S * 4,
+                    "d2h_bytes_per_step": B * cfg.num_classes * 4,
+                    "how": "ff_encode_host: pinned host ids+mask -> device, forward, logits -> host, stream sync; wall clock"},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk, "roofline": roof, "kernels": kernels, "variants": variants}
+    if world == 1 and not args.no_cpu_baseline:
+        ids0, mask0 = batches[0]
+        line["cpu_baseline"] = cpu_baseline(cfg, w, ids0, mask0)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,203 @@
+/* include/fastformers.h -- C ABI of the B200-native FastFormers encoder forward.
+ *
+ * FastFormers (arXiv 2010.13382) = knowledge distillation + structured pruning
+ * + 8-bit / 16-bit numerics + runtime fusion for Transformer NLU inference.
+ * This library is the data-parallel hot path of that recipe: the batched
+ * forward pass of a distilled, structurally pruned post-LN BERT/RoBERTa
+ * encoder classifier (PAPER.md "P:n" lines cited below; DESIGN.md "R<k>" =
+ * reading k of the paper).  Each layer l keeps its own number of attention
+ * heads A'_l and FFN width F'_l ("re-group and reconnect the remaining
+ * heads and hidden states"), and runs its four constant-weight GEMMs either in
+ * fp16 ("all the model parameters are converted into 16-bit floating
+ * point") or as dynamically quantized int8 ("8-bit quantized matrix
+ * multiplication ... dynamic quantization", per-row activation / per-output
+ * channel weight scales, R6-R8).  Q.K^T and P.V always stay in floating point
+ * ("we do not use 8-bit matrix product for the Q, K inner product").
+ *
+ * No C++ or torch types cross this boundary: plain pointers and sizes only.
+ * Device pointers are marked d_, host pointers h_.  All device work is
+ * enqueued on the caller's CUDA stream (cudaStream_t passed as void*; NULL =
+ * legacy default stream).  Every call returns ff_status and sets a
+ * thread-local message readable with ff_last_error(); no exception crosses
+ * the ABI.  Compute runs only in the sm_100a kernels of this library; there
+ * is no CPU fallback (a missing GPU / wrong arch is FF_E_CUDA).
+ *
+ * Call order (anything else returns FF_E_STATE):
+ *   ff_model_create -> ff_model_memory -> (caller allocates two device
+ *   buffers) -> ff_bind_memory -> ff_load_weights x N -> ff_finalize ->
+ *   ff_encode* / ff_encode_host* (+ ff_check) -> ff_model_destroy.
+ *
+ * Ownership: the CALLER owns every device buffer (weight arena, workspace,
+ * ids, mask, logits).  The library owns host metadata, TMA tensor maps and
+ * CUDA-graph executables only; ff_model_destroy frees those.  Weights are
+ * immutable after ff_finalize.  Concurrent ff_encode calls on one model race
+ * on its workspace: use one model (one binding) per concurrent stream.
+ */
+#ifndef FASTFORMERS_H_
+#define FASTFORMERS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FF_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define FF_API __attribute__((visibility("default")))
+#else
+#define FF_API
+#endif
+
+typedef struct ff_model ff_model; /* opaque */
+
+typedef enum {
+  FF_OK = 0,
+  FF_E_INVALID = 1,     /* bad argument / config value                         */
+  FF_E_SHAPE = 2,       /* unknown tensor name, wrong shape, size over capacity */
+  FF_E_STATE = 3,       /* call out of order                                    */
+  FF_E_CUDA = 4,        /* CUDA runtime / driver error (message has details)    */
+  FF_E_INPUT = 5,       /* data-dependent input error seen on the device        */
+  FF_E_UNSUPPORTED = 6, /* valid but unsupported geometry                       */
+  FF_E_NOMEM = 7        /* caller-provided buffer too small                     */
+} ff_status;
+
+typedef enum { FF_F16 = 0, FF_I8 = 1 } ff_dtype;
+
+/* Activation of the FFN ("We replace GELU with ReLU"; R2): GELU with
+ * erf (HF "gelu", default), ReLU, or the tanh approximation. */
+typedef enum { FF_ACT_GELU = 0, FF_ACT_RELU = 1, FF_ACT_GELU_TANH = 2 } ff_act;
+
+typedef struct {
+  int32_t abi_version;   /* must be FF_ABI_VERSION                                      */
+  int32_t num_layers;    /* L >= 1                                                       */
+  int32_t hidden;        /* H, multiple of 8, <= 1024                                    */
+  int32_t head_dim;      /* d, even, 2..128 (same in every layer)                       */
+  int32_t vocab_size;    /* V                                                            */
+  int32_t max_positions; /* P: max sequence length S (position table rows)              */
+  int32_t num_classes;   /* C >= 1                                                       */
+  float ln_eps;          /* LayerNorm epsilon: 1e-12 BERT, 1e-5 RoBERTa (R3)            */
+  int32_t act;           /* ff_act                                                       */
+  const int32_t *heads;  /* [num_layers] surviving heads A'_l >= 1 (copied at create)   */
+  const int32_t *ffn_dim;/* [num_layers] surviving FFN width F'_l >= 1 (copied)         */
+  const int32_t *dtype;  /* [num_layers] ff_dtype of the layer's GEMMs (copied)         */
+  int32_t max_tokens;    /* capacity: largest B*S passed to ff_encode (workspace size)  */
+} ff_config;
+
+FF_API int32_t ff_abi_version(void);
+FF_API const char *ff_last_error(void);
+
+/* Validate cfg and build the host-side plan for CUDA device `cuda_device`
+ * (must be sm_100).  *out receives the model.  Errors: FF_E_INVALID,
+ * FF_E_UNSUPPORTED (geometry the kernels do not cover), FF_E_CUDA. */
+FF_API ff_status ff_model_create(const ff_config *cfg, int32_t cuda_device, ff_model **out);
+
+/* Bytes the caller must allocate on the device: the packed weight arena and
+ * the activation workspace (one layer's worth, reused across layers). */
+FF_API ff_status ff_model_memory(const ff_model *m, size_t *weight_bytes, size_t *workspace_bytes);
+
+/* Hand the library the two caller-owned device buffers (256-B aligned).  The
+ * weight arena is zero-filled here (on `stream`).  FF_E_NOMEM if too small. */
+FF_API ff_status ff_bind_memory(ff_model *m, void *d_weights, size_t weight_bytes, void *d_workspace,
+                         size_t workspace_bytes, void *stream);
+
+/* Load one fp32 host tensor by its HuggingFace state_dict name (optional
+ * "bert."/"roberta." prefix; RoBERTa head aliases classifier.dense.* ->
+ * pooler.dense.*, classifier.out_proj.* -> classifier.*).  Layout is PyTorch
+ * [out, in] row-major.  Weight packing happens here once, on the GPU (P:104
+ * "the result of the packing operation needs to be properly cached"): GEMM
+ * weights of fp16 layers are cast to fp16, those of int8 layers quantized per
+ * output channel (scale = amax/127, RNE, R7-R8); Q|K|V are concatenated
+ * (fused QKV).  The host buffer may be reused when the call returns (it
+ * synchronizes `stream`).  Errors: FF_E_SHAPE (unknown name / wrong shape),
+ * FF_E_STATE (before ff_bind_memory or after ff_finalize), FF_E_CUDA. */
+FF_API ff_status ff_load_weights(ff_model *m, const char *name, const float *h_data, const int64_t *shape,
+                          int32_t rank, void *stream);
+
+/* All tensors present -> fold the token-type-0 row into the position table
+ * (R16), build TMA tensor maps, mark READY.  FF_E_STATE lists what is missing. */
+FF_API ff_status ff_finalize(ff_model *m, void *stream);
+
+/* The hot path: logits[B, C] (fp32) = classifier(pooler(encoder(ids, mask))).
+ * d_token_ids, d_mask: [batch, seq] int32 row-major on the device; mask is
+ * 1 for real tokens, 0 for padding; keys with mask 0 are excluded from the
+ * softmax (R4) and mask[b, 0] must be 1 (R5).  d_logits: [batch, C] fp32.
+ * Asynchronous on `stream`.  Host-checkable errors return at once: seq >
+ * max_positions or batch*seq > max_tokens -> FF_E_SHAPE.  Ids outside [0, V),
+ * a mask value not in {0,1} or mask[b,0] != 1 set a sticky device flag that
+ * ff_check reports as FF_E_INPUT (the bad row's logits are unspecified).
+ * With graphs enabled (default) the launch sequence is captured once per
+ * (batch, seq, buffer addresses) and replayed. */
+FF_API ff_status ff_encode(ff_model *m, const int32_t *d_token_ids, const int32_t *d_mask, int32_t batch,
+                    int32_t seq, float *d_logits, void *stream);
+
+/* End-to-end form of ff_encode on HOST buffers: copies ids/mask host->device
+ * into the workspace, runs ff_encode, copies logits device->host and
+ * synchronizes `stream` (pinned host memory gives full copy bandwidth). */
+FF_API ff_status ff_encode_host(ff_model *m, const int32_t *h_token_ids, const int32_t *h_mask, int32_t batch,
+                         int32_t seq, float *h_logits, void *stream);
+
+/* Synchronize `stream`; FF_E_INPUT (and clear the flag) if an input error was
+ * flagged by an earlier ff_encode, else FF_OK. */
+FF_API ff_status ff_check(ff_model *m, void *stream);
+
+/* Options: FF_OPT_GRAPHS (1 = capture/replay CUDA graphs, default 1). */
+#define FF_OPT_GRAPHS 1
+FF_API ff_status ff_set_option(ff_model *m, int32_t option, int64_t value);
+
+FF_API void ff_model_destroy(ff_model *m);
+
+/* Number of kernels one ff_encode launches for (batch, seq). */
+FF_API ff_status ff_launch_count(const ff_model *m, int32_t batch, int32_t seq, int32_t *count);
+
+/* Kernel kinds reported by ff_profile. */
+typedef enum {
+  FF_K_EMBED_LN = 0, FF_K_GEMM_F16 = 1, FF_K_GEMM_I8 = 2, FF_K_ATTENTION = 3, FF_K_QUANT = 4,
+  FF_K_ADD_LN = 5, FF_K_HEAD = 6
+} ff_kernel_kind;
+
+/* Run one forward WITHOUT graphs with a CUDA-event pair around every kernel
+ * launch on `stream`, synchronize, and return per launch its kind and device
+ * duration in ms (capacity = size of the output arrays; *count = launches). */
+FF_API ff_status ff_profile(ff_model *m, const int32_t *d_token_ids, const int32_t *d_mask, int32_t batch,
+                            int32_t seq, float *d_logits, int32_t capacity, int32_t *kinds, float *ms,
+                            int32_t *count, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Test / lockstep exports (not part of the user contract).
+ * ------------------------------------------------------------------------ */
+
+/* Run ff_encode and additionally copy the fp16 stage tensors of layer
+ * `layer` into caller device buffers (each packed row-major, NULL = skip):
+ * d_dump[0] X16 input [M,H], [1] QKV16 [M,3D], [2] CTX16 [M,D], [3] O16 [M,H],
+ * [4] H1_16 [M,H], [5] I16 [M,F], [6] Y16 [M,H], [7] X16 output [M,H]
+ * (M = batch*seq, D = A'_l*d, F = F'_l).  Never uses graphs. */
+FF_API ff_status ff_encode_trace(ff_model *m, const int32_t *d_token_ids, const int32_t *d_mask, int32_t batch,
+                          int32_t seq, float *d_logits, int32_t layer, void *const *d_dump, void *stream);
+
+/* One GEMM through the production tcgen05 kernel: C[M,N] = A[M,K] W[N,K]^T.
+ * dtype FF_F16: A, W fp16 (row pitches lda, ldw in elements, 16-B aligned
+ * rows); dtype FF_I8: A, W int8.  out_mode 0: raw accumulators (int32 for i8,
+ * fp32 for f16) into d_C with pitch ldc; out_mode 1: production epilogue
+ * (i8: fma(float(acc), sx[m]*sw[n], bias[n]); f16: acc + bias[n]; then act
+ * (act < 0 = none); fp16 output).  d_bias/d_sx/d_sw may be NULL where unused. */
+FF_API ff_status ff_debug_gemm(int32_t dtype, const void *d_A, int32_t lda, const void *d_W, int32_t ldw, int32_t M,
+                        int32_t N, int32_t K, int32_t out_mode, void *d_C, int32_t ldc, const float *d_bias,
+                        const float *d_sx, const float *d_sw, int32_t act, void *stream);
+
+/* Per-row int8 quantization of an fp16 matrix (R6-R8): d_q [M, ldq] s8,
+ * d_s [M] fp32 scales. */
+FF_API ff_status ff_debug_quant_rows(const void *d_x16, int32_t M, int32_t K, int32_t ldx, int8_t *d_q, int32_t ldq,
+                              float *d_s, void *stream);
+
+/* Fused masked-softmax attention of one layer: qkv16 [B*S, 3*A*d] -> ctx16
+ * [B*S, A*d] (packed rows). */
+FF_API ff_status ff_debug_attention(const void *d_qkv16, const int32_t *d_mask, int32_t B, int32_t S, int32_t A,
+                             int32_t d, void *d_ctx16, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASTFORMERS_H_ */

@@ -1,0 +1,83 @@
+// ff_kernels.h -- internal launcher interface between the host plan (ff_api.cu)
+// and the sm_100a kernels.  Not part of the C ABI.
+#pragma once
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ff {
+
+constexpr int kNumSMs = 148;
+
+enum Act { ACT_NONE = -1, ACT_GELU = 0, ACT_RELU = 1, ACT_GELU_TANH = 2 };
+
+// ---------------------------------------------------------------- GEMM
+// C[M,N] = A[M,K] * W[N,K]^T on tcgen05 (kind::f16 or kind::i8), TMA-fed.
+struct GemmParams {
+  int M, N, K;
+  int m_tiles, n_tiles, k_blocks;
+  void* out;               // fp16 [M, ldo] (out_mode 1) or 32-bit raw [M, ldo] (out_mode 0)
+  int ldo;                 // elements
+  int out_mode;            // 0 raw accumulators, 1 production epilogue
+  const float* bias;       // [N] or null
+  const float* row_scale;  // sx [M] (i8)
+  const float* col_scale;  // sw [N] (i8)
+  int act;                 // Act
+};
+
+struct GemmPlan {
+  CUtensorMap tmA, tmB;
+  GemmParams p;
+  int bn;       // N tile (128 or 256)
+  int i8;       // 1 = kind::i8
+  int grid;
+};
+
+// Encode a 2-D K-major tensor map for a GEMM operand: rows x cols elements of
+// `elem_bytes` (2 fp16 / 1 int8), row pitch in bytes, box = box_rows x 128 B,
+// 128-byte swizzle, zero fill out of bounds.
+bool make_operand_map(CUtensorMap* map, const void* base, int rows, int cols, int elem_bytes, size_t pitch_bytes,
+                      int box_rows, const char** err);
+// Fill a GemmPlan (tile choice, maps, grid) for A [M_rows x K] (pitch lda
+// elements) and W [N x K] (pitch ldw); M_rows >= M is the buffer capacity.
+bool plan_gemm(GemmPlan* g, bool i8, const void* A, int M_rows, int lda, const void* W, int ldw, int N, int K,
+               const char** err);
+// Update the per-call fields (M) of a plan.
+void plan_gemm_set_m(GemmPlan* g, int M);
+cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t s);
+
+// ------------------------------------------------------------ row kernels
+// X = LN(E_tok[id] + Ppos'[t]) -> x16 [M, ldx] (+ optional s8 xq [M, ldq], xs [M]).
+// Validates ids / mask into *err_flag (sticky bits).
+cudaError_t launch_embed_ln(const int32_t* ids, const int32_t* mask, int B, int S, int H, int V,
+                            const float* tok, const float* pos, const float* g, const float* b, float eps,
+                            __half* x16, int ldx, int8_t* xq, int ldq, float* xs, int* err_flag, cudaStream_t s);
+// y = LN(a + r) -> y16 (+ optional s8 yq, ys).
+cudaError_t launch_add_ln(const __half* a, int lda, const __half* r, int ldr, int M, int H, const float* g,
+                          const float* b, float eps, __half* y16, int ldy, int8_t* yq, int ldq, float* ys,
+                          cudaStream_t s);
+// Per-row symmetric int8 quantization of fp16 rows.
+cudaError_t launch_quant_rows(const __half* x, int ldx, int M, int K, int8_t* q, int ldq, float* scale,
+                              cudaStream_t s);
+// pooled = tanh(Wp x0 + bp); logits = Wc pooled + bc, x0 = row b*S of x16.
+cudaError_t launch_head(const __half* x16, int ldx, int B, int S, int H, int C, const float* Wp, const float* bp,
+                        const float* Wc, const float* bc, float* logits, cudaStream_t s);
+
+// ------------------------------------------------------------- attention
+size_t attention_smem_bytes(int S, int d);
+cudaError_t launch_attention(const __half* qkv, int ldqkv, const int32_t* mask, int B, int S, int A, int d,
+                             __half* ctx, int ldctx, cudaStream_t s);
+
+// ------------------------------------------------------- weight packing
+cudaError_t launch_cast_f16(const float* src, int N, int K, __half* dst, int ldd, cudaStream_t s);
+cudaError_t launch_quant_weight(const float* src, int N, int K, int8_t* dst, int ldd, float* scale,
+                                cudaStream_t s);
+cudaError_t launch_add_row(const float* src, int N, int K, const float* row, float* dst, cudaStream_t s);
+
+// One-time cudaFuncSetAttribute calls (outside any stream capture).
+cudaError_t prepare_gemm_kernels();
+cudaError_t prepare_attention_kernels();
+cudaError_t prepare_row_kernels();
+
+}  // namespace ff

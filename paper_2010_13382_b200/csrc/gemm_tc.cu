@@ -1,0 +1,332 @@
+// gemm_tc.cu -- the four constant-weight GEMMs of every encoder layer
+// (fused QKV, out-proj, FFN1, FFN2) on the 5th-gen
+// tensor cores.
+//
+//   C[M,N] = A[M,K] * W[N,K]^T  (both operands K-major, PyTorch [out,in] W)
+//   fp16 layers: tcgen05.mma kind::f16, fp32 accumulate
+//   int8 layers: tcgen05.mma kind::i8,  s32 accumulate (exact)
+//
+// Persistent, warp-specialised kernel, one CTA per SM:
+//   warp 0     TMA producer: 128x128B A tile + BNx128B W tile per k-block into
+//              a STAGES-deep ring of 128B-swizzled smem tiles (mbarrier full/empty)
+//   warp 1     MMA issuer: one thread issues 4 x tcgen05.mma (K = 32 bytes each)
+//              per k-block into a double-buffered TMEM accumulator (2 x BN cols)
+//   warp 2     TMEM allocator
+//   warps 4-7  epilogue: tcgen05.ld 32x32b.x32 -> registers (each thread owns one
+//              output row), fused epilogue, fp16 stores; overlaps the next
+//              tile's mainloop through the second accumulator.
+// Epilogue (out_mode 1):
+//   fp16: y = acc + b[n]
+//   int8: y = fma(float(acc), sx[m]*sw[n], b[n])          (DESIGN R13, bit-exact)
+//   then optional activation (GELU-erf / ReLU / GELU-tanh) in fp32 and
+//   RNE to fp16.  out_mode 0 stores the raw 32-bit accumulators (tests).
+#include <cstdio>
+#include "ff_kernels.h"
+#include "ptx.cuh"
+
+namespace ff {
+
+constexpr int BM = 128;
+constexpr int BK_BYTES = 128;  // one 128-byte swizzle row of K per k-block
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int A_BYTES = BM * BK_BYTES;
+  static constexpr int B_BYTES = BN * BK_BYTES;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;  // barriers + 1 KB alignment slack
+  static constexpr uint32_t TMEM_COLS = 2 * BN;
+};
+
+// Instruction descriptor (kind::f16 / kind::i8), both operands K-major:
+// c_format [4,6) (1 = f32, 2 = s32), a_format [7,10), b_format [10,13)
+// (f16 = 0; s8 = 1), N>>3 at [17,23), M>>4 at [24,29).
+template <bool I8, int BN>
+__device__ __forceinline__ constexpr uint32_t make_idesc() {
+  return (I8 ? (2u << 4) : (1u << 4)) | (I8 ? (1u << 7) : 0u) | (I8 ? (1u << 10) : 0u) |
+         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ float apply_act(float y, int act) {
+  if (act == ACT_GELU) return 0.5f * y * (1.0f + erff(y * 0.70710678118654752f));
+  if (act == ACT_RELU) return fmaxf(y, 0.0f);
+  if (act == ACT_GELU_TANH) {
+    const float u = 0.7978845608028654f * (y + 0.044715f * y * y * y);
+    return 0.5f * y * (1.0f + tanhf(u));
+  }
+  return y;
+}
+
+template <int BN, bool I8>
+__global__ void __launch_bounds__(256, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_tiles = p.m_tiles * p.n_tiles;
+  constexpr int KE = I8 ? 128 : 64;  // elements per k-block
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * KE, mt * BM, kEvictNormal);
+          tma_load_2d(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * KE, nt * BN, kEvictLast);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc<I8, BN>();
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = make_sw128_desc(sA + stage * Cfg::A_BYTES);
+          const uint64_t bdesc = make_sw128_desc(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {  // 4 x 32 bytes of K; +2 = +32 B in the >>4 address field
+            if (I8)
+              mma_i8(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            else
+              mma_f16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          }
+          mma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp - 4;  // TMEM lane quadrant this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = mt * BM + q * 32 + lane;
+      const bool row_ok = row < p.M;
+      float sx = 0.0f;
+      if (I8 && p.out_mode == 1 && row_ok) sx = p.row_scale[row];
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, r);
+        tmem_wait_ld();
+        const int n0 = nt * BN + c;
+        if (!row_ok || n0 >= p.N) continue;
+        const int nvalid = min(32, p.N - n0);
+        if (p.out_mode == 0) {
+          uint32_t* o = reinterpret_cast<uint32_t*>(p.out) + (size_t)row * p.ldo + n0;
+          if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) *reinterpret_cast<uint4*>(o + j) = make_uint4(r[j], r[j + 1], r[j + 2], r[j + 3]);
+          } else {
+            for (int j = 0; j < nvalid; ++j) o[j] = r[j];
+          }
+          continue;
+        }
+        float y[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int n = n0 + j;
+          const float b = (p.bias && n < p.N) ? __ldg(p.bias + n) : 0.0f;
+          float v;
+          if (I8) {
+            const float sw = (n < p.N) ? __ldg(p.col_scale + n) : 0.0f;
+            v = __fmaf_rn(__int2float_rn(static_cast<int>(r[j])), __fmul_rn(sx, sw), b);
+          } else {
+            v = __fadd_rn(__uint_as_float(r[j]), b);
+          }
+          y[j] = apply_act(v, p.act);
+        }
+        __half* o = reinterpret_cast<__half*>(p.out) + (size_t)row * p.ldo + n0;
+        if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            uint4 v;
+            v.x = pack_half2(y[j], y[j + 1]);
+            v.y = pack_half2(y[j + 2], y[j + 3]);
+            v.z = pack_half2(y[j + 4], y[j + 5]);
+            v.w = pack_half2(y[j + 6], y[j + 7]);
+            *reinterpret_cast<uint4*>(o + j) = v;
+          }
+        } else {
+          for (int j = 0; j < nvalid; ++j) o[j] = __float2half_rn(y[j]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------- host
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode_fn() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(ptr);
+  }
+  return fn;
+}
+
+bool make_operand_map(CUtensorMap* map, const void* base, int rows, int cols, int elem_bytes, size_t pitch_bytes,
+                      int box_rows, const char** err) {
+  PFN_encodeTiled enc = get_encode_fn();
+  if (!enc) {
+    *err = "cuTensorMapEncodeTiled unavailable";
+    return false;
+  }
+  if ((pitch_bytes & 15) || (reinterpret_cast<uintptr_t>(base) & 15)) {
+    *err = "TMA operand needs 16-byte aligned base and row pitch";
+    return false;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)pitch_bytes};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / elem_bytes), (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    *err = "cuTensorMapEncodeTiled failed";
+    return false;
+  }
+  return true;
+}
+
+static int pick_bn(int N) {
+  // Fewer wasted columns wins; ties prefer the wider tile (less A re-reading).
+  const int w256 = ((N + 255) / 256) * 256 - N;
+  const int w128 = ((N + 127) / 128) * 128 - N;
+  return (w256 <= w128) ? 256 : 128;
+}
+
+bool plan_gemm(GemmPlan* g, bool i8, const void* A, int M_rows, int lda, const void* W, int ldw, int N, int K,
+               const char** err) {
+  const int eb = i8 ? 1 : 2;
+  g->i8 = i8 ? 1 : 0;
+  g->bn = pick_bn(N);
+  if (!make_operand_map(&g->tmA, A, M_rows, K, eb, (size_t)lda * eb, BM, err)) return false;
+  if (!make_operand_map(&g->tmB, W, N, K, eb, (size_t)ldw * eb, g->bn, err)) return false;
+  g->p.N = N;
+  g->p.K = K;
+  g->p.n_tiles = (N + g->bn - 1) / g->bn;
+  g->p.k_blocks = (K * eb + BK_BYTES - 1) / BK_BYTES;
+  g->p.out = nullptr;
+  g->p.ldo = 0;
+  g->p.out_mode = 1;
+  g->p.bias = g->p.row_scale = g->p.col_scale = nullptr;
+  g->p.act = ACT_NONE;
+  plan_gemm_set_m(g, M_rows);
+  return true;
+}
+
+void plan_gemm_set_m(GemmPlan* g, int M) {
+  g->p.M = M;
+  g->p.m_tiles = (M + BM - 1) / BM;
+  const int tiles = g->p.m_tiles * g->p.n_tiles;
+  g->grid = tiles < kNumSMs ? tiles : kNumSMs;
+}
+
+template <int BN, bool I8>
+static cudaError_t set_attr() {
+  return cudaFuncSetAttribute(gemm_tc_kernel<BN, I8>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::SMEM);
+}
+
+cudaError_t prepare_gemm_kernels() {
+  cudaError_t e;
+  if ((e = set_attr<256, true>()) != cudaSuccess) return e;
+  if ((e = set_attr<128, true>()) != cudaSuccess) return e;
+  if ((e = set_attr<256, false>()) != cudaSuccess) return e;
+  return set_attr<128, false>();
+}
+
+template <int BN, bool I8>
+static cudaError_t launch_t(const GemmPlan& g, cudaStream_t s) {
+  if (g.grid <= 0) return cudaSuccess;
+  gemm_tc_kernel<BN, I8><<<g.grid, 256, GemmCfg<BN>::SMEM, s>>>(g.tmA, g.tmB, g.p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t s) {
+  if (g.i8) return g.bn == 256 ? launch_t<256, true>(g, s) : launch_t<128, true>(g, s);
+  return g.bn == 256 ? launch_t<256, false>(g, s) : launch_t<128, false>(g, s);
+}
+
+}  // namespace ff

@@ -1,0 +1,336 @@
+// rowops.cu -- the HBM-bound row kernels of the encoder forward and the
+// one-time weight packing kernels.
+//
+//   embed_ln   X = LN(E_tok[id] + P'[t]) -> fp16 (+ s8 rows)
+//   add_ln     Y = LN(a + r) -> fp16 (+ s8 rows)   (post-LN residual, a6/a10)
+//   quant_rows (q, s) = Q8row(x16)                                (a4/a8)
+//   head       logits = Wc tanh(Wp x0 + bp) + bc                  (a11)
+//   cast_f16 / quant_weight / add_row: weight packing at load     (a0)
+//
+// Row kernels use one warp per row with the row held in registers (H <= 1024
+// -> <= 32 fp32 per lane) and warp-shuffle reductions; two-pass mean /
+// variance in fp32.  Q8row (DESIGN R6-R8): scale = amax/127 (IEEE division,
+// 1.0 for an all-zero row), q = clamp(RNE(x/scale), -127, 127), computed from
+// the fp16-ROUNDED value so that the result does not depend on where the
+// quantizer is fused (R12).  No fast-math anywhere in this file.
+#include "ff_kernels.h"
+#include "ptx.cuh"
+
+namespace ff {
+
+namespace {
+
+constexpr int kMaxChunks = 8;  // float4 chunks per lane: H <= 8*4*32 = 1024
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ int8_t quant1(float x, float s) {
+  float v = rintf(__fdiv_rn(x, s));  // rintf = round-half-to-even
+  v = fminf(fmaxf(v, -127.0f), 127.0f);
+  return static_cast<int8_t>(static_cast<int>(v));
+}
+
+// LayerNorm of a row held as v[c][0..3] at columns 4*(lane + 32*c) (< H), then
+// R16 store and optional Q8row.  All lanes of the warp participate.
+__device__ __forceinline__ void ln_store(float (&v)[kMaxChunks][4], int nch, int H, int lane, const float* g,
+                                         const float* b, float eps, __half* y16, int8_t* yq, float* ys) {
+  float s = 0.0f;
+#pragma unroll
+  for (int c = 0; c < kMaxChunks; ++c)
+    if (c < nch && 4 * (lane + 32 * c) < H) s += (v[c][0] + v[c][1]) + (v[c][2] + v[c][3]);
+  const float mean = __fdiv_rn(warp_sum(s), (float)H);
+  float q = 0.0f;
+#pragma unroll
+  for (int c = 0; c < kMaxChunks; ++c)
+    if (c < nch && 4 * (lane + 32 * c) < H) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float dlt = v[c][j] - mean;
+        q = __fmaf_rn(dlt, dlt, q);
+      }
+    }
+  const float var = __fdiv_rn(warp_sum(q), (float)H);
+  const float rstd = 1.0f / sqrtf(var + eps);
+  float amax = 0.0f;
+#pragma unroll
+  for (int c = 0; c < kMaxChunks; ++c) {
+    const int col = 4 * (lane + 32 * c);
+    if (c < nch && col < H) {
+      const float4 gg = *reinterpret_cast<const float4*>(g + col);
+      const float4 bb = *reinterpret_cast<const float4*>(b + col);
+      const float gv[4] = {gg.x, gg.y, gg.z, gg.w}, bv[4] = {bb.x, bb.y, bb.z, bb.w};
+      __half h[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        h[j] = __float2half_rn((v[c][j] - mean) * rstd * gv[j] + bv[j]);
+        v[c][j] = __half2float(h[j]);  // keep the fp16-rounded value for Q8row
+        amax = fmaxf(amax, fabsf(v[c][j]));
+      }
+      __half2 pk[2] = {__halves2half2(h[0], h[1]), __halves2half2(h[2], h[3])};
+      *reinterpret_cast<uint2*>(y16 + col) = *reinterpret_cast<uint2*>(pk);
+    }
+  }
+  if (yq == nullptr) return;
+  amax = warp_max(amax);
+  const float sc = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 127.0f);
+#pragma unroll
+  for (int c = 0; c < kMaxChunks; ++c) {
+    const int col = 4 * (lane + 32 * c);
+    if (c < nch && col < H) {
+      char4 qq;
+      qq.x = quant1(v[c][0], sc);
+      qq.y = quant1(v[c][1], sc);
+      qq.z = quant1(v[c][2], sc);
+      qq.w = quant1(v[c][3], sc);
+      *reinterpret_cast<char4*>(yq + col) = qq;
+    }
+  }
+  if (lane == 0) *ys = sc;
+}
+
+__global__ void __launch_bounds__(256) embed_ln_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ mask,
+                                                      int M, int S, int H, int V, const float* __restrict__ tok,
+                                                      const float* __restrict__ pos, const float* __restrict__ g,
+                                                      const float* __restrict__ b, float eps, __half* x16, int ldx,
+                                                      int8_t* xq, int ldq, float* xs, int* err_flag) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= M) return;
+  int id = ids[row];
+  const int t = row % S;
+  if (lane == 0) {
+    const int mk = mask[row];
+    int bad = 0;
+    if (id < 0 || id >= V) bad |= 1;
+    if (mk != 0 && mk != 1) bad |= 2;
+    if (t == 0 && mk != 1) bad |= 4;
+    if (bad) atomicOr(err_flag, bad);
+  }
+  if (id < 0 || id >= V) id = 0;  // keep the gather in bounds; the row is flagged
+  const float* e = tok + (size_t)id * H;
+  const float* p = pos + (size_t)t * H;
+  const int nch = (H + 127) / 128;
+  float v[kMaxChunks][4];
+#pragma unroll
+  for (int c = 0; c < kMaxChunks; ++c) {
+    const int col = 4 * (lane + 32 * c);
+    if (c < nch && col < H) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(e + col));
+      const float4 pp = __ldg(reinterpret_cast<const float4*>(p + col));
+      v[c][0] = __fadd_rn(a.x, pp.x);
+      v[c][1] = __fadd_rn(a.y, pp.y);
+      v[c][2] = __fadd_rn(a.z, pp.z);
+      v[c][3] = __fadd_rn(a.w, pp.w);
+    }
+  }
+  ln_store(v, nch, H, lane, g, b, eps, x16 + (size_t)row * ldx, xq ? xq + (size_t)row * ldq : nullptr,
+           xs ? xs + row : nullptr);
+}
+
+__global__ void __launch_bounds__(256) add_ln_kernel(const __half* __restrict__ a, int lda, const __half* __restrict__ r,
+                                                    int ldr, int M, int H, const float* __restrict__ g,
+                                                    const float* __restrict__ b, float eps, __half* y16, int ldy,
+                                                    int8_t* yq, int ldq, float* ys) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const int nch = (H + 127) / 128;
+  float v[kMaxChunks][4];
+  const __half* ar = a + (size_t)row * lda;
+  const __half* rr = r + (size_t)row * ldr;
+#pragma unroll
+  for (int c = 0; c < kMaxChunks; ++c) {
+    const int col = 4 * (lane + 32 * c);
+    if (c < nch && col < H) {
+      const uint2 ua = *reinterpret_cast<const uint2*>(ar + col);
+      const uint2 ur = *reinterpret_cast<const uint2*>(rr + col);
+      const __half2* ha = reinterpret_cast<const __half2*>(&ua);
+      const __half2* hr = reinterpret_cast<const __half2*>(&ur);
+      const float2 a0 = __half22float2(ha[0]), a1 = __half22float2(ha[1]);
+      const float2 r0 = __half22float2(hr[0]), r1 = __half22float2(hr[1]);
+      v[c][0] = __fadd_rn(a0.x, r0.x);
+      v[c][1] = __fadd_rn(a0.y, r0.y);
+      v[c][2] = __fadd_rn(a1.x, r1.x);
+      v[c][3] = __fadd_rn(a1.y, r1.y);
+    }
+  }
+  ln_store(v, nch, H, lane, g, b, eps, y16 + (size_t)row * ldy, yq ? yq + (size_t)row * ldq : nullptr,
+           ys ? ys + row : nullptr);
+}
+
+// One warp per row; any K (two passes over the row: absmax, then quantize).
+__global__ void __launch_bounds__(256) quant_rows_kernel(const __half* __restrict__ x, int ldx, int M, int K,
+                                                        int8_t* __restrict__ q, int ldq, float* __restrict__ scale) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const __half* xr = x + (size_t)row * ldx;
+  int8_t* qr = q + (size_t)row * ldq;
+  float amax = 0.0f;
+  const bool vec = ((K & 7) == 0) && ((reinterpret_cast<uintptr_t>(xr) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(qr) & 7) == 0);
+  if (vec) {
+    for (int c = lane * 8; c < K; c += 256) {
+      const uint4 u = *reinterpret_cast<const uint4*>(xr + c);
+      const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __half22float2(h[j]);
+        amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
+      }
+    }
+  } else {
+    for (int c = lane; c < K; c += 32) amax = fmaxf(amax, fabsf(__half2float(xr[c])));
+  }
+  amax = warp_max(amax);
+  const float sc = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 127.0f);
+  if (vec) {
+    for (int c = lane * 8; c < K; c += 256) {
+      const uint4 u = *reinterpret_cast<const uint4*>(xr + c);
+      const __half2* h = reinterpret_cast<const __half2*>(&u);
+      int8_t o[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __half22float2(h[j]);
+        o[2 * j] = quant1(f.x, sc);
+        o[2 * j + 1] = quant1(f.y, sc);
+      }
+      *reinterpret_cast<uint2*>(qr + c) = *reinterpret_cast<uint2*>(o);
+    }
+  } else {
+    for (int c = lane; c < K; c += 32) qr[c] = quant1(__half2float(xr[c]), sc);
+  }
+  if (lane == 0) scale[row] = sc;
+}
+
+// Pooler + classifier, fp32 (DESIGN R15).  One CTA per group of 16 sequences:
+// x0 rows staged in smem, each warp produces pooled[.][j] for its j's (lanes
+// over k, coalesced weight rows), then the C logits per sequence.
+constexpr int kHeadSeqs = 16;
+__global__ void __launch_bounds__(256) head_kernel(const __half* __restrict__ x16, int ldx, int B, int S, int H, int C,
+                                                  const float* __restrict__ Wp, const float* __restrict__ bp,
+                                                  const float* __restrict__ Wc, const float* __restrict__ bc,
+                                                  float* __restrict__ logits) {
+  extern __shared__ float hsm[];
+  float* xs = hsm;                     // [kHeadSeqs][H]
+  float* ps = hsm + kHeadSeqs * H;     // [kHeadSeqs][H]
+  const int b0 = blockIdx.x * kHeadSeqs;
+  const int nb = min(kHeadSeqs, B - b0);
+  for (int i = threadIdx.x; i < kHeadSeqs * H; i += blockDim.x) {
+    const int bb = i / H, k = i - bb * H;
+    xs[i] = bb < nb ? __half2float(x16[(size_t)(b0 + bb) * S * ldx + k]) : 0.0f;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int j = warp; j < H; j += nw) {
+    float acc[kHeadSeqs];
+#pragma unroll
+    for (int bb = 0; bb < kHeadSeqs; ++bb) acc[bb] = 0.0f;
+    for (int k = lane; k < H; k += 32) {
+      const float w = __ldg(Wp + (size_t)j * H + k);
+#pragma unroll
+      for (int bb = 0; bb < kHeadSeqs; ++bb) acc[bb] = __fmaf_rn(w, xs[bb * H + k], acc[bb]);
+    }
+#pragma unroll
+    for (int bb = 0; bb < kHeadSeqs; ++bb) {
+      const float sdot = warp_sum(acc[bb]);
+      if (lane == 0) ps[bb * H + j] = tanhf(sdot + bp[j]);
+    }
+  }
+  __syncthreads();
+  for (int t = warp; t < nb * C; t += nw) {
+    const int bb = t / C, c = t - bb * C;
+    float acc = 0.0f;
+    for (int k = lane; k < H; k += 32) acc = __fmaf_rn(__ldg(Wc + (size_t)c * H + k), ps[bb * H + k], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) logits[(size_t)(b0 + bb) * C + c] = acc + bc[c];
+  }
+}
+
+__global__ void cast_f16_kernel(const float* __restrict__ src, int N, int K, __half* __restrict__ dst, int ldd) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (size_t)N * K) return;
+  const int n = (int)(i / K), k = (int)(i - (size_t)n * K);
+  dst[(size_t)n * ldd + k] = __float2half_rn(src[i]);
+}
+
+// Per-output-channel symmetric int8 weights (R7-R8).
+__global__ void __launch_bounds__(256) quant_weight_kernel(const float* __restrict__ src, int N, int K,
+                                                          int8_t* __restrict__ dst, int ldd, float* __restrict__ scale) {
+  const int n = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (n >= N) return;
+  const float* w = src + (size_t)n * K;
+  float amax = 0.0f;
+  for (int k = lane; k < K; k += 32) amax = fmaxf(amax, fabsf(w[k]));
+  amax = warp_max(amax);
+  const float sc = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 127.0f);
+  for (int k = lane; k < K; k += 32) dst[(size_t)n * ldd + k] = quant1(w[k], sc);
+  if (lane == 0) scale[n] = sc;
+}
+
+__global__ void add_row_kernel(const float* __restrict__ src, int N, int K, const float* __restrict__ row,
+                               float* __restrict__ dst) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (size_t)N * K) return;
+  dst[i] = __fadd_rn(src[i], row[i % K]);
+}
+
+}  // namespace
+
+cudaError_t launch_embed_ln(const int32_t* ids, const int32_t* mask, int B, int S, int H, int V, const float* tok,
+                            const float* pos, const float* g, const float* b, float eps, __half* x16, int ldx,
+                            int8_t* xq, int ldq, float* xs, int* err_flag, cudaStream_t s) {
+  const int M = B * S;
+  embed_ln_kernel<<<(M + 7) / 8, 256, 0, s>>>(ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs,
+                                             err_flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_add_ln(const __half* a, int lda, const __half* r, int ldr, int M, int H, const float* g,
+                          const float* b, float eps, __half* y16, int ldy, int8_t* yq, int ldq, float* ys,
+                          cudaStream_t s) {
+  add_ln_kernel<<<(M + 7) / 8, 256, 0, s>>>(a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quant_rows(const __half* x, int ldx, int M, int K, int8_t* q, int ldq, float* scale,
+                              cudaStream_t s) {
+  quant_rows_kernel<<<(M + 7) / 8, 256, 0, s>>>(x, ldx, M, K, q, ldq, scale);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_head(const __half* x16, int ldx, int B, int S, int H, int C, const float* Wp, const float* bp,
+                        const float* Wc, const float* bc, float* logits, cudaStream_t s) {
+  const size_t smem = 2 * kHeadSeqs * H * sizeof(float);
+  head_kernel<<<(B + kHeadSeqs - 1) / kHeadSeqs, 256, smem, s>>>(x16, ldx, B, S, H, C, Wp, bp, Wc, bc, logits);
+  return cudaGetLastError();
+}
+
+cudaError_t prepare_row_kernels() {
+  return cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kHeadSeqs * 1024 * 4);
+}
+
+cudaError_t launch_cast_f16(const float* src, int N, int K, __half* dst, int ldd, cudaStream_t s) {
+  const size_t n = (size_t)N * K;
+  cast_f16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, N, K, dst, ldd);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quant_weight(const float* src, int N, int K, int8_t* dst, int ldd, float* scale, cudaStream_t s) {
+  quant_weight_kernel<<<(N + 7) / 8, 256, 0, s>>>(src, N, K, dst, ldd, scale);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_add_row(const float* src, int N, int K, const float* row, float* dst, cudaStream_t s) {
+  const size_t n = (size_t)N * K;
+  add_row_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, N, K, row, dst);
+  return cudaGetLastError();
+}
+
+}  // namespace ff

@@ -1,0 +1,235 @@
+"""Thin ctypes binding of the C ABI in include/fastformers.h.
+
+Argument marshalling only: every step of the forward pass runs in the sm_100a
+kernels of ``libfastformers.so``.  PyTorch is used for device memory (the two
+caller-owned arenas and the ids / mask / logits tensors) and streams.  If the
+library is missing or the device is not a B200 this module raises -- there is
+no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Dict, Optional
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libfastformers.so")
+
+FF_OK, FF_E_INVALID, FF_E_SHAPE, FF_E_STATE, FF_E_CUDA, FF_E_INPUT, FF_E_UNSUPPORTED, FF_E_NOMEM = range(8)
+FF_F16, FF_I8 = 0, 1
+FF_OPT_GRAPHS = 1
+KERNEL_KINDS = ["embed_ln", "gemm_f16", "gemm_i8", "attention", "quant_rows", "add_ln", "head"]
+STATUS_NAMES = ["FF_OK", "FF_E_INVALID", "FF_E_SHAPE", "FF_E_STATE", "FF_E_CUDA", "FF_E_INPUT", "FF_E_UNSUPPORTED",
+                "FF_E_NOMEM"]
+
+EXPORTED = ["ff_abi_version", "ff_last_error", "ff_model_create", "ff_model_memory", "ff_bind_memory",
+            "ff_load_weights", "ff_finalize", "ff_encode", "ff_encode_host", "ff_check", "ff_set_option",
+            "ff_model_destroy", "ff_launch_count", "ff_profile", "ff_encode_trace", "ff_debug_gemm", "ff_debug_quant_rows",
+            "ff_debug_attention"]
+
+
+class FFError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < 8 else status}: {msg}")
+        self.status = status
+
+
+class FFConfig(ctypes.Structure):
+    _fields_ = [("abi_version", ctypes.c_int32), ("num_layers", ctypes.c_int32), ("hidden", ctypes.c_int32),
+                ("head_dim", ctypes.c_int32), ("vocab_size", ctypes.c_int32), ("max_positions", ctypes.c_int32),
+                ("num_classes", ctypes.c_int32), ("ln_eps", ctypes.c_float), ("act", ctypes.c_int32),
+                ("heads", ctypes.POINTER(ctypes.c_int32)), ("ffn_dim", ctypes.POINTER(ctypes.c_int32)),
+                ("dtype", ctypes.POINTER(ctypes.c_int32)), ("max_tokens", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libfastformers.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise FFError(FF_E_CUDA, f"{LIB_PATH} not built; run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_size_t
+        L.ff_abi_version.restype = i32
+        L.ff_last_error.restype = ctypes.c_char_p
+        L.ff_model_create.argtypes = [ctypes.POINTER(FFConfig), i32, ctypes.POINTER(vp)]
+        L.ff_model_memory.argtypes = [vp, ctypes.POINTER(sz), ctypes.POINTER(sz)]
+        L.ff_bind_memory.argtypes = [vp, vp, sz, vp, sz, vp]
+        L.ff_load_weights.argtypes = [vp, ctypes.c_char_p, vp, ctypes.POINTER(ctypes.c_int64), i32, vp]
+        L.ff_finalize.argtypes = [vp, vp]
+        L.ff_encode.argtypes = [vp, vp, vp, i32, i32, vp, vp]
+        L.ff_encode_host.argtypes = [vp, vp, vp, i32, i32, vp, vp]
+        L.ff_check.argtypes = [vp, vp]
+        L.ff_set_option.argtypes = [vp, i32, ctypes.c_int64]
+        L.ff_model_destroy.argtypes = [vp]
+        L.ff_model_destroy.restype = None
+        L.ff_launch_count.argtypes = [vp, i32, i32, ctypes.POINTER(i32)]
+        L.ff_profile.argtypes = [vp, vp, vp, i32, i32, vp, i32, vp, vp, ctypes.POINTER(i32), vp]
+        L.ff_encode_trace.argtypes = [vp, vp, vp, i32, i32, vp, i32, ctypes.POINTER(vp), vp]
+        L.ff_debug_gemm.argtypes = [i32, vp, i32, vp, i32, i32, i32, i32, i32, vp, i32, vp, vp, vp, i32, vp]
+        L.ff_debug_quant_rows.argtypes = [vp, i32, i32, i32, vp, i32, vp, vp]
+        L.ff_debug_attention.argtypes = [vp, vp, i32, i32, i32, i32, vp, vp]
+        for name in EXPORTED:
+            if name not in ("ff_abi_version", "ff_last_error", "ff_model_destroy"):
+                getattr(L, name).restype = i32
+        _lib = L
+    return _lib
+
+
+def check(status: int):
+    if status != FF_OK:
+        raise FFError(status, lib().ff_last_error().decode(errors="replace"))
+
+
+def _stream_ptr(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Encoder:
+    """One FastFormers encoder model on one GPU (weights packed once at load)."""
+
+    def __init__(self, cfg, weights: Dict[str, np.ndarray], max_tokens: Optional[int] = None, device: int = 0,
+                 use_graphs: bool = True):
+        import torch
+        L = lib()
+        self.cfg = cfg
+        self.device = torch.device("cuda", device)
+        self._heads = (ctypes.c_int32 * cfg.num_layers)(*cfg.heads)
+        self._ffn = (ctypes.c_int32 * cfg.num_layers)(*cfg.ffn_dim)
+        self._dt = (ctypes.c_int32 * cfg.num_layers)(*cfg.dtype)
+        self.max_tokens = int(max_tokens or cfg.batch * cfg.seq)
+        c = FFConfig(1, cfg.num_layers, cfg.hidden, cfg.head_dim, cfg.vocab_size, cfg.max_positions,
+                     cfg.num_classes, float(cfg.ln_eps), int(cfg.act), self._heads, self._ffn, self._dt,
+                     self.max_tokens)
+        h = ctypes.c_void_p()
+        check(L.ff_model_create(ctypes.byref(c), device, ctypes.byref(h)))
+        self.h = h
+        wb, wsb = ctypes.c_size_t(), ctypes.c_size_t()
+        check(L.ff_model_memory(self.h, ctypes.byref(wb), ctypes.byref(wsb)))
+        with torch.cuda.device(self.device):
+            self.weight_arena = torch.empty(wb.value, dtype=torch.uint8, device=self.device)
+            self.workspace = torch.empty(wsb.value, dtype=torch.uint8, device=self.device)
+            st = _stream_ptr()
+            check(L.ff_bind_memory(self.h, _ptr(self.weight_arena), wb.value, _ptr(self.workspace), wsb.value, st))
+            for name, w in weights.items():
+                a = np.ascontiguousarray(w, dtype=np.float32)
+                shape = (ctypes.c_int64 * a.ndim)(*a.shape)
+                check(L.ff_load_weights(self.h, name.encode(), ctypes.c_void_p(a.ctypes.data), shape, a.ndim, st))
+            check(L.ff_finalize(self.h, st))
+        if not use_graphs:
+            check(L.ff_set_option(self.h, FF_OPT_GRAPHS, 0))
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and _lib is not None:
+            _lib.ff_model_destroy(h)
+            self.h = None
+
+    def encode(self, ids, mask, logits=None, stream=None):
+        """ids, mask: int32 [B, S] CUDA tensors -> logits fp32 [B, C] (async on the stream)."""
+        import torch
+        B, S = ids.shape
+        assert ids.dtype == torch.int32 and mask.dtype == torch.int32 and ids.is_contiguous() and mask.is_contiguous()
+        if logits is None:
+            logits = torch.empty((B, self.cfg.num_classes), dtype=torch.float32, device=ids.device)
+        check(lib().ff_encode(self.h, _ptr(ids), _ptr(mask), B, S, _ptr(logits), _stream_ptr(stream)))
+        return logits
+
+    def encode_host(self, ids, mask, logits=None, stream=None):
+        """End-to-end: host (ideally pinned) int32 ids / mask -> host fp32 logits."""
+        import torch
+        B, S = ids.shape
+        if logits is None:
+            logits = torch.empty((B, self.cfg.num_classes), dtype=torch.float32).pin_memory()
+        check(lib().ff_encode_host(self.h, _ptr(ids), _ptr(mask), B, S, _ptr(logits), _stream_ptr(stream)))
+        return logits
+
+    def check_inputs(self, stream=None):
+        check(lib().ff_check(self.h, _stream_ptr(stream)))
+
+    def launch_count(self, B, S):
+        n = ctypes.c_int32()
+        check(lib().ff_launch_count(self.h, B, S, ctypes.byref(n)))
+        return n.value
+
+    def profile(self, ids, mask, logits=None, stream=None):
+        """One un-graphed forward with CUDA events around every launch.
+        Returns a list of (kind, ms) with kind in KERNEL_KINDS."""
+        import torch
+        B, S = ids.shape
+        if logits is None:
+            logits = torch.empty((B, self.cfg.num_classes), dtype=torch.float32, device=ids.device)
+        cap = 4096
+        kinds = (ctypes.c_int32 * cap)()
+        ms = (ctypes.c_float * cap)()
+        n = ctypes.c_int32()
+        check(lib().ff_profile(self.h, _ptr(ids), _ptr(mask), B, S, _ptr(logits), cap, ctypes.cast(kinds, ctypes.c_void_p),
+                               ctypes.cast(ms, ctypes.c_void_p), ctypes.byref(n), _stream_ptr(stream)))
+        return [(KERNEL_KINDS[kinds[i]], ms[i]) for i in range(n.value)]
+
+    def trace(self, ids, mask, layer: int):
+        """Run the forward and return layer `layer`'s fp16 stage tensors (packed, on device)."""
+        import torch
+        cfg = self.cfg
+        B, S = ids.shape
+        M, H = B * S, cfg.hidden
+        D, F = cfg.heads[layer] * cfg.head_dim, cfg.ffn_dim[layer]
+        names = ["x_in", "qkv", "ctx", "o", "h1", "i", "y", "x_out"]
+        cols = [H, 3 * D, D, H, H, F, H, H]
+        bufs = [torch.empty((M, c), dtype=torch.float16, device=ids.device) for c in cols]
+        ptrs = (ctypes.c_void_p * 8)(*[b.data_ptr() for b in bufs])
+        logits = torch.empty((B, cfg.num_classes), dtype=torch.float32, device=ids.device)
+        check(lib().ff_encode_trace(self.h, _ptr(ids), _ptr(mask), B, S, _ptr(logits), layer, ptrs, _stream_ptr()))
+        out = dict(zip(names, bufs))
+        out["logits"] = logits
+        return out
+
+
+# ------------------------------------------------------------ debug entry points
+def gemm(A, W, out_mode=0, bias=None, sx=None, sw=None, act=-1, out=None):
+    """C = A W^T through the production tcgen05 kernel.  A [M,K], W [N,K]: both
+    int8 (kind::i8) or both fp16 (kind::f16) CUDA tensors with 16-byte aligned rows."""
+    import torch
+    M, K = A.shape
+    N = W.shape[0]
+    i8 = A.dtype == torch.int8
+    if out is None:
+        if out_mode == 0:
+            out = torch.empty((M, N), dtype=torch.int32 if i8 else torch.float32, device=A.device)
+        else:
+            out = torch.empty((M, N), dtype=torch.float16, device=A.device)
+    nul = ctypes.c_void_p(None)
+    check(lib().ff_debug_gemm(FF_I8 if i8 else FF_F16, _ptr(A), A.stride(0), _ptr(W), W.stride(0), M, N, K, out_mode,
+                              _ptr(out), out.stride(0), _ptr(bias) if bias is not None else nul,
+                              _ptr(sx) if sx is not None else nul, _ptr(sw) if sw is not None else nul, act,
+                              _stream_ptr()))
+    return out
+
+
+def quant_rows(x16):
+    import torch
+    M, K = x16.shape
+    ldq = (K + 15) // 16 * 16
+    q = torch.empty((M, ldq), dtype=torch.int8, device=x16.device)
+    s = torch.empty(M, dtype=torch.float32, device=x16.device)
+    check(lib().ff_debug_quant_rows(_ptr(x16), M, K, x16.stride(0), _ptr(q), ldq, _ptr(s), _stream_ptr()))
+    return q[:, :K], s
+
+
+def attention(qkv16, mask, A, d):
+    import torch
+    B, S = mask.shape
+    ctx = torch.empty((B * S, A * d), dtype=torch.float16, device=qkv16.device)
+    check(lib().ff_debug_attention(_ptr(qkv16), _ptr(mask), B, S, A, d, _ptr(ctx), _stream_ptr()))
+    return ctx
