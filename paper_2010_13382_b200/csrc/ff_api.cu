@@ -79,7 +79,7 @@ struct ff_model {
   // workspace pitches (elements) and offsets
   int ldx16, ldx8, ldqkv, ldc16, ldc8, ldi16, ldi8;
   size_t ws_x16, ws_xq, ws_xs, ws_qkv, ws_ctx, ws_ctxq, ws_ctxs, ws_o, ws_h1, ws_h1q, ws_h1s, ws_i, ws_iq, ws_is;
-  size_t ws_err, ws_ids, ws_mask, ws_logits;
+  size_t ws_err, ws_ids, ws_mask, ws_logits, ws_pooled;
   size_t wsbytes = 0;
   uint8_t* dW = nullptr;
   uint8_t* dWS = nullptr;
@@ -182,6 +182,7 @@ void plan_memory(ff_model* m) {
   m->ws_ids = a.take(M * 4);
   m->ws_mask = a.take(M * 4);
   m->ws_logits = a.take(M * c.num_classes * 4);
+  m->ws_pooled = a.take(M * H * 4);  // pooler output [B <= max_tokens, H] fp32
   m->wsbytes = align_up(a.off, 256);
 }
 
@@ -206,6 +207,16 @@ ff_status build_gemm_plans(ff_model* m) {
       if (!ff::plan_gemm(&P.gp[i], P.dt == FF_I8, A, m->cfg.max_tokens, lda, m->dW + P.w[i], P.ldw[i], P.N[i],
                          P.K[i], &err))
         return fail(FF_E_CUDA, std::string("tensor map: ") + err);
+      void* out = nullptr;
+      int ldo = 0;
+      switch (i) {
+        case W_QKV: out = m->dWS + m->ws_qkv; ldo = m->ldqkv; break;
+        case W_O: out = m->dWS + m->ws_o; ldo = m->ldx16; break;
+        case W_FFN1: out = m->dWS + m->ws_i; ldo = m->ldi16; break;
+        default: out = m->dWS + m->ws_o; ldo = m->ldx16; break;
+      }
+      if (!ff::plan_gemm_output(&P.gp[i], out, ldo, &err))
+        return fail(FF_E_CUDA, std::string("output tensor map: ") + err);
     }
   }
   return FF_OK;
@@ -342,7 +353,7 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
   }
   // a11: pooler + classifier
   FF_LAUNCH(FF_K_HEAD, ff::launch_head(X16, m->ldx16, B, S, H, c.num_classes, m->w<float>(m->pool_w), m->w<float>(m->pool_b),
-                            m->w<float>(m->cls_w), m->w<float>(m->cls_b), logits, s),
+                            m->w<float>(m->cls_w), m->w<float>(m->cls_b), m->ws<float>(m->ws_pooled), logits, s),
             "head");
   return FF_OK;
 }
@@ -656,7 +667,7 @@ ff_status ff_launch_count(const ff_model* m, int32_t batch, int32_t seq, int32_t
   if (!m || !count) return fail(FF_E_INVALID, "null argument");
   (void)batch;
   (void)seq;
-  int n = 2;  // embed_ln + head
+  int n = 3;  // embed_ln + pooler + classifier
   for (const LayerPlan& P : m->L) n += 7 + (P.dt == FF_I8 ? 2 : 0);
   *count = n;
   return FF_OK;
@@ -706,8 +717,12 @@ ff_status ff_debug_gemm(int32_t dtype, const void* d_A, int32_t lda, const void*
   const char* err = nullptr;
   if (!ff::plan_gemm(&g, dtype == FF_I8, d_A, M, lda, d_W, ldw, N, K, &err))
     return fail(FF_E_INVALID, std::string("gemm plan: ") + err);
-  g.p.out = d_C;
-  g.p.ldo = ldc;
+  if (out_mode == 1) {
+    if (!ff::plan_gemm_output(&g, d_C, ldc, &err)) return fail(FF_E_INVALID, std::string("gemm output: ") + err);
+  } else {
+    g.p.out = d_C;
+    g.p.ldo = ldc;
+  }
   g.p.out_mode = out_mode;
   g.p.bias = d_bias;
   g.p.row_scale = d_sx;

@@ -27,11 +27,13 @@ struct GemmParams {
 };
 
 struct GemmPlan {
-  CUtensorMap tmA, tmB;
+  CUtensorMap tmA, tmB, tmC;  // A, W operands (128B swizzle); fp16 output (64B swizzle, 32x32 boxes)
   GemmParams p;
   int bn;       // N tile (128 or 256)
   int i8;       // 1 = kind::i8
   int grid;
+  int M_rows;   // row capacity of A / the output buffer
+  bool has_out_map;
 };
 
 // Encode a 2-D K-major tensor map for a GEMM operand: rows x cols elements of
@@ -43,6 +45,8 @@ bool make_operand_map(CUtensorMap* map, const void* base, int rows, int cols, in
 // elements) and W [N x K] (pitch ldw); M_rows >= M is the buffer capacity.
 bool plan_gemm(GemmPlan* g, bool i8, const void* A, int M_rows, int lda, const void* W, int ldw, int N, int K,
                const char** err);
+// Bind the fp16 output buffer [M_rows x N] (pitch ldo elements) of a plan.
+bool plan_gemm_output(GemmPlan* g, void* out, int ldo, const char** err);
 // Update the per-call fields (M) of a plan.
 void plan_gemm_set_m(GemmPlan* g, int M);
 cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t s);
@@ -62,7 +66,7 @@ cudaError_t launch_quant_rows(const __half* x, int ldx, int M, int K, int8_t* q,
                               cudaStream_t s);
 // pooled = tanh(Wp x0 + bp); logits = Wc pooled + bc, x0 = row b*S of x16.
 cudaError_t launch_head(const __half* x16, int ldx, int B, int S, int H, int C, const float* Wp, const float* bp,
-                        const float* Wc, const float* bc, float* logits, cudaStream_t s);
+                        const float* Wc, const float* bc, float* pooled, float* logits, cudaStream_t s);
 
 // ------------------------------------------------------------- attention
 size_t attention_smem_bytes(int S, int d);

@@ -6,20 +6,23 @@
 //   fp16 layers: tcgen05.mma kind::f16, fp32 accumulate
 //   int8 layers: tcgen05.mma kind::i8,  s32 accumulate (exact)
 //
-// Persistent, warp-specialised kernel, one CTA per SM:
-//   warp 0     TMA producer: 128x128B A tile + BNx128B W tile per k-block into
-//              a STAGES-deep ring of 128B-swizzled smem tiles (mbarrier full/empty)
-//   warp 1     MMA issuer: one thread issues 4 x tcgen05.mma (K = 32 bytes each)
-//              per k-block into a double-buffered TMEM accumulator (2 x BN cols)
-//   warp 2     TMEM allocator
-//   warps 4-7  epilogue: tcgen05.ld 32x32b.x32 -> registers (each thread owns one
-//              output row), fused epilogue, fp16 stores; overlaps the next
-//              tile's mainloop through the second accumulator.
+// Persistent, warp-specialised kernel, one CTA per SM, 384 threads:
+//   warp 0      TMA producer: 128x128B A tile + BNx128B W tile per k-block into
+//               a STAGES-deep ring of 128B-swizzled smem tiles (mbarrier full/empty)
+//   warp 1      MMA issuer: one thread issues 4 x tcgen05.mma (K = 32 bytes each)
+//               per k-block into a double-buffered TMEM accumulator (2 x BN cols)
+//   warp 2      TMEM allocator
+//   warps 4-11  epilogue: warp w drains TMEM lane quadrant w%4, column half
+//               (w-4)/4, with tcgen05.ld 32x32b.x32 (thread = output row),
+//               applies the fused epilogue in fp32, writes fp16 into a 64B-
+//               swizzled smem staging tile and issues a TMA bulk-tensor store
+//               per 32x32 block; overlaps the next tile's mainloop through the
+//               second accumulator.
 // Epilogue (out_mode 1):
 //   fp16: y = acc + b[n]
 //   int8: y = fma(float(acc), sx[m]*sw[n], b[n])          (DESIGN R13, bit-exact)
 //   then optional activation (GELU-erf / ReLU / GELU-tanh) in fp32 and
-//   RNE to fp16.  out_mode 0 stores the raw 32-bit accumulators (tests).
+//   RNE to fp16.  out_mode 0 stores the raw 32-bit accumulators (tests only).
 #include <cstdio>
 #include "ff_kernels.h"
 #include "ptx.cuh"
@@ -28,6 +31,9 @@ namespace ff {
 
 constexpr int BM = 128;
 constexpr int BK_BYTES = 128;  // one 128-byte swizzle row of K per k-block
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 128 + 32 * kEpiWarps;
+constexpr int kStageTile = 32 * 64;  // 32 rows x 32 fp16 staging block (2 KB)
 
 template <int BN>
 struct GemmCfg {
@@ -35,9 +41,11 @@ struct GemmCfg {
   static constexpr int A_BYTES = BM * BK_BYTES;
   static constexpr int B_BYTES = BN * BK_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int EPI_OFF = STAGES * STAGE_BYTES;
+  static constexpr int BAR_OFF = EPI_OFF + kEpiWarps * 2 * kStageTile;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;  // barriers + 1 KB alignment slack
   static constexpr uint32_t TMEM_COLS = 2 * BN;
+  static_assert(SMEM <= 227 * 1024, "smem budget");
 };
 
 // Instruction descriptor (kind::f16 / kind::i8), both operands K-major:
@@ -49,25 +57,74 @@ __device__ __forceinline__ constexpr uint32_t make_idesc() {
          ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
-__device__ __forceinline__ float apply_act(float y, int act) {
-  if (act == ACT_GELU) return 0.5f * y * (1.0f + erff(y * 0.70710678118654752f));
-  if (act == ACT_RELU) return fmaxf(y, 0.0f);
-  if (act == ACT_GELU_TANH) {
+template <int ACT>
+__device__ __forceinline__ float act_fn(float y) {
+  if (ACT == ACT_GELU) return 0.5f * y * (1.0f + erff(y * 0.70710678118654752f));
+  if (ACT == ACT_RELU) return fmaxf(y, 0.0f);
+  if (ACT == ACT_GELU_TANH) {
     const float u = 0.7978845608028654f * (y + 0.044715f * y * y * y);
     return 0.5f * y * (1.0f + tanhf(u));
   }
   return y;
 }
 
+// 32 columns [n0, n0+32) of this thread's row: dequant / bias / activation,
+// RNE to fp16, written as 4 x 16B chunks of a 64B-swizzled smem row.
+template <bool I8, int ACT>
+__device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float (&bias)[32], const float (&sw)[32],
+                                          float sx, uint8_t* srow, int lane) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t h[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float v[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int j = c * 8 + e * 2 + u;
+        if (I8)
+          v[u] = __fmaf_rn(__int2float_rn(static_cast<int>(r[j])), __fmul_rn(sx, sw[j]), bias[j]);
+        else
+          v[u] = __fadd_rn(__uint_as_float(r[j]), bias[j]);
+        v[u] = act_fn<ACT>(v[u]);
+      }
+      h[e] = pack_half2(v[0], v[1]);
+    }
+    const int pc = c ^ ((lane >> 1) & 3);  // SWIZZLE_64B: 16B chunk c of row `lane`
+    *reinterpret_cast<uint4*>(srow + pc * 16) = make_uint4(h[0], h[1], h[2], h[3]);
+  }
+}
+
+__device__ __forceinline__ void load32(float (&dst)[32], const float* src, int n0, int N) {
+  if (src == nullptr) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) dst[j] = 0.0f;
+  } else if (n0 + 32 <= N && ((reinterpret_cast<uintptr_t>(src + n0) & 15) == 0)) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+      const float4 f = __ldg(reinterpret_cast<const float4*>(src + n0 + j));
+      dst[j] = f.x;
+      dst[j + 1] = f.y;
+      dst[j + 2] = f.z;
+      dst[j + 3] = f.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) dst[j] = (n0 + j < N) ? __ldg(src + n0 + j) : 0.0f;
+  }
+}
+
 template <int BN, bool I8>
-__global__ void __launch_bounds__(256, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmC, GemmParams p) {
   using Cfg = GemmCfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint8_t* sEpi = smem + Cfg::EPI_OFF;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
@@ -78,13 +135,14 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    if (p.out_mode == 1) tma_prefetch(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -155,71 +213,71 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {
-    const int q = warp - 4;  // TMEM lane quadrant this warp may access
+    const int ew = warp - 4;
+    const int q = warp & 3;                 // TMEM lane quadrant this warp may access
+    const int c_lo = (ew >> 2) * (BN / 2);  // this warp's column half of the tile
+    uint8_t* stage_buf = sEpi + ew * 2 * kStageTile;
     int acc = 0;
     uint32_t acc_phase = 0;
+    int nbuf = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+      const int row0 = mt * BM + q * 32;
+      const int row = row0 + lane;
+      float sx = 0.0f;
+      if (I8 && p.out_mode == 1 && row < p.M) sx = p.row_scale[row];
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = mt * BM + q * 32 + lane;
-      const bool row_ok = row < p.M;
-      float sx = 0.0f;
-      if (I8 && p.out_mode == 1 && row_ok) sx = p.row_scale[row];
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = c_lo; c < c_lo + BN / 2; c += 32) {
+        const int n0 = nt * BN + c;
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, r);
-        tmem_wait_ld();
-        const int n0 = nt * BN + c;
-        if (!row_ok || n0 >= p.N) continue;
-        const int nvalid = min(32, p.N - n0);
-        if (p.out_mode == 0) {
-          uint32_t* o = reinterpret_cast<uint32_t*>(p.out) + (size_t)row * p.ldo + n0;
-          if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+        if (n0 >= p.N) {  // whole chunk beyond N (warp-uniform)
+          tmem_wait_ld();
+          continue;
+        }
+        if (p.out_mode == 0) {  // raw accumulators (tests)
+          tmem_wait_ld();
+          if (row < p.M) {
+            uint32_t* o = reinterpret_cast<uint32_t*>(p.out) + (size_t)row * p.ldo + n0;
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) *reinterpret_cast<uint4*>(o + j) = make_uint4(r[j], r[j + 1], r[j + 2], r[j + 3]);
-          } else {
-            for (int j = 0; j < nvalid; ++j) o[j] = r[j];
+            for (int j = 0; j < 32; ++j)
+              if (n0 + j < p.N) o[j] = r[j];
           }
           continue;
         }
-        float y[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int n = n0 + j;
-          const float b = (p.bias && n < p.N) ? __ldg(p.bias + n) : 0.0f;
-          float v;
-          if (I8) {
-            const float sw = (n < p.N) ? __ldg(p.col_scale + n) : 0.0f;
-            v = __fmaf_rn(__int2float_rn(static_cast<int>(r[j])), __fmul_rn(sx, sw), b);
-          } else {
-            v = __fadd_rn(__uint_as_float(r[j]), b);
-          }
-          y[j] = apply_act(v, p.act);
+        float bias[32], sw[32];
+        load32(bias, p.bias, n0, p.N);
+        if (I8) load32(sw, p.col_scale, n0, p.N);
+        uint8_t* buf = stage_buf + (nbuf & 1) * kStageTile;
+        if (lane == 0) bulk_wait_read<1>();  // the store that last used `buf` has read it
+        __syncwarp();
+        tmem_wait_ld();
+        uint8_t* srow = buf + lane * 64;
+        switch (p.act) {
+          case ACT_GELU: epi_chunk<I8, ACT_GELU>(r, bias, sw, sx, srow, lane); break;
+          case ACT_RELU: epi_chunk<I8, ACT_RELU>(r, bias, sw, sx, srow, lane); break;
+          case ACT_GELU_TANH: epi_chunk<I8, ACT_GELU_TANH>(r, bias, sw, sx, srow, lane); break;
+          default: epi_chunk<I8, ACT_NONE>(r, bias, sw, sx, srow, lane); break;
         }
-        __half* o = reinterpret_cast<__half*>(p.out) + (size_t)row * p.ldo + n0;
-        if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
-#pragma unroll
-          for (int j = 0; j < 32; j += 8) {
-            uint4 v;
-            v.x = pack_half2(y[j], y[j + 1]);
-            v.y = pack_half2(y[j + 2], y[j + 3]);
-            v.z = pack_half2(y[j + 4], y[j + 5]);
-            v.w = pack_half2(y[j + 6], y[j + 7]);
-            *reinterpret_cast<uint4*>(o + j) = v;
-          }
-        } else {
-          for (int j = 0; j < nvalid; ++j) o[j] = __float2half_rn(y[j]);
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmC, buf, n0, row0);
+          bulk_commit();
         }
+        ++nbuf;
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) bulk_wait<0>();
   }
   __syncthreads();
   if (warp == 2) {
@@ -245,29 +303,36 @@ static PFN_encodeTiled get_encode_fn() {
   return fn;
 }
 
-bool make_operand_map(CUtensorMap* map, const void* base, int rows, int cols, int elem_bytes, size_t pitch_bytes,
-                      int box_rows, const char** err) {
+static bool encode_2d(CUtensorMap* map, const void* base, int rows, int cols, CUtensorMapDataType dt, int elem_bytes,
+                      size_t pitch_bytes, int box_cols, int box_rows, CUtensorMapSwizzle sw, const char** err) {
   PFN_encodeTiled enc = get_encode_fn();
   if (!enc) {
     *err = "cuTensorMapEncodeTiled unavailable";
     return false;
   }
   if ((pitch_bytes & 15) || (reinterpret_cast<uintptr_t>(base) & 15)) {
-    *err = "TMA operand needs 16-byte aligned base and row pitch";
+    *err = "TMA tensor needs a 16-byte aligned base and row pitch";
     return false;
   }
+  (void)elem_bytes;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)pitch_bytes};
-  cuuint32_t box[2] = {(cuuint32_t)(128 / elem_bytes), (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
-                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     *err = "cuTensorMapEncodeTiled failed";
     return false;
   }
   return true;
+}
+
+bool make_operand_map(CUtensorMap* map, const void* base, int rows, int cols, int elem_bytes, size_t pitch_bytes,
+                      int box_rows, const char** err) {
+  return encode_2d(map, base, rows, cols,
+                   elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, elem_bytes,
+                   pitch_bytes, 128 / elem_bytes, box_rows, CU_TENSOR_MAP_SWIZZLE_128B, err);
 }
 
 static int pick_bn(int N) {
@@ -282,6 +347,8 @@ bool plan_gemm(GemmPlan* g, bool i8, const void* A, int M_rows, int lda, const v
   const int eb = i8 ? 1 : 2;
   g->i8 = i8 ? 1 : 0;
   g->bn = pick_bn(N);
+  g->M_rows = M_rows;
+  g->has_out_map = false;
   if (!make_operand_map(&g->tmA, A, M_rows, K, eb, (size_t)lda * eb, BM, err)) return false;
   if (!make_operand_map(&g->tmB, W, N, K, eb, (size_t)ldw * eb, g->bn, err)) return false;
   g->p.N = N;
@@ -295,6 +362,14 @@ bool plan_gemm(GemmPlan* g, bool i8, const void* A, int M_rows, int lda, const v
   g->p.act = ACT_NONE;
   plan_gemm_set_m(g, M_rows);
   return true;
+}
+
+bool plan_gemm_output(GemmPlan* g, void* out, int ldo, const char** err) {
+  g->p.out = out;
+  g->p.ldo = ldo;
+  g->has_out_map = true;
+  return encode_2d(&g->tmC, out, g->M_rows, g->p.N, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (size_t)ldo * 2, 32, 32,
+                   CU_TENSOR_MAP_SWIZZLE_64B, err);
 }
 
 void plan_gemm_set_m(GemmPlan* g, int M) {
@@ -320,11 +395,12 @@ cudaError_t prepare_gemm_kernels() {
 template <int BN, bool I8>
 static cudaError_t launch_t(const GemmPlan& g, cudaStream_t s) {
   if (g.grid <= 0) return cudaSuccess;
-  gemm_tc_kernel<BN, I8><<<g.grid, 256, GemmCfg<BN>::SMEM, s>>>(g.tmA, g.tmB, g.p);
+  gemm_tc_kernel<BN, I8><<<g.grid, kThreads, GemmCfg<BN>::SMEM, s>>>(g.tmA, g.tmB, g.tmC, g.p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t s) {
+  if (g.p.out_mode == 1 && !g.has_out_map) return cudaErrorInvalidValue;
   if (g.i8) return g.bn == 256 ? launch_t<256, true>(g, s) : launch_t<128, true>(g, s);
   return g.bn == 256 ? launch_t<256, false>(g, s) : launch_t<128, false>(g, s);
 }

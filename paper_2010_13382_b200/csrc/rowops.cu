@@ -209,48 +209,54 @@ __global__ void __launch_bounds__(256) quant_rows_kernel(const __half* __restric
   if (lane == 0) scale[row] = sc;
 }
 
-// Pooler + classifier, fp32 (DESIGN R15).  One CTA per group of 16 sequences:
-// x0 rows staged in smem, each warp produces pooled[.][j] for its j's (lanes
-// over k, coalesced weight rows), then the C logits per sequence.
+// Pooler + classifier, fp32 (DESIGN R15).  pooler_kernel: CTA = 32 output
+// features j x 16 sequences; the 16 x0 rows are staged in smem (fp16 -> fp32),
+// each warp owns 4 j's with lanes over k (coalesced Wp rows) and writes
+// pooled[b][j] = tanh(Wp[j] . x0_b + bp[j]).  classifier_kernel: one warp per
+// (b, c) logit.
 constexpr int kHeadSeqs = 16;
-__global__ void __launch_bounds__(256) head_kernel(const __half* __restrict__ x16, int ldx, int B, int S, int H, int C,
-                                                  const float* __restrict__ Wp, const float* __restrict__ bp,
-                                                  const float* __restrict__ Wc, const float* __restrict__ bc,
-                                                  float* __restrict__ logits) {
-  extern __shared__ float hsm[];
-  float* xs = hsm;                     // [kHeadSeqs][H]
-  float* ps = hsm + kHeadSeqs * H;     // [kHeadSeqs][H]
-  const int b0 = blockIdx.x * kHeadSeqs;
+constexpr int kHeadJ = 32;
+__global__ void __launch_bounds__(256) pooler_kernel(const __half* __restrict__ x16, int ldx, int B, int S, int H,
+                                                    const float* __restrict__ Wp, const float* __restrict__ bp,
+                                                    float* __restrict__ pooled) {
+  extern __shared__ float hsm[];  // [kHeadSeqs][H]
+  const int j0 = blockIdx.x * kHeadJ, b0 = blockIdx.y * kHeadSeqs;
   const int nb = min(kHeadSeqs, B - b0);
   for (int i = threadIdx.x; i < kHeadSeqs * H; i += blockDim.x) {
     const int bb = i / H, k = i - bb * H;
-    xs[i] = bb < nb ? __half2float(x16[(size_t)(b0 + bb) * S * ldx + k]) : 0.0f;
+    hsm[i] = bb < nb ? __half2float(x16[(size_t)(b0 + bb) * S * ldx + k]) : 0.0f;
   }
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int j = warp; j < H; j += nw) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int jj = 0; jj < kHeadJ / 8; ++jj) {
+    const int j = j0 + warp * (kHeadJ / 8) + jj;
+    if (j >= H) break;
     float acc[kHeadSeqs];
 #pragma unroll
     for (int bb = 0; bb < kHeadSeqs; ++bb) acc[bb] = 0.0f;
     for (int k = lane; k < H; k += 32) {
       const float w = __ldg(Wp + (size_t)j * H + k);
 #pragma unroll
-      for (int bb = 0; bb < kHeadSeqs; ++bb) acc[bb] = __fmaf_rn(w, xs[bb * H + k], acc[bb]);
+      for (int bb = 0; bb < kHeadSeqs; ++bb) acc[bb] = __fmaf_rn(w, hsm[bb * H + k], acc[bb]);
     }
 #pragma unroll
     for (int bb = 0; bb < kHeadSeqs; ++bb) {
       const float sdot = warp_sum(acc[bb]);
-      if (lane == 0) ps[bb * H + j] = tanhf(sdot + bp[j]);
+      if (lane == 0 && bb < nb) pooled[(size_t)(b0 + bb) * H + j] = tanhf(sdot + bp[j]);
     }
   }
-  __syncthreads();
-  for (int t = warp; t < nb * C; t += nw) {
-    const int bb = t / C, c = t - bb * C;
-    float acc = 0.0f;
-    for (int k = lane; k < H; k += 32) acc = __fmaf_rn(__ldg(Wc + (size_t)c * H + k), ps[bb * H + k], acc);
-    acc = warp_sum(acc);
-    if (lane == 0) logits[(size_t)(b0 + bb) * C + c] = acc + bc[c];
-  }
+}
+
+__global__ void __launch_bounds__(256) classifier_kernel(const float* __restrict__ pooled, int B, int H, int C,
+                                                        const float* __restrict__ Wc, const float* __restrict__ bc,
+                                                        float* __restrict__ logits) {
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (t >= B * C) return;
+  const int b = t / C, c = t - b * C;
+  float acc = 0.0f;
+  for (int k = lane; k < H; k += 32) acc = __fmaf_rn(__ldg(Wc + (size_t)c * H + k), pooled[(size_t)b * H + k], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) logits[t] = acc + bc[c];
 }
 
 __global__ void cast_f16_kernel(const float* __restrict__ src, int N, int K, __half* __restrict__ dst, int ldd) {
@@ -306,14 +312,18 @@ cudaError_t launch_quant_rows(const __half* x, int ldx, int M, int K, int8_t* q,
 }
 
 cudaError_t launch_head(const __half* x16, int ldx, int B, int S, int H, int C, const float* Wp, const float* bp,
-                        const float* Wc, const float* bc, float* logits, cudaStream_t s) {
-  const size_t smem = 2 * kHeadSeqs * H * sizeof(float);
-  head_kernel<<<(B + kHeadSeqs - 1) / kHeadSeqs, 256, smem, s>>>(x16, ldx, B, S, H, C, Wp, bp, Wc, bc, logits);
+                        const float* Wc, const float* bc, float* pooled, float* logits, cudaStream_t s) {
+  const size_t smem = kHeadSeqs * H * sizeof(float);
+  dim3 grid((H + kHeadJ - 1) / kHeadJ, (B + kHeadSeqs - 1) / kHeadSeqs);
+  pooler_kernel<<<grid, 256, smem, s>>>(x16, ldx, B, S, H, Wp, bp, pooled);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  classifier_kernel<<<(B * C + 7) / 8, 256, 0, s>>>(pooled, B, H, C, Wc, bc, logits);
   return cudaGetLastError();
 }
 
 cudaError_t prepare_row_kernels() {
-  return cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kHeadSeqs * 1024 * 4);
+  return cudaFuncSetAttribute(pooler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHeadSeqs * 1024 * 4);
 }
 
 cudaError_t launch_cast_f16(const float* src, int N, int K, __half* dst, int ldd, cudaStream_t s) {
