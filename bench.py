@@ -244,14 +244,26 @@ def run_ours(args):
     dids = [torch.from_numpy(i).cuda() for i, _ in batches]
     dmask = [torch.from_numpy(m).cuda() for _, m in batches]
     logits = torch.empty((B, cfg.num_classes), dtype=torch.float32, device="cuda")
-    gather_list = [torch.empty_like(logits) for _ in range(world)] if (world > 1 and rank == 0) else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
+    # Data parallelism (paper_2010_13382_b200/dist.py, tested with gloo): the
+    # global batch of step k is the concatenation of every rank's batch k; rank
+    # r encodes its contiguous shard and the logits are gathered to rank 0.
+    sharded = None
+    if world > 1:
+        from paper_2010_13382_b200.dist import ShardedEncoder
+        gids, gmask = [], []
+        for k in range(NB):
+            parts = [synth.make_inputs(cfg, seed=1000 + r * 10 ** 6 + k) for r in range(world)]
+            gids.append(torch.from_numpy(np.concatenate([p[0] for p in parts])).cuda())
+            gmask.append(torch.from_numpy(np.concatenate([p[1] for p in parts])).cuda())
+        sharded = ShardedEncoder(lambda i, m: enc.encode(i, m, logits))
 
     def step(k):
-        enc.encode(dids[k % NB], dmask[k % NB], logits)
-        if world > 1:
-            dist.gather(logits, gather_list, dst=0)
+        if sharded is not None:
+            sharded.encode_global(gids[k % NB], gmask[k % NB])
+        else:
+            enc.encode(dids[k % NB], dmask[k % NB], logits)
 
     for k in range(max(args.warmup, 3)):
         step(k)
@@ -300,9 +312,11 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
+    gather_list = [torch.empty_like(logits) for _ in range(world)] if (world > 1 and rank == 0) else None
     for k in range(e2e_steps):
         enc.encode_host(h_ids[k % NB], h_mask[k % NB], h_logits)
-        if world > 1:
+        if world > 1:  # the host logits of every rank end up on rank 0
+            logits.copy_(h_logits, non_blocking=True)
             dist.gather(logits, gather_list, dst=0)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0

@@ -182,7 +182,9 @@ FF_API ff_status ff_encode_trace(ff_model *m, const int32_t *d_token_ids, const 
  * rows); dtype FF_I8: A, W int8.  out_mode 0: raw accumulators (int32 for i8,
  * fp32 for f16) into d_C with pitch ldc; out_mode 1: production epilogue
  * (i8: fma(float(acc), sx[m]*sw[n], bias[n]); f16: acc + bias[n]; then act
- * (act < 0 = none); fp16 output).  d_bias/d_sx/d_sw may be NULL where unused. */
+ * (act < 0 = none); fp16 output).  d_bias/d_sx/d_sw may be NULL where unused.
+ * out_mode | 16 forces the CTA-pair (cta_group::2, 256-row tile) kernel,
+ * out_mode | 32 forces the single-CTA kernel (default: chosen by size). */
 FF_API ff_status ff_debug_gemm(int32_t dtype, const void *d_A, int32_t lda, const void *d_W, int32_t ldw, int32_t M,
                         int32_t N, int32_t K, int32_t out_mode, void *d_C, int32_t ldc, const float *d_bias,
                         const float *d_sx, const float *d_sw, int32_t act, void *stream);

@@ -297,7 +297,7 @@ cudaError_t launch_dp(const __half* qkv, int ld, const int32_t* mask, int B, int
   const int nbuf = 2 * one <= kSmemMax ? 2 : 1;
   const float scale = (float)(1.0 / sqrt((double)d));  // fp32(1/sqrt(d)) (R10)
   const int n_items = B * A * ((S + QT - 1) / QT);
-  const int per_sm = (int)(kSmemMax / (nbuf * one)) >= 2 ? 2 : 1;
+  const int per_sm = 1;  // ~240 registers x 256 threads: one resident CTA per SM
   const int grid = n_items < kNumSMs * per_sm ? n_items : kNumSMs * per_sm;
   attention_kernel<DP><<<grid, 256, nbuf * one, s>>>(qkv, ld, mask, B, S, A, d, scale, ctx, ldc, nbuf);
   return cudaGetLastError();

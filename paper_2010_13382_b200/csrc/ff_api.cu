@@ -713,10 +713,16 @@ ff_status ff_debug_gemm(int32_t dtype, const void* d_A, int32_t lda, const void*
     FF_CK(ff::prepare_gemm_kernels());
     prepared = true;
   }
+  const int force = out_mode >> 4;  // bit 4: force CTA pairs, bit 5: force single CTAs
+  out_mode &= 15;
   ff::GemmPlan g;
   const char* err = nullptr;
   if (!ff::plan_gemm(&g, dtype == FF_I8, d_A, M, lda, d_W, ldw, N, K, &err))
     return fail(FF_E_INVALID, std::string("gemm plan: ") + err);
+  if (force == 1 || force == 2) {
+    g.force_pair = force == 1 ? 1 : 0;
+    ff::plan_gemm_set_m(&g, M);
+  }
   if (out_mode == 1) {
     if (!ff::plan_gemm_output(&g, d_C, ldc, &err)) return fail(FF_E_INVALID, std::string("gemm output: ") + err);
   } else {

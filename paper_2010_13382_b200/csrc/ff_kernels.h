@@ -27,13 +27,15 @@ struct GemmParams {
 };
 
 struct GemmPlan {
-  CUtensorMap tmA, tmB, tmC;  // A, W operands (128B swizzle); fp16 output (64B swizzle, 32x32 boxes)
+  CUtensorMap tmA, tmB, tmB2, tmC;  // A, W (BN-row / BN/2-row boxes, 128B swizzle); fp16 output (64B swizzle)
   GemmParams p;
   int bn;       // N tile (128 or 256)
   int i8;       // 1 = kind::i8
   int grid;
   int M_rows;   // row capacity of A / the output buffer
   bool has_out_map;
+  int force_pair;   // -1 auto (pairs when >= 74 pair-tiles), 0 never, 1 always
+  bool pair;        // chosen for the current M
 };
 
 // Encode a 2-D K-major tensor map for a GEMM operand: rows x cols elements of

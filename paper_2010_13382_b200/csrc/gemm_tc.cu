@@ -35,12 +35,15 @@ constexpr int kEpiWarps = 8;
 constexpr int kThreads = 128 + 32 * kEpiWarps;
 constexpr int kStageTile = 32 * 64;  // 32 rows x 32 fp16 staging block (2 KB)
 
-template <int BN>
+// PAIR = CTA pair (cta_group::2): a 256-row tile per pair, each CTA loads its
+// 128 rows of A and its BN/2 rows of W, the leader issues M=256 MMAs.
+template <int BN, bool PAIR>
 struct GemmCfg {
-  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int TM = PAIR ? 256 : 128;  // rows per (pair-)tile
   static constexpr int A_BYTES = BM * BK_BYTES;
-  static constexpr int B_BYTES = BN * BK_BYTES;
+  static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (PAIR || BN == 128) ? 6 : 4;
   static constexpr int EPI_OFF = STAGES * STAGE_BYTES;
   static constexpr int BAR_OFF = EPI_OFF + kEpiWarps * 2 * kStageTile;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;  // barriers + 1 KB alignment slack
@@ -51,15 +54,36 @@ struct GemmCfg {
 // Instruction descriptor (kind::f16 / kind::i8), both operands K-major:
 // c_format [4,6) (1 = f32, 2 = s32), a_format [7,10), b_format [10,13)
 // (f16 = 0; s8 = 1), N>>3 at [17,23), M>>4 at [24,29).
-template <bool I8, int BN>
+template <bool I8, int TM, int BN>
 __device__ __forceinline__ constexpr uint32_t make_idesc() {
   return (I8 ? (2u << 4) : (1u << 4)) | (I8 ? (1u << 7) : 0u) | (I8 ? (1u << 10) : 0u) |
-         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+}
+
+// erf(x) for the GELU epilogue, branch-free: erf(t) = 1 - 2^(-t * P7(t)) on
+// t = |x| (clamped to 4, where erf rounds to 1 in fp32), P7 a degree-7
+// least-squares fit of -log2(erfc(t))/t.  |erf_fast - erf| <= 3e-7 absolute
+// (fp32 evaluation incl. ex2.approx), far below the fp16 rounding of the
+// GELU output (DESIGN R2); replaces erff, whose divergent branches made the
+// FFN1 epilogue the bottleneck of that GEMM.
+__device__ __forceinline__ float erf_fast(float x) {
+  const float t = fminf(fabsf(x), 4.0f);
+  float p = 4.5357247e-05f;
+  p = __fmaf_rn(p, t, -0.000445495f);
+  p = __fmaf_rn(p, t, 0.0014893987f);
+  p = __fmaf_rn(p, t, 0.0007746952f);
+  p = __fmaf_rn(p, t, -0.028253723f);
+  p = __fmaf_rn(p, t, 0.14848162f);
+  p = __fmaf_rn(p, t, 0.9184164f);
+  p = __fmaf_rn(p, t, 1.6279086f);
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-t * p));
+  return copysignf(1.0f - e, x);
 }
 
 template <int ACT>
 __device__ __forceinline__ float act_fn(float y) {
-  if (ACT == ACT_GELU) return 0.5f * y * (1.0f + erff(y * 0.70710678118654752f));
+  if (ACT == ACT_GELU) return 0.5f * y * (1.0f + erf_fast(y * 0.70710678118654752f));
   if (ACT == ACT_RELU) return fmaxf(y, 0.0f);
   if (ACT == ACT_GELU_TANH) {
     const float u = 0.7978845608028654f * (y + 0.044715f * y * y * y);
@@ -69,29 +93,23 @@ __device__ __forceinline__ float act_fn(float y) {
 }
 
 // 32 columns [n0, n0+32) of this thread's row: dequant / bias / activation,
-// RNE to fp16, written as 4 x 16B chunks of a 64B-swizzled smem row.
+// RNE to fp16, packed as 16 half2 words.
 template <bool I8, int ACT>
 __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float (&bias)[32], const float (&sw)[32],
-                                          float sx, uint8_t* srow, int lane) {
+                                          float sx, uint32_t (&h)[16]) {
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    uint32_t h[4];
+  for (int e = 0; e < 16; ++e) {
+    float v[2];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      float v[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int j = c * 8 + e * 2 + u;
-        if (I8)
-          v[u] = __fmaf_rn(__int2float_rn(static_cast<int>(r[j])), __fmul_rn(sx, sw[j]), bias[j]);
-        else
-          v[u] = __fadd_rn(__uint_as_float(r[j]), bias[j]);
-        v[u] = act_fn<ACT>(v[u]);
-      }
-      h[e] = pack_half2(v[0], v[1]);
+    for (int u = 0; u < 2; ++u) {
+      const int j = e * 2 + u;
+      if (I8)
+        v[u] = __fmaf_rn(__int2float_rn(static_cast<int>(r[j])), __fmul_rn(sx, sw[j]), bias[j]);
+      else
+        v[u] = __fadd_rn(__uint_as_float(r[j]), bias[j]);
+      v[u] = act_fn<ACT>(v[u]);
     }
-    const int pc = c ^ ((lane >> 1) & 3);  // SWIZZLE_64B: 16B chunk c of row `lane`
-    *reinterpret_cast<uint4*>(srow + pc * 16) = make_uint4(h[0], h[1], h[2], h[3]);
+    h[e] = pack_half2(v[0], v[1]);
   }
 }
 
@@ -114,12 +132,13 @@ __device__ __forceinline__ void load32(float (&dst)[32], const float* src, int n
   }
 }
 
-template <int BN, bool I8>
+template <int BN, bool I8, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, GemmParams p) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, PAIR>;
   constexpr int STAGES = Cfg::STAGES;
+  constexpr int TM = Cfg::TM;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -132,6 +151,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;  // 0 = leader of the pair
+  const int unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int nunits = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
@@ -142,16 +164,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kEpiWarps);
+      mbar_init(&tempty[a], (PAIR ? 2 : 1) * kEpiWarps);
     }
     fence_barrier_init();
   }
   if (warp == 2) {
-    tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
-    tmem_relinquish();
+    if (PAIR) {
+      tmem_alloc2(tmem_slot, Cfg::TMEM_COLS);
+      tmem_relinquish2();
+    } else {
+      tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+      tmem_relinquish();
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();  // peer barriers initialised before any remote signal
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -162,13 +190,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = unit; tile < num_tiles; tile += nunits) {
         const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+        const int arow = mt * TM + (int)rank * BM;
+        const int brow = nt * BN + (PAIR ? (int)rank * (BN / 2) : 0);
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-          tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * KE, mt * BM, kEvictNormal);
-          tma_load_2d(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * KE, nt * BN, kEvictLast);
+          if (PAIR) {
+            // the leader's full barrier counts the bytes of both CTAs' loads
+            if (rank == 0) mbar_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+            const uint32_t bar = mapa_shared(smem_u32(&full[stage]), 0);
+            tma_load_2d_pair(sA + stage * Cfg::A_BYTES, &tmA, bar, kb * KE, arow, kEvictNormal);
+            tma_load_2d_pair(sB + stage * Cfg::B_BYTES, &tmB, bar, kb * KE, brow, kEvictLast);
+          } else {
+            mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+            tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * KE, arow, kEvictNormal);
+            tma_load_2d(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * KE, brow, kEvictLast);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -177,13 +215,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc<I8, BN>();
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = make_idesc<I8, TM, BN>();
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = unit; tile < num_tiles; tile += nunits) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -194,18 +232,26 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t bdesc = make_sw128_desc(sB + stage * Cfg::B_BYTES);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {  // 4 x 32 bytes of K; +2 = +32 B in the >>4 address field
-            if (I8)
-              mma_i8(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
-            else
-              mma_f16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            const uint32_t accum = (kb | k) != 0;
+            if (PAIR) {
+              if (I8) mma_i8_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, accum);
+              else mma_f16_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, accum);
+            } else {
+              if (I8) mma_i8(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, accum);
+              else mma_f16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, accum);
+            }
           }
-          mma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
+          // frees the smem slot (of both CTAs) when these MMAs finish
+          if (PAIR) mma_commit_pair(&empty[stage], 0x3);
+          else mma_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        // accumulator ready for the epilogue warps (of both CTAs)
+        if (PAIR) mma_commit_pair(&tfull[acc], 0x3);
+        else mma_commit(&tfull[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -217,61 +263,86 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;                 // TMEM lane quadrant this warp may access
     const int c_lo = (ew >> 2) * (BN / 2);  // this warp's column half of the tile
     uint8_t* stage_buf = sEpi + ew * 2 * kStageTile;
+    const uint32_t tempty_leader0 = PAIR ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     int nbuf = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (int tile = unit; tile < num_tiles; tile += nunits) {
       const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
-      const int row0 = mt * BM + q * 32;
+      const int row0 = mt * TM + (int)rank * BM + q * 32;
       const int row = row0 + lane;
       float sx = 0.0f;
       if (I8 && p.out_mode == 1 && row < p.M) sx = p.row_scale[row];
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-#pragma unroll 1
-      for (int c = c_lo; c < c_lo + BN / 2; c += 32) {
-        const int n0 = nt * BN + c;
-        uint32_t r[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, r);
-        if (n0 >= p.N) {  // whole chunk beyond N (warp-uniform)
-          tmem_wait_ld();
-          continue;
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      // Release the accumulator to the MMA warp as soon as this warp's last
+      // TMEM load has completed (before its math and stores).
+      auto release_acc = [&]() {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (PAIR) mbar_arrive_remote(tempty_leader0 + acc * 8);  // the leader's barrier
+          else mbar_arrive(&tempty[acc]);
         }
-        if (p.out_mode == 0) {  // raw accumulators (tests)
+      };
+      if (p.out_mode == 0) {  // raw accumulators (tests only)
+#pragma unroll 1
+        for (int c = c_lo; c < c_lo + BN / 2; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(tbase + c, r);
           tmem_wait_ld();
-          if (row < p.M) {
+          const int n0 = nt * BN + c;
+          if (row < p.M && n0 < p.N) {
             uint32_t* o = reinterpret_cast<uint32_t*>(p.out) + (size_t)row * p.ldo + n0;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               if (n0 + j < p.N) o[j] = r[j];
           }
-          continue;
         }
-        float bias[32], sw[32];
-        load32(bias, p.bias, n0, p.N);
-        if (I8) load32(sw, p.col_scale, n0, p.N);
-        uint8_t* buf = stage_buf + (nbuf & 1) * kStageTile;
-        if (lane == 0) bulk_wait_read<1>();  // the store that last used `buf` has read it
-        __syncwarp();
-        tmem_wait_ld();
-        uint8_t* srow = buf + lane * 64;
-        switch (p.act) {
-          case ACT_GELU: epi_chunk<I8, ACT_GELU>(r, bias, sw, sx, srow, lane); break;
-          case ACT_RELU: epi_chunk<I8, ACT_RELU>(r, bias, sw, sx, srow, lane); break;
-          case ACT_GELU_TANH: epi_chunk<I8, ACT_GELU_TANH>(r, bias, sw, sx, srow, lane); break;
-          default: epi_chunk<I8, ACT_NONE>(r, bias, sw, sx, srow, lane); break;
+        release_acc();
+      } else {
+        // software pipeline: the TMEM load of chunk c+1 overlaps the stores of chunk c
+        uint32_t r[32];
+        tmem_ld32(tbase + c_lo, r);
+#pragma unroll 1
+        for (int c = c_lo; c < c_lo + BN / 2; c += 32) {
+          const int n0 = nt * BN + c;
+          const bool last = c + 32 >= c_lo + BN / 2;
+          float bias[32], sw[32];
+          load32(bias, p.bias, n0, p.N);
+          if (I8) load32(sw, p.col_scale, n0, p.N);
+          tmem_wait_ld();
+          if (last) release_acc();
+          uint32_t h[16];
+          switch (p.act) {
+            case ACT_GELU: epi_chunk<I8, ACT_GELU>(r, bias, sw, sx, h); break;
+            case ACT_RELU: epi_chunk<I8, ACT_RELU>(r, bias, sw, sx, h); break;
+            case ACT_GELU_TANH: epi_chunk<I8, ACT_GELU_TANH>(r, bias, sw, sx, h); break;
+            default: epi_chunk<I8, ACT_NONE>(r, bias, sw, sx, h); break;
+          }
+          if (!last) tmem_ld32(tbase + c + 32, r);
+          if (n0 < p.N) {  // warp-uniform; TMA clips the N tail of the chunk
+            uint8_t* buf = stage_buf + (nbuf & 1) * kStageTile;
+            if (lane == 0) bulk_wait_read<1>();  // the store that last used `buf` has read it
+            __syncwarp();
+            uint8_t* srow = buf + lane * 64;
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {  // SWIZZLE_64B: 16B chunk cc of row `lane`
+              const int pc = cc ^ ((lane >> 1) & 3);
+              *reinterpret_cast<uint4*>(srow + pc * 16) =
+                  make_uint4(h[4 * cc], h[4 * cc + 1], h[4 * cc + 2], h[4 * cc + 3]);
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmC, buf, n0, row0);
+              bulk_commit();
+            }
+            ++nbuf;
+          }
         }
-        fence_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          tma_store_2d(&tmC, buf, n0, row0);
-          bulk_commit();
-        }
-        ++nbuf;
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -279,10 +350,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (lane == 0) bulk_wait<0>();
   }
+  tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();  // no CTA leaves while its peer may still signal it
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    if (PAIR) tmem_dealloc2(tmem_base, Cfg::TMEM_COLS);
+    else tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
   }
 }
 
@@ -349,8 +423,11 @@ bool plan_gemm(GemmPlan* g, bool i8, const void* A, int M_rows, int lda, const v
   g->bn = pick_bn(N);
   g->M_rows = M_rows;
   g->has_out_map = false;
+  g->force_pair = -1;
   if (!make_operand_map(&g->tmA, A, M_rows, K, eb, (size_t)lda * eb, BM, err)) return false;
+  // W boxes cover BN rows (single CTA) or BN/2 rows (each CTA of a pair): two maps.
   if (!make_operand_map(&g->tmB, W, N, K, eb, (size_t)ldw * eb, g->bn, err)) return false;
+  if (!make_operand_map(&g->tmB2, W, N, K, eb, (size_t)ldw * eb, g->bn / 2, err)) return false;
   g->p.N = N;
   g->p.K = K;
   g->p.n_tiles = (N + g->bn - 1) / g->bn;
@@ -374,35 +451,64 @@ bool plan_gemm_output(GemmPlan* g, void* out, int ldo, const char** err) {
 
 void plan_gemm_set_m(GemmPlan* g, int M) {
   g->p.M = M;
-  g->p.m_tiles = (M + BM - 1) / BM;
+  // CTA pairs (M = 256 tiles) when there are enough tiles to fill the GPU.
+  const int pair_tiles = ((M + 255) / 256) * g->p.n_tiles;
+  g->pair = g->force_pair == 1 || (g->force_pair < 0 && pair_tiles >= kNumSMs / 2);
+  const int tm = g->pair ? 256 : BM;
+  g->p.m_tiles = (M + tm - 1) / tm;
   const int tiles = g->p.m_tiles * g->p.n_tiles;
-  g->grid = tiles < kNumSMs ? tiles : kNumSMs;
+  if (g->pair) {
+    const int pairs = tiles < kNumSMs / 2 ? tiles : kNumSMs / 2;
+    g->grid = 2 * pairs;
+  } else {
+    g->grid = tiles < kNumSMs ? tiles : kNumSMs;
+  }
 }
 
-template <int BN, bool I8>
+template <int BN, bool I8, bool PAIR>
 static cudaError_t set_attr() {
-  return cudaFuncSetAttribute(gemm_tc_kernel<BN, I8>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::SMEM);
+  return cudaFuncSetAttribute(gemm_tc_kernel<BN, I8, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              GemmCfg<BN, PAIR>::SMEM);
 }
 
 cudaError_t prepare_gemm_kernels() {
   cudaError_t e;
-  if ((e = set_attr<256, true>()) != cudaSuccess) return e;
-  if ((e = set_attr<128, true>()) != cudaSuccess) return e;
-  if ((e = set_attr<256, false>()) != cudaSuccess) return e;
-  return set_attr<128, false>();
+  if ((e = set_attr<256, true, false>()) != cudaSuccess) return e;
+  if ((e = set_attr<128, true, false>()) != cudaSuccess) return e;
+  if ((e = set_attr<256, false, false>()) != cudaSuccess) return e;
+  if ((e = set_attr<128, false, false>()) != cudaSuccess) return e;
+  if ((e = set_attr<256, true, true>()) != cudaSuccess) return e;
+  if ((e = set_attr<128, true, true>()) != cudaSuccess) return e;
+  if ((e = set_attr<256, false, true>()) != cudaSuccess) return e;
+  return set_attr<128, false, true>();
 }
 
-template <int BN, bool I8>
+template <int BN, bool I8, bool PAIR>
 static cudaError_t launch_t(const GemmPlan& g, cudaStream_t s) {
   if (g.grid <= 0) return cudaSuccess;
-  gemm_tc_kernel<BN, I8><<<g.grid, kThreads, GemmCfg<BN>::SMEM, s>>>(g.tmA, g.tmB, g.tmC, g.p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g.grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = GemmCfg<BN, PAIR>::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = PAIR ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, I8, PAIR>, g.tmA, PAIR ? g.tmB2 : g.tmB, g.tmC, g.p);
 }
 
 cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t s) {
   if (g.p.out_mode == 1 && !g.has_out_map) return cudaErrorInvalidValue;
-  if (g.i8) return g.bn == 256 ? launch_t<256, true>(g, s) : launch_t<128, true>(g, s);
-  return g.bn == 256 ? launch_t<256, false>(g, s) : launch_t<128, false>(g, s);
+  if (g.pair) {
+    if (g.i8) return g.bn == 256 ? launch_t<256, true, true>(g, s) : launch_t<128, true, true>(g, s);
+    return g.bn == 256 ? launch_t<256, false, true>(g, s) : launch_t<128, false, true>(g, s);
+  }
+  if (g.i8) return g.bn == 256 ? launch_t<256, true, false>(g, s) : launch_t<128, true, false>(g, s);
+  return g.bn == 256 ? launch_t<256, false, false>(g, s) : launch_t<128, false, false>(g, s);
 }
 
 }  // namespace ff

@@ -4,23 +4,23 @@
 //   embed_ln   X = LN(E_tok[id] + P'[t]) -> fp16 (+ s8 rows)
 //   add_ln     Y = LN(a + r) -> fp16 (+ s8 rows)   (post-LN residual, a6/a10)
 //   quant_rows (q, s) = Q8row(x16)                                (a4/a8)
-//   head       logits = Wc tanh(Wp x0 + bp) + bc                  (a11)
+//   pooler / classifier: logits = Wc tanh(Wp x0 + bp) + bc        (a11)
 //   cast_f16 / quant_weight / add_row: weight packing at load     (a0)
 //
-// Row kernels use one warp per row with the row held in registers (H <= 1024
-// -> <= 32 fp32 per lane) and warp-shuffle reductions; two-pass mean /
-// variance in fp32.  Q8row (DESIGN R6-R8): scale = amax/127 (IEEE division,
-// 1.0 for an all-zero row), q = clamp(RNE(x/scale), -127, 127), computed from
-// the fp16-ROUNDED value so that the result does not depend on where the
-// quantizer is fused (R12).  No fast-math anywhere in this file.
+// Row kernels: one warp per row, the whole row held in registers as 16-byte
+// chunks (8 elements; chunk c of lane l covers columns 8*(l + 32c)), so every
+// global access is a 16-byte vector and each row is read from HBM exactly
+// once; warp-shuffle reductions; two-pass mean / variance in fp32.
+// Q8row (DESIGN R6-R8): scale = amax/127 (IEEE division, 1.0 for an all-zero
+// row), q = clamp(RNE(x/scale), -127, 127), computed from the fp16-ROUNDED
+// value so the result does not depend on where the quantizer is fused (R12).
+// No fast-math anywhere in this file.
 #include "ff_kernels.h"
 #include "ptx.cuh"
 
 namespace ff {
 
 namespace {
-
-constexpr int kMaxChunks = 8;  // float4 chunks per lane: H <= 8*4*32 = 1024
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -39,21 +39,35 @@ __device__ __forceinline__ int8_t quant1(float x, float s) {
   return static_cast<int8_t>(static_cast<int>(v));
 }
 
-// LayerNorm of a row held as v[c][0..3] at columns 4*(lane + 32*c) (< H), then
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+  const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __half22float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+// LayerNorm of a row held as v[c][0..7] at columns 8*(lane + 32c) (< H), then
 // R16 store and optional Q8row.  All lanes of the warp participate.
-__device__ __forceinline__ void ln_store(float (&v)[kMaxChunks][4], int nch, int H, int lane, const float* g,
-                                         const float* b, float eps, __half* y16, int8_t* yq, float* ys) {
+template <int NCH>
+__device__ __forceinline__ void ln_store(float (&v)[NCH][8], int H, int lane, const float* __restrict__ g,
+                                         const float* __restrict__ b, float eps, __half* y16, int8_t* yq, float* ys) {
   float s = 0.0f;
 #pragma unroll
-  for (int c = 0; c < kMaxChunks; ++c)
-    if (c < nch && 4 * (lane + 32 * c) < H) s += (v[c][0] + v[c][1]) + (v[c][2] + v[c][3]);
+  for (int c = 0; c < NCH; ++c)
+    if (8 * (lane + 32 * c) < H) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += v[c][j];
+    }
   const float mean = __fdiv_rn(warp_sum(s), (float)H);
   float q = 0.0f;
 #pragma unroll
-  for (int c = 0; c < kMaxChunks; ++c)
-    if (c < nch && 4 * (lane + 32 * c) < H) {
+  for (int c = 0; c < NCH; ++c)
+    if (8 * (lane + 32 * c) < H) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < 8; ++j) {
         const float dlt = v[c][j] - mean;
         q = __fmaf_rn(dlt, dlt, q);
       }
@@ -62,41 +76,46 @@ __device__ __forceinline__ void ln_store(float (&v)[kMaxChunks][4], int nch, int
   const float rstd = 1.0f / sqrtf(var + eps);
   float amax = 0.0f;
 #pragma unroll
-  for (int c = 0; c < kMaxChunks; ++c) {
-    const int col = 4 * (lane + 32 * c);
-    if (c < nch && col < H) {
-      const float4 gg = *reinterpret_cast<const float4*>(g + col);
-      const float4 bb = *reinterpret_cast<const float4*>(b + col);
-      const float gv[4] = {gg.x, gg.y, gg.z, gg.w}, bv[4] = {bb.x, bb.y, bb.z, bb.w};
-      __half h[4];
+  for (int c = 0; c < NCH; ++c) {
+    const int col = 8 * (lane + 32 * c);
+    if (col < H) {
+      const float4 g0 = __ldg(reinterpret_cast<const float4*>(g + col));
+      const float4 g1 = __ldg(reinterpret_cast<const float4*>(g + col + 4));
+      const float4 b0 = __ldg(reinterpret_cast<const float4*>(b + col));
+      const float4 b1 = __ldg(reinterpret_cast<const float4*>(b + col + 4));
+      const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      uint32_t pk[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        h[j] = __float2half_rn((v[c][j] - mean) * rstd * gv[j] + bv[j]);
-        v[c][j] = __half2float(h[j]);  // keep the fp16-rounded value for Q8row
-        amax = fmaxf(amax, fabsf(v[c][j]));
+      for (int j = 0; j < 8; j += 2) {
+        const __half2 h = __floats2half2_rn((v[c][j] - mean) * rstd * gv[j] + bv[j],
+                                            (v[c][j + 1] - mean) * rstd * gv[j + 1] + bv[j + 1]);
+        const float2 hf = __half22float2(h);  // keep the fp16-rounded values for Q8row
+        v[c][j] = hf.x;
+        v[c][j + 1] = hf.y;
+        amax = fmaxf(amax, fmaxf(fabsf(hf.x), fabsf(hf.y)));
+        pk[j / 2] = *reinterpret_cast<const uint32_t*>(&h);
       }
-      __half2 pk[2] = {__halves2half2(h[0], h[1]), __halves2half2(h[2], h[3])};
-      *reinterpret_cast<uint2*>(y16 + col) = *reinterpret_cast<uint2*>(pk);
+      *reinterpret_cast<uint4*>(y16 + col) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     }
   }
   if (yq == nullptr) return;
   amax = warp_max(amax);
   const float sc = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 127.0f);
 #pragma unroll
-  for (int c = 0; c < kMaxChunks; ++c) {
-    const int col = 4 * (lane + 32 * c);
-    if (c < nch && col < H) {
-      char4 qq;
-      qq.x = quant1(v[c][0], sc);
-      qq.y = quant1(v[c][1], sc);
-      qq.z = quant1(v[c][2], sc);
-      qq.w = quant1(v[c][3], sc);
-      *reinterpret_cast<char4*>(yq + col) = qq;
+  for (int c = 0; c < NCH; ++c) {
+    const int col = 8 * (lane + 32 * c);
+    if (col < H) {
+      int8_t o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = quant1(v[c][j], sc);
+      *reinterpret_cast<uint2*>(yq + col) = *reinterpret_cast<const uint2*>(o);
     }
   }
   if (lane == 0) *ys = sc;
 }
 
+template <int NCH>
 __global__ void __launch_bounds__(256) embed_ln_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ mask,
                                                       int M, int S, int H, int V, const float* __restrict__ tok,
                                                       const float* __restrict__ pos, const float* __restrict__ g,
@@ -117,95 +136,115 @@ __global__ void __launch_bounds__(256) embed_ln_kernel(const int32_t* __restrict
   if (id < 0 || id >= V) id = 0;  // keep the gather in bounds; the row is flagged
   const float* e = tok + (size_t)id * H;
   const float* p = pos + (size_t)t * H;
-  const int nch = (H + 127) / 128;
-  float v[kMaxChunks][4];
+  float v[NCH][8];
 #pragma unroll
-  for (int c = 0; c < kMaxChunks; ++c) {
-    const int col = 4 * (lane + 32 * c);
-    if (c < nch && col < H) {
-      const float4 a = __ldg(reinterpret_cast<const float4*>(e + col));
-      const float4 pp = __ldg(reinterpret_cast<const float4*>(p + col));
-      v[c][0] = __fadd_rn(a.x, pp.x);
-      v[c][1] = __fadd_rn(a.y, pp.y);
-      v[c][2] = __fadd_rn(a.z, pp.z);
-      v[c][3] = __fadd_rn(a.w, pp.w);
+  for (int c = 0; c < NCH; ++c) {
+    const int col = 8 * (lane + 32 * c);
+    if (col < H) {
+      const float4 a0 = __ldg(reinterpret_cast<const float4*>(e + col));
+      const float4 a1 = __ldg(reinterpret_cast<const float4*>(e + col + 4));
+      const float4 p0 = __ldg(reinterpret_cast<const float4*>(p + col));
+      const float4 p1 = __ldg(reinterpret_cast<const float4*>(p + col + 4));
+      v[c][0] = __fadd_rn(a0.x, p0.x);
+      v[c][1] = __fadd_rn(a0.y, p0.y);
+      v[c][2] = __fadd_rn(a0.z, p0.z);
+      v[c][3] = __fadd_rn(a0.w, p0.w);
+      v[c][4] = __fadd_rn(a1.x, p1.x);
+      v[c][5] = __fadd_rn(a1.y, p1.y);
+      v[c][6] = __fadd_rn(a1.z, p1.z);
+      v[c][7] = __fadd_rn(a1.w, p1.w);
     }
   }
-  ln_store(v, nch, H, lane, g, b, eps, x16 + (size_t)row * ldx, xq ? xq + (size_t)row * ldq : nullptr,
-           xs ? xs + row : nullptr);
+  ln_store<NCH>(v, H, lane, g, b, eps, x16 + (size_t)row * ldx, xq ? xq + (size_t)row * ldq : nullptr,
+                xs ? xs + row : nullptr);
 }
 
+template <int NCH>
 __global__ void __launch_bounds__(256) add_ln_kernel(const __half* __restrict__ a, int lda, const __half* __restrict__ r,
                                                     int ldr, int M, int H, const float* __restrict__ g,
                                                     const float* __restrict__ b, float eps, __half* y16, int ldy,
                                                     int8_t* yq, int ldq, float* ys) {
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (row >= M) return;
-  const int nch = (H + 127) / 128;
-  float v[kMaxChunks][4];
   const __half* ar = a + (size_t)row * lda;
   const __half* rr = r + (size_t)row * ldr;
+  uint4 ua[NCH], ur[NCH];
 #pragma unroll
-  for (int c = 0; c < kMaxChunks; ++c) {
-    const int col = 4 * (lane + 32 * c);
-    if (c < nch && col < H) {
-      const uint2 ua = *reinterpret_cast<const uint2*>(ar + col);
-      const uint2 ur = *reinterpret_cast<const uint2*>(rr + col);
-      const __half2* ha = reinterpret_cast<const __half2*>(&ua);
-      const __half2* hr = reinterpret_cast<const __half2*>(&ur);
-      const float2 a0 = __half22float2(ha[0]), a1 = __half22float2(ha[1]);
-      const float2 r0 = __half22float2(hr[0]), r1 = __half22float2(hr[1]);
-      v[c][0] = __fadd_rn(a0.x, r0.x);
-      v[c][1] = __fadd_rn(a0.y, r0.y);
-      v[c][2] = __fadd_rn(a1.x, r1.x);
-      v[c][3] = __fadd_rn(a1.y, r1.y);
+  for (int c = 0; c < NCH; ++c) {  // all loads first: 2*NCH 16-byte requests in flight per lane
+    const int col = 8 * (lane + 32 * c);
+    if (col < H) {
+      ua[c] = __ldcs(reinterpret_cast<const uint4*>(ar + col));
+      ur[c] = __ldcs(reinterpret_cast<const uint4*>(rr + col));
     }
   }
-  ln_store(v, nch, H, lane, g, b, eps, y16 + (size_t)row * ldy, yq ? yq + (size_t)row * ldq : nullptr,
-           ys ? ys + row : nullptr);
+  float v[NCH][8];
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    if (8 * (lane + 32 * c) < H) {
+      float fa[8], fr[8];
+      unpack8(ua[c], fa);
+      unpack8(ur[c], fr);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[c][j] = __fadd_rn(fa[j], fr[j]);
+    }
+  }
+  ln_store<NCH>(v, H, lane, g, b, eps, y16 + (size_t)row * ldy, yq ? yq + (size_t)row * ldq : nullptr,
+                ys ? ys + row : nullptr);
 }
 
-// One warp per row; any K (two passes over the row: absmax, then quantize).
+// One warp per row, the row in registers (NCH 16-byte chunks per lane).
+template <int NCH>
 __global__ void __launch_bounds__(256) quant_rows_kernel(const __half* __restrict__ x, int ldx, int M, int K,
                                                         int8_t* __restrict__ q, int ldq, float* __restrict__ scale) {
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (row >= M) return;
   const __half* xr = x + (size_t)row * ldx;
   int8_t* qr = q + (size_t)row * ldq;
-  float amax = 0.0f;
-  const bool vec = ((K & 7) == 0) && ((reinterpret_cast<uintptr_t>(xr) & 15) == 0) &&
-                   ((reinterpret_cast<uintptr_t>(qr) & 7) == 0);
-  if (vec) {
-    for (int c = lane * 8; c < K; c += 256) {
-      const uint4 u = *reinterpret_cast<const uint4*>(xr + c);
-      const __half2* h = reinterpret_cast<const __half2*>(&u);
+  uint4 u[NCH];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 f = __half22float2(h[j]);
-        amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
-      }
+  for (int c = 0; c < NCH; ++c) {
+    const int col = 8 * (lane + 32 * c);
+    if (col < K) u[c] = __ldcs(reinterpret_cast<const uint4*>(xr + col));
+  }
+  float amax = 0.0f;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    if (8 * (lane + 32 * c) < K) {
+      float f[8];
+      unpack8(u[c], f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) amax = fmaxf(amax, fabsf(f[j]));
     }
-  } else {
-    for (int c = lane; c < K; c += 32) amax = fmaxf(amax, fabsf(__half2float(xr[c])));
   }
   amax = warp_max(amax);
   const float sc = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 127.0f);
-  if (vec) {
-    for (int c = lane * 8; c < K; c += 256) {
-      const uint4 u = *reinterpret_cast<const uint4*>(xr + c);
-      const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int col = 8 * (lane + 32 * c);
+    if (col < K) {
+      float f[8];
+      unpack8(u[c], f);
       int8_t o[8];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 f = __half22float2(h[j]);
-        o[2 * j] = quant1(f.x, sc);
-        o[2 * j + 1] = quant1(f.y, sc);
-      }
-      *reinterpret_cast<uint2*>(qr + c) = *reinterpret_cast<uint2*>(o);
+      for (int j = 0; j < 8; ++j) o[j] = quant1(f[j], sc);
+      *reinterpret_cast<uint2*>(qr + col) = *reinterpret_cast<const uint2*>(o);
     }
-  } else {
-    for (int c = lane; c < K; c += 32) qr[c] = quant1(__half2float(xr[c]), sc);
   }
+  if (lane == 0) scale[row] = sc;
+}
+
+// Generic fallback (K not a multiple of 8 or unaligned rows): element-wise.
+__global__ void __launch_bounds__(256) quant_rows_scalar_kernel(const __half* __restrict__ x, int ldx, int M, int K,
+                                                               int8_t* __restrict__ q, int ldq,
+                                                               float* __restrict__ scale) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const __half* xr = x + (size_t)row * ldx;
+  float amax = 0.0f;
+  for (int c = lane; c < K; c += 32) amax = fmaxf(amax, fabsf(__half2float(xr[c])));
+  amax = warp_max(amax);
+  const float sc = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 127.0f);
+  for (int c = lane; c < K; c += 32) q[(size_t)row * ldq + c] = quant1(__half2float(xr[c]), sc);
   if (lane == 0) scale[row] = sc;
 }
 
@@ -287,27 +326,54 @@ __global__ void add_row_kernel(const float* __restrict__ src, int N, int K, cons
   dst[i] = __fadd_rn(src[i], row[i % K]);
 }
 
+inline int chunks_for(int K) { return (K + 255) / 256; }  // 16-byte chunks per lane
+
 }  // namespace
 
 cudaError_t launch_embed_ln(const int32_t* ids, const int32_t* mask, int B, int S, int H, int V, const float* tok,
                             const float* pos, const float* g, const float* b, float eps, __half* x16, int ldx,
                             int8_t* xq, int ldq, float* xs, int* err_flag, cudaStream_t s) {
   const int M = B * S;
-  embed_ln_kernel<<<(M + 7) / 8, 256, 0, s>>>(ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs,
-                                             err_flag);
+  const unsigned grid = (M + 7) / 8;
+  switch (chunks_for(H)) {
+    case 1: embed_ln_kernel<1><<<grid, 256, 0, s>>>(ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs, err_flag); break;
+    case 2: embed_ln_kernel<2><<<grid, 256, 0, s>>>(ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs, err_flag); break;
+    case 3: embed_ln_kernel<3><<<grid, 256, 0, s>>>(ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs, err_flag); break;
+    default: embed_ln_kernel<4><<<grid, 256, 0, s>>>(ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs, err_flag); break;
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_add_ln(const __half* a, int lda, const __half* r, int ldr, int M, int H, const float* g,
                           const float* b, float eps, __half* y16, int ldy, int8_t* yq, int ldq, float* ys,
                           cudaStream_t s) {
-  add_ln_kernel<<<(M + 7) / 8, 256, 0, s>>>(a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys);
+  const unsigned grid = (M + 7) / 8;
+  switch (chunks_for(H)) {
+    case 1: add_ln_kernel<1><<<grid, 256, 0, s>>>(a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
+    case 2: add_ln_kernel<2><<<grid, 256, 0, s>>>(a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
+    case 3: add_ln_kernel<3><<<grid, 256, 0, s>>>(a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
+    default: add_ln_kernel<4><<<grid, 256, 0, s>>>(a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_quant_rows(const __half* x, int ldx, int M, int K, int8_t* q, int ldq, float* scale,
                               cudaStream_t s) {
-  quant_rows_kernel<<<(M + 7) / 8, 256, 0, s>>>(x, ldx, M, K, q, ldq, scale);
+  const unsigned grid = (M + 7) / 8;
+  const bool vec = (K % 8 == 0) && (ldx % 8 == 0) && (ldq % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(q) & 7) == 0) && K <= 4096;
+  if (!vec) {
+    quant_rows_scalar_kernel<<<grid, 256, 0, s>>>(x, ldx, M, K, q, ldq, scale);
+    return cudaGetLastError();
+  }
+  const int n = chunks_for(K);
+  if (n <= 1) quant_rows_kernel<1><<<grid, 256, 0, s>>>(x, ldx, M, K, q, ldq, scale);
+  else if (n <= 2) quant_rows_kernel<2><<<grid, 256, 0, s>>>(x, ldx, M, K, q, ldq, scale);
+  else if (n <= 4) quant_rows_kernel<4><<<grid, 256, 0, s>>>(x, ldx, M, K, q, ldq, scale);
+  else if (n <= 6) quant_rows_kernel<6><<<grid, 256, 0, s>>>(x, ldx, M, K, q, ldq, scale);
+  else if (n <= 8) quant_rows_kernel<8><<<grid, 256, 0, s>>>(x, ldx, M, K, q, ldq, scale);
+  else if (n <= 12) quant_rows_kernel<12><<<grid, 256, 0, s>>>(x, ldx, M, K, q, ldq, scale);
+  else quant_rows_kernel<16><<<grid, 256, 0, s>>>(x, ldx, M, K, q, ldq, scale);
   return cudaGetLastError();
 }
 

@@ -197,7 +197,7 @@ class Encoder:
 
 
 # ------------------------------------------------------------ debug entry points
-def gemm(A, W, out_mode=0, bias=None, sx=None, sw=None, act=-1, out=None):
+def gemm(A, W, out_mode=0, bias=None, sx=None, sw=None, act=-1, out=None, cta_pair=None):
     """C = A W^T through the production tcgen05 kernel.  A [M,K], W [N,K]: both
     int8 (kind::i8) or both fp16 (kind::f16) CUDA tensors with 16-byte aligned rows."""
     import torch
@@ -210,7 +210,8 @@ def gemm(A, W, out_mode=0, bias=None, sx=None, sw=None, act=-1, out=None):
         else:
             out = torch.empty((M, N), dtype=torch.float16, device=A.device)
     nul = ctypes.c_void_p(None)
-    check(lib().ff_debug_gemm(FF_I8 if i8 else FF_F16, _ptr(A), A.stride(0), _ptr(W), W.stride(0), M, N, K, out_mode,
+    mode = out_mode | (0 if cta_pair is None else (16 if cta_pair else 32))
+    check(lib().ff_debug_gemm(FF_I8 if i8 else FF_F16, _ptr(A), A.stride(0), _ptr(W), W.stride(0), M, N, K, mode,
                               _ptr(out), out.stride(0), _ptr(bias) if bias is not None else nul,
                               _ptr(sx) if sx is not None else nul, _ptr(sw) if sw is not None else nul, act,
                               _stream_ptr()))

@@ -32,12 +32,13 @@ I8_SHAPES = [
 ]
 
 
+@pytest.mark.parametrize("pair", [False, True])
 @pytest.mark.parametrize("M,N,K", I8_SHAPES)
-def test_gemm_i8_int32_accumulators_bit_exact(M, N, K):
+def test_gemm_i8_int32_accumulators_bit_exact(M, N, K, pair):
     rng = np.random.default_rng(M * 7 + N * 3 + K)
     A = rng.integers(-127, 128, (M, K), dtype=np.int8)
     W = rng.integers(-127, 128, (N, K), dtype=np.int8)
-    C = ffb.gemm(_pitched(A, torch.int8, 16), _pitched(W, torch.int8, 16), out_mode=0)
+    C = ffb.gemm(_pitched(A, torch.int8, 16), _pitched(W, torch.int8, 16), out_mode=0, cta_pair=pair)
     torch.cuda.synchronize()
     got = C.cpu().numpy()
     if M * N * K <= 3e8:
@@ -48,13 +49,14 @@ def test_gemm_i8_int32_accumulators_bit_exact(M, N, K):
     assert np.array_equal(got, ref), f"max diff {np.abs(got.astype(np.int64) - ref).max()}"
 
 
+@pytest.mark.parametrize("pair", [False, True])
 @pytest.mark.parametrize("M,N,K", [(128, 128, 64), (200, 936, 312), (1000, 1536, 768), (300, 768, 3072),
                                    (129, 1200, 312), (77, 1024, 4096)])
-def test_gemm_f16_fp32_accumulators_within_bound(M, N, K):
+def test_gemm_f16_fp32_accumulators_within_bound(M, N, K, pair):
     rng = np.random.default_rng(K)
     A = np.float16(rng.standard_normal((M, K)))
     W = np.float16(rng.standard_normal((N, K)) * 0.05)
-    C = ffb.gemm(_pitched(A, torch.float16, 8), _pitched(W, torch.float16, 8), out_mode=0)
+    C = ffb.gemm(_pitched(A, torch.float16, 8), _pitched(W, torch.float16, 8), out_mode=0, cta_pair=pair)
     torch.cuda.synchronize()
     got = C.cpu().numpy().astype(np.float64)
     A64, W64 = A.astype(np.float64), W.astype(np.float64)
@@ -63,8 +65,9 @@ def test_gemm_f16_fp32_accumulators_within_bound(M, N, K):
     assert np.all(np.abs(got - ref) <= bound), np.max(np.abs(got - ref) / bound)
 
 
+@pytest.mark.parametrize("pair", [False, True])
 @pytest.mark.parametrize("act", [-1, 0, 1, 2])
-def test_gemm_epilogues(act):
+def test_gemm_epilogues(act, pair):
     rng = np.random.default_rng(5 + act)
     M, N, K = 300, 640, 512
     A = rng.integers(-127, 128, (M, K), dtype=np.int8)
@@ -74,7 +77,7 @@ def test_gemm_epilogues(act):
     b = (rng.standard_normal(N) * 0.1).astype(np.float32)
     out = ffb.gemm(_pitched(A, torch.int8, 16), _pitched(W, torch.int8, 16), out_mode=1,
                    bias=torch.from_numpy(b).cuda(), sx=torch.from_numpy(sx).cuda(), sw=torch.from_numpy(sw).cuda(),
-                   act=act)
+                   act=act, cta_pair=pair)
     torch.cuda.synchronize()
     got = out.cpu().numpy().astype(np.float64)
     acc = A.astype(np.int64) @ W.astype(np.int64).T
