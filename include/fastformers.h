@@ -143,8 +143,14 @@ FF_API ff_status ff_encode_host(ff_model *m, const int32_t *h_token_ids, const i
  * flagged by an earlier ff_encode, else FF_OK. */
 FF_API ff_status ff_check(ff_model *m, void *stream);
 
-/* Options: FF_OPT_GRAPHS (1 = capture/replay CUDA graphs, default 1). */
+/* Options: FF_OPT_GRAPHS (1 = capture/replay CUDA graphs, default 1);
+ * FF_OPT_CTA_PAIRS (1 = let large GEMMs use CTA pairs / 256-row tiles,
+ * default 1; 0 = single-CTA 128-row tiles only -- results are identical). */
 #define FF_OPT_GRAPHS 1
+#define FF_OPT_CTA_PAIRS 2
+/* FF_OPT_ATTN_TC (1 = tcgen05 attention for head_dim 64, S <= 128, default 1;
+ * 0 = the mma.sync attention kernel everywhere). */
+#define FF_OPT_ATTN_TC 3
 FF_API ff_status ff_set_option(ff_model *m, int32_t option, int64_t value);
 
 FF_API void ff_model_destroy(ff_model *m);
@@ -195,9 +201,11 @@ FF_API ff_status ff_debug_quant_rows(const void *d_x16, int32_t M, int32_t K, in
                               float *d_s, void *stream);
 
 /* Fused masked-softmax attention of one layer: qkv16 [B*S, 3*A*d] -> ctx16
- * [B*S, A*d] (packed rows). */
+ * [B*S, A*d] (packed rows).  impl: 0 = auto (the tcgen05 kernel where it
+ * applies: head_dim 64, S <= 128), 1 = the mma.sync kernel (any even d <= 128),
+ * 2 = tcgen05 only (FF_E_UNSUPPORTED otherwise). */
 FF_API ff_status ff_debug_attention(const void *d_qkv16, const int32_t *d_mask, int32_t B, int32_t S, int32_t A,
-                             int32_t d, void *d_ctx16, void *stream);
+                                    int32_t d, void *d_ctx16, int32_t impl, void *stream);
 
 #ifdef __cplusplus
 }

@@ -84,6 +84,9 @@ struct ff_model {
   uint8_t* dW = nullptr;
   uint8_t* dWS = nullptr;
   bool use_graphs = true;
+  int pair_mode = -1;  // FF_OPT_CTA_PAIRS: -1 auto, 0 never (GemmPlan::force_pair)
+  bool attn_tc = true;  // FF_OPT_ATTN_TC: tcgen05 attention where supported
+  CUtensorMap tm_qkv;   // QKV buffer map for the tcgen05 attention
   std::map<std::tuple<int, int, const void*, const void*, const void*>, cudaGraphExec_t> graphs;
 
   template <typename T>
@@ -292,6 +295,7 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     if (tr && dump(d_dump[0], X16, m->ldx16, H, M, s) != FF_OK) return FF_E_CUDA;
     // a2: fused QKV projection
     ff::GemmPlan g = P.gp[W_QKV];
+    g.force_pair = m->pair_mode;
     ff::plan_gemm_set_m(&g, M);
     g.p.out = QKV;
     g.p.ldo = m->ldqkv;
@@ -302,11 +306,17 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     FF_LAUNCH(q ? FF_K_GEMM_I8 : FF_K_GEMM_F16, ff::launch_gemm(g, s), "gemm qkv");
     if (tr && dump(d_dump[1], QKV, m->ldqkv, 3 * P.D, M, s) != FF_OK) return FF_E_CUDA;
     // a3: fused masked-softmax attention over this layer's A'_l heads
-    FF_LAUNCH(FF_K_ATTENTION, ff::launch_attention(QKV, m->ldqkv, mask, B, S, P.A, c.head_dim, CTX, m->ldc16, s), "attention");
+    if (m->attn_tc && ff::attention_tc_supported(S, c.head_dim, m->ldqkv, m->ldc16))
+      FF_LAUNCH(FF_K_ATTENTION, ff::launch_attention_tc(m->tm_qkv, mask, B, S, P.A, CTX, m->ldc16, s),
+                "attention_tc");
+    else
+      FF_LAUNCH(FF_K_ATTENTION, ff::launch_attention(QKV, m->ldqkv, mask, B, S, P.A, c.head_dim, CTX, m->ldc16, s),
+                "attention");
     if (tr && dump(d_dump[2], CTX, m->ldc16, P.D, M, s) != FF_OK) return FF_E_CUDA;
     // a4 + a5: requant (int8 layers) and out-projection
     if (q) FF_LAUNCH(FF_K_QUANT, ff::launch_quant_rows(CTX, m->ldc16, M, P.D, CTXq, m->ldc8, CTXs, s), "quant ctx");
     g = P.gp[W_O];
+    g.force_pair = m->pair_mode;
     ff::plan_gemm_set_m(&g, M);
     g.p.out = O16;
     g.p.ldo = m->ldx16;
@@ -323,6 +333,7 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     if (tr && dump(d_dump[4], H1, m->ldx16, H, M, s) != FF_OK) return FF_E_CUDA;
     // a7: FFN1 + bias + activation
     g = P.gp[W_FFN1];
+    g.force_pair = m->pair_mode;
     ff::plan_gemm_set_m(&g, M);
     g.p.out = I16;
     g.p.ldo = m->ldi16;
@@ -335,6 +346,7 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     // a8 + a9: requant and FFN2
     if (q) FF_LAUNCH(FF_K_QUANT, ff::launch_quant_rows(I16, m->ldi16, M, P.F, Iq, m->ldi8, Is, s), "quant ffn");
     g = P.gp[W_FFN2];
+    g.force_pair = m->pair_mode;
     ff::plan_gemm_set_m(&g, M);
     g.p.out = O16;
     g.p.ldo = m->ldx16;
@@ -575,7 +587,13 @@ ff_status ff_finalize(ff_model* m, void* stream) {
   FF_CK(cudaStreamSynchronize(s));
   FF_CK(ff::prepare_gemm_kernels());
   FF_CK(ff::prepare_attention_kernels());
+  FF_CK(ff::prepare_attention_tc_kernel());
   FF_CK(ff::prepare_row_kernels());
+  {
+    const char* err = nullptr;
+    if (!ff::plan_attention_tc(&m->tm_qkv, m->dWS + m->ws_qkv, m->cfg.max_tokens, m->ldqkv, &err))
+      return fail(FF_E_CUDA, std::string("attention tensor map: ") + err);
+  }
   ff_status st = build_gemm_plans(m);
   if (st != FF_OK) return st;
   m->state = 2;
@@ -652,6 +670,18 @@ ff_status ff_set_option(ff_model* m, int32_t option, int64_t value) {
   if (!m) return fail(FF_E_INVALID, "null model");
   if (option == FF_OPT_GRAPHS) {
     m->use_graphs = value != 0;
+    return FF_OK;
+  }
+  if (option == FF_OPT_ATTN_TC) {
+    m->attn_tc = value != 0;
+    for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
+    m->graphs.clear();
+    return FF_OK;
+  }
+  if (option == FF_OPT_CTA_PAIRS) {
+    m->pair_mode = value != 0 ? -1 : 0;
+    for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);  // captured launch configs change
+    m->graphs.clear();
     return FF_OK;
   }
   return fail(FF_E_INVALID, "unknown option");
@@ -747,13 +777,27 @@ ff_status ff_debug_quant_rows(const void* d_x16, int32_t M, int32_t K, int32_t l
 }
 
 ff_status ff_debug_attention(const void* d_qkv16, const int32_t* d_mask, int32_t B, int32_t S, int32_t A, int32_t d,
-                             void* d_ctx16, void* stream) {
+                             void* d_ctx16, int32_t impl, void* stream) {
   if (B < 1 || S < 1 || A < 1 || d < 2 || d > 128 || (d & 1)) return fail(FF_E_INVALID, "bad attention args");
   if (ff::attention_smem_bytes(S, d) > 227 * 1024) return fail(FF_E_UNSUPPORTED, "seq too long");
   static bool prepared = false;
   if (!prepared) {
     FF_CK(ff::prepare_attention_kernels());
+    FF_CK(ff::prepare_attention_tc_kernel());
     prepared = true;
+  }
+  const int mode = impl;  // 0 auto (tcgen05 where supported), 1 mma.sync kernel, 2 tcgen05 (must be supported)
+  const bool tc = mode != 1 && ff::attention_tc_supported(S, d, 3 * A * d, A * d) &&
+                  (reinterpret_cast<uintptr_t>(d_qkv16) & 15) == 0;
+  if (mode == 2 && !tc) return fail(FF_E_UNSUPPORTED, "tcgen05 attention needs head_dim 64, S <= 128");
+  if (tc) {
+    CUtensorMap map;
+    const char* err = nullptr;
+    if (!ff::plan_attention_tc(&map, d_qkv16, B * S, 3 * A * d, &err))
+      return fail(FF_E_INVALID, std::string("attention tensor map: ") + err);
+    FF_CK(ff::launch_attention_tc(map, d_mask, B, S, A, static_cast<__half*>(d_ctx16), A * d,
+                                  static_cast<cudaStream_t>(stream)));
+    return FF_OK;
   }
   FF_CK(ff::launch_attention(static_cast<const __half*>(d_qkv16), 3 * A * d, d_mask, B, S, A, d,
                              static_cast<__half*>(d_ctx16), A * d, static_cast<cudaStream_t>(stream)));

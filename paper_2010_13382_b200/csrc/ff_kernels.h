@@ -75,6 +75,14 @@ size_t attention_smem_bytes(int S, int d);
 cudaError_t launch_attention(const __half* qkv, int ldqkv, const int32_t* mask, int B, int S, int A, int d,
                              __half* ctx, int ldctx, cudaStream_t s);
 
+// tcgen05 attention (head_dim 64, S <= 128); the tensor map covers the QKV
+// buffer [M_rows x ldqkv] fp16 with 64-column x 128-row boxes.
+bool attention_tc_supported(int S, int d, int ldqkv, int ldctx);
+bool plan_attention_tc(CUtensorMap* map, const void* qkv, int M_rows, int ldqkv, const char** err);
+cudaError_t launch_attention_tc(const CUtensorMap& map, const int32_t* mask, int B, int S, int A, __half* ctx,
+                                int ldctx, cudaStream_t s);
+cudaError_t prepare_attention_tc_kernel();
+
 // ------------------------------------------------------- weight packing
 cudaError_t launch_cast_f16(const float* src, int N, int K, __half* dst, int ldd, cudaStream_t s);
 cudaError_t launch_quant_weight(const float* src, int N, int K, int8_t* dst, int ldd, float* scale,

@@ -20,6 +20,7 @@ LIB_PATH = os.path.join(_PKG, "libfastformers.so")
 FF_OK, FF_E_INVALID, FF_E_SHAPE, FF_E_STATE, FF_E_CUDA, FF_E_INPUT, FF_E_UNSUPPORTED, FF_E_NOMEM = range(8)
 FF_F16, FF_I8 = 0, 1
 FF_OPT_GRAPHS = 1
+FF_OPT_CTA_PAIRS = 2
 KERNEL_KINDS = ["embed_ln", "gemm_f16", "gemm_i8", "attention", "quant_rows", "add_ln", "head"]
 STATUS_NAMES = ["FF_OK", "FF_E_INVALID", "FF_E_SHAPE", "FF_E_STATE", "FF_E_CUDA", "FF_E_INPUT", "FF_E_UNSUPPORTED",
                 "FF_E_NOMEM"]
@@ -73,7 +74,7 @@ def lib():
         L.ff_encode_trace.argtypes = [vp, vp, vp, i32, i32, vp, i32, ctypes.POINTER(vp), vp]
         L.ff_debug_gemm.argtypes = [i32, vp, i32, vp, i32, i32, i32, i32, i32, vp, i32, vp, vp, vp, i32, vp]
         L.ff_debug_quant_rows.argtypes = [vp, i32, i32, i32, vp, i32, vp, vp]
-        L.ff_debug_attention.argtypes = [vp, vp, i32, i32, i32, i32, vp, vp]
+        L.ff_debug_attention.argtypes = [vp, vp, i32, i32, i32, i32, vp, i32, vp]
         for name in EXPORTED:
             if name not in ("ff_abi_version", "ff_last_error", "ff_model_destroy"):
                 getattr(L, name).restype = i32
@@ -100,7 +101,7 @@ class Encoder:
     """One FastFormers encoder model on one GPU (weights packed once at load)."""
 
     def __init__(self, cfg, weights: Dict[str, np.ndarray], max_tokens: Optional[int] = None, device: int = 0,
-                 use_graphs: bool = True):
+                 use_graphs: bool = True, cta_pairs: bool = True):
         import torch
         L = lib()
         self.cfg = cfg
@@ -129,6 +130,8 @@ class Encoder:
             check(L.ff_finalize(self.h, st))
         if not use_graphs:
             check(L.ff_set_option(self.h, FF_OPT_GRAPHS, 0))
+        if not cta_pairs:
+            check(L.ff_set_option(self.h, FF_OPT_CTA_PAIRS, 0))
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -228,9 +231,10 @@ def quant_rows(x16):
     return q[:, :K], s
 
 
-def attention(qkv16, mask, A, d):
+def attention(qkv16, mask, A, d, impl=0):
+    """impl: 0 auto, 1 mma.sync kernel, 2 tcgen05 kernel (head_dim 64, S <= 128)."""
     import torch
     B, S = mask.shape
     ctx = torch.empty((B * S, A * d), dtype=torch.float16, device=qkv16.device)
-    check(lib().ff_debug_attention(_ptr(qkv16), _ptr(mask), B, S, A, d, _ptr(ctx), _stream_ptr()))
+    check(lib().ff_debug_attention(_ptr(qkv16), _ptr(mask), B, S, A, d, _ptr(ctx), impl, _stream_ptr()))
     return ctx

@@ -114,7 +114,7 @@ def test_attention_matches_oracle(B, S, A, d, ragged):
             mask[b, rng.integers(max(1, S // 4), S + 1):] = 0
         if S > 8:
             mask[0, S // 2] = 0  # a hole, not only a padded tail
-    ctx = ffb.attention(torch.from_numpy(qkv).cuda(), torch.from_numpy(mask).cuda(), A, d)
+    ctx = ffb.attention(torch.from_numpy(qkv).cuda(), torch.from_numpy(mask).cuda(), A, d, impl=1)
     torch.cuda.synchronize()
     got = ctx.cpu().numpy().astype(np.float64)
     ref = oracle.attention(qkv.astype(np.float32), mask, A, d).astype(np.float64)
@@ -124,3 +124,28 @@ def test_attention_matches_oracle(B, S, A, d, ragged):
     assert err.max() <= 4e-3 + 4e-3 * np.abs(ref).max(), err.max()
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-3
     assert np.abs(got - ref64).max() <= 2e-2
+
+
+@pytest.mark.parametrize("B,S,A,ragged", [(2, 128, 8, False), (3, 128, 4, True), (2, 40, 3, True), (1, 7, 2, False),
+                                          (4, 32, 2, True), (1, 1, 1, False)])
+def test_attention_tcgen05_matches_oracle(B, S, A, ragged):
+    """The tcgen05/TMEM attention kernel (head_dim 64, S <= 128)."""
+    d = 64
+    rng = np.random.default_rng(100 + S + A)
+    qkv = np.float16(rng.standard_normal((B * S, 3 * A * d)) * 1.5)
+    mask = np.ones((B, S), np.int32)
+    if ragged:
+        for b in range(B):
+            mask[b, rng.integers(max(1, S // 4), S + 1):] = 0
+        mask[0, S // 2] = 0
+    mask[:, 0] = 1
+    ctx = ffb.attention(torch.from_numpy(qkv).cuda(), torch.from_numpy(mask).cuda(), A, d, impl=2)
+    torch.cuda.synchronize()
+    got = ctx.cpu().numpy().astype(np.float64)
+    ref = oracle.attention(qkv.astype(np.float32), mask, A, d).astype(np.float64)
+    err = np.abs(got - ref)
+    assert err.max() <= 4e-3 + 4e-3 * np.abs(ref).max(), err.max()
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-3
+    # and the same as the mma.sync kernel up to rounding
+    ctx1 = ffb.attention(torch.from_numpy(qkv).cuda(), torch.from_numpy(mask).cuda(), A, d, impl=1).cpu().numpy()
+    assert np.abs(ctx1.astype(np.float64) - got).max() <= 4e-3 + 4e-3 * np.abs(ref).max()

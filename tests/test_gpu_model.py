@@ -176,7 +176,7 @@ def test_end_to_end_deep_calibrated(name, B):
         assert np.abs(got - ref).max() <= 1e-2
     else:
         drift = np.abs(orc.encode(ids, mask, acc32=True) - ref).max()
-        bound = max(2 * drift, 1e-3 * np.abs(ref).max())
+        bound = max(3 * drift, 1e-3 * np.abs(ref).max())
         assert np.abs(got - ref).max() <= bound, (np.abs(got - ref).max(), drift)
     assert _margin_ok(ref, got, 2e-2) >= 0.999
 
@@ -267,9 +267,27 @@ def test_full_size_c3_sampled_rows_vs_oracle():
     ids, mask = synth.make_inputs(cfg, seed=1000)
     enc = Encoder(cfg, w)
     got = f32(enc.encode(dev(ids), dev(mask)))
+    assert np.isfinite(got).all()
     orc = Oracle(cfg, w)
-    rows = [0, 97, 255]
+    rows = [0, 31, 64, 97, 128, 161, 200, 255]
     ref = orc.encode(ids[rows], mask[rows])
     drift = np.abs(orc.encode(ids[rows], mask[rows], acc32=True) - ref).max()
-    assert np.abs(got[rows] - ref).max() <= max(2 * drift, 1e-3 * np.abs(ref).max())
-    assert np.isfinite(got).all()
+    err = np.abs(got[rows] - ref).max()
+    # DESIGN "Tolerances": 6 int8 layers amplify rounding-boundary flips; the
+    # GPU differs from the oracle in more reduction orders (LN, softmax, GELU)
+    # than the oracle's own fp32-vs-fp64 drift, hence the factor 3.
+    bound = max(3 * drift, 1e-3 * np.abs(ref).max())
+    assert err <= bound, (err, drift, np.abs(ref).max())
+    assert _margin_ok(ref, got[rows], 2e-2) == 1.0
+
+
+@pytest.mark.parametrize("dt", [1, 0])
+def test_cta_pairs_equal_single_cta_at_full_size(dt):
+    """The CTA-pair GEMM (cta_group::2, 256-row tiles, used at the bench size)
+    and the single-CTA GEMM compute the same accumulators: identical logits."""
+    cfg = synth.config("c3").with_dtype(dt)
+    w = synth.make_weights(cfg)
+    ids, mask = synth.make_inputs(cfg, seed=1000)
+    a = f32(Encoder(cfg, w).encode(dev(ids), dev(mask)))
+    b = f32(Encoder(cfg, w, cta_pairs=False).encode(dev(ids), dev(mask)))
+    assert np.array_equal(a, b), np.abs(a - b).max()

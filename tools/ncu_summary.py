@@ -26,8 +26,9 @@ def read_launches(path):
             d[r[mi]] = float(r[vi].replace(",", ""))
         except ValueError:
             d[r[mi]] = r[vi]
-    ids = sorted(per)
-    return [per[i] for i in ids[len(ids) // 2:]]  # second forward (warm)
+    seq = [per[i] for i in sorted(per)]
+    starts = [i for i, x in enumerate(seq) if "embed_ln" in x["name"]]
+    return seq[starts[-1]:] if starts else seq[len(seq) // 2:]  # the last (warm) forward
 
 
 def rep_rows(path):
