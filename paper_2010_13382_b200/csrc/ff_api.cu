@@ -61,6 +61,9 @@ struct LayerPlan {
   size_t ln1g, ln1b, ln2g, ln2b;
   uint32_t loaded = 0;
   ff::GemmPlan gp[4];
+  // row-reduction GEMMs: [0] out-proj + LN1, [1] FFN1 + requant, [2] FFN2 + LN2
+  ff::RRPlan rp[3];
+  bool rr_ok[2] = {false, false};  // [0] LN fusion (N = H), [1] FFN1 requant fusion (N = F', int8)
 };
 
 }  // namespace
@@ -86,6 +89,7 @@ struct ff_model {
   bool use_graphs = true;
   int pair_mode = -1;  // FF_OPT_CTA_PAIRS: -1 auto, 0 never (GemmPlan::force_pair)
   bool attn_tc = true;  // FF_OPT_ATTN_TC: tcgen05 attention where supported
+  bool fused = true;    // FF_OPT_FUSED_EPILOGUES: cluster row-reduction GEMM epilogues
   CUtensorMap tm_qkv;   // QKV buffer map for the tcgen05 attention
   std::map<std::tuple<int, int, const void*, const void*, const void*>, cudaGraphExec_t> graphs;
 
@@ -221,6 +225,32 @@ ff_status build_gemm_plans(ff_model* m) {
       if (!ff::plan_gemm_output(&P.gp[i], out, ldo, &err))
         return fail(FF_E_CUDA, std::string("output tensor map: ") + err);
     }
+    // fused row-reduction epilogues where the output row fits a cluster (N = 256 x 1..8)
+    const bool q = P.dt == FF_I8;
+    const char* err = nullptr;
+    P.rr_ok[0] = ff::rr_supported(m->cfg.hidden);
+    P.rr_ok[1] = q && ff::rr_supported(P.F);
+    if (P.rr_ok[0]) {
+      int lda;
+      const void* A = gemm_a(m, P, W_O, &lda);
+      if (!ff::plan_rr(&P.rp[0], q, A, m->cfg.max_tokens, lda, m->dW + P.w[W_O], P.ldw[W_O], P.N[W_O], P.K[W_O],
+                       m->dWS + m->ws_h1, m->ldx16, &err))
+        return fail(FF_E_CUDA, std::string("rr tensor map: ") + err);
+      P.rp[0].p.mode = ff::RR_LN;
+      A = gemm_a(m, P, W_FFN2, &lda);
+      if (!ff::plan_rr(&P.rp[2], q, A, m->cfg.max_tokens, lda, m->dW + P.w[W_FFN2], P.ldw[W_FFN2], P.N[W_FFN2],
+                       P.K[W_FFN2], m->dWS + m->ws_x16, m->ldx16, &err))
+        return fail(FF_E_CUDA, std::string("rr tensor map: ") + err);
+      P.rp[2].p.mode = ff::RR_LN;
+    }
+    if (P.rr_ok[1]) {
+      int lda;
+      const void* A = gemm_a(m, P, W_FFN1, &lda);
+      if (!ff::plan_rr(&P.rp[1], true, A, m->cfg.max_tokens, lda, m->dW + P.w[W_FFN1], P.ldw[W_FFN1], P.N[W_FFN1],
+                       P.K[W_FFN1], m->dWS + m->ws_i, m->ldi16, &err))
+        return fail(FF_E_CUDA, std::string("rr tensor map: ") + err);
+      P.rp[1].p.mode = ff::RR_QUANT;
+    }
   }
   return FF_OK;
 }
@@ -315,6 +345,26 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     if (tr && dump(d_dump[2], CTX, m->ldc16, P.D, M, s) != FF_OK) return FF_E_CUDA;
     // a4 + a5: requant (int8 layers) and out-projection
     if (q) FF_LAUNCH(FF_K_QUANT, ff::launch_quant_rows(CTX, m->ldc16, M, P.D, CTXq, m->ldc8, CTXs, s), "quant ctx");
+    const bool fuse_ln = m->fused && P.rr_ok[0];
+    const bool fuse_q = m->fused && q && P.rr_ok[1];
+    if (fuse_ln) {
+      // a5 + a6 fused: H1 = LN1(R16(O) + X16) (+ s8 rows) in the out-proj epilogue
+      ff::RRPlan r = P.rp[0];
+      ff::plan_rr_set_m(&r, M);
+      r.p.bias = m->w<float>(P.bias[W_O]);
+      r.p.row_scale = q ? CTXs : nullptr;
+      r.p.col_scale = q ? m->w<float>(P.sw[W_O]) : nullptr;
+      r.p.residual = X16;
+      r.p.ldr = m->ldx16;
+      r.p.gamma = m->w<float>(P.ln1g);
+      r.p.beta = m->w<float>(P.ln1b);
+      r.p.eps = c.ln_eps;
+      r.p.store16 = 1;
+      r.p.outq = q ? H1q : nullptr;
+      r.p.ldq = m->ldx8;
+      r.p.out_scale = q ? H1s : nullptr;
+      FF_LAUNCH(q ? FF_K_GEMM_I8 : FF_K_GEMM_F16, ff::launch_rr(r, s), "gemm o + ln1");
+    } else {
     g = P.gp[W_O];
     g.force_pair = m->pair_mode;
     ff::plan_gemm_set_m(&g, M);
@@ -330,8 +380,25 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     FF_LAUNCH(FF_K_ADD_LN, ff::launch_add_ln(O16, m->ldx16, X16, m->ldx16, M, H, m->w<float>(P.ln1g), m->w<float>(P.ln1b),
                                 c.ln_eps, H1, m->ldx16, q ? H1q : nullptr, m->ldx8, q ? H1s : nullptr, s),
               "add_ln1");
+    }
     if (tr && dump(d_dump[4], H1, m->ldx16, H, M, s) != FF_OK) return FF_E_CUDA;
     // a7: FFN1 + bias + activation
+    if (fuse_q) {
+      // a7 + a8 fused: Iq, Is = Q8row(R16(act(FFN1))) in the FFN1 epilogue; the
+      // fp16 copy of I is only materialised when a trace asks for it
+      ff::RRPlan r = P.rp[1];
+      ff::plan_rr_set_m(&r, M);
+      r.p.bias = m->w<float>(P.bias[W_FFN1]);
+      r.p.row_scale = H1s;
+      r.p.col_scale = m->w<float>(P.sw[W_FFN1]);
+      r.p.act = c.act;
+      r.p.store16 = tr ? 1 : 0;
+      r.p.outq = Iq;
+      r.p.ldq = m->ldi8;
+      r.p.out_scale = Is;
+      FF_LAUNCH(FF_K_GEMM_I8, ff::launch_rr(r, s), "gemm ffn1 + quant");
+      if (tr && dump(d_dump[5], I16, m->ldi16, P.F, M, s) != FF_OK) return FF_E_CUDA;
+    } else {
     g = P.gp[W_FFN1];
     g.force_pair = m->pair_mode;
     ff::plan_gemm_set_m(&g, M);
@@ -345,6 +412,26 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     if (tr && dump(d_dump[5], I16, m->ldi16, P.F, M, s) != FF_OK) return FF_E_CUDA;
     // a8 + a9: requant and FFN2
     if (q) FF_LAUNCH(FF_K_QUANT, ff::launch_quant_rows(I16, m->ldi16, M, P.F, Iq, m->ldi8, Is, s), "quant ffn");
+    }
+    const bool nq = l + 1 < c.num_layers && m->L[l + 1].dt == FF_I8;
+    if (fuse_ln) {
+      // a9 + a10 fused: X16 = LN2(R16(Y) + H1) (+ s8 rows for the next int8 layer)
+      ff::RRPlan r = P.rp[2];
+      ff::plan_rr_set_m(&r, M);
+      r.p.bias = m->w<float>(P.bias[W_FFN2]);
+      r.p.row_scale = q ? Is : nullptr;
+      r.p.col_scale = q ? m->w<float>(P.sw[W_FFN2]) : nullptr;
+      r.p.residual = H1;
+      r.p.ldr = m->ldx16;
+      r.p.gamma = m->w<float>(P.ln2g);
+      r.p.beta = m->w<float>(P.ln2b);
+      r.p.eps = c.ln_eps;
+      r.p.store16 = 1;
+      r.p.outq = nq ? Xq : nullptr;
+      r.p.ldq = m->ldx8;
+      r.p.out_scale = nq ? Xs : nullptr;
+      FF_LAUNCH(q ? FF_K_GEMM_I8 : FF_K_GEMM_F16, ff::launch_rr(r, s), "gemm ffn2 + ln2");
+    } else {
     g = P.gp[W_FFN2];
     g.force_pair = m->pair_mode;
     ff::plan_gemm_set_m(&g, M);
@@ -357,10 +444,10 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     FF_LAUNCH(q ? FF_K_GEMM_I8 : FF_K_GEMM_F16, ff::launch_gemm(g, s), "gemm ffn2");
     if (tr && dump(d_dump[6], O16, m->ldx16, H, M, s) != FF_OK) return FF_E_CUDA;
     // a10: residual + LN2 (+ s8 rows when the next layer is int8)
-    const bool nq = l + 1 < c.num_layers && m->L[l + 1].dt == FF_I8;
     FF_LAUNCH(FF_K_ADD_LN, ff::launch_add_ln(O16, m->ldx16, H1, m->ldx16, M, H, m->w<float>(P.ln2g), m->w<float>(P.ln2b),
                                 c.ln_eps, X16, m->ldx16, nq ? Xq : nullptr, m->ldx8, nq ? Xs : nullptr, s),
               "add_ln2");
+    }
     if (tr && dump(d_dump[7], X16, m->ldx16, H, M, s) != FF_OK) return FF_E_CUDA;
   }
   // a11: pooler + classifier
@@ -588,6 +675,7 @@ ff_status ff_finalize(ff_model* m, void* stream) {
   FF_CK(ff::prepare_gemm_kernels());
   FF_CK(ff::prepare_attention_kernels());
   FF_CK(ff::prepare_attention_tc_kernel());
+  FF_CK(ff::prepare_rr_kernels());
   FF_CK(ff::prepare_row_kernels());
   {
     const char* err = nullptr;
@@ -672,6 +760,12 @@ ff_status ff_set_option(ff_model* m, int32_t option, int64_t value) {
     m->use_graphs = value != 0;
     return FF_OK;
   }
+  if (option == FF_OPT_FUSED_EPILOGUES) {
+    m->fused = value != 0;
+    for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
+    m->graphs.clear();
+    return FF_OK;
+  }
   if (option == FF_OPT_ATTN_TC) {
     m->attn_tc = value != 0;
     for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
@@ -698,7 +792,15 @@ ff_status ff_launch_count(const ff_model* m, int32_t batch, int32_t seq, int32_t
   (void)batch;
   (void)seq;
   int n = 3;  // embed_ln + pooler + classifier
-  for (const LayerPlan& P : m->L) n += 7 + (P.dt == FF_I8 ? 2 : 0);
+  for (const LayerPlan& P : m->L) {
+    const bool q = P.dt == FF_I8;
+    const bool fln = m->fused && P.rr_ok[0], fq = m->fused && P.rr_ok[1];
+    n += 2;                              // QKV GEMM + attention
+    n += q ? 1 : 0;                      // ctx requant
+    n += fln ? 1 : 2;                    // out-proj (+ add_ln1)
+    n += fq ? 1 : (q ? 2 : 1);           // FFN1 (+ requant)
+    n += fln ? 1 : 2;                    // FFN2 (+ add_ln2)
+  }
   *count = n;
   return FF_OK;
 }

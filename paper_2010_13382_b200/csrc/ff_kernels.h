@@ -53,6 +53,44 @@ bool plan_gemm_output(GemmPlan* g, void* out, int ldo, const char** err);
 void plan_gemm_set_m(GemmPlan* g, int M);
 cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t s);
 
+// -------------------------------------------- row-reduction GEMM epilogues
+// GEMM whose epilogue needs whole output rows: a cluster of CN = N/256 CTAs
+// spans the row (one 128x256 tile each) and exchanges per-row partials through
+// DSMEM (st.async + mbarrier).
+//   RR_LN:    y = LN(R16(acc-epilogue) + residual) -> fp16 [+ s8 rows + scale]
+//             (post-LN residual + LayerNorm fused into out-proj / FFN2)
+//   RR_QUANT: y = R16(act(acc-epilogue)) -> s8 rows + scale [+ fp16 copy]
+//             (FFN-intermediate requant fused into FFN1)
+enum RRMode { RR_LN = 1, RR_QUANT = 2 };
+struct RRParams {
+  int M, N, K, m_tiles, k_blocks;
+  int mode;
+  const float* bias;       // [N]
+  const float* row_scale;  // sx [M] (int8 A)
+  const float* col_scale;  // sw [N] (int8 W)
+  int act;                 // RR_QUANT
+  const __half* residual;  // RR_LN: [M, ldr]
+  int ldr;
+  const float* gamma;      // RR_LN
+  const float* beta;
+  float eps;
+  int store16;             // write the fp16 result through tmC
+  int8_t* outq;            // s8 rows [M, ldq] or null
+  int ldq;
+  float* out_scale;        // [M] or null
+};
+struct RRPlan {
+  CUtensorMap tmA, tmB, tmC;
+  RRParams p;
+  int i8, cn, grid, M_rows;
+};
+bool rr_supported(int N);
+bool plan_rr(RRPlan* g, bool i8, const void* A, int M_rows, int lda, const void* W, int ldw, int N, int K,
+             void* out16, int ldo, const char** err);
+void plan_rr_set_m(RRPlan* g, int M);
+cudaError_t launch_rr(const RRPlan& g, cudaStream_t s);
+cudaError_t prepare_rr_kernels();
+
 // ------------------------------------------------------------ row kernels
 // X = LN(E_tok[id] + Ppos'[t]) -> x16 [M, ldx] (+ optional s8 xq [M, ldq], xs [M]).
 // Validates ids / mask into *err_flag (sticky bits).

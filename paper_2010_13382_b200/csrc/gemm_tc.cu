@@ -360,6 +360,366 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ========================================================================
+// Row-reduction GEMM: C tile rows span a cluster of CN CTAs along N.
+// Same producer / MMA roles as gemm_tc_kernel (single-CTA MMA, BN = 256, 3
+// smem stages); the epilogue warps make several passes over their TMEM
+// accumulator (writing intermediates back into TMEM with tcgen05.st) and
+// combine per-row partials of all 2*CN column-halves of the row through
+// DSMEM: every thread st.async's its partial into a slot of every CTA of the
+// cluster, which signals an mbarrier armed with the expected bytes; each CTA
+// then sums the 2*CN partials in the same fixed order, so all CTAs derive
+// bit-identical row statistics.
+// ========================================================================
+constexpr int kRRStages = 3;
+constexpr int kRRBN = 256;
+struct RRCfg {
+  static constexpr int A_BYTES = BM * BK_BYTES;
+  static constexpr int B_BYTES = kRRBN * BK_BYTES;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int EPI_OFF = kRRStages * STAGE_BYTES;
+  static constexpr int RED_OFF = EPI_OFF + kEpiWarps * 2 * kStageTile;
+  static constexpr int RED_FLOATS = 2 * 8 * 2 * 128;  // [buf][rank<=8][half][row]
+  static constexpr int BAR_OFF = RED_OFF + RED_FLOATS * 4;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static_assert(SMEM <= 227 * 1024, "smem budget");
+};
+
+// tcgen05.ld of 16 columns (packed fp16 pairs written back by a previous pass).
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+__device__ __forceinline__ int8_t quant1_dev(float x, float s) {
+  float v = rintf(__fdiv_rn(x, s));  // RNE (R8), IEEE division (R6)
+  v = fminf(fmaxf(v, -127.0f), 127.0f);
+  return static_cast<int8_t>(static_cast<int>(v));
+}
+
+template <bool I8>
+__device__ __forceinline__ float dequant1(uint32_t r, float sx, float sw, float b) {
+  return I8 ? __fmaf_rn(__int2float_rn(static_cast<int>(r)), __fmul_rn(sx, sw), b) : __fadd_rn(__uint_as_float(r), b);
+}
+
+template <bool I8, int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_rr_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmC, RRParams p) {
+  constexpr int STAGES = kRRStages;
+  constexpr int BN = kRRBN;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * RRCfg::A_BYTES;
+  uint8_t* sEpi = smem + RRCfg::EPI_OFF;
+  float* red = reinterpret_cast<float*>(smem + RRCfg::RED_OFF);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + RRCfg::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* redbar = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(redbar + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int CN = (int)cluster_nctarank();
+  const int unit = (int)blockIdx.x / CN;
+  const int nunits = (int)gridDim.x / CN;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    if (p.store16) tma_prefetch(&tmC);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kEpiWarps);
+      mbar_init(&redbar[a], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_slot, 2 * BN);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // every CTA's reduction barriers exist before any st.async
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  constexpr int KE = I8 ? 128 : 64;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int mt = unit; mt < p.m_tiles; mt += nunits) {
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], RRCfg::STAGE_BYTES);
+          tma_load_2d(sA + stage * RRCfg::A_BYTES, &tmA, &full[stage], kb * KE, mt * BM, kEvictNormal);
+          tma_load_2d(sB + stage * RRCfg::B_BYTES, &tmB, &full[stage], kb * KE, (int)rank * BN, kEvictLast);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc<I8, BM, BN>();
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int mt = unit; mt < p.m_tiles; mt += nunits) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = make_sw128_desc(sA + stage * RRCfg::A_BYTES);
+          const uint64_t bdesc = make_sw128_desc(sB + stage * RRCfg::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (I8) mma_i8(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            else mma_f16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    const int q = warp & 3;
+    const int hf = ew >> 2;
+    const int c_lo = hf * (BN / 2);
+    const int rowl = q * 32 + lane;  // row within the 128-row tile
+    uint8_t* stage_buf = sEpi + ew * 2 * kStageTile;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int nbuf = 0;
+    int step = 0;  // reduction step counter (selects buffer / phase)
+    const float inv_n = 1.0f / (float)p.N;
+    (void)inv_n;
+
+    // Cluster-wide per-row reduction of v over the 2*CN column halves.
+    auto reduce_row = [&](float v, bool is_max) -> float {
+      const int b = step & 1;
+      const uint32_t ph = (uint32_t)(step >> 1) & 1u;
+      if (threadIdx.x == 128) mbar_expect_tx(&redbar[b], (uint32_t)CN * 2 * 128 * 4);
+      float* slot = red + (((b * 8 + (int)rank) * 2 + hf) * 128 + rowl);
+      const uint32_t s_local = smem_u32(slot), b_local = smem_u32(&redbar[b]);
+      for (int c = 0; c < CN; ++c) st_async_f32(mapa_shared(s_local, c), v, mapa_shared(b_local, c));
+      mbar_wait(&redbar[b], ph);
+      float r = is_max ? 0.0f : 0.0f;
+      for (int c = 0; c < CN; ++c)
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const float x = red[((b * 8 + c) * 2 + h2) * 128 + rowl];
+          r = is_max ? fmaxf(r, x) : r + x;
+        }
+      ++step;
+      return r;
+    };
+    auto store16 = [&](const uint32_t (&h)[16], int n0, int row0) {
+      uint8_t* buf = stage_buf + (nbuf & 1) * kStageTile;
+      if (lane == 0) bulk_wait_read<1>();
+      __syncwarp();
+      uint8_t* srow = buf + lane * 64;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const int pc = cc ^ ((lane >> 1) & 3);
+        *reinterpret_cast<uint4*>(srow + pc * 16) = make_uint4(h[4 * cc], h[4 * cc + 1], h[4 * cc + 2], h[4 * cc + 3]);
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(&tmC, buf, n0, row0);
+        bulk_commit();
+      }
+      ++nbuf;
+    };
+
+    for (int mt = unit; mt < p.m_tiles; mt += nunits) {
+      const int row0 = mt * BM + q * 32;
+      const int row = row0 + lane;
+      const bool row_ok = row < p.M;
+      const float sx = (I8 && row_ok) ? p.row_scale[row] : 0.0f;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      const int ncol0 = (int)rank * BN;
+      float amax = 0.0f;
+
+      if (MODE == RR_LN) {
+        // pass 1: x = R16(GEMM epilogue) + residual (R11); sum; x -> TMEM
+        float psum = 0.0f;
+#pragma unroll 1
+        for (int c = c_lo; c < c_lo + BN / 2; c += 32) {
+          const int n0 = ncol0 + c;
+          float bias[32], sw[32];
+          load32(bias, p.bias, n0, p.N);
+          if (I8) load32(sw, p.col_scale, n0, p.N);
+          uint4 rv[4];
+          const __half* rp = p.residual + (size_t)(row_ok ? row : 0) * p.ldr + n0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) rv[i] = __ldg(reinterpret_cast<const uint4*>(rp) + i);
+          uint32_t r[32];
+          tmem_ld32(tbase + c, r);
+          tmem_wait_ld();
+          const __half2* rh = reinterpret_cast<const __half2*>(rv);
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const float2 res = __half22float2(rh[j / 2]);
+            const float y0 = __half2float(__float2half_rn(dequant1<I8>(r[j], sx, sw[j], bias[j])));
+            const float y1 = __half2float(__float2half_rn(dequant1<I8>(r[j + 1], sx, sw[j + 1], bias[j + 1])));
+            const float x0 = __fadd_rn(y0, row_ok ? res.x : 0.0f), x1 = __fadd_rn(y1, row_ok ? res.y : 0.0f);
+            psum += x0;
+            psum += x1;
+            r[j] = __float_as_uint(x0);
+            r[j + 1] = __float_as_uint(x1);
+          }
+          tmem_st32(tbase + c, r);
+        }
+        tmem_wait_st();
+        const float mean = __fdiv_rn(reduce_row(psum, false), (float)p.N);
+        // pass 2: variance (two-pass)
+        float pvar = 0.0f;
+#pragma unroll 1
+        for (int c = c_lo; c < c_lo + BN / 2; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(tbase + c, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float dlt = __uint_as_float(r[j]) - mean;
+            pvar = __fmaf_rn(dlt, dlt, pvar);
+          }
+        }
+        const float var = __fdiv_rn(reduce_row(pvar, false), (float)p.N);
+        const float rstd = 1.0f / sqrtf(var + p.eps);
+        // pass 3: y = (x - mean) * rstd * g + b -> R16 -> fp16 store (+ packed y16 -> TMEM)
+#pragma unroll 1
+        for (int c = c_lo; c < c_lo + BN / 2; c += 32) {
+          const int n0 = ncol0 + c;
+          float g[32], bt[32];
+          load32(g, p.gamma, n0, p.N);
+          load32(bt, p.beta, n0, p.N);
+          uint32_t r[32];
+          tmem_ld32(tbase + c, r);
+          tmem_wait_ld();
+          uint32_t h[16];
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const float a0 = (__uint_as_float(r[j]) - mean) * rstd * g[j] + bt[j];
+            const float a1 = (__uint_as_float(r[j + 1]) - mean) * rstd * g[j + 1] + bt[j + 1];
+            const __half2 hh = __floats2half2_rn(a0, a1);
+            const float2 hf2 = __half22float2(hh);
+            amax = fmaxf(amax, fmaxf(fabsf(hf2.x), fabsf(hf2.y)));
+            h[j / 2] = *reinterpret_cast<const uint32_t*>(&hh);
+          }
+          if (p.outq) tmem_st16(tbase + c, h);
+          if (p.store16) store16(h, n0, row0);
+        }
+        if (p.outq) tmem_wait_st();
+      } else {  // RR_QUANT: y16 = R16(act(GEMM epilogue)); amax; packed y16 -> TMEM
+#pragma unroll 1
+        for (int c = c_lo; c < c_lo + BN / 2; c += 32) {
+          const int n0 = ncol0 + c;
+          float bias[32], sw[32];
+          load32(bias, p.bias, n0, p.N);
+          if (I8) load32(sw, p.col_scale, n0, p.N);
+          uint32_t r[32];
+          tmem_ld32(tbase + c, r);
+          tmem_wait_ld();
+          uint32_t h[16];
+          switch (p.act) {
+            case ACT_GELU: epi_chunk<I8, ACT_GELU>(r, bias, sw, sx, h); break;
+            case ACT_RELU: epi_chunk<I8, ACT_RELU>(r, bias, sw, sx, h); break;
+            case ACT_GELU_TANH: epi_chunk<I8, ACT_GELU_TANH>(r, bias, sw, sx, h); break;
+            default: epi_chunk<I8, ACT_NONE>(r, bias, sw, sx, h); break;
+          }
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h[e]));
+            amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
+          }
+          tmem_st16(tbase + c, h);
+          if (p.store16) store16(h, n0, row0);
+        }
+        tmem_wait_st();
+      }
+
+      if (p.outq) {
+        // Q8row over the whole row (R6-R8, R12): quantize the fp16-rounded values
+        const float rmax = reduce_row(amax, true);
+        const float sc = rmax == 0.0f ? 1.0f : __fdiv_rn(rmax, 127.0f);
+#pragma unroll 1
+        for (int c = c_lo; c < c_lo + BN / 2; c += 32) {
+          uint32_t h[16];
+          tmem_ld16(tbase + c, h);
+          tmem_wait_ld();
+          int8_t o[32];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h[e]));
+            o[2 * e] = quant1_dev(f.x, sc);
+            o[2 * e + 1] = quant1_dev(f.y, sc);
+          }
+          if (row_ok) {
+            uint4* dst = reinterpret_cast<uint4*>(p.outq + (size_t)row * p.ldq + ncol0 + c);
+            dst[0] = *reinterpret_cast<const uint4*>(&o[0]);
+            dst[1] = *reinterpret_cast<const uint4*>(&o[16]);
+          }
+        }
+        if (rank == 0 && hf == 0 && row_ok) p.out_scale[row] = sc;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // no CTA leaves while a peer may still st.async into it
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 2 * BN);
+  }
+}
+
 // ------------------------------------------------------------------- host
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -509,6 +869,79 @@ cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t s) {
   }
   if (g.i8) return g.bn == 256 ? launch_t<256, true, false>(g, s) : launch_t<128, true, false>(g, s);
   return g.bn == 256 ? launch_t<256, false, false>(g, s) : launch_t<128, false, false>(g, s);
+}
+
+// ------------------------------------------------- row-reduction GEMM host
+bool rr_supported(int N) { return N % kRRBN == 0 && N / kRRBN >= 1 && N / kRRBN <= 8; }
+
+bool plan_rr(RRPlan* g, bool i8, const void* A, int M_rows, int lda, const void* W, int ldw, int N, int K,
+             void* out16, int ldo, const char** err) {
+  if (!rr_supported(N)) {
+    *err = "row-reduction GEMM needs N = 256 * (1..8)";
+    return false;
+  }
+  const int eb = i8 ? 1 : 2;
+  g->i8 = i8 ? 1 : 0;
+  g->cn = N / kRRBN;
+  g->M_rows = M_rows;
+  if (!make_operand_map(&g->tmA, A, M_rows, K, eb, (size_t)lda * eb, BM, err)) return false;
+  if (!make_operand_map(&g->tmB, W, N, K, eb, (size_t)ldw * eb, kRRBN, err)) return false;
+  if (out16 != nullptr &&
+      !encode_2d(&g->tmC, out16, M_rows, N, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (size_t)ldo * 2, 32, 32,
+                 CU_TENSOR_MAP_SWIZZLE_64B, err))
+    return false;
+  RRParams& p = g->p;
+  p = RRParams{};
+  p.N = N;
+  p.K = K;
+  p.k_blocks = (K * eb + BK_BYTES - 1) / BK_BYTES;
+  p.act = ACT_NONE;
+  plan_rr_set_m(g, M_rows);
+  return true;
+}
+
+void plan_rr_set_m(RRPlan* g, int M) {
+  g->p.M = M;
+  g->p.m_tiles = (M + BM - 1) / BM;
+  const int max_clusters = kNumSMs / g->cn;
+  const int nc = g->p.m_tiles < max_clusters ? g->p.m_tiles : max_clusters;
+  g->grid = nc * g->cn;
+}
+
+template <bool I8, int MODE>
+static cudaError_t launch_rr_t(const RRPlan& g, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g.grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = RRCfg::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = g.cn;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_rr_kernel<I8, MODE>, g.tmA, g.tmB, g.tmC, g.p);
+}
+
+template <bool I8, int MODE>
+static cudaError_t set_rr_attr() {
+  return cudaFuncSetAttribute(gemm_rr_kernel<I8, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, RRCfg::SMEM);
+}
+
+cudaError_t prepare_rr_kernels() {
+  cudaError_t e;
+  if ((e = set_rr_attr<true, RR_LN>()) != cudaSuccess) return e;
+  if ((e = set_rr_attr<false, RR_LN>()) != cudaSuccess) return e;
+  if ((e = set_rr_attr<true, RR_QUANT>()) != cudaSuccess) return e;
+  return set_rr_attr<false, RR_QUANT>();
+}
+
+cudaError_t launch_rr(const RRPlan& g, cudaStream_t s) {
+  if (g.grid <= 0) return cudaSuccess;
+  if (g.p.mode == RR_LN) return g.i8 ? launch_rr_t<true, RR_LN>(g, s) : launch_rr_t<false, RR_LN>(g, s);
+  return g.i8 ? launch_rr_t<true, RR_QUANT>(g, s) : launch_rr_t<false, RR_QUANT>(g, s);
 }
 
 }  // namespace ff

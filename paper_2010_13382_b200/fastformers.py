@@ -21,6 +21,8 @@ FF_OK, FF_E_INVALID, FF_E_SHAPE, FF_E_STATE, FF_E_CUDA, FF_E_INPUT, FF_E_UNSUPPO
 FF_F16, FF_I8 = 0, 1
 FF_OPT_GRAPHS = 1
 FF_OPT_CTA_PAIRS = 2
+FF_OPT_ATTN_TC = 3
+FF_OPT_FUSED_EPILOGUES = 4
 KERNEL_KINDS = ["embed_ln", "gemm_f16", "gemm_i8", "attention", "quant_rows", "add_ln", "head"]
 STATUS_NAMES = ["FF_OK", "FF_E_INVALID", "FF_E_SHAPE", "FF_E_STATE", "FF_E_CUDA", "FF_E_INPUT", "FF_E_UNSUPPORTED",
                 "FF_E_NOMEM"]
@@ -101,7 +103,7 @@ class Encoder:
     """One FastFormers encoder model on one GPU (weights packed once at load)."""
 
     def __init__(self, cfg, weights: Dict[str, np.ndarray], max_tokens: Optional[int] = None, device: int = 0,
-                 use_graphs: bool = True, cta_pairs: bool = True):
+                 use_graphs: bool = True, cta_pairs: bool = True, attn_tc: bool = True, fused: bool = True):
         import torch
         L = lib()
         self.cfg = cfg
@@ -130,6 +132,11 @@ class Encoder:
             check(L.ff_finalize(self.h, st))
         if not use_graphs:
             check(L.ff_set_option(self.h, FF_OPT_GRAPHS, 0))
+        if not attn_tc:
+            check(L.ff_set_option(self.h, FF_OPT_ATTN_TC, 0))
+        if not fused:
+            check(L.ff_set_option(self.h, FF_OPT_FUSED_EPILOGUES, 0))
+        self.fused = fused
         if not cta_pairs:
             check(L.ff_set_option(self.h, FF_OPT_CTA_PAIRS, 0))
 

@@ -69,34 +69,63 @@ def build_case(name, ragged=True, act=None):
     return cfg, w, ids, mask
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("name", ["c1_i8", "c1_f16", "c1_mixed", "c2_i8", "c2_f16", "c3_i8", "c3_f16", "c4_f16",
                                   "c5_f16"])
-def test_stage_lockstep(name):
+def test_stage_lockstep(name, fused):
+    """fused=False: separate add_ln / quant kernels, every stage checked on the
+    GPU's own stage input.  fused=True: out-proj+LN1 / FFN1+requant / FFN2+LN2
+    run as cluster row-reduction GEMMs (O16 and Y16 never exist): H1 and X_out
+    are checked against the oracle's O-proj->LN1 and FFN2->LN2 from the GPU's
+    ctx / I inputs."""
     cfg, w, ids, mask = build_case(name)
-    enc = Encoder(cfg, w)
+    enc = Encoder(cfg, w, fused=fused)
     orc = Oracle(cfg, w)
     B, S = ids.shape
     layers = range(cfg.num_layers) if cfg.num_layers <= 4 else [0, cfg.num_layers - 1]
     for l in layers:
         t = {k: f32(v) for k, v in enc.trace(dev(ids), dev(mask), l).items()}
         i8 = cfg.dtype[l] == 1
-        checks = [
-            ("qkv", oracle.ST_QKV, t["x_in"], None, True),
-            ("ctx", oracle.ST_ATTN, t["qkv"], None, False),
-            ("o", oracle.ST_OPROJ, t["ctx"], None, True),
-            ("h1", oracle.ST_LN1, t["o"], t["x_in"], False),
-            ("i", oracle.ST_FFN1, t["h1"], None, cfg.act == synth.ACT_RELU),
-            ("y", oracle.ST_FFN2, t["i"], None, True),
-            ("x_out", oracle.ST_LN2, t["y"], t["h1"], False),
-        ]
-        for key, st, a, b, exact_if_i8 in checks:
-            ref = orc.stage(l, st, a, b, mask=mask, B=B, S=S)
+        st = lambda s_, a, b=None: orc.stage(l, s_, a, b, mask=mask, B=B, S=S)  # noqa: E731
+        if fused:
+            checks = [
+                ("qkv", lambda: st(oracle.ST_QKV, t["x_in"]), True),
+                ("ctx", lambda: st(oracle.ST_ATTN, t["qkv"]), False),
+                ("h1", lambda: st(oracle.ST_LN1, st(oracle.ST_OPROJ, t["ctx"]), t["x_in"]), False),
+                ("i", lambda: st(oracle.ST_FFN1, t["h1"]), cfg.act == synth.ACT_RELU),
+                ("x_out", lambda: st(oracle.ST_LN2, st(oracle.ST_FFN2, t["i"]), t["h1"]), False),
+            ]
+        else:
+            checks = [
+                ("qkv", lambda: st(oracle.ST_QKV, t["x_in"]), True),
+                ("ctx", lambda: st(oracle.ST_ATTN, t["qkv"]), False),
+                ("o", lambda: st(oracle.ST_OPROJ, t["ctx"]), True),
+                ("h1", lambda: st(oracle.ST_LN1, t["o"], t["x_in"]), False),
+                ("i", lambda: st(oracle.ST_FFN1, t["h1"]), cfg.act == synth.ACT_RELU),
+                ("y", lambda: st(oracle.ST_FFN2, t["i"]), True),
+                ("x_out", lambda: st(oracle.ST_LN2, t["y"], t["h1"]), False),
+            ]
+        for key, ref_fn, exact_if_i8 in checks:
+            ref = ref_fn()
             got = t[key]
             if i8 and exact_if_i8:
                 nbad = int((got != ref).sum())
                 assert nbad == 0, f"{name} layer {l} {key}: {nbad} elements differ (int8 stage must be bit-exact)"
             else:
-                assert_close16(got, ref, f"{name} layer {l} {key}")
+                assert_close16(got, ref, f"{name} layer {l} {key} fused={fused}")
+
+
+@pytest.mark.parametrize("name", ["c1_i8", "c3_i8", "c3_f16"])
+def test_fused_epilogues_match_unfused(name):
+    """Same layer input -> the fused cluster epilogues reproduce the unfused
+    kernels: identical FFN1 output (same epilogue math) and LN outputs that
+    differ only by the order of the LN sums (rare 1-ulp flips)."""
+    cfg, w, ids, mask = build_case(name)
+    a = {k: f32(v) for k, v in Encoder(cfg, w, fused=True).trace(dev(ids), dev(mask), 0).items()}
+    b = {k: f32(v) for k, v in Encoder(cfg, w, fused=False).trace(dev(ids), dev(mask), 0).items()}
+    for k in ("x_in", "qkv", "ctx"):
+        assert np.array_equal(a[k], b[k]), k
+    assert_close16(a["h1"], b["h1"], f"{name} h1")
 
 
 @pytest.mark.parametrize("name", ["c1_i8", "c2_i8", "c3_i8", "c3_f16"])
