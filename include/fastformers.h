@@ -151,11 +151,12 @@ FF_API ff_status ff_check(ff_model *m, void *stream);
 /* FF_OPT_ATTN_TC (1 = tcgen05 attention for head_dim 64, S <= 128, default 1;
  * 0 = the mma.sync attention kernel everywhere). */
 #define FF_OPT_ATTN_TC 3
-/* FF_OPT_FUSED_EPILOGUES (1 = default: where the output row is 256 x 1..8
- * columns, fuse residual + LayerNorm (+ s8 requant) into the out-proj / FFN2
- * GEMM epilogues and the FFN-intermediate requant into FFN1, using clusters
- * that span the row; 0 = separate add_ln / quant_rows kernels).  With 1,
- * ff_encode_trace does not fill the O16 / Y16 dumps (never materialised). */
+/* FF_OPT_FUSED_EPILOGUES (1: where the output row is 256 x 1..8 columns,
+ * fuse residual + LayerNorm (+ s8 requant) into the out-proj / FFN2 GEMM
+ * epilogues and the FFN-intermediate requant into FFN1, using clusters that
+ * span the row; 0 = default: separate add_ln / quant_rows kernels, currently
+ * faster).  With 1, ff_encode_trace does not fill the O16 / Y16 dumps (never
+ * materialised). */
 #define FF_OPT_FUSED_EPILOGUES 4
 FF_API ff_status ff_set_option(ff_model *m, int32_t option, int64_t value);
 

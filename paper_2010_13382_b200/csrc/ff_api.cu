@@ -89,7 +89,7 @@ struct ff_model {
   bool use_graphs = true;
   int pair_mode = -1;  // FF_OPT_CTA_PAIRS: -1 auto, 0 never (GemmPlan::force_pair)
   bool attn_tc = true;  // FF_OPT_ATTN_TC: tcgen05 attention where supported
-  bool fused = true;    // FF_OPT_FUSED_EPILOGUES: cluster row-reduction GEMM epilogues
+  bool fused = false;   // FF_OPT_FUSED_EPILOGUES: cluster row-reduction GEMM epilogues (opt-in)
   CUtensorMap tm_qkv;   // QKV buffer map for the tcgen05 attention
   std::map<std::tuple<int, int, const void*, const void*, const void*>, cudaGraphExec_t> graphs;
 

@@ -379,8 +379,12 @@ struct RRCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_OFF = kRRStages * STAGE_BYTES;
   static constexpr int RED_OFF = EPI_OFF + kEpiWarps * 2 * kStageTile;
-  static constexpr int RED_FLOATS = 2 * 8 * 2 * 128;  // [buf][rank<=8][half][row]
-  static constexpr int BAR_OFF = RED_OFF + RED_FLOATS * 4;
+  // received partials [buf][rank<=8][half][quadrant][val<=2][32 rows]
+  static constexpr int RED_FLOATS = 2 * 8 * 2 * 4 * 2 * 32;
+  // this CTA's outgoing partials [buf][half][quadrant][val][32 rows]
+  static constexpr int LOC_OFF = RED_OFF + RED_FLOATS * 4;
+  static constexpr int LOC_FLOATS = 2 * 2 * 4 * 2 * 32;
+  static constexpr int BAR_OFF = LOC_OFF + LOC_FLOATS * 4;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
   static_assert(SMEM <= 227 * 1024, "smem budget");
 };
@@ -529,23 +533,37 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float inv_n = 1.0f / (float)p.N;
     (void)inv_n;
 
-    // Cluster-wide per-row reduction of v over the 2*CN column halves.
-    auto reduce_row = [&](float v, bool is_max) -> float {
+    // Cluster exchange of NV per-row partials: every warp stages its 32 rows'
+    // values in smem and lane 0 bulk-copies the block (NV x 128 B) into the
+    // [rank][half][quadrant] slot of every CTA of the cluster; the copies
+    // complete_tx on the destination's barrier, armed for CN x 8 warps x NV x
+    // 128 B.  Returns the buffer holding all 2*CN partials of each row.
+    float* loc = reinterpret_cast<float*>(smem + RRCfg::LOC_OFF);
+    auto exchange = [&](float v0, float v1, int nv) -> int {
       const int b = step & 1;
       const uint32_t ph = (uint32_t)(step >> 1) & 1u;
-      if (threadIdx.x == 128) mbar_expect_tx(&redbar[b], (uint32_t)CN * 2 * 128 * 4);
-      float* slot = red + (((b * 8 + (int)rank) * 2 + hf) * 128 + rowl);
-      const uint32_t s_local = smem_u32(slot), b_local = smem_u32(&redbar[b]);
-      for (int c = 0; c < CN; ++c) st_async_f32(mapa_shared(s_local, c), v, mapa_shared(b_local, c));
+      float* mine = loc + (((b * 2 + hf) * 4 + q) * 2) * 32;
+      mine[lane] = v0;
+      if (nv > 1) mine[32 + lane] = v1;
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        if (threadIdx.x == 128) mbar_expect_tx(&redbar[b], (uint32_t)(CN * kEpiWarps * nv * 128));
+        const uint32_t dst = smem_u32(red + ((((b * 8 + (int)rank) * 2 + hf) * 4 + q) * 2) * 32);
+        const uint32_t bl = smem_u32(&redbar[b]);
+        for (int c = 0; c < CN; ++c) bulk_copy_s2c(mapa_shared(dst, c), mine, nv * 128, mapa_shared(bl, c));
+      }
       mbar_wait(&redbar[b], ph);
-      float r = is_max ? 0.0f : 0.0f;
-      for (int c = 0; c < CN; ++c)
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          const float x = red[((b * 8 + c) * 2 + h2) * 128 + rowl];
-          r = is_max ? fmaxf(r, x) : r + x;
-        }
       ++step;
+      return b;
+    };
+    auto partial = [&](int b, int c, int h2, int v) -> float {
+      return red[((((b * 8 + c) * 2 + h2) * 4 + q) * 2 + v) * 32 + lane];
+    };
+    auto reduce_max = [&](float v) -> float {
+      const int b = exchange(v, 0.0f, 1);
+      float r = 0.0f;
+      for (int c = 0; c < CN; ++c) r = fmaxf(r, fmaxf(partial(b, c, 0, 0), partial(b, c, 1, 0)));
       return r;
     };
     auto store16 = [&](const uint32_t (&h)[16], int n0, int row0) {
@@ -581,20 +599,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (MODE == RR_LN) {
         // pass 1: x = R16(GEMM epilogue) + residual (R11); sum; x -> TMEM
         float psum = 0.0f;
+        const __half* rrow = p.residual + (size_t)(row_ok ? row : 0) * p.ldr + ncol0;
+        uint4 rv[4];  // residual of the current chunk, prefetched one chunk ahead
+#pragma unroll
+        for (int i = 0; i < 4; ++i) rv[i] = __ldg(reinterpret_cast<const uint4*>(rrow + c_lo) + i);
 #pragma unroll 1
         for (int c = c_lo; c < c_lo + BN / 2; c += 32) {
           const int n0 = ncol0 + c;
           float bias[32], sw[32];
           load32(bias, p.bias, n0, p.N);
           if (I8) load32(sw, p.col_scale, n0, p.N);
-          uint4 rv[4];
-          const __half* rp = p.residual + (size_t)(row_ok ? row : 0) * p.ldr + n0;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) rv[i] = __ldg(reinterpret_cast<const uint4*>(rp) + i);
           uint32_t r[32];
           tmem_ld32(tbase + c, r);
           tmem_wait_ld();
-          const __half2* rh = reinterpret_cast<const __half2*>(rv);
+          const uint4 rcur[4] = {rv[0], rv[1], rv[2], rv[3]};
+          if (c + 32 < c_lo + BN / 2) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) rv[i] = __ldg(reinterpret_cast<const uint4*>(rrow + c + 32) + i);
+          }
+          const __half2* rh = reinterpret_cast<const __half2*>(rcur);
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
             const float2 res = __half22float2(rh[j / 2]);
@@ -609,9 +632,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st32(tbase + c, r);
         }
         tmem_wait_st();
-        const float mean = __fdiv_rn(reduce_row(psum, false), (float)p.N);
-        // pass 2: variance (two-pass)
-        float pvar = 0.0f;
+        // pass 2: this thread's 128 values, two-pass about their own mean
+        const float mean_t = psum * (1.0f / (BN / 2));
+        float m2_t = 0.0f;
 #pragma unroll 1
         for (int c = c_lo; c < c_lo + BN / 2; c += 32) {
           uint32_t r[32];
@@ -619,11 +642,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_wait_ld();
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            const float dlt = __uint_as_float(r[j]) - mean;
-            pvar = __fmaf_rn(dlt, dlt, pvar);
+            const float dlt = __uint_as_float(r[j]) - mean_t;
+            m2_t = __fmaf_rn(dlt, dlt, m2_t);
           }
         }
-        const float var = __fdiv_rn(reduce_row(pvar, false), (float)p.N);
+        // one cluster exchange of (mean_t, M2_t); Chan's parallel combination in
+        // a fixed order: mean = avg(mean_i), M2 = sum M2_i + n sum (mean_i - mean)^2
+        const int b = exchange(mean_t, m2_t, 2);
+        float msum = 0.0f;
+        for (int c = 0; c < CN; ++c) msum += partial(b, c, 0, 0) + partial(b, c, 1, 0);
+        const float mean = __fdiv_rn(msum, (float)(2 * CN));
+        float m2 = 0.0f;
+        for (int c = 0; c < CN; ++c)
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const float dm = partial(b, c, h2, 0) - mean;
+            m2 += partial(b, c, h2, 1) + (float)(BN / 2) * dm * dm;
+          }
+        const float var = __fdiv_rn(m2, (float)p.N);
         const float rstd = 1.0f / sqrtf(var + p.eps);
         // pass 3: y = (x - mean) * rstd * g + b -> R16 -> fp16 store (+ packed y16 -> TMEM)
 #pragma unroll 1
@@ -679,7 +715,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
       if (p.outq) {
         // Q8row over the whole row (R6-R8, R12): quantize the fp16-rounded values
-        const float rmax = reduce_row(amax, true);
+        const float rmax = reduce_max(amax);
         const float sc = rmax == 0.0f ? 1.0f : __fdiv_rn(rmax, 127.0f);
 #pragma unroll 1
         for (int c = c_lo; c < c_lo + BN / 2; c += 32) {
@@ -900,10 +936,43 @@ bool plan_rr(RRPlan* g, bool i8, const void* A, int M_rows, int lda, const void*
   return true;
 }
 
+template <bool I8, int MODE>
+static int rr_max_clusters_t(int cn) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cn * (kNumSMs / cn));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = RRCfg::SMEM;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cn;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, gemm_rr_kernel<I8, MODE>, &cfg) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = kNumSMs / cn;
+  }
+  return n;
+}
+
+// Clusters that can be co-resident (GPC packing of CN-CTA clusters), cached.
+static int rr_max_clusters(bool i8, int mode, int cn) {
+  static int cache[2][3][9] = {};
+  int& c = cache[i8 ? 1 : 0][mode][cn];
+  if (c == 0) {
+    if (mode == RR_LN) c = i8 ? rr_max_clusters_t<true, RR_LN>(cn) : rr_max_clusters_t<false, RR_LN>(cn);
+    else c = i8 ? rr_max_clusters_t<true, RR_QUANT>(cn) : rr_max_clusters_t<false, RR_QUANT>(cn);
+  }
+  return c;
+}
+
 void plan_rr_set_m(RRPlan* g, int M) {
   g->p.M = M;
   g->p.m_tiles = (M + BM - 1) / BM;
-  const int max_clusters = kNumSMs / g->cn;
+  const int max_clusters =
+      (g->p.mode == RR_LN || g->p.mode == RR_QUANT) ? rr_max_clusters(g->i8, g->p.mode, g->cn) : kNumSMs / g->cn;
   const int nc = g->p.m_tiles < max_clusters ? g->p.m_tiles : max_clusters;
   g->grid = nc * g->cn;
 }

@@ -218,6 +218,15 @@ __device__ __forceinline__ void st_async_f32(uint32_t remote_addr, float v, uint
                "r"(__float_as_uint(v)), "r"(remote_bar)
                : "memory");
 }
+// Bulk smem -> peer-smem copy (16B-aligned, size multiple of 16) that signals
+// its bytes on an mbarrier of the destination CTA.
+__device__ __forceinline__ void bulk_copy_s2c(uint32_t dst_cluster, const void* src, uint32_t bytes,
+                                              uint32_t bar_cluster) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   dst_cluster),
+               "r"(smem_u32(src)), "r"(bytes), "r"(bar_cluster)
+               : "memory");
+}
 __device__ __forceinline__ uint32_t cluster_nctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));

@@ -103,7 +103,7 @@ class Encoder:
     """One FastFormers encoder model on one GPU (weights packed once at load)."""
 
     def __init__(self, cfg, weights: Dict[str, np.ndarray], max_tokens: Optional[int] = None, device: int = 0,
-                 use_graphs: bool = True, cta_pairs: bool = True, attn_tc: bool = True, fused: bool = True):
+                 use_graphs: bool = True, cta_pairs: bool = True, attn_tc: bool = True, fused: bool = False):
         import torch
         L = lib()
         self.cfg = cfg
@@ -134,8 +134,7 @@ class Encoder:
             check(L.ff_set_option(self.h, FF_OPT_GRAPHS, 0))
         if not attn_tc:
             check(L.ff_set_option(self.h, FF_OPT_ATTN_TC, 0))
-        if not fused:
-            check(L.ff_set_option(self.h, FF_OPT_FUSED_EPILOGUES, 0))
+        check(L.ff_set_option(self.h, FF_OPT_FUSED_EPILOGUES, 1 if fused else 0))
         self.fused = fused
         if not cta_pairs:
             check(L.ff_set_option(self.h, FF_OPT_CTA_PAIRS, 0))
