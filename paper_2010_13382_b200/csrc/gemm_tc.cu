@@ -31,9 +31,18 @@ namespace ff {
 
 constexpr int BM = 128;
 constexpr int BK_BYTES = 128;  // one 128-byte swizzle row of K per k-block
-constexpr int kEpiWarps = 8;
+// gemm_tc_kernel: 16 epilogue warps (4 per TMEM lane quadrant, each owning a
+// quarter of the tile's columns), 16-column chunks, 32x16 fp16 staging blocks
+// stored with 32B swizzle.  <= 96 registers per thread at 640 threads.
+constexpr int kEpiWarps = 16;
 constexpr int kThreads = 128 + 32 * kEpiWarps;
-constexpr int kStageTile = 32 * 64;  // 32 rows x 32 fp16 staging block (2 KB)
+constexpr int kEpiCols = 16;
+constexpr int kStageTile = 32 * kEpiCols * 2;  // 1 KB
+// gemm_rr_kernel: 8 epilogue warps (2 per quadrant), 32-column chunks, 32x32
+// staging blocks with 64B swizzle.
+constexpr int kRREpiWarps = 8;
+constexpr int kRRThreads = 128 + 32 * kRREpiWarps;
+constexpr int kRRStageTile = 32 * 64;  // 2 KB
 
 // PAIR = CTA pair (cta_group::2): a 256-row tile per pair, each CTA loads its
 // 128 rows of A and its BN/2 rows of W, the leader issues M=256 MMAs.
@@ -92,13 +101,13 @@ __device__ __forceinline__ float act_fn(float y) {
   return y;
 }
 
-// 32 columns [n0, n0+32) of this thread's row: dequant / bias / activation,
-// RNE to fp16, packed as 16 half2 words.
-template <bool I8, int ACT>
-__device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float (&bias)[32], const float (&sw)[32],
-                                          float sx, uint32_t (&h)[16]) {
+// W columns [n0, n0+W) of this thread's row: dequant / bias / activation,
+// RNE to fp16, packed as W/2 half2 words.
+template <bool I8, int ACT, int W>
+__device__ __forceinline__ void epi_chunk(const uint32_t (&r)[W], const float (&bias)[W], const float (&sw)[W],
+                                          float sx, uint32_t (&h)[W / 2]) {
 #pragma unroll
-  for (int e = 0; e < 16; ++e) {
+  for (int e = 0; e < W / 2; ++e) {
     float v[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -113,13 +122,14 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], const float (
   }
 }
 
-__device__ __forceinline__ void load32(float (&dst)[32], const float* src, int n0, int N) {
+template <int W>
+__device__ __forceinline__ void loadN(float (&dst)[W], const float* src, int n0, int N) {
   if (src == nullptr) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) dst[j] = 0.0f;
-  } else if (n0 + 32 <= N && ((reinterpret_cast<uintptr_t>(src + n0) & 15) == 0)) {
+    for (int j = 0; j < W; ++j) dst[j] = 0.0f;
+  } else if (n0 + W <= N && ((reinterpret_cast<uintptr_t>(src + n0) & 15) == 0)) {
 #pragma unroll
-    for (int j = 0; j < 32; j += 4) {
+    for (int j = 0; j < W; j += 4) {
       const float4 f = __ldg(reinterpret_cast<const float4*>(src + n0 + j));
       dst[j] = f.x;
       dst[j + 1] = f.y;
@@ -128,8 +138,19 @@ __device__ __forceinline__ void load32(float (&dst)[32], const float* src, int n
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) dst[j] = (n0 + j < N) ? __ldg(src + n0 + j) : 0.0f;
+    for (int j = 0; j < W; ++j) dst[j] = (n0 + j < N) ? __ldg(src + n0 + j) : 0.0f;
   }
+}
+__device__ __forceinline__ void load32(float (&dst)[32], const float* src, int n0, int N) { loadN<32>(dst, src, n0, N); }
+
+// tcgen05.ld of 16 columns (32x32b.x16): thread t gets row (lane base + t).
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
 }
 
 template <int BN, bool I8, bool PAIR>
@@ -260,8 +281,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;
-    const int q = warp & 3;                 // TMEM lane quadrant this warp may access
-    const int c_lo = (ew >> 2) * (BN / 2);  // this warp's column half of the tile
+    const int q = warp & 3;                         // TMEM lane quadrant this warp may access
+    constexpr int WCOLS = BN / (kEpiWarps / 4);     // columns per warp (64 or 32)
+    const int c_lo = (ew >> 2) * WCOLS;             // this warp's column group of the tile
     uint8_t* stage_buf = sEpi + ew * 2 * kStageTile;
     const uint32_t tempty_leader0 = PAIR ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
     int acc = 0;
@@ -288,48 +310,48 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       if (p.out_mode == 0) {  // raw accumulators (tests only)
 #pragma unroll 1
-        for (int c = c_lo; c < c_lo + BN / 2; c += 32) {
-          uint32_t r[32];
-          tmem_ld32(tbase + c, r);
+        for (int c = c_lo; c < c_lo + WCOLS; c += kEpiCols) {
+          uint32_t r[kEpiCols];
+          tmem_ld16(tbase + c, r);
           tmem_wait_ld();
           const int n0 = nt * BN + c;
           if (row < p.M && n0 < p.N) {
             uint32_t* o = reinterpret_cast<uint32_t*>(p.out) + (size_t)row * p.ldo + n0;
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
+            for (int j = 0; j < kEpiCols; ++j)
               if (n0 + j < p.N) o[j] = r[j];
           }
         }
         release_acc();
       } else {
         // software pipeline: the TMEM load of chunk c+1 overlaps the stores of chunk c
-        uint32_t r[32];
-        tmem_ld32(tbase + c_lo, r);
+        uint32_t r[kEpiCols];
+        tmem_ld16(tbase + c_lo, r);
 #pragma unroll 1
-        for (int c = c_lo; c < c_lo + BN / 2; c += 32) {
+        for (int c = c_lo; c < c_lo + WCOLS; c += kEpiCols) {
           const int n0 = nt * BN + c;
-          const bool last = c + 32 >= c_lo + BN / 2;
-          float bias[32], sw[32];
-          load32(bias, p.bias, n0, p.N);
-          if (I8) load32(sw, p.col_scale, n0, p.N);
+          const bool last = c + kEpiCols >= c_lo + WCOLS;
+          float bias[kEpiCols], sw[kEpiCols];
+          loadN<kEpiCols>(bias, p.bias, n0, p.N);
+          if (I8) loadN<kEpiCols>(sw, p.col_scale, n0, p.N);
           tmem_wait_ld();
           if (last) release_acc();
-          uint32_t h[16];
+          uint32_t h[kEpiCols / 2];
           switch (p.act) {
-            case ACT_GELU: epi_chunk<I8, ACT_GELU>(r, bias, sw, sx, h); break;
-            case ACT_RELU: epi_chunk<I8, ACT_RELU>(r, bias, sw, sx, h); break;
-            case ACT_GELU_TANH: epi_chunk<I8, ACT_GELU_TANH>(r, bias, sw, sx, h); break;
-            default: epi_chunk<I8, ACT_NONE>(r, bias, sw, sx, h); break;
+            case ACT_GELU: epi_chunk<I8, ACT_GELU, kEpiCols>(r, bias, sw, sx, h); break;
+            case ACT_RELU: epi_chunk<I8, ACT_RELU, kEpiCols>(r, bias, sw, sx, h); break;
+            case ACT_GELU_TANH: epi_chunk<I8, ACT_GELU_TANH, kEpiCols>(r, bias, sw, sx, h); break;
+            default: epi_chunk<I8, ACT_NONE, kEpiCols>(r, bias, sw, sx, h); break;
           }
-          if (!last) tmem_ld32(tbase + c + 32, r);
+          if (!last) tmem_ld16(tbase + c + kEpiCols, r);
           if (n0 < p.N) {  // warp-uniform; TMA clips the N tail of the chunk
             uint8_t* buf = stage_buf + (nbuf & 1) * kStageTile;
             if (lane == 0) bulk_wait_read<1>();  // the store that last used `buf` has read it
             __syncwarp();
-            uint8_t* srow = buf + lane * 64;
+            uint8_t* srow = buf + lane * 32;
 #pragma unroll
-            for (int cc = 0; cc < 4; ++cc) {  // SWIZZLE_64B: 16B chunk cc of row `lane`
-              const int pc = cc ^ ((lane >> 1) & 3);
+            for (int cc = 0; cc < 2; ++cc) {  // SWIZZLE_32B: 16B chunk cc of 32B row `lane`
+              const int pc = cc ^ ((lane >> 2) & 1);
               *reinterpret_cast<uint4*>(srow + pc * 16) =
                   make_uint4(h[4 * cc], h[4 * cc + 1], h[4 * cc + 2], h[4 * cc + 3]);
             }
@@ -378,7 +400,7 @@ struct RRCfg {
   static constexpr int B_BYTES = kRRBN * BK_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_OFF = kRRStages * STAGE_BYTES;
-  static constexpr int RED_OFF = EPI_OFF + kEpiWarps * 2 * kStageTile;
+  static constexpr int RED_OFF = EPI_OFF + kRREpiWarps * 2 * kRRStageTile;
   // received partials [buf][rank<=8][half][quadrant][val<=2][32 rows]
   static constexpr int RED_FLOATS = 2 * 8 * 2 * 4 * 2 * 32;
   // this CTA's outgoing partials [buf][half][quadrant][val][32 rows]
@@ -389,15 +411,6 @@ struct RRCfg {
   static_assert(SMEM <= 227 * 1024, "smem budget");
 };
 
-// tcgen05.ld of 16 columns (packed fp16 pairs written back by a previous pass).
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
@@ -419,7 +432,7 @@ __device__ __forceinline__ float dequant1(uint32_t r, float sx, float sw, float 
 }
 
 template <bool I8, int MODE>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kRRThreads, 1)
     gemm_rr_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, RRParams p) {
   constexpr int STAGES = kRRStages;
@@ -452,7 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kEpiWarps);
+      mbar_init(&tempty[a], kRREpiWarps);
       mbar_init(&redbar[a], 1);
     }
     fence_barrier_init();
@@ -525,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int hf = ew >> 2;
     const int c_lo = hf * (BN / 2);
     const int rowl = q * 32 + lane;  // row within the 128-row tile
-    uint8_t* stage_buf = sEpi + ew * 2 * kStageTile;
+    uint8_t* stage_buf = sEpi + ew * 2 * kRRStageTile;
     int acc = 0;
     uint32_t acc_phase = 0;
     int nbuf = 0;
@@ -548,7 +561,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_async_smem();
       __syncwarp();
       if (lane == 0) {
-        if (threadIdx.x == 128) mbar_expect_tx(&redbar[b], (uint32_t)(CN * kEpiWarps * nv * 128));
+        if (threadIdx.x == 128) mbar_expect_tx(&redbar[b], (uint32_t)(CN * kRREpiWarps * nv * 128));
         const uint32_t dst = smem_u32(red + ((((b * 8 + (int)rank) * 2 + hf) * 4 + q) * 2) * 32);
         const uint32_t bl = smem_u32(&redbar[b]);
         for (int c = 0; c < CN; ++c) bulk_copy_s2c(mapa_shared(dst, c), mine, nv * 128, mapa_shared(bl, c));
@@ -567,7 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       return r;
     };
     auto store16 = [&](const uint32_t (&h)[16], int n0, int row0) {
-      uint8_t* buf = stage_buf + (nbuf & 1) * kStageTile;
+      uint8_t* buf = stage_buf + (nbuf & 1) * kRRStageTile;
       if (lane == 0) bulk_wait_read<1>();
       __syncwarp();
       uint8_t* srow = buf + lane * 64;
@@ -841,8 +854,8 @@ bool plan_gemm_output(GemmPlan* g, void* out, int ldo, const char** err) {
   g->p.out = out;
   g->p.ldo = ldo;
   g->has_out_map = true;
-  return encode_2d(&g->tmC, out, g->M_rows, g->p.N, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (size_t)ldo * 2, 32, 32,
-                   CU_TENSOR_MAP_SWIZZLE_64B, err);
+  return encode_2d(&g->tmC, out, g->M_rows, g->p.N, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (size_t)ldo * 2, kEpiCols,
+                   32, CU_TENSOR_MAP_SWIZZLE_32B, err);
 }
 
 void plan_gemm_set_m(GemmPlan* g, int M) {
@@ -940,7 +953,7 @@ template <bool I8, int MODE>
 static int rr_max_clusters_t(int cn) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cn * (kNumSMs / cn));
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(kRRThreads);
   cfg.dynamicSmemBytes = RRCfg::SMEM;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -981,7 +994,7 @@ template <bool I8, int MODE>
 static cudaError_t launch_rr_t(const RRPlan& g, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(g.grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(kRRThreads);
   cfg.dynamicSmemBytes = RRCfg::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];

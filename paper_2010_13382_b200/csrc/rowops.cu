@@ -39,6 +39,17 @@ __device__ __forceinline__ int8_t quant1(float x, float s) {
   return static_cast<int8_t>(static_cast<int>(v));
 }
 
+// Same result as quant1 (RNE of the correctly rounded quotient x/s), cheaper:
+// t = x * rcp(s) lies within 2 ulp of fl(x/s), so RNE(t) == RNE(fl(x/s))
+// unless t is within a few ulp of a half-integer; only then (rarely) divide.
+__device__ __forceinline__ int8_t quant1_fast(float x, float s, float rs) {
+  const float t = x * rs;
+  float v = rintf(t);
+  if (0.5f - fabsf(t - v) <= fabsf(t) * 4.76837158203125e-07f + 1e-30f) v = rintf(__fdiv_rn(x, s));
+  v = fminf(fmaxf(v, -127.0f), 127.0f);
+  return static_cast<int8_t>(static_cast<int>(v));
+}
+
 __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
   const __half2* h = reinterpret_cast<const __half2*>(&u);
 #pragma unroll
@@ -102,13 +113,14 @@ __device__ __forceinline__ void ln_store(float (&v)[NCH][8], int H, int lane, co
   if (yq == nullptr) return;
   amax = warp_max(amax);
   const float sc = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 127.0f);
+  const float rs = __frcp_rn(sc);
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
     const int col = 8 * (lane + 32 * c);
     if (col < H) {
       int8_t o[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = quant1(v[c][j], sc);
+      for (int j = 0; j < 8; ++j) o[j] = quant1_fast(v[c][j], sc, rs);
       *reinterpret_cast<uint2*>(yq + col) = *reinterpret_cast<const uint2*>(o);
     }
   }
@@ -164,48 +176,63 @@ __global__ void __launch_bounds__(256) add_ln_kernel(const __half* __restrict__ 
                                                     int ldr, int M, int H, const float* __restrict__ g,
                                                     const float* __restrict__ b, float eps, __half* y16, int ldy,
                                                     int8_t* yq, int ldq, float* ys) {
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (row >= M) return;
-  const __half* ar = a + (size_t)row * lda;
-  const __half* rr = r + (size_t)row * ldr;
+  // persistent grid-stride over rows; the next row's 2*NCH 16-byte loads are
+  // in flight while the current row is normalised and stored
+  const int lane = threadIdx.x & 31;
+  const int stride = gridDim.x * 8;
+  int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   uint4 ua[NCH], ur[NCH];
+  auto load_row = [&](int rw) {
 #pragma unroll
-  for (int c = 0; c < NCH; ++c) {  // all loads first: 2*NCH 16-byte requests in flight per lane
-    const int col = 8 * (lane + 32 * c);
-    if (col < H) {
-      ua[c] = __ldcs(reinterpret_cast<const uint4*>(ar + col));
-      ur[c] = __ldcs(reinterpret_cast<const uint4*>(rr + col));
+    for (int c = 0; c < NCH; ++c) {
+      const int col = 8 * (lane + 32 * c);
+      if (rw < M && col < H) {
+        ua[c] = __ldcs(reinterpret_cast<const uint4*>(a + (size_t)rw * lda + col));
+        ur[c] = __ldcs(reinterpret_cast<const uint4*>(r + (size_t)rw * ldr + col));
+      }
     }
-  }
-  float v[NCH][8];
+  };
+  load_row(row);
+  for (; row < M; row += stride) {
+    float v[NCH][8];
 #pragma unroll
-  for (int c = 0; c < NCH; ++c) {
-    if (8 * (lane + 32 * c) < H) {
-      float fa[8], fr[8];
-      unpack8(ua[c], fa);
-      unpack8(ur[c], fr);
+    for (int c = 0; c < NCH; ++c) {
+      if (8 * (lane + 32 * c) < H) {
+        float fa[8], fr[8];
+        unpack8(ua[c], fa);
+        unpack8(ur[c], fr);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[c][j] = __fadd_rn(fa[j], fr[j]);
+        for (int j = 0; j < 8; ++j) v[c][j] = __fadd_rn(fa[j], fr[j]);
+      }
     }
+    load_row(row + stride);
+    ln_store<NCH>(v, H, lane, g, b, eps, y16 + (size_t)row * ldy, yq ? yq + (size_t)row * ldq : nullptr,
+                  ys ? ys + row : nullptr);
   }
-  ln_store<NCH>(v, H, lane, g, b, eps, y16 + (size_t)row * ldy, yq ? yq + (size_t)row * ldq : nullptr,
-                ys ? ys + row : nullptr);
 }
 
 // One warp per row, the row in registers (NCH 16-byte chunks per lane).
 template <int NCH>
 __global__ void __launch_bounds__(256) quant_rows_kernel(const __half* __restrict__ x, int ldx, int M, int K,
                                                         int8_t* __restrict__ q, int ldq, float* __restrict__ scale) {
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (row >= M) return;
-  const __half* xr = x + (size_t)row * ldx;
+  const int lane = threadIdx.x & 31;
+  const int stride = gridDim.x * 8;
+  int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  uint4 un[NCH];  // next row, prefetched
+  auto load_row = [&](int rw) {
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      const int col = 8 * (lane + 32 * c);
+      if (rw < M && col < K) un[c] = __ldcs(reinterpret_cast<const uint4*>(x + (size_t)rw * ldx + col));
+    }
+  };
+  load_row(row);
+  for (; row < M; row += stride) {
   int8_t* qr = q + (size_t)row * ldq;
   uint4 u[NCH];
 #pragma unroll
-  for (int c = 0; c < NCH; ++c) {
-    const int col = 8 * (lane + 32 * c);
-    if (col < K) u[c] = __ldcs(reinterpret_cast<const uint4*>(xr + col));
-  }
+  for (int c = 0; c < NCH; ++c) u[c] = un[c];
+  load_row(row + stride);
   float amax = 0.0f;
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
@@ -218,6 +245,7 @@ __global__ void __launch_bounds__(256) quant_rows_kernel(const __half* __restric
   }
   amax = warp_max(amax);
   const float sc = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 127.0f);
+  const float rs = __frcp_rn(sc);
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
     const int col = 8 * (lane + 32 * c);
@@ -226,11 +254,23 @@ __global__ void __launch_bounds__(256) quant_rows_kernel(const __half* __restric
       unpack8(u[c], f);
       int8_t o[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = quant1(f[j], sc);
+      for (int j = 0; j < 8; ++j) o[j] = quant1_fast(f[j], sc, rs);
       *reinterpret_cast<uint2*>(qr + col) = *reinterpret_cast<const uint2*>(o);
     }
   }
   if (lane == 0) scale[row] = sc;
+  }
+}
+
+// Persistent grid for the row kernels: enough resident warps to keep ~2 rows
+// per warp in flight without a long tail.
+inline unsigned row_grid(int M) {
+  const unsigned want = (unsigned)((M + 7) / 8);
+  // measured on B200: one row per warp with many short CTAs (no cap) beats a
+  // persistent grid of 2-4 CTAs/SM for these kernels; the grid-stride loop
+  // keeps them correct for any grid size
+  (void)kNumSMs;
+  return want;
 }
 
 // Generic fallback (K not a multiple of 8 or unaligned rows): element-wise.
@@ -347,7 +387,7 @@ cudaError_t launch_embed_ln(const int32_t* ids, const int32_t* mask, int B, int 
 cudaError_t launch_add_ln(const __half* a, int lda, const __half* r, int ldr, int M, int H, const float* g,
                           const float* b, float eps, __half* y16, int ldy, int8_t* yq, int ldq, float* ys,
                           cudaStream_t s) {
-  const unsigned grid = (M + 7) / 8;
+  const unsigned grid = row_grid(M);
   switch (chunks_for(H)) {
     case 1: add_ln_kernel<1><<<grid, 256, 0, s>>>(a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
     case 2: add_ln_kernel<2><<<grid, 256, 0, s>>>(a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
@@ -359,13 +399,14 @@ cudaError_t launch_add_ln(const __half* a, int lda, const __half* r, int ldr, in
 
 cudaError_t launch_quant_rows(const __half* x, int ldx, int M, int K, int8_t* q, int ldq, float* scale,
                               cudaStream_t s) {
-  const unsigned grid = (M + 7) / 8;
+  unsigned grid = (M + 7) / 8;
   const bool vec = (K % 8 == 0) && (ldx % 8 == 0) && (ldq % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) &&
                    ((reinterpret_cast<uintptr_t>(q) & 7) == 0) && K <= 4096;
   if (!vec) {
     quant_rows_scalar_kernel<<<grid, 256, 0, s>>>(x, ldx, M, K, q, ldq, scale);
     return cudaGetLastError();
   }
+  grid = row_grid(M);
   const int n = chunks_for(K);
   if (n <= 1) quant_rows_kernel<1><<<grid, 256, 0, s>>>(x, ldx, M, K, q, ldq, scale);
   else if (n <= 2) quant_rows_kernel<2><<<grid, 256, 0, s>>>(x, ldx, M, K, q, ldq, scale);
