@@ -158,6 +158,10 @@ FF_API ff_status ff_check(ff_model *m, void *stream);
  * faster).  With 1, ff_encode_trace does not fill the O16 / Y16 dumps (never
  * materialised). */
 #define FF_OPT_FUSED_EPILOGUES 4
+/* FF_OPT_PDL (1 = default: launch every forward kernel with programmatic
+ * dependent launch so its prologue overlaps the previous kernel's tail;
+ * process-wide setting). */
+#define FF_OPT_PDL 5
 FF_API ff_status ff_set_option(ff_model *m, int32_t option, int64_t value);
 
 FF_API void ff_model_destroy(ff_model *m);

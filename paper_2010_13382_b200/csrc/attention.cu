@@ -90,6 +90,8 @@ __global__ void __launch_bounds__(256, 1) attention_kernel(const __half* __restr
   constexpr int LDS = DP + 8;
   constexpr int NT = KC / 8;  // n-tiles per chunk
   extern __shared__ __align__(16) uint8_t smem[];
+  griddep_wait();
+  griddep_launch();
   const int S16 = (S + 15) & ~15;
   const size_t buf_halves = (size_t)(QT + 2 * S16) * LDS;
   const size_t buf_bytes = buf_halves * 2 + (size_t)S16 * 4;
@@ -299,7 +301,8 @@ cudaError_t launch_dp(const __half* qkv, int ld, const int32_t* mask, int B, int
   const int n_items = B * A * ((S + QT - 1) / QT);
   const int per_sm = 1;  // ~240 registers x 256 threads: one resident CTA per SM
   const int grid = n_items < kNumSMs * per_sm ? n_items : kNumSMs * per_sm;
-  attention_kernel<DP><<<grid, 256, nbuf * one, s>>>(qkv, ld, mask, B, S, A, d, scale, ctx, ldc, nbuf);
+  launch_ex(attention_kernel<DP>, dim3(grid), dim3(256), nbuf * one, s, 1, qkv, ld, mask, B, S, A, d, scale, ctx, ldc,
+            nbuf);
   return cudaGetLastError();
 }
 

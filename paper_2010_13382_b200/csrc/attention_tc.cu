@@ -95,6 +95,8 @@ __global__ void __launch_bounds__(kThreadsTC, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  griddep_wait();  // QKV / mask come from the previous kernel
+  griddep_launch();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -241,7 +243,8 @@ cudaError_t launch_attention_tc(const CUtensorMap& map, const int32_t* mask, int
   const int n_items = B * A;
   const int grid = n_items < 2 * kNumSMs ? n_items : 2 * kNumSMs;
   const float scale = (float)(1.0 / sqrt((double)kD));
-  attention_tc_kernel<<<grid, kThreadsTC, SmemTC::TOTAL, s>>>(map, mask, B, S, A, scale, ctx, ldctx);
+  launch_ex(attention_tc_kernel, dim3(grid), dim3(kThreadsTC), SmemTC::TOTAL, s, 1, map, mask, B, S, A, scale, ctx,
+            ldctx);
   return cudaGetLastError();
 }
 

@@ -12,6 +12,10 @@
 #include "fastformers.h"
 #include "ff_kernels.h"
 
+namespace ff {
+bool g_pdl = true;  // FF_OPT_PDL: programmatic dependent launch between forward kernels
+}
+
 namespace {
 
 thread_local std::string g_err;
@@ -758,6 +762,12 @@ ff_status ff_set_option(ff_model* m, int32_t option, int64_t value) {
   if (!m) return fail(FF_E_INVALID, "null model");
   if (option == FF_OPT_GRAPHS) {
     m->use_graphs = value != 0;
+    return FF_OK;
+  }
+  if (option == FF_OPT_PDL) {  // process-wide
+    ff::g_pdl = value != 0;
+    for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
+    m->graphs.clear();
     return FF_OK;
   }
   if (option == FF_OPT_FUSED_EPILOGUES) {

@@ -203,6 +203,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (PAIR) cluster_sync();  // peer barriers initialised before any remote signal
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();  // A operand / scales come from the previous kernel
+  griddep_launch();
 
   const int num_tiles = p.m_tiles * p.n_tiles;
   constexpr int KE = I8 ? 128 : 64;  // elements per k-block
@@ -479,6 +481,8 @@ __global__ void __launch_bounds__(kRRThreads, 1)
   cluster_sync();  // every CTA's reduction barriers exist before any st.async
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();  // A operand / scales come from the previous kernel
+  griddep_launch();
   constexpr int KE = I8 ? 128 : 64;
 
   if (warp == 0) {
@@ -895,19 +899,8 @@ cudaError_t prepare_gemm_kernels() {
 template <int BN, bool I8, bool PAIR>
 static cudaError_t launch_t(const GemmPlan& g, cudaStream_t s) {
   if (g.grid <= 0) return cudaSuccess;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(g.grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = GemmCfg<BN, PAIR>::SMEM;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = PAIR ? 2 : 1;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, I8, PAIR>, g.tmA, PAIR ? g.tmB2 : g.tmB, g.tmC, g.p);
+  return launch_ex(gemm_tc_kernel<BN, I8, PAIR>, dim3(g.grid), dim3(kThreads), GemmCfg<BN, PAIR>::SMEM, s,
+                   PAIR ? 2 : 1, g.tmA, PAIR ? g.tmB2 : g.tmB, g.tmC, g.p);
 }
 
 cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t s) {
@@ -992,19 +985,8 @@ void plan_rr_set_m(RRPlan* g, int M) {
 
 template <bool I8, int MODE>
 static cudaError_t launch_rr_t(const RRPlan& g, cudaStream_t s) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(g.grid);
-  cfg.blockDim = dim3(kRRThreads);
-  cfg.dynamicSmemBytes = RRCfg::SMEM;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = g.cn;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gemm_rr_kernel<I8, MODE>, g.tmA, g.tmB, g.tmC, g.p);
+  return launch_ex(gemm_rr_kernel<I8, MODE>, dim3(g.grid), dim3(kRRThreads), RRCfg::SMEM, s, g.cn, g.tmA, g.tmB,
+                   g.tmC, g.p);
 }
 
 template <bool I8, int MODE>

@@ -75,6 +75,15 @@ constexpr uint64_t kEvictNormal = 0x1000000000000000ull;
 constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;
 constexpr uint64_t kEvictLast = 0x14F0000000000000ull;
 
+// ------------------------------------------- programmatic dependent launch
+// Every kernel of the forward calls griddep_wait() before its first global
+// memory access (so it observes the previous kernel's results) and then
+// griddep_launch() so the next kernel's CTAs can start their prologue (barrier
+// init, TMEM alloc, descriptor prefetch) on SMs this kernel has released.
+// Both are no-ops when the kernel was launched without the PDL attribute.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ------------------------------------------------------------------ cluster
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;

@@ -133,6 +133,8 @@ __global__ void __launch_bounds__(256) embed_ln_kernel(const int32_t* __restrict
                                                       const float* __restrict__ pos, const float* __restrict__ g,
                                                       const float* __restrict__ b, float eps, __half* x16, int ldx,
                                                       int8_t* xq, int ldq, float* xs, int* err_flag) {
+  griddep_wait();
+  griddep_launch();
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (row >= M) return;
   int id = ids[row];
@@ -176,6 +178,8 @@ __global__ void __launch_bounds__(256) add_ln_kernel(const __half* __restrict__ 
                                                     int ldr, int M, int H, const float* __restrict__ g,
                                                     const float* __restrict__ b, float eps, __half* y16, int ldy,
                                                     int8_t* yq, int ldq, float* ys) {
+  griddep_wait();
+  griddep_launch();
   // persistent grid-stride over rows; the next row's 2*NCH 16-byte loads are
   // in flight while the current row is normalised and stored
   const int lane = threadIdx.x & 31;
@@ -215,6 +219,8 @@ __global__ void __launch_bounds__(256) add_ln_kernel(const __half* __restrict__ 
 template <int NCH>
 __global__ void __launch_bounds__(256) quant_rows_kernel(const __half* __restrict__ x, int ldx, int M, int K,
                                                         int8_t* __restrict__ q, int ldq, float* __restrict__ scale) {
+  griddep_wait();
+  griddep_launch();
   const int lane = threadIdx.x & 31;
   const int stride = gridDim.x * 8;
   int row = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -277,6 +283,8 @@ inline unsigned row_grid(int M) {
 __global__ void __launch_bounds__(256) quant_rows_scalar_kernel(const __half* __restrict__ x, int ldx, int M, int K,
                                                                int8_t* __restrict__ q, int ldq,
                                                                float* __restrict__ scale) {
+  griddep_wait();
+  griddep_launch();
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (row >= M) return;
   const __half* xr = x + (size_t)row * ldx;
@@ -298,6 +306,8 @@ constexpr int kHeadJ = 32;
 __global__ void __launch_bounds__(256) pooler_kernel(const __half* __restrict__ x16, int ldx, int B, int S, int H,
                                                     const float* __restrict__ Wp, const float* __restrict__ bp,
                                                     float* __restrict__ pooled) {
+  griddep_wait();
+  griddep_launch();
   extern __shared__ float hsm[];  // [kHeadSeqs][H]
   const int j0 = blockIdx.x * kHeadJ, b0 = blockIdx.y * kHeadSeqs;
   const int nb = min(kHeadSeqs, B - b0);
@@ -329,6 +339,8 @@ __global__ void __launch_bounds__(256) pooler_kernel(const __half* __restrict__ 
 __global__ void __launch_bounds__(256) classifier_kernel(const float* __restrict__ pooled, int B, int H, int C,
                                                         const float* __restrict__ Wc, const float* __restrict__ bc,
                                                         float* __restrict__ logits) {
+  griddep_wait();
+  griddep_launch();
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (t >= B * C) return;
   const int b = t / C, c = t - b * C;
@@ -339,6 +351,7 @@ __global__ void __launch_bounds__(256) classifier_kernel(const float* __restrict
 }
 
 __global__ void cast_f16_kernel(const float* __restrict__ src, int N, int K, __half* __restrict__ dst, int ldd) {
+  griddep_wait();
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (size_t)N * K) return;
   const int n = (int)(i / K), k = (int)(i - (size_t)n * K);
@@ -348,6 +361,7 @@ __global__ void cast_f16_kernel(const float* __restrict__ src, int N, int K, __h
 // Per-output-channel symmetric int8 weights (R7-R8).
 __global__ void __launch_bounds__(256) quant_weight_kernel(const float* __restrict__ src, int N, int K,
                                                           int8_t* __restrict__ dst, int ldd, float* __restrict__ scale) {
+  griddep_wait();
   const int n = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (n >= N) return;
   const float* w = src + (size_t)n * K;
@@ -361,6 +375,7 @@ __global__ void __launch_bounds__(256) quant_weight_kernel(const float* __restri
 
 __global__ void add_row_kernel(const float* __restrict__ src, int N, int K, const float* __restrict__ row,
                                float* __restrict__ dst) {
+  griddep_wait();
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (size_t)N * K) return;
   dst[i] = __fadd_rn(src[i], row[i % K]);
@@ -376,10 +391,10 @@ cudaError_t launch_embed_ln(const int32_t* ids, const int32_t* mask, int B, int 
   const int M = B * S;
   const unsigned grid = (M + 7) / 8;
   switch (chunks_for(H)) {
-    case 1: embed_ln_kernel<1><<<grid, 256, 0, s>>>(ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs, err_flag); break;
-    case 2: embed_ln_kernel<2><<<grid, 256, 0, s>>>(ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs, err_flag); break;
-    case 3: embed_ln_kernel<3><<<grid, 256, 0, s>>>(ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs, err_flag); break;
-    default: embed_ln_kernel<4><<<grid, 256, 0, s>>>(ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs, err_flag); break;
+    case 1: launch_ex(embed_ln_kernel<1>, dim3(grid), dim3(256), 0, s, 1, ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs, err_flag); break;
+    case 2: launch_ex(embed_ln_kernel<2>, dim3(grid), dim3(256), 0, s, 1, ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs, err_flag); break;
+    case 3: launch_ex(embed_ln_kernel<3>, dim3(grid), dim3(256), 0, s, 1, ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs, err_flag); break;
+    default: launch_ex(embed_ln_kernel<4>, dim3(grid), dim3(256), 0, s, 1, ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs, err_flag); break;
   }
   return cudaGetLastError();
 }
@@ -389,10 +404,10 @@ cudaError_t launch_add_ln(const __half* a, int lda, const __half* r, int ldr, in
                           cudaStream_t s) {
   const unsigned grid = row_grid(M);
   switch (chunks_for(H)) {
-    case 1: add_ln_kernel<1><<<grid, 256, 0, s>>>(a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
-    case 2: add_ln_kernel<2><<<grid, 256, 0, s>>>(a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
-    case 3: add_ln_kernel<3><<<grid, 256, 0, s>>>(a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
-    default: add_ln_kernel<4><<<grid, 256, 0, s>>>(a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
+    case 1: launch_ex(add_ln_kernel<1>, dim3(grid), dim3(256), 0, s, 1, a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
+    case 2: launch_ex(add_ln_kernel<2>, dim3(grid), dim3(256), 0, s, 1, a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
+    case 3: launch_ex(add_ln_kernel<3>, dim3(grid), dim3(256), 0, s, 1, a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
+    default: launch_ex(add_ln_kernel<4>, dim3(grid), dim3(256), 0, s, 1, a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
   }
   return cudaGetLastError();
 }
@@ -403,18 +418,18 @@ cudaError_t launch_quant_rows(const __half* x, int ldx, int M, int K, int8_t* q,
   const bool vec = (K % 8 == 0) && (ldx % 8 == 0) && (ldq % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) &&
                    ((reinterpret_cast<uintptr_t>(q) & 7) == 0) && K <= 4096;
   if (!vec) {
-    quant_rows_scalar_kernel<<<grid, 256, 0, s>>>(x, ldx, M, K, q, ldq, scale);
+    launch_ex(quant_rows_scalar_kernel, dim3(grid), dim3(256), 0, s, 1, x, ldx, M, K, q, ldq, scale);
     return cudaGetLastError();
   }
   grid = row_grid(M);
   const int n = chunks_for(K);
-  if (n <= 1) quant_rows_kernel<1><<<grid, 256, 0, s>>>(x, ldx, M, K, q, ldq, scale);
-  else if (n <= 2) quant_rows_kernel<2><<<grid, 256, 0, s>>>(x, ldx, M, K, q, ldq, scale);
-  else if (n <= 4) quant_rows_kernel<4><<<grid, 256, 0, s>>>(x, ldx, M, K, q, ldq, scale);
-  else if (n <= 6) quant_rows_kernel<6><<<grid, 256, 0, s>>>(x, ldx, M, K, q, ldq, scale);
-  else if (n <= 8) quant_rows_kernel<8><<<grid, 256, 0, s>>>(x, ldx, M, K, q, ldq, scale);
-  else if (n <= 12) quant_rows_kernel<12><<<grid, 256, 0, s>>>(x, ldx, M, K, q, ldq, scale);
-  else quant_rows_kernel<16><<<grid, 256, 0, s>>>(x, ldx, M, K, q, ldq, scale);
+  if (n <= 1) launch_ex(quant_rows_kernel<1>, dim3(grid), dim3(256), 0, s, 1, x, ldx, M, K, q, ldq, scale);
+  else if (n <= 2) launch_ex(quant_rows_kernel<2>, dim3(grid), dim3(256), 0, s, 1, x, ldx, M, K, q, ldq, scale);
+  else if (n <= 4) launch_ex(quant_rows_kernel<4>, dim3(grid), dim3(256), 0, s, 1, x, ldx, M, K, q, ldq, scale);
+  else if (n <= 6) launch_ex(quant_rows_kernel<6>, dim3(grid), dim3(256), 0, s, 1, x, ldx, M, K, q, ldq, scale);
+  else if (n <= 8) launch_ex(quant_rows_kernel<8>, dim3(grid), dim3(256), 0, s, 1, x, ldx, M, K, q, ldq, scale);
+  else if (n <= 12) launch_ex(quant_rows_kernel<12>, dim3(grid), dim3(256), 0, s, 1, x, ldx, M, K, q, ldq, scale);
+  else launch_ex(quant_rows_kernel<16>, dim3(grid), dim3(256), 0, s, 1, x, ldx, M, K, q, ldq, scale);
   return cudaGetLastError();
 }
 
@@ -422,10 +437,10 @@ cudaError_t launch_head(const __half* x16, int ldx, int B, int S, int H, int C, 
                         const float* Wc, const float* bc, float* pooled, float* logits, cudaStream_t s) {
   const size_t smem = kHeadSeqs * H * sizeof(float);
   dim3 grid((H + kHeadJ - 1) / kHeadJ, (B + kHeadSeqs - 1) / kHeadSeqs);
-  pooler_kernel<<<grid, 256, smem, s>>>(x16, ldx, B, S, H, Wp, bp, pooled);
+  launch_ex(pooler_kernel, dim3(grid), dim3(256), smem, s, 1, x16, ldx, B, S, H, Wp, bp, pooled);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  classifier_kernel<<<(B * C + 7) / 8, 256, 0, s>>>(pooled, B, H, C, Wc, bc, logits);
+  launch_ex(classifier_kernel, dim3((B * C + 7) / 8), dim3(256), 0, s, 1, pooled, B, H, C, Wc, bc, logits);
   return cudaGetLastError();
 }
 
@@ -435,18 +450,18 @@ cudaError_t prepare_row_kernels() {
 
 cudaError_t launch_cast_f16(const float* src, int N, int K, __half* dst, int ldd, cudaStream_t s) {
   const size_t n = (size_t)N * K;
-  cast_f16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, N, K, dst, ldd);
+  launch_ex(cast_f16_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, 1, src, N, K, dst, ldd);
   return cudaGetLastError();
 }
 
 cudaError_t launch_quant_weight(const float* src, int N, int K, int8_t* dst, int ldd, float* scale, cudaStream_t s) {
-  quant_weight_kernel<<<(N + 7) / 8, 256, 0, s>>>(src, N, K, dst, ldd, scale);
+  launch_ex(quant_weight_kernel, dim3((N + 7) / 8), dim3(256), 0, s, 1, src, N, K, dst, ldd, scale);
   return cudaGetLastError();
 }
 
 cudaError_t launch_add_row(const float* src, int N, int K, const float* row, float* dst, cudaStream_t s) {
   const size_t n = (size_t)N * K;
-  add_row_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, N, K, row, dst);
+  launch_ex(add_row_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, 1, src, N, K, row, dst);
   return cudaGetLastError();
 }
 
