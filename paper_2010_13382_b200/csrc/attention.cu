@@ -301,7 +301,7 @@ cudaError_t launch_dp(const __half* qkv, int ld, const int32_t* mask, int B, int
   const int n_items = B * A * ((S + QT - 1) / QT);
   const int per_sm = 1;  // ~240 registers x 256 threads: one resident CTA per SM
   const int grid = n_items < kNumSMs * per_sm ? n_items : kNumSMs * per_sm;
-  launch_ex(attention_kernel<DP>, dim3(grid), dim3(256), nbuf * one, s, 1, qkv, ld, mask, B, S, A, d, scale, ctx, ldc,
+  launch_ex(attention_kernel<DP>, dim3(grid), dim3(256), nbuf * one, s, 0, qkv, ld, mask, B, S, A, d, scale, ctx, ldc,
             nbuf);
   return cudaGetLastError();
 }

@@ -243,7 +243,7 @@ cudaError_t launch_attention_tc(const CUtensorMap& map, const int32_t* mask, int
   const int n_items = B * A;
   const int grid = n_items < 2 * kNumSMs ? n_items : 2 * kNumSMs;
   const float scale = (float)(1.0 / sqrt((double)kD));
-  launch_ex(attention_tc_kernel, dim3(grid), dim3(kThreadsTC), SmemTC::TOTAL, s, 1, map, mask, B, S, A, scale, ctx,
+  launch_ex(attention_tc_kernel, dim3(grid), dim3(kThreadsTC), SmemTC::TOTAL, s, 0, map, mask, B, S, A, scale, ctx,
             ldctx);
   return cudaGetLastError();
 }

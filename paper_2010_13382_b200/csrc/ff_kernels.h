@@ -11,7 +11,8 @@ namespace ff {
 constexpr int kNumSMs = 148;
 
 // Launch with the programmatic-dependent-launch attribute (when enabled) and
-// an optional 1-D cluster.  All forward-pass kernels go through this.
+// an optional 1-D cluster (cluster = 0: no cluster attribute).  All
+// forward-pass kernels go through this.
 extern bool g_pdl;
 template <typename... KArgs, typename... Args>
 cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int cluster,
@@ -28,7 +29,7 @@ cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem
     attr[n].val.programmaticStreamSerializationAllowed = 1;
     ++n;
   }
-  if (cluster > 1) {
+  if (cluster >= 1) {  // 0 = plain launch; >= 1 = cluster launch (kernels using cluster PTX need it even for 1)
     attr[n].id = cudaLaunchAttributeClusterDimension;
     attr[n].val.clusterDim.x = cluster;
     attr[n].val.clusterDim.y = 1;

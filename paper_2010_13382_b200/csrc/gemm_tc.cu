@@ -900,7 +900,7 @@ template <int BN, bool I8, bool PAIR>
 static cudaError_t launch_t(const GemmPlan& g, cudaStream_t s) {
   if (g.grid <= 0) return cudaSuccess;
   return launch_ex(gemm_tc_kernel<BN, I8, PAIR>, dim3(g.grid), dim3(kThreads), GemmCfg<BN, PAIR>::SMEM, s,
-                   PAIR ? 2 : 1, g.tmA, PAIR ? g.tmB2 : g.tmB, g.tmC, g.p);
+                   PAIR ? 2 : 0, g.tmA, PAIR ? g.tmB2 : g.tmB, g.tmC, g.p);
 }
 
 cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t s) {

@@ -180,39 +180,33 @@ __global__ void __launch_bounds__(256) add_ln_kernel(const __half* __restrict__ 
                                                     int8_t* yq, int ldq, float* ys) {
   griddep_wait();
   griddep_launch();
-  // persistent grid-stride over rows; the next row's 2*NCH 16-byte loads are
-  // in flight while the current row is normalised and stored
+  // one row per warp (measured faster than a grid-stride loop with prefetch,
+  // which lowers occupancy); all 2*NCH 16-byte loads are issued up front
   const int lane = threadIdx.x & 31;
-  const int stride = gridDim.x * 8;
-  int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= M) return;
   uint4 ua[NCH], ur[NCH];
-  auto load_row = [&](int rw) {
 #pragma unroll
-    for (int c = 0; c < NCH; ++c) {
-      const int col = 8 * (lane + 32 * c);
-      if (rw < M && col < H) {
-        ua[c] = __ldcs(reinterpret_cast<const uint4*>(a + (size_t)rw * lda + col));
-        ur[c] = __ldcs(reinterpret_cast<const uint4*>(r + (size_t)rw * ldr + col));
-      }
+  for (int c = 0; c < NCH; ++c) {
+    const int col = 8 * (lane + 32 * c);
+    if (col < H) {
+      ua[c] = __ldcs(reinterpret_cast<const uint4*>(a + (size_t)row * lda + col));
+      ur[c] = __ldcs(reinterpret_cast<const uint4*>(r + (size_t)row * ldr + col));
     }
-  };
-  load_row(row);
-  for (; row < M; row += stride) {
-    float v[NCH][8];
-#pragma unroll
-    for (int c = 0; c < NCH; ++c) {
-      if (8 * (lane + 32 * c) < H) {
-        float fa[8], fr[8];
-        unpack8(ua[c], fa);
-        unpack8(ur[c], fr);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[c][j] = __fadd_rn(fa[j], fr[j]);
-      }
-    }
-    load_row(row + stride);
-    ln_store<NCH>(v, H, lane, g, b, eps, y16 + (size_t)row * ldy, yq ? yq + (size_t)row * ldq : nullptr,
-                  ys ? ys + row : nullptr);
   }
+  float v[NCH][8];
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    if (8 * (lane + 32 * c) < H) {
+      float fa[8], fr[8];
+      unpack8(ua[c], fa);
+      unpack8(ur[c], fr);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[c][j] = __fadd_rn(fa[j], fr[j]);
+    }
+  }
+  ln_store<NCH>(v, H, lane, g, b, eps, y16 + (size_t)row * ldy, yq ? yq + (size_t)row * ldq : nullptr,
+                ys ? ys + row : nullptr);
 }
 
 // One warp per row, the row in registers (NCH 16-byte chunks per lane).
@@ -391,10 +385,10 @@ cudaError_t launch_embed_ln(const int32_t* ids, const int32_t* mask, int B, int 
   const int M = B * S;
   const unsigned grid = (M + 7) / 8;
   switch (chunks_for(H)) {
-    case 1: launch_ex(embed_ln_kernel<1>, dim3(grid), dim3(256), 0, s, 1, ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs, err_flag); break;
-    case 2: launch_ex(embed_ln_kernel<2>, dim3(grid), dim3(256), 0, s, 1, ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs, err_flag); break;
-    case 3: launch_ex(embed_ln_kernel<3>, dim3(grid), dim3(256), 0, s, 1, ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs, err_flag); break;
-    default: launch_ex(embed_ln_kernel<4>, dim3(grid), dim3(256), 0, s, 1, ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs, err_flag); break;
+    case 1: launch_ex(embed_ln_kernel<1>, dim3(grid), dim3(256), 0, s, 0,ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs, err_flag); break;
+    case 2: launch_ex(embed_ln_kernel<2>, dim3(grid), dim3(256), 0, s, 0,ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs, err_flag); break;
+    case 3: launch_ex(embed_ln_kernel<3>, dim3(grid), dim3(256), 0, s, 0,ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs, err_flag); break;
+    default: launch_ex(embed_ln_kernel<4>, dim3(grid), dim3(256), 0, s, 0,ids, mask, M, S, H, V, tok, pos, g, b, eps, x16, ldx, xq, ldq, xs, err_flag); break;
   }
   return cudaGetLastError();
 }
@@ -404,10 +398,10 @@ cudaError_t launch_add_ln(const __half* a, int lda, const __half* r, int ldr, in
                           cudaStream_t s) {
   const unsigned grid = row_grid(M);
   switch (chunks_for(H)) {
-    case 1: launch_ex(add_ln_kernel<1>, dim3(grid), dim3(256), 0, s, 1, a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
-    case 2: launch_ex(add_ln_kernel<2>, dim3(grid), dim3(256), 0, s, 1, a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
-    case 3: launch_ex(add_ln_kernel<3>, dim3(grid), dim3(256), 0, s, 1, a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
-    default: launch_ex(add_ln_kernel<4>, dim3(grid), dim3(256), 0, s, 1, a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
+    case 1: launch_ex(add_ln_kernel<1>, dim3(grid), dim3(256), 0, s, 0,a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
+    case 2: launch_ex(add_ln_kernel<2>, dim3(grid), dim3(256), 0, s, 0,a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
+    case 3: launch_ex(add_ln_kernel<3>, dim3(grid), dim3(256), 0, s, 0,a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
+    default: launch_ex(add_ln_kernel<4>, dim3(grid), dim3(256), 0, s, 0,a, lda, r, ldr, M, H, g, b, eps, y16, ldy, yq, ldq, ys); break;
   }
   return cudaGetLastError();
 }
@@ -418,18 +412,18 @@ cudaError_t launch_quant_rows(const __half* x, int ldx, int M, int K, int8_t* q,
   const bool vec = (K % 8 == 0) && (ldx % 8 == 0) && (ldq % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) &&
                    ((reinterpret_cast<uintptr_t>(q) & 7) == 0) && K <= 4096;
   if (!vec) {
-    launch_ex(quant_rows_scalar_kernel, dim3(grid), dim3(256), 0, s, 1, x, ldx, M, K, q, ldq, scale);
+    launch_ex(quant_rows_scalar_kernel, dim3(grid), dim3(256), 0, s, 0,x, ldx, M, K, q, ldq, scale);
     return cudaGetLastError();
   }
   grid = row_grid(M);
   const int n = chunks_for(K);
-  if (n <= 1) launch_ex(quant_rows_kernel<1>, dim3(grid), dim3(256), 0, s, 1, x, ldx, M, K, q, ldq, scale);
-  else if (n <= 2) launch_ex(quant_rows_kernel<2>, dim3(grid), dim3(256), 0, s, 1, x, ldx, M, K, q, ldq, scale);
-  else if (n <= 4) launch_ex(quant_rows_kernel<4>, dim3(grid), dim3(256), 0, s, 1, x, ldx, M, K, q, ldq, scale);
-  else if (n <= 6) launch_ex(quant_rows_kernel<6>, dim3(grid), dim3(256), 0, s, 1, x, ldx, M, K, q, ldq, scale);
-  else if (n <= 8) launch_ex(quant_rows_kernel<8>, dim3(grid), dim3(256), 0, s, 1, x, ldx, M, K, q, ldq, scale);
-  else if (n <= 12) launch_ex(quant_rows_kernel<12>, dim3(grid), dim3(256), 0, s, 1, x, ldx, M, K, q, ldq, scale);
-  else launch_ex(quant_rows_kernel<16>, dim3(grid), dim3(256), 0, s, 1, x, ldx, M, K, q, ldq, scale);
+  if (n <= 1) launch_ex(quant_rows_kernel<1>, dim3(grid), dim3(256), 0, s, 0,x, ldx, M, K, q, ldq, scale);
+  else if (n <= 2) launch_ex(quant_rows_kernel<2>, dim3(grid), dim3(256), 0, s, 0,x, ldx, M, K, q, ldq, scale);
+  else if (n <= 4) launch_ex(quant_rows_kernel<4>, dim3(grid), dim3(256), 0, s, 0,x, ldx, M, K, q, ldq, scale);
+  else if (n <= 6) launch_ex(quant_rows_kernel<6>, dim3(grid), dim3(256), 0, s, 0,x, ldx, M, K, q, ldq, scale);
+  else if (n <= 8) launch_ex(quant_rows_kernel<8>, dim3(grid), dim3(256), 0, s, 0,x, ldx, M, K, q, ldq, scale);
+  else if (n <= 12) launch_ex(quant_rows_kernel<12>, dim3(grid), dim3(256), 0, s, 0,x, ldx, M, K, q, ldq, scale);
+  else launch_ex(quant_rows_kernel<16>, dim3(grid), dim3(256), 0, s, 0,x, ldx, M, K, q, ldq, scale);
   return cudaGetLastError();
 }
 
@@ -437,10 +431,10 @@ cudaError_t launch_head(const __half* x16, int ldx, int B, int S, int H, int C, 
                         const float* Wc, const float* bc, float* pooled, float* logits, cudaStream_t s) {
   const size_t smem = kHeadSeqs * H * sizeof(float);
   dim3 grid((H + kHeadJ - 1) / kHeadJ, (B + kHeadSeqs - 1) / kHeadSeqs);
-  launch_ex(pooler_kernel, dim3(grid), dim3(256), smem, s, 1, x16, ldx, B, S, H, Wp, bp, pooled);
+  launch_ex(pooler_kernel, dim3(grid), dim3(256), smem, s, 0,x16, ldx, B, S, H, Wp, bp, pooled);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  launch_ex(classifier_kernel, dim3((B * C + 7) / 8), dim3(256), 0, s, 1, pooled, B, H, C, Wc, bc, logits);
+  launch_ex(classifier_kernel, dim3((B * C + 7) / 8), dim3(256), 0, s, 0,pooled, B, H, C, Wc, bc, logits);
   return cudaGetLastError();
 }
 
@@ -450,18 +444,18 @@ cudaError_t prepare_row_kernels() {
 
 cudaError_t launch_cast_f16(const float* src, int N, int K, __half* dst, int ldd, cudaStream_t s) {
   const size_t n = (size_t)N * K;
-  launch_ex(cast_f16_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, 1, src, N, K, dst, ldd);
+  launch_ex(cast_f16_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, 0,src, N, K, dst, ldd);
   return cudaGetLastError();
 }
 
 cudaError_t launch_quant_weight(const float* src, int N, int K, int8_t* dst, int ldd, float* scale, cudaStream_t s) {
-  launch_ex(quant_weight_kernel, dim3((N + 7) / 8), dim3(256), 0, s, 1, src, N, K, dst, ldd, scale);
+  launch_ex(quant_weight_kernel, dim3((N + 7) / 8), dim3(256), 0, s, 0,src, N, K, dst, ldd, scale);
   return cudaGetLastError();
 }
 
 cudaError_t launch_add_row(const float* src, int N, int K, const float* row, float* dst, cudaStream_t s) {
   const size_t n = (size_t)N * K;
-  launch_ex(add_row_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, 1, src, N, K, row, dst);
+  launch_ex(add_row_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, 0,src, N, K, row, dst);
   return cudaGetLastError();
 }
 
