@@ -217,6 +217,17 @@ FF_API ff_status ff_debug_quant_rows(const void *d_x16, int32_t M, int32_t K, in
  * 2 = tcgen05 only (FF_E_UNSUPPORTED otherwise). */
 FF_API ff_status ff_debug_attention(const void *d_qkv16, const int32_t *d_mask, int32_t B, int32_t S, int32_t A,
                                     int32_t d, void *d_ctx16, int32_t impl, void *stream);
+/* The tcgen05 attention with the int8 ctx requant fused (a3 + a4; the path
+ * int8 layers take): ctx rows are quantized per row, Q8row (DESIGN R6-R8),
+ * from their fp16-rounded values.  d_ctxq: s8 [B*S x A*d] (pitch A*d),
+ * d_ctxs: fp32 [B*S] scales; d_ctx16 (optional, may be NULL) also receives
+ * the fp16 ctx.  Requires head_dim 64, S <= 128, 1 <= A <= 8 (else
+ * FF_E_UNSUPPORTED).  d_trace (optional, may be NULL): uint64 [grid x 32 x 8]
+ * per-CTA per-head event timestamps (%globaltimer, ns) for pipeline analysis;
+ * grid = min(B, 148). */
+FF_API ff_status ff_debug_attention_q8(const void *d_qkv16, const int32_t *d_mask, int32_t B, int32_t S, int32_t A,
+                                       int32_t d, void *d_ctx16, int8_t *d_ctxq, float *d_ctxs, uint64_t *d_trace,
+                                       void *stream);
 
 #ifdef __cplusplus
 }

@@ -3,22 +3,29 @@
 // headline configs (P:135 multi-head attention node fusion;
 // Q.K^T and P.V in floating point).
 //
-// One work item = (sequence b, head h < A'_l); 2 persistent CTAs per SM.
+// One work item = (sequence b, group of <= 8 heads); one persistent CTA per SM
+// walks the heads of its item with Q/K/V double-buffered across heads.
 //   warp 0     TMA: Q, K, V head slices (128 rows x 64 fp16, 128B-swizzled)
 //   warp 1     TMEM allocator + MMA issuer (one thread):
 //                S[128 x 128] (TMEM, fp32) = Q . K^T        kind::f16, K-major A/B
 //                O[128 x  64] (TMEM, fp32) = P . V          A = P (smem, K-major),
 //                                                            B = V (smem, MN-major)
-//   warps 2-5  softmax + epilogue, thread = query row (TMEM lane):
+//   warps 2-9  softmax + epilogue: TMEM lane quadrant = query rows, two warps
+//              per quadrant split the keys (and O's columns) in halves:
 //                s = fp32(q.k) * fp32(1/sqrt(d)), masked keys -> -inf (R4)
 //                p = exp(s - max) / sum  in fp32, P16 = R16(p)  (R9, normalized
 //                before P.V), written to smem in the 128B-swizzled K-major
-//                layout the MMA reads; ctx = R16(O) stored to HBM.
-// Row max / sum are thread-local (one thread owns a whole score row), so the
-// reduction order is a fixed sequential order.  Keys beyond S (S < 128) are
-// masked; Q rows beyond S are computed and not stored.
+//                layout the MMA reads; ctx = R16(O).
+// int8 layers (A <= 8): the R16 ctx of all heads of the row is parked in TMEM
+// (packed fp16 pairs, columns [256, 256 + 32 A)) and quantized per row (Q8row,
+// R6-R8) after the last head, so ctx goes to HBM once, as s8 rows + scale
+// (SURVEY 8(a) a3+a4 fused).  Otherwise ctx is stored as fp16 rows.
+// Row max / sum are combined across the two half-row threads through smem in
+// a fixed order.  Keys beyond S (S < 128) are masked; Q rows beyond S are
+// computed and not stored.
 #include "ff_kernels.h"
 #include "ptx.cuh"
+#include "quant.cuh"
 
 namespace ff {
 
@@ -27,17 +34,22 @@ namespace {
 constexpr int kQ = 128;             // queries per item (TMEM lanes)
 constexpr int kKeys = 128;          // keys (S <= 128)
 constexpr int kD = 64;              // head_dim
+constexpr int kMaxHeads = 8;        // heads per item
 constexpr int kTileBytes = 128 * 128;  // 128 rows x 128 B (64 fp16)
-constexpr int kThreadsTC = 192;
+constexpr int kKVStages = 3;
+constexpr int kSoftmaxWarps = 8;
+constexpr int kThreadsTC = 64 + 32 * kSoftmaxWarps;
+constexpr uint32_t kTmemO = 128;    // O[2]: columns [128, 192), [192, 256)
+constexpr uint32_t kTmemCtx = 256;  // packed ctx [256, 256 + 32 * heads)
 
 struct SmemTC {
-  static constexpr int Q = 0;
-  static constexpr int K = Q + kTileBytes;
-  static constexpr int V = K + kTileBytes;
-  static constexpr int P = V + kTileBytes;          // 2 k-blocks of 64 keys, 128B-swizzled
-  static constexpr int MASK = P + 2 * kTileBytes;   // kKeys floats
-  static constexpr int BAR = MASK + kKeys * 4;
-  static constexpr int TOTAL = BAR + 128 + 1024;    // barriers + alignment slack
+  static constexpr int SLOT = 3 * kTileBytes;                // Q, K, V of one head
+  static constexpr int P = kKVStages * SLOT;                 // P[2]: 2 k-blocks of 64 keys, 128B-swizzled
+  static constexpr int MASK = P + 2 * 2 * kTileBytes;        // kKeys floats
+  static constexpr int RED = MASK + kKeys * 4;               // [3][2][128] floats: max, sum, amax
+  static constexpr int BAR = RED + 3 * 2 * kQ * 4;
+  static constexpr int TOTAL = BAR + 256 + 1024;             // barriers + alignment slack
+  static_assert(TOTAL <= 227 * 1024, "smem budget");
 };
 
 // kind::f16, fp32 accumulate, M = 128; b_mn = 1 when B is MN-major.
@@ -56,39 +68,92 @@ __device__ __forceinline__ float ex2f(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// Debug timeline (ff_debug_attention_q8 with a trace buffer): globaltimer of
+// event e for head n of CTA c at trace[(c * kTraceHeads + n) * 8 + e].
+constexpr int kTraceHeads = 32;
+__device__ __forceinline__ void trace_ev(unsigned long long* trace, uint32_t n, int e) {
+  if (trace != nullptr && n < kTraceHeads) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    trace[((size_t)blockIdx.x * kTraceHeads + n) * 8 + e] = t;
+  }
+}
+__device__ __forceinline__ void softmax_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
-__global__ void __launch_bounds__(kThreadsTC, 2)
+// Walk of the heads one CTA processes: items blockIdx.x, +gridDim.x, ...;
+// each item = (sequence b, heads [h0, h0 + nh)).
+struct HeadIter {
+  int item, hl, b, h0, nh;
+  int n_items, n_groups, A, stride;
+  __device__ HeadIter(int first, int n_items_, int n_groups_, int A_, int stride_)
+      : item(first), hl(0), n_items(n_items_), n_groups(n_groups_), A(A_), stride(stride_) {
+    set();
+  }
+  __device__ void set() {
+    if (item < n_items) {
+      b = item / n_groups;
+      h0 = (item - b * n_groups) * kMaxHeads;
+      nh = min(A, h0 + kMaxHeads) - h0;
+    }
+  }
+  __device__ bool valid() const { return item < n_items; }
+  __device__ void next() {
+    if (++hl == nh) {
+      hl = 0;
+      item += stride;
+      set();
+    }
+  }
+};
+
+// Per-head schedule (n = this CTA's head counter; every role walks the same
+// sequence).  The MMA thread issues S(n) = Q K^T before O(n-1) = P V, and the
+// softmax warps run the ctx epilogue of head n-1 after publishing P(n), so the
+// softmax of one head overlaps the P.V MMA of the previous one:
+//   MMA:     .. S(n) | O(n-1) | S(n+1) | O(n) ..
+//   softmax: .. softmax(n) -> P[n&1] | epilogue(n-1) from O[(n-1)&1] | softmax(n+1) ..
+// Buffers: Q/K/V x3 stages (smem), S x1 (TMEM), P x2 (smem), O x2 (TMEM).
+__global__ void __launch_bounds__(kThreadsTC, 1)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const int32_t* __restrict__ mask, int B, int S,
-                        int A, float scale, __half* __restrict__ ctx, int ldc) {
+                        int A, float scale, __half* __restrict__ ctx, int ldc, int8_t* __restrict__ ctxq, int ldq,
+                        float* __restrict__ ctxs, const uint8_t* __restrict__ qkv_rows, int row_bytes,
+                        unsigned long long* __restrict__ trace) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SmemTC::BAR);
-  uint64_t* kv_full = bar + 0;   // TMA -> MMA
-  uint64_t* kv_empty = bar + 1;  // MMA (after P.V) -> TMA
-  uint64_t* s_full = bar + 2;    // MMA1 -> softmax
-  uint64_t* s_empty = bar + 3;   // softmax (S read) -> MMA1
-  uint64_t* p_full = bar + 4;    // softmax (P written) -> MMA2
-  uint64_t* o_full = bar + 5;    // MMA2 -> epilogue
-  uint64_t* o_empty = bar + 6;   // epilogue (O read) -> MMA2
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
+  uint64_t* kv_full = bar + 0;    // [3] TMA -> MMA
+  uint64_t* kv_empty = bar + 3;   // [3] MMA (after P.V) -> TMA
+  uint64_t* s_full = bar + 6;     // MMA1 -> softmax
+  uint64_t* s_empty = bar + 7;    // softmax (S read) -> MMA1
+  uint64_t* p_full = bar + 8;     // [2] softmax (P written) -> MMA2
+  uint64_t* o_full = bar + 10;    // [2] MMA2 -> epilogue
+  uint64_t* o_empty = bar + 12;   // [2] epilogue (O read) -> MMA2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
   float* sMask = reinterpret_cast<float*>(smem + SmemTC::MASK);
+  float* sRed = reinterpret_cast<float*>(smem + SmemTC::RED);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int D = A * kD;
-  const int n_items = B * A;
+  const int n_groups = (A + kMaxHeads - 1) / kMaxHeads;
+  const int n_items = B * n_groups;
+  constexpr int kSoftmaxThreads = 32 * kSoftmaxWarps;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmQKV);
-    mbar_init(kv_full, 1);
-    mbar_init(kv_empty, 1);
+    for (int i = 0; i < kKVStages; ++i) {
+      mbar_init(kv_full + i, 1);
+      mbar_init(kv_empty + i, 1);
+    }
     mbar_init(s_full, 1);
-    mbar_init(s_empty, 128);
-    mbar_init(p_full, 128);
-    mbar_init(o_full, 1);
-    mbar_init(o_empty, 128);
+    mbar_init(s_empty, kSoftmaxThreads);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(p_full + i, kSoftmaxThreads);
+      mbar_init(o_full + i, 1);
+      mbar_init(o_empty + i, kSoftmaxThreads);
+    }
     fence_barrier_init();
   }
   if (warp == 1) {
-    tmem_alloc(tmem_slot, 256);  // S: columns [0,128), O: [128,192)
+    tmem_alloc(tmem_slot, 512);  // S [0,128), O[2] [128,256), packed ctx [256, 512)
     tmem_relinquish();
   }
   tc_fence_before();
@@ -100,126 +165,267 @@ __global__ void __launch_bounds__(kThreadsTC, 2)
 
   if (warp == 0) {
     if (lane == 0) {
-      uint32_t ph = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ph ^= 1) {
-        const int b = item / A, h = item - b * A;
-        mbar_wait(kv_empty, ph ^ 1);
-        mbar_expect_tx(kv_full, 3 * kTileBytes);
-        tma_load_2d(smem + SmemTC::Q, &tmQKV, kv_full, h * kD, b * S, kEvictFirst);
-        tma_load_2d(smem + SmemTC::K, &tmQKV, kv_full, D + h * kD, b * S, kEvictFirst);
-        tma_load_2d(smem + SmemTC::V, &tmQKV, kv_full, 2 * D + h * kD, b * S, kEvictFirst);
+      // The head slices are 128-byte column strips of the QKV rows; fetched
+      // strip by strip straight from HBM they reopen each DRAM page once per
+      // head.  Prefetch an item's rows (contiguous, S x row_bytes) into L2 as
+      // a whole first: the current item at its start, the next one halfway.
+      auto prefetch_rows = [&](int item) {
+        if (item >= n_items) return;
+        const uint8_t* p0 = qkv_rows + (size_t)(item / n_groups) * S * row_bytes;
+        const size_t total = (size_t)S * row_bytes;
+        for (size_t off = 0; off < total; off += 32768)
+          bulk_prefetch_l2(p0 + off, (uint32_t)min((size_t)32768, total - off));
+      };
+      uint32_t n = 0;
+      for (HeadIter it(blockIdx.x, n_items, n_groups, A, gridDim.x); it.valid(); it.next(), ++n) {
+        if (n == 0) prefetch_rows(it.item);
+        if (it.hl == it.nh / 2) prefetch_rows(it.item + it.stride);
+        const int slot = n % kKVStages;
+        const int h = it.h0 + it.hl;
+        uint8_t* base = smem + slot * SmemTC::SLOT;
+        mbar_wait(kv_empty + slot, ((n / kKVStages) & 1) ^ 1);
+        trace_ev(trace, n, 0);
+        mbar_expect_tx(kv_full + slot, 3 * kTileBytes);
+        tma_load_2d(base, &tmQKV, kv_full + slot, h * kD, it.b * S, kEvictFirst);
+        tma_load_2d(base + kTileBytes, &tmQKV, kv_full + slot, D + h * kD, it.b * S, kEvictFirst);
+        tma_load_2d(base + 2 * kTileBytes, &tmQKV, kv_full + slot, 2 * D + h * kD, it.b * S, kEvictFirst);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t id1 = idesc_f16(kKeys, 0);  // S = Q K^T: N = 128 keys
       constexpr uint32_t id2 = idesc_f16(kD, 1);     // O = P V:   N = 64, V MN-major
-      uint32_t ph = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ph ^= 1) {
-        mbar_wait(kv_full, ph);
-        mbar_wait(s_empty, ph ^ 1);
+      auto issue_pv = [&](uint32_t m) {
+        const int ps = m & 1;
+        const int slot = m % kKVStages;
+        mbar_wait(p_full + ps, (m >> 1) & 1);
+        trace_ev(trace, m, 5);
+        mbar_wait(o_empty + ps, ((m >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint64_t qd = make_sw128_desc(smem + SmemTC::Q), kd = make_sw128_desc(smem + SmemTC::K);
-#pragma unroll
-        for (int k = 0; k < kD / 16; ++k) mma_f16(tmem, qd + 2 * k, kd + 2 * k, id1, k != 0);
-        mma_commit(s_full);
-        mbar_wait(p_full, ph);
-        mbar_wait(o_empty, ph ^ 1);
-        tc_fence_after();
+        uint8_t* P = smem + SmemTC::P + ps * 2 * kTileBytes;
+        uint8_t* V = smem + slot * SmemTC::SLOT + 2 * kTileBytes;
 #pragma unroll
         for (int k = 0; k < kKeys / 16; ++k) {
           // A = P: k-block k/4 (64 keys), +32 B per 16 keys inside the 128B row
-          const uint64_t pd = make_sw128_desc(smem + SmemTC::P + (k >> 2) * kTileBytes) + 2 * (k & 3);
+          const uint64_t pd = make_sw128_desc(P + (k >> 2) * kTileBytes) + 2 * (k & 3);
           // B = V (MN-major): 16 keys = two 8-row groups = 2048 B
-          const uint64_t vd = make_sw128_desc_mn(smem + SmemTC::V + k * 2048);
-          mma_f16(tmem + 128, pd, vd, id2, k != 0);
+          const uint64_t vd = make_sw128_desc_mn(V + k * 2048);
+          mma_f16(tmem + kTmemO + ps * kD, pd, vd, id2, k != 0);
         }
-        mma_commit(o_full);
-        mma_commit(kv_empty);  // Q/K/V (and P) smem free once these MMAs complete
+        mma_commit(o_full + ps);
+        mma_commit(kv_empty + slot);  // Q/K/V of head m free once these MMAs complete
+      };
+      uint32_t n = 0;
+      for (HeadIter it(blockIdx.x, n_items, n_groups, A, gridDim.x); it.valid(); it.next(), ++n) {
+        const int slot = n % kKVStages;
+        uint8_t* base = smem + slot * SmemTC::SLOT;
+        mbar_wait(kv_full + slot, (n / kKVStages) & 1);
+        trace_ev(trace, n, 1);
+        mbar_wait(s_empty, (n & 1) ^ 1);
+        trace_ev(trace, n, 2);
+        tc_fence_after();
+        const uint64_t qd = make_sw128_desc(base), kd = make_sw128_desc(base + kTileBytes);
+#pragma unroll
+        for (int k = 0; k < kD / 16; ++k) mma_f16(tmem, qd + 2 * k, kd + 2 * k, id1, k != 0);
+        mma_commit(s_full);
+        if (n > 0) issue_pv(n - 1);
       }
+      if (n > 0) issue_pv(n - 1);
     }
   } else {
-    const int q = warp & 3;  // TMEM lane quadrant
+    const int q = warp & 3;             // TMEM lane quadrant
+    const int half = (warp - 2) >> 2;   // keys [64 half, 64 half + 64), O columns [32 half, 32 half + 32)
     const int r = q * 32 + lane;
+    const int tid = threadIdx.x - 64;
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-    constexpr float kLog2e = 1.4426950408889634f;
-    uint32_t ph = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ph ^= 1) {
-      const int b = item / A, h = item - b * A;
-      // key mask of this sequence (keys >= S masked); consumed after s_full
-      const int tid = threadIdx.x - 64;
-      // sMask is rewritten per item: the previous item's softmax (same threads)
-      // finished reading it before p_full, so a named barrier suffices
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      sMask[tid] = (tid < S && __ldg(mask + (size_t)b * S + tid) != 0) ? 0.0f : -INFINITY;
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      mbar_wait(s_full, ph);
+    float* redMax = sRed;
+    float* redSum = sRed + 2 * kQ;
+    float* redAmax = sRed + 4 * kQ;
+    const float sl2 = scale * 1.4426950408889634f;
+    const bool fuse_q = ctxq != nullptr;
+    // the two warps sharing TMEM lane quadrant q (same rows, other key half)
+    const int pair_bar = 2 + q;
+    auto pair_sync = [pair_bar]() { asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory"); };
+    __half2 amax2 = __float2half2_rn(0.0f);  // |ctx| max of the row over the heads epilogued so far
+
+    // ctx epilogue of head m = head h of sequence b (local index hl): R16(O),
+    // fp16 store and/or parking in TMEM; after the item's last head, Q8row.
+    auto epilogue = [&](uint32_t m, int b, int h, int hl, bool last, int nh) {
+      const int os = m & 1;
+      const size_t grow = (size_t)b * S + r;
+      mbar_wait(o_full + os, (m >> 1) & 1);
+      if (threadIdx.x == 64) trace_ev(trace, m, 6);
       tc_fence_after();
-      uint32_t raw[kKeys / 32][32];
+      uint32_t o[32];
+      tmem_ld32(trow + kTmemO + os * kD + half * 32, o);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(o_empty + os);
+      uint32_t pk[16];
 #pragma unroll
-      for (int c = 0; c < kKeys / 32; ++c) tmem_ld32(trow + c * 32, raw[c]);
+      for (int i = 0; i < 16; ++i) {
+        pk[i] = pack_half2(__uint_as_float(o[2 * i]), __uint_as_float(o[2 * i + 1]));
+        amax2 = __hmax2(amax2, __habs2(*reinterpret_cast<const __half2*>(&pk[i])));
+      }
+      if (ctx != nullptr && r < S) {
+        uint4* dst = reinterpret_cast<uint4*>(ctx + grow * ldc + h * kD + half * 32);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) dst[c] = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+      }
+      if (!fuse_q) return;
+      tmem_st16(trow + kTmemCtx + hl * 32 + half * 16, pk);
+      if (!last) return;
+      // Q8row of the whole ctx row (R6-R8): amax over both halves, then
+      // quantize the parked fp16 values
+      tmem_wait_st();
+      redAmax[half * kQ + r] = fmaxf(__low2float(amax2), __high2float(amax2));
+      pair_sync();
+      const float am = fmaxf(redAmax[r], redAmax[kQ + r]);
+      amax2 = __float2half2_rn(0.0f);
+      const float sc = q8_scale(am);
+      const float rs = __frcp_rn(sc);
+      const int hbase = h - hl;
+      // Stage the s8 rows in the P buffer O(m) just finished reading (free
+      // until softmax(m+2)), 4 heads (128 x 256 B) per pass, 16-byte chunk cc
+      // of row r at [cc / 8][r][(cc % 8) ^ (r % 8)]; then store whole rows
+      // coalesced (one half-warp per 256-byte row segment).
+      uint8_t* stage = smem + SmemTC::P + (m & 1) * 2 * kTileBytes;
+      const int sw = (warp - 2);
+      for (int j0 = 0; j0 < nh; j0 += 4) {
+        const int nj = min(4, nh - j0);
+#pragma unroll 1
+        for (int jj = 0; jj < nj; ++jj) {
+          uint32_t v[1][16];
+          tmem_ld16(trow + kTmemCtx + (j0 + jj) * 32 + half * 16, v[0]);
+          tmem_wait_ld();
+          uint32_t w[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float2 a0 = __half22float2(*reinterpret_cast<const __half2*>(&v[0][2 * i]));
+            const float2 a1 = __half22float2(*reinterpret_cast<const __half2*>(&v[0][2 * i + 1]));
+            w[i] = q8_quant4(a0, a1, sc, rs);
+          }
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int cc = jj * 4 + half * 2 + k;
+            *reinterpret_cast<uint4*>(stage + (cc >> 3) * kTileBytes + r * 128 + (((cc & 7) ^ (r & 7)) << 4)) =
+                make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+          }
+        }
+        softmax_sync();
+        const int cc = lane & 15;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int row = sw * 16 + i * 2 + (lane >> 4);
+          if (cc < nj * 4 && row < S) {
+            const uint4 val =
+                *reinterpret_cast<const uint4*>(stage + (cc >> 3) * kTileBytes + row * 128 + (((cc & 7) ^ (row & 7)) << 4));
+            *reinterpret_cast<uint4*>(ctxq + ((size_t)b * S + row) * ldq + (hbase + j0) * kD + cc * 16) = val;
+          }
+        }
+        softmax_sync();
+      }
+      if (half == 0 && r < S) ctxs[grow] = sc;
+      if (threadIdx.x == 64) trace_ev(trace, m, 7);
+    };
+
+    uint32_t n = 0;
+    bool pend = false;  // epilogue of head n-1 outstanding
+    int pb = 0, ph_ = 0, phl = 0, pnh = 0;
+    bool plast = false;
+    // key mask of an item's sequence (keys >= S masked), fetched one item ahead
+    auto mask_of = [&](int item) -> int {
+      if (item >= n_items || tid >= S) return 0;
+      return __ldg(mask + (size_t)(item / n_groups) * S + tid);
+    };
+    int mval = mask_of(blockIdx.x);
+    for (HeadIter it(blockIdx.x, n_items, n_groups, A, gridDim.x); it.valid(); it.next(), ++n) {
+      if (it.hl == 0) {
+        // every softmax thread finished reading the previous item's mask
+        // before this barrier
+        softmax_sync();
+        if (tid < kKeys) sMask[tid] = mval != 0 ? 0.0f : -INFINITY;
+        softmax_sync();
+        mval = mask_of(it.item + it.stride);
+      }
+      mbar_wait(s_full, n & 1);
+      if (threadIdx.x == 64) trace_ev(trace, n, 3);
+      tc_fence_after();
+      uint32_t raw[2][32];
+      tmem_ld32(trow + half * 64, raw[0]);
+      tmem_ld32(trow + half * 64 + 32, raw[1]);
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(s_empty);
-      float s[kKeys];
-      float mx = -INFINITY;
+      // masked raw scores (mask bias 0 / -inf), row max in raw units, then
+      // p = exp2(log2(e)/sqrt(d) * (s - max)) as one FFMA per element; packed
+      // fp32 pairs throughout
+      float2 s2[32];
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      const float4* mk4 = reinterpret_cast<const float4*>(sMask) + half * 16;
 #pragma unroll
-      for (int j = 0; j < kKeys; ++j) {
-        s[j] = __fmul_rn(__uint_as_float(raw[j >> 5][j & 31]), scale) + sMask[j];
-        mx = fmaxf(mx, s[j]);
+      for (int j = 0; j < 64; j += 4) {
+        const float4 mk = mk4[j >> 2];
+        const uint32_t* rw = &raw[j >> 5][j & 31];
+        s2[j / 2] = add2(make_float2(__uint_as_float(rw[0]), __uint_as_float(rw[1])), make_float2(mk.x, mk.y));
+        s2[j / 2 + 1] = add2(make_float2(__uint_as_float(rw[2]), __uint_as_float(rw[3])), make_float2(mk.z, mk.w));
+        m4[0] = fmaxf(m4[0], s2[j / 2].x);
+        m4[1] = fmaxf(m4[1], s2[j / 2].y);
+        m4[2] = fmaxf(m4[2], s2[j / 2 + 1].x);
+        m4[3] = fmaxf(m4[3], s2[j / 2 + 1].y);
       }
-      float l = 0.0f;
+      float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+      redMax[half * kQ + r] = mx;
+      pair_sync();
+      mx = fmaxf(mx, redMax[(half ^ 1) * kQ + r]);
+      const float nmx = -__fmul_rn(mx, sl2);
+      const float2 sl2v = make_float2(sl2, sl2), nmxv = make_float2(nmx, nmx);
+      float2 l2a = make_float2(0.0f, 0.0f), l2b = make_float2(0.0f, 0.0f);
 #pragma unroll
-      for (int j = 0; j < kKeys; ++j) {
-        s[j] = ex2f((s[j] - mx) * kLog2e);
-        l += s[j];
+      for (int j = 0; j < 32; ++j) {
+        const float2 e = fma2(s2[j], sl2v, nmxv);
+        s2[j] = make_float2(ex2f(e.x), ex2f(e.y));
+        if (j & 1) l2b = add2(l2b, s2[j]); else l2a = add2(l2a, s2[j]);
       }
+      const float2 l2 = add2(l2a, l2b);
+      float l = l2.x + l2.y;
+      redSum[half * kQ + r] = l;
+      pair_sync();
+      l = redSum[r] + redSum[kQ + r];  // fixed order in both halves
       const float inv = __frcp_rn(l);
-      // P16 = R16(p) into the K-major 128B-swizzled tile: k-block kb holds keys
-      // [64kb, 64kb+64) of row r; 16B chunk c at (c ^ (r & 7)).
-      uint8_t* prow = smem + SmemTC::P + r * 128;
+      const float2 inv2 = make_float2(inv, inv);
+      // P16 = R16(p) into k-block `half` of the K-major 128B-swizzled tile
+      // P[n&1]: 16B chunk c of row r at (c ^ (r & 7)).  P[n&1] was last read
+      // by O(n-2), complete since epilogue(n-2) passed o_full.
+      uint8_t* prow = smem + SmemTC::P + (n & 1) * 2 * kTileBytes + half * kTileBytes + r * 128;
 #pragma unroll
-      for (int kb = 0; kb < 2; ++kb)
+      for (int c = 0; c < 8; ++c) {
+        uint32_t w[4];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const int j = kb * 64 + c * 8;
-          uint4 v;
-          v.x = pack_half2(s[j] * inv, s[j + 1] * inv);
-          v.y = pack_half2(s[j + 2] * inv, s[j + 3] * inv);
-          v.z = pack_half2(s[j + 4] * inv, s[j + 5] * inv);
-          v.w = pack_half2(s[j + 6] * inv, s[j + 7] * inv);
-          *reinterpret_cast<uint4*>(prow + kb * kTileBytes + ((c ^ (r & 7)) << 4)) = v;
+        for (int i = 0; i < 4; ++i) {
+          const float2 pn = mul2(s2[c * 4 + i], inv2);
+          w[i] = pack_half2(pn.x, pn.y);
         }
-      fence_async_smem();
-      mbar_arrive(p_full);
-      // epilogue: ctx row = R16(O row)
-      mbar_wait(o_full, ph);
-      tc_fence_after();
-      uint32_t o[64];
-      tmem_ld32(trow + 128, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
-      tmem_ld32(trow + 160, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
-      tmem_wait_ld();  // (o[] is a plain register array: both loads land before use)
-      tc_fence_before();
-      mbar_arrive(o_empty);
-      if (r < S) {
-        __half* dst = ctx + ((size_t)b * S + r) * ldc + h * kD;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          uint4 v;
-          v.x = pack_half2(__uint_as_float(o[c * 8 + 0]), __uint_as_float(o[c * 8 + 1]));
-          v.y = pack_half2(__uint_as_float(o[c * 8 + 2]), __uint_as_float(o[c * 8 + 3]));
-          v.z = pack_half2(__uint_as_float(o[c * 8 + 4]), __uint_as_float(o[c * 8 + 5]));
-          v.w = pack_half2(__uint_as_float(o[c * 8 + 6]), __uint_as_float(o[c * 8 + 7]));
-          *reinterpret_cast<uint4*>(dst + c * 8) = v;
-        }
+        *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
+      fence_async_smem();
+      mbar_arrive(p_full + (n & 1));
+      if (threadIdx.x == 64) trace_ev(trace, n, 4);
+      if (pend) epilogue(n - 1, pb, ph_, phl, plast, pnh);
+      pend = true;
+      pb = it.b;
+      ph_ = it.h0 + it.hl;
+      phl = it.hl;
+      pnh = it.nh;
+      plast = it.hl == it.nh - 1;
     }
+    if (pend) epilogue(n - 1, pb, ph_, phl, plast, pnh);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, 256);
+    tmem_dealloc(tmem, 512);
   }
 }
 
@@ -229,22 +435,28 @@ bool attention_tc_supported(int S, int d, int ldqkv, int ldctx) {
   return d == kD && S >= 1 && S <= kKeys && (ldqkv % 8) == 0 && (ldctx % 8) == 0;
 }
 
-bool plan_attention_tc(CUtensorMap* map, const void* qkv, int M_rows, int ldqkv, const char** err) {
+bool attention_tc_fuses_quant(int A) { return A >= 1 && A <= kMaxHeads; }
+
+bool plan_attention_tc(AttnTCPlan* plan, const void* qkv, int M_rows, int ldqkv, const char** err) {
   // [M_rows x ldqkv] fp16, 64-column x 128-row boxes, 128B swizzle
-  return make_operand_map(map, qkv, M_rows, ldqkv, 2, (size_t)ldqkv * 2, 128, err);
+  plan->qkv = qkv;
+  plan->ldqkv = ldqkv;
+  return make_operand_map(&plan->map, qkv, M_rows, ldqkv, 2, (size_t)ldqkv * 2, 128, err);
 }
 
 cudaError_t prepare_attention_tc_kernel() {
   return cudaFuncSetAttribute(attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemTC::TOTAL);
 }
 
-cudaError_t launch_attention_tc(const CUtensorMap& map, const int32_t* mask, int B, int S, int A, __half* ctx,
-                                int ldctx, cudaStream_t s) {
-  const int n_items = B * A;
-  const int grid = n_items < 2 * kNumSMs ? n_items : 2 * kNumSMs;
+cudaError_t launch_attention_tc(const AttnTCPlan& plan, const int32_t* mask, int B, int S, int A, __half* ctx,
+                                int ldctx, int8_t* ctxq, int ldq, float* ctxs, cudaStream_t s,
+                                unsigned long long* trace) {
+  if (ctxq != nullptr && !attention_tc_fuses_quant(A)) return cudaErrorInvalidValue;
+  const int n_items = B * ((A + kMaxHeads - 1) / kMaxHeads);
+  const int grid = n_items < kNumSMs ? n_items : kNumSMs;
   const float scale = (float)(1.0 / sqrt((double)kD));
-  launch_ex(attention_tc_kernel, dim3(grid), dim3(kThreadsTC), SmemTC::TOTAL, s, 0, map, mask, B, S, A, scale, ctx,
-            ldctx);
+  launch_ex(attention_tc_kernel, dim3(grid), dim3(kThreadsTC), SmemTC::TOTAL, s, 0, plan.map, mask, B, S, A, scale,
+            ctx, ldctx, ctxq, ldq, ctxs, static_cast<const uint8_t*>(plan.qkv), plan.ldqkv * 2, trace);
   return cudaGetLastError();
 }
 

@@ -94,7 +94,7 @@ struct ff_model {
   int pair_mode = -1;  // FF_OPT_CTA_PAIRS: -1 auto, 0 never (GemmPlan::force_pair)
   bool attn_tc = true;  // FF_OPT_ATTN_TC: tcgen05 attention where supported
   bool fused = false;   // FF_OPT_FUSED_EPILOGUES: cluster row-reduction GEMM epilogues (opt-in)
-  CUtensorMap tm_qkv;   // QKV buffer map for the tcgen05 attention
+  ff::AttnTCPlan tm_qkv;  // QKV buffer map for the tcgen05 attention
   std::map<std::tuple<int, int, const void*, const void*, const void*>, cudaGraphExec_t> graphs;
 
   template <typename T>
@@ -297,6 +297,12 @@ ff_status dump(void* dst, const void* src, int ld_elems, int cols, int M, cudaSt
   return FF_OK;
 }
 
+// int8 layer whose ctx requant (a4) runs inside the tcgen05 attention kernel.
+bool attention_fuses_quant(const ff_model* m, const LayerPlan& P, int S) {
+  return P.dt == FF_I8 && m->attn_tc && ff::attention_tc_supported(S, m->cfg.head_dim, m->ldqkv, m->ldc16) &&
+         ff::attention_tc_fuses_quant(P.A);
+}
+
 // The launch sequence of one encoder forward.
 ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int B, int S, float* logits,
                       cudaStream_t s, int trace_layer, void* const* d_dump, Prof* prof = nullptr) {
@@ -340,15 +346,20 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     FF_LAUNCH(q ? FF_K_GEMM_I8 : FF_K_GEMM_F16, ff::launch_gemm(g, s), "gemm qkv");
     if (tr && dump(d_dump[1], QKV, m->ldqkv, 3 * P.D, M, s) != FF_OK) return FF_E_CUDA;
     // a3: fused masked-softmax attention over this layer's A'_l heads
+    // (int8 layers: a4, the ctx requant, fused into the tcgen05 attention)
+    const bool att_q = attention_fuses_quant(m, P, S);
     if (m->attn_tc && ff::attention_tc_supported(S, c.head_dim, m->ldqkv, m->ldc16))
-      FF_LAUNCH(FF_K_ATTENTION, ff::launch_attention_tc(m->tm_qkv, mask, B, S, P.A, CTX, m->ldc16, s),
+      FF_LAUNCH(FF_K_ATTENTION,
+                ff::launch_attention_tc(m->tm_qkv, mask, B, S, P.A, (att_q && !tr) ? nullptr : CTX, m->ldc16,
+                                        att_q ? CTXq : nullptr, m->ldc8, att_q ? CTXs : nullptr, s),
                 "attention_tc");
     else
       FF_LAUNCH(FF_K_ATTENTION, ff::launch_attention(QKV, m->ldqkv, mask, B, S, P.A, c.head_dim, CTX, m->ldc16, s),
                 "attention");
     if (tr && dump(d_dump[2], CTX, m->ldc16, P.D, M, s) != FF_OK) return FF_E_CUDA;
     // a4 + a5: requant (int8 layers) and out-projection
-    if (q) FF_LAUNCH(FF_K_QUANT, ff::launch_quant_rows(CTX, m->ldc16, M, P.D, CTXq, m->ldc8, CTXs, s), "quant ctx");
+    if (q && !att_q)
+      FF_LAUNCH(FF_K_QUANT, ff::launch_quant_rows(CTX, m->ldc16, M, P.D, CTXq, m->ldc8, CTXs, s), "quant ctx");
     const bool fuse_ln = m->fused && P.rr_ok[0];
     const bool fuse_q = m->fused && q && P.rr_ok[1];
     if (fuse_ln) {
@@ -800,13 +811,12 @@ void ff_model_destroy(ff_model* m) {
 ff_status ff_launch_count(const ff_model* m, int32_t batch, int32_t seq, int32_t* count) {
   if (!m || !count) return fail(FF_E_INVALID, "null argument");
   (void)batch;
-  (void)seq;
   int n = 3;  // embed_ln + pooler + classifier
   for (const LayerPlan& P : m->L) {
     const bool q = P.dt == FF_I8;
     const bool fln = m->fused && P.rr_ok[0], fq = m->fused && P.rr_ok[1];
     n += 2;                              // QKV GEMM + attention
-    n += q ? 1 : 0;                      // ctx requant
+    n += (q && !attention_fuses_quant(m, P, seq)) ? 1 : 0;  // ctx requant
     n += fln ? 1 : 2;                    // out-proj (+ add_ln1)
     n += fq ? 1 : (q ? 2 : 1);           // FFN1 (+ requant)
     n += fln ? 1 : 2;                    // FFN2 (+ add_ln2)
@@ -903,16 +913,38 @@ ff_status ff_debug_attention(const void* d_qkv16, const int32_t* d_mask, int32_t
                   (reinterpret_cast<uintptr_t>(d_qkv16) & 15) == 0;
   if (mode == 2 && !tc) return fail(FF_E_UNSUPPORTED, "tcgen05 attention needs head_dim 64, S <= 128");
   if (tc) {
-    CUtensorMap map;
+    ff::AttnTCPlan map;
     const char* err = nullptr;
     if (!ff::plan_attention_tc(&map, d_qkv16, B * S, 3 * A * d, &err))
       return fail(FF_E_INVALID, std::string("attention tensor map: ") + err);
-    FF_CK(ff::launch_attention_tc(map, d_mask, B, S, A, static_cast<__half*>(d_ctx16), A * d,
+    FF_CK(ff::launch_attention_tc(map, d_mask, B, S, A, static_cast<__half*>(d_ctx16), A * d, nullptr, 0, nullptr,
                                   static_cast<cudaStream_t>(stream)));
     return FF_OK;
   }
   FF_CK(ff::launch_attention(static_cast<const __half*>(d_qkv16), 3 * A * d, d_mask, B, S, A, d,
                              static_cast<__half*>(d_ctx16), A * d, static_cast<cudaStream_t>(stream)));
+  return FF_OK;
+}
+
+ff_status ff_debug_attention_q8(const void* d_qkv16, const int32_t* d_mask, int32_t B, int32_t S, int32_t A,
+                                int32_t d, void* d_ctx16, int8_t* d_ctxq, float* d_ctxs, uint64_t* d_trace,
+                                void* stream) {
+  if (B < 1 || S < 1 || A < 1 || !d_ctxq || !d_ctxs) return fail(FF_E_INVALID, "bad attention args");
+  if (!ff::attention_tc_supported(S, d, 3 * A * d, A * d) || !ff::attention_tc_fuses_quant(A) ||
+      (reinterpret_cast<uintptr_t>(d_qkv16) & 15) != 0 || (A * d) % 16 != 0)
+    return fail(FF_E_UNSUPPORTED, "fused attention + requant needs head_dim 64, S <= 128, A <= 8");
+  static bool prepared = false;
+  if (!prepared) {
+    FF_CK(ff::prepare_attention_tc_kernel());
+    prepared = true;
+  }
+  ff::AttnTCPlan map;
+  const char* err = nullptr;
+  if (!ff::plan_attention_tc(&map, d_qkv16, B * S, 3 * A * d, &err))
+    return fail(FF_E_INVALID, std::string("attention tensor map: ") + err);
+  FF_CK(ff::launch_attention_tc(map, d_mask, B, S, A, static_cast<__half*>(d_ctx16), A * d, d_ctxq, A * d, d_ctxs,
+                                static_cast<cudaStream_t>(stream),
+                                reinterpret_cast<unsigned long long*>(d_trace)));
   return FF_OK;
 }
 

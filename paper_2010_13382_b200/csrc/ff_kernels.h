@@ -145,11 +145,20 @@ cudaError_t launch_attention(const __half* qkv, int ldqkv, const int32_t* mask, 
                              __half* ctx, int ldctx, cudaStream_t s);
 
 // tcgen05 attention (head_dim 64, S <= 128); the tensor map covers the QKV
-// buffer [M_rows x ldqkv] fp16 with 64-column x 128-row boxes.
+// buffer [M_rows x ldqkv] fp16 with 64-column x 128-row boxes.  Writes the
+// fp16 ctx rows when ctx != null and, when ctxq != null (requires
+// attention_tc_fuses_quant(A)), the Q8row s8 ctx rows + per-row scales.
 bool attention_tc_supported(int S, int d, int ldqkv, int ldctx);
-bool plan_attention_tc(CUtensorMap* map, const void* qkv, int M_rows, int ldqkv, const char** err);
-cudaError_t launch_attention_tc(const CUtensorMap& map, const int32_t* mask, int B, int S, int A, __half* ctx,
-                                int ldctx, cudaStream_t s);
+bool attention_tc_fuses_quant(int A);
+struct AttnTCPlan {
+  CUtensorMap map;
+  const void* qkv;  // QKV rows (contiguous: ldqkv fp16 per row)
+  int ldqkv;
+};
+bool plan_attention_tc(AttnTCPlan* plan, const void* qkv, int M_rows, int ldqkv, const char** err);
+cudaError_t launch_attention_tc(const AttnTCPlan& plan, const int32_t* mask, int B, int S, int A, __half* ctx,
+                                int ldctx, int8_t* ctxq, int ldq, float* ctxs, cudaStream_t s,
+                                unsigned long long* trace = nullptr);
 cudaError_t prepare_attention_tc_kernel();
 
 // ------------------------------------------------------- weight packing

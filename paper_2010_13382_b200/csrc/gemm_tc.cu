@@ -26,6 +26,7 @@
 #include <cstdio>
 #include "ff_kernels.h"
 #include "ptx.cuh"
+#include "quant.cuh"
 
 namespace ff {
 
@@ -101,24 +102,52 @@ __device__ __forceinline__ float act_fn(float y) {
   return y;
 }
 
+// GELU of a pair on packed fp32 (FFMA2 / FMUL2): same erf_fast polynomial,
+// g = h + h * erf(y / sqrt 2) with h = y / 2.
+__device__ __forceinline__ float2 gelu2(float2 y) {
+  const float2 u = mul2(y, make_float2(0.70710678118654752f, 0.70710678118654752f));
+  const float2 t = make_float2(fminf(fabsf(u.x), 4.0f), fminf(fabsf(u.y), 4.0f));
+  float2 p = make_float2(4.5357247e-05f, 4.5357247e-05f);
+  p = fma2(p, t, make_float2(-0.000445495f, -0.000445495f));
+  p = fma2(p, t, make_float2(0.0014893987f, 0.0014893987f));
+  p = fma2(p, t, make_float2(0.0007746952f, 0.0007746952f));
+  p = fma2(p, t, make_float2(-0.028253723f, -0.028253723f));
+  p = fma2(p, t, make_float2(0.14848162f, 0.14848162f));
+  p = fma2(p, t, make_float2(0.9184164f, 0.9184164f));
+  p = fma2(p, t, make_float2(1.6279086f, 1.6279086f));
+  const float2 a = mul2(t, p);
+  float2 e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(-a.x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(-a.y));
+  const float2 er = sub2(make_float2(1.0f, 1.0f), e);
+  const float2 erf = make_float2(copysignf(er.x, u.x), copysignf(er.y, u.y));
+  const float2 h = mul2(y, make_float2(0.5f, 0.5f));
+  return fma2(h, erf, h);
+}
+
 // W columns [n0, n0+W) of this thread's row: dequant / bias / activation,
-// RNE to fp16, packed as W/2 half2 words.
+// RNE to fp16, packed as W/2 half2 words (pairs on packed fp32 arithmetic).
 template <bool I8, int ACT, int W>
 __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[W], const float (&bias)[W], const float (&sw)[W],
                                           float sx, uint32_t (&h)[W / 2]) {
 #pragma unroll
   for (int e = 0; e < W / 2; ++e) {
-    float v[2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int j = e * 2 + u;
-      if (I8)
-        v[u] = __fmaf_rn(__int2float_rn(static_cast<int>(r[j])), __fmul_rn(sx, sw[j]), bias[j]);
-      else
-        v[u] = __fadd_rn(__uint_as_float(r[j]), bias[j]);
-      v[u] = act_fn<ACT>(v[u]);
+    const int j = 2 * e;
+    const float2 b = make_float2(bias[j], bias[j + 1]);
+    float2 v;
+    if (I8) {
+      const float2 a = make_float2(__int2float_rn(static_cast<int>(r[j])), __int2float_rn(static_cast<int>(r[j + 1])));
+      v = fma2(a, mul2(make_float2(sx, sx), make_float2(sw[j], sw[j + 1])), b);
+    } else {
+      v = add2(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), b);
     }
-    h[e] = pack_half2(v[0], v[1]);
+    if (ACT == ACT_GELU) {
+      v = gelu2(v);
+    } else if (ACT != ACT_NONE) {
+      v.x = act_fn<ACT>(v.x);
+      v.y = act_fn<ACT>(v.y);
+    }
+    h[e] = pack_half2(v.x, v.y);
   }
 }
 
@@ -144,14 +173,6 @@ __device__ __forceinline__ void loadN(float (&dst)[W], const float* src, int n0,
 __device__ __forceinline__ void load32(float (&dst)[32], const float* src, int n0, int N) { loadN<32>(dst, src, n0, N); }
 
 // tcgen05.ld of 16 columns (32x32b.x16): thread t gets row (lane base + t).
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-}
 
 template <int BN, bool I8, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -161,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int STAGES = Cfg::STAGES;
   constexpr int TM = Cfg::TM;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
   uint8_t* sEpi = smem + Cfg::EPI_OFF;
@@ -413,20 +434,6 @@ struct RRCfg {
   static_assert(SMEM <= 227 * 1024, "smem budget");
 };
 
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
-      : "memory");
-}
-
-__device__ __forceinline__ int8_t quant1_dev(float x, float s) {
-  float v = rintf(__fdiv_rn(x, s));  // RNE (R8), IEEE division (R6)
-  v = fminf(fmaxf(v, -127.0f), 127.0f);
-  return static_cast<int8_t>(static_cast<int>(v));
-}
 
 template <bool I8>
 __device__ __forceinline__ float dequant1(uint32_t r, float sx, float sw, float b) {
@@ -440,7 +447,7 @@ __global__ void __launch_bounds__(kRRThreads, 1)
   constexpr int STAGES = kRRStages;
   constexpr int BN = kRRBN;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * RRCfg::A_BYTES;
   uint8_t* sEpi = smem + RRCfg::EPI_OFF;
@@ -733,7 +740,7 @@ __global__ void __launch_bounds__(kRRThreads, 1)
       if (p.outq) {
         // Q8row over the whole row (R6-R8, R12): quantize the fp16-rounded values
         const float rmax = reduce_max(amax);
-        const float sc = rmax == 0.0f ? 1.0f : __fdiv_rn(rmax, 127.0f);
+        const float sc = q8_scale(rmax);
 #pragma unroll 1
         for (int c = c_lo; c < c_lo + BN / 2; c += 32) {
           uint32_t h[16];
@@ -743,8 +750,8 @@ __global__ void __launch_bounds__(kRRThreads, 1)
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
             const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h[e]));
-            o[2 * e] = quant1_dev(f.x, sc);
-            o[2 * e + 1] = quant1_dev(f.y, sc);
+            o[2 * e] = q8_quant1(f.x, sc);
+            o[2 * e + 1] = q8_quant1(f.y, sc);
           }
           if (row_ok) {
             uint4* dst = reinterpret_cast<uint4*>(p.outq + (size_t)row * p.ldq + ncol0 + c);

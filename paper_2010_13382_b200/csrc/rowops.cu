@@ -17,6 +17,7 @@
 // No fast-math anywhere in this file.
 #include "ff_kernels.h"
 #include "ptx.cuh"
+#include "quant.cuh"
 
 namespace ff {
 
@@ -33,21 +34,12 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
-__device__ __forceinline__ int8_t quant1(float x, float s) {
-  float v = rintf(__fdiv_rn(x, s));  // rintf = round-half-to-even
-  v = fminf(fmaxf(v, -127.0f), 127.0f);
-  return static_cast<int8_t>(static_cast<int>(v));
-}
-
-// Same result as quant1 (RNE of the correctly rounded quotient x/s), cheaper:
-// t = x * rcp(s) lies within 2 ulp of fl(x/s), so RNE(t) == RNE(fl(x/s))
-// unless t is within a few ulp of a half-integer; only then (rarely) divide.
-__device__ __forceinline__ int8_t quant1_fast(float x, float s, float rs) {
-  const float t = x * rs;
-  float v = rintf(t);
-  if (0.5f - fabsf(t - v) <= fabsf(t) * 4.76837158203125e-07f + 1e-30f) v = rintf(__fdiv_rn(x, s));
-  v = fminf(fmaxf(v, -127.0f), 127.0f);
-  return static_cast<int8_t>(static_cast<int>(v));
+// Q8row of 8 fp16-rounded values (R6-R8), packed s8x8.
+__device__ __forceinline__ uint2 quant8(const float (&f)[8], float sc, float rs) {
+  uint2 o;
+  o.x = q8_quant4(make_float2(f[0], f[1]), make_float2(f[2], f[3]), sc, rs);
+  o.y = q8_quant4(make_float2(f[4], f[5]), make_float2(f[6], f[7]), sc, rs);
+  return o;
 }
 
 __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
@@ -112,16 +104,13 @@ __device__ __forceinline__ void ln_store(float (&v)[NCH][8], int H, int lane, co
   }
   if (yq == nullptr) return;
   amax = warp_max(amax);
-  const float sc = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 127.0f);
+  const float sc = q8_scale(amax);
   const float rs = __frcp_rn(sc);
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
     const int col = 8 * (lane + 32 * c);
     if (col < H) {
-      int8_t o[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = quant1_fast(v[c][j], sc, rs);
-      *reinterpret_cast<uint2*>(yq + col) = *reinterpret_cast<const uint2*>(o);
+      *reinterpret_cast<uint2*>(yq + col) = quant8(v[c], sc, rs);
     }
   }
   if (lane == 0) *ys = sc;
@@ -244,7 +233,7 @@ __global__ void __launch_bounds__(256) quant_rows_kernel(const __half* __restric
     }
   }
   amax = warp_max(amax);
-  const float sc = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 127.0f);
+  const float sc = q8_scale(amax);
   const float rs = __frcp_rn(sc);
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
@@ -252,10 +241,7 @@ __global__ void __launch_bounds__(256) quant_rows_kernel(const __half* __restric
     if (col < K) {
       float f[8];
       unpack8(u[c], f);
-      int8_t o[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = quant1_fast(f[j], sc, rs);
-      *reinterpret_cast<uint2*>(qr + col) = *reinterpret_cast<const uint2*>(o);
+      *reinterpret_cast<uint2*>(qr + col) = quant8(f, sc, rs);
     }
   }
   if (lane == 0) scale[row] = sc;
@@ -285,8 +271,8 @@ __global__ void __launch_bounds__(256) quant_rows_scalar_kernel(const __half* __
   float amax = 0.0f;
   for (int c = lane; c < K; c += 32) amax = fmaxf(amax, fabsf(__half2float(xr[c])));
   amax = warp_max(amax);
-  const float sc = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 127.0f);
-  for (int c = lane; c < K; c += 32) q[(size_t)row * ldq + c] = quant1(__half2float(xr[c]), sc);
+  const float sc = q8_scale(amax);
+  for (int c = lane; c < K; c += 32) q[(size_t)row * ldq + c] = q8_quant1(__half2float(xr[c]), sc);
   if (lane == 0) scale[row] = sc;
 }
 
@@ -362,8 +348,8 @@ __global__ void __launch_bounds__(256) quant_weight_kernel(const float* __restri
   float amax = 0.0f;
   for (int k = lane; k < K; k += 32) amax = fmaxf(amax, fabsf(w[k]));
   amax = warp_max(amax);
-  const float sc = amax == 0.0f ? 1.0f : __fdiv_rn(amax, 127.0f);
-  for (int k = lane; k < K; k += 32) dst[(size_t)n * ldd + k] = quant1(w[k], sc);
+  const float sc = q8_scale(amax);
+  for (int k = lane; k < K; k += 32) dst[(size_t)n * ldd + k] = q8_quant1(w[k], sc);
   if (lane == 0) scale[n] = sc;
 }
 

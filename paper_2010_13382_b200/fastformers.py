@@ -30,7 +30,7 @@ STATUS_NAMES = ["FF_OK", "FF_E_INVALID", "FF_E_SHAPE", "FF_E_STATE", "FF_E_CUDA"
 EXPORTED = ["ff_abi_version", "ff_last_error", "ff_model_create", "ff_model_memory", "ff_bind_memory",
             "ff_load_weights", "ff_finalize", "ff_encode", "ff_encode_host", "ff_check", "ff_set_option",
             "ff_model_destroy", "ff_launch_count", "ff_profile", "ff_encode_trace", "ff_debug_gemm", "ff_debug_quant_rows",
-            "ff_debug_attention"]
+            "ff_debug_attention", "ff_debug_attention_q8"]
 
 
 class FFError(RuntimeError):
@@ -77,6 +77,7 @@ def lib():
         L.ff_debug_gemm.argtypes = [i32, vp, i32, vp, i32, i32, i32, i32, i32, vp, i32, vp, vp, vp, i32, vp]
         L.ff_debug_quant_rows.argtypes = [vp, i32, i32, i32, vp, i32, vp, vp]
         L.ff_debug_attention.argtypes = [vp, vp, i32, i32, i32, i32, vp, i32, vp]
+        L.ff_debug_attention_q8.argtypes = [vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp]
         for name in EXPORTED:
             if name not in ("ff_abi_version", "ff_last_error", "ff_model_destroy"):
                 getattr(L, name).restype = i32
@@ -244,3 +245,18 @@ def attention(qkv16, mask, A, d, impl=0):
     ctx = torch.empty((B * S, A * d), dtype=torch.float16, device=qkv16.device)
     check(lib().ff_debug_attention(_ptr(qkv16), _ptr(mask), B, S, A, d, _ptr(ctx), impl, _stream_ptr()))
     return ctx
+
+
+def attention_q8(qkv16, mask, A, d, with_ctx16=True, trace=None):
+    """tcgen05 attention with the int8 ctx requant fused: (ctx16 or None, q s8, scales).
+    trace: optional int64 CUDA tensor [min(B,148), 32, 8] for event timestamps."""
+    import torch
+    B, S = mask.shape
+    dev = qkv16.device
+    ctx = torch.empty((B * S, A * d), dtype=torch.float16, device=dev) if with_ctx16 else None
+    q = torch.empty((B * S, A * d), dtype=torch.int8, device=dev)
+    s = torch.empty(B * S, dtype=torch.float32, device=dev)
+    check(lib().ff_debug_attention_q8(_ptr(qkv16), _ptr(mask), B, S, A, d, _ptr(ctx) if ctx is not None else None,
+                                      _ptr(q), _ptr(s), _ptr(trace) if trace is not None else None,
+                                      _stream_ptr()))
+    return ctx, q, s

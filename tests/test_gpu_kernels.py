@@ -95,6 +95,9 @@ def test_quant_rows_bit_exact_vs_oracle():
         x[0] = 0
         x[1, :4] = np.float16([127.0, 62.5, 63.5, -62.5])
         x[1, 4:] = 0
+        # ties of x/s with s = 3 (x * rcp(s) lands one ulp off the tie)
+        x[2, :6] = np.float16([381.0, 10.5, 4.5, 13.5, -10.5, 7.5])
+        x[2, 6:] = np.float16(rng.integers(-254, 254, K - 6) * 1.5)
         q, s = ffb.quant_rows(_pitched(x, torch.float16, 8))
         torch.cuda.synchronize()
         rq, rs = oracle.q8row(x.astype(np.float32))
@@ -127,7 +130,7 @@ def test_attention_matches_oracle(B, S, A, d, ragged):
 
 
 @pytest.mark.parametrize("B,S,A,ragged", [(2, 128, 8, False), (3, 128, 4, True), (2, 40, 3, True), (1, 7, 2, False),
-                                          (4, 32, 2, True), (1, 1, 1, False)])
+                                          (4, 32, 2, True), (1, 1, 1, False), (2, 64, 12, True), (3, 128, 16, False)])
 def test_attention_tcgen05_matches_oracle(B, S, A, ragged):
     """The tcgen05/TMEM attention kernel (head_dim 64, S <= 128)."""
     d = 64
@@ -149,3 +152,32 @@ def test_attention_tcgen05_matches_oracle(B, S, A, ragged):
     # and the same as the mma.sync kernel up to rounding
     ctx1 = ffb.attention(torch.from_numpy(qkv).cuda(), torch.from_numpy(mask).cuda(), A, d, impl=1).cpu().numpy()
     assert np.abs(ctx1.astype(np.float64) - got).max() <= 4e-3 + 4e-3 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("B,S,A,ragged", [(2, 128, 8, False), (3, 128, 4, True), (2, 40, 3, True), (1, 7, 2, False),
+                                          (1, 1, 1, False), (5, 128, 8, True), (150, 16, 2, True)])
+def test_attention_fused_requant(B, S, A, ragged):
+    """a3 + a4 fused (the int8-layer path): ctx within the attention bound of
+    the oracle, and the s8 rows / scales bit-exact Q8row of the kernel's own
+    fp16 ctx (DESIGN R6-R8, R12)."""
+    d = 64
+    rng = np.random.default_rng(300 + S + A + B)
+    qkv = np.float16(rng.standard_normal((B * S, 3 * A * d)) * 1.5)
+    mask = np.ones((B, S), np.int32)
+    if ragged:
+        for b in range(B):
+            mask[b, rng.integers(max(1, S // 4), S + 1):] = 0
+        mask[0, S // 2] = 0
+    mask[:, 0] = 1
+    qkv_d, mask_d = torch.from_numpy(qkv).cuda(), torch.from_numpy(mask).cuda()
+    ctx, q, sc = ffb.attention_q8(qkv_d, mask_d, A, d)
+    torch.cuda.synchronize()
+    got = ctx.cpu().numpy()
+    ref = oracle.attention(qkv.astype(np.float32), mask, A, d).astype(np.float64)
+    assert np.abs(got.astype(np.float64) - ref).max() <= 4e-3 + 4e-3 * np.abs(ref).max()
+    rq, rs = oracle.q8row(got.astype(np.float32))
+    np.testing.assert_array_equal(q.cpu().numpy(), rq)
+    np.testing.assert_array_equal(sc.cpu().numpy(), rs)
+    # without the fp16 copy: the same s8 rows
+    _, q2, s2 = ffb.attention_q8(qkv_d, mask_d, A, d, with_ctx16=False)
+    assert torch.equal(q2, q) and torch.equal(s2, sc)
