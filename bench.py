@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--seq", type=int, default=None)
     ap.add_argument("--no-variants", action="store_true", help="skip the fp16 side measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fused", type=int, default=None,
+                    help="1/0: force the fused GEMM+LayerNorm / GEMM+requant epilogues on/off (default: library default)")
     return ap.parse_args()
 
 
@@ -238,7 +240,8 @@ def run_ours(args):
     cfg = workload(args)
     B, S = cfg.batch, cfg.seq
     w = synth.make_weights(cfg)
-    enc = Encoder(cfg, w, max_tokens=B * S, device=local)
+    enc_kw = {} if args.fused is None else {"fused": bool(args.fused)}
+    enc = Encoder(cfg, w, max_tokens=B * S, device=local, **enc_kw)
     NB = 4
     batches = [synth.make_inputs(cfg, seed=1000 + rank * 10 ** 6 + k) for k in range(NB)]
     dids = [torch.from_numpy(i).cuda() for i, _ in batches]
@@ -329,7 +332,7 @@ def run_ours(args):
     variants = {}
     if not args.no_variants and world == 1:
         cfg16 = cfg.with_dtype(0)
-        enc16 = Encoder(cfg16, w, max_tokens=B * S, device=local)
+        enc16 = Encoder(cfg16, w, max_tokens=B * S, device=local, **enc_kw)
         for k in range(5):
             enc16.encode(dids[k % NB], dmask[k % NB], logits)
         torch.cuda.synchronize()

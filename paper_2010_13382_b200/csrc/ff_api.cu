@@ -193,7 +193,7 @@ void plan_memory(ff_model* m) {
   m->ws_ids = a.take(M * 4);
   m->ws_mask = a.take(M * 4);
   m->ws_logits = a.take(M * c.num_classes * 4);
-  m->ws_pooled = a.take(M * H * 4);  // pooler output [B <= max_tokens, H] fp32
+  m->ws_pooled = a.take(M * H * 4);  // pooler split-K partials [<= S][B][H] fp32
   m->wsbytes = align_up(a.off, 256);
 }
 

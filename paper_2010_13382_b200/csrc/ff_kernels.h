@@ -136,8 +136,9 @@ cudaError_t launch_add_ln(const __half* a, int lda, const __half* r, int ldr, in
 cudaError_t launch_quant_rows(const __half* x, int ldx, int M, int K, int8_t* q, int ldq, float* scale,
                               cudaStream_t s);
 // pooled = tanh(Wp x0 + bp); logits = Wc pooled + bc, x0 = row b*S of x16.
+// part: fp32 scratch of at least B x S x H floats (split-K partials).
 cudaError_t launch_head(const __half* x16, int ldx, int B, int S, int H, int C, const float* Wp, const float* bp,
-                        const float* Wc, const float* bc, float* pooled, float* logits, cudaStream_t s);
+                        const float* Wc, const float* bc, float* part, float* logits, cudaStream_t s);
 
 // ------------------------------------------------------------- attention
 size_t attention_smem_bytes(int S, int d);

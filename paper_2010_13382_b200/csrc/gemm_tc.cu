@@ -726,11 +726,10 @@ __global__ void __launch_bounds__(kRRThreads, 1)
             case ACT_GELU_TANH: epi_chunk<I8, ACT_GELU_TANH>(r, bias, sw, sx, h); break;
             default: epi_chunk<I8, ACT_NONE>(r, bias, sw, sx, h); break;
           }
+          __half2 am2 = __float2half2_rn(0.0f);
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h[e]));
-            amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
-          }
+          for (int e = 0; e < 16; ++e) am2 = __hmax2(am2, __habs2(*reinterpret_cast<const __half2*>(&h[e])));
+          amax = fmaxf(amax, fmaxf(__low2float(am2), __high2float(am2)));
           tmem_st16(tbase + c, h);
           if (p.store16) store16(h, n0, row0);
         }
@@ -741,22 +740,21 @@ __global__ void __launch_bounds__(kRRThreads, 1)
         // Q8row over the whole row (R6-R8, R12): quantize the fp16-rounded values
         const float rmax = reduce_max(amax);
         const float sc = q8_scale(rmax);
+        const float rs = __frcp_rn(sc);
 #pragma unroll 1
         for (int c = c_lo; c < c_lo + BN / 2; c += 32) {
           uint32_t h[16];
           tmem_ld16(tbase + c, h);
           tmem_wait_ld();
-          int8_t o[32];
+          uint32_t o[8];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h[e]));
-            o[2 * e] = q8_quant1(f.x, sc);
-            o[2 * e + 1] = q8_quant1(f.y, sc);
-          }
+          for (int e = 0; e < 8; ++e)
+            o[e] = q8_quant4(__half22float2(*reinterpret_cast<const __half2*>(&h[2 * e])),
+                             __half22float2(*reinterpret_cast<const __half2*>(&h[2 * e + 1])), sc, rs);
           if (row_ok) {
             uint4* dst = reinterpret_cast<uint4*>(p.outq + (size_t)row * p.ldq + ncol0 + c);
-            dst[0] = *reinterpret_cast<const uint4*>(&o[0]);
-            dst[1] = *reinterpret_cast<const uint4*>(&o[16]);
+            dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+            dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
           }
         }
         if (rank == 0 && hf == 0 && row_ok) p.out_scale[row] = sc;

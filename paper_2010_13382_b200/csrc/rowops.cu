@@ -53,31 +53,37 @@ __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
 }
 
 // LayerNorm of a row held as v[c][0..7] at columns 8*(lane + 32c) (< H), then
-// R16 store and optional Q8row.  All lanes of the warp participate.
+// R16 store and optional Q8row.  All lanes of the warp participate.  Packed
+// fp32 pair arithmetic (FADD2 / FFMA2 / FMUL2) throughout; two-pass mean /
+// variance.
 template <int NCH>
 __device__ __forceinline__ void ln_store(float (&v)[NCH][8], int H, int lane, const float* __restrict__ g,
                                          const float* __restrict__ b, float eps, __half* y16, int8_t* yq, float* ys) {
-  float s = 0.0f;
+  float2 s2 = make_float2(0.0f, 0.0f);
 #pragma unroll
   for (int c = 0; c < NCH; ++c)
     if (8 * (lane + 32 * c) < H) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) s += v[c][j];
+      for (int j = 0; j < 8; j += 2) s2 = add2(s2, make_float2(v[c][j], v[c][j + 1]));
     }
-  const float mean = __fdiv_rn(warp_sum(s), (float)H);
-  float q = 0.0f;
+  const float mean = __fdiv_rn(warp_sum(s2.x + s2.y), (float)H);
+  const float2 mean2 = make_float2(mean, mean);
+  float2 q2 = make_float2(0.0f, 0.0f);
 #pragma unroll
   for (int c = 0; c < NCH; ++c)
     if (8 * (lane + 32 * c) < H) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float dlt = v[c][j] - mean;
-        q = __fmaf_rn(dlt, dlt, q);
+      for (int j = 0; j < 8; j += 2) {
+        const float2 d = sub2(make_float2(v[c][j], v[c][j + 1]), mean2);
+        v[c][j] = d.x;  // v now holds the deviations
+        v[c][j + 1] = d.y;
+        q2 = fma2(d, d, q2);
       }
     }
-  const float var = __fdiv_rn(warp_sum(q), (float)H);
+  const float var = __fdiv_rn(warp_sum(q2.x + q2.y), (float)H);
   const float rstd = 1.0f / sqrtf(var + eps);
-  float amax = 0.0f;
+  const float2 rstd2 = make_float2(rstd, rstd);
+  __half2 amax2 = __float2half2_rn(0.0f);
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
     const int col = 8 * (lane + 32 * c);
@@ -86,24 +92,26 @@ __device__ __forceinline__ void ln_store(float (&v)[NCH][8], int H, int lane, co
       const float4 g1 = __ldg(reinterpret_cast<const float4*>(g + col + 4));
       const float4 b0 = __ldg(reinterpret_cast<const float4*>(b + col));
       const float4 b1 = __ldg(reinterpret_cast<const float4*>(b + col + 4));
-      const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      const float2 gv[4] = {make_float2(g0.x, g0.y), make_float2(g0.z, g0.w), make_float2(g1.x, g1.y),
+                            make_float2(g1.z, g1.w)};
+      const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                            make_float2(b1.z, b1.w)};
       uint32_t pk[4];
 #pragma unroll
-      for (int j = 0; j < 8; j += 2) {
-        const __half2 h = __floats2half2_rn((v[c][j] - mean) * rstd * gv[j] + bv[j],
-                                            (v[c][j + 1] - mean) * rstd * gv[j + 1] + bv[j + 1]);
+      for (int j = 0; j < 4; ++j) {
+        const float2 y = fma2(mul2(make_float2(v[c][2 * j], v[c][2 * j + 1]), rstd2), gv[j], bv[j]);
+        const __half2 h = __floats2half2_rn(y.x, y.y);
+        amax2 = __hmax2(amax2, __habs2(h));
         const float2 hf = __half22float2(h);  // keep the fp16-rounded values for Q8row
-        v[c][j] = hf.x;
-        v[c][j + 1] = hf.y;
-        amax = fmaxf(amax, fmaxf(fabsf(hf.x), fabsf(hf.y)));
-        pk[j / 2] = *reinterpret_cast<const uint32_t*>(&h);
+        v[c][2 * j] = hf.x;
+        v[c][2 * j + 1] = hf.y;
+        pk[j] = *reinterpret_cast<const uint32_t*>(&h);
       }
       *reinterpret_cast<uint4*>(y16 + col) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     }
   }
   if (yq == nullptr) return;
-  amax = warp_max(amax);
+  const float amax = warp_max(fmaxf(__low2float(amax2), __high2float(amax2)));
   const float sc = q8_scale(amax);
   const float rs = __frcp_rn(sc);
 #pragma unroll
@@ -191,7 +199,11 @@ __global__ void __launch_bounds__(256) add_ln_kernel(const __half* __restrict__ 
       unpack8(ua[c], fa);
       unpack8(ur[c], fr);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[c][j] = __fadd_rn(fa[j], fr[j]);
+      for (int j = 0; j < 8; j += 2) {
+        const float2 t = add2(make_float2(fa[j], fa[j + 1]), make_float2(fr[j], fr[j + 1]));
+        v[c][j] = t.x;
+        v[c][j + 1] = t.y;
+      }
     }
   }
   ln_store<NCH>(v, H, lane, g, b, eps, y16 + (size_t)row * ldy, yq ? yq + (size_t)row * ldq : nullptr,
@@ -222,17 +234,16 @@ __global__ void __launch_bounds__(256) quant_rows_kernel(const __half* __restric
 #pragma unroll
   for (int c = 0; c < NCH; ++c) u[c] = un[c];
   load_row(row + stride);
-  float amax = 0.0f;
+  __half2 amax2 = __float2half2_rn(0.0f);
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
     if (8 * (lane + 32 * c) < K) {
-      float f[8];
-      unpack8(u[c], f);
+      const __half2* hw = reinterpret_cast<const __half2*>(&u[c]);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) amax = fmaxf(amax, fabsf(f[j]));
+      for (int j = 0; j < 4; ++j) amax2 = __hmax2(amax2, __habs2(hw[j]));
     }
   }
-  amax = warp_max(amax);
+  const float amax = warp_max(fmaxf(__low2float(amax2), __high2float(amax2)));
   const float sc = q8_scale(amax);
   const float rs = __frcp_rn(sc);
 #pragma unroll
@@ -276,58 +287,130 @@ __global__ void __launch_bounds__(256) quant_rows_scalar_kernel(const __half* __
   if (lane == 0) scale[row] = sc;
 }
 
-// Pooler + classifier, fp32 (DESIGN R15).  pooler_kernel: CTA = 32 output
-// features j x 16 sequences; the 16 x0 rows are staged in smem (fp16 -> fp32),
-// each warp owns 4 j's with lanes over k (coalesced Wp rows) and writes
-// pooled[b][j] = tanh(Wp[j] . x0_b + bp[j]).  classifier_kernel: one warp per
-// (b, c) logit.
-constexpr int kHeadSeqs = 16;
-constexpr int kHeadJ = 32;
+// Pooler + classifier, fp32 (DESIGN R15).
+// pooler_kernel: split-K partial products of the [B x H] x [H x H]^T pooler
+// GEMM.  CTA = 64 sequences x 64 output features j x one K-slice (kPoolK
+// columns); the x0 rows (fp16 -> fp32) and Wp rows of the slice are staged in
+// smem with 16-byte loads (rows padded by 4 floats); each thread owns 4
+// sequences x 4 features (float4 k-steps: 8 LDS.128 per 64 FFMA).
+// part[ks][b][j] = sum over slice ks of Wp[j][k] x0_b[k].
+// head_kernel: CTA per sequence, thread per feature j: pooled_j =
+// tanh(sum_ks part[ks][b][j] + bp[j]) (fixed order), then logits[b][c] =
+// Wc[c] . pooled + bc[c] by a fixed-order block reduction.
+constexpr int kPoolT = 64, kPoolK = 128, kPoolLd = kPoolK + 4;
+constexpr size_t kPoolSmem = 2 * kPoolT * kPoolLd * sizeof(float);
 __global__ void __launch_bounds__(256) pooler_kernel(const __half* __restrict__ x16, int ldx, int B, int S, int H,
-                                                    const float* __restrict__ Wp, const float* __restrict__ bp,
-                                                    float* __restrict__ pooled) {
+                                                    const float* __restrict__ Wp, int cps, float* __restrict__ part) {
   griddep_wait();
   griddep_launch();
-  extern __shared__ float hsm[];  // [kHeadSeqs][H]
-  const int j0 = blockIdx.x * kHeadJ, b0 = blockIdx.y * kHeadSeqs;
-  const int nb = min(kHeadSeqs, B - b0);
-  for (int i = threadIdx.x; i < kHeadSeqs * H; i += blockDim.x) {
-    const int bb = i / H, k = i - bb * H;
-    hsm[i] = bb < nb ? __half2float(x16[(size_t)(b0 + bb) * S * ldx + k]) : 0.0f;
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int jj = 0; jj < kHeadJ / 8; ++jj) {
-    const int j = j0 + warp * (kHeadJ / 8) + jj;
-    if (j >= H) break;
-    float acc[kHeadSeqs];
+  extern __shared__ __align__(16) float psm[];
+  float* xs = psm;
+  float* ws = psm + kPoolT * kPoolLd;
+  const int j0 = blockIdx.x * kPoolT, b0 = blockIdx.y * kPoolT, ks = blockIdx.z;
+  const int tid = threadIdx.x;
+  const int tb = tid >> 4, tj = tid & 15;  // sequences b0 + tb + 16u, features j0 + tj + 16v
+  float acc[4][4];
 #pragma unroll
-    for (int bb = 0; bb < kHeadSeqs; ++bb) acc[bb] = 0.0f;
-    for (int k = lane; k < H; k += 32) {
-      const float w = __ldg(Wp + (size_t)j * H + k);
+  for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int bb = 0; bb < kHeadSeqs; ++bb) acc[bb] = __fmaf_rn(w, hsm[bb * H + k], acc[bb]);
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0f;
+  const int kend = min(H, (ks + 1) * cps * kPoolK);
+  for (int k0 = ks * cps * kPoolK; k0 < kend; k0 += kPoolK) {
+    const int kw = min(kPoolK, kend - k0);
+    // x0 slice: 64 rows x kw fp16 (8 per 16-byte load); Wp slice: 64 rows x kw fp32 (4 per load)
+    for (int i = tid; i < kPoolT * (kPoolK / 8); i += 256) {
+      const int bb = i / (kPoolK / 8), kk = (i - bb * (kPoolK / 8)) * 8;
+      float f[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (b0 + bb < B && kk < kw) {
+        const __half* src = x16 + (size_t)(b0 + bb) * S * ldx + k0 + kk;
+        if (kk + 8 <= kw) {
+          unpack8(*reinterpret_cast<const uint4*>(src), f);
+        } else {
+          for (int e = 0; e < kw - kk; ++e) f[e] = __half2float(src[e]);
+        }
+      }
+      float4* d = reinterpret_cast<float4*>(xs + bb * kPoolLd + kk);
+      d[0] = make_float4(f[0], f[1], f[2], f[3]);
+      d[1] = make_float4(f[4], f[5], f[6], f[7]);
     }
-#pragma unroll
-    for (int bb = 0; bb < kHeadSeqs; ++bb) {
-      const float sdot = warp_sum(acc[bb]);
-      if (lane == 0 && bb < nb) pooled[(size_t)(b0 + bb) * H + j] = tanhf(sdot + bp[j]);
+    for (int i = tid; i < kPoolT * (kPoolK / 4); i += 256) {
+      const int jj = i / (kPoolK / 4), kk = (i - jj * (kPoolK / 4)) * 4;
+      float4 v = make_float4(0, 0, 0, 0);
+      if (j0 + jj < H && kk < kw) {
+        const float* src = Wp + (size_t)(j0 + jj) * H + k0 + kk;
+        if (kk + 4 <= kw && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+          v = __ldg(reinterpret_cast<const float4*>(src));
+        } else {
+          float t[4] = {0, 0, 0, 0};
+          for (int e = 0; e < min(4, kw - kk); ++e) t[e] = __ldg(src + e);
+          v = make_float4(t[0], t[1], t[2], t[3]);
+        }
+      }
+      *reinterpret_cast<float4*>(ws + jj * kPoolLd + kk) = v;
     }
+    __syncthreads();
+#pragma unroll 2
+    for (int k = 0; k < kPoolK; k += 4) {
+      float4 xv[4], wv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) xv[u] = *reinterpret_cast<const float4*>(xs + (tb + 16 * u) * kPoolLd + k);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) wv[v] = *reinterpret_cast<const float4*>(ws + (tj + 16 * v) * kPoolLd + k);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          acc[u][v] = __fmaf_rn(xv[u].x, wv[v].x, acc[u][v]);
+          acc[u][v] = __fmaf_rn(xv[u].y, wv[v].y, acc[u][v]);
+          acc[u][v] = __fmaf_rn(xv[u].z, wv[v].z, acc[u][v]);
+          acc[u][v] = __fmaf_rn(xv[u].w, wv[v].w, acc[u][v]);
+        }
+    }
+    __syncthreads();
   }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int b = b0 + tb + 16 * u, j = j0 + tj + 16 * v;
+      if (b < B && j < H) part[((size_t)ks * B + b) * H + j] = acc[u][v];
+    }
 }
 
-__global__ void __launch_bounds__(256) classifier_kernel(const float* __restrict__ pooled, int B, int H, int C,
-                                                        const float* __restrict__ Wc, const float* __restrict__ bc,
-                                                        float* __restrict__ logits) {
+constexpr int kHeadThreads = 256, kHeadClasses = 8;
+__global__ void __launch_bounds__(kHeadThreads) head_kernel(const float* __restrict__ part, int nks, int B, int H,
+                                                           int C, const float* __restrict__ bp,
+                                                           const float* __restrict__ Wc, const float* __restrict__ bc,
+                                                           float* __restrict__ logits) {
   griddep_wait();
   griddep_launch();
-  const int t = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (t >= B * C) return;
-  const int b = t / C, c = t - b * C;
-  float acc = 0.0f;
-  for (int k = lane; k < H; k += 32) acc = __fmaf_rn(__ldg(Wc + (size_t)c * H + k), pooled[(size_t)b * H + k], acc);
-  acc = warp_sum(acc);
-  if (lane == 0) logits[t] = acc + bc[c];
+  __shared__ float red[kHeadThreads / 32][kHeadClasses];
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int c0 = 0; c0 < C; c0 += kHeadClasses) {
+    float acc[kHeadClasses];
+#pragma unroll
+    for (int c = 0; c < kHeadClasses; ++c) acc[c] = 0.0f;
+    for (int j = tid; j < H; j += kHeadThreads) {
+      float z = 0.0f;
+      for (int ks = 0; ks < nks; ++ks) z += part[((size_t)ks * B + b) * H + j];
+      const float pj = tanhf(z + bp[j]);
+#pragma unroll
+      for (int c = 0; c < kHeadClasses; ++c)
+        if (c0 + c < C) acc[c] = __fmaf_rn(__ldg(Wc + (size_t)(c0 + c) * H + j), pj, acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < kHeadClasses; ++c) {
+      const float v = warp_sum(acc[c]);
+      if (lane == 0) red[warp][c] = v;
+    }
+    __syncthreads();
+    if (tid < kHeadClasses && c0 + tid < C) {
+      float v = 0.0f;
+      for (int w = 0; w < kHeadThreads / 32; ++w) v += red[w][tid];
+      logits[(size_t)b * C + c0 + tid] = v + bc[c0 + tid];
+    }
+    __syncthreads();
+  }
 }
 
 __global__ void cast_f16_kernel(const float* __restrict__ src, int N, int K, __half* __restrict__ dst, int ldd) {
@@ -414,18 +497,22 @@ cudaError_t launch_quant_rows(const __half* x, int ldx, int M, int K, int8_t* q,
 }
 
 cudaError_t launch_head(const __half* x16, int ldx, int B, int S, int H, int C, const float* Wp, const float* bp,
-                        const float* Wc, const float* bc, float* pooled, float* logits, cudaStream_t s) {
-  const size_t smem = kHeadSeqs * H * sizeof(float);
-  dim3 grid((H + kHeadJ - 1) / kHeadJ, (B + kHeadSeqs - 1) / kHeadSeqs);
-  launch_ex(pooler_kernel, dim3(grid), dim3(256), smem, s, 0,x16, ldx, B, S, H, Wp, bp, pooled);
+                        const float* Wc, const float* bc, float* part, float* logits, cudaStream_t s) {
+  // nks K slices of cps kPoolK-column chunks; part holds nks x B x H floats,
+  // within the caller's B x S x H scratch (nks <= S)
+  const int chunks = (H + kPoolK - 1) / kPoolK;
+  const int cps = (chunks + min(chunks, S) - 1) / min(chunks, S);
+  const int nks = (chunks + cps - 1) / cps;
+  dim3 grid((H + kPoolT - 1) / kPoolT, (B + kPoolT - 1) / kPoolT, nks);
+  launch_ex(pooler_kernel, grid, dim3(256), kPoolSmem, s, 0, x16, ldx, B, S, H, Wp, cps, part);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  launch_ex(classifier_kernel, dim3((B * C + 7) / 8), dim3(256), 0, s, 0,pooled, B, H, C, Wc, bc, logits);
+  launch_ex(head_kernel, dim3(B), dim3(kHeadThreads), 0, s, 0, (const float*)part, nks, B, H, C, bp, Wc, bc, logits);
   return cudaGetLastError();
 }
 
 cudaError_t prepare_row_kernels() {
-  return cudaFuncSetAttribute(pooler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHeadSeqs * 1024 * 4);
+  return cudaFuncSetAttribute(pooler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPoolSmem);
 }
 
 cudaError_t launch_cast_f16(const float* src, int N, int K, __half* dst, int ldd, cudaStream_t s) {
