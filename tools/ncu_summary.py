@@ -93,7 +93,7 @@ def main():
                 f(d, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
                 f(d, "dram__bytes_read.sum"), f(d, "dram__bytes_write.sum"),
                 f(d, "lts__throughput.avg.pct_of_peak_sustained_elapsed"),
-                f(d, "dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+                f(d, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
                 ", ".join(f"{n} {v:.0f}" for v, n in st)))
         lines.append("")
     open(a.out, "w").write("\n".join(lines) + "\n")
