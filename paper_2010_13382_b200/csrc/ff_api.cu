@@ -855,6 +855,8 @@ ff_status ff_profile(ff_model* m, const int32_t* d_token_ids, const int32_t* d_m
   return FF_OK;
 }
 
+static unsigned long long* g_debug_trace = nullptr;  // ff_debug_set_trace
+
 ff_status ff_debug_gemm(int32_t dtype, const void* d_A, int32_t lda, const void* d_W, int32_t ldw, int32_t M,
                         int32_t N, int32_t K, int32_t out_mode, void* d_C, int32_t ldc, const float* d_bias,
                         const float* d_sx, const float* d_sw, int32_t act, void* stream) {
@@ -886,7 +888,13 @@ ff_status ff_debug_gemm(int32_t dtype, const void* d_A, int32_t lda, const void*
   g.p.row_scale = d_sx;
   g.p.col_scale = d_sw;
   g.p.act = act;
+  g.p.trace = g_debug_trace;
   FF_CK(ff::launch_gemm(g, static_cast<cudaStream_t>(stream)));
+  return FF_OK;
+}
+
+ff_status ff_debug_set_trace(uint64_t* d_trace) {
+  g_debug_trace = reinterpret_cast<unsigned long long*>(d_trace);
   return FF_OK;
 }
 

@@ -55,6 +55,7 @@ struct GemmParams {
   const float* row_scale;  // sx [M] (i8)
   const float* col_scale;  // sw [N] (i8)
   int act;                 // Act
+  unsigned long long* trace;  // debug timeline (ff_debug_set_trace), null in production
 };
 
 struct GemmPlan {

@@ -37,8 +37,8 @@ constexpr int BK_BYTES = 128;  // one 128-byte swizzle row of K per k-block
 // stored with 32B swizzle.  <= 96 registers per thread at 640 threads.
 constexpr int kEpiWarps = 16;
 constexpr int kThreads = 128 + 32 * kEpiWarps;
-constexpr int kEpiCols = 16;
-constexpr int kStageTile = 32 * kEpiCols * 2;  // 1 KB
+constexpr int kEpiCols = 32;                     // columns per epilogue chunk (two 16-column TMEM loads)
+constexpr int kStageTile = 32 * kEpiCols * 2;  // 2 KB: 32 rows x 64 B, 64-byte swizzle
 // gemm_rr_kernel: 8 epilogue warps (2 per quadrant), 32-column chunks, 32x32
 // staging blocks with 64B swizzle.
 constexpr int kRREpiWarps = 8;
@@ -53,9 +53,10 @@ struct GemmCfg {
   static constexpr int A_BYTES = BM * BK_BYTES;
   static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (PAIR || BN == 128) ? 6 : 4;
+  static constexpr int STAGES = (PAIR || BN == 128) ? 4 : 3;
   static constexpr int EPI_OFF = STAGES * STAGE_BYTES;
-  static constexpr int BAR_OFF = EPI_OFF + kEpiWarps * 2 * kStageTile;
+  static constexpr int PAR_OFF = EPI_OFF + kEpiWarps * 2 * kStageTile;  // [acc][bias | col scale][BN] fp32
+  static constexpr int BAR_OFF = PAR_OFF + 2 * 2 * BN * 4;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;  // barriers + 1 KB alignment slack
   static constexpr uint32_t TMEM_COLS = 2 * BN;
   static_assert(SMEM <= 227 * 1024, "smem budget");
@@ -70,30 +71,34 @@ __device__ __forceinline__ constexpr uint32_t make_idesc() {
          ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
 }
 
-// erf(x) for the GELU epilogue, branch-free: erf(t) = 1 - 2^(-t * P7(t)) on
-// t = |x| (clamped to 4, where erf rounds to 1 in fp32), P7 a degree-7
-// least-squares fit of -log2(erfc(t))/t.  |erf_fast - erf| <= 3e-7 absolute
-// (fp32 evaluation incl. ex2.approx), far below the fp16 rounding of the
-// GELU output (DESIGN R2); replaces erff, whose divergent branches made the
-// FFN1 epilogue the bottleneck of that GEMM.
-__device__ __forceinline__ float erf_fast(float x) {
-  const float t = fminf(fabsf(x), 4.0f);
-  float p = 4.5357247e-05f;
-  p = __fmaf_rn(p, t, -0.000445495f);
-  p = __fmaf_rn(p, t, 0.0014893987f);
-  p = __fmaf_rn(p, t, 0.0007746952f);
-  p = __fmaf_rn(p, t, -0.028253723f);
-  p = __fmaf_rn(p, t, 0.14848162f);
-  p = __fmaf_rn(p, t, 0.9184164f);
-  p = __fmaf_rn(p, t, 1.6279086f);
-  float e;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-t * p));
-  return copysignf(1.0f - e, x);
-}
+// GELU(y) = y/2 (1 + erf(y / sqrt 2)) for the FFN1 epilogue, branch-free.
+// With s = |y| (clamped to 4 sqrt 2, where erf rounds to 1 in fp32) and
+// e = erfc(s / sqrt 2) = 2^(-s * P6(s)):  GELU(y) = y/2 * (2 - e) for y >= 0
+// and y/2 * e for y < 0 — no cancellation on the negative side.  P6 is a
+// degree-6 fit of -log2(erfc(s / sqrt 2)) / s weighted for the RELATIVE error
+// of e (<= 3.9e-6; 1/sqrt 2 folded into the coefficients).  Against the exact
+// GELU rounded to fp16, 0.4% of outputs differ, by at most 1 fp16 ulp (DESIGN
+// R2; was 1.6% / 2 ulp with a degree-7 absolute-error erf fit).  Replaces
+// erff, whose divergent branches made the FFN1 epilogue the GEMM's bottleneck.
+constexpr float kG6 = 1.7657696e-06f, kG5 = -6.0254122e-05f, kG4 = 9.2013367e-04f, kG3 = -8.4673585e-03f,
+                kG2 = 5.3876434e-02f, kG1 = 4.5855144e-01f, kG0 = 1.1512122f;
+constexpr float kGeluClamp = 5.6568542f;  // 4 sqrt 2
 
 template <int ACT>
 __device__ __forceinline__ float act_fn(float y) {
-  if (ACT == ACT_GELU) return 0.5f * y * (1.0f + erf_fast(y * 0.70710678118654752f));
+  if (ACT == ACT_GELU) {
+    const float s = fminf(fabsf(y), kGeluClamp);
+    float p = kG6;
+    p = __fmaf_rn(p, s, kG5);
+    p = __fmaf_rn(p, s, kG4);
+    p = __fmaf_rn(p, s, kG3);
+    p = __fmaf_rn(p, s, kG2);
+    p = __fmaf_rn(p, s, kG1);
+    p = __fmaf_rn(p, s, kG0);
+    float e;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-s * p));
+    return (0.5f * y) * (y >= 0.0f ? 2.0f - e : e);
+  }
   if (ACT == ACT_RELU) return fmaxf(y, 0.0f);
   if (ACT == ACT_GELU_TANH) {
     const float u = 0.7978845608028654f * (y + 0.044715f * y * y * y);
@@ -102,27 +107,23 @@ __device__ __forceinline__ float act_fn(float y) {
   return y;
 }
 
-// GELU of a pair on packed fp32 (FFMA2 / FMUL2): same erf_fast polynomial,
-// g = h + h * erf(y / sqrt 2) with h = y / 2.
+// GELU of a pair on packed fp32 (FFMA2 / FMUL2), same arithmetic as act_fn.
 __device__ __forceinline__ float2 gelu2(float2 y) {
-  const float2 u = mul2(y, make_float2(0.70710678118654752f, 0.70710678118654752f));
-  const float2 t = make_float2(fminf(fabsf(u.x), 4.0f), fminf(fabsf(u.y), 4.0f));
-  float2 p = make_float2(4.5357247e-05f, 4.5357247e-05f);
-  p = fma2(p, t, make_float2(-0.000445495f, -0.000445495f));
-  p = fma2(p, t, make_float2(0.0014893987f, 0.0014893987f));
-  p = fma2(p, t, make_float2(0.0007746952f, 0.0007746952f));
-  p = fma2(p, t, make_float2(-0.028253723f, -0.028253723f));
-  p = fma2(p, t, make_float2(0.14848162f, 0.14848162f));
-  p = fma2(p, t, make_float2(0.9184164f, 0.9184164f));
-  p = fma2(p, t, make_float2(1.6279086f, 1.6279086f));
-  const float2 a = mul2(t, p);
+  const float2 s = make_float2(fminf(fabsf(y.x), kGeluClamp), fminf(fabsf(y.y), kGeluClamp));
+  float2 p = make_float2(kG6, kG6);
+  p = fma2(p, s, make_float2(kG5, kG5));
+  p = fma2(p, s, make_float2(kG4, kG4));
+  p = fma2(p, s, make_float2(kG3, kG3));
+  p = fma2(p, s, make_float2(kG2, kG2));
+  p = fma2(p, s, make_float2(kG1, kG1));
+  p = fma2(p, s, make_float2(kG0, kG0));
+  const float2 a = mul2(s, p);
   float2 e;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(-a.x));
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(-a.y));
-  const float2 er = sub2(make_float2(1.0f, 1.0f), e);
-  const float2 erf = make_float2(copysignf(er.x, u.x), copysignf(er.y, u.y));
-  const float2 h = mul2(y, make_float2(0.5f, 0.5f));
-  return fma2(h, erf, h);
+  const float2 t = sub2(make_float2(2.0f, 2.0f), e);
+  const float2 sel = make_float2(y.x >= 0.0f ? t.x : e.x, y.y >= 0.0f ? t.y : e.y);
+  return mul2(mul2(y, make_float2(0.5f, 0.5f)), sel);
 }
 
 // W columns [n0, n0+W) of this thread's row: dequant / bias / activation,
@@ -140,6 +141,35 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[W], const float (&
       v = fma2(a, mul2(make_float2(sx, sx), make_float2(sw[j], sw[j + 1])), b);
     } else {
       v = add2(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), b);
+    }
+    if (ACT == ACT_GELU) {
+      v = gelu2(v);
+    } else if (ACT != ACT_NONE) {
+      v.x = act_fn<ACT>(v.x);
+      v.y = act_fn<ACT>(v.y);
+    }
+    h[e] = pack_half2(v.x, v.y);
+  }
+}
+
+// 32 columns of this thread's row (r[0]: columns 0-15, r[1]: 16-31), bias /
+// column scales read from smem (bs / ss, broadcast LDS.64 per pair):
+// dequant / bias / activation, RNE to fp16, packed as 16 half2 words.
+template <bool I8, int ACT>
+__device__ __forceinline__ void epi32(const uint32_t (&r)[2][16], const float* bs, const float* ss, float sx,
+                                      uint32_t (&h)[16]) {
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const int j = 2 * e;
+    const uint32_t r0 = r[j >> 4][j & 15], r1 = r[j >> 4][(j & 15) + 1];
+    const float2 b = *reinterpret_cast<const float2*>(bs + j);
+    float2 v;
+    if (I8) {
+      const float2 sw2 = *reinterpret_cast<const float2*>(ss + j);
+      const float2 a = make_float2(__int2float_rn(static_cast<int>(r0)), __int2float_rn(static_cast<int>(r1)));
+      v = fma2(a, mul2(make_float2(sx, sx), sw2), b);
+    } else {
+      v = add2(make_float2(__uint_as_float(r0), __uint_as_float(r1)), b);
     }
     if (ACT == ACT_GELU) {
       v = gelu2(v);
@@ -173,6 +203,21 @@ __device__ __forceinline__ void loadN(float (&dst)[W], const float* src, int n0,
 __device__ __forceinline__ void load32(float (&dst)[32], const float* src, int n0, int N) { loadN<32>(dst, src, n0, N); }
 
 // tcgen05.ld of 16 columns (32x32b.x16): thread t gets row (lane base + t).
+
+// Debug timeline: globaltimer of event e for local tile t of CTA c at
+// trace[(c * kTraceTiles + t) * 24 + e] (events: 0 acc free seen by MMA, 1
+// first operands seen, 2 accumulator committed, 3 tfull seen by epilogue
+// warp 0, 4 accumulator released, 5 epilogue done, 6 first load issued;
+// epilogue warp 0, chunk i < 4: 8+3i TMEM load landed, 9+3i staging buffer
+// free, 10+3i store issued).
+constexpr int kTraceTiles = 64;
+__device__ __forceinline__ void gemm_trace(unsigned long long* trace, int t, int e) {
+  if (trace != nullptr && t < kTraceTiles) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+    trace[((size_t)blockIdx.x * kTraceTiles + t) * 24 + e] = v;
+  }
+}
 
 template <int BN, bool I8, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -234,12 +279,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = unit; tile < num_tiles; tile += nunits) {
+      int lt = 0;
+      for (int tile = unit; tile < num_tiles; tile += nunits, ++lt) {
         const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
         const int arow = mt * TM + (int)rank * BM;
         const int brow = nt * BN + (PAIR ? (int)rank * (BN / 2) : 0);
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
+          if (kb == 0) gemm_trace(p.trace, lt, 6);
           if (PAIR) {
             // the leader's full barrier counts the bytes of both CTAs' loads
             if (rank == 0) mbar_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
@@ -265,12 +312,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = unit; tile < num_tiles; tile += nunits) {
+      int lt = 0;
+      for (int tile = unit; tile < num_tiles; tile += nunits, ++lt) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
+        gemm_trace(p.trace, lt, 0);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&full[stage], phase);
+          if (kb == 0) gemm_trace(p.trace, lt, 1);
           tc_fence_after();
           const uint64_t adesc = make_sw128_desc(sA + stage * Cfg::A_BYTES);
           const uint64_t bdesc = make_sw128_desc(sB + stage * Cfg::B_BYTES);
@@ -296,6 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // accumulator ready for the epilogue warps (of both CTAs)
         if (PAIR) mma_commit_pair(&tfull[acc], 0x3);
         else mma_commit(&tfull[acc]);
+        gemm_trace(p.trace, lt, 2);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -312,13 +363,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     int nbuf = 0;
-    for (int tile = unit; tile < num_tiles; tile += nunits) {
+    int lt = 0;
+    const bool tr0 = ew == 0 && lane == 0;
+    float* sPar = reinterpret_cast<float*>(smem + Cfg::PAR_OFF);
+    const int et = ew * 32 + lane;  // 0 .. 511
+    for (int tile = unit; tile < num_tiles; tile += nunits, ++lt) {
       const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
       const int row0 = mt * TM + (int)rank * BM + q * 32;
       const int row = row0 + lane;
       float sx = 0.0f;
       if (I8 && p.out_mode == 1 && row < p.M) sx = p.row_scale[row];
+      // this tile's bias / column scales -> smem (double-buffered by acc; the
+      // barrier of tile t+1 orders every warp's reads of tile t before the
+      // writes of tile t+2), read by the chunks with low-latency LDS
+      float* par = sPar + acc * 2 * BN;
+      if (p.out_mode == 1 && et < 2 * BN) {
+        const int col = nt * BN + (et % BN);
+        const float* src = et < BN ? p.bias : p.col_scale;
+        par[et] = (src != nullptr && col < p.N) ? __ldg(src + col) : 0.0f;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
       mbar_wait(&tfull[acc], acc_phase);
+      if (tr0) gemm_trace(p.trace, lt, 3);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       // Release the accumulator to the MMA warp as soon as this warp's last
@@ -330,12 +396,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (PAIR) mbar_arrive_remote(tempty_leader0 + acc * 8);  // the leader's barrier
           else mbar_arrive(&tempty[acc]);
         }
+        if (tr0) gemm_trace(p.trace, lt, 4);
       };
       if (p.out_mode == 0) {  // raw accumulators (tests only)
 #pragma unroll 1
         for (int c = c_lo; c < c_lo + WCOLS; c += kEpiCols) {
           uint32_t r[kEpiCols];
-          tmem_ld16(tbase + c, r);
+          tmem_ld32(tbase + c, r);
           tmem_wait_ld();
           const int n0 = nt * BN + c;
           if (row < p.M && n0 < p.N) {
@@ -347,34 +414,39 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         release_acc();
       } else {
-        // software pipeline: the TMEM load of chunk c+1 overlaps the stores of chunk c
-        uint32_t r[kEpiCols];
-        tmem_ld16(tbase + c_lo, r);
+        // software pipeline: the TMEM loads of chunk c+1 overlap the stores of chunk c
+        uint32_t r[2][16];
+        tmem_ld16(tbase + c_lo, r[0]);
+        tmem_ld16(tbase + c_lo + 16, r[1]);
 #pragma unroll 1
         for (int c = c_lo; c < c_lo + WCOLS; c += kEpiCols) {
           const int n0 = nt * BN + c;
           const bool last = c + kEpiCols >= c_lo + WCOLS;
-          float bias[kEpiCols], sw[kEpiCols];
-          loadN<kEpiCols>(bias, p.bias, n0, p.N);
-          if (I8) loadN<kEpiCols>(sw, p.col_scale, n0, p.N);
           tmem_wait_ld();
+          const int ci = (c - c_lo) / kEpiCols;
+          if (tr0 && ci < 4) gemm_trace(p.trace, lt, 8 + 3 * ci);
           if (last) release_acc();
-          uint32_t h[kEpiCols / 2];
+          uint32_t h[16];
           switch (p.act) {
-            case ACT_GELU: epi_chunk<I8, ACT_GELU, kEpiCols>(r, bias, sw, sx, h); break;
-            case ACT_RELU: epi_chunk<I8, ACT_RELU, kEpiCols>(r, bias, sw, sx, h); break;
-            case ACT_GELU_TANH: epi_chunk<I8, ACT_GELU_TANH, kEpiCols>(r, bias, sw, sx, h); break;
-            default: epi_chunk<I8, ACT_NONE, kEpiCols>(r, bias, sw, sx, h); break;
+            case ACT_GELU: epi32<I8, ACT_GELU>(r, par + c, par + BN + c, sx, h); break;
+            case ACT_RELU: epi32<I8, ACT_RELU>(r, par + c, par + BN + c, sx, h); break;
+            case ACT_GELU_TANH: epi32<I8, ACT_GELU_TANH>(r, par + c, par + BN + c, sx, h); break;
+            default: epi32<I8, ACT_NONE>(r, par + c, par + BN + c, sx, h); break;
           }
-          if (!last) tmem_ld16(tbase + c + kEpiCols, r);
+          if (!last) {
+            tmem_ld16(tbase + c + kEpiCols, r[0]);
+            tmem_ld16(tbase + c + kEpiCols + 16, r[1]);
+          }
+          if (tr0 && ci < 4) gemm_trace(p.trace, lt, 20 + ci);
           if (n0 < p.N) {  // warp-uniform; TMA clips the N tail of the chunk
             uint8_t* buf = stage_buf + (nbuf & 1) * kStageTile;
             if (lane == 0) bulk_wait_read<1>();  // the store that last used `buf` has read it
             __syncwarp();
-            uint8_t* srow = buf + lane * 32;
+            if (tr0 && ci < 4) gemm_trace(p.trace, lt, 9 + 3 * ci);
+            uint8_t* srow = buf + lane * 64;
 #pragma unroll
-            for (int cc = 0; cc < 2; ++cc) {  // SWIZZLE_32B: 16B chunk cc of 32B row `lane`
-              const int pc = cc ^ ((lane >> 2) & 1);
+            for (int cc = 0; cc < 4; ++cc) {  // SWIZZLE_64B: 16B chunk cc of 64B row `lane`
+              const int pc = cc ^ ((lane >> 1) & 3);
               *reinterpret_cast<uint4*>(srow + pc * 16) =
                   make_uint4(h[4 * cc], h[4 * cc + 1], h[4 * cc + 2], h[4 * cc + 3]);
             }
@@ -384,10 +456,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_store_2d(&tmC, buf, n0, row0);
               bulk_commit();
             }
+            if (tr0 && ci < 4) gemm_trace(p.trace, lt, 10 + 3 * ci);
             ++nbuf;
           }
         }
       }
+      if (tr0) gemm_trace(p.trace, lt, 5);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -855,6 +929,7 @@ bool plan_gemm(GemmPlan* g, bool i8, const void* A, int M_rows, int lda, const v
   g->p.out_mode = 1;
   g->p.bias = g->p.row_scale = g->p.col_scale = nullptr;
   g->p.act = ACT_NONE;
+  g->p.trace = nullptr;
   plan_gemm_set_m(g, M_rows);
   return true;
 }
@@ -864,7 +939,7 @@ bool plan_gemm_output(GemmPlan* g, void* out, int ldo, const char** err) {
   g->p.ldo = ldo;
   g->has_out_map = true;
   return encode_2d(&g->tmC, out, g->M_rows, g->p.N, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (size_t)ldo * 2, kEpiCols,
-                   32, CU_TENSOR_MAP_SWIZZLE_32B, err);
+                   32, CU_TENSOR_MAP_SWIZZLE_64B, err);
 }
 
 void plan_gemm_set_m(GemmPlan* g, int M) {

@@ -30,7 +30,7 @@ STATUS_NAMES = ["FF_OK", "FF_E_INVALID", "FF_E_SHAPE", "FF_E_STATE", "FF_E_CUDA"
 EXPORTED = ["ff_abi_version", "ff_last_error", "ff_model_create", "ff_model_memory", "ff_bind_memory",
             "ff_load_weights", "ff_finalize", "ff_encode", "ff_encode_host", "ff_check", "ff_set_option",
             "ff_model_destroy", "ff_launch_count", "ff_profile", "ff_encode_trace", "ff_debug_gemm", "ff_debug_quant_rows",
-            "ff_debug_attention", "ff_debug_attention_q8"]
+            "ff_debug_attention", "ff_debug_attention_q8", "ff_debug_set_trace"]
 
 
 class FFError(RuntimeError):
@@ -78,6 +78,7 @@ def lib():
         L.ff_debug_quant_rows.argtypes = [vp, i32, i32, i32, vp, i32, vp, vp]
         L.ff_debug_attention.argtypes = [vp, vp, i32, i32, i32, i32, vp, i32, vp]
         L.ff_debug_attention_q8.argtypes = [vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp]
+        L.ff_debug_set_trace.argtypes = [vp]
         for name in EXPORTED:
             if name not in ("ff_abi_version", "ff_last_error", "ff_model_destroy"):
                 getattr(L, name).restype = i32
@@ -260,3 +261,9 @@ def attention_q8(qkv16, mask, A, d, with_ctx16=True, trace=None):
                                       _ptr(q), _ptr(s), _ptr(trace) if trace is not None else None,
                                       _stream_ptr()))
     return ctx, q, s
+
+
+def set_gemm_trace(trace=None):
+    """Debug: record per-tile timestamps of subsequent debug GEMMs into `trace`
+    (zeroed int64 CUDA tensor [grid, 64, 8]); None switches it off."""
+    check(lib().ff_debug_set_trace(_ptr(trace) if trace is not None else None))
