@@ -217,10 +217,12 @@ FF_API ff_status ff_debug_quant_rows(const void *d_x16, int32_t M, int32_t K, in
  * 2 = tcgen05 only (FF_E_UNSUPPORTED otherwise). */
 FF_API ff_status ff_debug_attention(const void *d_qkv16, const int32_t *d_mask, int32_t B, int32_t S, int32_t A,
                                     int32_t d, void *d_ctx16, int32_t impl, void *stream);
-/* Debug timeline for subsequent ff_debug_gemm launches (NULL = off): uint64
- * [grid x 64 x 24] per-CTA per-tile %globaltimer stamps (events documented in
- * csrc/gemm_tc.cu); the buffer must be zeroed by the caller. */
-FF_API ff_status ff_debug_set_trace(uint64_t *d_trace);
+/* Debug timeline (NULL = off): uint64 [grid x 64 x 24] per-CTA per-tile
+ * %globaltimer stamps (events documented in csrc/gemm_tc.cu); the buffer must
+ * be zeroed by the caller.  which = 0: subsequent ff_debug_gemm launches;
+ * 1 / 2 / 3: the layer-0 fused out-proj+LN / FFN1+requant / FFN2+LN GEMM of
+ * subsequent forwards (FF_OPT_FUSED_EPILOGUES). */
+FF_API ff_status ff_debug_set_trace(uint64_t *d_trace, int32_t which);
 
 /* The tcgen05 attention with the int8 ctx requant fused (a3 + a4; the path
  * int8 layers take): ctx rows are quantized per row, Q8row (DESIGN R6-R8),

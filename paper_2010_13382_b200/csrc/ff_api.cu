@@ -241,11 +241,16 @@ ff_status build_gemm_plans(ff_model* m) {
                        m->dWS + m->ws_h1, m->ldx16, &err))
         return fail(FF_E_CUDA, std::string("rr tensor map: ") + err);
       P.rp[0].p.mode = ff::RR_LN;
+      if (!ff::plan_rr_io(&P.rp[0], m->dWS + m->ws_x16, m->ldx16, q ? m->dWS + m->ws_h1q : nullptr, m->ldx8, &err))
+        return fail(FF_E_CUDA, std::string("rr tensor map: ") + err);
       A = gemm_a(m, P, W_FFN2, &lda);
       if (!ff::plan_rr(&P.rp[2], q, A, m->cfg.max_tokens, lda, m->dW + P.w[W_FFN2], P.ldw[W_FFN2], P.N[W_FFN2],
                        P.K[W_FFN2], m->dWS + m->ws_x16, m->ldx16, &err))
         return fail(FF_E_CUDA, std::string("rr tensor map: ") + err);
       P.rp[2].p.mode = ff::RR_LN;
+      const bool nq = l + 1 < m->L.size() && m->L[l + 1].dt == FF_I8;
+      if (!ff::plan_rr_io(&P.rp[2], m->dWS + m->ws_h1, m->ldx16, nq ? m->dWS + m->ws_xq : nullptr, m->ldx8, &err))
+        return fail(FF_E_CUDA, std::string("rr tensor map: ") + err);
     }
     if (P.rr_ok[1]) {
       int lda;
@@ -254,6 +259,8 @@ ff_status build_gemm_plans(ff_model* m) {
                        P.K[W_FFN1], m->dWS + m->ws_i, m->ldi16, &err))
         return fail(FF_E_CUDA, std::string("rr tensor map: ") + err);
       P.rp[1].p.mode = ff::RR_QUANT;
+      if (!ff::plan_rr_io(&P.rp[1], nullptr, 0, m->dWS + m->ws_iq, m->ldi8, &err))
+        return fail(FF_E_CUDA, std::string("rr tensor map: ") + err);
     }
   }
   return FF_OK;
@@ -302,6 +309,11 @@ bool attention_fuses_quant(const ff_model* m, const LayerPlan& P, int S) {
   return P.dt == FF_I8 && m->attn_tc && ff::attention_tc_supported(S, m->cfg.head_dim, m->ldqkv, m->ldc16) &&
          ff::attention_tc_fuses_quant(P.A);
 }
+
+// ff_debug_set_trace: timeline buffer and target (0 debug GEMMs; 1 / 2 / 3 the
+// layer-0 fused out-proj+LN / FFN1+requant / FFN2+LN of the next forward).
+static unsigned long long* g_debug_trace = nullptr;
+static int g_debug_trace_which = 0;
 
 // The launch sequence of one encoder forward.
 ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int B, int S, float* logits,
@@ -378,6 +390,7 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
       r.p.outq = q ? H1q : nullptr;
       r.p.ldq = m->ldx8;
       r.p.out_scale = q ? H1s : nullptr;
+      r.p.trace = (l == 0 && g_debug_trace_which == 1) ? g_debug_trace : nullptr;
       FF_LAUNCH(q ? FF_K_GEMM_I8 : FF_K_GEMM_F16, ff::launch_rr(r, s), "gemm o + ln1");
     } else {
     g = P.gp[W_O];
@@ -411,6 +424,7 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
       r.p.outq = Iq;
       r.p.ldq = m->ldi8;
       r.p.out_scale = Is;
+      r.p.trace = (l == 0 && g_debug_trace_which == 2) ? g_debug_trace : nullptr;
       FF_LAUNCH(FF_K_GEMM_I8, ff::launch_rr(r, s), "gemm ffn1 + quant");
       if (tr && dump(d_dump[5], I16, m->ldi16, P.F, M, s) != FF_OK) return FF_E_CUDA;
     } else {
@@ -445,6 +459,7 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
       r.p.outq = nq ? Xq : nullptr;
       r.p.ldq = m->ldx8;
       r.p.out_scale = nq ? Xs : nullptr;
+      r.p.trace = (l == 0 && g_debug_trace_which == 3) ? g_debug_trace : nullptr;
       FF_LAUNCH(q ? FF_K_GEMM_I8 : FF_K_GEMM_F16, ff::launch_rr(r, s), "gemm ffn2 + ln2");
     } else {
     g = P.gp[W_FFN2];
@@ -855,8 +870,6 @@ ff_status ff_profile(ff_model* m, const int32_t* d_token_ids, const int32_t* d_m
   return FF_OK;
 }
 
-static unsigned long long* g_debug_trace = nullptr;  // ff_debug_set_trace
-
 ff_status ff_debug_gemm(int32_t dtype, const void* d_A, int32_t lda, const void* d_W, int32_t ldw, int32_t M,
                         int32_t N, int32_t K, int32_t out_mode, void* d_C, int32_t ldc, const float* d_bias,
                         const float* d_sx, const float* d_sw, int32_t act, void* stream) {
@@ -888,13 +901,14 @@ ff_status ff_debug_gemm(int32_t dtype, const void* d_A, int32_t lda, const void*
   g.p.row_scale = d_sx;
   g.p.col_scale = d_sw;
   g.p.act = act;
-  g.p.trace = g_debug_trace;
+  g.p.trace = g_debug_trace_which == 0 ? g_debug_trace : nullptr;
   FF_CK(ff::launch_gemm(g, static_cast<cudaStream_t>(stream)));
   return FF_OK;
 }
 
-ff_status ff_debug_set_trace(uint64_t* d_trace) {
+ff_status ff_debug_set_trace(uint64_t* d_trace, int32_t which) {
   g_debug_trace = reinterpret_cast<unsigned long long*>(d_trace);
+  g_debug_trace_which = which;
   return FF_OK;
 }
 

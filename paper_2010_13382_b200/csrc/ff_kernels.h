@@ -110,9 +110,12 @@ struct RRParams {
   int8_t* outq;            // s8 rows [M, ldq] or null
   int ldq;
   float* out_scale;        // [M] or null
+  unsigned long long* trace;  // debug timeline (ff_debug_set_trace), null in production
 };
 struct RRPlan {
   CUtensorMap tmA, tmB, tmC;
+  CUtensorMap tmR;  // residual fp16 [M_rows x N], 32 x 32 boxes (RR_LN)
+  CUtensorMap tmQ;  // s8 output [M_rows x N], 32 x 32 boxes (when outq is used)
   RRParams p;
   int i8, cn, grid, M_rows;
 };
@@ -120,6 +123,8 @@ bool rr_supported(int N);
 bool plan_rr(RRPlan* g, bool i8, const void* A, int M_rows, int lda, const void* W, int ldw, int N, int K,
              void* out16, int ldo, const char** err);
 void plan_rr_set_m(RRPlan* g, int M);
+// Bind the residual (RR_LN) and s8 output buffers (either may be null) of a plan.
+bool plan_rr_io(RRPlan* g, const void* residual, int ldr, void* outq, int ldq, const char** err);
 cudaError_t launch_rr(const RRPlan& g, cudaStream_t s);
 cudaError_t prepare_rr_kernels();
 

@@ -39,9 +39,9 @@ constexpr int kEpiWarps = 16;
 constexpr int kThreads = 128 + 32 * kEpiWarps;
 constexpr int kEpiCols = 32;                     // columns per epilogue chunk (two 16-column TMEM loads)
 constexpr int kStageTile = 32 * kEpiCols * 2;  // 2 KB: 32 rows x 64 B, 64-byte swizzle
-// gemm_rr_kernel: 8 epilogue warps (2 per quadrant), 32-column chunks, 32x32
-// staging blocks with 64B swizzle.
-constexpr int kRREpiWarps = 8;
+// gemm_rr_kernel: 16 epilogue warps (4 per quadrant, 64 columns each),
+// 32-column chunks, 32x32 fp16 staging blocks with 64B swizzle.
+constexpr int kRREpiWarps = 16;
 constexpr int kRRThreads = 128 + 32 * kRREpiWarps;
 constexpr int kRRStageTile = 32 * 64;  // 2 KB
 
@@ -480,58 +480,59 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ========================================================================
-// Row-reduction GEMM: C tile rows span a cluster of CN CTAs along N.
-// Same producer / MMA roles as gemm_tc_kernel (single-CTA MMA, BN = 256, 3
-// smem stages); the epilogue warps make several passes over their TMEM
-// accumulator (writing intermediates back into TMEM with tcgen05.st) and
-// combine per-row partials of all 2*CN column-halves of the row through
-// DSMEM: every thread st.async's its partial into a slot of every CTA of the
-// cluster, which signals an mbarrier armed with the expected bytes; each CTA
-// then sums the 2*CN partials in the same fixed order, so all CTAs derive
-// bit-identical row statistics.
+// Row-reduction GEMM: C tile rows span a cluster of CN CTAs along N (one
+// 128x256 tile per CTA; CTA `rank` always owns columns [256 rank, +256), so
+// its bias / column scales / LN gamma, beta are staged in smem once).
+// Same producer / MMA roles as gemm_tc_kernel (single-CTA MMA, 3 smem
+// stages, double-buffered TMEM accumulator); 16 epilogue warps, warp (q, g)
+// owning rows [32q, 32q+32) x columns [64g, 64g+64) of the tile.  Passes over
+// the accumulator keep intermediates in TMEM (tcgen05.st).  Row statistics:
+// the 4 column-group partials of a row are combined inside the CTA (smem,
+// one warp per quadrant), the CTA partial is bulk-copied into every CTA of
+// the cluster (cp.async.bulk.shared::cluster, completion on an mbarrier armed
+// with the expected bytes), and every CTA combines the CN partials in the
+// same fixed order, so all derive bit-identical statistics.
+//   RR_LN:    x = R16(dequant(acc) + bias) + residual (R11); LN over the row
+//             (per-thread two-pass mean / M2, Chan combination); y16 = R16(LN)
+//             -> fp16 rows (TMA) [+ Q8row s8 rows + scale]
+//   RR_QUANT: y16 = R16(act(dequant(acc) + bias)) [-> fp16 rows]; Q8row s8
+//             rows + scale (the FFN-intermediate requant)
 // ========================================================================
 constexpr int kRRStages = 3;
 constexpr int kRRBN = 256;
+constexpr int kRRMaxCN = 8;
 struct RRCfg {
   static constexpr int A_BYTES = BM * BK_BYTES;
   static constexpr int B_BYTES = kRRBN * BK_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int EPI_OFF = kRRStages * STAGE_BYTES;
-  static constexpr int RED_OFF = EPI_OFF + kRREpiWarps * 2 * kRRStageTile;
-  // received partials [buf][rank<=8][half][quadrant][val<=2][32 rows]
-  static constexpr int RED_FLOATS = 2 * 8 * 2 * 4 * 2 * 32;
-  // this CTA's outgoing partials [buf][half][quadrant][val][32 rows]
-  static constexpr int LOC_OFF = RED_OFF + RED_FLOATS * 4;
-  static constexpr int LOC_FLOATS = 2 * 2 * 4 * 2 * 32;
-  static constexpr int BAR_OFF = LOC_OFF + LOC_FLOATS * 4;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static constexpr int EPI_OFF = kRRStages * STAGE_BYTES;                 // staging [warp] 2 KB
+  static constexpr int PAR_OFF = EPI_OFF + kRREpiWarps * kRRStageTile;    // [bias|sw|gamma|beta][256] fp32
+  static constexpr int LOC_OFF = PAR_OFF + 4 * kRRBN * 4;                 // [g 4][q 4][v 2][32] fp32
+  static constexpr int MYP_OFF = LOC_OFF + 4 * 4 * 2 * 32 * 4;            // [b 2][q 4][v 2][32] fp32
+  static constexpr int RED_OFF = MYP_OFF + 2 * 4 * 2 * 32 * 4;            // [b 2][rank 8][q 4][v 2][32] fp32
+  static constexpr int BAR_OFF = RED_OFF + 2 * kRRMaxCN * 4 * 2 * 32 * 4;
+  static constexpr int SMEM = BAR_OFF + 512 + 1024;
   static_assert(SMEM <= 227 * 1024, "smem budget");
 };
-
-
-template <bool I8>
-__device__ __forceinline__ float dequant1(uint32_t r, float sx, float sw, float b) {
-  return I8 ? __fmaf_rn(__int2float_rn(static_cast<int>(r)), __fmul_rn(sx, sw), b) : __fadd_rn(__uint_as_float(r), b);
-}
 
 template <bool I8, int MODE>
 __global__ void __launch_bounds__(kRRThreads, 1)
     gemm_rr_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmC, RRParams p) {
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmR,
+                   const __grid_constant__ CUtensorMap tmQ, RRParams p) {
   constexpr int STAGES = kRRStages;
   constexpr int BN = kRRBN;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * RRCfg::A_BYTES;
-  uint8_t* sEpi = smem + RRCfg::EPI_OFF;
-  float* red = reinterpret_cast<float*>(smem + RRCfg::RED_OFF);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + RRCfg::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* redbar = tempty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(redbar + 2);
+  uint64_t* resbar = redbar + 2;  // [kRREpiWarps] per-warp residual TMA loads
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(resbar + kRREpiWarps);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -542,6 +543,8 @@ __global__ void __launch_bounds__(kRRThreads, 1)
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     if (p.store16) tma_prefetch(&tmC);
+    if (MODE == RR_LN) tma_prefetch(&tmR);
+    if (p.outq) tma_prefetch(&tmQ);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -551,6 +554,7 @@ __global__ void __launch_bounds__(kRRThreads, 1)
       mbar_init(&tempty[a], kRREpiWarps);
       mbar_init(&redbar[a], 1);
     }
+    for (int w = 0; w < kRREpiWarps; ++w) mbar_init(&resbar[w], 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -559,10 +563,10 @@ __global__ void __launch_bounds__(kRRThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  cluster_sync();  // every CTA's reduction barriers exist before any st.async
+  cluster_sync();  // every CTA's reduction barriers exist before any remote copy
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  griddep_wait();  // A operand / scales come from the previous kernel
+  griddep_wait();  // A operand / scales / residual come from the previous kernel
   griddep_launch();
   constexpr int KE = I8 ? 128 : 64;
 
@@ -590,12 +594,15 @@ __global__ void __launch_bounds__(kRRThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int mt = unit; mt < p.m_tiles; mt += nunits) {
+      int lt = 0;
+      for (int mt = unit; mt < p.m_tiles; mt += nunits, ++lt) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
+        gemm_trace(p.trace, lt, 0);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&full[stage], phase);
+          if (kb == 0) gemm_trace(p.trace, lt, 1);
           tc_fence_after();
           const uint64_t adesc = make_sw128_desc(sA + stage * RRCfg::A_BYTES);
           const uint64_t bdesc = make_sw128_desc(sB + stage * RRCfg::B_BYTES);
@@ -611,6 +618,7 @@ __global__ void __launch_bounds__(kRRThreads, 1)
           }
         }
         mma_commit(&tfull[acc]);
+        gemm_trace(p.trace, lt, 2);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -619,56 +627,90 @@ __global__ void __launch_bounds__(kRRThreads, 1)
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;
-    const int q = warp & 3;
-    const int hf = ew >> 2;
-    const int c_lo = hf * (BN / 2);
-    const int rowl = q * 32 + lane;  // row within the 128-row tile
-    uint8_t* stage_buf = sEpi + ew * 2 * kRRStageTile;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    int nbuf = 0;
-    int step = 0;  // reduction step counter (selects buffer / phase)
-    const float inv_n = 1.0f / (float)p.N;
-    (void)inv_n;
-
-    // Cluster exchange of NV per-row partials: every warp stages its 32 rows'
-    // values in smem and lane 0 bulk-copies the block (NV x 128 B) into the
-    // [rank][half][quadrant] slot of every CTA of the cluster; the copies
-    // complete_tx on the destination's barrier, armed for CN x 8 warps x NV x
-    // 128 B.  Returns the buffer holding all 2*CN partials of each row.
+    const int q = warp & 3;        // TMEM lane quadrant: rows [32q, 32q+32)
+    const int g = ew >> 2;         // column group: [64g, 64g+64) of the CTA's 256
+    const int c_lo = g * 64;
+    const int ncol0 = (int)rank * BN;
+    float* par = reinterpret_cast<float*>(smem + RRCfg::PAR_OFF);
     float* loc = reinterpret_cast<float*>(smem + RRCfg::LOC_OFF);
-    auto exchange = [&](float v0, float v1, int nv) -> int {
+    float* myp = reinterpret_cast<float*>(smem + RRCfg::MYP_OFF);
+    float* red = reinterpret_cast<float*>(smem + RRCfg::RED_OFF);
+    uint8_t* stage_buf = smem + RRCfg::EPI_OFF + ew * kRRStageTile;
+    // this CTA's column parameters, once: bias, column scale, gamma, beta
+    for (int i = ew * 32 + lane; i < 4 * BN; i += 32 * kRREpiWarps) {
+      const int kind = i / BN, col = ncol0 + (i % BN);
+      const float* src = kind == 0 ? p.bias : kind == 1 ? p.col_scale : kind == 2 ? p.gamma : p.beta;
+      par[i] = (src != nullptr && col < p.N) ? __ldg(src + col) : 0.0f;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kRREpiWarps) : "memory");
+    const float* pbias = par + c_lo;
+    const float* psw = par + BN + c_lo;
+    const float* pgam = par + 2 * BN + c_lo;
+    const float* pbet = par + 3 * BN + c_lo;
+
+    int step = 0;  // exchange counter (buffer b = step & 1, phase (step >> 1) & 1)
+    // Row combine of nv per-thread values: in-CTA over the 4 column groups,
+    // then across the cluster.  STATS: (mean, M2) of 64 values each -> (mean,
+    // M2) of the full row; MAX: max.  Every thread returns the row result.
+    auto exchange = [&](float v0, float v1, bool stats, float& o0, float& o1) {
+      const int nv = stats ? 2 : 1;
       const int b = step & 1;
       const uint32_t ph = (uint32_t)(step >> 1) & 1u;
-      float* mine = loc + (((b * 2 + hf) * 4 + q) * 2) * 32;
-      mine[lane] = v0;
-      if (nv > 1) mine[32 + lane] = v1;
-      fence_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        if (threadIdx.x == 128) mbar_expect_tx(&redbar[b], (uint32_t)(CN * kRREpiWarps * nv * 128));
-        const uint32_t dst = smem_u32(red + ((((b * 8 + (int)rank) * 2 + hf) * 4 + q) * 2) * 32);
-        const uint32_t bl = smem_u32(&redbar[b]);
-        for (int c = 0; c < CN; ++c) bulk_copy_s2c(mapa_shared(dst, c), mine, nv * 128, mapa_shared(bl, c));
+      loc[((g * 4 + q) * 2 + 0) * 32 + lane] = v0;
+      if (stats) loc[((g * 4 + q) * 2 + 1) * 32 + lane] = v1;
+      asm volatile("bar.sync %0, 128;" ::"r"(2 + q) : "memory");
+      if (g == 0) {
+        float r0, r1 = 0.0f;
+        const float a0 = loc[((0 * 4 + q) * 2) * 32 + lane], a1 = loc[((1 * 4 + q) * 2) * 32 + lane];
+        const float a2 = loc[((2 * 4 + q) * 2) * 32 + lane], a3 = loc[((3 * 4 + q) * 2) * 32 + lane];
+        if (stats) {
+          r0 = ((a0 + a1) + (a2 + a3)) * 0.25f;
+          const float d0 = a0 - r0, d1 = a1 - r0, d2 = a2 - r0, d3 = a3 - r0;
+          const float m0 = loc[((0 * 4 + q) * 2 + 1) * 32 + lane], m1 = loc[((1 * 4 + q) * 2 + 1) * 32 + lane];
+          const float m2 = loc[((2 * 4 + q) * 2 + 1) * 32 + lane], m3 = loc[((3 * 4 + q) * 2 + 1) * 32 + lane];
+          r1 = ((m0 + m1) + (m2 + m3)) + 64.0f * ((d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3));
+        } else {
+          r0 = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
+        }
+        float* mine = myp + ((b * 4 + q) * 2) * 32;
+        mine[lane] = r0;
+        if (stats) mine[32 + lane] = r1;
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (q == 0) mbar_expect_tx(&redbar[b], (uint32_t)(CN * 4 * nv * 128));
+          const uint32_t dst = smem_u32(red + (((b * kRRMaxCN + (int)rank) * 4 + q) * 2) * 32);
+          const uint32_t bl = smem_u32(&redbar[b]);
+          for (int c = 0; c < CN; ++c) bulk_copy_s2c(mapa_shared(dst, c), mine, nv * 128, mapa_shared(bl, c));
+        }
       }
       mbar_wait(&redbar[b], ph);
       ++step;
-      return b;
+      if (stats) {
+        float msum = 0.0f;
+        for (int c = 0; c < CN; ++c) msum += red[(((b * kRRMaxCN + c) * 4 + q) * 2) * 32 + lane];
+        const float mean = msum / (float)CN;
+        float m2 = 0.0f, dd = 0.0f;
+        for (int c = 0; c < CN; ++c) {
+          const float* rc = red + (((b * kRRMaxCN + c) * 4 + q) * 2) * 32;
+          const float dm = rc[lane] - mean;
+          m2 += rc[32 + lane];
+          dd = __fmaf_rn(dm, dm, dd);
+        }
+        o0 = mean;
+        o1 = m2 + (float)BN * dd;
+      } else {
+        float mx = 0.0f;
+        for (int c = 0; c < CN; ++c) mx = fmaxf(mx, red[(((b * kRRMaxCN + c) * 4 + q) * 2) * 32 + lane]);
+        o0 = mx;
+        o1 = 0.0f;
+      }
     };
-    auto partial = [&](int b, int c, int h2, int v) -> float {
-      return red[((((b * 8 + c) * 2 + h2) * 4 + q) * 2 + v) * 32 + lane];
-    };
-    auto reduce_max = [&](float v) -> float {
-      const int b = exchange(v, 0.0f, 1);
-      float r = 0.0f;
-      for (int c = 0; c < CN; ++c) r = fmaxf(r, fmaxf(partial(b, c, 0, 0), partial(b, c, 1, 0)));
-      return r;
-    };
+    // fp16 staging + TMA store of a 32-row x 32-column block (64B swizzle)
     auto store16 = [&](const uint32_t (&h)[16], int n0, int row0) {
-      uint8_t* buf = stage_buf + (nbuf & 1) * kRRStageTile;
-      if (lane == 0) bulk_wait_read<1>();
+      if (lane == 0) bulk_wait_read<0>();
       __syncwarp();
-      uint8_t* srow = buf + lane * 64;
+      uint8_t* srow = stage_buf + lane * 64;
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) {
         const int pc = cc ^ ((lane >> 1) & 3);
@@ -677,162 +719,185 @@ __global__ void __launch_bounds__(kRRThreads, 1)
       fence_async_smem();
       __syncwarp();
       if (lane == 0) {
-        tma_store_2d(&tmC, buf, n0, row0);
+        tma_store_2d(&tmC, stage_buf, n0, row0);
         bulk_commit();
       }
-      ++nbuf;
     };
 
-    for (int mt = unit; mt < p.m_tiles; mt += nunits) {
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int lt = 0;
+    uint32_t rphase = 0;  // resbar[ew] phase
+    const bool tr0 = ew == 0 && lane == 0;
+    for (int mt = unit; mt < p.m_tiles; mt += nunits, ++lt) {
       const int row0 = mt * BM + q * 32;
       const int row = row0 + lane;
       const bool row_ok = row < p.M;
       const float sx = (I8 && row_ok) ? p.row_scale[row] : 0.0f;
+      const float2 sx2 = make_float2(sx, sx);
+      if (MODE == RR_LN) {
+        // residual of the NEXT tile -> L2 (its TMA loads then hit L2, not
+        // HBM); this thread's 128 bytes of its row = one line
+        const int nrow = row + nunits * BM;
+        if (nrow < p.M) prefetch_l2(p.residual + (size_t)nrow * p.ldr + ncol0 + c_lo);
+        if (mt == unit && row_ok) prefetch_l2(p.residual + (size_t)row * p.ldr + ncol0 + c_lo);
+        // residual block of chunk 0 -> the warp's staging buffer, in flight
+        // while the accumulator is still being computed
+        if (lane == 0) {
+          bulk_wait_read<0>();  // the staging buffer's previous store has been read
+          mbar_expect_tx(&resbar[ew], 32 * 64);
+          tma_load_2d(stage_buf, &tmR, &resbar[ew], ncol0 + c_lo, row0, kEvictFirst);
+        }
+      }
       mbar_wait(&tfull[acc], acc_phase);
+      if (tr0) gemm_trace(p.trace, lt, 3);
       tc_fence_after();
-      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-      const int ncol0 = (int)rank * BN;
-      float amax = 0.0f;
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c_lo;
+      __half2 amax2 = __float2half2_rn(0.0f);
 
       if (MODE == RR_LN) {
-        // pass 1: x = R16(GEMM epilogue) + residual (R11); sum; x -> TMEM
-        float psum = 0.0f;
-        const __half* rrow = p.residual + (size_t)(row_ok ? row : 0) * p.ldr + ncol0;
-        uint4 rv[4];  // residual of the current chunk, prefetched one chunk ahead
-#pragma unroll
-        for (int i = 0; i < 4; ++i) rv[i] = __ldg(reinterpret_cast<const uint4*>(rrow + c_lo) + i);
+        // pass 1: x = R16(dequant + bias) + residual -> TMEM (in place); sum.
+        // The residual block (32 rows x 32 columns fp16) arrives by TMA in
+        // the warp's staging buffer (64B swizzle); each thread reads its row.
+        float2 s2 = make_float2(0.0f, 0.0f);
 #pragma unroll 1
-        for (int c = c_lo; c < c_lo + BN / 2; c += 32) {
-          const int n0 = ncol0 + c;
-          float bias[32], sw[32];
-          load32(bias, p.bias, n0, p.N);
-          if (I8) load32(sw, p.col_scale, n0, p.N);
+        for (int ch = 0; ch < 2; ++ch) {
           uint32_t r[32];
-          tmem_ld32(tbase + c, r);
+          tmem_ld32(tbase + ch * 32, r);
+          mbar_wait(&resbar[ew], (uint32_t)(rphase & 1));
+          ++rphase;
+          uint4 rv[4];
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc)
+            rv[cc] = *reinterpret_cast<const uint4*>(stage_buf + lane * 64 + ((cc ^ ((lane >> 1) & 3)) << 4));
+          __syncwarp();  // every lane has read the block before it is reused
+          if (ch == 0 && lane == 0) {  // chunk 1's residual block, overlapping chunk 0's math
+            mbar_expect_tx(&resbar[ew], 32 * 64);
+            tma_load_2d(stage_buf, &tmR, &resbar[ew], ncol0 + c_lo + 32, row0, kEvictFirst);
+          }
           tmem_wait_ld();
-          const uint4 rcur[4] = {rv[0], rv[1], rv[2], rv[3]};
-          if (c + 32 < c_lo + BN / 2) {
+          const __half2* rh = reinterpret_cast<const __half2*>(rv);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) rv[i] = __ldg(reinterpret_cast<const uint4*>(rrow + c + 32) + i);
+          for (int e = 0; e < 16; ++e) {
+            const int j = ch * 32 + 2 * e;
+            const float2 bb = *reinterpret_cast<const float2*>(pbias + j);
+            float2 y;
+            if (I8) {
+              const float2 a = make_float2(__int2float_rn(static_cast<int>(r[2 * e])),
+                                           __int2float_rn(static_cast<int>(r[2 * e + 1])));
+              y = fma2(a, mul2(sx2, *reinterpret_cast<const float2*>(psw + j)), bb);
+            } else {
+              y = add2(make_float2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])), bb);
+            }
+            const float2 y16 = __half22float2(__floats2half2_rn(y.x, y.y));
+            const float2 x = add2(y16, __half22float2(rh[e]));
+            s2 = add2(s2, x);
+            r[2 * e] = __float_as_uint(x.x);
+            r[2 * e + 1] = __float_as_uint(x.y);
           }
-          const __half2* rh = reinterpret_cast<const __half2*>(rcur);
-#pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            const float2 res = __half22float2(rh[j / 2]);
-            const float y0 = __half2float(__float2half_rn(dequant1<I8>(r[j], sx, sw[j], bias[j])));
-            const float y1 = __half2float(__float2half_rn(dequant1<I8>(r[j + 1], sx, sw[j + 1], bias[j + 1])));
-            const float x0 = __fadd_rn(y0, row_ok ? res.x : 0.0f), x1 = __fadd_rn(y1, row_ok ? res.y : 0.0f);
-            psum += x0;
-            psum += x1;
-            r[j] = __float_as_uint(x0);
-            r[j + 1] = __float_as_uint(x1);
-          }
-          tmem_st32(tbase + c, r);
+          tmem_st32(tbase + ch * 32, r);
         }
         tmem_wait_st();
-        // pass 2: this thread's 128 values, two-pass about their own mean
-        const float mean_t = psum * (1.0f / (BN / 2));
-        float m2_t = 0.0f;
+        const float mean_t = (s2.x + s2.y) * (1.0f / 64.0f);
+        const float2 mt2 = make_float2(mean_t, mean_t);
+        float2 q2 = make_float2(0.0f, 0.0f);
 #pragma unroll 1
-        for (int c = c_lo; c < c_lo + BN / 2; c += 32) {
+        for (int ch = 0; ch < 2; ++ch) {
           uint32_t r[32];
-          tmem_ld32(tbase + c, r);
+          tmem_ld32(tbase + ch * 32, r);
           tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float dlt = __uint_as_float(r[j]) - mean_t;
-            m2_t = __fmaf_rn(dlt, dlt, m2_t);
+          for (int e = 0; e < 16; ++e) {
+            const float2 d = sub2(make_float2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])), mt2);
+            q2 = fma2(d, d, q2);
           }
         }
-        // one cluster exchange of (mean_t, M2_t); Chan's parallel combination in
-        // a fixed order: mean = avg(mean_i), M2 = sum M2_i + n sum (mean_i - mean)^2
-        const int b = exchange(mean_t, m2_t, 2);
-        float msum = 0.0f;
-        for (int c = 0; c < CN; ++c) msum += partial(b, c, 0, 0) + partial(b, c, 1, 0);
-        const float mean = __fdiv_rn(msum, (float)(2 * CN));
-        float m2 = 0.0f;
-        for (int c = 0; c < CN; ++c)
-#pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2) {
-            const float dm = partial(b, c, h2, 0) - mean;
-            m2 += partial(b, c, h2, 1) + (float)(BN / 2) * dm * dm;
-          }
+        float mean, m2;
+        if (tr0) gemm_trace(p.trace, lt, 8);
+        exchange(mean_t, q2.x + q2.y, true, mean, m2);
+        if (tr0) gemm_trace(p.trace, lt, 9);
         const float var = __fdiv_rn(m2, (float)p.N);
         const float rstd = 1.0f / sqrtf(var + p.eps);
-        // pass 3: y = (x - mean) * rstd * g + b -> R16 -> fp16 store (+ packed y16 -> TMEM)
+        const float2 mean2 = make_float2(mean, mean), rstd2 = make_float2(rstd, rstd);
+        // pass 2: y16 = R16((x - mean) * rstd * gamma + beta) -> fp16 store, amax, packed -> TMEM
 #pragma unroll 1
-        for (int c = c_lo; c < c_lo + BN / 2; c += 32) {
-          const int n0 = ncol0 + c;
-          float g[32], bt[32];
-          load32(g, p.gamma, n0, p.N);
-          load32(bt, p.beta, n0, p.N);
+        for (int ch = 0; ch < 2; ++ch) {
           uint32_t r[32];
-          tmem_ld32(tbase + c, r);
+          tmem_ld32(tbase + ch * 32, r);
           tmem_wait_ld();
           uint32_t h[16];
 #pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            const float a0 = (__uint_as_float(r[j]) - mean) * rstd * g[j] + bt[j];
-            const float a1 = (__uint_as_float(r[j + 1]) - mean) * rstd * g[j + 1] + bt[j + 1];
-            const __half2 hh = __floats2half2_rn(a0, a1);
-            const float2 hf2 = __half22float2(hh);
-            amax = fmaxf(amax, fmaxf(fabsf(hf2.x), fabsf(hf2.y)));
-            h[j / 2] = *reinterpret_cast<const uint32_t*>(&hh);
+          for (int e = 0; e < 16; ++e) {
+            const int j = ch * 32 + 2 * e;
+            const float2 d = sub2(make_float2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])), mean2);
+            const float2 y = fma2(mul2(d, rstd2), *reinterpret_cast<const float2*>(pgam + j),
+                                  *reinterpret_cast<const float2*>(pbet + j));
+            const __half2 hh = __floats2half2_rn(y.x, y.y);
+            amax2 = __hmax2(amax2, __habs2(hh));
+            h[e] = *reinterpret_cast<const uint32_t*>(&hh);
           }
-          if (p.outq) tmem_st16(tbase + c, h);
-          if (p.store16) store16(h, n0, row0);
+          if (p.outq) tmem_st16(tbase + ch * 32, h);
+          if (p.store16) store16(h, ncol0 + c_lo + ch * 32, row0);
         }
         if (p.outq) tmem_wait_st();
-      } else {  // RR_QUANT: y16 = R16(act(GEMM epilogue)); amax; packed y16 -> TMEM
+      } else {  // RR_QUANT: y16 = R16(act(dequant + bias)); amax; packed y16 -> TMEM
 #pragma unroll 1
-        for (int c = c_lo; c < c_lo + BN / 2; c += 32) {
-          const int n0 = ncol0 + c;
-          float bias[32], sw[32];
-          load32(bias, p.bias, n0, p.N);
-          if (I8) load32(sw, p.col_scale, n0, p.N);
-          uint32_t r[32];
-          tmem_ld32(tbase + c, r);
+        for (int ch = 0; ch < 2; ++ch) {
+          uint32_t r[2][16];
+          tmem_ld16(tbase + ch * 32, r[0]);
+          tmem_ld16(tbase + ch * 32 + 16, r[1]);
           tmem_wait_ld();
           uint32_t h[16];
           switch (p.act) {
-            case ACT_GELU: epi_chunk<I8, ACT_GELU>(r, bias, sw, sx, h); break;
-            case ACT_RELU: epi_chunk<I8, ACT_RELU>(r, bias, sw, sx, h); break;
-            case ACT_GELU_TANH: epi_chunk<I8, ACT_GELU_TANH>(r, bias, sw, sx, h); break;
-            default: epi_chunk<I8, ACT_NONE>(r, bias, sw, sx, h); break;
+            case ACT_GELU: epi32<I8, ACT_GELU>(r, pbias + ch * 32, psw + ch * 32, sx, h); break;
+            case ACT_RELU: epi32<I8, ACT_RELU>(r, pbias + ch * 32, psw + ch * 32, sx, h); break;
+            case ACT_GELU_TANH: epi32<I8, ACT_GELU_TANH>(r, pbias + ch * 32, psw + ch * 32, sx, h); break;
+            default: epi32<I8, ACT_NONE>(r, pbias + ch * 32, psw + ch * 32, sx, h); break;
           }
-          __half2 am2 = __float2half2_rn(0.0f);
 #pragma unroll
-          for (int e = 0; e < 16; ++e) am2 = __hmax2(am2, __habs2(*reinterpret_cast<const __half2*>(&h[e])));
-          amax = fmaxf(amax, fmaxf(__low2float(am2), __high2float(am2)));
-          tmem_st16(tbase + c, h);
-          if (p.store16) store16(h, n0, row0);
+          for (int e = 0; e < 16; ++e) amax2 = __hmax2(amax2, __habs2(*reinterpret_cast<const __half2*>(&h[e])));
+          tmem_st16(tbase + ch * 32, h);
+          if (p.store16) store16(h, ncol0 + c_lo + ch * 32, row0);
         }
         tmem_wait_st();
       }
 
+      if (tr0) gemm_trace(p.trace, lt, 10);
       if (p.outq) {
-        // Q8row over the whole row (R6-R8, R12): quantize the fp16-rounded values
-        const float rmax = reduce_max(amax);
+        // Q8row over the whole row (R6-R8, R12) from the fp16-rounded values
+        float rmax, unused;
+        exchange(fmaxf(__low2float(amax2), __high2float(amax2)), 0.0f, false, rmax, unused);
+        if (tr0) gemm_trace(p.trace, lt, 11);
         const float sc = q8_scale(rmax);
         const float rs = __frcp_rn(sc);
 #pragma unroll 1
-        for (int c = c_lo; c < c_lo + BN / 2; c += 32) {
+        for (int ch = 0; ch < 2; ++ch) {
           uint32_t h[16];
-          tmem_ld16(tbase + c, h);
+          tmem_ld16(tbase + ch * 32, h);
           tmem_wait_ld();
           uint32_t o[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e)
             o[e] = q8_quant4(__half22float2(*reinterpret_cast<const __half2*>(&h[2 * e])),
                              __half22float2(*reinterpret_cast<const __half2*>(&h[2 * e + 1])), sc, rs);
-          if (row_ok) {
-            uint4* dst = reinterpret_cast<uint4*>(p.outq + (size_t)row * p.ldq + ncol0 + c);
-            dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
-            dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+          // s8 block 32 rows x 32 B through the staging buffer (32B swizzle) + TMA store
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc)
+            *reinterpret_cast<uint4*>(stage_buf + lane * 32 + ((cc ^ ((lane >> 2) & 1)) << 4)) =
+                make_uint4(o[4 * cc], o[4 * cc + 1], o[4 * cc + 2], o[4 * cc + 3]);
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmQ, stage_buf, ncol0 + c_lo + ch * 32, row0);
+            bulk_commit();
           }
+          if (tr0) gemm_trace(p.trace, lt, 12 + ch);
         }
-        if (rank == 0 && hf == 0 && row_ok) p.out_scale[row] = sc;
+        if (rank == 0 && g == 0 && row_ok) p.out_scale[row] = sc;
       }
+      if (tr0) gemm_trace(p.trace, lt, 5);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -845,7 +910,7 @@ __global__ void __launch_bounds__(kRRThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  cluster_sync();  // no CTA leaves while a peer may still st.async into it
+  cluster_sync();  // no CTA leaves while a peer may still copy into it
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 2 * BN);
@@ -1022,6 +1087,18 @@ bool plan_rr(RRPlan* g, bool i8, const void* A, int M_rows, int lda, const void*
   return true;
 }
 
+bool plan_rr_io(RRPlan* g, const void* residual, int ldr, void* outq, int ldq, const char** err) {
+  if (residual != nullptr &&
+      !encode_2d(&g->tmR, const_cast<void*>(residual), g->M_rows, g->p.N, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                 (size_t)ldr * 2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B, err))
+    return false;
+  if (outq != nullptr &&
+      !encode_2d(&g->tmQ, outq, g->M_rows, g->p.N, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, (size_t)ldq, 32, 32,
+                 CU_TENSOR_MAP_SWIZZLE_32B, err))
+    return false;
+  return true;
+}
+
 template <bool I8, int MODE>
 static int rr_max_clusters_t(int cn) {
   cudaLaunchConfig_t cfg = {};
@@ -1066,7 +1143,7 @@ void plan_rr_set_m(RRPlan* g, int M) {
 template <bool I8, int MODE>
 static cudaError_t launch_rr_t(const RRPlan& g, cudaStream_t s) {
   return launch_ex(gemm_rr_kernel<I8, MODE>, dim3(g.grid), dim3(kRRThreads), RRCfg::SMEM, s, g.cn, g.tmA, g.tmB,
-                   g.tmC, g.p);
+                   g.tmC, g.tmR, g.tmQ, g.p);
 }
 
 template <bool I8, int MODE>

@@ -46,6 +46,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // ---------------------------------------------------------------------- TMA
+// Prefetch the cache line holding addr into L2.
+__device__ __forceinline__ void prefetch_l2(const void* addr) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(addr));
+}
 // Bulk prefetch of [addr, addr + bytes) into L2 (bytes: multiple of 16).
 __device__ __forceinline__ void bulk_prefetch_l2(const void* addr, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(addr), "r"(bytes) : "memory");

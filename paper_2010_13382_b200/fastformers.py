@@ -78,7 +78,7 @@ def lib():
         L.ff_debug_quant_rows.argtypes = [vp, i32, i32, i32, vp, i32, vp, vp]
         L.ff_debug_attention.argtypes = [vp, vp, i32, i32, i32, i32, vp, i32, vp]
         L.ff_debug_attention_q8.argtypes = [vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp]
-        L.ff_debug_set_trace.argtypes = [vp]
+        L.ff_debug_set_trace.argtypes = [vp, i32]
         for name in EXPORTED:
             if name not in ("ff_abi_version", "ff_last_error", "ff_model_destroy"):
                 getattr(L, name).restype = i32
@@ -263,7 +263,8 @@ def attention_q8(qkv16, mask, A, d, with_ctx16=True, trace=None):
     return ctx, q, s
 
 
-def set_gemm_trace(trace=None):
-    """Debug: record per-tile timestamps of subsequent debug GEMMs into `trace`
-    (zeroed int64 CUDA tensor [grid, 64, 8]); None switches it off."""
-    check(lib().ff_debug_set_trace(_ptr(trace) if trace is not None else None))
+def set_gemm_trace(trace=None, which=0):
+    """Debug: record per-tile timestamps into `trace` (zeroed int64 CUDA tensor
+    [grid, 64, 24]) — which = 0: subsequent debug GEMMs; 1/2/3: the layer-0
+    fused out-proj+LN / FFN1+requant / FFN2+LN of subsequent forwards."""
+    check(lib().ff_debug_set_trace(_ptr(trace) if trace is not None else None, which))
