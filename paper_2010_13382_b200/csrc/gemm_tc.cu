@@ -755,12 +755,20 @@ __global__ void __launch_bounds__(kRRThreads, 1)
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c_lo;
       __half2 amax2 = __float2half2_rn(0.0f);
 
+      // TMEM reads are the scarce resource here (64 B/clk/SM: every pass over
+      // the 128 KB accumulator costs ~1 us): the accumulator is read once,
+      // x is written back (tcgen05.st, 4x faster than reads) and read once
+      // more for the LN pass; the packed fp16 results stay in registers
+      // across the amax exchange.
+      uint32_t hq[32];  // this thread's 64 output values, packed fp16 (Q8row input)
       if (MODE == RR_LN) {
-        // pass 1: x = R16(dequant + bias) + residual -> TMEM (in place); sum.
-        // The residual block (32 rows x 32 columns fp16) arrives by TMA in
-        // the warp's staging buffer (64B swizzle); each thread reads its row.
-        float2 s2 = make_float2(0.0f, 0.0f);
-#pragma unroll 1
+        // pass 1: x = R16(dequant + bias) + residual (registers); shifted
+        // sums (shift = the thread's first x) for the local mean / M2.  The
+        // residual block (32 rows x 32 columns fp16) arrives by TMA in the
+        // warp's staging buffer (64B swizzle); each thread reads its row.
+        float2 sd = make_float2(0.0f, 0.0f), sq = make_float2(0.0f, 0.0f);
+        float2 shift = make_float2(0.0f, 0.0f);
+#pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
           uint32_t r[32];
           tmem_ld32(tbase + ch * 32, r);
@@ -791,41 +799,37 @@ __global__ void __launch_bounds__(kRRThreads, 1)
             }
             const float2 y16 = __half22float2(__floats2half2_rn(y.x, y.y));
             const float2 x = add2(y16, __half22float2(rh[e]));
-            s2 = add2(s2, x);
+            if (ch == 0 && e == 0) shift = make_float2(x.x, x.x);
+            const float2 d = sub2(x, shift);
+            sd = add2(sd, d);
+            sq = fma2(d, d, sq);
             r[2 * e] = __float_as_uint(x.x);
             r[2 * e + 1] = __float_as_uint(x.y);
           }
-          tmem_st32(tbase + ch * 32, r);
+          tmem_st32(tbase + ch * 32, r);  // x replaces the accumulator columns
         }
         tmem_wait_st();
-        const float mean_t = (s2.x + s2.y) * (1.0f / 64.0f);
-        const float2 mt2 = make_float2(mean_t, mean_t);
-        float2 q2 = make_float2(0.0f, 0.0f);
-#pragma unroll 1
-        for (int ch = 0; ch < 2; ++ch) {
-          uint32_t r[32];
-          tmem_ld32(tbase + ch * 32, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const float2 d = sub2(make_float2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])), mt2);
-            q2 = fma2(d, d, q2);
-          }
-        }
+        const float sdt = sd.x + sd.y;
+        const float mean_t = shift.x + sdt * (1.0f / 64.0f);
+        const float m2_t = fmaxf((sq.x + sq.y) - sdt * sdt * (1.0f / 64.0f), 0.0f);
         float mean, m2;
         if (tr0) gemm_trace(p.trace, lt, 8);
-        exchange(mean_t, q2.x + q2.y, true, mean, m2);
+        exchange(mean_t, m2_t, true, mean, m2);
         if (tr0) gemm_trace(p.trace, lt, 9);
         const float var = __fdiv_rn(m2, (float)p.N);
         const float rstd = 1.0f / sqrtf(var + p.eps);
         const float2 mean2 = make_float2(mean, mean), rstd2 = make_float2(rstd, rstd);
-        // pass 2: y16 = R16((x - mean) * rstd * gamma + beta) -> fp16 store, amax, packed -> TMEM
-#pragma unroll 1
+        // pass 2: y16 = R16((x - mean) * rstd * gamma + beta) -> fp16 store, amax
+#pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
           uint32_t r[32];
           tmem_ld32(tbase + ch * 32, r);
           tmem_wait_ld();
-          uint32_t h[16];
+          if (ch == 1) {  // the accumulator columns have been read for the last time
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+          }
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
             const int j = ch * 32 + 2 * e;
@@ -834,19 +838,27 @@ __global__ void __launch_bounds__(kRRThreads, 1)
                                   *reinterpret_cast<const float2*>(pbet + j));
             const __half2 hh = __floats2half2_rn(y.x, y.y);
             amax2 = __hmax2(amax2, __habs2(hh));
-            h[e] = *reinterpret_cast<const uint32_t*>(&hh);
+            hq[ch * 16 + e] = *reinterpret_cast<const uint32_t*>(&hh);
           }
-          if (p.outq) tmem_st16(tbase + ch * 32, h);
-          if (p.store16) store16(h, ncol0 + c_lo + ch * 32, row0);
+          if (p.store16) {
+            uint32_t h[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) h[e] = hq[ch * 16 + e];
+            store16(h, ncol0 + c_lo + ch * 32, row0);
+          }
         }
-        if (p.outq) tmem_wait_st();
-      } else {  // RR_QUANT: y16 = R16(act(dequant + bias)); amax; packed y16 -> TMEM
-#pragma unroll 1
+      } else {  // RR_QUANT: y16 = R16(act(dequant + bias)) (registers); amax
+#pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
           uint32_t r[2][16];
           tmem_ld16(tbase + ch * 32, r[0]);
           tmem_ld16(tbase + ch * 32 + 16, r[1]);
           tmem_wait_ld();
+          if (ch == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+          }
           uint32_t h[16];
           switch (p.act) {
             case ACT_GELU: epi32<I8, ACT_GELU>(r, pbias + ch * 32, psw + ch * 32, sx, h); break;
@@ -855,11 +867,12 @@ __global__ void __launch_bounds__(kRRThreads, 1)
             default: epi32<I8, ACT_NONE>(r, pbias + ch * 32, psw + ch * 32, sx, h); break;
           }
 #pragma unroll
-          for (int e = 0; e < 16; ++e) amax2 = __hmax2(amax2, __habs2(*reinterpret_cast<const __half2*>(&h[e])));
-          tmem_st16(tbase + ch * 32, h);
+          for (int e = 0; e < 16; ++e) {
+            amax2 = __hmax2(amax2, __habs2(*reinterpret_cast<const __half2*>(&h[e])));
+            hq[ch * 16 + e] = h[e];
+          }
           if (p.store16) store16(h, ncol0 + c_lo + ch * 32, row0);
         }
-        tmem_wait_st();
       }
 
       if (tr0) gemm_trace(p.trace, lt, 10);
@@ -870,16 +883,13 @@ __global__ void __launch_bounds__(kRRThreads, 1)
         if (tr0) gemm_trace(p.trace, lt, 11);
         const float sc = q8_scale(rmax);
         const float rs = __frcp_rn(sc);
-#pragma unroll 1
+#pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
-          uint32_t h[16];
-          tmem_ld16(tbase + ch * 32, h);
-          tmem_wait_ld();
           uint32_t o[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e)
-            o[e] = q8_quant4(__half22float2(*reinterpret_cast<const __half2*>(&h[2 * e])),
-                             __half22float2(*reinterpret_cast<const __half2*>(&h[2 * e + 1])), sc, rs);
+            o[e] = q8_quant4(__half22float2(*reinterpret_cast<const __half2*>(&hq[ch * 16 + 2 * e])),
+                             __half22float2(*reinterpret_cast<const __half2*>(&hq[ch * 16 + 2 * e + 1])), sc, rs);
           // s8 block 32 rows x 32 B through the staging buffer (32B swizzle) + TMA store
           if (lane == 0) bulk_wait_read<0>();
           __syncwarp();
@@ -898,9 +908,6 @@ __global__ void __launch_bounds__(kRRThreads, 1)
         if (rank == 0 && g == 0 && row_ok) p.out_scale[row] = sc;
       }
       if (tr0) gemm_trace(p.trace, lt, 5);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -967,6 +974,7 @@ bool make_operand_map(CUtensorMap* map, const void* base, int rows, int cols, in
 }
 
 static int pick_bn(int N) {
+  // (measured: 128-column tiles for the N = 768 / 1536 GEMMs of C3 are 6-15% slower)
   // Fewer wasted columns wins; ties prefer the wider tile (less A re-reading).
   const int w256 = ((N + 255) / 256) * 256 - N;
   const int w128 = ((N + 127) / 128) * 128 - N;
