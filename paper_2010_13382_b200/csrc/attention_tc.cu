@@ -37,11 +37,7 @@ constexpr int kD = 64;              // head_dim
 constexpr int kMaxHeads = 8;        // heads per item
 constexpr int kTileBytes = 128 * 128;  // 128 rows x 128 B (64 fp16)
 constexpr int kKVStages = 3;
-constexpr int kSoftmaxWarps = 16;
-constexpr int kSplit = kSoftmaxWarps / 4;  // softmax warps per TMEM lane quadrant (same rows)
-constexpr int kKW = kKeys / kSplit;        // keys per warp (32)
-constexpr int kOW = kD / kSplit;           // O / ctx columns per warp (16)
-static_assert(kSplit == 4, "the row-sum combine below is written for 4 parts");
+constexpr int kSoftmaxWarps = 8;
 constexpr int kThreadsTC = 64 + 32 * kSoftmaxWarps;
 constexpr uint32_t kTmemO = 128;    // O[2]: columns [128, 192), [192, 256)
 constexpr uint32_t kTmemCtx = 256;  // packed ctx [256, 256 + 32 * heads)
@@ -50,8 +46,8 @@ struct SmemTC {
   static constexpr int SLOT = 3 * kTileBytes;                // Q, K, V of one head
   static constexpr int P = kKVStages * SLOT;                 // P[2]: 2 k-blocks of 64 keys, 128B-swizzled
   static constexpr int MASK = P + 2 * 2 * kTileBytes;        // kKeys floats
-  static constexpr int RED = MASK + kKeys * 4;               // [3][kSplit][128] floats: max, sum, amax
-  static constexpr int BAR = RED + 3 * kSplit * kQ * 4;
+  static constexpr int RED = MASK + kKeys * 4;               // [3][2][128] floats: max, sum, amax
+  static constexpr int BAR = RED + 3 * 2 * kQ * 4;
   static constexpr int TOTAL = BAR + 256 + 1024;             // barriers + alignment slack
   static_assert(TOTAL <= 227 * 1024, "smem budget");
 };
@@ -82,7 +78,7 @@ __device__ __forceinline__ void trace_ev(unsigned long long* trace, uint32_t n, 
     trace[((size_t)blockIdx.x * kTraceHeads + n) * 8 + e] = t;
   }
 }
-__device__ __forceinline__ void softmax_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kSoftmaxWarps) : "memory"); }
+__device__ __forceinline__ void softmax_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 // Walk of the heads one CTA processes: items blockIdx.x, +gridDim.x, ...;
 // each item = (sequence b, heads [h0, h0 + nh)).
@@ -237,19 +233,19 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       if (n > 0) issue_pv(n - 1);
     }
   } else {
-    const int q = warp & 3;            // TMEM lane quadrant
-    const int part = (warp - 2) >> 2;  // keys [kKW part, +kKW), O columns [kOW part, +kOW)
+    const int q = warp & 3;             // TMEM lane quadrant
+    const int half = (warp - 2) >> 2;   // keys [64 half, 64 half + 64), O columns [32 half, 32 half + 32)
     const int r = q * 32 + lane;
     const int tid = threadIdx.x - 64;
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
     float* redMax = sRed;
-    float* redSum = sRed + kSplit * kQ;
-    float* redAmax = sRed + 2 * kSplit * kQ;
+    float* redSum = sRed + 2 * kQ;
+    float* redAmax = sRed + 4 * kQ;
     const float sl2 = scale * 1.4426950408889634f;
     const bool fuse_q = ctxq != nullptr;
-    // the kSplit warps sharing TMEM lane quadrant q (same rows, other keys)
-    const int group_bar = 2 + q;
-    auto group_sync = [group_bar]() { asm volatile("bar.sync %0, %1;" ::"r"(group_bar), "n"(32 * kSplit) : "memory"); };
+    // the two warps sharing TMEM lane quadrant q (same rows, other key half)
+    const int pair_bar = 2 + q;
+    auto pair_sync = [pair_bar]() { asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory"); };
     __half2 amax2 = __float2half2_rn(0.0f);  // |ctx| max of the row over the heads epilogued so far
 
     // ctx epilogue of head m = head h of sequence b (local index hl): R16(O),
@@ -260,33 +256,31 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       mbar_wait(o_full + os, (m >> 1) & 1);
       if (threadIdx.x == 64) trace_ev(trace, m, 6);
       tc_fence_after();
-      uint32_t o[kOW];
-      tmem_ld16(trow + kTmemO + os * kD + part * kOW, o);
+      uint32_t o[32];
+      tmem_ld32(trow + kTmemO + os * kD + half * 32, o);
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(o_empty + os);
-      uint32_t pk[kOW / 2];
+      uint32_t pk[16];
 #pragma unroll
-      for (int i = 0; i < kOW / 2; ++i) {
+      for (int i = 0; i < 16; ++i) {
         pk[i] = pack_half2(__uint_as_float(o[2 * i]), __uint_as_float(o[2 * i + 1]));
         amax2 = __hmax2(amax2, __habs2(*reinterpret_cast<const __half2*>(&pk[i])));
       }
       if (ctx != nullptr && r < S) {
-        uint4* dst = reinterpret_cast<uint4*>(ctx + grow * ldc + h * kD + part * kOW);
+        uint4* dst = reinterpret_cast<uint4*>(ctx + grow * ldc + h * kD + half * 32);
 #pragma unroll
-        for (int c = 0; c < kOW / 8; ++c) dst[c] = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        for (int c = 0; c < 4; ++c) dst[c] = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
       }
       if (!fuse_q) return;
-      tmem_st8(trow + kTmemCtx + hl * 32 + part * (kOW / 2), pk);
+      tmem_st16(trow + kTmemCtx + hl * 32 + half * 16, pk);
       if (!last) return;
-      // Q8row of the whole ctx row (R6-R8): amax over the kSplit parts, then
+      // Q8row of the whole ctx row (R6-R8): amax over both halves, then
       // quantize the parked fp16 values
       tmem_wait_st();
-      redAmax[part * kQ + r] = fmaxf(__low2float(amax2), __high2float(amax2));
-      group_sync();
-      float am = redAmax[r];
-#pragma unroll
-      for (int pp = 1; pp < kSplit; ++pp) am = fmaxf(am, redAmax[pp * kQ + r]);
+      redAmax[half * kQ + r] = fmaxf(__low2float(amax2), __high2float(amax2));
+      pair_sync();
+      const float am = fmaxf(redAmax[r], redAmax[kQ + r]);
       amax2 = __float2half2_rn(0.0f);
       const float sc = q8_scale(am);
       const float rs = __frcp_rn(sc);
@@ -296,30 +290,33 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       // of row r at [cc / 8][r][(cc % 8) ^ (r % 8)]; then store whole rows
       // coalesced (one half-warp per 256-byte row segment).
       uint8_t* stage = smem + SmemTC::P + (m & 1) * 2 * kTileBytes;
-      const int sw = warp - 2;
+      const int sw = (warp - 2);
       for (int j0 = 0; j0 < nh; j0 += 4) {
         const int nj = min(4, nh - j0);
 #pragma unroll 1
         for (int jj = 0; jj < nj; ++jj) {
-          uint32_t v[8];
-          tmem_ld8(trow + kTmemCtx + (j0 + jj) * 32 + part * (kOW / 2), v);
+          uint32_t v[1][16];
+          tmem_ld16(trow + kTmemCtx + (j0 + jj) * 32 + half * 16, v[0]);
           tmem_wait_ld();
-          uint32_t w[4];
+          uint32_t w[8];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float2 a0 = __half22float2(*reinterpret_cast<const __half2*>(&v[2 * i]));
-            const float2 a1 = __half22float2(*reinterpret_cast<const __half2*>(&v[2 * i + 1]));
+          for (int i = 0; i < 8; ++i) {
+            const float2 a0 = __half22float2(*reinterpret_cast<const __half2*>(&v[0][2 * i]));
+            const float2 a1 = __half22float2(*reinterpret_cast<const __half2*>(&v[0][2 * i + 1]));
             w[i] = q8_quant4(a0, a1, sc, rs);
           }
-          const int cc = jj * 4 + part;  // 16-byte chunk: bytes [64 jj + 16 part, +16) of the pass row
-          *reinterpret_cast<uint4*>(stage + (cc >> 3) * kTileBytes + r * 128 + (((cc & 7) ^ (r & 7)) << 4)) =
-              make_uint4(w[0], w[1], w[2], w[3]);
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int cc = jj * 4 + half * 2 + k;
+            *reinterpret_cast<uint4*>(stage + (cc >> 3) * kTileBytes + r * 128 + (((cc & 7) ^ (r & 7)) << 4)) =
+                make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+          }
         }
         softmax_sync();
         const int cc = lane & 15;
 #pragma unroll
-        for (int i = 0; i < kQ / (2 * kSoftmaxWarps); ++i) {
-          const int row = sw * (kQ / kSoftmaxWarps) + i * 2 + (lane >> 4);
+        for (int i = 0; i < 8; ++i) {
+          const int row = sw * 16 + i * 2 + (lane >> 4);
           if (cc < nj * 4 && row < S) {
             const uint4 val =
                 *reinterpret_cast<const uint4*>(stage + (cc >> 3) * kTileBytes + row * 128 + (((cc & 7) ^ (row & 7)) << 4));
@@ -328,7 +325,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
         softmax_sync();
       }
-      if (part == 0 && r < S) ctxs[grow] = sc;
+      if (half == 0 && r < S) ctxs[grow] = sc;
       if (threadIdx.x == 64) trace_ev(trace, m, 7);
     };
 
@@ -354,67 +351,62 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       mbar_wait(s_full, n & 1);
       if (threadIdx.x == 64) trace_ev(trace, n, 3);
       tc_fence_after();
-      uint32_t raw[kKW];
-      tmem_ld32(trow + part * kKW, raw);
+      uint32_t raw[2][32];
+      tmem_ld32(trow + half * 64, raw[0]);
+      tmem_ld32(trow + half * 64 + 32, raw[1]);
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(s_empty);
       // masked raw scores (mask bias 0 / -inf), row max in raw units, then
       // p = exp2(log2(e)/sqrt(d) * (s - max)) as one FFMA per element; packed
       // fp32 pairs throughout
-      float2 s2[kKW / 2];
+      float2 s2[32];
       float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-      const float4* mk4 = reinterpret_cast<const float4*>(sMask) + part * (kKW / 4);
+      const float4* mk4 = reinterpret_cast<const float4*>(sMask) + half * 16;
 #pragma unroll
-      for (int j = 0; j < kKW; j += 4) {
+      for (int j = 0; j < 64; j += 4) {
         const float4 mk = mk4[j >> 2];
-        s2[j / 2] = add2(make_float2(__uint_as_float(raw[j]), __uint_as_float(raw[j + 1])), make_float2(mk.x, mk.y));
-        s2[j / 2 + 1] =
-            add2(make_float2(__uint_as_float(raw[j + 2]), __uint_as_float(raw[j + 3])), make_float2(mk.z, mk.w));
+        const uint32_t* rw = &raw[j >> 5][j & 31];
+        s2[j / 2] = add2(make_float2(__uint_as_float(rw[0]), __uint_as_float(rw[1])), make_float2(mk.x, mk.y));
+        s2[j / 2 + 1] = add2(make_float2(__uint_as_float(rw[2]), __uint_as_float(rw[3])), make_float2(mk.z, mk.w));
         m4[0] = fmaxf(m4[0], s2[j / 2].x);
         m4[1] = fmaxf(m4[1], s2[j / 2].y);
         m4[2] = fmaxf(m4[2], s2[j / 2 + 1].x);
         m4[3] = fmaxf(m4[3], s2[j / 2 + 1].y);
       }
       float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-      redMax[part * kQ + r] = mx;
-      group_sync();
-      mx = redMax[r];
-#pragma unroll
-      for (int pp = 1; pp < kSplit; ++pp) mx = fmaxf(mx, redMax[pp * kQ + r]);
+      redMax[half * kQ + r] = mx;
+      pair_sync();
+      mx = fmaxf(mx, redMax[(half ^ 1) * kQ + r]);
       const float nmx = -__fmul_rn(mx, sl2);
       const float2 sl2v = make_float2(sl2, sl2), nmxv = make_float2(nmx, nmx);
       float2 l2a = make_float2(0.0f, 0.0f), l2b = make_float2(0.0f, 0.0f);
 #pragma unroll
-      for (int j = 0; j < kKW / 2; ++j) {
+      for (int j = 0; j < 32; ++j) {
         const float2 e = fma2(s2[j], sl2v, nmxv);
         s2[j] = make_float2(ex2f(e.x), ex2f(e.y));
         if (j & 1) l2b = add2(l2b, s2[j]); else l2a = add2(l2a, s2[j]);
       }
       const float2 l2 = add2(l2a, l2b);
-      redSum[part * kQ + r] = l2.x + l2.y;
-      group_sync();
-      // fixed order in every part: ((l0 + l1) + (l2 + l3))
-      const float l = (redSum[r] + redSum[kQ + r]) + (redSum[2 * kQ + r] + redSum[3 * kQ + r]);
+      float l = l2.x + l2.y;
+      redSum[half * kQ + r] = l;
+      pair_sync();
+      l = redSum[r] + redSum[kQ + r];  // fixed order in both halves
       const float inv = __frcp_rn(l);
       const float2 inv2 = make_float2(inv, inv);
-      // P16 = R16(p) into the K-major 128B-swizzled tile P[n&1]: keys
-      // [kKW part, +kKW) live in k-block (kKW part) / 64, 16B chunks
-      // c0 .. c0+3 of row r (c0 = ((kKW part) % 64) / 8), stored at chunk
-      // (c ^ (r & 7)).  P[n&1] was last read by O(n-2), complete since
-      // epilogue(n-2) passed o_full.
-      const int k0 = part * kKW;
-      uint8_t* prow = smem + SmemTC::P + (n & 1) * 2 * kTileBytes + (k0 >> 6) * kTileBytes + r * 128;
-      const int c0 = (k0 & 63) >> 3;
+      // P16 = R16(p) into k-block `half` of the K-major 128B-swizzled tile
+      // P[n&1]: 16B chunk c of row r at (c ^ (r & 7)).  P[n&1] was last read
+      // by O(n-2), complete since epilogue(n-2) passed o_full.
+      uint8_t* prow = smem + SmemTC::P + (n & 1) * 2 * kTileBytes + half * kTileBytes + r * 128;
 #pragma unroll
-      for (int c = 0; c < kKW / 8; ++c) {
+      for (int c = 0; c < 8; ++c) {
         uint32_t w[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const float2 pn = mul2(s2[c * 4 + i], inv2);
           w[i] = pack_half2(pn.x, pn.y);
         }
-        *reinterpret_cast<uint4*>(prow + (((c0 + c) ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
       fence_async_smem();
       mbar_arrive(p_full + (n & 1));
