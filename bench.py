@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--seq", type=int, default=None)
     ap.add_argument("--no-variants", action="store_true", help="skip the fp16 side measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dynamic", action="store_true", help="skip the dynamic-length batching side measurement")
     ap.add_argument("--fused", type=int, default=None,
                     help="1/0: force the fused GEMM+LayerNorm / GEMM+requant epilogues on/off (default: library default)")
     return ap.parse_args()
@@ -124,6 +125,60 @@ class ClockSampler:
 
 
 # --------------------------------------------------------- cpu baseline
+def dynamic_length_variant(cfg, enc, B, S, stream, flush, n_batches=16, lo=None, seed=4242):
+    """the same encoder on a ragged corpus (lengths ~ U[S/4, S],
+    n_batches x B sequences), batched three ways (paper P:161):
+    fixed_pad(S), dynamic (own max, rounded to 8), dynamic_sorted (length-sorted,
+    order restored).  Device time per mode (CUDA events around all its batches,
+    ids / masks already resident, L2 flushed before each mode, median of 3
+    interleaved repetitions), padded-token and MAC ratios vs fixed padding."""
+    import numpy as np
+    import torch
+    from paper_2010_13382_b200 import batching
+
+    lo = lo or max(1, S // 4)
+    n = n_batches * B
+    lengths = batching.ragged_lengths(n, lo, S, seed)
+    corpus = batching.make_corpus(cfg, lengths, seed + 1)
+    out = {"corpus": f"{n} sequences, lengths U[{lo},{S}] (mean {lengths.mean():.1f}), batch {B}",
+           "unit": "sequences/s", "modes": {}}
+    base_macs = None
+    plans, devs = {}, {}
+    for mode in batching.MODES:
+        plans[mode] = batching.make_batches(lengths, B, mode, fixed_len=S, multiple=8)
+        devs[mode] = []
+        for b in plans[mode]:
+            ids, mask = batching.pack(corpus, b)
+            devs[mode].append((torch.from_numpy(ids).cuda(), torch.from_numpy(mask).cuda(),
+                               torch.empty((len(b.index), cfg.num_classes), dtype=torch.float32, device="cuda")))
+        for i, m, lg in devs[mode]:  # warm-up: one graph capture per batch
+            enc.encode(i, m, lg)
+    torch.cuda.synchronize()
+    times = {mode: [] for mode in batching.MODES}
+    for rep in range(3):  # modes interleaved, median of 3
+        for mode in batching.MODES:
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for i, m, lg in devs[mode]:
+                enc.encode(i, m, lg)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times[mode].append(e0.elapsed_time(e1))
+    for mode in batching.MODES:
+        plan = plans[mode]
+        ms = sorted(times[mode])[1]
+        mc = batching.macs(cfg, plan)
+        base_macs = base_macs or mc
+        out["modes"][mode] = {"value": n / (ms / 1e3), "ms": ms, "padded_tokens": batching.padded_tokens(plan),
+                              "mac_ratio_vs_fixed": mc / base_macs,
+                              "distinct_shapes": len({(len(b.index), b.seq) for b in plan})}
+    f = out["modes"]["fixed_pad"]["value"]
+    for mode in batching.MODES:
+        out["modes"][mode]["speedup_vs_fixed"] = out["modes"][mode]["value"] / f
+    return out
+
+
 def cpu_baseline(cfg, weights, ids, mask, per_core=8):
     """The oracle as it stands, multi-instance on the host cores (one
     single-threaded instance per core, whole sequences): `per_core`
@@ -352,6 +407,8 @@ def run_ours(args):
                             "gemm_frac_of_peak": gemm_flops(cfg16, B, S) / (g16 / 1e3) / 1e12 /
                                                  peaks["bf16_tflops_sustained"]}
         del enc16
+        if not args.no_dynamic:
+            variants["dynamic_length"] = dynamic_length_variant(cfg, enc, B, S, stream, flush)
 
     if world > 1:
         dist.barrier()

@@ -325,3 +325,31 @@ def test_cta_pairs_equal_single_cta_at_full_size(dt):
     a = f32(Encoder(cfg, w).encode(dev(ids), dev(mask)))
     b = f32(Encoder(cfg, w, cta_pairs=False).encode(dev(ids), dev(mask)))
     assert np.array_equal(a, b), np.abs(a - b).max()
+
+
+@pytest.mark.parametrize("name,dtype", [("c1", [1, 1]), ("c1", [0, 0]), ("c1", [1, 0]), ("c3", [1] * 6)])
+def test_dynamic_batching_modes_identical(name, dtype):
+    """SURVEY 8(f) NEXT-1 / S:458: the CUDA path's logits do not depend on the
+    batching mode (padding is inert): fixed_pad, dynamic and dynamic_sorted
+    give bit-identical logits; and they match the oracle."""
+    from paper_2010_13382_b200 import batching
+    cfg = synth.config(name).with_dtype(dtype)
+    w = synth.make_weights(cfg)
+    n, bs = (13, 4) if name == "c1" else (40, 16)
+    enc = Encoder(cfg, w, max_tokens=bs * cfg.seq)
+    lengths = batching.ragged_lengths(n, max(1, cfg.seq // 4), cfg.seq, seed=21)
+    corpus = batching.make_corpus(cfg, lengths, seed=22)
+
+    def run(ids, mask):
+        out = enc.encode(torch.from_numpy(ids).cuda(), torch.from_numpy(mask).cuda())
+        return out.cpu().numpy()
+
+    ref = batching.classify(run, corpus, bs, "fixed_pad", fixed_len=cfg.seq)
+    for mode, mult in [("dynamic", 1), ("dynamic_sorted", 1), ("dynamic_sorted", 8)]:
+        got = batching.classify(run, corpus, bs, mode, fixed_len=cfg.seq, multiple=mult)
+        np.testing.assert_array_equal(got, ref)
+    if name == "c1":
+        orc = oracle.Oracle(cfg, w)
+        exp = batching.classify(lambda i, m: orc.encode(i, m), corpus, bs, "dynamic")
+        tol = 1e-3 if all(dtype) else 1e-2
+        assert np.abs(ref - exp).max() <= tol * max(1.0, np.abs(exp).max())
