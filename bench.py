@@ -248,7 +248,8 @@ def run_reference(args):
             "config": config_json(cfg, args, 1), "impl": "reference",
             "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "oracle",
                              "sample": f"{cores} sequences per step (one oracle instance per core), {steps} steps"
-                                       f" (capped from --steps {args.steps} to fit ~3 min)"},
+                                       + (f" (capped from --steps {args.steps} to fit ~3 min)" if steps < args.steps
+                                          else "")},
             "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
