@@ -59,6 +59,8 @@ def lib():
         L.or_prepared_weight.argtypes = [P, c_int, c_int, i8p, f32p, f32p]
         L.or_q8row.argtypes = [f32p, c_int, c_int, i8p, f32p]
         L.or_quant_weight.argtypes = [f32p, c_int, c_int, i8p, f32p]
+        L.or_q8tensor.argtypes = [f32p, c_int, c_int, ctypes.POINTER(ctypes.c_uint8), f32p, i32p]
+        L.or_set_act_quant.argtypes = [P, c_int]
         L.or_gemm_s8.argtypes = [i8p, i8p, c_int, c_int, c_int, i32p]
         L.or_r16.argtypes = [f32p, ctypes.c_size_t, f32p]
         L.or_act.argtypes = [f32p, ctypes.c_size_t, c_int, f64p]
@@ -91,7 +93,9 @@ class Oracle:
     object with fields num_layers, hidden, head_dim, vocab_size, max_positions,
     num_classes, ln_eps, act, heads, ffn_dim, dtype (ints: 0 = f16, 1 = i8)."""
 
-    def __init__(self, cfg, weights: dict | None = None):
+    def __init__(self, cfg, weights: dict | None = None, act_quant: int = 0):
+        """act_quant: int8 activation quantizer, 0 = Q8row (per row, default),
+        1 = Q8tensor (per tensor, u8 with zero point; DESIGN R22)."""
         L = lib()
         self.cfg = cfg
         heads = _i32(cfg.heads)
@@ -102,6 +106,7 @@ class Oracle:
                              _p(ffn, ctypes.c_int32), _p(dt, ctypes.c_int32))
         if not self.h:
             raise RuntimeError("or_create failed: " + L.or_last_error().decode())
+        _check(L.or_set_act_quant(self.h, int(act_quant)))
         if weights is not None:
             self.load(weights)
 
@@ -181,6 +186,17 @@ def q8row(x):
     s = np.zeros(M, np.float32)
     lib().or_q8row(_p(x, ctypes.c_float), M, K, _p(q, ctypes.c_int8), _p(s, ctypes.c_float))
     return q, s
+
+
+def q8tensor(x):
+    """Per-tensor u8 quantization with zero point (DESIGN R22): (q u8, scale, zp)."""
+    x = _f32(x)
+    M, K = x.shape if x.ndim == 2 else (1, x.size)
+    q = np.zeros(x.shape, np.uint8)
+    s = np.zeros(1, np.float32)
+    z = np.zeros(1, np.int32)
+    lib().or_q8tensor(_p(x, ctypes.c_float), M, K, _p(q, ctypes.c_uint8), _p(s, ctypes.c_float), _p(z, ctypes.c_int32))
+    return q, float(s[0]), int(z[0])
 
 
 def quant_weight(W):

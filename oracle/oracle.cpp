@@ -75,6 +75,35 @@ void q8row(const float* x, int K, int8_t* q, float* s_out) {
   *s_out = s;
 }
 
+// Q8tensor (DESIGN R22; "the quantization range for the input matrix
+// is selected for entire input tensor", dynamic u8 quantization with a zero
+// point as in the FBGEMM / PyTorch dynamic-quantization recipe the paper
+// cites): over the whole [M, K] tensor,
+//   lo = min(0, min x), hi = max(0, max x), scale = (hi - lo) / 255 (fp32
+//   IEEE; 1.0 for an all-zero tensor), zp = clamp(RNE(-lo / scale), 0, 255),
+//   q = clamp(RNE(x / scale) + zp, 0, 255)  (u8).
+void q8tensor(const float* x, size_t n, uint8_t* q, float* scale_out, int* zp_out) {
+  float lo = 0.0f, hi = 0.0f;
+  for (size_t i = 0; i < n; ++i) {
+    lo = std::fmin(lo, x[i]);
+    hi = std::fmax(hi, x[i]);
+  }
+  float s = (hi - lo) / 255.0f;
+  if (s == 0.0f) s = 1.0f;
+  float z = std::nearbyint(-lo / s);
+  if (z < 0.0f) z = 0.0f;
+  if (z > 255.0f) z = 255.0f;
+  const int zp = (int)z;
+  for (size_t i = 0; i < n; ++i) {
+    float v = std::nearbyint(x[i] / s) + (float)zp;
+    if (v < 0.0f) v = 0.0f;
+    if (v > 255.0f) v = 255.0f;
+    q[i] = (uint8_t)v;
+  }
+  *scale_out = s;
+  *zp_out = zp;
+}
+
 // Per-output-channel weight quantization ("quantization range ... for
 // each column separately"; DESIGN R7): W is [N, K] (PyTorch
 // [out, in]); channel n = row n.
@@ -94,6 +123,7 @@ struct Layer {
 
 struct Model {
   int L, H, d, V, P, C, act;
+  int act_quant = 0;  // int8 activation quantizer: 0 Q8row (per row), 1 Q8tensor (per tensor, u8 + zero point)
   float eps;
   std::vector<Layer> layers;
   std::map<std::string, std::vector<float>> t;  // non-layer tensors
@@ -164,7 +194,6 @@ const char* kTopKeys[] = {"embeddings.word_embeddings.weight", "embeddings.posit
 void linear(const Model& mdl, const Layer& ly, int which, const std::vector<float>& Wf,
             const std::vector<float>& b, int N, int K, const double* x64, const float* x16,
             int M, int mode, int acc32, double* y64, float* y32) {
-  (void)mdl;
   if (mode == MODE_REF64) {
     for (int m = 0; m < M; ++m)
       for (int n = 0; n < N; ++n) {
@@ -192,12 +221,31 @@ void linear(const Model& mdl, const Layer& ly, int which, const std::vector<floa
       }
     return;
   }
+  const std::vector<int8_t>& Wq = ly.wq[which];
+  const std::vector<float>& sw = ly.sw[which];
+  if (mdl.act_quant == 1) {
+    // per-tensor u8 activations with zero point: acc = sum_k q * w (int32,
+    // exact), corrected by zp * sum_k w[n][k] (exact), then dequantized
+    std::vector<uint8_t> xq((size_t)M * K);
+    float st;
+    int zp;
+    q8tensor(x16, (size_t)M * K, xq.data(), &st, &zp);
+    for (int n = 0; n < N; ++n) {
+      int32_t colsum = 0;
+      for (int k = 0; k < K; ++k) colsum += (int32_t)Wq[(size_t)n * K + k];
+      for (int m = 0; m < M; ++m) {
+        int32_t acc = 0;
+        for (int k = 0; k < K; ++k) acc += (int32_t)xq[(size_t)m * K + k] * (int32_t)Wq[(size_t)n * K + k];
+        const int32_t corr = acc - zp * colsum;
+        y32[(size_t)m * N + n] = std::fma((float)corr, st * sw[n], b[n]);
+      }
+    }
+    return;
+  }
   // int8 (per-row activation scale, per-channel weight scale)
   std::vector<int8_t> xq((size_t)M * K);
   std::vector<float> sx(M);
   for (int m = 0; m < M; ++m) q8row(x16 + (size_t)m * K, K, &xq[(size_t)m * K], &sx[m]);
-  const std::vector<int8_t>& Wq = ly.wq[which];
-  const std::vector<float>& sw = ly.sw[which];
   for (int m = 0; m < M; ++m)
     for (int n = 0; n < N; ++n) {
       int32_t acc = 0;
@@ -647,6 +695,18 @@ int or_prepared_weight(void* h, int l, int which, int8_t* q, float* s, float* w1
 // ---- primitives (stage-level pins) ----
 int or_q8row(const float* x, int M, int K, int8_t* q, float* s) {
   for (int m = 0; m < M; ++m) q8row(x + (size_t)m * K, K, q + (size_t)m * K, s + m);
+  return 0;
+}
+
+int or_q8tensor(const float* x, int M, int K, uint8_t* q, float* scale, int* zp) {
+  q8tensor(x, (size_t)M * K, q, scale, zp);
+  return 0;
+}
+
+// Activation quantizer of the int8 layers: 0 Q8row (default), 1 Q8tensor.
+int or_set_act_quant(void* h, int mode) {
+  if (!h || (mode != 0 && mode != 1)) return -1;
+  static_cast<Model*>(h)->act_quant = mode;
   return 0;
 }
 

@@ -39,6 +39,7 @@ constexpr int kEpiWarps = 16;
 constexpr int kThreads = 128 + 32 * kEpiWarps;
 constexpr int kEpiCols = 32;                     // columns per epilogue chunk (two 16-column TMEM loads)
 constexpr int kStageTile = 32 * kEpiCols * 2;  // 2 KB: 32 rows x 64 B, 64-byte swizzle
+constexpr int kStageBufs = 1;                  // staging buffers per epilogue warp
 // gemm_rr_kernel: 16 epilogue warps (4 per quadrant, 64 columns each),
 // 32-column chunks, 32x32 fp16 staging blocks with 64B swizzle.
 constexpr int kRREpiWarps = 16;
@@ -53,9 +54,9 @@ struct GemmCfg {
   static constexpr int A_BYTES = BM * BK_BYTES;
   static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (PAIR || BN == 128) ? 4 : 3;
+  static constexpr int STAGES = (PAIR || BN == 128) ? 5 : 3;
   static constexpr int EPI_OFF = STAGES * STAGE_BYTES;
-  static constexpr int PAR_OFF = EPI_OFF + kEpiWarps * 2 * kStageTile;  // [acc][bias | col scale][BN] fp32
+  static constexpr int PAR_OFF = EPI_OFF + kEpiWarps * kStageBufs * kStageTile;  // [acc][bias | col scale][BN] fp32
   static constexpr int BAR_OFF = PAR_OFF + 2 * 2 * BN * 4;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;  // barriers + 1 KB alignment slack
   static constexpr uint32_t TMEM_COLS = 2 * BN;
@@ -358,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;                         // TMEM lane quadrant this warp may access
     constexpr int WCOLS = BN / (kEpiWarps / 4);     // columns per warp (64 or 32)
     const int c_lo = (ew >> 2) * WCOLS;             // this warp's column group of the tile
-    uint8_t* stage_buf = sEpi + ew * 2 * kStageTile;
+    uint8_t* stage_buf = sEpi + ew * kStageBufs * kStageTile;
     const uint32_t tempty_leader0 = PAIR ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -439,8 +440,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (tr0 && ci < 4) gemm_trace(p.trace, lt, 20 + ci);
           if (n0 < p.N) {  // warp-uniform; TMA clips the N tail of the chunk
-            uint8_t* buf = stage_buf + (nbuf & 1) * kStageTile;
-            if (lane == 0) bulk_wait_read<1>();  // the store that last used `buf` has read it
+            uint8_t* buf = stage_buf + (nbuf % kStageBufs) * kStageTile;
+            if (lane == 0) bulk_wait_read<kStageBufs - 1>();  // the store that last used `buf` has read it
             __syncwarp();
             if (tr0 && ci < 4) gemm_trace(p.trace, lt, 9 + 3 * ci);
             uint8_t* srow = buf + lane * 64;

@@ -370,3 +370,72 @@ def test_invalid_inputs_rejected():
     m2[1, 0] = 0
     with pytest.raises(RuntimeError):
         o.encode(ids, m2)
+
+
+# ------------------------------------- per-tensor u8 activations (NEXT-2)
+def test_q8tensor_worked_example():
+    # DESIGN R22 by hand: x = [-1, 0, 2, 3]: lo = -1, hi = 3, scale = fl(4/255),
+    # zp = RNE(1/scale) = RNE(63.75) = 64; q = RNE(x/scale) + 64 with
+    # 2/scale = 127.4999.. -> 127 and 3/scale = 191.2499.. -> 191 (fl(4/255) >
+    # 4/255), -1/scale -> -64: q = [0, 64, 191, 255]
+    q, s, z = oracle.q8tensor(np.array([[-1, 0, 2, 3]], np.float32))
+    assert s == np.float32(4.0) / np.float32(255.0) and z == 64
+    np.testing.assert_array_equal(q, [[0, 64, 191, 255]])
+    # all-positive tensor: lo = 0 -> zp = 0; all-zero tensor: scale 1, q = 0
+    q, s, z = oracle.q8tensor(np.array([[0.5, 1.0]], np.float32))
+    assert z == 0 and q[0, 1] == 255
+    q, s, z = oracle.q8tensor(np.zeros((2, 3), np.float32))
+    assert s == 1.0 and z == 0 and not q.any()
+
+
+def test_q8tensor_round_trip_bound():
+    # P:104 / S:152 analogue: |(q - zp) * scale - x| <= scale / 2 (plus the
+    # zero-point rounding) for every element of the tensor
+    rng = np.random.default_rng(12)
+    for shift in (0.0, 0.7, -0.7):
+        x = np.float16(rng.standard_normal((37, 91)) * 2 + shift).astype(np.float32)
+        q, s, z = oracle.q8tensor(x)
+        assert 0 <= z <= 255
+        deq = (q.astype(np.float64) - z) * s
+        assert np.abs(deq - x).max() <= s * 1.0 + 1e-7  # s/2 from x, s/2 from the nudged zero point
+        lo, hi = min(0.0, x.min()), max(0.0, x.max())
+        assert abs(s - (hi - lo) / 255) <= 1e-6 * abs(s)
+
+
+def test_linear_i8_per_tensor_vs_dequantized_fp64():
+    """The per-tensor int8 linear equals the fp64 product of the DEQUANTIZED
+    operands (the zp * colsum correction is exact in int32), up to the fp32
+    epilogue and fp16 output roundings."""
+    rng = np.random.default_rng(4)
+    H, A, d = 256, 4, 64
+    Wo = (rng.standard_normal((H, A * d)) * 0.02).astype(np.float32)
+    bo = (rng.standard_normal(H) * 0.02).astype(np.float32)
+    cfg = small_cfg(num_layers=1, hidden=H, heads=[A], ffn_dim=[256], dtype=[1])
+    o = Oracle(cfg, act_quant=1)
+    w = synth.make_weights(cfg)
+    w["encoder.layer.0.attention.output.dense.weight"] = Wo
+    w["encoder.layer.0.attention.output.dense.bias"] = bo
+    o.load(w)
+    x = np.float16(rng.standard_normal((64, A * d)) + 0.3).astype(np.float32)
+    y = o.stage(0, oracle.ST_OPROJ, x).astype(np.float64)
+    q, s, z = oracle.q8tensor(x)
+    wq, sw = oracle.quant_weight(Wo)
+    ref = ((q.astype(np.float64) - z) * s) @ (wq.astype(np.float64) * sw[:, None].astype(np.float64)).T + bo
+    # the stage output is rounded to fp16 (half an ulp) after the fp32 epilogue
+    assert np.all(np.abs(y - ref) <= np.abs(ref) * 2.0 ** -11 + 4e-6 * np.abs(ref).max())
+    # and it is a different quantizer from Q8row (per row) on the same input
+    o_row = Oracle(cfg, w)
+    assert not np.array_equal(o_row.stage(0, oracle.ST_OPROJ, x), y.astype(np.float32))
+
+
+def test_per_tensor_and_per_row_accuracy_vs_ref64_c1():
+    """Both int8 activation quantizers stay close to the fp64 reference; the
+    per-row scheme (the north_star's) is the more accurate on average."""
+    cfg = synth.config("c1").with_dtype([1, 1])
+    w = synth.make_weights(cfg)
+    ids, mask = synth.make_inputs(cfg, seed=31)
+    ref = Oracle(cfg, w).encode(ids, mask, mode=MODE_REF64, fp64_logits=True)
+    e_row = np.abs(Oracle(cfg, w).encode(ids, mask) - ref).max()
+    e_ten = np.abs(Oracle(cfg, w, act_quant=1).encode(ids, mask) - ref).max()
+    scale = np.abs(ref).max()
+    assert e_row <= 0.05 * scale and e_ten <= 0.1 * scale
