@@ -408,6 +408,24 @@ def run_ours(args):
                             "gemm_frac_of_peak": gemm_flops(cfg16, B, S) / (g16 / 1e3) / 1e12 /
                                                  peaks["bf16_tflops_sustained"]}
         del enc16
+        if cfg.dtype[0] == 1:
+            # NEXT-2 (DESIGN R22): the paper's per-tensor u8 activation quantizer
+            encpt = Encoder(cfg, w, max_tokens=B * S, device=local, act_quant=1)
+            for k in range(5):
+                encpt.encode(dids[k % NB], dmask[k % NB], logits)
+            torch.cuda.synchronize()
+            evp = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(50)]
+            for k in range(50):
+                flush.zero_()
+                evp[k][0].record(stream)
+                encpt.encode(dids[k % NB], dmask[k % NB], logits)
+                evp[k][1].record(stream)
+            torch.cuda.synchronize()
+            tp = sum(a.elapsed_time(b) for a, b in evp)
+            variants["int8_per_tensor_u8"] = {"value": B * 50 / (tp / 1e3), "unit": "sequences/s",
+                                              "ms_per_step": tp / 50,
+                                              "what": "per-tensor u8 activations + zero point (P:104, DESIGN R22)"}
+            del encpt
         if not args.no_dynamic:
             variants["dynamic_length"] = dynamic_length_variant(cfg, enc, B, S, stream, flush)
 

@@ -162,6 +162,13 @@ FF_API ff_status ff_check(ff_model *m, void *stream);
  * dependent launch so its prologue overlaps the previous kernel's tail;
  * process-wide setting). */
 #define FF_OPT_PDL 5
+/* FF_OPT_ACT_QUANT: activation quantizer of the int8 layers.  0 = default:
+ * Q8row, per-row symmetric s8 (north_star; DESIGN R6-R8); 1 = Q8tensor, the
+ * paper's per-tensor dynamic range as u8 with a zero point, u8 x s8
+ * tcgen05 GEMMs with an exact zero-point x column-sum correction (DESIGN
+ * R22).  1 disables FF_OPT_FUSED_EPILOGUES and breaks batch / padding
+ * invariance by construction (the range spans the whole batch). */
+#define FF_OPT_ACT_QUANT 6
 FF_API ff_status ff_set_option(ff_model *m, int32_t option, int64_t value);
 
 FF_API void ff_model_destroy(ff_model *m);

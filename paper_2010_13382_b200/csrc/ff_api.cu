@@ -61,7 +61,7 @@ const char* kTopKeys[9] = {"embeddings.word_embeddings.weight", "embeddings.posi
 struct LayerPlan {
   int A, F, dt, D;
   int N[4], K[4], ldw[4];  // GEMM shapes; ldw = packed row pitch in elements
-  size_t w[4], sw[4], bias[4];
+  size_t w[4], sw[4], bias[4], cs[4];  // cs: int32 weight column sums (int8 layers)
   size_t ln1g, ln1b, ln2g, ln2b;
   uint32_t loaded = 0;
   ff::GemmPlan gp[4];
@@ -86,7 +86,7 @@ struct ff_model {
   // workspace pitches (elements) and offsets
   int ldx16, ldx8, ldqkv, ldc16, ldc8, ldi16, ldi8;
   size_t ws_x16, ws_xq, ws_xs, ws_qkv, ws_ctx, ws_ctxq, ws_ctxs, ws_o, ws_h1, ws_h1q, ws_h1s, ws_i, ws_iq, ws_is;
-  size_t ws_err, ws_ids, ws_mask, ws_logits, ws_pooled;
+  size_t ws_err, ws_ids, ws_mask, ws_logits, ws_pooled, ws_tq;
   size_t wsbytes = 0;
   uint8_t* dW = nullptr;
   uint8_t* dWS = nullptr;
@@ -94,6 +94,7 @@ struct ff_model {
   int pair_mode = -1;  // FF_OPT_CTA_PAIRS: -1 auto, 0 never (GemmPlan::force_pair)
   bool attn_tc = true;  // FF_OPT_ATTN_TC: tcgen05 attention where supported
   bool fused = false;   // FF_OPT_FUSED_EPILOGUES: cluster row-reduction GEMM epilogues (opt-in)
+  int act_quant = 0;    // FF_OPT_ACT_QUANT: 0 per-row s8, 1 per-tensor u8 + zero point
   ff::AttnTCPlan tm_qkv;  // QKV buffer map for the tcgen05 attention
   std::map<std::tuple<int, int, const void*, const void*, const void*>, cudaGraphExec_t> graphs;
 
@@ -149,6 +150,7 @@ void plan_memory(ff_model* m) {
       P.ldw[i] = round_up(Ks[i], 16 / eb);
       P.w[i] = wa.take((size_t)Ns[i] * P.ldw[i] * eb);
       P.sw[i] = P.dt == FF_I8 ? wa.take((size_t)Ns[i] * 4) : 0;
+      P.cs[i] = P.dt == FF_I8 ? wa.take((size_t)Ns[i] * 4) : 0;
       P.bias[i] = wa.take((size_t)Ns[i] * 4);
     }
     P.ln1g = wa.take((size_t)H * 4);
@@ -190,6 +192,7 @@ void plan_memory(ff_model* m) {
   m->ws_iq = q ? a.take(M * m->ldi8) : 0;
   m->ws_is = q ? a.take(M * 4) : 0;
   m->ws_err = a.take(256);
+  m->ws_tq = a.take(256);  // per-tensor quantizer: uint mm[2], float qp[2]
   m->ws_ids = a.take(M * 4);
   m->ws_mask = a.take(M * 4);
   m->ws_logits = a.take(M * c.num_classes * 4);
@@ -334,7 +337,22 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
   __half* I16 = m->ws<__half>(m->ws_i);
   int8_t* Iq = m->ws<int8_t>(m->ws_iq);
   float* Is = m->ws<float>(m->ws_is);
-  const bool l0q = m->L[0].dt == FF_I8;
+  // per-tensor u8 activations (FF_OPT_ACT_QUANT = 1, DESIGN R22): the s8
+  // producers write fp16 only and every int8 GEMM input is quantized as a
+  // whole tensor right before its GEMM
+  const bool pt = m->act_quant == 1;
+  const bool l0q = m->L[0].dt == FF_I8 && !pt;
+  unsigned* tq_mm = reinterpret_cast<unsigned*>(m->dWS + m->ws_tq);
+  float* tq_qp = reinterpret_cast<float*>(m->dWS + m->ws_tq + 64);
+  auto tensor_quant = [&](const __half* x, int ldx, int K, int8_t* q8, int ldq, ff::GemmPlan& gp,
+                          const LayerPlan& P, int which) -> ff_status {
+    FF_LAUNCH(FF_K_QUANT, ff::launch_quant_tensor(x, ldx, M, K, tq_mm, reinterpret_cast<uint8_t*>(q8), ldq, tq_qp, s),
+              "quant tensor");
+    gp.p.row_scale = nullptr;
+    gp.p.tensor_qp = tq_qp;
+    gp.p.colsum = m->w<int>(P.cs[which]);
+    return FF_OK;
+  };
 
   FF_LAUNCH(FF_K_EMBED_LN, ff::launch_embed_ln(ids, mask, B, S, H, c.vocab_size, m->w<float>(m->emb_tok), m->w<float>(m->emb_pos),
                                 m->w<float>(m->emb_g), m->w<float>(m->emb_b), c.ln_eps, X16, m->ldx16,
@@ -355,11 +373,12 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     g.p.row_scale = q ? Xs : nullptr;
     g.p.col_scale = q ? m->w<float>(P.sw[W_QKV]) : nullptr;
     g.p.act = ff::ACT_NONE;
+    if (q && pt && tensor_quant(X16, m->ldx16, H, Xq, m->ldx8, g, P, W_QKV) != FF_OK) return FF_E_CUDA;
     FF_LAUNCH(q ? FF_K_GEMM_I8 : FF_K_GEMM_F16, ff::launch_gemm(g, s), "gemm qkv");
     if (tr && dump(d_dump[1], QKV, m->ldqkv, 3 * P.D, M, s) != FF_OK) return FF_E_CUDA;
     // a3: fused masked-softmax attention over this layer's A'_l heads
     // (int8 layers: a4, the ctx requant, fused into the tcgen05 attention)
-    const bool att_q = attention_fuses_quant(m, P, S);
+    const bool att_q = attention_fuses_quant(m, P, S) && !pt;
     if (m->attn_tc && ff::attention_tc_supported(S, c.head_dim, m->ldqkv, m->ldc16))
       FF_LAUNCH(FF_K_ATTENTION,
                 ff::launch_attention_tc(m->tm_qkv, mask, B, S, P.A, (att_q && !tr) ? nullptr : CTX, m->ldc16,
@@ -370,10 +389,10 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
                 "attention");
     if (tr && dump(d_dump[2], CTX, m->ldc16, P.D, M, s) != FF_OK) return FF_E_CUDA;
     // a4 + a5: requant (int8 layers) and out-projection
-    if (q && !att_q)
+    if (q && !att_q && !pt)
       FF_LAUNCH(FF_K_QUANT, ff::launch_quant_rows(CTX, m->ldc16, M, P.D, CTXq, m->ldc8, CTXs, s), "quant ctx");
-    const bool fuse_ln = m->fused && P.rr_ok[0];
-    const bool fuse_q = m->fused && q && P.rr_ok[1];
+    const bool fuse_ln = m->fused && !pt && P.rr_ok[0];
+    const bool fuse_q = m->fused && !pt && q && P.rr_ok[1];
     if (fuse_ln) {
       // a5 + a6 fused: H1 = LN1(R16(O) + X16) (+ s8 rows) in the out-proj epilogue
       ff::RRPlan r = P.rp[0];
@@ -402,11 +421,13 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     g.p.row_scale = q ? CTXs : nullptr;
     g.p.col_scale = q ? m->w<float>(P.sw[W_O]) : nullptr;
     g.p.act = ff::ACT_NONE;
+    if (q && pt && tensor_quant(CTX, m->ldc16, P.D, CTXq, m->ldc8, g, P, W_O) != FF_OK) return FF_E_CUDA;
     FF_LAUNCH(q ? FF_K_GEMM_I8 : FF_K_GEMM_F16, ff::launch_gemm(g, s), "gemm o");
     if (tr && dump(d_dump[3], O16, m->ldx16, H, M, s) != FF_OK) return FF_E_CUDA;
     // a6: residual + LN1 (+ s8 rows for FFN1)
     FF_LAUNCH(FF_K_ADD_LN, ff::launch_add_ln(O16, m->ldx16, X16, m->ldx16, M, H, m->w<float>(P.ln1g), m->w<float>(P.ln1b),
-                                c.ln_eps, H1, m->ldx16, q ? H1q : nullptr, m->ldx8, q ? H1s : nullptr, s),
+                                c.ln_eps, H1, m->ldx16, (q && !pt) ? H1q : nullptr, m->ldx8,
+                                (q && !pt) ? H1s : nullptr, s),
               "add_ln1");
     }
     if (tr && dump(d_dump[4], H1, m->ldx16, H, M, s) != FF_OK) return FF_E_CUDA;
@@ -437,12 +458,13 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     g.p.row_scale = q ? H1s : nullptr;
     g.p.col_scale = q ? m->w<float>(P.sw[W_FFN1]) : nullptr;
     g.p.act = c.act;
+    if (q && pt && tensor_quant(H1, m->ldx16, H, H1q, m->ldx8, g, P, W_FFN1) != FF_OK) return FF_E_CUDA;
     FF_LAUNCH(q ? FF_K_GEMM_I8 : FF_K_GEMM_F16, ff::launch_gemm(g, s), "gemm ffn1");
     if (tr && dump(d_dump[5], I16, m->ldi16, P.F, M, s) != FF_OK) return FF_E_CUDA;
     // a8 + a9: requant and FFN2
-    if (q) FF_LAUNCH(FF_K_QUANT, ff::launch_quant_rows(I16, m->ldi16, M, P.F, Iq, m->ldi8, Is, s), "quant ffn");
+    if (q && !pt) FF_LAUNCH(FF_K_QUANT, ff::launch_quant_rows(I16, m->ldi16, M, P.F, Iq, m->ldi8, Is, s), "quant ffn");
     }
-    const bool nq = l + 1 < c.num_layers && m->L[l + 1].dt == FF_I8;
+    const bool nq = l + 1 < c.num_layers && m->L[l + 1].dt == FF_I8 && !pt;
     if (fuse_ln) {
       // a9 + a10 fused: X16 = LN2(R16(Y) + H1) (+ s8 rows for the next int8 layer)
       ff::RRPlan r = P.rp[2];
@@ -471,6 +493,7 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     g.p.row_scale = q ? Is : nullptr;
     g.p.col_scale = q ? m->w<float>(P.sw[W_FFN2]) : nullptr;
     g.p.act = ff::ACT_NONE;
+    if (q && pt && tensor_quant(I16, m->ldi16, P.F, Iq, m->ldi8, g, P, W_FFN2) != FF_OK) return FF_E_CUDA;
     FF_LAUNCH(q ? FF_K_GEMM_I8 : FF_K_GEMM_F16, ff::launch_gemm(g, s), "gemm ffn2");
     if (tr && dump(d_dump[6], O16, m->ldx16, H, M, s) != FF_OK) return FF_E_CUDA;
     // a10: residual + LN2 (+ s8 rows when the next layer is int8)
@@ -707,6 +730,12 @@ ff_status ff_finalize(ff_model* m, void* stream) {
   FF_CK(ff::prepare_attention_tc_kernel());
   FF_CK(ff::prepare_rr_kernels());
   FF_CK(ff::prepare_row_kernels());
+  for (LayerPlan& P : m->L)  // zero-point corrections of the per-tensor u8 mode (DESIGN R22)
+    if (P.dt == FF_I8)
+      for (int i = 0; i < 4; ++i)
+        FF_CK(ff::launch_weight_colsum(reinterpret_cast<const int8_t*>(m->dW + P.w[i]), P.ldw[i], P.N[i], P.K[i],
+                                       reinterpret_cast<int*>(m->dW + P.cs[i]), s));
+  FF_CK(cudaStreamSynchronize(s));
   {
     const char* err = nullptr;
     if (!ff::plan_attention_tc(&m->tm_qkv, m->dWS + m->ws_qkv, m->cfg.max_tokens, m->ldqkv, &err))
@@ -796,6 +825,13 @@ ff_status ff_set_option(ff_model* m, int32_t option, int64_t value) {
     m->graphs.clear();
     return FF_OK;
   }
+  if (option == FF_OPT_ACT_QUANT) {
+    if (value != 0 && value != 1) return fail(FF_E_INVALID, "FF_OPT_ACT_QUANT must be 0 or 1");
+    m->act_quant = (int)value;
+    for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
+    m->graphs.clear();
+    return FF_OK;
+  }
   if (option == FF_OPT_FUSED_EPILOGUES) {
     m->fused = value != 0;
     for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
@@ -829,6 +865,10 @@ ff_status ff_launch_count(const ff_model* m, int32_t batch, int32_t seq, int32_t
   int n = 3;  // embed_ln + pooler + classifier
   for (const LayerPlan& P : m->L) {
     const bool q = P.dt == FF_I8;
+    if (m->act_quant == 1) {  // per-tensor u8: 4 GEMMs + attention + 2 add_ln, 2 quant kernels per int8 GEMM
+      n += 7 + (q ? 8 : 0);
+      continue;
+    }
     const bool fln = m->fused && P.rr_ok[0], fq = m->fused && P.rr_ok[1];
     n += 2;                              // QKV GEMM + attention
     n += (q && !attention_fuses_quant(m, P, seq)) ? 1 : 0;  // ctx requant

@@ -56,6 +56,11 @@ struct GemmParams {
   const float* col_scale;  // sw [N] (i8)
   int act;                 // Act
   unsigned long long* trace;  // debug timeline (ff_debug_set_trace), null in production
+  // per-tensor u8 activations (DESIGN R22; null = per-row s8): A is u8, the
+  // epilogue uses tensor_qp[0] (scale), tensor_qp[1] (zero point) and
+  // colsum[n] = sum_k wq[n][k]
+  const float* tensor_qp;
+  const int* colsum;
 };
 
 struct GemmPlan {
@@ -138,6 +143,13 @@ cudaError_t launch_embed_ln(const int32_t* ids, const int32_t* mask, int B, int 
 cudaError_t launch_add_ln(const __half* a, int lda, const __half* r, int ldr, int M, int H, const float* g,
                           const float* b, float eps, __half* y16, int ldy, int8_t* yq, int ldq, float* ys,
                           cudaStream_t s);
+// Per-tensor u8 quantization with zero point (DESIGN R22) of fp16 rows
+// [M, K] (K % 8 == 0): mm = 2 uint scratch (reset here), q = u8 [M, ldq],
+// qp[0] = scale, qp[1] = zero point.
+cudaError_t launch_quant_tensor(const __half* x, int ldx, int M, int K, unsigned* mm, uint8_t* q, int ldq, float* qp,
+                                cudaStream_t s);
+// colsum[n] = sum_k wq[n][k] of packed s8 weights.
+cudaError_t launch_weight_colsum(const int8_t* wq, int ldw, int N, int K, int* colsum, cudaStream_t s);
 // Per-row symmetric int8 quantization of fp16 rows.
 cudaError_t launch_quant_rows(const __half* x, int ldx, int M, int K, int8_t* q, int ldq, float* scale,
                               cudaStream_t s);

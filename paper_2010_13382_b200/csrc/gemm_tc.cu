@@ -56,8 +56,9 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (PAIR || BN == 128) ? 5 : 3;
   static constexpr int EPI_OFF = STAGES * STAGE_BYTES;
-  static constexpr int PAR_OFF = EPI_OFF + kEpiWarps * kStageBufs * kStageTile;  // [acc][bias | col scale][BN] fp32
-  static constexpr int BAR_OFF = PAR_OFF + 2 * 2 * BN * 4;
+  // [acc][bias | col scale | weight column sums (int)][BN]
+  static constexpr int PAR_OFF = EPI_OFF + kEpiWarps * kStageBufs * kStageTile;
+  static constexpr int BAR_OFF = PAR_OFF + 2 * 3 * BN * 4;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;  // barriers + 1 KB alignment slack
   static constexpr uint32_t TMEM_COLS = 2 * BN;
   static_assert(SMEM <= 227 * 1024, "smem budget");
@@ -156,13 +157,20 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[W], const float (&
 // 32 columns of this thread's row (r[0]: columns 0-15, r[1]: 16-31), bias /
 // column scales read from smem (bs / ss, broadcast LDS.64 per pair):
 // dequant / bias / activation, RNE to fp16, packed as 16 half2 words.
-template <bool I8, int ACT>
+// PT (per-tensor u8 activations, DESIGN R22): acc - zp * colsum[n] (exact
+// in int32, cs = column sums) replaces acc; PT = false: per-row s8 scheme.
+template <bool I8, int ACT, bool PT = false>
 __device__ __forceinline__ void epi32(const uint32_t (&r)[2][16], const float* bs, const float* ss, float sx,
-                                      uint32_t (&h)[16]) {
+                                      uint32_t (&h)[16], const int* cs = nullptr, int zp = 0) {
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
     const int j = 2 * e;
-    const uint32_t r0 = r[j >> 4][j & 15], r1 = r[j >> 4][(j & 15) + 1];
+    uint32_t r0 = r[j >> 4][j & 15], r1 = r[j >> 4][(j & 15) + 1];
+    if (I8 && PT) {
+      const int2 c2 = *reinterpret_cast<const int2*>(cs + j);
+      r0 = (uint32_t)((int)r0 - zp * c2.x);
+      r1 = (uint32_t)((int)r1 - zp * c2.y);
+    }
     const float2 b = *reinterpret_cast<const float2*>(bs + j);
     float2 v;
     if (I8) {
@@ -220,7 +228,9 @@ __device__ __forceinline__ void gemm_trace(unsigned long long* trace, int t, int
   }
 }
 
-template <int BN, bool I8, bool PAIR>
+// PT: per-tensor u8 activations with a zero point (DESIGN R22; I8 only), a
+// separate instantiation so the per-row kernel's registers are unaffected.
+template <int BN, bool I8, bool PAIR, bool PT = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, GemmParams p) {
@@ -308,7 +318,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
-      constexpr uint32_t idesc = make_idesc<I8, TM, BN>();
+      // per-tensor u8 activations (DESIGN R22): a_format u8 (bit 7 clear)
+      constexpr uint32_t idesc = make_idesc<I8, TM, BN>() & (PT ? ~(1u << 7) : ~0u);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -373,15 +384,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row0 = mt * TM + (int)rank * BM + q * 32;
       const int row = row0 + lane;
       float sx = 0.0f;
-      if (I8 && p.out_mode == 1 && row < p.M) sx = p.row_scale[row];
+      if (I8 && p.out_mode == 1 && row < p.M) sx = PT ? p.tensor_qp[0] : p.row_scale[row];
+      const int zp = (PT && p.out_mode == 1) ? (int)p.tensor_qp[1] : 0;
       // this tile's bias / column scales -> smem (double-buffered by acc; the
       // barrier of tile t+1 orders every warp's reads of tile t before the
       // writes of tile t+2), read by the chunks with low-latency LDS
-      float* par = sPar + acc * 2 * BN;
-      if (p.out_mode == 1 && et < 2 * BN) {
-        const int col = nt * BN + (et % BN);
-        const float* src = et < BN ? p.bias : p.col_scale;
-        par[et] = (src != nullptr && col < p.N) ? __ldg(src + col) : 0.0f;
+      float* par = sPar + acc * 3 * BN;
+      if (p.out_mode == 1) {
+        const int npar = PT ? 3 * BN : 2 * BN;
+        for (int i = et; i < npar; i += 32 * kEpiWarps) {
+          const int col = nt * BN + (i % BN);
+          if (i < 2 * BN) {
+            const float* src = i < BN ? p.bias : p.col_scale;
+            par[i] = (src != nullptr && col < p.N) ? __ldg(src + col) : 0.0f;
+          } else {
+            reinterpret_cast<int*>(par)[i] = (p.colsum != nullptr && col < p.N) ? __ldg(p.colsum + col) : 0;
+          }
+        }
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
       mbar_wait(&tfull[acc], acc_phase);
@@ -428,11 +447,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (tr0 && ci < 4) gemm_trace(p.trace, lt, 8 + 3 * ci);
           if (last) release_acc();
           uint32_t h[16];
-          switch (p.act) {
-            case ACT_GELU: epi32<I8, ACT_GELU>(r, par + c, par + BN + c, sx, h); break;
-            case ACT_RELU: epi32<I8, ACT_RELU>(r, par + c, par + BN + c, sx, h); break;
-            case ACT_GELU_TANH: epi32<I8, ACT_GELU_TANH>(r, par + c, par + BN + c, sx, h); break;
-            default: epi32<I8, ACT_NONE>(r, par + c, par + BN + c, sx, h); break;
+          if (PT) {  // per-tensor u8 activations
+            const int* cs = reinterpret_cast<const int*>(par + 2 * BN + c);
+            switch (p.act) {
+              case ACT_GELU: epi32<I8, ACT_GELU, true>(r, par + c, par + BN + c, sx, h, cs, zp); break;
+              case ACT_RELU: epi32<I8, ACT_RELU, true>(r, par + c, par + BN + c, sx, h, cs, zp); break;
+              case ACT_GELU_TANH: epi32<I8, ACT_GELU_TANH, true>(r, par + c, par + BN + c, sx, h, cs, zp); break;
+              default: epi32<I8, ACT_NONE, true>(r, par + c, par + BN + c, sx, h, cs, zp); break;
+            }
+          } else {
+            switch (p.act) {
+              case ACT_GELU: epi32<I8, ACT_GELU>(r, par + c, par + BN + c, sx, h); break;
+              case ACT_RELU: epi32<I8, ACT_RELU>(r, par + c, par + BN + c, sx, h); break;
+              case ACT_GELU_TANH: epi32<I8, ACT_GELU_TANH>(r, par + c, par + BN + c, sx, h); break;
+              default: epi32<I8, ACT_NONE>(r, par + c, par + BN + c, sx, h); break;
+            }
           }
           if (!last) {
             tmem_ld16(tbase + c + kEpiCols, r[0]);
@@ -1004,6 +1033,8 @@ bool plan_gemm(GemmPlan* g, bool i8, const void* A, int M_rows, int lda, const v
   g->p.bias = g->p.row_scale = g->p.col_scale = nullptr;
   g->p.act = ACT_NONE;
   g->p.trace = nullptr;
+  g->p.tensor_qp = nullptr;
+  g->p.colsum = nullptr;
   plan_gemm_set_m(g, M_rows);
   return true;
 }
@@ -1034,7 +1065,10 @@ void plan_gemm_set_m(GemmPlan* g, int M) {
 
 template <int BN, bool I8, bool PAIR>
 static cudaError_t set_attr() {
-  return cudaFuncSetAttribute(gemm_tc_kernel<BN, I8, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, I8, PAIR, false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN, PAIR>::SMEM);
+  if (e != cudaSuccess || !I8) return e;
+  return cudaFuncSetAttribute(gemm_tc_kernel<BN, I8, PAIR, I8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               GemmCfg<BN, PAIR>::SMEM);
 }
 
@@ -1053,7 +1087,10 @@ cudaError_t prepare_gemm_kernels() {
 template <int BN, bool I8, bool PAIR>
 static cudaError_t launch_t(const GemmPlan& g, cudaStream_t s) {
   if (g.grid <= 0) return cudaSuccess;
-  return launch_ex(gemm_tc_kernel<BN, I8, PAIR>, dim3(g.grid), dim3(kThreads), GemmCfg<BN, PAIR>::SMEM, s,
+  if (I8 && g.p.tensor_qp != nullptr)
+    return launch_ex(gemm_tc_kernel<BN, I8, PAIR, I8>, dim3(g.grid), dim3(kThreads), GemmCfg<BN, PAIR>::SMEM, s,
+                     PAIR ? 2 : 0, g.tmA, PAIR ? g.tmB2 : g.tmB, g.tmC, g.p);
+  return launch_ex(gemm_tc_kernel<BN, I8, PAIR, false>, dim3(g.grid), dim3(kThreads), GemmCfg<BN, PAIR>::SMEM, s,
                    PAIR ? 2 : 0, g.tmA, PAIR ? g.tmB2 : g.tmB, g.tmC, g.p);
 }
 

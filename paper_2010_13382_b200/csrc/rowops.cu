@@ -475,6 +475,99 @@ cudaError_t launch_add_ln(const __half* a, int lda, const __half* r, int ldr, in
   return cudaGetLastError();
 }
 
+// ---------------------------------------------- per-tensor u8 (DESIGN R22)
+namespace {
+
+// mm[0] = bits of max(0, max x), mm[1] = bits of max(0, -min x): both
+// non-negative floats, whose bit patterns order like the values, so an
+// integer atomicMax is an exact (order-independent) float max.
+__global__ void __launch_bounds__(256) tensor_minmax_kernel(const __half* __restrict__ x, int ldx, int M, int K,
+                                                           unsigned* __restrict__ mm) {
+  griddep_wait();
+  griddep_launch();
+  float hi = 0.0f, nlo = 0.0f;
+  const int kc = K / 8;  // 16-byte chunks per row (K % 8 == 0)
+  const size_t n = (size_t)M * kc;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / kc, c = i - r * kc;
+    float f[8];
+    unpack8(__ldg(reinterpret_cast<const uint4*>(x + r * ldx + c * 8)), f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      hi = fmaxf(hi, f[j]);
+      nlo = fmaxf(nlo, -f[j]);
+    }
+  }
+  hi = warp_max(hi);
+  nlo = warp_max(nlo);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(mm, __float_as_uint(hi));
+    atomicMax(mm + 1, __float_as_uint(nlo));
+  }
+}
+
+// q = clamp(RNE(x / scale) + zp, 0, 255), scale = (hi - lo) / 255 (1 for an
+// all-zero tensor), zp = clamp(RNE(-lo / scale), 0, 255); IEEE divisions as
+// in the definition.  qp[0] = scale, qp[1] = zp for the GEMM epilogue.
+__global__ void __launch_bounds__(256) tensor_quant_kernel(const __half* __restrict__ x, int ldx, int M, int K,
+                                                          const unsigned* __restrict__ mm, uint8_t* __restrict__ q,
+                                                          int ldq, float* __restrict__ qp) {
+  griddep_wait();
+  griddep_launch();
+  const float hi = __uint_as_float(mm[0]), nlo = __uint_as_float(mm[1]);
+  float sc = __fdiv_rn(__fadd_rn(hi, nlo), 255.0f);  // (hi - lo) / 255 with lo = -nlo
+  if (sc == 0.0f) sc = 1.0f;
+  const float zp = fminf(fmaxf(rintf(__fdiv_rn(nlo, sc)), 0.0f), 255.0f);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    qp[0] = sc;
+    qp[1] = zp;
+  }
+  const int kc = K / 8;
+  const size_t n = (size_t)M * kc;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / kc, c = i - r * kc;
+    float f[8];
+    unpack8(__ldg(reinterpret_cast<const uint4*>(x + r * ldx + c * 8)), f);
+    uint32_t b[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) b[j] = (uint32_t)fminf(fmaxf(rintf(__fdiv_rn(f[j], sc)) + zp, 0.0f), 255.0f);
+    *reinterpret_cast<uint2*>(q + r * ldq + c * 8) =
+        make_uint2(b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24), b[4] | (b[5] << 8) | (b[6] << 16) | (b[7] << 24));
+  }
+}
+
+// colsum[n] = sum_k wq[n][k] (the zero-point correction of u8 x s8 GEMMs).
+__global__ void __launch_bounds__(256) weight_colsum_kernel(const int8_t* __restrict__ wq, int ldw, int N, int K,
+                                                           int* __restrict__ colsum) {
+  griddep_wait();
+  const int n = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (n >= N) return;
+  int acc = 0;
+  for (int k = lane; k < K; k += 32) acc += wq[(size_t)n * ldw + k];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) colsum[n] = acc;
+}
+
+}  // namespace
+
+cudaError_t launch_quant_tensor(const __half* x, int ldx, int M, int K, unsigned* mm, uint8_t* q, int ldq, float* qp,
+                                cudaStream_t s) {
+  if (K % 8 || ldx % 8 || ldq % 8) return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemsetAsync(mm, 0, 2 * sizeof(unsigned), s);
+  if (e != cudaSuccess) return e;
+  launch_ex(tensor_minmax_kernel, dim3(2 * kNumSMs), dim3(256), 0, s, 0, x, ldx, M, K, mm);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  launch_ex(tensor_quant_kernel, dim3(4 * kNumSMs), dim3(256), 0, s, 0, x, ldx, M, K, (const unsigned*)mm, q, ldq, qp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_weight_colsum(const int8_t* wq, int ldw, int N, int K, int* colsum, cudaStream_t s) {
+  launch_ex(weight_colsum_kernel, dim3((N + 7) / 8), dim3(256), 0, s, 0, wq, ldw, N, K, colsum);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_quant_rows(const __half* x, int ldx, int M, int K, int8_t* q, int ldq, float* scale,
                               cudaStream_t s) {
   unsigned grid = (M + 7) / 8;

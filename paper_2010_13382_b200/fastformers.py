@@ -23,6 +23,8 @@ FF_OPT_GRAPHS = 1
 FF_OPT_CTA_PAIRS = 2
 FF_OPT_ATTN_TC = 3
 FF_OPT_FUSED_EPILOGUES = 4
+FF_OPT_PDL = 5
+FF_OPT_ACT_QUANT = 6
 KERNEL_KINDS = ["embed_ln", "gemm_f16", "gemm_i8", "attention", "quant_rows", "add_ln", "head"]
 STATUS_NAMES = ["FF_OK", "FF_E_INVALID", "FF_E_SHAPE", "FF_E_STATE", "FF_E_CUDA", "FF_E_INPUT", "FF_E_UNSUPPORTED",
                 "FF_E_NOMEM"]
@@ -105,7 +107,8 @@ class Encoder:
     """One FastFormers encoder model on one GPU (weights packed once at load)."""
 
     def __init__(self, cfg, weights: Dict[str, np.ndarray], max_tokens: Optional[int] = None, device: int = 0,
-                 use_graphs: bool = True, cta_pairs: bool = True, attn_tc: bool = True, fused: bool = False):
+                 use_graphs: bool = True, cta_pairs: bool = True, attn_tc: bool = True, fused: bool = False,
+                 act_quant: int = 0):
         import torch
         L = lib()
         self.cfg = cfg
@@ -138,6 +141,9 @@ class Encoder:
             check(L.ff_set_option(self.h, FF_OPT_ATTN_TC, 0))
         check(L.ff_set_option(self.h, FF_OPT_FUSED_EPILOGUES, 1 if fused else 0))
         self.fused = fused
+        # int8 activation quantizer: 0 per-row s8 (default), 1 per-tensor u8 + zero point
+        check(L.ff_set_option(self.h, FF_OPT_ACT_QUANT, int(act_quant)))
+        self.act_quant = act_quant
         if not cta_pairs:
             check(L.ff_set_option(self.h, FF_OPT_CTA_PAIRS, 0))
 

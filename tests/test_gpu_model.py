@@ -402,3 +402,46 @@ def test_full_size_c3_fused_epilogues_sampled_rows():
     drift = np.abs(_oracle_rows_parallel(orc, ids, mask, rows, acc32=True) - ref).max()
     assert np.abs(got[rows] - ref).max() <= max(3 * drift, 1e-3 * np.abs(ref).max())
     assert _margin_ok(ref, got[rows], 2e-2) == 1.0
+
+
+@pytest.mark.parametrize("name,B,S", [("c1", 4, 32), ("c2", 4, 128), ("c3", 6, 128)])
+def test_per_tensor_u8_activations_vs_oracle(name, B, S):
+    """NEXT-2 (DESIGN R22): per-tensor u8 activations with a zero point,
+    u8 x s8 tcgen05 GEMMs + exact zp * colsum correction, against the oracle
+    running the same quantizer (whole-batch statistics, so the whole batch is
+    compared); the drift bound of DESIGN §3."""
+    cfg = synth.config(name).with_dtype(1).with_batch(B, S)
+    w = synth.make_weights(cfg)
+    ids, mask = synth.make_inputs(cfg, B=B, S=S, ragged=True, seed=123)
+    enc = Encoder(cfg, w, act_quant=1)
+    got = f32(enc.encode(dev(ids), dev(mask)))
+    orc = Oracle(cfg, w, act_quant=1)
+    ref = orc.encode(ids, mask)
+    drift = np.abs(orc.encode(ids, mask, acc32=True) - ref).max()
+    err = np.abs(got - ref).max()
+    assert err <= max(3 * drift, 1e-3 * np.abs(ref).max()), (err, drift)
+    assert _margin_ok(ref, got, 2e-2) >= 0.999
+    # a genuinely different quantizer from the per-row default
+    row = f32(Encoder(cfg, w).encode(dev(ids), dev(mask)))
+    assert not np.array_equal(row, got)
+    assert enc.launch_count(B, S) == 3 + cfg.num_layers * 15
+
+
+def test_per_tensor_quantizer_kernel_bit_exact():
+    """The per-tensor u8 quantizer kernels (min/max reduction + quantize)
+    reproduce the oracle's Q8tensor bit for bit through the model's first
+    GEMM input: the u8 tensor is not exported, so compare the layer-0 stage
+    through the trace (QKV output) with the oracle stage run on the GPU's own
+    layer input."""
+    cfg = synth.config("c1").with_dtype([1, 1])
+    w = synth.make_weights(cfg)
+    B, S = cfg.batch, cfg.seq
+    ids, mask = synth.make_inputs(cfg, B=B, S=S, ragged=True, seed=5)
+    enc = Encoder(cfg, w, act_quant=1)
+    dumps = enc.trace(dev(ids), dev(mask), 0)
+    orc = Oracle(cfg, w, act_quant=1)
+    x_in = f32(dumps["x_in"])
+    qkv_ref = orc.stage(0, oracle.ST_QKV, x_in)
+    # same u8 tensor, same scale / zero point, exact int32 accumulation and
+    # correction, the same fp32 fma epilogue: bit-identical fp16 outputs
+    np.testing.assert_array_equal(f32(dumps["qkv"]), qkv_ref)
