@@ -6,21 +6,25 @@
 //   fp16 layers: tcgen05.mma kind::f16, fp32 accumulate
 //   int8 layers: tcgen05.mma kind::i8,  s32 accumulate (exact)
 //
-// Persistent, warp-specialised kernel, one CTA per SM, 384 threads:
-//   warp 0      TMA producer: 128x128B A tile + BNx128B W tile per k-block into
-//               a STAGES-deep ring of 128B-swizzled smem tiles (mbarrier full/empty)
+// Persistent, warp-specialised kernel, one CTA (or CTA pair) per SM, 640 threads:
+//   warp 0      TMA producer: 128x128B A tile + (BN or BN/2)x128B W tile per
+//               k-block into a STAGES-deep ring of 128B-swizzled smem tiles
+//               (mbarrier full/empty); CTA pairs (cta_group::2) split W
 //   warp 1      MMA issuer: one thread issues 4 x tcgen05.mma (K = 32 bytes each)
 //               per k-block into a double-buffered TMEM accumulator (2 x BN cols)
 //   warp 2      TMEM allocator
-//   warps 4-11  epilogue: warp w drains TMEM lane quadrant w%4, column half
-//               (w-4)/4, with tcgen05.ld 32x32b.x32 (thread = output row),
-//               applies the fused epilogue in fp32, writes fp16 into a 64B-
-//               swizzled smem staging tile and issues a TMA bulk-tensor store
-//               per 32x32 block; overlaps the next tile's mainloop through the
-//               second accumulator.
+//   warps 4-19  epilogue: warp w drains TMEM lane quadrant w%4, column quarter
+//               (w-4)/4, with tcgen05.ld 32x32b.x16 (thread = output row) in
+//               32-column chunks, applies the fused epilogue on packed fp32
+//               pairs, writes fp16 into a 64B-swizzled smem staging block and
+//               issues a TMA bulk-tensor store per 32x32 block; bias / column
+//               scales are staged in smem per tile; the accumulator is released
+//               as soon as its last TMEM load completed, so the next tile's
+//               mainloop overlaps this epilogue.
 // Epilogue (out_mode 1):
 //   fp16: y = acc + b[n]
 //   int8: y = fma(float(acc), sx[m]*sw[n], b[n])          (DESIGN R13, bit-exact)
+//         per-tensor u8 variant (PT): acc - zp * colsum[n] first (R22)
 //   then optional activation (GELU-erf / ReLU / GELU-tanh) in fp32 and
 //   RNE to fp16.  out_mode 0 stores the raw 32-bit accumulators (tests only).
 #include <cstdio>
@@ -33,8 +37,8 @@ namespace ff {
 constexpr int BM = 128;
 constexpr int BK_BYTES = 128;  // one 128-byte swizzle row of K per k-block
 // gemm_tc_kernel: 16 epilogue warps (4 per TMEM lane quadrant, each owning a
-// quarter of the tile's columns), 16-column chunks, 32x16 fp16 staging blocks
-// stored with 32B swizzle.  <= 96 registers per thread at 640 threads.
+// quarter of the tile's columns), 32-column chunks, 32x32 fp16 staging blocks
+// stored with 64B swizzle.  <= 96 registers per thread at 640 threads.
 constexpr int kEpiWarps = 16;
 constexpr int kThreads = 128 + 32 * kEpiWarps;
 constexpr int kEpiCols = 32;                     // columns per epilogue chunk (two 16-column TMEM loads)
@@ -128,32 +132,6 @@ __device__ __forceinline__ float2 gelu2(float2 y) {
   return mul2(mul2(y, make_float2(0.5f, 0.5f)), sel);
 }
 
-// W columns [n0, n0+W) of this thread's row: dequant / bias / activation,
-// RNE to fp16, packed as W/2 half2 words (pairs on packed fp32 arithmetic).
-template <bool I8, int ACT, int W>
-__device__ __forceinline__ void epi_chunk(const uint32_t (&r)[W], const float (&bias)[W], const float (&sw)[W],
-                                          float sx, uint32_t (&h)[W / 2]) {
-#pragma unroll
-  for (int e = 0; e < W / 2; ++e) {
-    const int j = 2 * e;
-    const float2 b = make_float2(bias[j], bias[j + 1]);
-    float2 v;
-    if (I8) {
-      const float2 a = make_float2(__int2float_rn(static_cast<int>(r[j])), __int2float_rn(static_cast<int>(r[j + 1])));
-      v = fma2(a, mul2(make_float2(sx, sx), make_float2(sw[j], sw[j + 1])), b);
-    } else {
-      v = add2(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), b);
-    }
-    if (ACT == ACT_GELU) {
-      v = gelu2(v);
-    } else if (ACT != ACT_NONE) {
-      v.x = act_fn<ACT>(v.x);
-      v.y = act_fn<ACT>(v.y);
-    }
-    h[e] = pack_half2(v.x, v.y);
-  }
-}
-
 // 32 columns of this thread's row (r[0]: columns 0-15, r[1]: 16-31), bias /
 // column scales read from smem (bs / ss, broadcast LDS.64 per pair):
 // dequant / bias / activation, RNE to fp16, packed as 16 half2 words.
@@ -190,26 +168,6 @@ __device__ __forceinline__ void epi32(const uint32_t (&r)[2][16], const float* b
   }
 }
 
-template <int W>
-__device__ __forceinline__ void loadN(float (&dst)[W], const float* src, int n0, int N) {
-  if (src == nullptr) {
-#pragma unroll
-    for (int j = 0; j < W; ++j) dst[j] = 0.0f;
-  } else if (n0 + W <= N && ((reinterpret_cast<uintptr_t>(src + n0) & 15) == 0)) {
-#pragma unroll
-    for (int j = 0; j < W; j += 4) {
-      const float4 f = __ldg(reinterpret_cast<const float4*>(src + n0 + j));
-      dst[j] = f.x;
-      dst[j + 1] = f.y;
-      dst[j + 2] = f.z;
-      dst[j + 3] = f.w;
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < W; ++j) dst[j] = (n0 + j < N) ? __ldg(src + n0 + j) : 0.0f;
-  }
-}
-__device__ __forceinline__ void load32(float (&dst)[32], const float* src, int n0, int N) { loadN<32>(dst, src, n0, N); }
 
 // tcgen05.ld of 16 columns (32x32b.x16): thread t gets row (lane base + t).
 

@@ -263,12 +263,6 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-// One-sided DSMEM store that signals its bytes on an mbarrier of the target CTA.
-__device__ __forceinline__ void st_async_f32(uint32_t remote_addr, float v, uint32_t remote_bar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(remote_addr),
-               "r"(__float_as_uint(v)), "r"(remote_bar)
-               : "memory");
-}
 // Bulk smem -> peer-smem copy (16B-aligned, size multiple of 16) that signals
 // its bytes on an mbarrier of the destination CTA.
 __device__ __forceinline__ void bulk_copy_s2c(uint32_t dst_cluster, const void* src, uint32_t bytes,
