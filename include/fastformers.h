@@ -169,6 +169,13 @@ FF_API ff_status ff_check(ff_model *m, void *stream);
  * R22).  1 disables FF_OPT_FUSED_EPILOGUES and breaks batch / padding
  * invariance by construction (the range spans the whole batch). */
 #define FF_OPT_ACT_QUANT 6
+/* FF_OPT_GEMM_MC (process-wide): 1 = CTA-pair GEMMs run as clusters of two
+ * pairs stacked along M that share each W k-block by TMA multicast (half the
+ * W bytes per SM from L2); 0 = independent pairs.  Results are identical. */
+#define FF_OPT_GEMM_MC 7
+/* Set `option` to `value` on model m (invalidates its captured graphs).  The
+ * process-wide options FF_OPT_PDL and FF_OPT_GEMM_MC may be set with m = NULL.
+ * FF_E_INVALID for an unknown option / bad value / NULL m otherwise. */
 FF_API ff_status ff_set_option(ff_model *m, int32_t option, int64_t value);
 
 FF_API void ff_model_destroy(ff_model *m);

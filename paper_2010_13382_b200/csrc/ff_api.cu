@@ -14,6 +14,7 @@
 
 namespace ff {
 bool g_pdl = true;  // FF_OPT_PDL: programmatic dependent launch between forward kernels
+int g_gemm_mc = 0;  // FF_OPT_GEMM_MC: CTA-pair GEMMs in clusters of two pairs sharing W by multicast
 }
 
 namespace {
@@ -814,6 +815,14 @@ ff_status ff_check(ff_model* m, void* stream) {
 }
 
 ff_status ff_set_option(ff_model* m, int32_t option, int64_t value) {
+  if (!m && option == FF_OPT_GEMM_MC) {  // process-wide options may be set without a model
+    ff::g_gemm_mc = value != 0 ? 1 : 0;
+    return FF_OK;
+  }
+  if (!m && option == FF_OPT_PDL) {
+    ff::g_pdl = value != 0;
+    return FF_OK;
+  }
   if (!m) return fail(FF_E_INVALID, "null model");
   if (option == FF_OPT_GRAPHS) {
     m->use_graphs = value != 0;
@@ -821,6 +830,12 @@ ff_status ff_set_option(ff_model* m, int32_t option, int64_t value) {
   }
   if (option == FF_OPT_PDL) {  // process-wide
     ff::g_pdl = value != 0;
+    for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
+    m->graphs.clear();
+    return FF_OK;
+  }
+  if (option == FF_OPT_GEMM_MC) {  // process-wide
+    ff::g_gemm_mc = value != 0 ? 1 : 0;
     for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
     m->graphs.clear();
     return FF_OK;
@@ -920,7 +935,8 @@ ff_status ff_debug_gemm(int32_t dtype, const void* d_A, int32_t lda, const void*
     FF_CK(ff::prepare_gemm_kernels());
     prepared = true;
   }
-  const int force = out_mode >> 4;  // bit 4: force CTA pairs, bit 5: force single CTAs
+  const int force = (out_mode >> 4) & 3;  // bit 4: force CTA pairs, bit 5: force single CTAs
+  const int noload = (out_mode >> 6) & 1;  // bit 6: MMA-rate probe (operand loads skipped, results garbage)
   out_mode &= 15;
   ff::GemmPlan g;
   const char* err = nullptr;
@@ -942,6 +958,7 @@ ff_status ff_debug_gemm(int32_t dtype, const void* d_A, int32_t lda, const void*
   g.p.col_scale = d_sw;
   g.p.act = act;
   g.p.trace = g_debug_trace_which == 0 ? g_debug_trace : nullptr;
+  g.p.dbg_noload = noload;
   FF_CK(ff::launch_gemm(g, static_cast<cudaStream_t>(stream)));
   return FF_OK;
 }

@@ -61,10 +61,11 @@ struct GemmParams {
   // colsum[n] = sum_k wq[n][k]
   const float* tensor_qp;
   const int* colsum;
+  int dbg_noload;  // debug MMA-rate probe: skip the operand loads (ff_debug_gemm bit 6; 0 in production)
 };
 
 struct GemmPlan {
-  CUtensorMap tmA, tmB, tmB2, tmC;  // A, W (BN-row / BN/2-row boxes, 128B swizzle); fp16 output (64B swizzle)
+  CUtensorMap tmA, tmB, tmB2, tmB4, tmC;  // A, W (BN / BN/2 / BN/4-row boxes, 128B swizzle); fp16 output (64B swizzle)
   GemmParams p;
   int bn;       // N tile (128 or 256)
   int i8;       // 1 = kind::i8
@@ -73,7 +74,9 @@ struct GemmPlan {
   bool has_out_map;
   int force_pair;   // -1 auto (pairs when >= 74 pair-tiles), 0 never, 1 always
   bool pair;        // chosen for the current M
+  bool mc;          // pairs run as clusters of two with W multicast (g_gemm_mc)
 };
+extern int g_gemm_mc;  // FF_OPT_GEMM_MC: 1 = CTA-pair GEMMs share W k-blocks by TMA multicast
 
 // Encode a 2-D K-major tensor map for a GEMM operand: rows x cols elements of
 // `elem_bytes` (2 fp16 / 1 int8), row pitch in bytes, box = box_rows x 128 B,

@@ -188,10 +188,17 @@ __device__ __forceinline__ void gemm_trace(unsigned long long* trace, int t, int
 
 // PT: per-tensor u8 activations with a zero point (DESIGN R22; I8 only), a
 // separate instantiation so the per-row kernel's registers are unaffected.
-template <int BN, bool I8, bool PAIR, bool PT = false>
+// MC (PAIR only): clusters of two CTA pairs stacked along M that work on row
+// tiles (2j, 2j+1) of the same column tile in lockstep and share its W
+// k-blocks: CTA r of pair q TMA-loads rows [q BN/4, +BN/4) of its W half and
+// multicasts them into CTA r of both pairs, halving the W bytes each SM pulls
+// from L2 (A stays per pair).  A stage's smem is refilled only when both pair
+// leaders' MMAs have consumed it (empty barriers count two commits).
+template <int BN, bool I8, bool PAIR, bool PT = false, bool MC = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, GemmParams p) {
+  static_assert(!MC || (PAIR && !PT), "W multicast is a CTA-pair variant");
   using Cfg = GemmCfg<BN, PAIR>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int TM = Cfg::TM;
@@ -207,16 +214,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = PAIR ? cluster_ctarank() : 0;  // 0 = leader of the pair
-  const int unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int nunits = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const uint32_t crank = PAIR ? cluster_ctarank() : 0;
+  const uint32_t rank = crank & 1;                    // 0 = leader of the pair
+  const uint32_t pq = MC ? (crank >> 1) : 0;          // pair index in an MC cluster
+  const uint32_t lead = crank & ~1u;                  // cluster rank of this pair's leader
+  const int unit = MC ? (int)(blockIdx.x >> 2) : PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int nunits = MC ? (int)(gridDim.x >> 2) : PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     if (p.out_mode == 1) tma_prefetch(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC ? 2 : 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -241,7 +251,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   griddep_wait();  // A operand / scales come from the previous kernel
   griddep_launch();
 
-  const int num_tiles = p.m_tiles * p.n_tiles;
+  // MC: a cluster tile = row tiles (2j, 2j+1) x one column tile; pair pq takes
+  // row tile 2j + pq (past the last row tile when m_tiles is odd: it runs on
+  // zero-filled / unused rows and stores nothing)
+  const int num_tiles = (MC ? (p.m_tiles + 1) / 2 : p.m_tiles) * p.n_tiles;
   constexpr int KE = I8 ? 128 : 64;  // elements per k-block
 
   if (warp == 0) {
@@ -250,18 +263,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int lt = 0;
       for (int tile = unit; tile < num_tiles; tile += nunits, ++lt) {
-        const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+        const int ct = tile / p.n_tiles, nt = tile - ct * p.n_tiles;
+        const int mt = MC ? 2 * ct + (int)pq : ct;
         const int arow = mt * TM + (int)rank * BM;
         const int brow = nt * BN + (PAIR ? (int)rank * (BN / 2) : 0);
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (kb == 0) gemm_trace(p.trace, lt, 6);
-          if (PAIR) {
+          if (p.dbg_noload) {  // MMA-rate probe: operands left as they are in smem
+            if (rank == 0) mbar_arrive(&full[stage]);
+          } else if (PAIR) {
             // the leader's full barrier counts the bytes of both CTAs' loads
             if (rank == 0) mbar_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
-            const uint32_t bar = mapa_shared(smem_u32(&full[stage]), 0);
+            const uint32_t bar = mapa_shared(smem_u32(&full[stage]), lead);
             tma_load_2d_pair(sA + stage * Cfg::A_BYTES, &tmA, bar, kb * KE, arow, kEvictNormal);
-            tma_load_2d_pair(sB + stage * Cfg::B_BYTES, &tmB, bar, kb * KE, brow, kEvictLast);
+            if (MC) {  // quarter pq of the pair's W rows, into CTA `rank` of both pairs
+              tma_load_2d_pair_mc(sB + stage * Cfg::B_BYTES + pq * (BN / 4) * BK_BYTES, &tmB, bar, kb * KE,
+                                  brow + (int)pq * (BN / 4), (uint16_t)(0x5u << rank), kEvictLast);
+            } else {
+              tma_load_2d_pair(sB + stage * Cfg::B_BYTES, &tmB, bar, kb * KE, brow, kEvictLast);
+            }
           } else {
             mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
             tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * KE, arow, kEvictNormal);
@@ -305,8 +326,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               else mma_f16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, accum);
             }
           }
-          // frees the smem slot (of both CTAs) when these MMAs finish
-          if (PAIR) mma_commit_pair(&empty[stage], 0x3);
+          // frees the smem slot (of both CTAs; MC: of all four, each counting
+          // both pair leaders) when these MMAs finish
+          if (PAIR) mma_commit_pair(&empty[stage], MC ? 0xF : 0x3);
           else mma_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
@@ -314,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         // accumulator ready for the epilogue warps (of both CTAs)
-        if (PAIR) mma_commit_pair(&tfull[acc], 0x3);
+        if (PAIR) mma_commit_pair(&tfull[acc], (uint16_t)(0x3u << lead));
         else mma_commit(&tfull[acc]);
         gemm_trace(p.trace, lt, 2);
         if (++acc == 2) {
@@ -329,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int WCOLS = BN / (kEpiWarps / 4);     // columns per warp (64 or 32)
     const int c_lo = (ew >> 2) * WCOLS;             // this warp's column group of the tile
     uint8_t* stage_buf = sEpi + ew * kStageBufs * kStageTile;
-    const uint32_t tempty_leader0 = PAIR ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
+    const uint32_t tempty_leader0 = PAIR ? mapa_shared(smem_u32(&tempty[0]), lead) : 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     int nbuf = 0;
@@ -338,7 +360,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* sPar = reinterpret_cast<float*>(smem + Cfg::PAR_OFF);
     const int et = ew * 32 + lane;  // 0 .. 511
     for (int tile = unit; tile < num_tiles; tile += nunits, ++lt) {
-      const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+      const int ct = tile / p.n_tiles, nt = tile - ct * p.n_tiles;
+      const int mt = MC ? 2 * ct + (int)pq : ct;
       const int row0 = mt * TM + (int)rank * BM + q * 32;
       const int row = row0 + lane;
       float sx = 0.0f;
@@ -426,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_ld16(tbase + c + kEpiCols + 16, r[1]);
           }
           if (tr0 && ci < 4) gemm_trace(p.trace, lt, 20 + ci);
-          if (n0 < p.N) {  // warp-uniform; TMA clips the N tail of the chunk
+          if (n0 < p.N && row0 < p.M) {  // warp-uniform; TMA clips the N tail of the chunk
             uint8_t* buf = stage_buf + (nbuf % kStageBufs) * kStageTile;
             if (lane == 0) bulk_wait_read<kStageBufs - 1>();  // the store that last used `buf` has read it
             __syncwarp();
@@ -981,6 +1004,7 @@ bool plan_gemm(GemmPlan* g, bool i8, const void* A, int M_rows, int lda, const v
   // W boxes cover BN rows (single CTA) or BN/2 rows (each CTA of a pair): two maps.
   if (!make_operand_map(&g->tmB, W, N, K, eb, (size_t)ldw * eb, g->bn, err)) return false;
   if (!make_operand_map(&g->tmB2, W, N, K, eb, (size_t)ldw * eb, g->bn / 2, err)) return false;
+  if (!make_operand_map(&g->tmB4, W, N, K, eb, (size_t)ldw * eb, g->bn / 4, err)) return false;
   g->p.N = N;
   g->p.K = K;
   g->p.n_tiles = (N + g->bn - 1) / g->bn;
@@ -1005,6 +1029,8 @@ bool plan_gemm_output(GemmPlan* g, void* out, int ldo, const char** err) {
                    32, CU_TENSOR_MAP_SWIZZLE_64B, err);
 }
 
+int gemm_mc_max_clusters(bool i8, int bn);
+
 void plan_gemm_set_m(GemmPlan* g, int M) {
   g->p.M = M;
   // CTA pairs (M = 256 tiles) when there are enough tiles to fill the GPU.
@@ -1013,7 +1039,13 @@ void plan_gemm_set_m(GemmPlan* g, int M) {
   const int tm = g->pair ? 256 : BM;
   g->p.m_tiles = (M + tm - 1) / tm;
   const int tiles = g->p.m_tiles * g->p.n_tiles;
-  if (g->pair) {
+  g->mc = g->pair && g_gemm_mc != 0;
+  g->p.dbg_noload = 0;
+  if (g->mc) {
+    const int ctiles = ((g->p.m_tiles + 1) / 2) * g->p.n_tiles;
+    const int maxc = gemm_mc_max_clusters(g->i8 != 0, g->bn);
+    g->grid = 4 * (ctiles < maxc ? ctiles : maxc);
+  } else if (g->pair) {
     const int pairs = tiles < kNumSMs / 2 ? tiles : kNumSMs / 2;
     g->grid = 2 * pairs;
   } else {
@@ -1021,11 +1053,48 @@ void plan_gemm_set_m(GemmPlan* g, int M) {
   }
 }
 
+template <int BN, bool I8>
+static int gemm_mc_max_clusters_t() {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kNumSMs);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = GemmCfg<BN, true>::SMEM;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 4;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<BN, I8, true, false, true>, &cfg) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    return kNumSMs / 4;
+  }
+  return n;
+}
+
+// Co-resident 4-CTA clusters of the MC GEMM (cached per variant).
+int gemm_mc_max_clusters(bool i8, int bn) {
+  static int cache[4] = {0, 0, 0, 0};
+  const int k = (i8 ? 2 : 0) + (bn == 256 ? 1 : 0);
+  if (cache[k] == 0)
+    cache[k] = i8 ? (bn == 256 ? gemm_mc_max_clusters_t<256, true>() : gemm_mc_max_clusters_t<128, true>())
+                  : (bn == 256 ? gemm_mc_max_clusters_t<256, false>() : gemm_mc_max_clusters_t<128, false>());
+  return cache[k];
+}
+
 template <int BN, bool I8, bool PAIR>
 static cudaError_t set_attr() {
   cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, I8, PAIR, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN, PAIR>::SMEM);
-  if (e != cudaSuccess || !I8) return e;
+  if (e != cudaSuccess) return e;
+  if (PAIR) {
+    e = cudaFuncSetAttribute(gemm_tc_kernel<BN, I8, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             GemmCfg<BN, true>::SMEM);
+    if (e != cudaSuccess) return e;
+  }
+  if (!I8) return e;
   return cudaFuncSetAttribute(gemm_tc_kernel<BN, I8, PAIR, I8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               GemmCfg<BN, PAIR>::SMEM);
 }
@@ -1045,6 +1114,9 @@ cudaError_t prepare_gemm_kernels() {
 template <int BN, bool I8, bool PAIR>
 static cudaError_t launch_t(const GemmPlan& g, cudaStream_t s) {
   if (g.grid <= 0) return cudaSuccess;
+  if (PAIR && g.mc && g.p.tensor_qp == nullptr)  // (per-tensor u8 runs the plain pair kernel)
+    return launch_ex(gemm_tc_kernel<BN, I8, true, false, true>, dim3(g.grid), dim3(kThreads),
+                     GemmCfg<BN, true>::SMEM, s, 4, g.tmA, g.tmB4, g.tmC, g.p);
   if (I8 && g.p.tensor_qp != nullptr)
     return launch_ex(gemm_tc_kernel<BN, I8, PAIR, I8>, dim3(g.grid), dim3(kThreads), GemmCfg<BN, PAIR>::SMEM, s,
                      PAIR ? 2 : 0, g.tmA, PAIR ? g.tmB2 : g.tmB, g.tmC, g.p);

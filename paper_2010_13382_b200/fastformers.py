@@ -25,6 +25,7 @@ FF_OPT_ATTN_TC = 3
 FF_OPT_FUSED_EPILOGUES = 4
 FF_OPT_PDL = 5
 FF_OPT_ACT_QUANT = 6
+FF_OPT_GEMM_MC = 7
 KERNEL_KINDS = ["embed_ln", "gemm_f16", "gemm_i8", "attention", "quant_rows", "add_ln", "head"]
 STATUS_NAMES = ["FF_OK", "FF_E_INVALID", "FF_E_SHAPE", "FF_E_STATE", "FF_E_CUDA", "FF_E_INPUT", "FF_E_UNSUPPORTED",
                 "FF_E_NOMEM"]
@@ -214,6 +215,12 @@ class Encoder:
 
 
 # ------------------------------------------------------------ debug entry points
+def set_gemm_mc(on: bool):
+    """FF_OPT_GEMM_MC (process-wide): CTA-pair GEMMs in clusters of two pairs
+    sharing W k-blocks by TMA multicast."""
+    check(lib().ff_set_option(None, FF_OPT_GEMM_MC, 1 if on else 0))
+
+
 def gemm(A, W, out_mode=0, bias=None, sx=None, sw=None, act=-1, out=None, cta_pair=None):
     """C = A W^T through the production tcgen05 kernel.  A [M,K], W [N,K]: both
     int8 (kind::i8) or both fp16 (kind::f16) CUDA tensors with 16-byte aligned rows."""
