@@ -37,7 +37,8 @@ def _compile(src: str, verbose: bool) -> str:
     newest_dep = max(os.path.getmtime(p) for p in headers() + [src])
     if os.path.exists(obj) and os.path.getmtime(obj) >= newest_dep:
         return obj
-    cmd = [NVCC, *ARCH, *FLAGS, "-Xptxas", "-v" if verbose else "-O3", "-c", src, "-o", obj]
+    extra = os.environ.get("FF_NVCC_EXTRA", "").split()  # experiment-only defines
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-Xptxas", "-v" if verbose else "-O3", "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
