@@ -250,6 +250,49 @@ FF_API ff_status ff_debug_attention_q8(const void *d_qkv16, const int32_t *d_mas
                                        int32_t d, void *d_ctx16, int8_t *d_ctxq, float *d_ctxs, uint64_t *d_trace,
                                        void *stream);
 
+/* ------------------------------------------------------------------------
+ * Structured-pruning importance scores (PAPER.md P:93:
+ * "we add a mask variable to each attention head for the gradient computation
+ * of the heads.  Next, we run forward and backward passes of the model on the
+ * entire validation data set, then the absolute values of the gradients are
+ * accumulated.")  A scorer holds the UNPRUNED model in fp32 and, per batch,
+ * runs the encoder forward keeping its activations, the classifier's mean
+ * cross-entropy against the labels (DESIGN R24), and the backward pass, adding
+ * |dL/dxi[l][h]| (head mask on the context of head h, R23) and |dL/dnu[l][f]|
+ * (FFN-unit mask after the activation) to fp64 score arrays.  Selection and
+ * reconnection of the kept units ("re-group and reconnect") are host
+ * steps (paper_2010_13382_b200/pruning.py) whose result is a new ff_config.
+ * Errors: ff_scorer_last_error() (thread-local).  Same call order as the
+ * model: create -> memory -> bind -> load_weights x N -> finalize -> score*.
+ * cfg: as for ff_model_create (dtype ignored: fp32 throughout; C <= 64);
+ * workspace grows with max_tokens * (layers x (12 H + 4 D + 2 F + A * max_positions)). */
+typedef struct ff_scorer ff_scorer;
+FF_API const char *ff_scorer_last_error(void);
+FF_API ff_status ff_scorer_create(const ff_config *cfg, int32_t cuda_device, ff_scorer **out);
+/* fp32 weight arena and workspace sizes (bytes) the caller must allocate. */
+FF_API ff_status ff_scorer_memory(const ff_scorer *s, size_t *weight_bytes, size_t *workspace_bytes);
+/* Caller-owned device arenas, 256-byte aligned, at least the sizes above. */
+FF_API ff_status ff_scorer_bind_memory(ff_scorer *s, void *d_weights, size_t weight_bytes, void *d_workspace,
+                                       size_t workspace_bytes);
+/* Same HF names / shapes as ff_load_weights (fp32 host data, copied before
+ * return); FF_E_SHAPE for an unknown name or a wrong shape. */
+FF_API ff_status ff_scorer_load_weights(ff_scorer *s, const char *name, const float *h_data, const int64_t *shape,
+                                        int32_t rank, void *stream);
+/* FF_E_STATE unless every tensor was loaded. */
+FF_API ff_status ff_scorer_finalize(ff_scorer *s, void *stream);
+/* One batch (device buffers, async on `stream`): d_ids / d_mask int32 [B, S]
+ * (mask[b][0] must be 1), d_labels int32 [B] in [0, C).  Accumulates into
+ * d_head_scores fp64 [num_layers x max_l heads[l]] and d_ffn_scores fp64
+ * [num_layers x max_l ffn_dim[l]] (row l holds layer l's units; the caller
+ * zeroes them before the first batch).  d_loss (optional) fp32 [1] receives
+ * this batch's mean cross-entropy, d_logits (optional) fp32 [B x C] its
+ * logits.  FF_E_SHAPE if B*S > max_tokens or S > max_positions. */
+FF_API ff_status ff_score_batch(ff_scorer *s, const int32_t *d_ids, const int32_t *d_mask, const int32_t *d_labels,
+                                int32_t batch, int32_t seq, double *d_head_scores, double *d_ffn_scores,
+                                float *d_loss, float *d_logits, void *stream);
+/* Frees host state only (the arenas belong to the caller). */
+FF_API void ff_scorer_destroy(ff_scorer *s);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,748 @@
+// importance.cu -- structured-pruning importance scores on the GPU (SURVEY
+// 8(f) NEXT-3): "we add a mask variable to each attention head
+// for the gradient computation of the heads.  Next, we run forward and
+// backward passes of the model on the entire validation data set, then the
+// absolute values of the gradients are accumulated."
+//
+// One ff_score_batch call = the fp32 encoder forward of the UNPRUNED model
+// with every activation the backward needs kept in the workspace, the
+// classifier's mean cross-entropy (DESIGN R24), then the reverse pass layer by
+// layer down to layer 0's input, reducing on the way
+//   dL/dxi[l,h] = sum_{t, j in head h} ctx[t,j] * dctx[t,j]     (head mask, R23)
+//   dL/dnu[l,f] = sum_t act[t,f] * dact[t,f]                     (FFN-unit mask)
+// and adding their absolute values to fp64 score arrays.
+// Masks are 1, so the forward is the plain encoder (post-LN BERT, R1-R4, R10,
+// R16); the masked keys get probability 0 and padded rows carry no gradient.
+//
+// First version: fp32 throughout, contractions on a generic strided batched
+// SIMT SGEMM (64x64 tiles, 4x4 per thread) -- this pass runs once over a
+// validation set, offline; it is not the serving hot path.  Parity against
+// the fp64 oracle (oracle/importance.py) in tests/test_gpu_importance.py.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fastformers.h"
+#include "ff_kernels.h"
+
+namespace {
+
+thread_local std::string g_serr;
+ff_status sfail(ff_status s, const std::string& msg) {
+  g_serr = msg;
+  return s;
+}
+#define SC_CK(x)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (x);                                                                \
+    if (e_ != cudaSuccess) return sfail(FF_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// ------------------------------------------------------------------ SGEMM
+// C[z](m, n) (+)= alpha * sum_k A[z](m, k) * B[z](k, n) (+ bias[n]) with
+// z = b * nh + h and arbitrary element strides: every transpose of the
+// forward / backward contractions is a stride choice.
+struct SG {
+  const float* A;
+  long long sAb, sAh, sAm, sAk;
+  const float* B;
+  long long sBb, sBh, sBk, sBn;
+  float* C;
+  long long sCb, sCh, sCm;  // n stride 1
+  const float* bias;
+  int M, N, K, nh;
+  float alpha;
+  int accumulate;
+};
+
+constexpr int TBM = 64, TBN = 64, TBK = 16;
+
+__global__ void __launch_bounds__(256) sgemm_kernel(SG g) {
+  __shared__ float As[TBK][TBM + 4];
+  __shared__ float Bs[TBK][TBN + 4];
+  const int z = blockIdx.z, zb = z / g.nh, zh = z - zb * g.nh;
+  const float* A = g.A + zb * g.sAb + zh * g.sAh;
+  const float* B = g.B + zb * g.sBb + zh * g.sBh;
+  float* C = g.C + zb * g.sCb + zh * g.sCh;
+  const int m0 = blockIdx.y * TBM, n0 = blockIdx.x * TBN;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const bool a_kfast = g.sAk == 1, b_nfast = g.sBn == 1;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < g.K; k0 += TBK) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = tid + i * 256;
+      const int mm = a_kfast ? e / TBK : e % TBM, kk = a_kfast ? e % TBK : e / TBM;
+      const int m = m0 + mm, k = k0 + kk;
+      As[kk][mm] = (m < g.M && k < g.K) ? A[m * g.sAm + k * g.sAk] : 0.0f;
+      const int nn = b_nfast ? e % TBN : e / TBK, kb = b_nfast ? e / TBN : e % TBK;
+      const int n = n0 + nn, k2 = k0 + kb;
+      Bs[kb][nn] = (n < g.N && k2 < g.K) ? B[k2 * g.sBk + n * g.sBn] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TBK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[i] = As[kk][ty + 16 * i];
+        b[i] = Bs[kk][tx + 16 * i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty + 16 * i;
+    if (m >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx + 16 * j;
+      if (n >= g.N) continue;
+      float v = g.alpha * acc[i][j];
+      if (g.bias) v += g.bias[n];
+      float* c = C + m * g.sCm + n;
+      *c = g.accumulate ? *c + v : v;
+    }
+  }
+}
+
+cudaError_t sgemm(const SG& g, int nz, cudaStream_t s) {
+  dim3 grid((g.N + TBN - 1) / TBN, (g.M + TBM - 1) / TBM, nz);
+  sgemm_kernel<<<grid, 256, 0, s>>>(g);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------- row reductions
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.0f;
+  for (int i = 0; i < nw; ++i) t += red[i];  // fixed order: deterministic
+  return t;
+}
+__device__ __forceinline__ float block_max(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = -INFINITY;
+  for (int i = 0; i < nw; ++i) t = fmaxf(t, red[i]);
+  return t;
+}
+
+// y = LN(x) per row (biased variance, eps inside the sqrt); keeps xh and rstd.
+// x = a + b (b may be null); embedding variant gathers a row of the tables.
+__device__ void ln_row(const float* x, int H, const float* gam, const float* bet, float eps, float* y, float* xh,
+                       float* rstd_out, float* red) {
+  float s = 0.0f;
+  for (int j = threadIdx.x; j < H; j += blockDim.x) s += x[j];
+  const float mu = block_sum(s, red) / H;
+  float v = 0.0f;
+  for (int j = threadIdx.x; j < H; j += blockDim.x) {
+    const float t = x[j] - mu;
+    v += t * t;
+  }
+  const float rs = rsqrtf(block_sum(v, red) / H + eps);
+  for (int j = threadIdx.x; j < H; j += blockDim.x) {
+    const float h = (x[j] - mu) * rs;
+    if (xh) xh[j] = h;
+    y[j] = h * gam[j] + bet[j];
+  }
+  if (threadIdx.x == 0 && rstd_out) *rstd_out = rs;
+}
+
+__global__ void embed_ln_f32_kernel(const int* ids, int S, int H, const float* tok, const float* pos,
+                                    const float* type0, const float* g, const float* b, float eps, float* X) {
+  extern __shared__ float sm[];
+  float* row = sm;
+  float* red = sm + H;
+  const int r = blockIdx.x, si = r % S;
+  const float* t = tok + (size_t)ids[r] * H;
+  const float* p = pos + (size_t)si * H;
+  for (int j = threadIdx.x; j < H; j += blockDim.x) row[j] = t[j] + p[j] + type0[j];
+  ln_row(row, H, g, b, eps, X + (size_t)r * H, nullptr, nullptr, red);
+}
+
+__global__ void add_ln_f32_kernel(const float* a, const float* r, int H, const float* g, const float* b, float eps,
+                                  float* y, float* xh, float* rstd) {
+  extern __shared__ float sm[];
+  float* row = sm;
+  float* red = sm + H;
+  const size_t o = (size_t)blockIdx.x * H;
+  for (int j = threadIdx.x; j < H; j += blockDim.x) row[j] = a[o + j] + r[o + j];
+  ln_row(row, H, g, b, eps, y + o, xh + o, rstd + blockIdx.x, red);
+}
+
+// dX = rstd * (dxh - mean(dxh) - xh * mean(dxh * xh)), dxh = dY * gamma.
+__global__ void ln_bwd_kernel(const float* dy, const float* g, const float* xh, const float* rstd, int H, float* dx) {
+  extern __shared__ float red[];
+  const size_t o = (size_t)blockIdx.x * H;
+  float s1 = 0.0f, s2 = 0.0f;
+  for (int j = threadIdx.x; j < H; j += blockDim.x) {
+    const float d = dy[o + j] * g[j];
+    s1 += d;
+    s2 += d * xh[o + j];
+  }
+  const float m1 = block_sum(s1, red) / H;
+  const float m2 = block_sum(s2, red) / H;
+  const float rs = rstd[blockIdx.x];
+  for (int j = threadIdx.x; j < H; j += blockDim.x) dx[o + j] = rs * (dy[o + j] * g[j] - m1 - xh[o + j] * m2);
+}
+
+// P = softmax(scale * S) over the valid keys of the row (masked keys: 0).
+// Rows: z = (b, h), i; S buffer [B, A, S, S].
+__global__ void softmax_fwd_kernel(float* P, const int* mask, int S, int A, float scale) {
+  __shared__ float red[32];
+  const size_t row = blockIdx.x;
+  const int b = (int)(row / ((size_t)A * S));
+  float* p = P + row * S;
+  const int* mk = mask + (size_t)b * S;
+  float mx = -INFINITY;
+  for (int j = threadIdx.x; j < S; j += blockDim.x)
+    if (mk[j]) mx = fmaxf(mx, p[j] * scale);
+  mx = block_max(mx, red);
+  float sum = 0.0f;
+  for (int j = threadIdx.x; j < S; j += blockDim.x) {
+    const float e = mk[j] ? expf(p[j] * scale - mx) : 0.0f;
+    p[j] = e;
+    sum += e;
+  }
+  const float inv = 1.0f / block_sum(sum, red);
+  for (int j = threadIdx.x; j < S; j += blockDim.x) p[j] *= inv;
+}
+
+// dS = scale * P * (dP - sum_j P dP), in place on dP.
+__global__ void softmax_bwd_kernel(const float* P, float* dP, int S, float scale) {
+  __shared__ float red[32];
+  const size_t o = (size_t)blockIdx.x * S;
+  float s = 0.0f;
+  for (int j = threadIdx.x; j < S; j += blockDim.x) s += P[o + j] * dP[o + j];
+  const float t = block_sum(s, red);
+  for (int j = threadIdx.x; j < S; j += blockDim.x) dP[o + j] = scale * P[o + j] * (dP[o + j] - t);
+}
+
+__device__ __forceinline__ float act_f(float u, int act) {
+  if (act == ff::ACT_GELU) return 0.5f * u * (1.0f + erff(u * 0.70710678118654752f));
+  if (act == ff::ACT_RELU) return fmaxf(u, 0.0f);
+  const float c = 0.7978845608028654f;
+  return 0.5f * u * (1.0f + tanhf(c * (u + 0.044715f * u * u * u)));
+}
+__device__ __forceinline__ float act_g(float u, int act) {
+  if (act == ff::ACT_GELU)
+    return 0.5f * (1.0f + erff(u * 0.70710678118654752f)) + u * expf(-0.5f * u * u) * 0.3989422804014327f;
+  if (act == ff::ACT_RELU) return u > 0.0f ? 1.0f : 0.0f;
+  const float c = 0.7978845608028654f;
+  const float t = tanhf(c * (u + 0.044715f * u * u * u));
+  return 0.5f * (1.0f + t) + 0.5f * u * (1.0f - t * t) * c * (1.0f + 3.0f * 0.044715f * u * u);
+}
+__global__ void act_fwd_kernel(const float* U, float* Aout, size_t n, int act) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    Aout[i] = act_f(U[i], act);
+}
+__global__ void act_bwd_kernel(const float* U, float* dA, size_t n, int act) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dA[i] *= act_g(U[i], act);
+}
+
+// Classifier head of sequence b, forward and backward (block per sequence):
+// pool = tanh(Wp x0 + bp), logits = Wc pool + bc, loss_b = CE; writes
+// dX[b*S + 0, :] = Wp^T ((Wc^T dlogits) * (1 - pool^2)), dlogits = (p - y) / B.
+__global__ void head_fwd_bwd_kernel(const float* X, int S, int H, int C, int B, const float* Wp, const float* bp,
+                                    const float* Wc, const float* bc, const int* labels, float* dX, float* loss_b,
+                                    float* logits_out) {
+  extern __shared__ float sm[];
+  float* x0 = sm;            // [H]
+  float* pool = sm + H;      // [H]
+  float* dpre = sm + 2 * H;  // [H]
+  float* lg = sm + 3 * H;    // [C] (C <= 64)
+  float* red = lg + 64;
+  const int b = blockIdx.x;
+  const float* xr = X + (size_t)b * S * H;
+  for (int j = threadIdx.x; j < H; j += blockDim.x) x0[j] = xr[j];
+  __syncthreads();
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int o = w; o < H; o += nw) {  // warp per pooler output
+    float s = 0.0f;
+    for (int j = l; j < H; j += 32) s += Wp[(size_t)o * H + j] * x0[j];
+#pragma unroll
+    for (int q = 16; q > 0; q >>= 1) s += __shfl_xor_sync(0xffffffffu, s, q);
+    if (l == 0) pool[o] = tanhf(s + bp[o]);
+  }
+  __syncthreads();
+  for (int c = w; c < C; c += nw) {
+    float s = 0.0f;
+    for (int j = l; j < H; j += 32) s += Wc[(size_t)c * H + j] * pool[j];
+#pragma unroll
+    for (int q = 16; q > 0; q >>= 1) s += __shfl_xor_sync(0xffffffffu, s, q);
+    if (l == 0) lg[c] = s + bc[c];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float mx = -INFINITY;
+    for (int c = 0; c < C; ++c) mx = fmaxf(mx, lg[c]);
+    float se = 0.0f;
+    for (int c = 0; c < C; ++c) se += expf(lg[c] - mx);
+    const float lse = logf(se);
+    loss_b[b] = lse - (lg[labels[b]] - mx);
+    for (int c = 0; c < C; ++c) {
+      if (logits_out) logits_out[(size_t)b * C + c] = lg[c];
+      lg[c] = (expf(lg[c] - mx - lse) - (c == labels[b] ? 1.0f : 0.0f)) / (float)B;  // dlogits
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < H; j += blockDim.x) {
+    float s = 0.0f;
+    for (int c = 0; c < C; ++c) s += Wc[(size_t)c * H + j] * lg[c];
+    dpre[j] = s * (1.0f - pool[j] * pool[j]);
+  }
+  __syncthreads();
+  float* dx0 = dX + (size_t)b * S * H;
+  for (int j = threadIdx.x; j < H; j += blockDim.x) {
+    float s = 0.0f;
+    for (int o = 0; o < H; ++o) s += Wp[(size_t)o * H + j] * dpre[o];
+    dx0[j] = s;
+  }
+  (void)red;
+}
+
+__global__ void loss_mean_kernel(const float* loss_b, int B, float* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    float s = 0.0f;
+    for (int b = 0; b < B; ++b) s += loss_b[b];
+    *out = s / B;
+  }
+}
+
+// colg[c] = sum_r X[r, c] * dX[r, c] over M rows (fixed order per column):
+// block = 32 columns x 8 row groups.
+__global__ void colprod_kernel(const float* X, const float* dX, int M, int ncols, int ld, float* colg) {
+  __shared__ float part[8][33];
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31), rg = threadIdx.x >> 5;
+  float s = 0.0f;
+  if (c < ncols)
+    for (int r = rg; r < M; r += 8) s += X[(size_t)r * ld + c] * dX[(size_t)r * ld + c];
+  part[rg][threadIdx.x & 31] = s;
+  __syncthreads();
+  if (rg == 0 && c < ncols) {
+    float t = 0.0f;
+    for (int i = 0; i < 8; ++i) t += part[i][threadIdx.x & 31];
+    colg[c] = t;
+  }
+}
+// scores[u] += | sum_{c in [u*group, +group)} colg[c] |
+__global__ void group_abs_add_kernel(const float* colg, int units, int group, double* scores) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= units) return;
+  double s = 0.0;
+  for (int i = 0; i < group; ++i) s += (double)colg[u * group + i];
+  scores[u] += fabs(s);
+}
+
+__global__ void copy_kernel(const float* a, float* b, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    b[i] = a[i];
+}
+
+size_t al(size_t x) { return (x + 255) / 256 * 256; }
+
+const char* kSLayer[16] = {
+    "attention.self.query.weight", "attention.self.key.weight", "attention.self.value.weight",
+    "attention.self.query.bias", "attention.self.key.bias", "attention.self.value.bias",
+    "attention.output.dense.weight", "attention.output.dense.bias", "attention.output.LayerNorm.weight",
+    "attention.output.LayerNorm.bias", "intermediate.dense.weight", "intermediate.dense.bias",
+    "output.dense.weight", "output.dense.bias", "output.LayerNorm.weight", "output.LayerNorm.bias"};
+
+struct SLayer {
+  int A, D, F;
+  size_t wqkv, bqkv, wo, bo, g1, b1, w1, bi1, w2, bi2, g2, b2;  // weight offsets
+  size_t X, QKV, P, Cx, Y1, XH1, R1, U, Act, XH2, R2;          // saved activations (workspace)
+  uint32_t loaded = 0;
+};
+
+}  // namespace
+
+struct ff_scorer {
+  ff_config cfg;
+  std::vector<int> heads, ffn;
+  int device = 0, state = 0;
+  std::vector<SLayer> L;
+  size_t tok, pos, type0, eg, eb, pw, pb, cw, cb;
+  uint32_t top_loaded = 0;
+  size_t wbytes = 0, wsbytes = 0;
+  size_t Xout, dX, dZ, dY1, dAm, dC, dP, dQKV, colg, lossb, ids, mask, labels;
+  int Dmax = 0, Fmax = 0, Amax = 0;
+  uint8_t* dW = nullptr;
+  uint8_t* dWS = nullptr;
+  float* w(size_t o) const { return reinterpret_cast<float*>(dW + o); }
+  float* ws(size_t o) const { return reinterpret_cast<float*>(dWS + o); }
+};
+
+namespace {
+
+void plan_scorer(ff_scorer* m) {
+  const ff_config& c = m->cfg;
+  const size_t H = c.hidden, M = c.max_tokens, Sm = c.max_positions;
+  size_t o = 0;
+  auto take = [&](size_t floats) {
+    const size_t r = o;
+    o = al(o + floats * 4);
+    return r;
+  };
+  m->tok = take((size_t)c.vocab_size * H);
+  m->pos = take(Sm * H);
+  m->type0 = take(H);
+  m->eg = take(H);
+  m->eb = take(H);
+  m->L.resize(c.num_layers);
+  for (int l = 0; l < c.num_layers; ++l) {
+    SLayer& P = m->L[l];
+    P.A = m->heads[l];
+    P.D = P.A * c.head_dim;
+    P.F = m->ffn[l];
+    m->Dmax = std::max(m->Dmax, P.D);
+    m->Fmax = std::max(m->Fmax, P.F);
+    m->Amax = std::max(m->Amax, P.A);
+    P.wqkv = take((size_t)3 * P.D * H);
+    P.bqkv = take((size_t)3 * P.D);
+    P.wo = take(H * P.D);
+    P.bo = take(H);
+    P.g1 = take(H);
+    P.b1 = take(H);
+    P.w1 = take((size_t)P.F * H);
+    P.bi1 = take(P.F);
+    P.w2 = take(H * P.F);
+    P.bi2 = take(H);
+    P.g2 = take(H);
+    P.b2 = take(H);
+  }
+  m->pw = take(H * H);
+  m->pb = take(H);
+  m->cw = take((size_t)c.num_classes * H);
+  m->cb = take(c.num_classes);
+  m->wbytes = o;
+
+  o = 0;
+  for (int l = 0; l < c.num_layers; ++l) {
+    SLayer& P = m->L[l];
+    P.X = take(M * H);
+    P.QKV = take(M * 3 * P.D);
+    P.P = take(M * P.A * Sm);  // [B, A, S, S] = M * A * S floats
+    P.Cx = take(M * P.D);
+    P.Y1 = take(M * H);
+    P.XH1 = take(M * H);
+    P.R1 = take(M);
+    P.U = take(M * P.F);
+    P.Act = take(M * P.F);
+    P.XH2 = take(M * H);
+    P.R2 = take(M);
+  }
+  m->Xout = take(M * H);
+  m->dX = take(M * H);
+  m->dZ = take(M * H);
+  m->dY1 = take(M * H);
+  m->dAm = take(M * m->Fmax);
+  m->dC = take(M * m->Dmax);
+  m->dP = take(M * m->Amax * Sm);
+  m->dQKV = take(M * 3 * m->Dmax);
+  m->colg = take(std::max(m->Fmax, m->Dmax));
+  m->lossb = take(M);
+  m->wsbytes = o;
+}
+
+SG lin(const float* X, int M, int K, const float* W, const float* bias, float* Y, int N) {
+  // Y[M, N] = X[M, K] W[N, K]^T + bias
+  SG g{};
+  g.A = X; g.sAm = K; g.sAk = 1;
+  g.B = W; g.sBk = 1; g.sBn = K;
+  g.C = Y; g.sCm = N;
+  g.bias = bias; g.M = M; g.N = N; g.K = K; g.nh = 1; g.alpha = 1.0f;
+  return g;
+}
+SG lin_back(const float* dY, int M, int N, const float* W, int K, float* dX, bool acc) {
+  // dX[M, K] (+)= dY[M, N] W[N, K]
+  SG g{};
+  g.A = dY; g.sAm = N; g.sAk = 1;
+  g.B = W; g.sBk = K; g.sBn = 1;
+  g.C = dX; g.sCm = K;
+  g.M = M; g.N = K; g.K = N; g.nh = 1; g.alpha = 1.0f; g.accumulate = acc ? 1 : 0;
+  return g;
+}
+
+ff_status launch_ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) return sfail(FF_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return FF_OK;
+}
+#define SL(x, what)                                   \
+  do {                                                \
+    ff_status s_ = launch_ck((x), what);              \
+    if (s_ != FF_OK) return s_;                       \
+  } while (0)
+
+int rows_threads(int H) { return H >= 512 ? 256 : 128; }
+
+ff_status score_batch(ff_scorer* m, const int* ids, const int* mask, const int* labels, int B, int S, double* hsc,
+                      double* fsc, float* loss, float* logits, cudaStream_t s) {
+  const ff_config& c = m->cfg;
+  const int H = c.hidden, d = c.head_dim, M = B * S, C = c.num_classes;
+  const float scale = 1.0f / sqrtf((float)d);
+  const int rt = rows_threads(H);
+  const size_t lnsm = (size_t)(H + 32) * 4;
+  // ---- forward, keeping what the backward needs
+  embed_ln_f32_kernel<<<M, rt, lnsm, s>>>(ids, S, H, m->w(m->tok), m->w(m->pos), m->w(m->type0), m->w(m->eg),
+                                          m->w(m->eb), c.ln_eps, m->ws(m->L[0].X));
+  SL(cudaGetLastError(), "embed_ln");
+  for (int l = 0; l < c.num_layers; ++l) {
+    SLayer& P = m->L[l];
+    const int A = P.A, D = P.D, F = P.F;
+    float* X = m->ws(P.X);
+    float* QKV = m->ws(P.QKV);
+    SL(sgemm(lin(X, M, H, m->w(P.wqkv), m->w(P.bqkv), QKV, 3 * D), 1, s), "qkv");
+    // S = Q K^T per (b, h) into P, then softmax in place
+    SG g{};
+    g.A = QKV; g.sAb = (long long)S * 3 * D; g.sAh = d; g.sAm = 3 * D; g.sAk = 1;
+    g.B = QKV + D; g.sBb = (long long)S * 3 * D; g.sBh = d; g.sBk = 1; g.sBn = 3 * D;
+    g.C = m->ws(P.P); g.sCb = (long long)A * S * S; g.sCh = (long long)S * S; g.sCm = S;
+    g.M = S; g.N = S; g.K = d; g.nh = A; g.alpha = 1.0f;
+    SL(sgemm(g, B * A, s), "qk");
+    softmax_fwd_kernel<<<B * A * S, 128, 0, s>>>(m->ws(P.P), mask, S, A, scale);
+    SL(cudaGetLastError(), "softmax");
+    // ctx = P V
+    g = SG{};
+    g.A = m->ws(P.P); g.sAb = (long long)A * S * S; g.sAh = (long long)S * S; g.sAm = S; g.sAk = 1;
+    g.B = QKV + 2 * D; g.sBb = (long long)S * 3 * D; g.sBh = d; g.sBk = 3 * D; g.sBn = 1;
+    g.C = m->ws(P.Cx); g.sCb = (long long)S * D; g.sCh = d; g.sCm = D;
+    g.M = S; g.N = d; g.K = S; g.nh = A; g.alpha = 1.0f;
+    SL(sgemm(g, B * A, s), "pv");
+    float* O = m->ws(m->dZ);  // scratch for the projection outputs
+    SL(sgemm(lin(m->ws(P.Cx), M, D, m->w(P.wo), m->w(P.bo), O, H), 1, s), "oproj");
+    add_ln_f32_kernel<<<M, rt, lnsm, s>>>(O, X, H, m->w(P.g1), m->w(P.b1), c.ln_eps, m->ws(P.Y1), m->ws(P.XH1),
+                                          m->ws(P.R1));
+    SL(cudaGetLastError(), "ln1");
+    SL(sgemm(lin(m->ws(P.Y1), M, H, m->w(P.w1), m->w(P.bi1), m->ws(P.U), F), 1, s), "ffn1");
+    act_fwd_kernel<<<1184, 256, 0, s>>>(m->ws(P.U), m->ws(P.Act), (size_t)M * F, c.act);
+    SL(cudaGetLastError(), "act");
+    SL(sgemm(lin(m->ws(P.Act), M, F, m->w(P.w2), m->w(P.bi2), O, H), 1, s), "ffn2");
+    float* Xn = l + 1 < c.num_layers ? m->ws(m->L[l + 1].X) : m->ws(m->Xout);
+    add_ln_f32_kernel<<<M, rt, lnsm, s>>>(O, m->ws(P.Y1), H, m->w(P.g2), m->w(P.b2), c.ln_eps, Xn, m->ws(P.XH2),
+                                          m->ws(P.R2));
+    SL(cudaGetLastError(), "ln2");
+  }
+  // ---- head: loss and the gradient at position 0 of the last layer
+  SC_CK(cudaMemsetAsync(m->ws(m->dX), 0, (size_t)M * H * 4, s));
+  head_fwd_bwd_kernel<<<B, 256, (size_t)(3 * H + 64 + 32) * 4, s>>>(
+      m->ws(m->Xout), S, H, C, B, m->w(m->pw), m->w(m->pb), m->w(m->cw), m->w(m->cb), labels, m->ws(m->dX),
+      m->ws(m->lossb), logits);
+  SL(cudaGetLastError(), "head");
+  if (loss) {
+    loss_mean_kernel<<<1, 32, 0, s>>>(m->ws(m->lossb), B, loss);
+    SL(cudaGetLastError(), "loss");
+  }
+  // ---- backward, layer by layer
+  const int sc_ld = std::max(m->Amax, 1);
+  for (int l = c.num_layers - 1; l >= 0; --l) {
+    SLayer& P = m->L[l];
+    const int A = P.A, D = P.D, F = P.F;
+    float* dX = m->ws(m->dX);
+    float* dZ = m->ws(m->dZ);
+    float* dY1 = m->ws(m->dY1);
+    float* dAm = m->ws(m->dAm);
+    ln_bwd_kernel<<<M, rt, 32 * 4, s>>>(dX, m->w(P.g2), m->ws(P.XH2), m->ws(P.R2), H, dZ);  // d(o2 + y1)
+    SL(cudaGetLastError(), "ln2 bwd");
+    SL(sgemm(lin_back(dZ, M, H, m->w(P.w2), F, dAm, false), 1, s), "ffn2 bwd");  // d(act * nu)
+    colprod_kernel<<<(F + 31) / 32, 256, 0, s>>>(m->ws(P.Act), dAm, M, F, F, m->ws(m->colg));
+    group_abs_add_kernel<<<(F + 127) / 128, 128, 0, s>>>(m->ws(m->colg), F, 1, fsc + (size_t)l * m->Fmax);
+    act_bwd_kernel<<<1184, 256, 0, s>>>(m->ws(P.U), dAm, (size_t)M * F, c.act);
+    copy_kernel<<<1184, 256, 0, s>>>(dZ, dY1, (size_t)M * H);
+    SL(sgemm(lin_back(dAm, M, F, m->w(P.w1), H, dY1, true), 1, s), "ffn1 bwd");
+    ln_bwd_kernel<<<M, rt, 32 * 4, s>>>(dY1, m->w(P.g1), m->ws(P.XH1), m->ws(P.R1), H, dZ);  // d(o + x)
+    SL(cudaGetLastError(), "ln1 bwd");
+    float* dC = m->ws(m->dC);
+    SL(sgemm(lin_back(dZ, M, H, m->w(P.wo), D, dC, false), 1, s), "oproj bwd");
+    colprod_kernel<<<(D + 31) / 32, 256, 0, s>>>(m->ws(P.Cx), dC, M, D, D, m->ws(m->colg));
+    group_abs_add_kernel<<<1, 128, 0, s>>>(m->ws(m->colg), A, d, hsc + (size_t)l * sc_ld);
+    // attention backward per (b, h)
+    float* QKV = m->ws(P.QKV);
+    float* dQKV = m->ws(m->dQKV);
+    float* dP = m->ws(m->dP);
+    const float* Pm = m->ws(P.P);
+    SG g{};  // dP = dC V^T
+    g.A = dC; g.sAb = (long long)S * D; g.sAh = d; g.sAm = D; g.sAk = 1;
+    g.B = QKV + 2 * D; g.sBb = (long long)S * 3 * D; g.sBh = d; g.sBk = 1; g.sBn = 3 * D;
+    g.C = dP; g.sCb = (long long)A * S * S; g.sCh = (long long)S * S; g.sCm = S;
+    g.M = S; g.N = S; g.K = d; g.nh = A; g.alpha = 1.0f;
+    SL(sgemm(g, B * A, s), "dP");
+    g = SG{};  // dV = P^T dC
+    g.A = Pm; g.sAb = (long long)A * S * S; g.sAh = (long long)S * S; g.sAm = 1; g.sAk = S;
+    g.B = dC; g.sBb = (long long)S * D; g.sBh = d; g.sBk = D; g.sBn = 1;
+    g.C = dQKV + 2 * D; g.sCb = (long long)S * 3 * D; g.sCh = d; g.sCm = 3 * D;
+    g.M = S; g.N = d; g.K = S; g.nh = A; g.alpha = 1.0f;
+    SL(sgemm(g, B * A, s), "dV");
+    softmax_bwd_kernel<<<B * A * S, 128, 0, s>>>(Pm, dP, S, scale);  // dP -> dS (scaled)
+    SL(cudaGetLastError(), "softmax bwd");
+    g = SG{};  // dQ = dS K
+    g.A = dP; g.sAb = (long long)A * S * S; g.sAh = (long long)S * S; g.sAm = S; g.sAk = 1;
+    g.B = QKV + D; g.sBb = (long long)S * 3 * D; g.sBh = d; g.sBk = 3 * D; g.sBn = 1;
+    g.C = dQKV; g.sCb = (long long)S * 3 * D; g.sCh = d; g.sCm = 3 * D;
+    g.M = S; g.N = d; g.K = S; g.nh = A; g.alpha = 1.0f;
+    SL(sgemm(g, B * A, s), "dQ");
+    g = SG{};  // dK = dS^T Q
+    g.A = dP; g.sAb = (long long)A * S * S; g.sAh = (long long)S * S; g.sAm = 1; g.sAk = S;
+    g.B = QKV; g.sBb = (long long)S * 3 * D; g.sBh = d; g.sBk = 3 * D; g.sBn = 1;
+    g.C = dQKV + D; g.sCb = (long long)S * 3 * D; g.sCh = d; g.sCm = 3 * D;
+    g.M = S; g.N = d; g.K = S; g.nh = A; g.alpha = 1.0f;
+    SL(sgemm(g, B * A, s), "dK");
+    if (l > 0) {  // gradient w.r.t. the layer input (residual + QKV path)
+      copy_kernel<<<1184, 256, 0, s>>>(dZ, dX, (size_t)M * H);
+      SL(sgemm(lin_back(dQKV, M, 3 * D, m->w(P.wqkv), H, dX, true), 1, s), "qkv bwd");
+    }
+  }
+  return FF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ff_scorer_last_error(void) { return g_serr.c_str(); }
+
+ff_status ff_scorer_create(const ff_config* cfg, int32_t cuda_device, ff_scorer** out) {
+  if (!cfg || !out) return sfail(FF_E_INVALID, "null argument");
+  if (cfg->abi_version != FF_ABI_VERSION) return sfail(FF_E_INVALID, "abi_version mismatch");
+  if (cfg->num_layers < 1 || cfg->hidden < 1 || cfg->head_dim < 1 || cfg->vocab_size < 1 ||
+      cfg->max_positions < 1 || cfg->num_classes < 1 || cfg->num_classes > 64 || cfg->max_tokens < 1 ||
+      !cfg->heads || !cfg->ffn_dim || cfg->act < 0 || cfg->act > 2)
+    return sfail(FF_E_INVALID, "invalid config");
+  auto* m = new ff_scorer();
+  m->cfg = *cfg;
+  m->heads.assign(cfg->heads, cfg->heads + cfg->num_layers);
+  m->ffn.assign(cfg->ffn_dim, cfg->ffn_dim + cfg->num_layers);
+  for (int l = 0; l < cfg->num_layers; ++l)
+    if (m->heads[l] < 1 || m->ffn[l] < 1) {
+      delete m;
+      return sfail(FF_E_INVALID, "heads / ffn_dim must be >= 1");
+    }
+  m->cfg.heads = m->heads.data();
+  m->cfg.ffn_dim = m->ffn.data();
+  m->cfg.dtype = nullptr;
+  m->device = cuda_device;
+  plan_scorer(m);
+  *out = m;
+  return FF_OK;
+}
+
+ff_status ff_scorer_memory(const ff_scorer* m, size_t* weight_bytes, size_t* workspace_bytes) {
+  if (!m || !weight_bytes || !workspace_bytes) return sfail(FF_E_INVALID, "null argument");
+  *weight_bytes = m->wbytes;
+  *workspace_bytes = m->wsbytes;
+  return FF_OK;
+}
+
+ff_status ff_scorer_bind_memory(ff_scorer* m, void* d_weights, size_t wbytes, void* d_workspace, size_t wsbytes) {
+  if (!m || !d_weights || !d_workspace) return sfail(FF_E_INVALID, "null argument");
+  if (wbytes < m->wbytes || wsbytes < m->wsbytes) return sfail(FF_E_INVALID, "arena too small");
+  if (((uintptr_t)d_weights | (uintptr_t)d_workspace) & 255) return sfail(FF_E_INVALID, "arenas must be 256-B aligned");
+  m->dW = static_cast<uint8_t*>(d_weights);
+  m->dWS = static_cast<uint8_t*>(d_workspace);
+  m->state = 1;
+  return FF_OK;
+}
+
+ff_status ff_scorer_load_weights(ff_scorer* m, const char* name, const float* host, const int64_t* shape,
+                                 int32_t rank, void* stream) {
+  if (!m || !name || !host || !shape) return sfail(FF_E_INVALID, "null argument");
+  if (m->state < 1) return sfail(FF_E_STATE, "bind memory first");
+  std::string n(name);
+  for (const char* p : {"bert.", "roberta."})
+    if (n.compare(0, std::strlen(p), p) == 0) n = n.substr(std::strlen(p));
+  const int H = m->cfg.hidden, d = m->cfg.head_dim;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  size_t numel = 1;
+  for (int i = 0; i < rank; ++i) numel *= (size_t)shape[i];
+  auto put = [&](size_t off, size_t expect) -> ff_status {
+    if (numel != expect) return sfail(FF_E_SHAPE, "wrong shape for " + std::string(name));
+    SC_CK(cudaMemcpyAsync(m->dW + off, host, numel * 4, cudaMemcpyHostToDevice, s));
+    SC_CK(cudaStreamSynchronize(s));  // host buffer may be freed after return
+    return FF_OK;
+  };
+  const ff_config& c = m->cfg;
+  if (n == "embeddings.word_embeddings.weight") { m->top_loaded |= 1; return put(m->tok, (size_t)c.vocab_size * H); }
+  if (n == "embeddings.position_embeddings.weight") {
+    if (shape[0] < c.max_positions) return sfail(FF_E_SHAPE, "position table shorter than max_positions");
+    numel = (size_t)c.max_positions * H;
+    m->top_loaded |= 2;
+    return put(m->pos, numel);
+  }
+  if (n == "embeddings.token_type_embeddings.weight") { numel = H; m->top_loaded |= 4; return put(m->type0, H); }
+  if (n == "embeddings.LayerNorm.weight") { m->top_loaded |= 8; return put(m->eg, H); }
+  if (n == "embeddings.LayerNorm.bias") { m->top_loaded |= 16; return put(m->eb, H); }
+  if (n == "pooler.dense.weight" || n == "classifier.dense.weight") { m->top_loaded |= 32; return put(m->pw, (size_t)H * H); }
+  if (n == "pooler.dense.bias" || n == "classifier.dense.bias") { m->top_loaded |= 64; return put(m->pb, H); }
+  if (n == "classifier.weight" || n == "classifier.out_proj.weight") { m->top_loaded |= 128; return put(m->cw, (size_t)c.num_classes * H); }
+  if (n == "classifier.bias" || n == "classifier.out_proj.bias") { m->top_loaded |= 256; return put(m->cb, c.num_classes); }
+  int l = -1, used = 0;
+  if (std::sscanf(n.c_str(), "encoder.layer.%d.%n", &l, &used) == 1 && l >= 0 && l < c.num_layers) {
+    const std::string key = n.substr(used);
+    SLayer& P = m->L[l];
+    const size_t D = P.D, F = P.F;
+    for (int k = 0; k < 16; ++k) {
+      if (key != kSLayer[k]) continue;
+      P.loaded |= 1u << k;
+      switch (k) {
+        case 0: case 1: case 2: return put(P.wqkv + (size_t)k * D * H * 4, D * H);
+        case 3: case 4: case 5: return put(P.bqkv + (size_t)(k - 3) * D * 4, D);
+        case 6: return put(P.wo, (size_t)H * D);
+        case 7: return put(P.bo, H);
+        case 8: return put(P.g1, H);
+        case 9: return put(P.b1, H);
+        case 10: return put(P.w1, F * H);
+        case 11: return put(P.bi1, F);
+        case 12: return put(P.w2, (size_t)H * F);
+        case 13: return put(P.bi2, H);
+        case 14: return put(P.g2, H);
+        default: return put(P.b2, H);
+      }
+    }
+  }
+  (void)d;
+  return sfail(FF_E_SHAPE, "unknown tensor " + std::string(name));
+}
+
+ff_status ff_scorer_finalize(ff_scorer* m, void* stream) {
+  if (!m) return sfail(FF_E_INVALID, "null argument");
+  if (m->state < 1) return sfail(FF_E_STATE, "bind memory first");
+  if (m->top_loaded != 511u) return sfail(FF_E_STATE, "missing embedding / pooler / classifier tensors");
+  for (auto& P : m->L)
+    if (P.loaded != 0xFFFFu) return sfail(FF_E_STATE, "missing layer tensors");
+  (void)stream;
+  m->state = 2;
+  return FF_OK;
+}
+
+ff_status ff_score_batch(ff_scorer* m, const int32_t* d_ids, const int32_t* d_mask, const int32_t* d_labels,
+                         int32_t batch, int32_t seq, double* d_head_scores, double* d_ffn_scores, float* d_loss,
+                         float* d_logits, void* stream) {
+  if (!m || !d_ids || !d_mask || !d_labels || !d_head_scores || !d_ffn_scores)
+    return sfail(FF_E_INVALID, "null argument");
+  if (m->state != 2) return sfail(FF_E_STATE, "ff_scorer_finalize first");
+  if (batch < 1 || seq < 1 || seq > m->cfg.max_positions || (int64_t)batch * seq > m->cfg.max_tokens)
+    return sfail(FF_E_SHAPE, "batch * seq exceeds max_tokens or seq > max_positions");
+  return score_batch(m, d_ids, d_mask, d_labels, batch, seq, d_head_scores, d_ffn_scores, d_loss, d_logits,
+                     static_cast<cudaStream_t>(stream));
+}
+
+void ff_scorer_destroy(ff_scorer* m) { delete m; }
+
+}  // extern "C"

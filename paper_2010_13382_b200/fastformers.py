@@ -33,7 +33,9 @@ STATUS_NAMES = ["FF_OK", "FF_E_INVALID", "FF_E_SHAPE", "FF_E_STATE", "FF_E_CUDA"
 EXPORTED = ["ff_abi_version", "ff_last_error", "ff_model_create", "ff_model_memory", "ff_bind_memory",
             "ff_load_weights", "ff_finalize", "ff_encode", "ff_encode_host", "ff_check", "ff_set_option",
             "ff_model_destroy", "ff_launch_count", "ff_profile", "ff_encode_trace", "ff_debug_gemm", "ff_debug_quant_rows",
-            "ff_debug_attention", "ff_debug_attention_q8", "ff_debug_set_trace"]
+            "ff_debug_attention", "ff_debug_attention_q8", "ff_debug_set_trace",
+            "ff_scorer_last_error", "ff_scorer_create", "ff_scorer_memory", "ff_scorer_bind_memory",
+            "ff_scorer_load_weights", "ff_scorer_finalize", "ff_score_batch", "ff_scorer_destroy"]
 
 
 class FFError(RuntimeError):
@@ -82,8 +84,18 @@ def lib():
         L.ff_debug_attention.argtypes = [vp, vp, i32, i32, i32, i32, vp, i32, vp]
         L.ff_debug_attention_q8.argtypes = [vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp]
         L.ff_debug_set_trace.argtypes = [vp, i32]
+        L.ff_scorer_last_error.restype = ctypes.c_char_p
+        L.ff_scorer_create.argtypes = [ctypes.POINTER(FFConfig), i32, ctypes.POINTER(vp)]
+        L.ff_scorer_memory.argtypes = [vp, ctypes.POINTER(sz), ctypes.POINTER(sz)]
+        L.ff_scorer_bind_memory.argtypes = [vp, vp, sz, vp, sz]
+        L.ff_scorer_load_weights.argtypes = [vp, ctypes.c_char_p, vp, ctypes.POINTER(ctypes.c_int64), i32, vp]
+        L.ff_scorer_finalize.argtypes = [vp, vp]
+        L.ff_score_batch.argtypes = [vp, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp]
+        L.ff_scorer_destroy.argtypes = [vp]
+        L.ff_scorer_destroy.restype = None
         for name in EXPORTED:
-            if name not in ("ff_abi_version", "ff_last_error", "ff_model_destroy"):
+            if name not in ("ff_abi_version", "ff_last_error", "ff_model_destroy", "ff_scorer_last_error",
+                            "ff_scorer_destroy"):
                 getattr(L, name).restype = i32
         _lib = L
     return _lib
@@ -281,3 +293,74 @@ def set_gemm_trace(trace=None, which=0):
     [grid, 64, 24]) — which = 0: subsequent debug GEMMs; 1/2/3: the layer-0
     fused out-proj+LN / FFN1+requant / FFN2+LN of subsequent forwards."""
     check(lib().ff_debug_set_trace(_ptr(trace) if trace is not None else None, which))
+
+
+def _scheck(status: int):
+    if status != FF_OK:
+        raise FFError(status, lib().ff_scorer_last_error().decode(errors="replace"))
+
+
+class Scorer:
+    """Structured-pruning importance scorer on one GPU (C-ABI ff_scorer_*;
+    SURVEY 8(f) NEXT-3, PAPER.md P:93).  Holds the UNPRUNED model in fp32;
+    ``score(ids, mask, labels)`` adds |dL/dmask| of every head and FFN unit
+    to ``head_scores`` [L, max heads] / ``ffn_scores`` [L, max ffn] (fp64,
+    device) and returns the batch's mean cross-entropy (device scalar)."""
+
+    def __init__(self, cfg, weights: Dict[str, np.ndarray], max_tokens: Optional[int] = None, device: int = 0):
+        import torch
+        L = lib()
+        self.cfg = cfg
+        self.device = torch.device("cuda", device)
+        self._heads = (ctypes.c_int32 * cfg.num_layers)(*cfg.heads)
+        self._ffn = (ctypes.c_int32 * cfg.num_layers)(*cfg.ffn_dim)
+        self._dt = (ctypes.c_int32 * cfg.num_layers)(*([0] * cfg.num_layers))
+        self.max_tokens = int(max_tokens or cfg.batch * cfg.seq)
+        c = FFConfig(1, cfg.num_layers, cfg.hidden, cfg.head_dim, cfg.vocab_size, cfg.max_positions,
+                     cfg.num_classes, float(cfg.ln_eps), int(cfg.act), self._heads, self._ffn, self._dt,
+                     self.max_tokens)
+        h = ctypes.c_void_p()
+        _scheck(L.ff_scorer_create(ctypes.byref(c), device, ctypes.byref(h)))
+        self.h = h
+        wb, wsb = ctypes.c_size_t(), ctypes.c_size_t()
+        _scheck(L.ff_scorer_memory(self.h, ctypes.byref(wb), ctypes.byref(wsb)))
+        with torch.cuda.device(self.device):
+            self.weight_arena = torch.empty(wb.value, dtype=torch.uint8, device=self.device)
+            self.workspace = torch.empty(wsb.value, dtype=torch.uint8, device=self.device)
+            _scheck(L.ff_scorer_bind_memory(self.h, _ptr(self.weight_arena), wb.value, _ptr(self.workspace),
+                                            wsb.value))
+            st = _stream_ptr()
+            for name, w in weights.items():
+                a = np.ascontiguousarray(w, dtype=np.float32)
+                shape = (ctypes.c_int64 * a.ndim)(*a.shape)
+                _scheck(L.ff_scorer_load_weights(self.h, name.encode(), ctypes.c_void_p(a.ctypes.data), shape,
+                                                 a.ndim, st))
+            _scheck(L.ff_scorer_finalize(self.h, st))
+            self.head_scores = torch.zeros((cfg.num_layers, max(cfg.heads)), dtype=torch.float64,
+                                           device=self.device)
+            self.ffn_scores = torch.zeros((cfg.num_layers, max(cfg.ffn_dim)), dtype=torch.float64,
+                                          device=self.device)
+            self.loss = torch.zeros(1, dtype=torch.float32, device=self.device)
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and _lib is not None:
+            _lib.ff_scorer_destroy(h)
+
+    def reset(self):
+        self.head_scores.zero_()
+        self.ffn_scores.zero_()
+
+    def score(self, ids, mask, labels, logits=None, stream=None):
+        B, S = ids.shape
+        nul = ctypes.c_void_p(None)
+        _scheck(lib().ff_score_batch(self.h, _ptr(ids), _ptr(mask), _ptr(labels), B, S, _ptr(self.head_scores),
+                                     _ptr(self.ffn_scores), _ptr(self.loss),
+                                     _ptr(logits) if logits is not None else nul, _stream_ptr(stream)))
+        return self.loss
+
+    def scores(self):
+        """(head_scores [L][A_l], ffn_scores [L][F_l]) as numpy, trimmed per layer."""
+        hs, fs = self.head_scores.cpu().numpy(), self.ffn_scores.cpu().numpy()
+        return ([hs[l, :self.cfg.heads[l]] for l in range(self.cfg.num_layers)],
+                [fs[l, :self.cfg.ffn_dim[l]] for l in range(self.cfg.num_layers)])

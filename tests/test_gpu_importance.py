@@ -1,0 +1,113 @@
+"""GPU parity of the importance scorer (C-ABI ff_score_batch; SURVEY 8(f)
+NEXT-3) against the fp64 oracle (oracle/importance.py).
+
+Tolerance: the scorer runs fp32 end to end; a score is a sum over
+B*S tokens of products of forward activations and back-propagated gradients,
+so its fp32-vs-fp64 error is relative to the layer's score scale, not to the
+(possibly cancelling) score itself: |gpu - ref| <= 1e-4 |ref| + 2e-5 max_l(ref)
+(measured, tools/importance_err.py: <= 2.2e-6 of the layer max on all three
+configs, so the bound has ~10x headroom)."""
+import numpy as np
+import pytest
+
+from oracle import importance as imp
+from paper_2010_13382_b200 import fastformers as ffb
+from paper_2010_13382_b200 import pruning, synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _batch(cfg, B, S, seed, ragged=True):
+    rng = np.random.default_rng(seed)
+    ids = rng.integers(5, cfg.vocab_size, (B, S)).astype(np.int32)
+    ids[:, 0] = cfg.cls_id
+    mask = np.ones((B, S), np.int32)
+    if ragged:
+        for b in range(B):
+            mask[b, rng.integers(max(1, S // 4), S + 1):] = 0
+    labels = rng.integers(0, cfg.num_classes, B).astype(np.int32)
+    return ids, mask, labels
+
+
+def _cuda(*arrs):
+    return [torch.from_numpy(a).cuda() for a in arrs]
+
+
+def _close(gpu, ref):
+    for l, (g, r) in enumerate(zip(gpu, ref)):
+        tol = 1e-4 * np.abs(r) + 2e-5 * np.abs(r).max()
+        bad = np.abs(g - r) > tol
+        assert not bad.any(), (l, np.abs(g - r).max(), np.abs(r).max(), int(bad.sum()))
+
+
+def _tiny():
+    return synth.ModelConfig("tiny_score", 2, 32, 8, [4, 3], [16, 12], [0, 0], 50, 16, 3, 1e-12, batch=3, seq=7,
+                             cls_id=1)
+
+
+CONFIGS = [
+    ("tiny", _tiny, 3, 7, 0.3),
+    ("c2_shape", lambda: synth.config("c2"), 8, 64, 0.02),               # TinyBERT 4L/312/12 heads d=26/1200
+    ("c3_unpruned", lambda: synth.config("c3_unpruned"), 4, 64, 0.02),   # distilroberta 6L/768/12/3072
+]
+
+
+@pytest.mark.parametrize("name,mk,B,S,std", CONFIGS)
+def test_scores_match_oracle(name, mk, B, S, std):
+    cfg = mk()
+    w = synth.make_weights(cfg, std=std)
+    batches = [_batch(cfg, B, S, 100 + i) for i in range(2)]
+    sc = ffb.Scorer(cfg, w, max_tokens=B * S)
+    losses = []
+    for ids, mask, labels in batches:
+        lg = torch.empty((B, cfg.num_classes), dtype=torch.float32, device="cuda")
+        loss = sc.score(*_cuda(ids, mask, labels), logits=lg)
+        losses.append(float(loss.item()))
+        ref_loss, ref_logits, _, _ = imp.forward_backward(cfg, w, ids, mask, labels)
+        assert abs(losses[-1] - ref_loss) <= 1e-5 * max(1.0, abs(ref_loss))
+        np.testing.assert_allclose(lg.cpu().numpy(), ref_logits, rtol=0, atol=1e-4)
+    hs, fs = sc.scores()
+    rh, rf, _ = imp.compute_importance(cfg, w, batches)
+    _close(hs, rh)
+    _close(fs, rf)
+
+
+def test_dead_head_exactly_zero_and_padding_inert():
+    cfg = synth.config("c2")
+    w = synth.make_weights(cfg)
+    d = cfg.head_dim
+    w["encoder.layer.1.attention.output.dense.weight"][:, 5 * d:6 * d] = 0.0
+    ids, mask, labels = _batch(cfg, 6, 48, 7)
+    sc = ffb.Scorer(cfg, w, max_tokens=6 * 64)
+    sc.score(*_cuda(ids, mask, labels))
+    hs, fs = sc.scores()
+    assert hs[1][5] == 0.0 and (np.delete(hs[1], 5) > 0).all()
+    # the same sequences padded to S = 64: same scores up to fp32 reduction order
+    ids2 = np.concatenate([ids, np.full((6, 16), 9, np.int32)], axis=1)
+    mask2 = np.concatenate([mask, np.zeros((6, 16), np.int32)], axis=1)
+    sc.reset()
+    sc.score(*_cuda(ids2, mask2, labels))
+    hs2, fs2 = sc.scores()
+    _close(hs2, hs)
+    _close(fs2, fs)
+
+
+def test_selection_from_gpu_scores_matches_oracle():
+    """Top-k per layer (R25) from GPU scores equals the oracle's, for
+    units whose score is not within the fp32 tolerance of the k-th boundary."""
+    cfg = synth.config("c2")
+    w = synth.make_weights(cfg)
+    batches = [_batch(cfg, 8, 64, 300 + i) for i in range(2)]
+    sc = ffb.Scorer(cfg, w, max_tokens=8 * 64)
+    for b in batches:
+        sc.score(*_cuda(*b))
+    hs, fs = sc.scores()
+    rh, rf, _ = imp.compute_importance(cfg, w, batches)
+    for gs, rs, keep in ((hs, rh, 6), (fs, rf, 600)):
+        for l in range(cfg.num_layers):
+            kept_gpu = set(pruning.select_keep(gs[l], keep))
+            kept_ref = set(imp.select_keep(rs[l], keep))
+            kth = np.sort(rs[l])[::-1][keep - 1]
+            near = {i for i in range(len(rs[l])) if abs(rs[l][i] - kth) <= 1e-4 * kth + 2e-5 * rs[l].max()}
+            assert kept_gpu - near == kept_ref - near, l
