@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-variants", action="store_true", help="skip the fp16 side measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dynamic", action="store_true", help="skip the dynamic-length batching side measurement")
+    ap.add_argument("--no-importance", action="store_true", help="skip the importance-scoring side measurement")
     ap.add_argument("--fused", type=int, default=None,
                     help="1/0: force the fused GEMM+LayerNorm / GEMM+requant epilogues on/off (default: library default)")
     return ap.parse_args()
@@ -177,6 +178,64 @@ def dynamic_length_variant(cfg, enc, B, S, stream, flush, n_batches=16, lo=None,
     for mode in batching.MODES:
         out["modes"][mode]["speedup_vs_fixed"] = out["modes"][mode]["value"] / f
     return out
+
+
+def importance_variant(stream, flush, B=32, S=128, n=10):
+    """the GPU importance-scoring pass (forward +
+    backward + mask-gradient reductions, ff_score_batch) on the UNPRUNED
+    distilroberta shape the paper prunes, B x S synthetic labelled
+    batches.  Device time per batch (CUDA events, L2 flushed), algorithmic
+    FLOPs (forward GEMMs + attention + the backward's input-gradient GEMMs and
+    4 attention-backward GEMMs; no weight gradients are needed) against the
+    fp32 FMA peak (148 SMs x 128 lanes x 2 x max SM clock), and the
+    fp64 oracle timed on one sequence on one host core for context."""
+    import numpy as np
+    import torch
+    from paper_2010_13382_b200 import synth
+    from paper_2010_13382_b200.fastformers import Scorer
+
+    cfg = synth.config("c3_unpruned")
+    w = synth.make_weights(cfg)
+    sc = Scorer(cfg, w, max_tokens=B * S)
+    rng = np.random.default_rng(77)
+    data = []
+    for k in range(4):
+        ids, mask = synth.make_inputs(cfg, B, S, seed=5000 + k)
+        labels = rng.integers(0, cfg.num_classes, B).astype(np.int32)
+        data.append([torch.from_numpy(a).cuda() for a in (ids, mask, labels)])
+    for k in range(2):
+        sc.score(*data[k % 4])
+    torch.cuda.synchronize()
+    ts = []
+    for k in range(n):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sc.score(*data[k % 4])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = sorted(ts)[len(ts) // 2]
+    H, d = cfg.hidden, cfg.head_dim
+    fwd = cfg.flops_per_seq(S) * B
+    lin = sum(2.0 * S * (H * 3 * A * d + A * d * H + 2 * H * F) for A, F in zip(cfg.heads, cfg.ffn_dim)) * B
+    lin -= 2.0 * S * H * 3 * cfg.heads[0] * d * B  # layer 0's input gradient is not needed
+    att = sum(2.0 * 2 * A * S * S * d for A in cfg.heads) * B
+    flops = fwd + lin + 2 * att
+    peaks, _ = load_peaks()
+    peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    ach = flops / (ms / 1e3) / 1e12
+    from oracle import importance as imp
+    ids, mask, labels = (t[:1].cpu().numpy() for t in data[0])
+    t0 = time.perf_counter()
+    imp.forward_backward(cfg, w, ids, mask, labels)
+    t_or = time.perf_counter() - t0
+    return {"workload": f"c3_unpruned (6L H768 12 heads FFN 3072, P:97) importance scoring, batch {B} x seq {S}",
+            "value": B / (ms / 1e3), "unit": "sequences/s", "ms_per_batch": ms,
+            "roofline": {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                         "algorithmic": f"{flops / 1e9:.1f} GFLOP per batch (fwd + input-gradient bwd)"},
+            "cpu_baseline": {"value": 1.0 / t_or, "unit": "sequences/s", "cores": 1, "kind": "oracle",
+                           "sample": "1 sequence, numpy fp64 forward + backward"}}
 
 
 def cpu_baseline(cfg, weights, ids, mask, per_core=8):
@@ -428,6 +487,8 @@ def run_ours(args):
             del encpt
         if not args.no_dynamic:
             variants["dynamic_length"] = dynamic_length_variant(cfg, enc, B, S, stream, flush)
+        if not args.no_importance:
+            variants["importance_scoring"] = importance_variant(stream, flush)
 
     if world > 1:
         dist.barrier()
