@@ -248,8 +248,36 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     auto pair_sync = [pair_bar]() { asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory"); };
     __half2 amax2 = __float2half2_rn(0.0f);  // |ctx| max of the row over the heads epilogued so far
 
+    // Q8row of a finished item (R6-R8) is applied lazily: its packed fp16 ctx
+    // stays parked in TMEM and head j of it is quantized and stored by the
+    // epilogue of head j of the CTA's NEXT item, right before that head parks
+    // its own ctx in the same columns (all fused items have nh = A <= 8 heads),
+    // so no epilogue stalls on a whole item's requant; the CTA's last item is
+    // flushed after the loop.  Per row: its scale (sc, rs), sequence and head base.
+    bool qpend = false;
+    int qb = 0, qhbase = 0;
+    float qsc = 1.0f, qrs = 1.0f;
+    auto flush_head = [&](int j) {  // quantize + store parked head j of the pending item
+      uint32_t v[16];
+      tmem_ld16(trow + kTmemCtx + j * 32 + half * 16, v);
+      tmem_wait_ld();
+      uint32_t w[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float2 a0 = __half22float2(*reinterpret_cast<const __half2*>(&v[2 * i]));
+        const float2 a1 = __half22float2(*reinterpret_cast<const __half2*>(&v[2 * i + 1]));
+        w[i] = q8_quant4(a0, a1, qsc, qrs);
+      }
+      if (r < S) {  // this thread's 32 s8 values: one full 32-byte sector of the row
+        uint4* dst = reinterpret_cast<uint4*>(ctxq + ((size_t)qb * S + r) * ldq + (qhbase + j) * kD + half * 32);
+        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+      }
+    };
+
     // ctx epilogue of head m = head h of sequence b (local index hl): R16(O),
-    // fp16 store and/or parking in TMEM; after the item's last head, Q8row.
+    // fp16 store and/or parking in TMEM; after the item's last head, its row
+    // scale (the row amax over all heads).
     auto epilogue = [&](uint32_t m, int b, int h, int hl, bool last, int nh) {
       const int os = m & 1;
       const size_t grow = (size_t)b * S + r;
@@ -273,59 +301,24 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         for (int c = 0; c < 4; ++c) dst[c] = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
       }
       if (!fuse_q) return;
+      if (qpend) flush_head(hl);  // frees parking slot hl (the load completed above)
       tmem_st16(trow + kTmemCtx + hl * 32 + half * 16, pk);
       if (!last) return;
-      // Q8row of the whole ctx row (R6-R8): amax over both halves, then
-      // quantize the parked fp16 values
+      // row amax over both halves -> this item's row scale; its heads are
+      // quantized by the next item's epilogues (or after the loop)
       tmem_wait_st();
       redAmax[half * kQ + r] = fmaxf(__low2float(amax2), __high2float(amax2));
       pair_sync();
       const float am = fmaxf(redAmax[r], redAmax[kQ + r]);
+      pair_sync();  // both partners read redAmax before the next item's writes
       amax2 = __float2half2_rn(0.0f);
-      const float sc = q8_scale(am);
-      const float rs = __frcp_rn(sc);
-      const int hbase = h - hl;
-      // Stage the s8 rows in the P buffer O(m) just finished reading (free
-      // until softmax(m+2)), 4 heads (128 x 256 B) per pass, 16-byte chunk cc
-      // of row r at [cc / 8][r][(cc % 8) ^ (r % 8)]; then store whole rows
-      // coalesced (one half-warp per 256-byte row segment).
-      uint8_t* stage = smem + SmemTC::P + (m & 1) * 2 * kTileBytes;
-      const int sw = (warp - 2);
-      for (int j0 = 0; j0 < nh; j0 += 4) {
-        const int nj = min(4, nh - j0);
-#pragma unroll 1
-        for (int jj = 0; jj < nj; ++jj) {
-          uint32_t v[1][16];
-          tmem_ld16(trow + kTmemCtx + (j0 + jj) * 32 + half * 16, v[0]);
-          tmem_wait_ld();
-          uint32_t w[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float2 a0 = __half22float2(*reinterpret_cast<const __half2*>(&v[0][2 * i]));
-            const float2 a1 = __half22float2(*reinterpret_cast<const __half2*>(&v[0][2 * i + 1]));
-            w[i] = q8_quant4(a0, a1, sc, rs);
-          }
-#pragma unroll
-          for (int k = 0; k < 2; ++k) {
-            const int cc = jj * 4 + half * 2 + k;
-            *reinterpret_cast<uint4*>(stage + (cc >> 3) * kTileBytes + r * 128 + (((cc & 7) ^ (r & 7)) << 4)) =
-                make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
-          }
-        }
-        softmax_sync();
-        const int cc = lane & 15;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int row = sw * 16 + i * 2 + (lane >> 4);
-          if (cc < nj * 4 && row < S) {
-            const uint4 val =
-                *reinterpret_cast<const uint4*>(stage + (cc >> 3) * kTileBytes + row * 128 + (((cc & 7) ^ (row & 7)) << 4));
-            *reinterpret_cast<uint4*>(ctxq + ((size_t)b * S + row) * ldq + (hbase + j0) * kD + cc * 16) = val;
-          }
-        }
-        softmax_sync();
-      }
-      if (half == 0 && r < S) ctxs[grow] = sc;
+      qsc = q8_scale(am);
+      qrs = __frcp_rn(qsc);
+      qb = b;
+      qhbase = h - hl;
+      qpend = true;
+      (void)nh;
+      if (half == 0 && r < S) ctxs[grow] = qsc;
       if (threadIdx.x == 64) trace_ev(trace, m, 7);
     };
 
@@ -420,6 +413,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       plast = it.hl == it.nh - 1;
     }
     if (pend) epilogue(n - 1, pb, ph_, phl, plast, pnh);
+    if (qpend)
+      for (int j = 0; j < pnh; ++j) flush_head(j);
   }
   tc_fence_before();
   __syncthreads();
