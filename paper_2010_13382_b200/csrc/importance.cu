@@ -14,9 +14,10 @@
 // Masks are 1, so the forward is the plain encoder (post-LN BERT, R1-R4, R10,
 // R16); the masked keys get probability 0 and padded rows carry no gradient.
 //
-// First version: fp32 throughout, contractions on a generic strided batched
-// SIMT SGEMM (64x64 tiles, 4x4 per thread) -- this pass runs once over a
-// validation set, offline; it is not the serving hot path.  Parity against
+// fp32 throughout; every contraction runs on a generic strided batched SIMT
+// SGEMM (128x128 tiles / 8x8 per thread for the linears, 64x64 / 4x4 for the
+// per-head attention products) -- this pass runs once over a validation set,
+// offline; it is not the serving hot path.  Parity against
 // the fp64 oracle (oracle/importance.py) in tests/test_gpu_importance.py.
 #include <cmath>
 #include <cstdio>
@@ -113,9 +114,96 @@ __global__ void __launch_bounds__(256) sgemm_kernel(SG g) {
   }
 }
 
+// Large-tile variant for the encoder linears: 128x128 tiles, 8x8 outputs per
+// thread (rows ty*4 + {0..3} and 64 + ty*4 + {0..3}, same for columns, so the
+// fragment reads are conflict-free LDS.128), k-tiles of 8 double-buffered in
+// smem with the next tile's global loads held in registers during the FMAs.
+constexpr int LBM = 128, LBN = 128, LBK = 8;
+
+__global__ void __launch_bounds__(256, 2) sgemm128_kernel(SG g) {
+  __shared__ __align__(16) float As[2][LBK][LBM + 4];  // +4: conflict-free transposing stores
+  __shared__ __align__(16) float Bs[2][LBK][LBN + 4];
+  const int z = blockIdx.z, zb = z / g.nh, zh = z - zb * g.nh;
+  const float* A = g.A + zb * g.sAb + zh * g.sAh;
+  const float* B = g.B + zb * g.sBb + zh * g.sBh;
+  float* C = g.C + zb * g.sCb + zh * g.sCh;
+  const int m0 = blockIdx.y * LBM, n0 = blockIdx.x * LBN;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const bool a_kfast = g.sAk == 1, b_nfast = g.sBn == 1;
+  float ra[4], rb[4];
+  auto gload = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = tid + i * 256;
+      const int mm = a_kfast ? e / LBK : e % LBM, kk = a_kfast ? e % LBK : e / LBM;
+      const int m = m0 + mm, k = k0 + kk;
+      ra[i] = (m < g.M && k < g.K) ? A[m * g.sAm + k * g.sAk] : 0.0f;
+      const int nn = b_nfast ? e % LBN : e / LBK, kb = b_nfast ? e / LBN : e % LBK;
+      const int n = n0 + nn, k2 = k0 + kb;
+      rb[i] = (n < g.N && k2 < g.K) ? B[k2 * g.sBk + n * g.sBn] : 0.0f;
+    }
+  };
+  auto sstore = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = tid + i * 256;
+      const int mm = a_kfast ? e / LBK : e % LBM, kk = a_kfast ? e % LBK : e / LBM;
+      As[buf][kk][mm] = ra[i];
+      const int nn = b_nfast ? e % LBN : e / LBK, kb = b_nfast ? e / LBN : e % LBK;
+      Bs[buf][kb][nn] = rb[i];
+    }
+  };
+  float acc[8][8] = {};
+  gload(0);
+  sstore(0);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < g.K; k0 += LBK) {
+    const bool more = k0 + LBK < g.K;
+    if (more) gload(k0 + LBK);
+#pragma unroll
+    for (int kk = 0; kk < LBK; ++kk) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][64 + ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][64 + tx * 4]);
+      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    if (more) {
+      sstore(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+    if (m >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+      if (n >= g.N) continue;
+      float v = g.alpha * acc[i][j];
+      if (g.bias) v += g.bias[n];
+      float* c = C + m * g.sCm + n;
+      *c = g.accumulate ? *c + v : v;
+    }
+  }
+}
+
 cudaError_t sgemm(const SG& g, int nz, cudaStream_t s) {
-  dim3 grid((g.N + TBN - 1) / TBN, (g.M + TBM - 1) / TBM, nz);
-  sgemm_kernel<<<grid, 256, 0, s>>>(g);
+  if (g.M >= 256 && g.N >= 256) {
+    dim3 grid((g.N + LBN - 1) / LBN, (g.M + LBM - 1) / LBM, nz);
+    sgemm128_kernel<<<grid, 256, 0, s>>>(g);
+  } else {
+    dim3 grid((g.N + TBN - 1) / TBN, (g.M + TBM - 1) / TBM, nz);
+    sgemm_kernel<<<grid, 256, 0, s>>>(g);
+  }
   return cudaGetLastError();
 }
 
@@ -326,28 +414,32 @@ __global__ void loss_mean_kernel(const float* loss_b, int B, float* out) {
   }
 }
 
-// colg[c] = sum_r X[r, c] * dX[r, c] over M rows (fixed order per column):
-// block = 32 columns x 8 row groups.
+// colg[chunk][c] = sum over the rows of chunk `blockIdx.y` (of kRowChunks) of
+// X[r, c] * dX[r, c] (fixed order): block = 32 columns x 8 row groups.
+constexpr int kRowChunks = 16;
 __global__ void colprod_kernel(const float* X, const float* dX, int M, int ncols, int ld, float* colg) {
   __shared__ float part[8][33];
   const int c = blockIdx.x * 32 + (threadIdx.x & 31), rg = threadIdx.x >> 5;
+  const int rows = (M + kRowChunks - 1) / kRowChunks;
+  const int r0 = blockIdx.y * rows, r1 = min(M, r0 + rows);
   float s = 0.0f;
   if (c < ncols)
-    for (int r = rg; r < M; r += 8) s += X[(size_t)r * ld + c] * dX[(size_t)r * ld + c];
+    for (int r = r0 + rg; r < r1; r += 8) s += X[(size_t)r * ld + c] * dX[(size_t)r * ld + c];
   part[rg][threadIdx.x & 31] = s;
   __syncthreads();
   if (rg == 0 && c < ncols) {
     float t = 0.0f;
     for (int i = 0; i < 8; ++i) t += part[i][threadIdx.x & 31];
-    colg[c] = t;
+    colg[(size_t)blockIdx.y * ncols + c] = t;
   }
 }
-// scores[u] += | sum_{c in [u*group, +group)} colg[c] |
-__global__ void group_abs_add_kernel(const float* colg, int units, int group, double* scores) {
+// scores[u] += | sum_{c in [u*group, +group)} sum_chunks colg[chunk][c] |
+__global__ void group_abs_add_kernel(const float* colg, int ncols, int units, int group, double* scores) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= units) return;
   double s = 0.0;
-  for (int i = 0; i < group; ++i) s += (double)colg[u * group + i];
+  for (int ch = 0; ch < kRowChunks; ++ch)
+    for (int i = 0; i < group; ++i) s += (double)colg[(size_t)ch * ncols + u * group + i];
   scores[u] += fabs(s);
 }
 
@@ -457,7 +549,7 @@ void plan_scorer(ff_scorer* m) {
   m->dC = take(M * m->Dmax);
   m->dP = take(M * m->Amax * Sm);
   m->dQKV = take(M * 3 * m->Dmax);
-  m->colg = take(std::max(m->Fmax, m->Dmax));
+  m->colg = take((size_t)kRowChunks * std::max(m->Fmax, m->Dmax));
   m->lossb = take(M);
   m->wsbytes = o;
 }
@@ -562,8 +654,8 @@ ff_status score_batch(ff_scorer* m, const int* ids, const int* mask, const int* 
     ln_bwd_kernel<<<M, rt, 32 * 4, s>>>(dX, m->w(P.g2), m->ws(P.XH2), m->ws(P.R2), H, dZ);  // d(o2 + y1)
     SL(cudaGetLastError(), "ln2 bwd");
     SL(sgemm(lin_back(dZ, M, H, m->w(P.w2), F, dAm, false), 1, s), "ffn2 bwd");  // d(act * nu)
-    colprod_kernel<<<(F + 31) / 32, 256, 0, s>>>(m->ws(P.Act), dAm, M, F, F, m->ws(m->colg));
-    group_abs_add_kernel<<<(F + 127) / 128, 128, 0, s>>>(m->ws(m->colg), F, 1, fsc + (size_t)l * m->Fmax);
+    colprod_kernel<<<dim3((F + 31) / 32, kRowChunks), 256, 0, s>>>(m->ws(P.Act), dAm, M, F, F, m->ws(m->colg));
+    group_abs_add_kernel<<<(F + 127) / 128, 128, 0, s>>>(m->ws(m->colg), F, F, 1, fsc + (size_t)l * m->Fmax);
     act_bwd_kernel<<<1184, 256, 0, s>>>(m->ws(P.U), dAm, (size_t)M * F, c.act);
     copy_kernel<<<1184, 256, 0, s>>>(dZ, dY1, (size_t)M * H);
     SL(sgemm(lin_back(dAm, M, F, m->w(P.w1), H, dY1, true), 1, s), "ffn1 bwd");
@@ -571,8 +663,8 @@ ff_status score_batch(ff_scorer* m, const int* ids, const int* mask, const int* 
     SL(cudaGetLastError(), "ln1 bwd");
     float* dC = m->ws(m->dC);
     SL(sgemm(lin_back(dZ, M, H, m->w(P.wo), D, dC, false), 1, s), "oproj bwd");
-    colprod_kernel<<<(D + 31) / 32, 256, 0, s>>>(m->ws(P.Cx), dC, M, D, D, m->ws(m->colg));
-    group_abs_add_kernel<<<1, 128, 0, s>>>(m->ws(m->colg), A, d, hsc + (size_t)l * sc_ld);
+    colprod_kernel<<<dim3((D + 31) / 32, kRowChunks), 256, 0, s>>>(m->ws(P.Cx), dC, M, D, D, m->ws(m->colg));
+    group_abs_add_kernel<<<1, 128, 0, s>>>(m->ws(m->colg), D, A, d, hsc + (size_t)l * sc_ld);
     // attention backward per (b, h)
     float* QKV = m->ws(P.QKV);
     float* dQKV = m->ws(m->dQKV);
