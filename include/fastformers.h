@@ -154,8 +154,8 @@ FF_API ff_status ff_check(ff_model *m, void *stream);
 /* FF_OPT_FUSED_EPILOGUES (1: where the output row is 256 x 1..8 columns,
  * fuse residual + LayerNorm (+ s8 requant) into the out-proj / FFN2 GEMM
  * epilogues and the FFN-intermediate requant into FFN1, using clusters that
- * span the row; 0 = default: separate add_ln / quant_rows kernels, currently
- * faster).  With 1, ff_encode_trace does not fill the O16 / Y16 dumps (never
+ * span the row; 0: separate add_ln / quant_rows kernels everywhere; the
+ * default is FF_OPT_FUSED_MASK = 2, the FFN1 fusion only).  With 1, ff_encode_trace does not fill the O16 / Y16 dumps (never
  * materialised). */
 #define FF_OPT_FUSED_EPILOGUES 4
 /* FF_OPT_PDL (1 = default: launch every forward kernel with programmatic
@@ -173,6 +173,12 @@ FF_API ff_status ff_check(ff_model *m, void *stream);
  * pairs stacked along M that share each W k-block by TMA multicast (half the
  * W bytes per SM from L2); 0 = independent pairs.  Results are identical. */
 #define FF_OPT_GEMM_MC 7
+/* FF_OPT_FUSED_MASK: per-fusion control of FF_OPT_FUSED_EPILOGUES (which sets
+ * 0 or 7): bit 0 out-proj + residual + LN1, bit 1 FFN1 + activation + requant
+ * (int8 layers), bit 2 FFN2 + residual + LN2.  Value 0..7; default 2 (the
+ * FFN1 fusion is bit-identical to the separate kernels and measured faster;
+ * the LN fusions change the LN summation order and were slower alone). */
+#define FF_OPT_FUSED_MASK 8
 /* Set `option` to `value` on model m (invalidates its captured graphs).  The
  * process-wide options FF_OPT_PDL and FF_OPT_GEMM_MC may be set with m = NULL.
  * FF_E_INVALID for an unknown option / bad value / NULL m otherwise. */
@@ -186,7 +192,9 @@ FF_API ff_status ff_launch_count(const ff_model *m, int32_t batch, int32_t seq, 
 /* Kernel kinds reported by ff_profile. */
 typedef enum {
   FF_K_EMBED_LN = 0, FF_K_GEMM_F16 = 1, FF_K_GEMM_I8 = 2, FF_K_ATTENTION = 3, FF_K_QUANT = 4,
-  FF_K_ADD_LN = 5, FF_K_HEAD = 6
+  FF_K_ADD_LN = 5, FF_K_HEAD = 6,
+  /* row-reduction GEMMs (FF_OPT_FUSED_MASK): GEMM + fused LayerNorm / requant */
+  FF_K_GEMM_RR_F16 = 7, FF_K_GEMM_RR_I8 = 8
 } ff_kernel_kind;
 
 /* Run one forward WITHOUT graphs with a CUDA-event pair around every kernel

@@ -94,7 +94,8 @@ struct ff_model {
   bool use_graphs = true;
   int pair_mode = -1;  // FF_OPT_CTA_PAIRS: -1 auto, 0 never (GemmPlan::force_pair)
   bool attn_tc = true;  // FF_OPT_ATTN_TC: tcgen05 attention where supported
-  bool fused = false;   // FF_OPT_FUSED_EPILOGUES: cluster row-reduction GEMM epilogues (opt-in)
+  int fused = 2;  // FF_OPT_FUSED_EPILOGUES / _MASK: cluster row-reduction GEMM epilogues,
+                 // bit 0 out-proj + LN1, bit 1 FFN1 + requant (default), bit 2 FFN2 + LN2
   int act_quant = 0;    // FF_OPT_ACT_QUANT: 0 per-row s8, 1 per-tensor u8 + zero point
   ff::AttnTCPlan tm_qkv;  // QKV buffer map for the tcgen05 attention
   std::map<std::tuple<int, int, const void*, const void*, const void*>, cudaGraphExec_t> graphs;
@@ -392,8 +393,9 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     // a4 + a5: requant (int8 layers) and out-projection
     if (q && !att_q && !pt)
       FF_LAUNCH(FF_K_QUANT, ff::launch_quant_rows(CTX, m->ldc16, M, P.D, CTXq, m->ldc8, CTXs, s), "quant ctx");
-    const bool fuse_ln = m->fused && !pt && P.rr_ok[0];
-    const bool fuse_q = m->fused && !pt && q && P.rr_ok[1];
+    const bool fuse_ln = (m->fused & 1) && !pt && P.rr_ok[0];
+    const bool fuse_q = (m->fused & 2) && !pt && q && P.rr_ok[1];
+    const bool fuse_ln2 = (m->fused & 4) && !pt && P.rr_ok[0];
     if (fuse_ln) {
       // a5 + a6 fused: H1 = LN1(R16(O) + X16) (+ s8 rows) in the out-proj epilogue
       ff::RRPlan r = P.rp[0];
@@ -411,7 +413,7 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
       r.p.ldq = m->ldx8;
       r.p.out_scale = q ? H1s : nullptr;
       r.p.trace = (l == 0 && g_debug_trace_which == 1) ? g_debug_trace : nullptr;
-      FF_LAUNCH(q ? FF_K_GEMM_I8 : FF_K_GEMM_F16, ff::launch_rr(r, s), "gemm o + ln1");
+      FF_LAUNCH(q ? FF_K_GEMM_RR_I8 : FF_K_GEMM_RR_F16, ff::launch_rr(r, s), "gemm o + ln1");
     } else {
     g = P.gp[W_O];
     g.force_pair = m->pair_mode;
@@ -447,7 +449,7 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
       r.p.ldq = m->ldi8;
       r.p.out_scale = Is;
       r.p.trace = (l == 0 && g_debug_trace_which == 2) ? g_debug_trace : nullptr;
-      FF_LAUNCH(FF_K_GEMM_I8, ff::launch_rr(r, s), "gemm ffn1 + quant");
+      FF_LAUNCH(FF_K_GEMM_RR_I8, ff::launch_rr(r, s), "gemm ffn1 + quant");
       if (tr && dump(d_dump[5], I16, m->ldi16, P.F, M, s) != FF_OK) return FF_E_CUDA;
     } else {
     g = P.gp[W_FFN1];
@@ -466,7 +468,7 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     if (q && !pt) FF_LAUNCH(FF_K_QUANT, ff::launch_quant_rows(I16, m->ldi16, M, P.F, Iq, m->ldi8, Is, s), "quant ffn");
     }
     const bool nq = l + 1 < c.num_layers && m->L[l + 1].dt == FF_I8 && !pt;
-    if (fuse_ln) {
+    if (fuse_ln2) {
       // a9 + a10 fused: X16 = LN2(R16(Y) + H1) (+ s8 rows for the next int8 layer)
       ff::RRPlan r = P.rp[2];
       ff::plan_rr_set_m(&r, M);
@@ -483,7 +485,7 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
       r.p.ldq = m->ldx8;
       r.p.out_scale = nq ? Xs : nullptr;
       r.p.trace = (l == 0 && g_debug_trace_which == 3) ? g_debug_trace : nullptr;
-      FF_LAUNCH(q ? FF_K_GEMM_I8 : FF_K_GEMM_F16, ff::launch_rr(r, s), "gemm ffn2 + ln2");
+      FF_LAUNCH(q ? FF_K_GEMM_RR_I8 : FF_K_GEMM_RR_F16, ff::launch_rr(r, s), "gemm ffn2 + ln2");
     } else {
     g = P.gp[W_FFN2];
     g.force_pair = m->pair_mode;
@@ -848,7 +850,14 @@ ff_status ff_set_option(ff_model* m, int32_t option, int64_t value) {
     return FF_OK;
   }
   if (option == FF_OPT_FUSED_EPILOGUES) {
-    m->fused = value != 0;
+    m->fused = value != 0 ? 7 : 0;
+    for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
+    m->graphs.clear();
+    return FF_OK;
+  }
+  if (option == FF_OPT_FUSED_MASK) {
+    if (value < 0 || value > 7) return fail(FF_E_INVALID, "FF_OPT_FUSED_MASK must be in 0..7");
+    m->fused = (int)value;
     for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
     m->graphs.clear();
     return FF_OK;
@@ -884,12 +893,13 @@ ff_status ff_launch_count(const ff_model* m, int32_t batch, int32_t seq, int32_t
       n += 7 + (q ? 8 : 0);
       continue;
     }
-    const bool fln = m->fused && P.rr_ok[0], fq = m->fused && P.rr_ok[1];
+    const bool fln = (m->fused & 1) && P.rr_ok[0], fq = (m->fused & 2) && q && P.rr_ok[1];
+    const bool fln2 = (m->fused & 4) && P.rr_ok[0];
     n += 2;                              // QKV GEMM + attention
     n += (q && !attention_fuses_quant(m, P, seq)) ? 1 : 0;  // ctx requant
     n += fln ? 1 : 2;                    // out-proj (+ add_ln1)
     n += fq ? 1 : (q ? 2 : 1);           // FFN1 (+ requant)
-    n += fln ? 1 : 2;                    // FFN2 (+ add_ln2)
+    n += fln2 ? 1 : 2;                   // FFN2 (+ add_ln2)
   }
   *count = n;
   return FF_OK;

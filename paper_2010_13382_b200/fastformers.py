@@ -26,7 +26,9 @@ FF_OPT_FUSED_EPILOGUES = 4
 FF_OPT_PDL = 5
 FF_OPT_ACT_QUANT = 6
 FF_OPT_GEMM_MC = 7
-KERNEL_KINDS = ["embed_ln", "gemm_f16", "gemm_i8", "attention", "quant_rows", "add_ln", "head"]
+FF_OPT_FUSED_MASK = 8
+KERNEL_KINDS = ["embed_ln", "gemm_f16", "gemm_i8", "attention", "quant_rows", "add_ln", "head", "gemm_rr_f16",
+                "gemm_rr_i8"]
 STATUS_NAMES = ["FF_OK", "FF_E_INVALID", "FF_E_SHAPE", "FF_E_STATE", "FF_E_CUDA", "FF_E_INPUT", "FF_E_UNSUPPORTED",
                 "FF_E_NOMEM"]
 
@@ -120,7 +122,7 @@ class Encoder:
     """One FastFormers encoder model on one GPU (weights packed once at load)."""
 
     def __init__(self, cfg, weights: Dict[str, np.ndarray], max_tokens: Optional[int] = None, device: int = 0,
-                 use_graphs: bool = True, cta_pairs: bool = True, attn_tc: bool = True, fused: bool = False,
+                 use_graphs: bool = True, cta_pairs: bool = True, attn_tc: bool = True, fused=None,
                  act_quant: int = 0):
         import torch
         L = lib()
@@ -152,13 +154,25 @@ class Encoder:
             check(L.ff_set_option(self.h, FF_OPT_GRAPHS, 0))
         if not attn_tc:
             check(L.ff_set_option(self.h, FF_OPT_ATTN_TC, 0))
-        check(L.ff_set_option(self.h, FF_OPT_FUSED_EPILOGUES, 1 if fused else 0))
+        # fused: None = library default (FF_OPT_FUSED_MASK 2: FFN1 + requant), False / True
+        # (none / all three fusions) or a FF_OPT_FUSED_MASK bitmask
+        if fused is None:
+            pass
+        elif isinstance(fused, bool):
+            check(L.ff_set_option(self.h, FF_OPT_FUSED_EPILOGUES, 1 if fused else 0))
+        else:
+            check(L.ff_set_option(self.h, FF_OPT_FUSED_MASK, int(fused)))
         self.fused = fused
         # int8 activation quantizer: 0 per-row s8 (default), 1 per-tensor u8 + zero point
         check(L.ff_set_option(self.h, FF_OPT_ACT_QUANT, int(act_quant)))
         self.act_quant = act_quant
         if not cta_pairs:
             check(L.ff_set_option(self.h, FF_OPT_CTA_PAIRS, 0))
+
+    def set_fused(self, mask: int):
+        """FF_OPT_FUSED_MASK: bit 0 out-proj+LN1, bit 1 FFN1+requant, bit 2 FFN2+LN2."""
+        check(lib().ff_set_option(self.h, FF_OPT_FUSED_MASK, int(mask)))
+        self.fused = mask
 
     def __del__(self):
         h = getattr(self, "h", None)

@@ -445,3 +445,21 @@ def test_per_tensor_quantizer_kernel_bit_exact():
     # same u8 tensor, same scale / zero point, exact int32 accumulation and
     # correction, the same fp32 fma epilogue: bit-identical fp16 outputs
     np.testing.assert_array_equal(f32(dumps["qkv"]), qkv_ref)
+
+
+@pytest.mark.parametrize("name,B,S", [("c1", 4, 32), ("c2", 16, 128), ("c3", 256, 128)])
+def test_default_ffn1_fusion_bit_identical_to_separate_kernels(name, B, S):
+    """The default FF_OPT_FUSED_MASK = 2 (FFN1 + GELU + per-row requant in one
+    cluster row-reduction GEMM) computes Q8row from the same R16 values as the
+    separate quant_rows kernel (R12), so the logits are bit-identical to the
+    fully unfused path (mask 0), which the lockstep tests check stage by stage."""
+    cfg = synth.config(name).with_dtype(1).with_batch(B, S)
+    w = synth.make_weights(cfg)
+    ids, mask = synth.make_inputs(cfg, B=B, S=S, ragged=True, seed=77)
+    fused = Encoder(cfg, w)
+    n_fused, n_sep = fused.launch_count(B, S), Encoder(cfg, w, fused=False).launch_count(B, S)
+    fusable = cfg.ffn_dim[0] % 256 == 0  # row = 256 x 1..8 columns (C2's F' = 1200 is not)
+    assert (n_fused < n_sep) if fusable else (n_fused == n_sep)
+    a = fused.encode(dev(ids), dev(mask)).cpu()
+    b = Encoder(cfg, w, fused=False).encode(dev(ids), dev(mask)).cpu()
+    assert torch.equal(a, b)
