@@ -511,6 +511,27 @@ def run_ours(args):
                                               "ms_per_step": tp / 50,
                                               "what": "per-tensor u8 activations + zero point (P:104, DESIGN R22)"}
             del encpt
+        if cfg.dtype[0] == 1:
+            # all three cluster row-reduction epilogues (FF_OPT_FUSED_MASK 7): out-proj + LN1,
+            # FFN1 + requant, FFN2 + LN2 (LN sums in another order: not bit-identical)
+            encf = Encoder(cfg, w, max_tokens=B * S, device=local, fused=7)
+            for k in range(5):
+                encf.encode(dids[k % NB], dmask[k % NB], logits)
+            torch.cuda.synchronize()
+            evf = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(50)]
+            for k in range(50):
+                flush.zero_()
+                evf[k][0].record(stream)
+                encf.encode(dids[k % NB], dmask[k % NB], logits)
+                evf[k][1].record(stream)
+            torch.cuda.synchronize()
+            tf = sum(a.elapsed_time(b) for a, b in evf)
+            variants["fused_ln_epilogues"] = {
+                "value": B * 50 / (tf / 1e3), "unit": "sequences/s", "ms_per_step": tf / 50,
+                "what": "FF_OPT_FUSED_MASK 7: residual + LayerNorm (+ s8 rows) fused into the out-proj / FFN2 "
+                        "GEMM epilogues as well (cluster row reductions); LN sums in another order, so not "
+                        "bit-identical to the default; the GEMM kernels then carry the LN work"}
+            del encf
         if not args.no_dynamic:
             variants["dynamic_length"] = dynamic_length_variant(cfg, enc, B, S, stream, flush)
         if not args.no_importance:

@@ -179,8 +179,13 @@ FF_API ff_status ff_check(ff_model *m, void *stream);
  * FFN1 fusion is bit-identical to the separate kernels and measured faster;
  * the LN fusions change the LN summation order and were slower alone). */
 #define FF_OPT_FUSED_MASK 8
+/* FF_OPT_PDL_RR (process-wide, may be set with m = NULL): 1 = the LN-mode
+ * row-reduction GEMMs (FF_OPT_FUSED_MASK bits 0 / 2) also launch with PDL;
+ * default 0 (with PDL they slowed the step by 5-10%). */
+#define FF_OPT_PDL_RR 9
 /* Set `option` to `value` on model m (invalidates its captured graphs).  The
- * process-wide options FF_OPT_PDL and FF_OPT_GEMM_MC may be set with m = NULL.
+ * process-wide options FF_OPT_PDL, FF_OPT_GEMM_MC and FF_OPT_PDL_RR may be set
+ * with m = NULL.
  * FF_E_INVALID for an unknown option / bad value / NULL m otherwise. */
 FF_API ff_status ff_set_option(ff_model *m, int32_t option, int64_t value);
 

@@ -14,9 +14,18 @@ constexpr int kNumSMs = 148;
 // an optional 1-D cluster (cluster = 0: no cluster attribute).  All
 // forward-pass kernels go through this.
 extern bool g_pdl;
+extern bool g_pdl_rr;  // FF_OPT_PDL_RR: PDL attribute on the row-reduction GEMM launches too
+template <typename... KArgs, typename... Args>
+cudaError_t launch_ex_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                          int cluster, Args... args);
 template <typename... KArgs, typename... Args>
 cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int cluster,
                       Args... args) {
+  return launch_ex_pdl(g_pdl, kern, grid, block, smem, s, cluster, args...);
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_ex_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                          int cluster, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -24,7 +33,7 @@ cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   int n = 0;
-  if (g_pdl) {
+  if (pdl) {
     attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[n].val.programmaticStreamSerializationAllowed = 1;
     ++n;

@@ -1218,8 +1218,10 @@ void plan_rr_set_m(RRPlan* g, int M) {
 
 template <bool I8, int MODE>
 static cudaError_t launch_rr_t(const RRPlan& g, cudaStream_t s) {
-  return launch_ex(gemm_rr_kernel<I8, MODE>, dim3(g.grid), dim3(kRRThreads), RRCfg::SMEM, s, g.cn, g.tmA, g.tmB,
-                   g.tmC, g.tmR, g.tmQ, g.p);
+  // LN-mode row-reduction GEMMs launch without PDL unless FF_OPT_PDL_RR (measured)
+  const bool pdl = g_pdl && (MODE != RR_LN || g_pdl_rr);
+  return launch_ex_pdl(pdl, gemm_rr_kernel<I8, MODE>, dim3(g.grid), dim3(kRRThreads), RRCfg::SMEM, s, g.cn, g.tmA,
+                       g.tmB, g.tmC, g.tmR, g.tmQ, g.p);
 }
 
 template <bool I8, int MODE>
