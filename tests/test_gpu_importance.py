@@ -111,3 +111,27 @@ def test_selection_from_gpu_scores_matches_oracle():
             kth = np.sort(rs[l])[::-1][keep - 1]
             near = {i for i in range(len(rs[l])) if abs(rs[l][i] - kth) <= 1e-4 * kth + 2e-5 * rs[l].max()}
             assert kept_gpu - near == kept_ref - near, l
+
+
+def test_score_prune_reconnect_encode_end_to_end():
+    """P:93 end to end on the GPU: score the unpruned distilroberta shape
+    (ff_score_batch), keep 8 of 12 heads and 1536 of 3072 FFN units per layer
+    (pruning.prune: the C3 geometry), build the pruned int8 encoder from
+    the reconnected weights and check its logits against the C++ oracle of the
+    same pruned model (DESIGN §3 drift bound)."""
+    import oracle
+    cfg = synth.config("c3_unpruned").with_dtype(1)
+    w = synth.make_weights(cfg)
+    sc = ffb.Scorer(cfg, w, max_tokens=8 * 64)
+    for i in range(2):
+        sc.score(*_cuda(*_batch(cfg, 8, 64, 900 + i)))
+    hs, fs = sc.scores()
+    pcfg, pw, kept_h, kept_f = pruning.prune(cfg, w, hs, fs, head_ratio=8 / 12, ffn_ratio=0.5)
+    assert pcfg.heads == [8] * 6 and pcfg.ffn_dim == [1536] * 6
+    assert all(len(set(k)) == len(k) for k in kept_h + kept_f)
+    ids, mask, _ = _batch(pcfg, 6, 128, 950)
+    got = ffb.Encoder(pcfg, pw).encode(*_cuda(ids, mask)).cpu().numpy()
+    orc = oracle.Oracle(pcfg, pw)
+    ref = orc.encode(ids, mask)
+    drift = np.abs(orc.encode(ids, mask, acc32=True) - ref).max()
+    assert np.abs(got - ref).max() <= max(3 * drift, 1e-3 * np.abs(ref).max())
