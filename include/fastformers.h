@@ -183,9 +183,14 @@ FF_API ff_status ff_check(ff_model *m, void *stream);
  * row-reduction GEMMs (FF_OPT_FUSED_MASK bits 0 / 2) also launch with PDL;
  * default 0 (with PDL they slowed the step by 5-10%). */
 #define FF_OPT_PDL_RR 9
+/* FF_OPT_GEMM_BALANCE (process-wide, may be set with m = NULL): 1 = CTA-pair
+ * GEMMs (BN = 256) split a last wave that fills at most half of the pairs
+ * into half-width tiles; 0 = default (no end-to-end gain measured).  Results
+ * are identical. */
+#define FF_OPT_GEMM_BALANCE 10
 /* Set `option` to `value` on model m (invalidates its captured graphs).  The
- * process-wide options FF_OPT_PDL, FF_OPT_GEMM_MC and FF_OPT_PDL_RR may be set
- * with m = NULL.
+ * process-wide options FF_OPT_PDL, FF_OPT_GEMM_MC, FF_OPT_PDL_RR and
+ * FF_OPT_GEMM_BALANCE may be set with m = NULL.
  * FF_E_INVALID for an unknown option / bad value / NULL m otherwise. */
 FF_API ff_status ff_set_option(ff_model *m, int32_t option, int64_t value);
 

@@ -70,6 +70,7 @@ struct GemmParams {
   // colsum[n] = sum_k wq[n][k]
   const float* tensor_qp;
   const int* colsum;
+  int balance;     // split the last partial wave of pair tiles into half-width tiles (g_gemm_balance)
   int dbg_noload;  // debug MMA-rate probe: skip the operand loads (ff_debug_gemm bit 6; 0 in production)
 };
 
@@ -85,6 +86,7 @@ struct GemmPlan {
   bool pair;        // chosen for the current M
   bool mc;          // pairs run as clusters of two with W multicast (g_gemm_mc)
 };
+extern int g_gemm_balance;  // FF_OPT_GEMM_BALANCE: tail balancing of the pair GEMMs
 extern int g_gemm_mc;  // FF_OPT_GEMM_MC: 1 = CTA-pair GEMMs share W k-blocks by TMA multicast
 
 // Encode a 2-D K-major tensor map for a GEMM operand: rows x cols elements of

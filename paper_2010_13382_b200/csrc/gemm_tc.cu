@@ -194,10 +194,16 @@ __device__ __forceinline__ void gemm_trace(unsigned long long* trace, int t, int
 // multicasts them into CTA r of both pairs, halving the W bytes each SM pulls
 // from L2 (A stays per pair).  A stage's smem is refilled only when both pair
 // leaders' MMAs have consumed it (empty barriers count two commits).
+// Tail balancing (PAIR, not MC; p.balance): when the last wave of pair tiles
+// would occupy at most half of the pairs, its tiles are split into two
+// half-width tiles (N = BN/2, W boxes of BN/4 rows per CTA from tmBh) spread
+// over twice as many pairs, so the kernel's critical path ends half a tile
+// earlier (the N = 768 GEMMs of C3: 384 tiles on 74 pairs = 5 waves + 14).
 template <int BN, bool I8, bool PAIR, bool PT = false, bool MC = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmC, GemmParams p) {
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmBh,
+                   GemmParams p) {
   static_assert(!MC || (PAIR && !PT), "W multicast is a CTA-pair variant");
   using Cfg = GemmCfg<BN, PAIR>;
   constexpr int STAGES = Cfg::STAGES;
@@ -254,7 +260,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   // MC: a cluster tile = row tiles (2j, 2j+1) x one column tile; pair pq takes
   // row tile 2j + pq (past the last row tile when m_tiles is odd: it runs on
   // zero-filled / unused rows and stores nothing)
-  const int num_tiles = (MC ? (p.m_tiles + 1) / 2 : p.m_tiles) * p.n_tiles;
+  const int num_full = (MC ? (p.m_tiles + 1) / 2 : p.m_tiles) * p.n_tiles;
+  int split_from = num_full, num_tiles = num_full;
+  if (PAIR && !MC && BN == 256 && p.balance) {
+    const int rem = num_full % nunits;
+    if (rem > 0 && 2 * rem <= nunits) {
+      split_from = num_full - rem;
+      num_tiles = split_from + 2 * rem;
+    }
+  }
+  // virtual tile v -> (linear tile, half): half -1 = full width, 0 / 1 = the
+  // lower / upper BN/2 columns of a split tail tile
+  auto decode = [&](int v, int& t, int& half) {
+    if (v < split_from) {
+      t = v;
+      half = -1;
+    } else {
+      t = split_from + ((v - split_from) >> 1);
+      half = (v - split_from) & 1;
+    }
+  };
   constexpr int KE = I8 ? 128 : 64;  // elements per k-block
 
   if (warp == 0) {
@@ -262,11 +287,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int lt = 0;
-      for (int tile = unit; tile < num_tiles; tile += nunits, ++lt) {
+      for (int v = unit; v < num_tiles; v += nunits, ++lt) {
+        int tile, half;
+        decode(v, tile, half);
         const int ct = tile / p.n_tiles, nt = tile - ct * p.n_tiles;
         const int mt = MC ? 2 * ct + (int)pq : ct;
         const int arow = mt * TM + (int)rank * BM;
-        const int brow = nt * BN + (PAIR ? (int)rank * (BN / 2) : 0);
+        const int brow = half < 0 ? nt * BN + (PAIR ? (int)rank * (BN / 2) : 0)
+                                  : nt * BN + half * (BN / 2) + (int)rank * (BN / 4);
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (kb == 0) gemm_trace(p.trace, lt, 6);
@@ -274,10 +302,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (rank == 0) mbar_arrive(&full[stage]);
           } else if (PAIR) {
             // the leader's full barrier counts the bytes of both CTAs' loads
-            if (rank == 0) mbar_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+            if (rank == 0)
+              mbar_expect_tx(&full[stage], half < 0 ? 2 * Cfg::STAGE_BYTES : 2 * (Cfg::A_BYTES + Cfg::B_BYTES / 2));
             const uint32_t bar = mapa_shared(smem_u32(&full[stage]), lead);
             tma_load_2d_pair(sA + stage * Cfg::A_BYTES, &tmA, bar, kb * KE, arow, kEvictNormal);
-            if (MC) {  // quarter pq of the pair's W rows, into CTA `rank` of both pairs
+            if (half >= 0) {  // split tail tile: BN/4 rows of W per CTA
+              tma_load_2d_pair(sB + stage * Cfg::B_BYTES, &tmBh, bar, kb * KE, brow, kEvictLast);
+            } else if (MC) {  // quarter pq of the pair's W rows, into CTA `rank` of both pairs
               tma_load_2d_pair_mc(sB + stage * Cfg::B_BYTES + pq * (BN / 4) * BK_BYTES, &tmB, bar, kb * KE,
                                   brow + (int)pq * (BN / 4), (uint16_t)(0x5u << rank), kEvictLast);
             } else {
@@ -298,13 +329,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       // per-tensor u8 activations (DESIGN R22): a_format u8 (bit 7 clear)
-      constexpr uint32_t idesc = make_idesc<I8, TM, BN>() & (PT ? ~(1u << 7) : ~0u);
+      constexpr uint32_t idesc_full = make_idesc<I8, TM, BN>() & (PT ? ~(1u << 7) : ~0u);
+      constexpr uint32_t idesc_half = make_idesc<I8, TM, BN / 2>() & (PT ? ~(1u << 7) : ~0u);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       int lt = 0;
-      for (int tile = unit; tile < num_tiles; tile += nunits, ++lt) {
+      for (int v = unit; v < num_tiles; v += nunits, ++lt) {
+        const uint32_t idesc = v < split_from ? idesc_full : idesc_half;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         gemm_trace(p.trace, lt, 0);
         tc_fence_after();
@@ -349,7 +382,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = warp - 4;
     const int q = warp & 3;                         // TMEM lane quadrant this warp may access
     constexpr int WCOLS = BN / (kEpiWarps / 4);     // columns per warp (64 or 32)
-    const int c_lo = (ew >> 2) * WCOLS;             // this warp's column group of the tile
     uint8_t* stage_buf = sEpi + ew * kStageBufs * kStageTile;
     const uint32_t tempty_leader0 = PAIR ? mapa_shared(smem_u32(&tempty[0]), lead) : 0;
     int acc = 0;
@@ -359,9 +391,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool tr0 = ew == 0 && lane == 0;
     float* sPar = reinterpret_cast<float*>(smem + Cfg::PAR_OFF);
     const int et = ew * 32 + lane;  // 0 .. 511
-    for (int tile = unit; tile < num_tiles; tile += nunits, ++lt) {
+    for (int v = unit; v < num_tiles; v += nunits, ++lt) {
+      int tile, half;
+      decode(v, tile, half);
       const int ct = tile / p.n_tiles, nt = tile - ct * p.n_tiles;
       const int mt = MC ? 2 * ct + (int)pq : ct;
+      const int nb = nt * BN + (half > 0 ? BN / 2 : 0);  // first output column of this tile
+      // a split tail tile (BN = 256) spreads its 128 columns over all 16 warps (32 each)
+      const int wcols = half < 0 ? WCOLS : WCOLS / 2;
+      const int c_lo = (ew >> 2) * wcols;  // this warp's column group of the tile
       const int row0 = mt * TM + (int)rank * BM + q * 32;
       const int row = row0 + lane;
       float sx = 0.0f;
@@ -374,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (p.out_mode == 1) {
         const int npar = PT ? 3 * BN : 2 * BN;
         for (int i = et; i < npar; i += 32 * kEpiWarps) {
-          const int col = nt * BN + (i % BN);
+          const int col = nb + (i % BN);
           if (i < 2 * BN) {
             const float* src = i < BN ? p.bias : p.col_scale;
             par[i] = (src != nullptr && col < p.N) ? __ldg(src + col) : 0.0f;
@@ -401,11 +439,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       if (p.out_mode == 0) {  // raw accumulators (tests only)
 #pragma unroll 1
-        for (int c = c_lo; c < c_lo + WCOLS; c += kEpiCols) {
+        for (int c = c_lo; c < c_lo + wcols; c += kEpiCols) {
           uint32_t r[kEpiCols];
           tmem_ld32(tbase + c, r);
           tmem_wait_ld();
-          const int n0 = nt * BN + c;
+          const int n0 = nb + c;
           if (row < p.M && n0 < p.N) {
             uint32_t* o = reinterpret_cast<uint32_t*>(p.out) + (size_t)row * p.ldo + n0;
 #pragma unroll
@@ -420,9 +458,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld16(tbase + c_lo, r[0]);
         tmem_ld16(tbase + c_lo + 16, r[1]);
 #pragma unroll 1
-        for (int c = c_lo; c < c_lo + WCOLS; c += kEpiCols) {
-          const int n0 = nt * BN + c;
-          const bool last = c + kEpiCols >= c_lo + WCOLS;
+        for (int c = c_lo; c < c_lo + wcols; c += kEpiCols) {
+          const int n0 = nb + c;
+          const bool last = c + kEpiCols >= c_lo + wcols;
           tmem_wait_ld();
           const int ci = (c - c_lo) / kEpiCols;
           if (tr0 && ci < 4) gemm_trace(p.trace, lt, 8 + 3 * ci);
@@ -1040,6 +1078,7 @@ void plan_gemm_set_m(GemmPlan* g, int M) {
   g->p.m_tiles = (M + tm - 1) / tm;
   const int tiles = g->p.m_tiles * g->p.n_tiles;
   g->mc = g->pair && g_gemm_mc != 0;
+  g->p.balance = g_gemm_balance;
   g->p.dbg_noload = 0;
   if (g->mc) {
     const int ctiles = ((g->p.m_tiles + 1) / 2) * g->p.n_tiles;
@@ -1116,12 +1155,12 @@ static cudaError_t launch_t(const GemmPlan& g, cudaStream_t s) {
   if (g.grid <= 0) return cudaSuccess;
   if (PAIR && g.mc && g.p.tensor_qp == nullptr)  // (per-tensor u8 runs the plain pair kernel)
     return launch_ex(gemm_tc_kernel<BN, I8, true, false, true>, dim3(g.grid), dim3(kThreads),
-                     GemmCfg<BN, true>::SMEM, s, 4, g.tmA, g.tmB4, g.tmC, g.p);
+                     GemmCfg<BN, true>::SMEM, s, 4, g.tmA, g.tmB4, g.tmC, g.tmB4, g.p);
   if (I8 && g.p.tensor_qp != nullptr)
     return launch_ex(gemm_tc_kernel<BN, I8, PAIR, I8>, dim3(g.grid), dim3(kThreads), GemmCfg<BN, PAIR>::SMEM, s,
-                     PAIR ? 2 : 0, g.tmA, PAIR ? g.tmB2 : g.tmB, g.tmC, g.p);
+                     PAIR ? 2 : 0, g.tmA, PAIR ? g.tmB2 : g.tmB, g.tmC, g.tmB4, g.p);
   return launch_ex(gemm_tc_kernel<BN, I8, PAIR, false>, dim3(g.grid), dim3(kThreads), GemmCfg<BN, PAIR>::SMEM, s,
-                   PAIR ? 2 : 0, g.tmA, PAIR ? g.tmB2 : g.tmB, g.tmC, g.p);
+                   PAIR ? 2 : 0, g.tmA, PAIR ? g.tmB2 : g.tmB, g.tmC, g.tmB4, g.p);
 }
 
 cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t s) {

@@ -28,6 +28,7 @@ FF_OPT_ACT_QUANT = 6
 FF_OPT_GEMM_MC = 7
 FF_OPT_FUSED_MASK = 8
 FF_OPT_PDL_RR = 9
+FF_OPT_GEMM_BALANCE = 10
 KERNEL_KINDS = ["embed_ln", "gemm_f16", "gemm_i8", "attention", "quant_rows", "add_ln", "head", "gemm_rr_f16",
                 "gemm_rr_i8"]
 STATUS_NAMES = ["FF_OK", "FF_E_INVALID", "FF_E_SHAPE", "FF_E_STATE", "FF_E_CUDA", "FF_E_INPUT", "FF_E_UNSUPPORTED",
@@ -246,6 +247,11 @@ def set_gemm_mc(on: bool):
     """FF_OPT_GEMM_MC (process-wide): CTA-pair GEMMs in clusters of two pairs
     sharing W k-blocks by TMA multicast."""
     check(lib().ff_set_option(None, FF_OPT_GEMM_MC, 1 if on else 0))
+
+
+def set_gemm_balance(on: bool):
+    """FF_OPT_GEMM_BALANCE (process-wide): split the last partial wave of CTA-pair tiles."""
+    check(lib().ff_set_option(None, FF_OPT_GEMM_BALANCE, 1 if on else 0))
 
 
 def gemm(A, W, out_mode=0, bias=None, sx=None, sw=None, act=-1, out=None, cta_pair=None):

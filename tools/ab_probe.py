@@ -12,7 +12,8 @@ sys.path.insert(0, ".")
 from paper_2010_13382_b200 import synth  # noqa: E402
 from paper_2010_13382_b200 import fastformers as ffb  # noqa: E402
 
-OPTS = {"gemm_mc": lambda enc, on: ffb.set_gemm_mc(on)}
+OPTS = {"gemm_mc": lambda enc, on: ffb.set_gemm_mc(on),
+        "gemm_balance": lambda enc, on: ffb.set_gemm_balance(on)}
 for _m in range(1, 8):  # FF_OPT_FUSED_MASK bits: 1 out-proj+LN1, 2 FFN1+requant, 4 FFN2+LN2
     OPTS[f"fused{_m}"] = (lambda m: lambda enc, on: enc.set_fused(m if on else 0))(_m)
 
