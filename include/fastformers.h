@@ -188,9 +188,13 @@ FF_API ff_status ff_check(ff_model *m, void *stream);
  * into half-width tiles; 0 = default (no end-to-end gain measured).  Results
  * are identical. */
 #define FF_OPT_GEMM_BALANCE 10
+/* FF_OPT_PDL_KINDS (process-wide, may be set with m = NULL): bitmask over
+ * ff_kernel_kind of the forward launches that use PDL (default all; only
+ * while FF_OPT_PDL = 1). */
+#define FF_OPT_PDL_KINDS 11
 /* Set `option` to `value` on model m (invalidates its captured graphs).  The
- * process-wide options FF_OPT_PDL, FF_OPT_GEMM_MC, FF_OPT_PDL_RR and
- * FF_OPT_GEMM_BALANCE may be set with m = NULL.
+ * process-wide options FF_OPT_PDL, FF_OPT_GEMM_MC, FF_OPT_PDL_RR,
+ * FF_OPT_GEMM_BALANCE and FF_OPT_PDL_KINDS may be set with m = NULL.
  * FF_E_INVALID for an unknown option / bad value / NULL m otherwise. */
 FF_API ff_status ff_set_option(ff_model *m, int32_t option, int64_t value);
 

@@ -15,6 +15,8 @@
 namespace ff {
 bool g_pdl = true;  // FF_OPT_PDL: programmatic dependent launch between forward kernels
 bool g_pdl_rr = false;  // FF_OPT_PDL_RR: PDL on the LN-mode row-reduction GEMMs (measured slower)
+int g_cur_kind = 0;              // kernel kind of the launch in progress (FF_LAUNCH)
+unsigned g_pdl_kinds = 0xFFFFFFFFu;  // FF_OPT_PDL_KINDS: kinds (bit = ff_kernel_kind) launched with PDL
 int g_gemm_balance = 0;  // FF_OPT_GEMM_BALANCE: split the last partial wave of pair tiles (measured: no gain)
 int g_gemm_mc = 0;  // FF_OPT_GEMM_MC: CTA-pair GEMMs in clusters of two pairs sharing W by multicast
 }
@@ -295,6 +297,7 @@ struct Prof {
 
 #define FF_LAUNCH(kind_, x, what)                   \
   do {                                              \
+    ff::g_cur_kind = (kind_);                       \
     if (prof) {                                     \
       prof->kind.push_back(kind_);                  \
       prof->mark(s);                                \
@@ -821,6 +824,14 @@ ff_status ff_check(ff_model* m, void* stream) {
 ff_status ff_set_option(ff_model* m, int32_t option, int64_t value) {
   if (!m && option == FF_OPT_GEMM_MC) {  // process-wide options may be set without a model
     ff::g_gemm_mc = value != 0 ? 1 : 0;
+    return FF_OK;
+  }
+  if (option == FF_OPT_PDL_KINDS) {  // process-wide
+    ff::g_pdl_kinds = (unsigned)value;
+    if (m) {
+      for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
+      m->graphs.clear();
+    }
     return FF_OK;
   }
   if (option == FF_OPT_GEMM_BALANCE) {  // process-wide

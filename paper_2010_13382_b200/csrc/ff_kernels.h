@@ -14,6 +14,8 @@ constexpr int kNumSMs = 148;
 // an optional 1-D cluster (cluster = 0: no cluster attribute).  All
 // forward-pass kernels go through this.
 extern bool g_pdl;
+extern int g_cur_kind;         // kind (ff_kernel_kind) of the forward launch in progress
+extern unsigned g_pdl_kinds;   // FF_OPT_PDL_KINDS: bit k = kind k launches with PDL
 extern bool g_pdl_rr;  // FF_OPT_PDL_RR: PDL attribute on the row-reduction GEMM launches too
 template <typename... KArgs, typename... Args>
 cudaError_t launch_ex_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
@@ -21,7 +23,7 @@ cudaError_t launch_ex_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 bloc
 template <typename... KArgs, typename... Args>
 cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int cluster,
                       Args... args) {
-  return launch_ex_pdl(g_pdl, kern, grid, block, smem, s, cluster, args...);
+  return launch_ex_pdl(g_pdl && ((g_pdl_kinds >> g_cur_kind) & 1u), kern, grid, block, smem, s, cluster, args...);
 }
 template <typename... KArgs, typename... Args>
 cudaError_t launch_ex_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,

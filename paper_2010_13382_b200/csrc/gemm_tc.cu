@@ -1258,7 +1258,7 @@ void plan_rr_set_m(RRPlan* g, int M) {
 template <bool I8, int MODE>
 static cudaError_t launch_rr_t(const RRPlan& g, cudaStream_t s) {
   // LN-mode row-reduction GEMMs launch without PDL unless FF_OPT_PDL_RR (measured)
-  const bool pdl = g_pdl && (MODE != RR_LN || g_pdl_rr);
+  const bool pdl = g_pdl && ((g_pdl_kinds >> g_cur_kind) & 1u) && (MODE != RR_LN || g_pdl_rr);
   return launch_ex_pdl(pdl, gemm_rr_kernel<I8, MODE>, dim3(g.grid), dim3(kRRThreads), RRCfg::SMEM, s, g.cn, g.tmA,
                        g.tmB, g.tmC, g.tmR, g.tmQ, g.p);
 }

@@ -29,6 +29,7 @@ FF_OPT_GEMM_MC = 7
 FF_OPT_FUSED_MASK = 8
 FF_OPT_PDL_RR = 9
 FF_OPT_GEMM_BALANCE = 10
+FF_OPT_PDL_KINDS = 11
 KERNEL_KINDS = ["embed_ln", "gemm_f16", "gemm_i8", "attention", "quant_rows", "add_ln", "head", "gemm_rr_f16",
                 "gemm_rr_i8"]
 STATUS_NAMES = ["FF_OK", "FF_E_INVALID", "FF_E_SHAPE", "FF_E_STATE", "FF_E_CUDA", "FF_E_INPUT", "FF_E_UNSUPPORTED",
