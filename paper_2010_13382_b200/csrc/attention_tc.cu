@@ -165,21 +165,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // The head slices are 128-byte column strips of the QKV rows; fetched
-      // strip by strip straight from HBM they reopen each DRAM page once per
-      // head.  Prefetch an item's rows (contiguous, S x row_bytes) into L2 as
-      // a whole first: the current item at its start, the next one halfway.
-      auto prefetch_rows = [&](int item) {
-        if (item >= n_items) return;
-        const uint8_t* p0 = qkv_rows + (size_t)(item / n_groups) * S * row_bytes;
-        const size_t total = (size_t)S * row_bytes;
-        for (size_t off = 0; off < total; off += 32768)
-          bulk_prefetch_l2(p0 + off, (uint32_t)min((size_t)32768, total - off));
-      };
+      // (An L2 bulk prefetch of each item's QKV rows, meant to open each DRAM
+      // page once per item, measured 5.5 us slower per C3 launch: the QKV
+      // buffer was just written by the projection GEMM and is largely still
+      // in L2, and the prefetch queued ahead of the first head's loads.)
+      (void)qkv_rows;
+      (void)row_bytes;
       uint32_t n = 0;
       for (HeadIter it(blockIdx.x, n_items, n_groups, A, gridDim.x); it.valid(); it.next(), ++n) {
-        if (n == 0) prefetch_rows(it.item);
-        if (it.hl == it.nh / 2) prefetch_rows(it.item + it.stride);
         const int slot = n % kKVStages;
         const int h = it.h0 + it.hl;
         uint8_t* base = smem + slot * SmemTC::SLOT;
