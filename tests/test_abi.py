@@ -94,3 +94,24 @@ def test_null_model_calls_are_rejected(built):
     assert built.ff_encode(None, None, None, 1, 1, None, None) == ffb.FF_E_INVALID
     assert built.ff_check(None, None) == ffb.FF_E_INVALID
     assert built.ff_finalize(None, None) == ffb.FF_E_INVALID
+
+
+def test_process_wide_options_without_a_model(built):
+    """FF_OPT_PDL / GEMM_MC / PDL_RR / GEMM_BALANCE / PDL_KINDS are process-wide
+    and accept m = NULL (no device work); model options need a model."""
+    for opt, on, off in ((ffb.FF_OPT_GEMM_MC, 1, 0), (ffb.FF_OPT_PDL_RR, 1, 0), (ffb.FF_OPT_GEMM_BALANCE, 1, 0),
+                         (ffb.FF_OPT_PDL_KINDS, 0x3, 0xFFFFFFFF), (ffb.FF_OPT_PDL, 0, 1)):
+        assert built.ff_set_option(None, opt, on) == ffb.FF_OK
+        assert built.ff_set_option(None, opt, off) == ffb.FF_OK
+    assert built.ff_set_option(None, ffb.FF_OPT_PDL_RR, 0) == ffb.FF_OK  # restore the default
+    assert built.ff_set_option(None, ffb.FF_OPT_FUSED_MASK, 2) == ffb.FF_E_INVALID
+    assert built.ff_set_option(None, ffb.FF_OPT_GRAPHS, 1) == ffb.FF_E_INVALID
+    assert built.ff_set_option(None, 999, 1) == ffb.FF_E_INVALID
+
+
+def test_scorer_config_validation_before_device(built):
+    c, keep = _cfg(num_classes=65)
+    h = ctypes.c_void_p()
+    assert built.ff_scorer_create(ctypes.byref(c), 0, ctypes.byref(h)) == ffb.FF_E_INVALID
+    assert built.ff_scorer_last_error()
+    assert built.ff_score_batch(None, None, None, None, 1, 1, None, None, None, None, None) == ffb.FF_E_INVALID
