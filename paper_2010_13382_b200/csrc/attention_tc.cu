@@ -4,7 +4,7 @@
 // Q.K^T and P.V in floating point).
 //
 // One work item = (sequence b, group of <= 8 heads); one persistent CTA per SM
-// walks the heads of its item with Q/K/V double-buffered across heads.
+// walks the heads of its items with Q/K/V triple-buffered across heads.
 //   warp 0     TMA: Q, K, V head slices (128 rows x 64 fp16, 128B-swizzled)
 //   warp 1     TMEM allocator + MMA issuer (one thread):
 //                S[128 x 128] (TMEM, fp32) = Q . K^T        kind::f16, K-major A/B
@@ -17,9 +17,12 @@
 //                before P.V), written to smem in the 128B-swizzled K-major
 //                layout the MMA reads; ctx = R16(O).
 // int8 layers (A <= 8): the R16 ctx of all heads of the row is parked in TMEM
-// (packed fp16 pairs, columns [256, 256 + 32 A)) and quantized per row (Q8row,
-// R6-R8) after the last head, so ctx goes to HBM once, as s8 rows + scale
-// (SURVEY 8(a) a3+a4 fused).  Otherwise ctx is stored as fp16 rows.
+// (packed fp16 pairs, columns [256, 256 + 32 A)); after the item's last head
+// the row scale (Q8row, R6-R8) is known, and head j of the item is quantized
+// and stored by the epilogue of head j of the CTA's next item (the last item
+// after the loop), so ctx goes to HBM once, as s8 rows + scale (SURVEY 8(a)
+// a3+a4 fused) without a per-item requant stall.  Otherwise ctx is stored as
+// fp16 rows.
 // Row max / sum are combined across the two half-row threads through smem in
 // a fixed order.  Keys beyond S (S < 128) are masked; Q rows beyond S are
 // computed and not stored.
