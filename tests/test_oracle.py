@@ -439,3 +439,50 @@ def test_per_tensor_and_per_row_accuracy_vs_ref64_c1():
     e_ten = np.abs(Oracle(cfg, w, act_quant=1).encode(ids, mask) - ref).max()
     scale = np.abs(ref).max()
     assert e_row <= 0.05 * scale and e_ten <= 0.1 * scale
+
+
+def test_per_tensor_linear_vs_pytorch_fbgemm_dynamic():
+    """SURVEY 8(f) NEXT-2 pin: the oracle's per-tensor u8 (zero point) x
+    per-channel s8 linear against PyTorch's FBGEMM dynamic quantized linear
+    (the paper's CPU int8 path), activation range not reduced.  The two
+    differ only in the weight scale convention (amax / 127 here, R7; amax /
+    127.5 with codes in [-128, 127] in PyTorch) and the zero-point choice, so
+    both sit within the int8 error envelope of the fp64 product and close to
+    each other; a wrong zero-point correction (zp * colsum) would be off by
+    orders of magnitude."""
+    torch = pytest.importorskip("torch")
+    if "fbgemm" not in torch.backends.quantized.supported_engines:
+        pytest.skip("no FBGEMM engine")
+    import warnings
+    rng = np.random.default_rng(21)
+    H, A, d, M = 256, 4, 64, 64
+    Wo = (rng.standard_normal((H, A * d)) * 0.02).astype(np.float32)
+    bo = (rng.standard_normal(H) * 0.02).astype(np.float32)
+    cfg = small_cfg(num_layers=1, hidden=H, heads=[A], ffn_dim=[256], dtype=[1])
+    w = synth.make_weights(cfg)
+    w["encoder.layer.0.attention.output.dense.weight"] = Wo
+    w["encoder.layer.0.attention.output.dense.bias"] = bo
+    o = Oracle(cfg, w, act_quant=1)
+    x = np.float16(rng.standard_normal((M, A * d)) + 0.3).astype(np.float32)
+    ours = o.stage(0, oracle.ST_OPROJ, x).astype(np.float64)
+    lin = torch.nn.Linear(A * d, H)
+    with torch.no_grad():
+        lin.weight.copy_(torch.from_numpy(Wo))
+        lin.bias.copy_(torch.from_numpy(bo))
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        torch.backends.quantized.engine = "fbgemm"
+        from torch.ao.quantization import per_channel_dynamic_qconfig, quantize_dynamic
+        q = quantize_dynamic(torch.nn.Sequential(lin), {torch.nn.Linear: per_channel_dynamic_qconfig},
+                             dtype=torch.qint8)[0]
+        fb = torch.ops.quantized.linear_dynamic(torch.from_numpy(x), q._packed_params._packed_params,
+                                                False).numpy().astype(np.float64)
+    ref = x.astype(np.float64) @ Wo.astype(np.float64).T + bo
+    rel = lambda a: np.linalg.norm(a - ref) / np.linalg.norm(ref)
+    assert rel(ours) < 2e-2 and rel(fb) < 2e-2, (rel(ours), rel(fb))  # measured 1.16e-2 and 1.14e-2
+    assert np.linalg.norm(ours - fb) / np.linalg.norm(ref) < 1.5e-2
+    # the zero point matters: dropping its correction is a gross error
+    qx, s, z = oracle.q8tensor(x)
+    wq, sw = oracle.quant_weight(Wo)
+    no_zp = (qx.astype(np.float64) * s) @ (wq.astype(np.float64) * sw[:, None]).T + bo
+    assert rel(no_zp) > 10 * rel(ours)
