@@ -312,6 +312,11 @@ FF_API ff_status ff_scorer_finalize(ff_scorer *s, void *stream);
 FF_API ff_status ff_score_batch(ff_scorer *s, const int32_t *d_ids, const int32_t *d_mask, const int32_t *d_labels,
                                 int32_t batch, int32_t seq, double *d_head_scores, double *d_ffn_scores,
                                 float *d_loss, float *d_logits, void *stream);
+/* Synchronize `stream`; FF_E_INPUT (and clear the flag) if an earlier
+ * ff_score_batch saw a token id outside [0, V), a mask value not 0/1 or
+ * mask[b][0] != 1, or a label outside [0, C) (such inputs are read as 0, never
+ * out of bounds, and that batch's scores are not meaningful), else FF_OK. */
+FF_API ff_status ff_scorer_check(ff_scorer *s, void *stream);
 /* Frees host state only (the arenas belong to the caller). */
 FF_API void ff_scorer_destroy(ff_scorer *s);
 

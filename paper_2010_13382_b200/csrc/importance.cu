@@ -31,6 +31,18 @@
 namespace {
 
 thread_local std::string g_serr;
+
+// Makes the scorer's device current for one API call, restoring the caller's.
+struct SDev {
+  int prev = -1;
+  explicit SDev(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~SDev() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
 ff_status sfail(ff_status s, const std::string& msg) {
   g_serr = msg;
   return s;
@@ -252,13 +264,24 @@ __device__ void ln_row(const float* x, int H, const float* gam, const float* bet
   if (threadIdx.x == 0 && rstd_out) *rstd_out = rs;
 }
 
-__global__ void embed_ln_f32_kernel(const int* ids, int S, int H, const float* tok, const float* pos,
-                                    const float* type0, const float* g, const float* b, float eps, float* X) {
+// Input errors (sticky flag, ff_scorer_check): bit 0 token id outside [0, V)
+// (read as id 0), bit 1 mask[b][0] != 1 or a mask value not 0/1, bit 2 label
+// outside [0, C) (read as 0) -- no out-of-bounds access on bad input.
+__global__ void embed_ln_f32_kernel(const int* ids, const int* mask, int S, int H, int V, const float* tok,
+                                    const float* pos, const float* type0, const float* g, const float* b, float eps,
+                                    float* X, int* err) {
   extern __shared__ float sm[];
   float* row = sm;
   float* red = sm + H;
   const int r = blockIdx.x, si = r % S;
-  const float* t = tok + (size_t)ids[r] * H;
+  int id = ids[r];
+  if (threadIdx.x == 0) {
+    const int mk = mask[r];
+    if (id < 0 || id >= V) atomicOr(err, 1);
+    if ((mk != 0 && mk != 1) || (si == 0 && mk != 1)) atomicOr(err, 2);
+  }
+  if (id < 0 || id >= V) id = 0;
+  const float* t = tok + (size_t)id * H;
   const float* p = pos + (size_t)si * H;
   for (int j = threadIdx.x; j < H; j += blockDim.x) row[j] = t[j] + p[j] + type0[j];
   ln_row(row, H, g, b, eps, X + (size_t)r * H, nullptr, nullptr, red);
@@ -350,7 +373,7 @@ __global__ void act_bwd_kernel(const float* U, float* dA, size_t n, int act) {
 // dX[b*S + 0, :] = Wp^T ((Wc^T dlogits) * (1 - pool^2)), dlogits = (p - y) / B.
 __global__ void head_fwd_bwd_kernel(const float* X, int S, int H, int C, int B, const float* Wp, const float* bp,
                                     const float* Wc, const float* bc, const int* labels, float* dX, float* loss_b,
-                                    float* logits_out) {
+                                    float* logits_out, int* err) {
   extern __shared__ float sm[];
   float* x0 = sm;            // [H]
   float* pool = sm + H;      // [H]
@@ -384,10 +407,15 @@ __global__ void head_fwd_bwd_kernel(const float* X, int S, int H, int C, int B, 
     float se = 0.0f;
     for (int c = 0; c < C; ++c) se += expf(lg[c] - mx);
     const float lse = logf(se);
-    loss_b[b] = lse - (lg[labels[b]] - mx);
+    int lab = labels[b];
+    if (lab < 0 || lab >= C) {
+      atomicOr(err, 4);
+      lab = 0;
+    }
+    loss_b[b] = lse - (lg[lab] - mx);
     for (int c = 0; c < C; ++c) {
       if (logits_out) logits_out[(size_t)b * C + c] = lg[c];
-      lg[c] = (expf(lg[c] - mx - lse) - (c == labels[b] ? 1.0f : 0.0f)) / (float)B;  // dlogits
+      lg[c] = (expf(lg[c] - mx - lse) - (c == lab ? 1.0f : 0.0f)) / (float)B;  // dlogits
     }
   }
   __syncthreads();
@@ -474,7 +502,7 @@ struct ff_scorer {
   size_t tok, pos, type0, eg, eb, pw, pb, cw, cb;
   uint32_t top_loaded = 0;
   size_t wbytes = 0, wsbytes = 0;
-  size_t Xout, dX, dZ, dY1, dAm, dC, dP, dQKV, colg, lossb, ids, mask, labels;
+  size_t Xout, dX, dZ, dY1, dAm, dC, dP, dQKV, colg, lossb, errf, ids, mask, labels;
   int Dmax = 0, Fmax = 0, Amax = 0;
   uint8_t* dW = nullptr;
   uint8_t* dWS = nullptr;
@@ -551,6 +579,7 @@ void plan_scorer(ff_scorer* m) {
   m->dQKV = take(M * 3 * m->Dmax);
   m->colg = take((size_t)kRowChunks * std::max(m->Fmax, m->Dmax));
   m->lossb = take(M);
+  m->errf = take(64);
   m->wsbytes = o;
 }
 
@@ -593,8 +622,9 @@ ff_status score_batch(ff_scorer* m, const int* ids, const int* mask, const int* 
   const int rt = rows_threads(H);
   const size_t lnsm = (size_t)(H + 32) * 4;
   // ---- forward, keeping what the backward needs
-  embed_ln_f32_kernel<<<M, rt, lnsm, s>>>(ids, S, H, m->w(m->tok), m->w(m->pos), m->w(m->type0), m->w(m->eg),
-                                          m->w(m->eb), c.ln_eps, m->ws(m->L[0].X));
+  int* errf = reinterpret_cast<int*>(m->dWS + m->errf);
+  embed_ln_f32_kernel<<<M, rt, lnsm, s>>>(ids, mask, S, H, c.vocab_size, m->w(m->tok), m->w(m->pos), m->w(m->type0),
+                                          m->w(m->eg), m->w(m->eb), c.ln_eps, m->ws(m->L[0].X), errf);
   SL(cudaGetLastError(), "embed_ln");
   for (int l = 0; l < c.num_layers; ++l) {
     SLayer& P = m->L[l];
@@ -636,7 +666,7 @@ ff_status score_batch(ff_scorer* m, const int* ids, const int* mask, const int* 
   SC_CK(cudaMemsetAsync(m->ws(m->dX), 0, (size_t)M * H * 4, s));
   head_fwd_bwd_kernel<<<B, 256, (size_t)(3 * H + 64 + 32) * 4, s>>>(
       m->ws(m->Xout), S, H, C, B, m->w(m->pw), m->w(m->pb), m->w(m->cw), m->w(m->cb), labels, m->ws(m->dX),
-      m->ws(m->lossb), logits);
+      m->ws(m->lossb), logits, errf);
   SL(cudaGetLastError(), "head");
   if (loss) {
     loss_mean_kernel<<<1, 32, 0, s>>>(m->ws(m->lossb), B, loss);
@@ -748,6 +778,8 @@ ff_status ff_scorer_bind_memory(ff_scorer* m, void* d_weights, size_t wbytes, vo
   if (((uintptr_t)d_weights | (uintptr_t)d_workspace) & 255) return sfail(FF_E_INVALID, "arenas must be 256-B aligned");
   m->dW = static_cast<uint8_t*>(d_weights);
   m->dWS = static_cast<uint8_t*>(d_workspace);
+  SDev dg_(m->device);
+  SC_CK(cudaMemset(m->dWS + m->errf, 0, 64));
   m->state = 1;
   return FF_OK;
 }
@@ -765,6 +797,7 @@ ff_status ff_scorer_load_weights(ff_scorer* m, const char* name, const float* ho
   for (int i = 0; i < rank; ++i) numel *= (size_t)shape[i];
   auto put = [&](size_t off, size_t expect) -> ff_status {
     if (numel != expect) return sfail(FF_E_SHAPE, "wrong shape for " + std::string(name));
+    SDev dg_(m->device);
     SC_CK(cudaMemcpyAsync(m->dW + off, host, numel * 4, cudaMemcpyHostToDevice, s));
     SC_CK(cudaStreamSynchronize(s));  // host buffer may be freed after return
     return FF_OK;
@@ -831,8 +864,27 @@ ff_status ff_score_batch(ff_scorer* m, const int32_t* d_ids, const int32_t* d_ma
   if (m->state != 2) return sfail(FF_E_STATE, "ff_scorer_finalize first");
   if (batch < 1 || seq < 1 || seq > m->cfg.max_positions || (int64_t)batch * seq > m->cfg.max_tokens)
     return sfail(FF_E_SHAPE, "batch * seq exceeds max_tokens or seq > max_positions");
+  SDev dg_(m->device);
   return score_batch(m, d_ids, d_mask, d_labels, batch, seq, d_head_scores, d_ffn_scores, d_loss, d_logits,
                      static_cast<cudaStream_t>(stream));
+}
+
+ff_status ff_scorer_check(ff_scorer* m, void* stream) {
+  if (!m) return sfail(FF_E_INVALID, "null argument");
+  if (m->state < 1) return sfail(FF_E_STATE, "bind memory first");
+  SDev dg_(m->device);
+  SC_CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  int flag = 0;
+  SC_CK(cudaMemcpy(&flag, m->dWS + m->errf, 4, cudaMemcpyDeviceToHost));
+  if (flag) {
+    SC_CK(cudaMemset(m->dWS + m->errf, 0, 4));
+    std::string why;
+    if (flag & 1) why += " token id outside [0, vocab)";
+    if (flag & 2) why += " mask value not 0/1 or mask[b,0] != 1";
+    if (flag & 4) why += " label outside [0, num_classes)";
+    return sfail(FF_E_INPUT, "input error:" + why);
+  }
+  return FF_OK;
 }
 
 void ff_scorer_destroy(ff_scorer* m) { delete m; }

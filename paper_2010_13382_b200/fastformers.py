@@ -40,7 +40,7 @@ EXPORTED = ["ff_abi_version", "ff_last_error", "ff_model_create", "ff_model_memo
             "ff_model_destroy", "ff_launch_count", "ff_profile", "ff_encode_trace", "ff_debug_gemm", "ff_debug_quant_rows",
             "ff_debug_attention", "ff_debug_attention_q8", "ff_debug_set_trace",
             "ff_scorer_last_error", "ff_scorer_create", "ff_scorer_memory", "ff_scorer_bind_memory",
-            "ff_scorer_load_weights", "ff_scorer_finalize", "ff_score_batch", "ff_scorer_destroy"]
+            "ff_scorer_load_weights", "ff_scorer_finalize", "ff_score_batch", "ff_scorer_check", "ff_scorer_destroy"]
 
 
 class FFError(RuntimeError):
@@ -96,6 +96,7 @@ def lib():
         L.ff_scorer_load_weights.argtypes = [vp, ctypes.c_char_p, vp, ctypes.POINTER(ctypes.c_int64), i32, vp]
         L.ff_scorer_finalize.argtypes = [vp, vp]
         L.ff_score_batch.argtypes = [vp, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp]
+        L.ff_scorer_check.argtypes = [vp, vp]
         L.ff_scorer_destroy.argtypes = [vp]
         L.ff_scorer_destroy.restype = None
         for name in EXPORTED:
@@ -380,6 +381,10 @@ class Scorer:
                                      _ptr(self.ffn_scores), _ptr(self.loss),
                                      _ptr(logits) if logits is not None else nul, _stream_ptr(stream)))
         return self.loss
+
+    def check_inputs(self, stream=None):
+        """ff_scorer_check: raises FFError(FF_E_INPUT) if a scored batch had invalid ids / mask / labels."""
+        _scheck(lib().ff_scorer_check(self.h, _stream_ptr(stream)))
 
     def scores(self):
         """(head_scores [L][A_l], ffn_scores [L][F_l]) as numpy, trimmed per layer."""

@@ -135,3 +135,27 @@ def test_score_prune_reconnect_encode_end_to_end():
     ref = orc.encode(ids, mask)
     drift = np.abs(orc.encode(ids, mask, acc32=True) - ref).max()
     assert np.abs(got - ref).max() <= max(3 * drift, 1e-3 * np.abs(ref).max())
+
+
+def test_scorer_flags_invalid_inputs_without_faulting():
+    """Token ids outside [0, V), mask[b, 0] = 0 and labels outside [0, C) are
+    read as 0 (no out-of-bounds access) and reported by ff_scorer_check."""
+    cfg = _tiny()
+    w = synth.make_weights(cfg, std=0.3)
+    sc = ffb.Scorer(cfg, w, max_tokens=3 * 7)
+    ids, mask, labels = _batch(cfg, 3, 7, 5)
+    sc.score(*_cuda(ids, mask, labels))
+    sc.check_inputs()  # clean batch: no error
+    for bad in ("id", "mask", "label"):
+        i2, m2, l2 = ids.copy(), mask.copy(), labels.copy()
+        if bad == "id":
+            i2[1, 2] = cfg.vocab_size + 7
+        elif bad == "mask":
+            m2[2, 0] = 0
+        else:
+            l2[0] = cfg.num_classes
+        sc.score(*_cuda(i2, m2, l2))
+        with pytest.raises(ffb.FFError) as e:
+            sc.check_inputs()
+        assert e.value.status == ffb.FF_E_INPUT
+        sc.check_inputs()  # the flag was cleared
