@@ -782,8 +782,11 @@ ff_status ff_encode(ff_model* m, const int32_t* d_token_ids, const int32_t* d_ma
   return FF_OK;
 }
 
-ff_status ff_encode_host(ff_model* m, const int32_t* h_token_ids, const int32_t* h_mask, int32_t batch, int32_t seq,
-                         float* h_logits, void* stream) {
+// ff_encode_host / ff_encode_host_async: copies in, forward, copy out on the
+// caller's stream (stream order makes the shared workspace ids / mask / logits
+// buffers safe to reuse by the next call); the sync form then waits.
+static ff_status encode_host_impl(ff_model* m, const int32_t* h_token_ids, const int32_t* h_mask, int32_t batch,
+                                  int32_t seq, float* h_logits, void* stream, bool sync) {
   ff_status st = check_call(m, batch, seq);
   if (st != FF_OK) return st;
   if (!h_token_ids || !h_mask || !h_logits) return fail(FF_E_INVALID, "null buffer");
@@ -798,8 +801,18 @@ ff_status ff_encode_host(ff_model* m, const int32_t* h_token_ids, const int32_t*
   st = ff_encode(m, ids, mask, batch, seq, logits, stream);
   if (st != FF_OK) return st;
   FF_CK(cudaMemcpyAsync(h_logits, logits, (size_t)batch * m->cfg.num_classes * 4, cudaMemcpyDeviceToHost, s));
-  FF_CK(cudaStreamSynchronize(s));
+  if (sync) FF_CK(cudaStreamSynchronize(s));
   return FF_OK;
+}
+
+ff_status ff_encode_host(ff_model* m, const int32_t* h_token_ids, const int32_t* h_mask, int32_t batch, int32_t seq,
+                         float* h_logits, void* stream) {
+  return encode_host_impl(m, h_token_ids, h_mask, batch, seq, h_logits, stream, true);
+}
+
+ff_status ff_encode_host_async(ff_model* m, const int32_t* h_token_ids, const int32_t* h_mask, int32_t batch,
+                               int32_t seq, float* h_logits, void* stream) {
+  return encode_host_impl(m, h_token_ids, h_mask, batch, seq, h_logits, stream, false);
 }
 
 ff_status ff_check(ff_model* m, void* stream) {

@@ -36,7 +36,7 @@ STATUS_NAMES = ["FF_OK", "FF_E_INVALID", "FF_E_SHAPE", "FF_E_STATE", "FF_E_CUDA"
                 "FF_E_NOMEM"]
 
 EXPORTED = ["ff_abi_version", "ff_last_error", "ff_model_create", "ff_model_memory", "ff_bind_memory",
-            "ff_load_weights", "ff_finalize", "ff_encode", "ff_encode_host", "ff_check", "ff_set_option",
+            "ff_load_weights", "ff_finalize", "ff_encode", "ff_encode_host", "ff_encode_host_async", "ff_check", "ff_set_option",
             "ff_model_destroy", "ff_launch_count", "ff_profile", "ff_encode_trace", "ff_debug_gemm", "ff_debug_quant_rows",
             "ff_debug_attention", "ff_debug_attention_q8", "ff_debug_set_trace",
             "ff_scorer_last_error", "ff_scorer_create", "ff_scorer_memory", "ff_scorer_bind_memory",
@@ -77,6 +77,7 @@ def lib():
         L.ff_finalize.argtypes = [vp, vp]
         L.ff_encode.argtypes = [vp, vp, vp, i32, i32, vp, vp]
         L.ff_encode_host.argtypes = [vp, vp, vp, i32, i32, vp, vp]
+        L.ff_encode_host_async.argtypes = [vp, vp, vp, i32, i32, vp, vp]
         L.ff_check.argtypes = [vp, vp]
         L.ff_set_option.argtypes = [vp, i32, ctypes.c_int64]
         L.ff_model_destroy.argtypes = [vp]
@@ -201,6 +202,13 @@ class Encoder:
         if logits is None:
             logits = torch.empty((B, self.cfg.num_classes), dtype=torch.float32).pin_memory()
         check(lib().ff_encode_host(self.h, _ptr(ids), _ptr(mask), B, S, _ptr(logits), _stream_ptr(stream)))
+        return logits
+
+    def encode_host_async(self, ids, mask, logits, stream=None):
+        """ff_encode_host_async: pinned host ids / mask -> pinned host logits, enqueued
+        without synchronizing (read `logits` only after the stream is synchronized)."""
+        B, S = ids.shape
+        check(lib().ff_encode_host_async(self.h, _ptr(ids), _ptr(mask), B, S, _ptr(logits), _stream_ptr(stream)))
         return logits
 
     def check_inputs(self, stream=None):

@@ -463,3 +463,19 @@ def test_default_ffn1_fusion_bit_identical_to_separate_kernels(name, B, S):
     a = fused.encode(dev(ids), dev(mask)).cpu()
     b = Encoder(cfg, w, fused=False).encode(dev(ids), dev(mask)).cpu()
     assert torch.equal(a, b)
+
+
+def test_encode_host_async_matches_sync():
+    """ff_encode_host_async (no per-call sync, stream-ordered workspace reuse)
+    returns the same logits as ff_encode_host for several batches in flight."""
+    cfg = synth.config("c1").with_dtype(1)
+    w = synth.make_weights(cfg)
+    enc = Encoder(cfg, w)
+    batches = [synth.make_inputs(cfg, seed=700 + k, ragged=True) for k in range(4)]
+    host = [(torch.from_numpy(i).pin_memory(), torch.from_numpy(m).pin_memory()) for i, m in batches]
+    outs = [torch.empty((cfg.batch, cfg.num_classes), dtype=torch.float32).pin_memory() for _ in batches]
+    for (i, m), o in zip(host, outs):
+        enc.encode_host_async(i, m, o)
+    torch.cuda.synchronize()
+    for (i, m), o in zip(host, outs):
+        assert torch.equal(o, enc.encode_host(i, m))
