@@ -139,12 +139,16 @@ FF_API ff_status ff_encode(ff_model *m, const int32_t *d_token_ids, const int32_
 FF_API ff_status ff_encode_host(ff_model *m, const int32_t *h_token_ids, const int32_t *h_mask, int32_t batch,
                          int32_t seq, float *h_logits, void *stream);
 
-/* Pipelined form of ff_encode_host: the same copies and forward enqueued on
- * `stream` WITHOUT the final synchronization, so a serving loop can enqueue
- * batch k+1 while batch k runs.  h_token_ids / h_mask must stay valid and
- * unchanged, and h_logits must not be read, until the stream has been
- * synchronized (cudaStreamSynchronize or ff_check); pinned host memory is
- * required for the copies to be asynchronous. */
+/* Pipelined form of ff_encode_host: enqueued WITHOUT the final
+ * synchronization, so a serving loop can enqueue batch k+1 while batch k
+ * runs.  The ids / mask copies run on a library-owned copy stream into one of
+ * two workspace input sets (alternating per call, each reused only after the
+ * forward that last read it), so the next batch's upload overlaps the current
+ * forward; the forward and the logits copy run on `stream`.  h_token_ids /
+ * h_mask must stay valid and unchanged, and h_logits must not be read, until
+ * `stream` has been synchronized (cudaStreamSynchronize or ff_check); pinned
+ * host memory is required for the copies to be asynchronous.  Use one stream
+ * per model for these calls. */
 FF_API ff_status ff_encode_host_async(ff_model *m, const int32_t *h_token_ids, const int32_t *h_mask, int32_t batch,
                                       int32_t seq, float *h_logits, void *stream);
 

@@ -92,6 +92,11 @@ struct ff_model {
   int ldx16, ldx8, ldqkv, ldc16, ldc8, ldi16, ldi8;
   size_t ws_x16, ws_xq, ws_xs, ws_qkv, ws_ctx, ws_ctxq, ws_ctxs, ws_o, ws_h1, ws_h1q, ws_h1s, ws_i, ws_iq, ws_is;
   size_t ws_err, ws_ids, ws_mask, ws_logits, ws_pooled, ws_tq;
+  size_t ws_ids2, ws_mask2, ws_logits2;  // second host-I/O set (ff_encode_host_async double buffering)
+  // ff_encode_host_async: a copy stream brings set k+1's ids / mask in while set k computes
+  cudaStream_t io_stream = nullptr;
+  cudaEvent_t io_ready[2] = {nullptr, nullptr}, io_free[2] = {nullptr, nullptr};
+  int io_set = 0;
   size_t wsbytes = 0;
   uint8_t* dW = nullptr;
   uint8_t* dWS = nullptr;
@@ -202,6 +207,9 @@ void plan_memory(ff_model* m) {
   m->ws_ids = a.take(M * 4);
   m->ws_mask = a.take(M * 4);
   m->ws_logits = a.take(M * c.num_classes * 4);
+  m->ws_ids2 = a.take(M * 4);
+  m->ws_mask2 = a.take(M * 4);
+  m->ws_logits2 = a.take(M * c.num_classes * 4);
   m->ws_pooled = a.take(M * H * 4);  // pooler split-K partials [<= S][B][H] fp32
   m->wsbytes = align_up(a.off, 256);
 }
@@ -812,7 +820,36 @@ ff_status ff_encode_host(ff_model* m, const int32_t* h_token_ids, const int32_t*
 
 ff_status ff_encode_host_async(ff_model* m, const int32_t* h_token_ids, const int32_t* h_mask, int32_t batch,
                                int32_t seq, float* h_logits, void* stream) {
-  return encode_host_impl(m, h_token_ids, h_mask, batch, seq, h_logits, stream, false);
+  ff_status st = check_call(m, batch, seq);
+  if (st != FF_OK) return st;
+  if (!h_token_ids || !h_mask || !h_logits) return fail(FF_E_INVALID, "null buffer");
+  DeviceGuard dg(m->device);
+  if (!m->io_stream) {
+    FF_CK(cudaStreamCreateWithFlags(&m->io_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      FF_CK(cudaEventCreateWithFlags(&m->io_ready[i], cudaEventDisableTiming));
+      FF_CK(cudaEventCreateWithFlags(&m->io_free[i], cudaEventDisableTiming));
+      FF_CK(cudaEventRecord(m->io_free[i], static_cast<cudaStream_t>(stream)));
+    }
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int k = m->io_set;
+  m->io_set ^= 1;
+  const size_t n = (size_t)batch * seq;
+  int32_t* ids = m->ws<int32_t>(k ? m->ws_ids2 : m->ws_ids);
+  int32_t* mask = m->ws<int32_t>(k ? m->ws_mask2 : m->ws_mask);
+  float* logits = m->ws<float>(k ? m->ws_logits2 : m->ws_logits);
+  // inputs of set k on the copy stream, once the forward that last used set k is done
+  FF_CK(cudaStreamWaitEvent(m->io_stream, m->io_free[k], 0));
+  FF_CK(cudaMemcpyAsync(ids, h_token_ids, n * 4, cudaMemcpyHostToDevice, m->io_stream));
+  FF_CK(cudaMemcpyAsync(mask, h_mask, n * 4, cudaMemcpyHostToDevice, m->io_stream));
+  FF_CK(cudaEventRecord(m->io_ready[k], m->io_stream));
+  FF_CK(cudaStreamWaitEvent(s, m->io_ready[k], 0));
+  st = ff_encode(m, ids, mask, batch, seq, logits, stream);
+  if (st != FF_OK) return st;
+  FF_CK(cudaMemcpyAsync(h_logits, logits, (size_t)batch * m->cfg.num_classes * 4, cudaMemcpyDeviceToHost, s));
+  FF_CK(cudaEventRecord(m->io_free[k], s));
+  return FF_OK;
 }
 
 ff_status ff_check(ff_model* m, void* stream) {
@@ -922,6 +959,14 @@ ff_status ff_set_option(ff_model* m, int32_t option, int64_t value) {
 void ff_model_destroy(ff_model* m) {
   if (!m) return;
   for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
+  if (m->io_stream) {
+    cudaStreamSynchronize(m->io_stream);
+    cudaStreamDestroy(m->io_stream);
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(m->io_ready[i]);
+      cudaEventDestroy(m->io_free[i]);
+    }
+  }
   delete m;
 }
 
