@@ -322,8 +322,8 @@ def kernel_bytes(kind, cfg, B, S):
     F = sum(cfg.ffn_dim) / len(cfg.ffn_dim)
     D = A * d
     q = cfg.dtype[0] == 1
-    if kind == "attention":
-        return M * 3 * D * 2 + M * 4 + M * D * 2
+    if kind == "attention":  # int8 layers store s8 ctx + row scales (fused requant), fp16 layers fp16 ctx
+        return M * 3 * D * 2 + M * 4 + (M * D + 4 * M if q else M * D * 2)
     if kind == "add_ln":
         return M * H * 2 * 2 + M * H * 2 + (M * H + M * 4 if q else 0) + 2 * H * 4
     if kind == "quant_rows":
