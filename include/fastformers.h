@@ -205,9 +205,16 @@ FF_API ff_status ff_check(ff_model *m, void *stream);
  * ff_kernel_kind of the forward launches that use PDL (default all; only
  * while FF_OPT_PDL = 1). */
 #define FF_OPT_PDL_KINDS 11
+/* FF_OPT_ATTN_SPLIT (process-wide, may be set with m = NULL): 1 = the
+ * tcgen05 attention may run as clusters of 2-8 CTAs that split each
+ * sequence's heads (row amax of the fused int8 requant exchanged through
+ * DSMEM) when that lowers the heads on the busiest CTA; 0 = default, one CTA
+ * per sequence (splits measured slower on C3).  Results are identical. */
+#define FF_OPT_ATTN_SPLIT 12
 /* Set `option` to `value` on model m (invalidates its captured graphs).  The
  * process-wide options FF_OPT_PDL, FF_OPT_GEMM_MC, FF_OPT_PDL_RR,
- * FF_OPT_GEMM_BALANCE and FF_OPT_PDL_KINDS may be set with m = NULL.
+ * FF_OPT_GEMM_BALANCE, FF_OPT_PDL_KINDS and FF_OPT_ATTN_SPLIT may be set with
+ * m = NULL.
  * FF_E_INVALID for an unknown option / bad value / NULL m otherwise. */
 FF_API ff_status ff_set_option(ff_model *m, int32_t option, int64_t value);
 

@@ -876,6 +876,14 @@ ff_status ff_set_option(ff_model* m, int32_t option, int64_t value) {
     ff::g_gemm_mc = value != 0 ? 1 : 0;
     return FF_OK;
   }
+  if (option == FF_OPT_ATTN_SPLIT) {  // process-wide
+    ff::g_attn_split = value != 0 ? 1 : 0;
+    if (m) {
+      for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
+      m->graphs.clear();
+    }
+    return FF_OK;
+  }
   if (option == FF_OPT_PDL_KINDS) {  // process-wide
     ff::g_pdl_kinds = (unsigned)value;
     if (m) {

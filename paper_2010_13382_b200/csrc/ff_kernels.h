@@ -88,6 +88,7 @@ struct GemmPlan {
   bool pair;        // chosen for the current M
   bool mc;          // pairs run as clusters of two with W multicast (g_gemm_mc)
 };
+extern int g_attn_split;  // FF_OPT_ATTN_SPLIT (attention_tc.cu): clusters may split a sequence's heads
 extern int g_gemm_balance;  // FF_OPT_GEMM_BALANCE: tail balancing of the pair GEMMs
 extern int g_gemm_mc;  // FF_OPT_GEMM_MC: 1 = CTA-pair GEMMs share W k-blocks by TMA multicast
 

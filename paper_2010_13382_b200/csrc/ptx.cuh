@@ -109,6 +109,13 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
   return r;
 }
+// 4-byte store into another CTA's smem (shared::cluster address) whose
+// completion is counted as 4 tx bytes on that CTA's mbarrier.
+__device__ __forceinline__ void st_async_f32(uint32_t cluster_addr, float v, uint32_t cluster_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(cluster_addr),
+               "r"(__float_as_uint(v)), "r"(cluster_bar)
+               : "memory");
+}
 // Arrive on an mbarrier of another CTA of the cluster (default .release.cta
 // semantics, as CUTLASS's ClusterBarrier::arrive(cta_id)); used after
 // tcgen05.fence::before_thread_sync to hand a drained TMEM accumulator back.

@@ -30,6 +30,7 @@ FF_OPT_FUSED_MASK = 8
 FF_OPT_PDL_RR = 9
 FF_OPT_GEMM_BALANCE = 10
 FF_OPT_PDL_KINDS = 11
+FF_OPT_ATTN_SPLIT = 12
 KERNEL_KINDS = ["embed_ln", "gemm_f16", "gemm_i8", "attention", "quant_rows", "add_ln", "head", "gemm_rr_f16",
                 "gemm_rr_i8"]
 STATUS_NAMES = ["FF_OK", "FF_E_INVALID", "FF_E_SHAPE", "FF_E_STATE", "FF_E_CUDA", "FF_E_INPUT", "FF_E_UNSUPPORTED",
@@ -262,6 +263,11 @@ def set_gemm_mc(on: bool):
 def set_gemm_balance(on: bool):
     """FF_OPT_GEMM_BALANCE (process-wide): split the last partial wave of CTA-pair tiles."""
     check(lib().ff_set_option(None, FF_OPT_GEMM_BALANCE, 1 if on else 0))
+
+
+def set_attn_split(on: bool):
+    """FF_OPT_ATTN_SPLIT (process-wide): clusters may split a sequence's heads in the tcgen05 attention."""
+    check(lib().ff_set_option(None, FF_OPT_ATTN_SPLIT, 1 if on else 0))
 
 
 def gemm(A, W, out_mode=0, bias=None, sx=None, sw=None, act=-1, out=None, cta_pair=None):

@@ -13,6 +13,7 @@ import pytest
 
 import oracle
 from oracle import Oracle
+from paper_2010_13382_b200 import fastformers as ffb
 from paper_2010_13382_b200 import synth
 from paper_2010_13382_b200.fastformers import FF_E_INPUT, FF_E_SHAPE, Encoder, FFError
 
@@ -479,3 +480,22 @@ def test_encode_host_async_matches_sync():
     torch.cuda.synchronize()
     for (i, m), o in zip(host, outs):
         assert torch.equal(o, enc.encode_host(i, m))
+
+
+@pytest.mark.parametrize("name,B,S", [("c1", 4, 32), ("c3", 256, 128), ("c3", 37, 96)])
+@pytest.mark.parametrize("dt", [1, 0])
+def test_attention_cluster_head_split_identical(name, B, S, dt):
+    """FF_OPT_ATTN_SPLIT: clusters of CTAs splitting each sequence's heads (the
+    fused int8 requant's row amax exchanged through DSMEM) give bit-identical
+    logits to one CTA per sequence."""
+    cfg = synth.config(name).with_dtype(dt).with_batch(B, S)
+    w = synth.make_weights(cfg)
+    ids, mask = synth.make_inputs(cfg, B=B, S=S, ragged=True, seed=91)
+    out = {}
+    try:
+        for split in (False, True):
+            ffb.set_attn_split(split)
+            out[split] = Encoder(cfg, w).encode(dev(ids), dev(mask)).cpu()
+    finally:
+        ffb.set_attn_split(False)
+    assert torch.equal(out[True], out[False])
