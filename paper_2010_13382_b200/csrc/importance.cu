@@ -208,7 +208,54 @@ __global__ void __launch_bounds__(256, 2) sgemm128_kernel(SG g) {
   }
 }
 
+// Split-K for the narrow linears (N = H = 768 at M = 4096 gives 192 big tiles,
+// 0.65 of a wave at 2 CTAs per SM): the K range is cut into `splits` equal
+// parts computed by one launch (grid z = split, partials to g_sk_ws) and
+// summed in a fixed order by splitk_reduce_kernel (+ bias, + C if accumulating).
+float* g_sk_ws = nullptr;  // scratch of the scorer being run (set by score_batch)
+size_t g_sk_cap = 0;       // floats
+
+__global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits, int M, int N,
+                                     const float* __restrict__ bias, float* C, long long sCm, int accumulate) {
+  const size_t n_el = (size_t)M * N;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n_el; i += (size_t)gridDim.x * blockDim.x) {
+    const int m = (int)(i / N), n = (int)(i - (size_t)m * N);
+    float v = 0.0f;
+    for (int s = 0; s < splits; ++s) v += part[(size_t)s * n_el + i];
+    if (bias) v += bias[n];
+    float* c = C + m * sCm + n;
+    *c = accumulate ? *c + v : v;
+  }
+}
+
 cudaError_t sgemm(const SG& g, int nz, cudaStream_t s) {
+  const long long big_tiles = (long long)((g.N + LBN - 1) / LBN) * ((g.M + LBM - 1) / LBM) * nz;
+  if (nz == 1 && g.M >= 256 && g.N >= 256 && big_tiles < 2 * ff::kNumSMs && g_sk_ws != nullptr) {
+    int splits = 0;
+    for (int cand = 4; cand >= 2; --cand)
+      if (g.K % cand == 0 && g.K / cand >= 256 && (size_t)cand * g.M * g.N <= g_sk_cap) {
+        splits = cand;
+        break;
+      }
+    if (splits > 0) {
+      const int klen = g.K / splits;
+      SG gs = g;
+      gs.K = klen;
+      gs.nh = 1;
+      gs.sAb = (long long)klen * g.sAk;
+      gs.sBb = (long long)klen * g.sBk;
+      gs.C = g_sk_ws;
+      gs.sCb = (long long)g.M * g.N;
+      gs.sCm = g.N;
+      gs.bias = nullptr;
+      gs.accumulate = 0;
+      dim3 grid((g.N + LBN - 1) / LBN, (g.M + LBM - 1) / LBM, splits);
+      sgemm128_kernel<<<grid, 256, 0, s>>>(gs);
+      splitk_reduce_kernel<<<4 * ff::kNumSMs, 256, 0, s>>>(g_sk_ws, splits, g.M, g.N, g.bias, g.C, g.sCm,
+                                                            g.accumulate);
+      return cudaGetLastError();
+    }
+  }
   if (g.M >= 256 && g.N >= 256) {
     dim3 grid((g.N + LBN - 1) / LBN, (g.M + LBM - 1) / LBM, nz);
     sgemm128_kernel<<<grid, 256, 0, s>>>(g);
@@ -502,7 +549,7 @@ struct ff_scorer {
   size_t tok, pos, type0, eg, eb, pw, pb, cw, cb;
   uint32_t top_loaded = 0;
   size_t wbytes = 0, wsbytes = 0;
-  size_t Xout, dX, dZ, dY1, dAm, dC, dP, dQKV, colg, lossb, errf, ids, mask, labels;
+  size_t Xout, dX, dZ, dY1, dAm, dC, dP, dQKV, colg, lossb, errf, skws, ids, mask, labels;
   int Dmax = 0, Fmax = 0, Amax = 0;
   uint8_t* dW = nullptr;
   uint8_t* dWS = nullptr;
@@ -578,6 +625,7 @@ void plan_scorer(ff_scorer* m) {
   m->dP = take(M * m->Amax * Sm);
   m->dQKV = take(M * 3 * m->Dmax);
   m->colg = take((size_t)kRowChunks * std::max(m->Fmax, m->Dmax));
+  m->skws = take(4 * M * std::max((size_t)H, (size_t)m->Dmax));  // split-K partials
   m->lossb = take(M);
   m->errf = take(64);
   m->wsbytes = o;
@@ -621,6 +669,8 @@ ff_status score_batch(ff_scorer* m, const int* ids, const int* mask, const int* 
   const float scale = 1.0f / sqrtf((float)d);
   const int rt = rows_threads(H);
   const size_t lnsm = (size_t)(H + 32) * 4;
+  g_sk_ws = m->ws(m->skws);  // split-K scratch of this scorer (stream-ordered use)
+  g_sk_cap = 4 * (size_t)c.max_tokens * (size_t)std::max(H, m->Dmax);
   // ---- forward, keeping what the backward needs
   int* errf = reinterpret_cast<int*>(m->dWS + m->errf);
   embed_ln_f32_kernel<<<M, rt, lnsm, s>>>(ids, mask, S, H, c.vocab_size, m->w(m->tok), m->w(m->pos), m->w(m->type0),
