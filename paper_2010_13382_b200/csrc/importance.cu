@@ -418,28 +418,30 @@ __global__ void act_bwd_kernel(const float* U, float* dA, size_t n, int act) {
 // Classifier head of sequence b, forward and backward (block per sequence):
 // pool = tanh(Wp x0 + bp), logits = Wc pool + bc, loss_b = CE; writes
 // dX[b*S + 0, :] = Wp^T ((Wc^T dlogits) * (1 - pool^2)), dlogits = (p - y) / B.
-__global__ void head_fwd_bwd_kernel(const float* X, int S, int H, int C, int B, const float* Wp, const float* bp,
-                                    const float* Wc, const float* bc, const int* labels, float* dX, float* loss_b,
-                                    float* logits_out, int* err) {
-  extern __shared__ float sm[];
-  float* x0 = sm;            // [H]
-  float* pool = sm + H;      // [H]
-  float* dpre = sm + 2 * H;  // [H]
-  float* lg = sm + 3 * H;    // [C] (C <= 64)
-  float* red = lg + 64;
-  const int b = blockIdx.x;
-  const float* xr = X + (size_t)b * S * H;
-  for (int j = threadIdx.x; j < H; j += blockDim.x) x0[j] = xr[j];
-  __syncthreads();
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int o = w; o < H; o += nw) {  // warp per pooler output
-    float s = 0.0f;
-    for (int j = l; j < H; j += 32) s += Wp[(size_t)o * H + j] * x0[j];
+// Classifier head forward and backward in three launches (the single-CTA-per-
+// sequence version was latency-bound: 2 x H^2 MACs on 32 SMs):
+// head_pool_kernel (grid B x H/8, warp per pooler output): pool = tanh(Wp x0 + bp);
+// head_loss_kernel (CTA per sequence): logits = Wc pool + bc, loss_b = CE,
+//   dlogits = (p - y) / B, dpre = (Wc^T dlogits) * (1 - pool^2);
+// head_dx_kernel (grid B x H/256, thread per feature): dX[b*S + 0, j] = sum_o Wp[o][j] dpre[o].
+__global__ void head_pool_kernel(const float* X, int S, int H, const float* Wp, const float* bp, float* pool) {
+  const int b = blockIdx.x, w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int o = blockIdx.y * 8 + w;
+  if (o >= H) return;
+  const float* x0 = X + (size_t)b * S * H;
+  float s = 0.0f;
+  for (int j = l; j < H; j += 32) s += Wp[(size_t)o * H + j] * x0[j];
 #pragma unroll
-    for (int q = 16; q > 0; q >>= 1) s += __shfl_xor_sync(0xffffffffu, s, q);
-    if (l == 0) pool[o] = tanhf(s + bp[o]);
-  }
-  __syncthreads();
+  for (int q = 16; q > 0; q >>= 1) s += __shfl_xor_sync(0xffffffffu, s, q);
+  if (l == 0) pool[(size_t)b * H + o] = tanhf(s + bp[o]);
+}
+
+__global__ void head_loss_kernel(const float* pool_all, int H, int C, int B, const float* Wc, const float* bc,
+                                 const int* labels, float* loss_b, float* logits_out, float* dpre_all, int* err) {
+  __shared__ float lg[64];
+  const int b = blockIdx.x;
+  const float* pool = pool_all + (size_t)b * H;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int c = w; c < C; c += nw) {
     float s = 0.0f;
     for (int j = l; j < H; j += 32) s += Wc[(size_t)c * H + j] * pool[j];
@@ -469,16 +471,17 @@ __global__ void head_fwd_bwd_kernel(const float* X, int S, int H, int C, int B, 
   for (int j = threadIdx.x; j < H; j += blockDim.x) {
     float s = 0.0f;
     for (int c = 0; c < C; ++c) s += Wc[(size_t)c * H + j] * lg[c];
-    dpre[j] = s * (1.0f - pool[j] * pool[j]);
+    dpre_all[(size_t)b * H + j] = s * (1.0f - pool[j] * pool[j]);
   }
-  __syncthreads();
-  float* dx0 = dX + (size_t)b * S * H;
-  for (int j = threadIdx.x; j < H; j += blockDim.x) {
-    float s = 0.0f;
-    for (int o = 0; o < H; ++o) s += Wp[(size_t)o * H + j] * dpre[o];
-    dx0[j] = s;
-  }
-  (void)red;
+}
+
+__global__ void head_dx_kernel(const float* dpre_all, int S, int H, const float* Wp, float* dX) {
+  const int b = blockIdx.x, j = blockIdx.y * blockDim.x + threadIdx.x;
+  if (j >= H) return;
+  const float* dpre = dpre_all + (size_t)b * H;
+  float s = 0.0f;
+  for (int o = 0; o < H; ++o) s += Wp[(size_t)o * H + j] * dpre[o];
+  dX[(size_t)b * S * H + j] = s;
 }
 
 __global__ void loss_mean_kernel(const float* loss_b, int B, float* out) {
@@ -549,7 +552,7 @@ struct ff_scorer {
   size_t tok, pos, type0, eg, eb, pw, pb, cw, cb;
   uint32_t top_loaded = 0;
   size_t wbytes = 0, wsbytes = 0;
-  size_t Xout, dX, dZ, dY1, dAm, dC, dP, dQKV, colg, lossb, errf, skws, ids, mask, labels;
+  size_t Xout, dX, dZ, dY1, dAm, dC, dP, dQKV, colg, lossb, errf, skws, headws, ids, mask, labels;
   int Dmax = 0, Fmax = 0, Amax = 0;
   uint8_t* dW = nullptr;
   uint8_t* dWS = nullptr;
@@ -626,6 +629,7 @@ void plan_scorer(ff_scorer* m) {
   m->dQKV = take(M * 3 * m->Dmax);
   m->colg = take((size_t)kRowChunks * std::max(m->Fmax, m->Dmax));
   m->skws = take(4 * M * std::max((size_t)H, (size_t)m->Dmax));  // split-K partials
+  m->headws = take(2 * M * H);                                     // head: pool, dpre [B x H] each
   m->lossb = take(M);
   m->errf = take(64);
   m->wsbytes = o;
@@ -714,9 +718,14 @@ ff_status score_batch(ff_scorer* m, const int* ids, const int* mask, const int* 
   }
   // ---- head: loss and the gradient at position 0 of the last layer
   SC_CK(cudaMemsetAsync(m->ws(m->dX), 0, (size_t)M * H * 4, s));
-  head_fwd_bwd_kernel<<<B, 256, (size_t)(3 * H + 64 + 32) * 4, s>>>(
-      m->ws(m->Xout), S, H, C, B, m->w(m->pw), m->w(m->pb), m->w(m->cw), m->w(m->cb), labels, m->ws(m->dX),
-      m->ws(m->lossb), logits, errf);
+  {
+    float* pool = m->ws(m->headws);
+    float* dpre = pool + (size_t)B * H;
+    head_pool_kernel<<<dim3(B, (H + 7) / 8), 256, 0, s>>>(m->ws(m->Xout), S, H, m->w(m->pw), m->w(m->pb), pool);
+    head_loss_kernel<<<B, 256, 0, s>>>(pool, H, C, B, m->w(m->cw), m->w(m->cb), labels, m->ws(m->lossb), logits, dpre,
+                                       errf);
+    head_dx_kernel<<<dim3(B, (H + 255) / 256), 256, 0, s>>>(dpre, S, H, m->w(m->pw), m->ws(m->dX));
+  }
   SL(cudaGetLastError(), "head");
   if (loss) {
     loss_mean_kernel<<<1, 32, 0, s>>>(m->ws(m->lossb), B, loss);
