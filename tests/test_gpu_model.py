@@ -499,3 +499,20 @@ def test_attention_cluster_head_split_identical(name, B, S, dt):
     finally:
         ffb.set_attn_split(False)
     assert torch.equal(out[True], out[False])
+
+
+@pytest.mark.parametrize("mask_bits", [1, 3, 4, 5, 6, 7])
+def test_every_fusion_mask_within_drift_bound(mask_bits):
+    """FF_OPT_FUSED_MASK combinations with a LayerNorm fusion (the LN sums run in
+    another order): C3-shaped int8 logits (B 16, ragged) within the
+    DESIGN §3 drift bound of the oracle, like the default path."""
+    cfg = synth.config("c3").with_dtype(1).with_batch(16, 128)
+    w = synth.make_weights(cfg)
+    ids, mask = synth.make_inputs(cfg, B=16, S=128, ragged=True, seed=55)
+    got = f32(Encoder(cfg, w, fused=mask_bits).encode(dev(ids), dev(mask)))
+    orc = Oracle(cfg, w)
+    rows = [0, 5, 15]
+    ref = orc.encode(ids[rows], mask[rows])
+    drift = np.abs(orc.encode(ids[rows], mask[rows], acc32=True) - ref).max()
+    assert np.abs(got[rows] - ref).max() <= max(3 * drift, 1e-3 * np.abs(ref).max())
+    assert (got[rows].argmax(1) == ref.argmax(1)).all() or _margin_ok(ref, got[rows], 2e-2) == 1.0
