@@ -54,7 +54,11 @@ def parse():
     ap.add_argument("--no-dynamic", action="store_true", help="skip the dynamic-length batching side measurement")
     ap.add_argument("--no-importance", action="store_true", help="skip the importance-scoring side measurement")
     ap.add_argument("--fused", type=int, default=None,
-                    help="1/0: force the fused GEMM+LayerNorm / GEMM+requant epilogues on/off (default: library default)")
+                    help="FF_OPT_FUSED_MASK 0..7 (bit 0 out-proj+LN1, bit 1 FFN1+requant, bit 2 FFN2+LN2); "
+                         "default: the library default")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C2 / C3-unpruned / C4 / C5 side measurements")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="weak: B sequences per GPU per step; strong: the config's batch split across the GPUs")
     return ap.parse_args()
 
 
@@ -65,12 +69,12 @@ def workload(args):
     return cfg
 
 
-def config_json(cfg, args, n):
+def config_json(cfg, args, n, G):
     idx = {"c1": 0, "c2": 1, "c3": 2, "c4": 3, "c5": 4}.get(cfg.name)
     return {"workload": f"BASELINE configs[{idx}] {cfg.name}: {cfg.num_layers}L H{cfg.hidden} heads{sorted(set(cfg.heads))} "
                         f"FFN{sorted(set(cfg.ffn_dim))} {args.dtype}, random-init weights",
-            "batch_per_gpu": cfg.batch, "global_batch": cfg.batch * n, "seq_len": cfg.seq,
-            "parallelism": f"dp{n} (batch sharding, NCCL gather of logits)",
+            "batch_per_gpu": G // n, "global_batch": G, "seq_len": cfg.seq,
+            "parallelism": f"dp{n} (batch sharding, async NCCL gather of logits)",
             "l2": "flushed between timed steps (256 MiB memset), per-step CUDA events",
             "inputs": "synthetic ids U[5,V) + CLS, all-ones mask (fixed seq), 4 rotating batches per rank"}
 
@@ -304,7 +308,7 @@ def run_reference(args):
     line = {"metric": "sequences/sec at seq 128 (int8 encoder forward, pruned distilroberta shape)", "value": value,
             "unit": unit, "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": wall / steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8" if args.dtype == "i8" else "f16", "data": "synthetic (random-init weights, random ids)",
-            "config": config_json(cfg, args, 1), "impl": "reference",
+            "config": config_json(cfg, args, 1, cfg.batch), "impl": "reference",
             "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "oracle",
                              "sample": f"{cores} sequences per step (one oracle instance per core), {steps} steps"
                                        + (f" (capped from --steps {args.steps} to fit ~3 min)" if steps < args.steps
@@ -314,9 +318,39 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ ours
+ROLE_NAMES = ("qkv", "oproj", "ffn1", "ffn2")
+RR_SUFFIX = {"oproj": "_ln1", "ffn1": "_quant", "ffn2": "_ln2"}
+
+
+def gemm_shapes(cfg, role):
+    """(N, K) of a GEMM role per layer."""
+    H, d = cfg.hidden, cfg.head_dim
+    out = []
+    for A, F in zip(cfg.heads, cfg.ffn_dim):
+        D = A * d
+        out.append({"qkv": (3 * D, H), "oproj": (H, D), "ffn1": (F, H), "ffn2": (H, F)}[role])
+    return out
+
+
+def role_of_launches(kinds):
+    """Map one forward's launch kinds (ff_profile order) to roles: the k-th GEMM
+    launch of a layer is QKV / out-proj / FFN1 / FFN2 (plain or with a fused
+    row-reduction epilogue, ff_api.cu run_forward)."""
+    roles, g = [], 0
+    for k in kinds:
+        if k.startswith("gemm"):
+            r = ROLE_NAMES[g % 4]
+            g += 1
+            dt = k.rsplit("_", 1)[1]
+            roles.append(f"gemm_{r}{RR_SUFFIX.get(r, '') if k.startswith('gemm_rr') else ''}_{dt}")
+        else:
+            roles.append(k)
+    return roles
+
+
 def kernel_bytes(kind, cfg, B, S):
     """Algorithmic HBM bytes of one launch of an HBM-bound kernel kind (mean
-    over the layer's launches of that kind), DESIGN.md 'Roofline'."""
+    over the layer's launches of that kind), DESIGN.md §6."""
     M, H, d = B * S, cfg.hidden, cfg.head_dim
     A = sum(cfg.heads) / len(cfg.heads)
     F = sum(cfg.ffn_dim) / len(cfg.ffn_dim)
@@ -334,34 +368,151 @@ def kernel_bytes(kind, cfg, B, S):
     return None
 
 
-def gemm_flops(cfg, B, S):
-    return cfg.gemm_flops_per_seq(S) * B
+def gemm_role_work(role, cfg, B, S):
+    """(ops, algorithmic HBM bytes) per launch of a GEMM role (mean over
+    layers): ops = 2 M N K; bytes = A read once + W read once + outputs
+    (fp16, or s8 + row scales for the FFN1 requant fusion) + the residual
+    read of the LN fusions."""
+    M = B * S
+    base = role.split("_")[1]
+    i8 = role.endswith("_i8")
+    eb = 1 if i8 else 2
+    shapes = gemm_shapes(cfg, base)
+    ops = sum(2.0 * M * N * K for N, K in shapes) / len(shapes)
+    by = 0.0
+    for N, K in shapes:
+        b = M * K * eb + N * K * eb
+        if "_quant" in role:
+            b += M * N + 4 * M
+        elif "_ln" in role:
+            b += M * N * 2 + M * N * 2 + ((M * N + 4 * M) if i8 else 0)
+        else:
+            b += M * N * 2
+        by += b
+    return ops, by / len(shapes)
 
 
-def fused_mask(enc):
-    """FF_OPT_FUSED_MASK in effect for an Encoder (None = library default 2)."""
-    f = enc.fused
-    return 2 if f is None else (7 if f is True else 0 if f is False else int(f))
+def profile_roles(enc, ids, mask, n=3):
+    """Per-role device time of one forward: ff_profile (CUDA events around every
+    launch on the launching stream, un-graphed) averaged over n forwards."""
+    acc = {}
+    for _ in range(n):
+        prof = enc.profile(ids, mask)
+        for role, (kind, ms) in zip(role_of_launches([k for k, _ in prof]), prof):
+            acc.setdefault(role, []).append(ms)
+    return {r: {"ms_per_step": sum(v) / n, "launches_per_step": len(v) // n} for r, v in acc.items()}
 
 
-def gemm_flops_by_kind(cfg, B, S, mask):
-    """Algorithmic GEMM ops per step split between plain tcgen05 GEMM launches
-    ('gemm') and row-reduction GEMMs with fused LN / requant ('gemm_rr'),
-    following ff_api.cu's fusion rules (row = 256 x 1..8 columns; the FFN1
-    requant fusion only in int8 layers)."""
-    H, d, M = cfg.hidden, cfg.head_dim, B * S
-    rr_row = lambda n: n % 256 == 0 and 1 <= n // 256 <= 8
-    plain = rr = 0.0
-    for A, F, dt in zip(cfg.heads, cfg.ffn_dim, cfg.dtype):
-        D = A * d
-        plain += 2.0 * M * H * 3 * D  # QKV
-        for bit, fl, ok in ((1, 2.0 * M * D * H, rr_row(H)), (2, 2.0 * M * H * F, dt == 1 and rr_row(F)),
-                            (4, 2.0 * M * F * H, rr_row(H))):
-            if (mask & bit) and ok:
-                rr += fl
-            else:
-                plain += fl
-    return {"gemm": plain, "gemm_rr": rr}
+def roofline_table(prof, cfg, B, S, peaks):
+    """Per role: achieved vs the measured peak.  GEMMs: tensor (int8 = 2 x the
+    measured bf16 BURST peak, the nominal int8/bf16 ratio; kernels timed one by
+    one inside a forward, so the burst figure applies) and the combined
+    tensor + HBM bound max(ops / P_tensor, bytes / P_hbm) / time; HBM-bound
+    kernels: algorithmic bytes / time against the measured copy bandwidth."""
+    hbm = peaks["hbm_gbs"]
+    total = sum(e["ms_per_step"] for e in prof.values())
+    out = {}
+    for role, e in sorted(prof.items(), key=lambda kv: -kv[1]["ms_per_step"]):
+        n = e["launches_per_step"]
+        us = e["ms_per_step"] / n * 1e3
+        ent = {"ms_per_step": e["ms_per_step"], "share": e["ms_per_step"] / total, "launches_per_step": n,
+               "avg_launch_us": us}
+        if role.startswith("gemm"):
+            ops, by = gemm_role_work(role, cfg, B, S)
+            pk = peaks["bf16_tflops"] * (2.0 if role.endswith("i8") else 1.0)
+            ach = ops / (us * 1e-6) / 1e12
+            t_star = max(ops / (pk * 1e12), by / (hbm * 1e9))
+            ent.update({"achieved": ach, "unit": "TOP/s" if role.endswith("i8") else "TFLOP/s", "peak": pk,
+                        "frac": ach / pk, "algorithmic_ops": ops, "algorithmic_bytes": by,
+                        "bound": "tensor" if ops / pk / 1e12 >= by / hbm / 1e9 else "hbm",
+                        "combined_frac": t_star / (us * 1e-6)})
+        else:
+            by = kernel_bytes(role, cfg, B, S)
+            if by is not None:
+                ach = by / (us * 1e-6) / 1e9
+                ent.update({"achieved": ach, "unit": "GB/s", "peak": hbm, "frac": ach / hbm, "bound": "hbm",
+                            "algorithmic_bytes": by})
+        out[role] = ent
+    return out
+
+
+def plain_gemm_class(table):
+    """All plain (unfused) tcgen05 GEMM launches of a step as one class."""
+    ops = t = 0.0
+    pk = None
+    for role, e in table.items():
+        if role.startswith("gemm") and not any(x in role for x in ("_ln1", "_ln2", "_quant")):
+            ops += e["algorithmic_ops"] * e["launches_per_step"]
+            t += e["ms_per_step"] * 1e-3
+            pk = e["peak"]
+    if t == 0:
+        return None
+    return {"achieved": ops / t / 1e12, "peak": pk, "frac": ops / t / 1e12 / pk, "ms_per_step": t * 1e3}
+
+
+def dominant_roofline(table, traffic_key, peak_src):
+    dom = max(table, key=lambda r: table[r]["ms_per_step"])
+    d = table[dom]
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(f"{traffic_key}_{dom}")
+    if dom.startswith("gemm"):
+        return {"bound": "tensor", "achieved": d["achieved"], "peak": d["peak"], "unit": d["unit"],
+                "frac": d["frac"], "traffic": traffic, "kernel": dom, "combined_frac": d["combined_frac"],
+                "peak_source": f"{peak_src}: bf16_tflops (burst) x {'2 (nominal int8/bf16 ratio)' if dom.endswith('i8') else '1'}",
+                "algorithmic": f"{d['algorithmic_ops'] / 1e9:.1f} G{'OP' if dom.endswith('i8') else 'FLOP'} and "
+                               f"{d['algorithmic_bytes'] / 1e6:.1f} MB per launch, {d['launches_per_step']} launches "
+                               "per step (DESIGN.md §6)"}
+    return {"bound": "hbm", "achieved": d.get("achieved"), "peak": d.get("peak"), "unit": "GB/s",
+            "frac": d.get("frac"), "traffic": traffic, "kernel": dom, "peak_source": f"{peak_src}: hbm_gbs"}
+
+
+def time_forward(enc, dids, dmask, logits, stream, flush, steps, warmup=3):
+    """Device time of `steps` graph-replayed forwards (CUDA events per step on
+    the launching stream, L2 flushed before each step); returns ms per step."""
+    import torch
+    for k in range(warmup):
+        enc.encode(dids[k % len(dids)], dmask[k % len(dids)], logits)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for k in range(steps):
+        flush.zero_()
+        evs[k][0].record(stream)
+        enc.encode(dids[k % len(dids)], dmask[k % len(dids)], logits)
+        evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in evs) / steps
+
+
+def config_variant(name, dtype, stream, flush, peaks, peak_src, steps=20, **enc_kw):
+    """One BASELINE / SURVEY 8(d) d1 configuration at its own batch and seq:
+    throughput, the per-role roofline table and its dominant kernel."""
+    import torch
+    from paper_2010_13382_b200 import synth
+    from paper_2010_13382_b200.fastformers import Encoder
+    cfg = synth.config(name).with_dtype(dtype)
+    B, S = cfg.batch, cfg.seq
+    w = synth.make_weights(cfg)
+    enc = Encoder(cfg, w, max_tokens=B * S, **enc_kw)
+    ins = [synth.make_inputs(cfg, seed=1000 + k) for k in range(2)]
+    dids = [torch.from_numpy(i).cuda() for i, _ in ins]
+    dmask = [torch.from_numpy(m).cuda() for _, m in ins]
+    logits = torch.empty((B, cfg.num_classes), dtype=torch.float32, device="cuda")
+    ms = time_forward(enc, dids, dmask, logits, stream, flush, steps)
+    table = roofline_table(profile_roles(enc, dids[0], dmask[0]), cfg, B, S, peaks)
+    dt = "i8" if dtype == 1 else "f16"
+    out = {"workload": f"{name}: {cfg.num_layers}L H{cfg.hidden} heads{sorted(set(cfg.heads))} "
+                       f"FFN{sorted(set(cfg.ffn_dim))} {dt}, B {B} x S {S}",
+           "value": B / (ms / 1e3), "unit": "sequences/s", "ms_per_step": ms,
+           "roofline": dominant_roofline(table, f"{name}_{dt}", peak_src),
+           "plain_gemms": plain_gemm_class(table),
+           "kernels": {r: {k: (round(v, 4) if isinstance(v, float) else v) for k, v in e.items()
+                           if k in ("avg_launch_us", "launches_per_step", "share", "achieved", "frac",
+                                    "combined_frac", "unit")} for r, e in table.items()}}
+    del enc
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_ours(args):
@@ -377,170 +528,199 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines (rank / nranks) in the log
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = workload(args)
-    B, S = cfg.batch, cfg.seq
+    # weak scaling: every rank owns B sequences per step (global batch world x B);
+    # strong scaling: the global batch B is split across the ranks
+    strong = args.scaling == "strong"
+    G = cfg.batch if strong else cfg.batch * world  # global batch per step
+    from paper_2010_13382_b200.dist import ShardedEncoder, shard_range
+    lo, hi = shard_range(G, world, rank)
+    B, S = hi - lo, cfg.seq  # this rank's rows per step
     w = synth.make_weights(cfg)
-    enc_kw = {} if args.fused is None else {"fused": bool(args.fused)}
-    enc = Encoder(cfg, w, max_tokens=B * S, device=local, **enc_kw)
+    enc_kw = {} if args.fused is None else {"fused": args.fused}
+    enc = Encoder(cfg, w, max_tokens=max(B, 1) * S, device=local, **enc_kw)
     NB = 4
-    batches = [synth.make_inputs(cfg, seed=1000 + rank * 10 ** 6 + k) for k in range(NB)]
-    dids = [torch.from_numpy(i).cuda() for i, _ in batches]
-    dmask = [torch.from_numpy(m).cuda() for _, m in batches]
+    # the global batch of step k (replicated request queue): rank r's weak-scaling
+    # batch is r's own seeded batch, so every rank encodes exactly its own rows
+    gbatches = []
+    for k in range(NB):
+        if strong:
+            gbatches.append(synth.make_inputs(cfg, B=G, seed=1000 + k))
+        else:
+            parts = [synth.make_inputs(cfg, seed=1000 + r * 10 ** 6 + k) for r in range(world)]
+            gbatches.append((np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts])))
+    gids = [torch.from_numpy(i).cuda() for i, _ in gbatches]
+    gmask = [torch.from_numpy(m).cuda() for _, m in gbatches]
+    dids = [g[lo:hi].contiguous() for g in gids]  # this rank's shard (profiling, fp16 side runs)
+    dmask = [g[lo:hi].contiguous() for g in gmask]
     logits = torch.empty((B, cfg.num_classes), dtype=torch.float32, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
-    # Data parallelism (paper_2010_13382_b200/dist.py, tested with gloo): the
-    # global batch of step k is the concatenation of every rank's batch k; rank
-    # r encodes its contiguous shard and the logits are gathered to rank 0.
+    # Data parallelism (paper_2010_13382_b200/dist.py): each rank encodes its
+    # contiguous shard of the global batch; the logits are gathered to rank 0
+    # over NCCL on a side stream, overlapping the next step's forward.
     sharded = None
     if world > 1:
-        from paper_2010_13382_b200.dist import ShardedEncoder
-        gids, gmask = [], []
-        for k in range(NB):
-            parts = [synth.make_inputs(cfg, seed=1000 + r * 10 ** 6 + k) for r in range(world)]
-            gids.append(torch.from_numpy(np.concatenate([p[0] for p in parts])).cuda())
-            gmask.append(torch.from_numpy(np.concatenate([p[1] for p in parts])).cuda())
-        sharded = ShardedEncoder(lambda i, m: enc.encode(i, m, logits))
+        sharded = ShardedEncoder(lambda i, m, o: enc.encode(i, m, o), cfg.num_classes, G, device=f"cuda:{local}")
 
     def step(k):
         if sharded is not None:
-            sharded.encode_global(gids[k % NB], gmask[k % NB])
-        else:
-            enc.encode(dids[k % NB], dmask[k % NB], logits)
+            return sharded.submit(gids[k % NB], gmask[k % NB])
+        enc.encode(dids[k % NB], dmask[k % NB], logits)
+        return None
 
     for k in range(max(args.warmup, 3)):
-        step(k)
+        p = step(k)
+        if p is not None:
+            p.result()
     enc.check_inputs()
     torch.cuda.synchronize()
 
     # ---- per-kernel device times (CUDA events around each launch on the stream)
-    prof_runs = [enc.profile(dids[0], dmask[0]) for _ in range(3)]
-    by_kind = {}
-    for run in prof_runs:
-        for kind, ms in run:
-            by_kind.setdefault(kind, []).append(ms)
-    n_prof = len(prof_runs)
+    peaks, peak_src = load_peaks()
+    table = roofline_table(profile_roles(enc, dids[0], dmask[0]), cfg, B, S, peaks)
     launches_per_step = enc.launch_count(B, S)
 
     # ---- timed region
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    tail = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
     clocks = ClockSampler(local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     clocks.start()
+    pend = []
     for k in range(args.steps):
         flush.zero_()
         evs[k][0].record(stream)
-        step(args.warmup + k)
+        p = step(args.warmup + k)
         evs[k][1].record(stream)
+        if p is not None:
+            pend.append(p)
+            if len(pend) == sharded.depth:  # the oldest slot is reused by the next submit
+                pend.pop(0).wait()
+    tail[0].record(stream)
+    for p in pend:  # the last gathers: the only ones not hidden behind a forward
+        p.wait()
+    tail[1].record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    t_ms = sum(a.elapsed_time(b) for a, b in evs)
+    t_ms = sum(a.elapsed_time(b) for a, b in evs) + tail[0].elapsed_time(tail[1])
     t = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_ms = float(t.item())
-    value = world * B * args.steps / (t_ms / 1e3)
+    value = G * args.steps / (t_ms / 1e3)
 
     # ---- end to end through the public API with host buffers (pinned)
-    h_ids = [torch.from_numpy(i).pin_memory() for i, _ in batches]
-    h_mask = [torch.from_numpy(m).pin_memory() for _, m in batches]
-    h_logits = torch.empty((B, cfg.num_classes), dtype=torch.float32).pin_memory()
     e2e_steps = min(args.steps, 50)
-    for k in range(3):
-        enc.encode_host(h_ids[k % NB], h_mask[k % NB], h_logits)
-    if world > 1:
-        dist.barrier()
-    # one pinned result buffer per step: every step's logits are copied back
-    h_out = [torch.empty((B, cfg.num_classes), dtype=torch.float32).pin_memory() for _ in range(e2e_steps)]
-    t0 = time.perf_counter()
-    gather_list = [torch.empty_like(logits) for _ in range(world)] if (world > 1 and rank == 0) else None
-    for k in range(e2e_steps):
-        if world > 1:  # the host logits of every rank end up on rank 0
-            enc.encode_host(h_ids[k % NB], h_mask[k % NB], h_logits)
-            logits.copy_(h_logits, non_blocking=True)
-            dist.gather(logits, gather_list, dst=0)
-        else:  # pipelined serving loop: enqueue step k+1 while step k runs
+    if world == 1:
+        # pipelined serving loop: ff_encode_host_async copies ids / mask in, runs
+        # the forward and copies the logits to a per-step pinned host buffer
+        h_ids = [torch.from_numpy(i).pin_memory() for i, _ in gbatches]
+        h_mask = [torch.from_numpy(m).pin_memory() for _, m in gbatches]
+        h_out = [torch.empty((B, cfg.num_classes), dtype=torch.float32).pin_memory() for _ in range(e2e_steps)]
+        for k in range(3):
+            enc.encode_host_async(h_ids[k % NB], h_mask[k % NB], h_out[0])
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k in range(e2e_steps):
             enc.encode_host_async(h_ids[k % NB], h_mask[k % NB], h_out[k])
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    if world == 1:  # every step's result was read back: spot-check it against the device path
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
         enc.encode(dids[(e2e_steps - 1) % NB], dmask[(e2e_steps - 1) % NB], logits)
         torch.cuda.synchronize()
         assert torch.equal(h_out[-1], logits.cpu()), "e2e logits differ from the device path"
-
+        h2d, d2h = 2 * B * S * 4, B * cfg.num_classes * 4
+        how = ("ff_encode_host_async per step (pinned host ids+mask -> device, forward, logits -> a per-step "
+               "pinned host buffer), one stream sync after the steps; wall clock")
+    else:
+        # every rank: its shard's ids / mask from pinned host memory -> device
+        # (non-blocking), the sharded forward + async NCCL gather, and on rank 0
+        # the gathered global logits -> pinned host memory
+        h_ids = [torch.from_numpy(np.ascontiguousarray(i[lo:hi])).pin_memory() for i, _ in gbatches]
+        h_mask = [torch.from_numpy(np.ascontiguousarray(m[lo:hi])).pin_memory() for _, m in gbatches]
+        d_in = [(torch.empty((G, S), dtype=torch.int32, device="cuda"),
+                 torch.empty((G, S), dtype=torch.int32, device="cuda")) for _ in range(2)]
+        h_out = [torch.empty((G, cfg.num_classes), dtype=torch.float32).pin_memory() for _ in range(e2e_steps)]
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pend = []
+        for k in range(e2e_steps):
+            di, dm = d_in[k % 2]
+            di[lo:hi].copy_(h_ids[k % NB], non_blocking=True)
+            dm[lo:hi].copy_(h_mask[k % NB], non_blocking=True)
+            p = sharded.submit(di, dm)
+            pend.append((k, p))
+            if len(pend) == sharded.depth:
+                kk, pp = pend.pop(0)
+                r = pp.result()
+                if r is not None:
+                    h_out[kk].copy_(r, non_blocking=True)
+        for kk, pp in pend:
+            r = pp.result()
+            if r is not None:
+                h_out[kk].copy_(r, non_blocking=True)
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        h2d, d2h = 2 * B * S * 4, (G * cfg.num_classes * 4 if rank == 0 else 0)
+        how = ("per rank: pinned host ids+mask of its shard -> device, sharded forward, async NCCL gather of the "
+               "logits to rank 0, rank 0 copies the global logits to pinned host memory; wall clock, max over ranks")
     te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = world * B * e2e_steps / float(te.item())
+    e2e_value = G * e2e_steps / float(te.item())
 
-    # ---- fp16 side measurement of the same geometry (metric names fp16 & int8)
+    # ---- side measurements (1 GPU): the fp16 variant, the other fusion
+    # masks, the NEXT rows and the other SURVEY 8(d) d1 configurations
     variants = {}
     if not args.no_variants and world == 1:
         cfg16 = cfg.with_dtype(0)
         enc16 = Encoder(cfg16, w, max_tokens=B * S, device=local, **enc_kw)
-        for k in range(5):
-            enc16.encode(dids[k % NB], dmask[k % NB], logits)
-        torch.cuda.synchronize()
-        ev16 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(50)]
-        for k in range(50):
-            flush.zero_()
-            ev16[k][0].record(stream)
-            enc16.encode(dids[k % NB], dmask[k % NB], logits)
-            ev16[k][1].record(stream)
-        torch.cuda.synchronize()
-        t16 = sum(a.elapsed_time(b) for a, b in ev16)
-        p16 = enc16.profile(dids[0], dmask[0])
-        g16 = sum(ms for kd, ms in p16 if kd.startswith("gemm"))
-        peaks, _ = load_peaks()
-        variants["fp16"] = {"value": B * 50 / (t16 / 1e3), "unit": "sequences/s", "ms_per_step": t16 / 50,
-                            "gemm_tflops": gemm_flops(cfg16, B, S) / (g16 / 1e3) / 1e12,
-                            "gemm_frac_of_peak": gemm_flops(cfg16, B, S) / (g16 / 1e3) / 1e12 /
-                                                 peaks["bf16_tflops_sustained"]}
+        ms16 = time_forward(enc16, dids, dmask, logits, stream, flush, 50)
+        t16 = roofline_table(profile_roles(enc16, dids[0], dmask[0]), cfg16, B, S, peaks)
+        variants["fp16"] = {"value": B / (ms16 / 1e3), "unit": "sequences/s", "ms_per_step": ms16,
+                            "roofline": dominant_roofline(t16, f"{cfg.name}_f16", peak_src),
+                            "plain_gemms": plain_gemm_class(t16)}
         del enc16
         if cfg.dtype[0] == 1:
+            for fm in (0, 2, 7):
+                if fm == enc.fused_mask():  # the headline line already measures it
+                    continue
+                encm = Encoder(cfg, w, max_tokens=B * S, device=local, fused=fm)
+                msm = time_forward(encm, dids, dmask, logits, stream, flush, 50)
+                variants[f"fused_mask_{fm}"] = {
+                    "value": B / (msm / 1e3), "unit": "sequences/s", "ms_per_step": msm,
+                    "what": {0: "no fused epilogues (separate add_ln / quant_rows kernels)",
+                             2: "FFN1 + GELU + requant fused (round-1 default)",
+                             7: "all three cluster row-reduction epilogues (out-proj + LN1, FFN1 + requant, "
+                                "FFN2 + LN2)"}[fm]}
+                del encm
             # NEXT-2 (DESIGN R22): the paper's per-tensor u8 activation quantizer
             encpt = Encoder(cfg, w, max_tokens=B * S, device=local, act_quant=1)
-            for k in range(5):
-                encpt.encode(dids[k % NB], dmask[k % NB], logits)
-            torch.cuda.synchronize()
-            evp = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(50)]
-            for k in range(50):
-                flush.zero_()
-                evp[k][0].record(stream)
-                encpt.encode(dids[k % NB], dmask[k % NB], logits)
-                evp[k][1].record(stream)
-            torch.cuda.synchronize()
-            tp = sum(a.elapsed_time(b) for a, b in evp)
-            variants["int8_per_tensor_u8"] = {"value": B * 50 / (tp / 1e3), "unit": "sequences/s",
-                                              "ms_per_step": tp / 50,
+            mspt = time_forward(encpt, dids, dmask, logits, stream, flush, 50)
+            variants["int8_per_tensor_u8"] = {"value": B / (mspt / 1e3), "unit": "sequences/s", "ms_per_step": mspt,
                                               "what": "per-tensor u8 activations + zero point (P:104, DESIGN R22)"}
             del encpt
-        if cfg.dtype[0] == 1:
-            # all three cluster row-reduction epilogues (FF_OPT_FUSED_MASK 7): out-proj + LN1,
-            # FFN1 + requant, FFN2 + LN2 (LN sums in another order: not bit-identical)
-            encf = Encoder(cfg, w, max_tokens=B * S, device=local, fused=7)
-            for k in range(5):
-                encf.encode(dids[k % NB], dmask[k % NB], logits)
-            torch.cuda.synchronize()
-            evf = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(50)]
-            for k in range(50):
-                flush.zero_()
-                evf[k][0].record(stream)
-                encf.encode(dids[k % NB], dmask[k % NB], logits)
-                evf[k][1].record(stream)
-            torch.cuda.synchronize()
-            tf = sum(a.elapsed_time(b) for a, b in evf)
-            variants["fused_ln_epilogues"] = {
-                "value": B * 50 / (tf / 1e3), "unit": "sequences/s", "ms_per_step": tf / 50,
-                "what": "FF_OPT_FUSED_MASK 7: residual + LayerNorm (+ s8 rows) fused into the out-proj / FFN2 "
-                        "GEMM epilogues as well (cluster row reductions); LN sums in another order, so not "
-                        "bit-identical to the default; the GEMM kernels then carry the LN work"}
-            del encf
+        torch.cuda.empty_cache()
+        if not args.no_configs:
+            cv = {}
+            for name, dt in (("c2", 1), ("c2", 0), ("c2_9_900", 1), ("c2_8_600", 1), ("c3_unpruned", 1),
+                             ("c4", 0), ("c5", 0)):
+                cv[f"{name}_{'i8' if dt else 'f16'}"] = config_variant(name, dt, stream, flush, peaks, peak_src,
+                                                                      **enc_kw)
+            if cfg.name == "c3" and cfg.dtype[0] == 1:
+                cv["pruning_speedup_c3_vs_unpruned"] = {
+                    "value": value / cv["c3_unpruned_i8"]["value"],
+                    "what": "C3 (heads 12->8, FFN 3072->1536) over the unpruned distilroberta shape, int8, "
+                            "B 256 S 128 (paper P:97: 2.97x for 50%/75% pruning on CPU)"}
+            variants["configs"] = cv
         if not args.no_dynamic:
             variants["dynamic_length"] = dynamic_length_variant(cfg, enc, B, S, stream, flush)
         if not args.no_importance:
@@ -553,65 +733,21 @@ def run_ours(args):
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel class
-    peaks, peak_src = load_peaks()
-    step_prof_ms = {k: sum(v) / n_prof for k, v in by_kind.items()}
-    split = gemm_flops_by_kind(cfg, B, S, fused_mask(enc))
-    total_prof = sum(step_prof_ms.values())
-    dom = max(step_prof_ms, key=step_prof_ms.get)
-    kernels = {}
-    for kind, per_step in sorted(step_prof_ms.items(), key=lambda kv: -kv[1]):
-        n_launch = len(by_kind[kind]) // n_prof
-        ent = {"ms_per_step": per_step, "share": per_step / total_prof, "launches_per_step": n_launch,
-               "avg_launch_us": per_step / n_launch * 1e3}
-        if kind.startswith("gemm"):
-            ach = split["gemm_rr" if kind.startswith("gemm_rr") else "gemm"] / (per_step / 1e3) / 1e12
-            pk = peaks["bf16_tflops_sustained"] * (2.0 if kind.endswith("i8") else 1.0)
-            ent.update({"achieved": ach, "unit": "TFLOP/s", "peak": pk, "frac": ach / pk})
-            if kind.startswith("gemm_rr"):
-                ent["what"] = ("GEMM with a fused row-reduction epilogue (FF_OPT_FUSED_MASK "
-                               f"{fused_mask(enc)}: FFN1 + GELU + per-row requant); achieved = its GEMM ops only")
-        else:
-            by = kernel_bytes(kind, cfg, B, S)
-            if by is not None:
-                ach = by / (per_step / n_launch / 1e3) / 1e9
-                ent.update({"achieved": ach, "unit": "GB/s", "peak": peaks["hbm_gbs"], "frac": ach / peaks["hbm_gbs"]})
-        kernels[kind] = ent
-    d = kernels[dom]
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        tj = json.load(open(tp))
-        key = f"{cfg.name}_{args.dtype}_{dom}"
-        if key in tj:
-            traffic = tj[key]
-    if dom.startswith("gemm"):
-        roof = {"bound": "tensor", "achieved": d["achieved"], "peak": d["peak"], "unit": "TFLOP/s",
-                "frac": d["frac"], "traffic": traffic, "kernel": dom,
-                "peak_source": f"{peak_src}: bf16 sustained x {'2 (int8/bf16 nominal ratio)' if dom.endswith('i8') else '1'}",
-                "algorithmic": f"{split['gemm_rr' if dom.startswith('gemm_rr') else 'gemm'] / 1e9:.1f} "
-                               f"G{'OP' if dom.endswith('i8') else 'FLOP'} per step over "
-                               f"{d['launches_per_step']} launches (DESIGN.md Roofline)"}
-    else:
-        roof = {"bound": "hbm", "achieved": d.get("achieved"), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": d.get("frac"), "traffic": traffic, "kernel": dom, "peak_source": peak_src}
-
+    dt = "i8" if args.dtype == "i8" else "f16"
+    roof = dominant_roofline(table, f"{cfg.name}_{dt}", peak_src)
     line = {"metric": "sequences/sec at seq 128 (int8 encoder forward, pruned distilroberta shape)",
             "value": value, "unit": "sequences/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "int8" if args.dtype == "i8" else "f16", "data": "synthetic (random-init weights, random ids)",
-            "config": config_json(cfg, args, world),
-            "e2e": {"value": e2e_value, "unit": "sequences/s", "h2d_bytes_per_step": 2 * B * S * 4,
-                    "d2h_bytes_per_step": B * cfg.num_classes * 4,
-                    "how": ("ff_encode_host_async per step (pinned host ids+mask -> device, forward, logits -> a "
-                            "per-step pinned host buffer), one stream sync after the steps; wall clock" if world == 1
-                            else "ff_encode_host per step (copies in, forward, logits to host, sync) + NCCL gather "
-                                 "of the logits to rank 0; wall clock")},
+            "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong" if strong else "weak",
+            "vs_baseline": None, "dtype": "int8" if args.dtype == "i8" else "f16",
+            "data": "synthetic (random-init weights, random ids)",
+            "config": config_json(cfg, args, world, G),
+            "e2e": {"value": e2e_value, "unit": "sequences/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "how": how},
             "gpu_launches": launches_per_step * args.steps,
-            "clocks": clk, "roofline": roof, "kernels": kernels, "variants": variants}
+            "clocks": clk, "roofline": roof, "plain_gemms": plain_gemm_class(table), "kernels": table,
+            "variants": variants}
     if world == 1 and not args.no_cpu_baseline:
-        ids0, mask0 = batches[0]
-        line["cpu_baseline"] = cpu_baseline(cfg, w, ids0, mask0)
+        line["cpu_baseline"] = cpu_baseline(cfg, w, *gbatches[0])
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

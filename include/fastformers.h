@@ -171,9 +171,9 @@ FF_API ff_status ff_check(ff_model *m, void *stream);
  * default is FF_OPT_FUSED_MASK = 2, the FFN1 fusion only).  With 1, ff_encode_trace does not fill the O16 / Y16 dumps (never
  * materialised). */
 #define FF_OPT_FUSED_EPILOGUES 4
-/* FF_OPT_PDL (1 = default: launch every forward kernel with programmatic
- * dependent launch so its prologue overlaps the previous kernel's tail;
- * process-wide setting). */
+/* FF_OPT_PDL (1 = default: launch every forward kernel of this model with
+ * programmatic dependent launch so its prologue overlaps the previous
+ * kernel's tail; per model). */
 #define FF_OPT_PDL 5
 /* FF_OPT_ACT_QUANT: activation quantizer of the int8 layers.  0 = default:
  * Q8row, per-row symmetric s8 (north_star; DESIGN R6-R8); 1 = Q8tensor, the
@@ -182,41 +182,26 @@ FF_API ff_status ff_check(ff_model *m, void *stream);
  * R22).  1 disables FF_OPT_FUSED_EPILOGUES and breaks batch / padding
  * invariance by construction (the range spans the whole batch). */
 #define FF_OPT_ACT_QUANT 6
-/* FF_OPT_GEMM_MC (process-wide): 1 = CTA-pair GEMMs run as clusters of two
- * pairs stacked along M that share each W k-block by TMA multicast (half the
- * W bytes per SM from L2); 0 = independent pairs.  Results are identical. */
-#define FF_OPT_GEMM_MC 7
 /* FF_OPT_FUSED_MASK: per-fusion control of FF_OPT_FUSED_EPILOGUES (which sets
  * 0 or 7): bit 0 out-proj + residual + LN1, bit 1 FFN1 + activation + requant
  * (int8 layers), bit 2 FFN2 + residual + LN2.  Value 0..7; default 2 (the
  * FFN1 fusion is bit-identical to the separate kernels and measured faster;
  * the LN fusions change the LN summation order and were slower alone). */
 #define FF_OPT_FUSED_MASK 8
-/* FF_OPT_PDL_RR (process-wide, may be set with m = NULL): 1 = the LN-mode
- * row-reduction GEMMs (FF_OPT_FUSED_MASK bits 0 / 2) also launch with PDL;
- * default 0 (with PDL they slowed the step by 5-10%). */
+/* FF_OPT_PDL_RR (per model): 1 = the LN-mode row-reduction GEMMs
+ * (FF_OPT_FUSED_MASK bits 0 / 2) also launch with PDL; default 0 (with PDL
+ * they slowed the step by 5-10%). */
 #define FF_OPT_PDL_RR 9
-/* FF_OPT_GEMM_BALANCE (process-wide, may be set with m = NULL): 1 = CTA-pair
- * GEMMs (BN = 256) split a last wave that fills at most half of the pairs
- * into half-width tiles; 0 = default (no end-to-end gain measured).  Results
- * are identical. */
-#define FF_OPT_GEMM_BALANCE 10
-/* FF_OPT_PDL_KINDS (process-wide, may be set with m = NULL): bitmask over
- * ff_kernel_kind of the forward launches that use PDL (default all; only
- * while FF_OPT_PDL = 1). */
-#define FF_OPT_PDL_KINDS 11
-/* FF_OPT_ATTN_SPLIT (process-wide, may be set with m = NULL): 1 = the
- * tcgen05 attention may run as clusters of 2-8 CTAs that split each
- * sequence's heads (row amax of the fused int8 requant exchanged through
- * DSMEM) when that lowers the heads on the busiest CTA; 0 = default, one CTA
- * per sequence (splits measured slower on C3).  Results are identical. */
-#define FF_OPT_ATTN_SPLIT 12
-/* Set `option` to `value` on model m (invalidates its captured graphs).  The
- * process-wide options FF_OPT_PDL, FF_OPT_GEMM_MC, FF_OPT_PDL_RR,
- * FF_OPT_GEMM_BALANCE, FF_OPT_PDL_KINDS and FF_OPT_ATTN_SPLIT may be set with
- * m = NULL.
- * FF_E_INVALID for an unknown option / bad value / NULL m otherwise. */
+/* Set `option` to `value` on model m (invalidates its captured graphs).  Every
+ * option is per model: the library holds no process-wide mutable state on the
+ * launch path, so models may be driven from different host threads (one
+ * thread at a time per model).  Option ids 7, 10, 11 and 12 (round-1
+ * experiments measured slower and removed) are rejected.
+ * FF_E_INVALID for an unknown option / bad value / NULL m. */
 FF_API ff_status ff_set_option(ff_model *m, int32_t option, int64_t value);
+/* Read the current value of `option` on model m into *value (host pointer).
+ * FF_E_INVALID for an unknown option / NULL m / NULL value. */
+FF_API ff_status ff_get_option(const ff_model *m, int32_t option, int64_t *value);
 
 FF_API void ff_model_destroy(ff_model *m);
 

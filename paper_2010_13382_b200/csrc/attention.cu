@@ -20,6 +20,7 @@
 // P.V pass (exact normalized form, no flash-style output rescaling).
 #include "ff_kernels.h"
 #include "ptx.cuh"
+#include "quant.cuh"
 
 namespace ff {
 
@@ -241,15 +242,15 @@ __global__ void __launch_bounds__(256, 1) attention_kernel(const __half* __restr
           l1 = quad_sum(l1);
         }
         const float i0 = __frcp_rn(l0), i1 = __frcp_rn(l1);
-        // normalize in fp32, round P to fp16 (R9), then P.V on the tensor cores
+        // normalize in fp32 (IEEE e / l), round P to fp16 (R9), then P.V on the tensor cores
 #pragma unroll
         for (int t = 0; t < NT / 2; ++t) {
           if (kb + t * 16 < S16) {
             uint32_t pa[4];
-            pa[0] = pack_half2(s[2 * t][0] * i0, s[2 * t][1] * i0);
-            pa[1] = pack_half2(s[2 * t][2] * i1, s[2 * t][3] * i1);
-            pa[2] = pack_half2(s[2 * t + 1][0] * i0, s[2 * t + 1][1] * i0);
-            pa[3] = pack_half2(s[2 * t + 1][2] * i1, s[2 * t + 1][3] * i1);
+            pa[0] = pack_half2(div_cr(s[2 * t][0], l0, i0), div_cr(s[2 * t][1], l0, i0));
+            pa[1] = pack_half2(div_cr(s[2 * t][2], l1, i1), div_cr(s[2 * t][3], l1, i1));
+            pa[2] = pack_half2(div_cr(s[2 * t + 1][0], l0, i0), div_cr(s[2 * t + 1][1], l0, i0));
+            pa[3] = pack_half2(div_cr(s[2 * t + 1][2], l1, i1), div_cr(s[2 * t + 1][3], l1, i1));
             const __half* vrow = sV + (kb + t * 16 + (lane & 15)) * LDS;
 #pragma unroll
             for (int dn = 0; dn < DP / 8; ++dn) {

@@ -50,8 +50,7 @@ struct SmemTC {
   static constexpr int P = kKVStages * SLOT;                 // P[2]: 2 k-blocks of 64 keys, 128B-swizzled
   static constexpr int MASK = P + 2 * 2 * kTileBytes;        // kKeys floats
   static constexpr int RED = MASK + kKeys * 4;               // [3][2][128] floats: max, sum, amax
-  static constexpr int XAM = RED + 3 * 2 * kQ * 4;              // [2][8][128] floats: cluster row amax
-  static constexpr int BAR = XAM + 2 * 8 * kQ * 4;
+  static constexpr int BAR = RED + 3 * 2 * kQ * 4;
   static constexpr int TOTAL = BAR + 256 + 1024;             // barriers + alignment slack
   static_assert(TOTAL <= 227 * 1024, "smem budget");
 };
@@ -86,27 +85,18 @@ __device__ __forceinline__ void softmax_sync() { asm volatile("bar.sync 1, 256;"
 
 // Walk of the heads one CTA processes: items blockIdx.x, +gridDim.x, ...;
 // each item = (sequence b, heads [h0, h0 + nh)).
-// Cluster mode (hcount > 0): items are sequences and this CTA takes heads
-// [hbase, hbase + hcount) of each (the cluster's CTAs split the heads).
 struct HeadIter {
   int item, hl, b, h0, nh;
-  int n_items, n_groups, A, stride, hbase, hcount;
-  __device__ HeadIter(int first, int n_items_, int n_groups_, int A_, int stride_, int hbase_ = 0, int hcount_ = 0)
-      : item(first), hl(0), n_items(n_items_), n_groups(n_groups_), A(A_), stride(stride_), hbase(hbase_),
-        hcount(hcount_) {
+  int n_items, n_groups, A, stride;
+  __device__ HeadIter(int first, int n_items_, int n_groups_, int A_, int stride_)
+      : item(first), hl(0), n_items(n_items_), n_groups(n_groups_), A(A_), stride(stride_) {
     set();
   }
   __device__ void set() {
     if (item < n_items) {
-      if (hcount > 0) {
-        b = item;
-        h0 = hbase;
-        nh = hcount;
-      } else {
-        b = item / n_groups;
-        h0 = (item - b * n_groups) * kMaxHeads;
-        nh = min(A, h0 + kMaxHeads) - h0;
-      }
+      b = item / n_groups;
+      h0 = (item - b * n_groups) * kMaxHeads;
+      nh = min(A, h0 + kMaxHeads) - h0;
     }
   }
   __device__ bool valid() const { return item < n_items; }
@@ -130,7 +120,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const int32_t* __restrict__ mask, int B, int S,
                         int A, float scale, __half* __restrict__ ctx, int ldc, int8_t* __restrict__ ctxq, int ldq,
                         float* __restrict__ ctxs, const uint8_t* __restrict__ qkv_rows, int row_bytes,
-                        unsigned long long* __restrict__ trace, int cn) {
+                        unsigned long long* __restrict__ trace) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SmemTC::BAR);
@@ -141,21 +131,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   uint64_t* p_full = bar + 8;     // [2] softmax (P written) -> MMA2
   uint64_t* o_full = bar + 10;    // [2] MMA2 -> epilogue
   uint64_t* o_empty = bar + 12;   // [2] epilogue (O read) -> MMA2
-  uint64_t* xbar = bar + 14;      // [2] cluster row-amax exchange (cn > 1)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
-  float* sXam = reinterpret_cast<float*>(smem + SmemTC::XAM);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
   float* sMask = reinterpret_cast<float*>(smem + SmemTC::MASK);
   float* sRed = reinterpret_cast<float*>(smem + SmemTC::RED);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int D = A * kD;
-  // cn > 1: a cluster of cn CTAs per sequence, CTA `crank` taking A / cn heads
-  const int crank = cn > 1 ? (int)cluster_ctarank() : 0;
-  const int hpc = cn > 1 ? A / cn : 0;
-  const int n_groups = cn > 1 ? 1 : (A + kMaxHeads - 1) / kMaxHeads;
+  const int n_groups = (A + kMaxHeads - 1) / kMaxHeads;
   const int n_items = B * n_groups;
-  const int it_first = cn > 1 ? (int)blockIdx.x / cn : (int)blockIdx.x;
-  const int it_stride = cn > 1 ? (int)gridDim.x / cn : (int)gridDim.x;
+  const int it_first = (int)blockIdx.x;
+  const int it_stride = (int)gridDim.x;
   constexpr int kSoftmaxThreads = 32 * kSoftmaxWarps;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmQKV);
@@ -169,7 +154,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       mbar_init(p_full + i, kSoftmaxThreads);
       mbar_init(o_full + i, 1);
       mbar_init(o_empty + i, kSoftmaxThreads);
-      mbar_init(xbar + i, 1);
     }
     fence_barrier_init();
   }
@@ -179,7 +163,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (cn > 1) cluster_sync();  // peers' exchange barriers exist before any remote store
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   griddep_wait();  // QKV / mask come from the previous kernel
@@ -194,7 +177,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       (void)qkv_rows;
       (void)row_bytes;
       uint32_t n = 0;
-      for (HeadIter it(it_first, n_items, n_groups, A, it_stride, crank * hpc, hpc); it.valid(); it.next(), ++n) {
+      for (HeadIter it(it_first, n_items, n_groups, A, it_stride); it.valid(); it.next(), ++n) {
         const int slot = n % kKVStages;
         const int h = it.h0 + it.hl;
         uint8_t* base = smem + slot * SmemTC::SLOT;
@@ -231,7 +214,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         mma_commit(kv_empty + slot);  // Q/K/V of head m free once these MMAs complete
       };
       uint32_t n = 0;
-      for (HeadIter it(it_first, n_items, n_groups, A, it_stride, crank * hpc, hpc); it.valid(); it.next(), ++n) {
+      for (HeadIter it(it_first, n_items, n_groups, A, it_stride); it.valid(); it.next(), ++n) {
         const int slot = n % kKVStages;
         uint8_t* base = smem + slot * SmemTC::SLOT;
         mbar_wait(kv_full + slot, (n / kKVStages) & 1);
@@ -256,7 +239,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     float* redMax = sRed;
     float* redSum = sRed + 2 * kQ;
     float* redAmax = sRed + 4 * kQ;
-    const float sl2 = scale * 1.4426950408889634f;
     const bool fuse_q = ctxq != nullptr;
     // the two warps sharing TMEM lane quadrant q (same rows, other key half)
     const int pair_bar = 2 + q;
@@ -272,22 +254,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     bool qpend = false;
     int qb = 0, qhbase = 0;
     float qsc = 1.0f, qrs = 1.0f;
-    // cn > 1: the row amax is the max over the cluster's CTAs (each holds
-    // A / cn heads of the row): every CTA st.async's its per-row amax into
-    // slot [buffer][crank][row] of each peer, counted on the peer's xbar[buffer];
-    // resolved lazily, right before the first flush of the pending item
-    bool qneed = false;
-    int xs = 0, qx = 0;  // exchange counter, exchange of the pending item
-    auto resolve = [&]() {
-      const int xb = qx & 1;
-      mbar_wait(xbar + xb, (uint32_t)(qx >> 1) & 1u);
-      float am = 0.0f;
-      for (int c = 0; c < cn; ++c) am = fmaxf(am, sXam[(xb * 8 + c) * kQ + r]);
-      qsc = q8_scale(am);
-      qrs = __frcp_rn(qsc);
-      if (crank == 0 && half == 0 && r < S) ctxs[(size_t)qb * S + r] = qsc;
-      qneed = false;
-    };
     auto flush_head = [&](int j) {  // quantize + store parked head j of the pending item
       uint32_t v[16];
       tmem_ld16(trow + kTmemCtx + j * 32 + half * 16, v);
@@ -332,7 +298,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         for (int c = 0; c < 4; ++c) dst[c] = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
       }
       if (!fuse_q) return;
-      if (qneed) resolve();
       if (qpend) flush_head(hl);  // frees parking slot hl (the load completed above)
       tmem_st16(trow + kTmemCtx + hl * 32 + half * 16, pk);
       if (!last) return;
@@ -348,21 +313,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       qhbase = h - hl;
       qpend = true;
       (void)nh;
-      if (cn > 1) {
-        const int xb = xs & 1;
-        if (threadIdx.x == 64) mbar_expect_tx(xbar + xb, (uint32_t)(cn * kQ * 4));
-        if (half == 0) {
-          const uint32_t slot = smem_u32(sXam + (xb * 8 + crank) * kQ + r);
-          const uint32_t xbr = smem_u32(xbar + xb);
-          for (int c = 0; c < cn; ++c) st_async_f32(mapa_shared(slot, (uint32_t)c), am, mapa_shared(xbr, (uint32_t)c));
-        }
-        qx = xs++;
-        qneed = true;
-      } else {
-        qsc = q8_scale(am);
-        qrs = __frcp_rn(qsc);
-        if (half == 0 && r < S) ctxs[grow] = qsc;
-      }
+      qsc = q8_scale(am);
+      qrs = __frcp_rn(qsc);
+      if (half == 0 && r < S) ctxs[grow] = qsc;
       if (threadIdx.x == 64) trace_ev(trace, m, 7);
     };
 
@@ -376,7 +329,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       return __ldg(mask + (size_t)(item / n_groups) * S + tid);
     };
     int mval = mask_of(it_first);
-    for (HeadIter it(it_first, n_items, n_groups, A, it_stride, crank * hpc, hpc); it.valid(); it.next(), ++n) {
+    for (HeadIter it(it_first, n_items, n_groups, A, it_stride); it.valid(); it.next(), ++n) {
       if (it.hl == 0) {
         // every softmax thread finished reading the previous item's mask
         // before this barrier
@@ -394,9 +347,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(s_empty);
-      // masked raw scores (mask bias 0 / -inf), row max in raw units, then
-      // p = exp2(log2(e)/sqrt(d) * (s - max)) as one FFMA per element; packed
-      // fp32 pairs throughout
+      // s = RN(raw * fp32(1/sqrt d)) (+ mask bias 0 / -inf in the same FFMA),
+      // the row max, x = s - max and e = exp2(x * log2 e): the oracle's
+      // rounding points (R9, R10; the exp itself is ex2.approx); packed fp32
+      // pairs throughout
+      const float2 cd2 = make_float2(scale, scale);
       float2 s2[32];
       float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
       const float4* mk4 = reinterpret_cast<const float4*>(sMask) + half * 16;
@@ -404,8 +359,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       for (int j = 0; j < 64; j += 4) {
         const float4 mk = mk4[j >> 2];
         const uint32_t* rw = &raw[j >> 5][j & 31];
-        s2[j / 2] = add2(make_float2(__uint_as_float(rw[0]), __uint_as_float(rw[1])), make_float2(mk.x, mk.y));
-        s2[j / 2 + 1] = add2(make_float2(__uint_as_float(rw[2]), __uint_as_float(rw[3])), make_float2(mk.z, mk.w));
+        s2[j / 2] = fma2(make_float2(__uint_as_float(rw[0]), __uint_as_float(rw[1])), cd2, make_float2(mk.x, mk.y));
+        s2[j / 2 + 1] =
+            fma2(make_float2(__uint_as_float(rw[2]), __uint_as_float(rw[3])), cd2, make_float2(mk.z, mk.w));
         m4[0] = fmaxf(m4[0], s2[j / 2].x);
         m4[1] = fmaxf(m4[1], s2[j / 2].y);
         m4[2] = fmaxf(m4[2], s2[j / 2 + 1].x);
@@ -415,12 +371,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       redMax[half * kQ + r] = mx;
       pair_sync();
       mx = fmaxf(mx, redMax[(half ^ 1) * kQ + r]);
-      const float nmx = -__fmul_rn(mx, sl2);
-      const float2 sl2v = make_float2(sl2, sl2), nmxv = make_float2(nmx, nmx);
+      const float2 l2e = make_float2(1.4426950408889634f, 1.4426950408889634f), mxv = make_float2(mx, mx);
       float2 l2a = make_float2(0.0f, 0.0f), l2b = make_float2(0.0f, 0.0f);
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const float2 e = fma2(s2[j], sl2v, nmxv);
+        const float2 e = mul2(sub2(s2[j], mxv), l2e);
         s2[j] = make_float2(ex2f(e.x), ex2f(e.y));
         if (j & 1) l2b = add2(l2b, s2[j]); else l2a = add2(l2a, s2[j]);
       }
@@ -430,7 +385,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       pair_sync();
       l = redSum[r] + redSum[kQ + r];  // fixed order in both halves
       const float inv = __frcp_rn(l);
-      const float2 inv2 = make_float2(inv, inv);
+      const float2 inv2 = make_float2(inv, inv), lv2 = make_float2(l, l);
       // P16 = R16(p) into k-block `half` of the K-major 128B-swizzled tile
       // P[n&1]: 16B chunk c of row r at (c ^ (r & 7)).  P[n&1] was last read
       // by O(n-2), complete since epilogue(n-2) passed o_full.
@@ -440,7 +395,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         uint32_t w[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const float2 pn = mul2(s2[c * 4 + i], inv2);
+          const float2 pn = div2_cr(s2[c * 4 + i], lv2, inv2);  // IEEE e / l (R9)
           w[i] = pack_half2(pn.x, pn.y);
         }
         *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
@@ -457,13 +412,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       plast = it.hl == it.nh - 1;
     }
     if (pend) epilogue(n - 1, pb, ph_, phl, plast, pnh);
-    if (qneed) resolve();
     if (qpend)
       for (int j = 0; j < pnh; ++j) flush_head(j);
   }
   tc_fence_before();
   __syncthreads();
-  if (cn > 1) cluster_sync();  // no CTA leaves while a peer may still store into it
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -489,70 +442,15 @@ cudaError_t prepare_attention_tc_kernel() {
   return cudaFuncSetAttribute(attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemTC::TOTAL);
 }
 
-// Co-resident clusters of cn attention CTAs (cached).
-static int attn_max_clusters(int cn) {
-  static int cache[9] = {0};
-  if (cn <= 1) return kNumSMs;
-  if (cache[cn] == 0) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(cn * (kNumSMs / cn));
-    cfg.blockDim = dim3(kThreadsTC);
-    cfg.dynamicSmemBytes = SmemTC::TOTAL;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = cn;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, attention_tc_kernel, &cfg) != cudaSuccess || n < 1) {
-      cudaGetLastError();
-      n = 1;
-    }
-    cache[cn] = n;
-  }
-  return cache[cn];
-}
-
-// FF_OPT_ATTN_SPLIT: let clusters split a sequence's heads when that balances
-// better.  Off by default: on C3 (B 256, A 8) forced splits measured 47.6 /
-// 49.6 / 59.8 us per launch for clusters of 2 / 4 / 8 vs 43.4 us unsplit (more
-// item transitions and exchanges; only 33 four-CTA clusters fit).
-int g_attn_split = 0;
-
 cudaError_t launch_attention_tc(const AttnTCPlan& plan, const int32_t* mask, int B, int S, int A, __half* ctx,
                                 int ldctx, int8_t* ctxq, int ldq, float* ctxs, cudaStream_t s,
                                 unsigned long long* trace) {
   if (ctxq != nullptr && !attention_tc_fuses_quant(A)) return cudaErrorInvalidValue;
   const float scale = (float)(1.0 / sqrt((double)kD));
-  // heads per CTA on the busiest CTA: cn = 1 -> ceil(items / 148) * heads per item;
-  // cn > 1 (A <= 8, cn | A) -> ceil(B / clusters) * A / cn; the smallest wins
-  int best_cn = 1;
   const int n_items = B * ((A + kMaxHeads - 1) / kMaxHeads);
-  long long best = (long long)((n_items + kNumSMs - 1) / kNumSMs) * (A < kMaxHeads ? A : kMaxHeads);
-  if (g_attn_split && A <= kMaxHeads && trace == nullptr) {
-    for (int cn = 2; cn <= 8; cn *= 2) {
-      if (A % cn != 0) continue;
-      const int ncl = attn_max_clusters(cn);
-      const long long cost = (long long)((B + ncl - 1) / ncl) * (A / cn);
-      if (cost < best) {
-        best = cost;
-        best_cn = cn;
-      }
-    }
-  }
-  if (best_cn > 1) {
-    const int ncl = attn_max_clusters(best_cn);
-    const int grid = best_cn * (B < ncl ? B : ncl);
-    launch_ex(attention_tc_kernel, dim3(grid), dim3(kThreadsTC), SmemTC::TOTAL, s, best_cn, plan.map, mask, B, S,
-              A, scale, ctx, ldctx, ctxq, ldq, ctxs, static_cast<const uint8_t*>(plan.qkv), plan.ldqkv * 2, trace,
-              best_cn);
-  } else {
-    const int grid = n_items < kNumSMs ? n_items : kNumSMs;
-    launch_ex(attention_tc_kernel, dim3(grid), dim3(kThreadsTC), SmemTC::TOTAL, s, 0, plan.map, mask, B, S, A,
-              scale, ctx, ldctx, ctxq, ldq, ctxs, static_cast<const uint8_t*>(plan.qkv), plan.ldqkv * 2, trace, 1);
-  }
+  const int grid = n_items < kNumSMs ? n_items : kNumSMs;
+  launch_ex(attention_tc_kernel, dim3(grid), dim3(kThreadsTC), SmemTC::TOTAL, s, 0, plan.map, mask, B, S, A, scale,
+            ctx, ldctx, ctxq, ldq, ctxs, static_cast<const uint8_t*>(plan.qkv), plan.ldqkv * 2, trace);
   return cudaGetLastError();
 }
 

@@ -13,12 +13,7 @@
 #include "ff_kernels.h"
 
 namespace ff {
-bool g_pdl = true;  // FF_OPT_PDL: programmatic dependent launch between forward kernels
-bool g_pdl_rr = false;  // FF_OPT_PDL_RR: PDL on the LN-mode row-reduction GEMMs (measured slower)
-int g_cur_kind = 0;              // kernel kind of the launch in progress (FF_LAUNCH)
-unsigned g_pdl_kinds = 0xFFFFFFFFu;  // FF_OPT_PDL_KINDS: kinds (bit = ff_kernel_kind) launched with PDL
-int g_gemm_balance = 0;  // FF_OPT_GEMM_BALANCE: split the last partial wave of pair tiles (measured: no gain)
-int g_gemm_mc = 0;  // FF_OPT_GEMM_MC: CTA-pair GEMMs in clusters of two pairs sharing W by multicast
+thread_local LaunchPolicy tl_launch;  // set per forward by LaunchScope (ff_kernels.h)
 }
 
 namespace {
@@ -106,8 +101,17 @@ struct ff_model {
   int fused = 2;  // FF_OPT_FUSED_EPILOGUES / _MASK: cluster row-reduction GEMM epilogues,
                  // bit 0 out-proj + LN1, bit 1 FFN1 + requant (default), bit 2 FFN2 + LN2
   int act_quant = 0;    // FF_OPT_ACT_QUANT: 0 per-row s8, 1 per-tensor u8 + zero point
+  ff::LaunchPolicy launch{true, false};  // FF_OPT_PDL / FF_OPT_PDL_RR of this model's forwards
   ff::AttnTCPlan tm_qkv;  // QKV buffer map for the tcgen05 attention
-  std::map<std::tuple<int, int, const void*, const void*, const void*>, cudaGraphExec_t> graphs;
+  // CUDA-graph cache of ff_encode, keyed by (batch, seq, ids, mask, logits);
+  // bounded: the least recently used graph is destroyed beyond kMaxGraphs
+  struct CachedGraph {
+    cudaGraphExec_t exec;
+    uint64_t last_use;
+  };
+  static constexpr size_t kMaxGraphs = 64;
+  std::map<std::tuple<int, int, const void*, const void*, const void*>, CachedGraph> graphs;
+  uint64_t graph_clock = 0;
 
   template <typename T>
   T* w(size_t off) const { return reinterpret_cast<T*>(dW + off); }
@@ -116,6 +120,11 @@ struct ff_model {
 };
 
 namespace {
+
+void drop_graphs(ff_model* m) {
+  for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second.exec);
+  m->graphs.clear();
+}
 
 struct DeviceGuard {
   int prev = -1;
@@ -305,7 +314,6 @@ struct Prof {
 
 #define FF_LAUNCH(kind_, x, what)                   \
   do {                                              \
-    ff::g_cur_kind = (kind_);                       \
     if (prof) {                                     \
       prof->kind.push_back(kind_);                  \
       prof->mark(s);                                \
@@ -336,6 +344,7 @@ static int g_debug_trace_which = 0;
 // The launch sequence of one encoder forward.
 ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int B, int S, float* logits,
                       cudaStream_t s, int trace_layer, void* const* d_dump, Prof* prof = nullptr) {
+  const ff::LaunchScope launch_scope(m->launch);  // this model's PDL policy for the launches below
   const ff_config& c = m->cfg;
   const int H = c.hidden, M = B * S;
   __half* X16 = m->ws<__half>(m->ws_x16);
@@ -774,6 +783,14 @@ ff_status ff_encode(ff_model* m, const int32_t* d_token_ids, const int32_t* d_ma
   auto key = std::make_tuple((int)batch, (int)seq, (const void*)d_token_ids, (const void*)d_mask, (const void*)d_logits);
   auto it = m->graphs.find(key);
   if (it == m->graphs.end()) {
+    if (m->graphs.size() >= ff_model::kMaxGraphs) {  // evict the least recently used graph
+      auto lru = m->graphs.begin();
+      for (auto g = m->graphs.begin(); g != m->graphs.end(); ++g)
+        if (g->second.last_use < lru->second.last_use) lru = g;
+      FF_CK(cudaStreamSynchronize(s));  // (rare) its last launch may still be in flight
+      cudaGraphExecDestroy(lru->second.exec);
+      m->graphs.erase(lru);
+    }
     cudaGraph_t graph;
     FF_CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     st = run_forward(m, d_token_ids, d_mask, batch, seq, d_logits, s, -1, nullptr);
@@ -784,9 +801,10 @@ ff_status ff_encode(ff_model* m, const int32_t* d_token_ids, const int32_t* d_ma
     e = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return fail(FF_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
-    it = m->graphs.emplace(key, exec).first;
+    it = m->graphs.emplace(key, ff_model::CachedGraph{exec, 0}).first;
   }
-  FF_CK(cudaGraphLaunch(it->second, s));
+  it->second.last_use = ++m->graph_clock;
+  FF_CK(cudaGraphLaunch(it->second.exec, s));
   return FF_OK;
 }
 
@@ -872,101 +890,64 @@ ff_status ff_check(ff_model* m, void* stream) {
 }
 
 ff_status ff_set_option(ff_model* m, int32_t option, int64_t value) {
-  if (!m && option == FF_OPT_GEMM_MC) {  // process-wide options may be set without a model
-    ff::g_gemm_mc = value != 0 ? 1 : 0;
-    return FF_OK;
-  }
-  if (option == FF_OPT_ATTN_SPLIT) {  // process-wide
-    ff::g_attn_split = value != 0 ? 1 : 0;
-    if (m) {
-      for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
-      m->graphs.clear();
-    }
-    return FF_OK;
-  }
-  if (option == FF_OPT_PDL_KINDS) {  // process-wide
-    ff::g_pdl_kinds = (unsigned)value;
-    if (m) {
-      for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
-      m->graphs.clear();
-    }
-    return FF_OK;
-  }
-  if (option == FF_OPT_GEMM_BALANCE) {  // process-wide
-    ff::g_gemm_balance = value != 0 ? 1 : 0;
-    if (m) {
-      for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
-      m->graphs.clear();
-    }
-    return FF_OK;
-  }
-  if (option == FF_OPT_PDL_RR) {  // process-wide
-    ff::g_pdl_rr = value != 0;
-    if (m) {
-      for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
-      m->graphs.clear();
-    }
-    return FF_OK;
-  }
-  if (!m && option == FF_OPT_PDL) {
-    ff::g_pdl = value != 0;
-    return FF_OK;
-  }
   if (!m) return fail(FF_E_INVALID, "null model");
   if (option == FF_OPT_GRAPHS) {
     m->use_graphs = value != 0;
     return FF_OK;
   }
-  if (option == FF_OPT_PDL) {  // process-wide
-    ff::g_pdl = value != 0;
-    for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
-    m->graphs.clear();
-    return FF_OK;
-  }
-  if (option == FF_OPT_GEMM_MC) {  // process-wide
-    ff::g_gemm_mc = value != 0 ? 1 : 0;
-    for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
-    m->graphs.clear();
+  if (option == FF_OPT_PDL || option == FF_OPT_PDL_RR) {
+    (option == FF_OPT_PDL ? m->launch.pdl : m->launch.pdl_rr) = value != 0;
+    drop_graphs(m);  // captured launch attributes change
     return FF_OK;
   }
   if (option == FF_OPT_ACT_QUANT) {
     if (value != 0 && value != 1) return fail(FF_E_INVALID, "FF_OPT_ACT_QUANT must be 0 or 1");
     m->act_quant = (int)value;
-    for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
-    m->graphs.clear();
+    drop_graphs(m);
     return FF_OK;
   }
   if (option == FF_OPT_FUSED_EPILOGUES) {
     m->fused = value != 0 ? 7 : 0;
-    for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
-    m->graphs.clear();
+    drop_graphs(m);
     return FF_OK;
   }
   if (option == FF_OPT_FUSED_MASK) {
     if (value < 0 || value > 7) return fail(FF_E_INVALID, "FF_OPT_FUSED_MASK must be in 0..7");
     m->fused = (int)value;
-    for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
-    m->graphs.clear();
+    drop_graphs(m);
     return FF_OK;
   }
   if (option == FF_OPT_ATTN_TC) {
     m->attn_tc = value != 0;
-    for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
-    m->graphs.clear();
+    drop_graphs(m);
     return FF_OK;
   }
   if (option == FF_OPT_CTA_PAIRS) {
     m->pair_mode = value != 0 ? -1 : 0;
-    for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);  // captured launch configs change
-    m->graphs.clear();
+    drop_graphs(m);  // captured launch configs change
     return FF_OK;
   }
   return fail(FF_E_INVALID, "unknown option");
 }
 
+ff_status ff_get_option(const ff_model* m, int32_t option, int64_t* value) {
+  if (!m || !value) return fail(FF_E_INVALID, "null argument");
+  switch (option) {
+    case FF_OPT_GRAPHS: *value = m->use_graphs ? 1 : 0; return FF_OK;
+    case FF_OPT_CTA_PAIRS: *value = m->pair_mode == 0 ? 0 : 1; return FF_OK;
+    case FF_OPT_ATTN_TC: *value = m->attn_tc ? 1 : 0; return FF_OK;
+    case FF_OPT_FUSED_EPILOGUES: *value = m->fused == 7 ? 1 : 0; return FF_OK;
+    case FF_OPT_PDL: *value = m->launch.pdl ? 1 : 0; return FF_OK;
+    case FF_OPT_ACT_QUANT: *value = m->act_quant; return FF_OK;
+    case FF_OPT_FUSED_MASK: *value = m->fused; return FF_OK;
+    case FF_OPT_PDL_RR: *value = m->launch.pdl_rr ? 1 : 0; return FF_OK;
+    default: return fail(FF_E_INVALID, "unknown option");
+  }
+}
+
 void ff_model_destroy(ff_model* m) {
   if (!m) return;
-  for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
+  drop_graphs(m);
   if (m->io_stream) {
     cudaStreamSynchronize(m->io_stream);
     cudaStreamDestroy(m->io_stream);

@@ -10,20 +10,31 @@ namespace ff {
 
 constexpr int kNumSMs = 148;
 
-// Launch with the programmatic-dependent-launch attribute (when enabled) and
-// an optional 1-D cluster (cluster = 0: no cluster attribute).  All
-// forward-pass kernels go through this.
-extern bool g_pdl;
-extern int g_cur_kind;         // kind (ff_kernel_kind) of the forward launch in progress
-extern unsigned g_pdl_kinds;   // FF_OPT_PDL_KINDS: bit k = kind k launches with PDL
-extern bool g_pdl_rr;  // FF_OPT_PDL_RR: PDL attribute on the row-reduction GEMM launches too
+// Launch policy of the forward being enqueued: the model's FF_OPT_PDL /
+// FF_OPT_PDL_RR settings, installed for the duration of one run_forward on the
+// calling thread (LaunchScope).  Thread-local, so models driven from several
+// host threads never see each other's settings; outside a forward (weight
+// packing) launches carry no PDL attribute.
+struct LaunchPolicy {
+  bool pdl = false;     // programmatic dependent launch between forward kernels
+  bool pdl_rr = false;  // ... also on the LN-mode row-reduction GEMMs (measured slower)
+};
+extern thread_local LaunchPolicy tl_launch;
+struct LaunchScope {
+  LaunchPolicy saved;
+  explicit LaunchScope(const LaunchPolicy& p) : saved(tl_launch) { tl_launch = p; }
+  ~LaunchScope() { tl_launch = saved; }
+};
+// Launch with the programmatic-dependent-launch attribute (when the policy
+// enables it) and an optional 1-D cluster (cluster = 0: no cluster
+// attribute).  All forward-pass kernels go through this.
 template <typename... KArgs, typename... Args>
 cudaError_t launch_ex_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                           int cluster, Args... args);
 template <typename... KArgs, typename... Args>
 cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int cluster,
                       Args... args) {
-  return launch_ex_pdl(g_pdl && ((g_pdl_kinds >> g_cur_kind) & 1u), kern, grid, block, smem, s, cluster, args...);
+  return launch_ex_pdl(tl_launch.pdl, kern, grid, block, smem, s, cluster, args...);
 }
 template <typename... KArgs, typename... Args>
 cudaError_t launch_ex_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
@@ -72,12 +83,11 @@ struct GemmParams {
   // colsum[n] = sum_k wq[n][k]
   const float* tensor_qp;
   const int* colsum;
-  int balance;     // split the last partial wave of pair tiles into half-width tiles (g_gemm_balance)
   int dbg_noload;  // debug MMA-rate probe: skip the operand loads (ff_debug_gemm bit 6; 0 in production)
 };
 
 struct GemmPlan {
-  CUtensorMap tmA, tmB, tmB2, tmB4, tmC;  // A, W (BN / BN/2 / BN/4-row boxes, 128B swizzle); fp16 output (64B swizzle)
+  CUtensorMap tmA, tmB, tmB2, tmC;  // A, W (BN / BN/2-row boxes, 128B swizzle); fp16 output (64B swizzle)
   GemmParams p;
   int bn;       // N tile (128 or 256)
   int i8;       // 1 = kind::i8
@@ -86,11 +96,7 @@ struct GemmPlan {
   bool has_out_map;
   int force_pair;   // -1 auto (pairs when >= 74 pair-tiles), 0 never, 1 always
   bool pair;        // chosen for the current M
-  bool mc;          // pairs run as clusters of two with W multicast (g_gemm_mc)
 };
-extern int g_attn_split;  // FF_OPT_ATTN_SPLIT (attention_tc.cu): clusters may split a sequence's heads
-extern int g_gemm_balance;  // FF_OPT_GEMM_BALANCE: tail balancing of the pair GEMMs
-extern int g_gemm_mc;  // FF_OPT_GEMM_MC: 1 = CTA-pair GEMMs share W k-blocks by TMA multicast
 
 // Encode a 2-D K-major tensor map for a GEMM operand: rows x cols elements of
 // `elem_bytes` (2 fp16 / 1 int8), row pitch in bytes, box = box_rows x 128 B,

@@ -78,29 +78,31 @@ __device__ __forceinline__ constexpr uint32_t make_idesc() {
 }
 
 // GELU(y) = y/2 (1 + erf(y / sqrt 2)) for the FFN1 epilogue, branch-free.
-// With s = |y| (clamped to 4 sqrt 2, where erf rounds to 1 in fp32) and
-// e = erfc(s / sqrt 2) = 2^(-s * P6(s)):  GELU(y) = y/2 * (2 - e) for y >= 0
-// and y/2 * e for y < 0 — no cancellation on the negative side.  P6 is a
-// degree-6 fit of -log2(erfc(s / sqrt 2)) / s weighted for the RELATIVE error
-// of e (<= 3.9e-6; 1/sqrt 2 folded into the coefficients).  Against the exact
-// GELU rounded to fp16, 0.4% of outputs differ, by at most 1 fp16 ulp (DESIGN
-// R2; was 1.6% / 2 ulp with a degree-7 absolute-error erf fit).  Replaces
-// erff, whose divergent branches made the FFN1 epilogue the GEMM's bottleneck.
-constexpr float kG6 = 1.7657696e-06f, kG5 = -6.0254122e-05f, kG4 = 9.2013367e-04f, kG3 = -8.4673585e-03f,
-                kG2 = 5.3876434e-02f, kG1 = 4.5855144e-01f, kG0 = 1.1512122f;
-constexpr float kGeluClamp = 5.6568542f;  // 4 sqrt 2
+// With s = |y| (clamped to 6.5, beyond which GELU(y) rounds to y, resp. to 0
+// in fp16) and e = erfc(s / sqrt 2) = 2^(-s * P11(s)):  GELU(y) = y/2 * (2 - e)
+// for y >= 0 and y/2 * e for y < 0 -- no cancellation on the negative side.
+// P11 is a degree-11 Chebyshev-weighted fit of -log2(erfc(s / sqrt 2)) / s on
+// [0, 6.5] (relative error of e <= 1.2e-8 before the fp32 evaluation).
+// Measured on the GPU (tools/micro/exp_accuracy.cu, 2^28 points): <= 8 fp32
+// ulp on |y| <= 2 and 0.0066% of outputs whose fp16 rounding differs from
+// RN16(RN32(exact GELU)) -- the oracle's rounding point (DESIGN R2) -- against
+// 0.21% for the round-1 degree-6 fit.  Replaces erff, whose divergent
+// branches made the FFN1 epilogue the GEMM's bottleneck.
+// P11 coefficients, highest degree first (Horner)
+#define FF_GELU_P11(X)                                                                                        \
+  X(1.91209187e-10f) X(-8.90500740e-09f) X(1.86934614e-07f) X(-2.33101059e-06f) X(1.90286646e-05f)           \
+  X(-1.03522529e-04f) X(3.35359509e-04f) X(-6.75584961e-05f) X(-6.90312125e-03f) X(5.24297878e-02f)          \
+  X(4.59220439e-01f) X(1.15110457e+00f)
+constexpr float kGeluClamp = 6.5f;
 
 template <int ACT>
 __device__ __forceinline__ float act_fn(float y) {
   if (ACT == ACT_GELU) {
     const float s = fminf(fabsf(y), kGeluClamp);
-    float p = kG6;
-    p = __fmaf_rn(p, s, kG5);
-    p = __fmaf_rn(p, s, kG4);
-    p = __fmaf_rn(p, s, kG3);
-    p = __fmaf_rn(p, s, kG2);
-    p = __fmaf_rn(p, s, kG1);
-    p = __fmaf_rn(p, s, kG0);
+    float p = 0.0f;
+#define FF_H1(c) p = __fmaf_rn(p, s, c);
+    FF_GELU_P11(FF_H1)
+#undef FF_H1
     float e;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-s * p));
     return (0.5f * y) * (y >= 0.0f ? 2.0f - e : e);
@@ -116,13 +118,10 @@ __device__ __forceinline__ float act_fn(float y) {
 // GELU of a pair on packed fp32 (FFMA2 / FMUL2), same arithmetic as act_fn.
 __device__ __forceinline__ float2 gelu2(float2 y) {
   const float2 s = make_float2(fminf(fabsf(y.x), kGeluClamp), fminf(fabsf(y.y), kGeluClamp));
-  float2 p = make_float2(kG6, kG6);
-  p = fma2(p, s, make_float2(kG5, kG5));
-  p = fma2(p, s, make_float2(kG4, kG4));
-  p = fma2(p, s, make_float2(kG3, kG3));
-  p = fma2(p, s, make_float2(kG2, kG2));
-  p = fma2(p, s, make_float2(kG1, kG1));
-  p = fma2(p, s, make_float2(kG0, kG0));
+  float2 p = make_float2(0.0f, 0.0f);
+#define FF_H2(c) p = fma2(p, s, make_float2(c, c));
+  FF_GELU_P11(FF_H2)
+#undef FF_H2
   const float2 a = mul2(s, p);
   float2 e;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(-a.x));
@@ -188,23 +187,13 @@ __device__ __forceinline__ void gemm_trace(unsigned long long* trace, int t, int
 
 // PT: per-tensor u8 activations with a zero point (DESIGN R22; I8 only), a
 // separate instantiation so the per-row kernel's registers are unaffected.
-// MC (PAIR only): clusters of two CTA pairs stacked along M that work on row
-// tiles (2j, 2j+1) of the same column tile in lockstep and share its W
-// k-blocks: CTA r of pair q TMA-loads rows [q BN/4, +BN/4) of its W half and
-// multicasts them into CTA r of both pairs, halving the W bytes each SM pulls
-// from L2 (A stays per pair).  A stage's smem is refilled only when both pair
-// leaders' MMAs have consumed it (empty barriers count two commits).
-// Tail balancing (PAIR, not MC; p.balance): when the last wave of pair tiles
-// would occupy at most half of the pairs, its tiles are split into two
-// half-width tiles (N = BN/2, W boxes of BN/4 rows per CTA from tmBh) spread
-// over twice as many pairs, so the kernel's critical path ends half a tile
-// earlier (the N = 768 GEMMs of C3: 384 tiles on 74 pairs = 5 waves + 14).
-template <int BN, bool I8, bool PAIR, bool PT = false, bool MC = false>
+// (Measured and removed: W multicast across clusters of two CTA pairs, and
+// splitting the last partial wave of pair tiles into half-width tiles; DESIGN
+// section 6.)
+template <int BN, bool I8, bool PAIR, bool PT = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmBh,
-                   GemmParams p) {
-  static_assert(!MC || (PAIR && !PT), "W multicast is a CTA-pair variant");
+                   const __grid_constant__ CUtensorMap tmC, GemmParams p) {
   using Cfg = GemmCfg<BN, PAIR>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int TM = Cfg::TM;
@@ -220,19 +209,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t crank = PAIR ? cluster_ctarank() : 0;
-  const uint32_t rank = crank & 1;                    // 0 = leader of the pair
-  const uint32_t pq = MC ? (crank >> 1) : 0;          // pair index in an MC cluster
-  const uint32_t lead = crank & ~1u;                  // cluster rank of this pair's leader
-  const int unit = MC ? (int)(blockIdx.x >> 2) : PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int nunits = MC ? (int)(gridDim.x >> 2) : PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;  // 0 = leader of the pair
+  const int unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int nunits = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     if (p.out_mode == 1) tma_prefetch(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], MC ? 2 : 1);
+      mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -257,29 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   griddep_wait();  // A operand / scales come from the previous kernel
   griddep_launch();
 
-  // MC: a cluster tile = row tiles (2j, 2j+1) x one column tile; pair pq takes
-  // row tile 2j + pq (past the last row tile when m_tiles is odd: it runs on
-  // zero-filled / unused rows and stores nothing)
-  const int num_full = (MC ? (p.m_tiles + 1) / 2 : p.m_tiles) * p.n_tiles;
-  int split_from = num_full, num_tiles = num_full;
-  if (PAIR && !MC && BN == 256 && p.balance) {
-    const int rem = num_full % nunits;
-    if (rem > 0 && 2 * rem <= nunits) {
-      split_from = num_full - rem;
-      num_tiles = split_from + 2 * rem;
-    }
-  }
-  // virtual tile v -> (linear tile, half): half -1 = full width, 0 / 1 = the
-  // lower / upper BN/2 columns of a split tail tile
-  auto decode = [&](int v, int& t, int& half) {
-    if (v < split_from) {
-      t = v;
-      half = -1;
-    } else {
-      t = split_from + ((v - split_from) >> 1);
-      half = (v - split_from) & 1;
-    }
-  };
+  const int num_tiles = p.m_tiles * p.n_tiles;
   constexpr int KE = I8 ? 128 : 64;  // elements per k-block
 
   if (warp == 0) {
@@ -287,14 +251,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int lt = 0;
-      for (int v = unit; v < num_tiles; v += nunits, ++lt) {
-        int tile, half;
-        decode(v, tile, half);
-        const int ct = tile / p.n_tiles, nt = tile - ct * p.n_tiles;
-        const int mt = MC ? 2 * ct + (int)pq : ct;
+      for (int tile = unit; tile < num_tiles; tile += nunits, ++lt) {
+        const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
         const int arow = mt * TM + (int)rank * BM;
-        const int brow = half < 0 ? nt * BN + (PAIR ? (int)rank * (BN / 2) : 0)
-                                  : nt * BN + half * (BN / 2) + (int)rank * (BN / 4);
+        const int brow = nt * BN + (PAIR ? (int)rank * (BN / 2) : 0);
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (kb == 0) gemm_trace(p.trace, lt, 6);
@@ -302,18 +262,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (rank == 0) mbar_arrive(&full[stage]);
           } else if (PAIR) {
             // the leader's full barrier counts the bytes of both CTAs' loads
-            if (rank == 0)
-              mbar_expect_tx(&full[stage], half < 0 ? 2 * Cfg::STAGE_BYTES : 2 * (Cfg::A_BYTES + Cfg::B_BYTES / 2));
-            const uint32_t bar = mapa_shared(smem_u32(&full[stage]), lead);
+            if (rank == 0) mbar_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+            const uint32_t bar = mapa_shared(smem_u32(&full[stage]), 0);
             tma_load_2d_pair(sA + stage * Cfg::A_BYTES, &tmA, bar, kb * KE, arow, kEvictNormal);
-            if (half >= 0) {  // split tail tile: BN/4 rows of W per CTA
-              tma_load_2d_pair(sB + stage * Cfg::B_BYTES, &tmBh, bar, kb * KE, brow, kEvictLast);
-            } else if (MC) {  // quarter pq of the pair's W rows, into CTA `rank` of both pairs
-              tma_load_2d_pair_mc(sB + stage * Cfg::B_BYTES + pq * (BN / 4) * BK_BYTES, &tmB, bar, kb * KE,
-                                  brow + (int)pq * (BN / 4), (uint16_t)(0x5u << rank), kEvictLast);
-            } else {
-              tma_load_2d_pair(sB + stage * Cfg::B_BYTES, &tmB, bar, kb * KE, brow, kEvictLast);
-            }
+            tma_load_2d_pair(sB + stage * Cfg::B_BYTES, &tmB, bar, kb * KE, brow, kEvictLast);
           } else {
             mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
             tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * KE, arow, kEvictNormal);
@@ -329,15 +281,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       // per-tensor u8 activations (DESIGN R22): a_format u8 (bit 7 clear)
-      constexpr uint32_t idesc_full = make_idesc<I8, TM, BN>() & (PT ? ~(1u << 7) : ~0u);
-      constexpr uint32_t idesc_half = make_idesc<I8, TM, BN / 2>() & (PT ? ~(1u << 7) : ~0u);
+      constexpr uint32_t idesc = make_idesc<I8, TM, BN>() & (PT ? ~(1u << 7) : ~0u);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       int lt = 0;
-      for (int v = unit; v < num_tiles; v += nunits, ++lt) {
-        const uint32_t idesc = v < split_from ? idesc_full : idesc_half;
+      for (int tile = unit; tile < num_tiles; tile += nunits, ++lt) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         gemm_trace(p.trace, lt, 0);
         tc_fence_after();
@@ -359,9 +309,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               else mma_f16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, accum);
             }
           }
-          // frees the smem slot (of both CTAs; MC: of all four, each counting
-          // both pair leaders) when these MMAs finish
-          if (PAIR) mma_commit_pair(&empty[stage], MC ? 0xF : 0x3);
+          // frees the smem slot (of both CTAs) when these MMAs finish
+          if (PAIR) mma_commit_pair(&empty[stage], 0x3);
           else mma_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
@@ -369,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         // accumulator ready for the epilogue warps (of both CTAs)
-        if (PAIR) mma_commit_pair(&tfull[acc], (uint16_t)(0x3u << lead));
+        if (PAIR) mma_commit_pair(&tfull[acc], 0x3);
         else mma_commit(&tfull[acc]);
         gemm_trace(p.trace, lt, 2);
         if (++acc == 2) {
@@ -383,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;                         // TMEM lane quadrant this warp may access
     constexpr int WCOLS = BN / (kEpiWarps / 4);     // columns per warp (64 or 32)
     uint8_t* stage_buf = sEpi + ew * kStageBufs * kStageTile;
-    const uint32_t tempty_leader0 = PAIR ? mapa_shared(smem_u32(&tempty[0]), lead) : 0;
+    const uint32_t tempty_leader0 = PAIR ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     int nbuf = 0;
@@ -391,14 +340,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool tr0 = ew == 0 && lane == 0;
     float* sPar = reinterpret_cast<float*>(smem + Cfg::PAR_OFF);
     const int et = ew * 32 + lane;  // 0 .. 511
-    for (int v = unit; v < num_tiles; v += nunits, ++lt) {
-      int tile, half;
-      decode(v, tile, half);
-      const int ct = tile / p.n_tiles, nt = tile - ct * p.n_tiles;
-      const int mt = MC ? 2 * ct + (int)pq : ct;
-      const int nb = nt * BN + (half > 0 ? BN / 2 : 0);  // first output column of this tile
-      // a split tail tile (BN = 256) spreads its 128 columns over all 16 warps (32 each)
-      const int wcols = half < 0 ? WCOLS : WCOLS / 2;
+    for (int tile = unit; tile < num_tiles; tile += nunits, ++lt) {
+      const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+      const int nb = nt * BN;  // first output column of this tile
+      constexpr int wcols = WCOLS;
       const int c_lo = (ew >> 2) * wcols;  // this warp's column group of the tile
       const int row0 = mt * TM + (int)rank * BM + q * 32;
       const int row = row0 + lane;
@@ -1042,7 +987,6 @@ bool plan_gemm(GemmPlan* g, bool i8, const void* A, int M_rows, int lda, const v
   // W boxes cover BN rows (single CTA) or BN/2 rows (each CTA of a pair): two maps.
   if (!make_operand_map(&g->tmB, W, N, K, eb, (size_t)ldw * eb, g->bn, err)) return false;
   if (!make_operand_map(&g->tmB2, W, N, K, eb, (size_t)ldw * eb, g->bn / 2, err)) return false;
-  if (!make_operand_map(&g->tmB4, W, N, K, eb, (size_t)ldw * eb, g->bn / 4, err)) return false;
   g->p.N = N;
   g->p.K = K;
   g->p.n_tiles = (N + g->bn - 1) / g->bn;
@@ -1067,8 +1011,6 @@ bool plan_gemm_output(GemmPlan* g, void* out, int ldo, const char** err) {
                    32, CU_TENSOR_MAP_SWIZZLE_64B, err);
 }
 
-int gemm_mc_max_clusters(bool i8, int bn);
-
 void plan_gemm_set_m(GemmPlan* g, int M) {
   g->p.M = M;
   // CTA pairs (M = 256 tiles) when there are enough tiles to fill the GPU.
@@ -1077,14 +1019,8 @@ void plan_gemm_set_m(GemmPlan* g, int M) {
   const int tm = g->pair ? 256 : BM;
   g->p.m_tiles = (M + tm - 1) / tm;
   const int tiles = g->p.m_tiles * g->p.n_tiles;
-  g->mc = g->pair && g_gemm_mc != 0;
-  g->p.balance = g_gemm_balance;
   g->p.dbg_noload = 0;
-  if (g->mc) {
-    const int ctiles = ((g->p.m_tiles + 1) / 2) * g->p.n_tiles;
-    const int maxc = gemm_mc_max_clusters(g->i8 != 0, g->bn);
-    g->grid = 4 * (ctiles < maxc ? ctiles : maxc);
-  } else if (g->pair) {
+  if (g->pair) {
     const int pairs = tiles < kNumSMs / 2 ? tiles : kNumSMs / 2;
     g->grid = 2 * pairs;
   } else {
@@ -1092,47 +1028,11 @@ void plan_gemm_set_m(GemmPlan* g, int M) {
   }
 }
 
-template <int BN, bool I8>
-static int gemm_mc_max_clusters_t() {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(kNumSMs);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = GemmCfg<BN, true>::SMEM;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 4;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<BN, I8, true, false, true>, &cfg) != cudaSuccess || n < 1) {
-    cudaGetLastError();
-    return kNumSMs / 4;
-  }
-  return n;
-}
-
-// Co-resident 4-CTA clusters of the MC GEMM (cached per variant).
-int gemm_mc_max_clusters(bool i8, int bn) {
-  static int cache[4] = {0, 0, 0, 0};
-  const int k = (i8 ? 2 : 0) + (bn == 256 ? 1 : 0);
-  if (cache[k] == 0)
-    cache[k] = i8 ? (bn == 256 ? gemm_mc_max_clusters_t<256, true>() : gemm_mc_max_clusters_t<128, true>())
-                  : (bn == 256 ? gemm_mc_max_clusters_t<256, false>() : gemm_mc_max_clusters_t<128, false>());
-  return cache[k];
-}
-
 template <int BN, bool I8, bool PAIR>
 static cudaError_t set_attr() {
   cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, I8, PAIR, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN, PAIR>::SMEM);
   if (e != cudaSuccess) return e;
-  if (PAIR) {
-    e = cudaFuncSetAttribute(gemm_tc_kernel<BN, I8, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             GemmCfg<BN, true>::SMEM);
-    if (e != cudaSuccess) return e;
-  }
   if (!I8) return e;
   return cudaFuncSetAttribute(gemm_tc_kernel<BN, I8, PAIR, I8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               GemmCfg<BN, PAIR>::SMEM);
@@ -1153,14 +1053,11 @@ cudaError_t prepare_gemm_kernels() {
 template <int BN, bool I8, bool PAIR>
 static cudaError_t launch_t(const GemmPlan& g, cudaStream_t s) {
   if (g.grid <= 0) return cudaSuccess;
-  if (PAIR && g.mc && g.p.tensor_qp == nullptr)  // (per-tensor u8 runs the plain pair kernel)
-    return launch_ex(gemm_tc_kernel<BN, I8, true, false, true>, dim3(g.grid), dim3(kThreads),
-                     GemmCfg<BN, true>::SMEM, s, 4, g.tmA, g.tmB4, g.tmC, g.tmB4, g.p);
   if (I8 && g.p.tensor_qp != nullptr)
     return launch_ex(gemm_tc_kernel<BN, I8, PAIR, I8>, dim3(g.grid), dim3(kThreads), GemmCfg<BN, PAIR>::SMEM, s,
-                     PAIR ? 2 : 0, g.tmA, PAIR ? g.tmB2 : g.tmB, g.tmC, g.tmB4, g.p);
+                     PAIR ? 2 : 0, g.tmA, PAIR ? g.tmB2 : g.tmB, g.tmC, g.p);
   return launch_ex(gemm_tc_kernel<BN, I8, PAIR, false>, dim3(g.grid), dim3(kThreads), GemmCfg<BN, PAIR>::SMEM, s,
-                   PAIR ? 2 : 0, g.tmA, PAIR ? g.tmB2 : g.tmB, g.tmC, g.tmB4, g.p);
+                   PAIR ? 2 : 0, g.tmA, PAIR ? g.tmB2 : g.tmB, g.tmC, g.p);
 }
 
 cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t s) {
@@ -1258,7 +1155,7 @@ void plan_rr_set_m(RRPlan* g, int M) {
 template <bool I8, int MODE>
 static cudaError_t launch_rr_t(const RRPlan& g, cudaStream_t s) {
   // LN-mode row-reduction GEMMs launch without PDL unless FF_OPT_PDL_RR (measured)
-  const bool pdl = g_pdl && ((g_pdl_kinds >> g_cur_kind) & 1u) && (MODE != RR_LN || g_pdl_rr);
+  const bool pdl = tl_launch.pdl && (MODE != RR_LN || tl_launch.pdl_rr);
   return launch_ex_pdl(pdl, gemm_rr_kernel<I8, MODE>, dim3(g.grid), dim3(kRRThreads), RRCfg::SMEM, s, g.cn, g.tmA,
                        g.tmB, g.tmC, g.tmR, g.tmQ, g.p);
 }

@@ -210,10 +210,13 @@ __global__ void __launch_bounds__(256, 2) sgemm128_kernel(SG g) {
 
 // Split-K for the narrow linears (N = H = 768 at M = 4096 gives 192 big tiles,
 // 0.65 of a wave at 2 CTAs per SM): the K range is cut into `splits` equal
-// parts computed by one launch (grid z = split, partials to g_sk_ws) and
-// summed in a fixed order by splitk_reduce_kernel (+ bias, + C if accumulating).
-float* g_sk_ws = nullptr;  // scratch of the scorer being run (set by score_batch)
-size_t g_sk_cap = 0;       // floats
+// parts computed by one launch (grid z = split, partials to the scorer's own
+// split-K scratch `sk`) and summed in a fixed order by splitk_reduce_kernel
+// (+ bias, + C if accumulating).
+struct SplitKScratch {
+  float* ws = nullptr;  // the calling scorer's workspace slice (stream-ordered use)
+  size_t cap = 0;       // floats
+};
 
 __global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits, int M, int N,
                                      const float* __restrict__ bias, float* C, long long sCm, int accumulate) {
@@ -228,12 +231,12 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits,
   }
 }
 
-cudaError_t sgemm(const SG& g, int nz, cudaStream_t s) {
+cudaError_t sgemm(const SG& g, int nz, cudaStream_t s, const SplitKScratch& sk = SplitKScratch()) {
   const long long big_tiles = (long long)((g.N + LBN - 1) / LBN) * ((g.M + LBM - 1) / LBM) * nz;
-  if (nz == 1 && g.M >= 256 && g.N >= 256 && big_tiles < 2 * ff::kNumSMs && g_sk_ws != nullptr) {
+  if (nz == 1 && g.M >= 256 && g.N >= 256 && big_tiles < 2 * ff::kNumSMs && sk.ws != nullptr) {
     int splits = 0;
     for (int cand = 4; cand >= 2; --cand)
-      if (g.K % cand == 0 && g.K / cand >= 256 && (size_t)cand * g.M * g.N <= g_sk_cap) {
+      if (g.K % cand == 0 && g.K / cand >= 256 && (size_t)cand * g.M * g.N <= sk.cap) {
         splits = cand;
         break;
       }
@@ -244,14 +247,14 @@ cudaError_t sgemm(const SG& g, int nz, cudaStream_t s) {
       gs.nh = 1;
       gs.sAb = (long long)klen * g.sAk;
       gs.sBb = (long long)klen * g.sBk;
-      gs.C = g_sk_ws;
+      gs.C = sk.ws;
       gs.sCb = (long long)g.M * g.N;
       gs.sCm = g.N;
       gs.bias = nullptr;
       gs.accumulate = 0;
       dim3 grid((g.N + LBN - 1) / LBN, (g.M + LBM - 1) / LBM, splits);
       sgemm128_kernel<<<grid, 256, 0, s>>>(gs);
-      splitk_reduce_kernel<<<4 * ff::kNumSMs, 256, 0, s>>>(g_sk_ws, splits, g.M, g.N, g.bias, g.C, g.sCm,
+      splitk_reduce_kernel<<<4 * ff::kNumSMs, 256, 0, s>>>(sk.ws, splits, g.M, g.N, g.bias, g.C, g.sCm,
                                                             g.accumulate);
       return cudaGetLastError();
     }
@@ -673,8 +676,9 @@ ff_status score_batch(ff_scorer* m, const int* ids, const int* mask, const int* 
   const float scale = 1.0f / sqrtf((float)d);
   const int rt = rows_threads(H);
   const size_t lnsm = (size_t)(H + 32) * 4;
-  g_sk_ws = m->ws(m->skws);  // split-K scratch of this scorer (stream-ordered use)
-  g_sk_cap = 4 * (size_t)c.max_tokens * (size_t)std::max(H, m->Dmax);
+  SplitKScratch sk;  // split-K scratch of this scorer (stream-ordered use)
+  sk.ws = m->ws(m->skws);
+  sk.cap = 4 * (size_t)c.max_tokens * (size_t)std::max(H, m->Dmax);
   // ---- forward, keeping what the backward needs
   int* errf = reinterpret_cast<int*>(m->dWS + m->errf);
   embed_ln_f32_kernel<<<M, rt, lnsm, s>>>(ids, mask, S, H, c.vocab_size, m->w(m->tok), m->w(m->pos), m->w(m->type0),
@@ -685,7 +689,7 @@ ff_status score_batch(ff_scorer* m, const int* ids, const int* mask, const int* 
     const int A = P.A, D = P.D, F = P.F;
     float* X = m->ws(P.X);
     float* QKV = m->ws(P.QKV);
-    SL(sgemm(lin(X, M, H, m->w(P.wqkv), m->w(P.bqkv), QKV, 3 * D), 1, s), "qkv");
+    SL(sgemm(lin(X, M, H, m->w(P.wqkv), m->w(P.bqkv), QKV, 3 * D), 1, s, sk), "qkv");
     // S = Q K^T per (b, h) into P, then softmax in place
     SG g{};
     g.A = QKV; g.sAb = (long long)S * 3 * D; g.sAh = d; g.sAm = 3 * D; g.sAk = 1;
@@ -703,14 +707,14 @@ ff_status score_batch(ff_scorer* m, const int* ids, const int* mask, const int* 
     g.M = S; g.N = d; g.K = S; g.nh = A; g.alpha = 1.0f;
     SL(sgemm(g, B * A, s), "pv");
     float* O = m->ws(m->dZ);  // scratch for the projection outputs
-    SL(sgemm(lin(m->ws(P.Cx), M, D, m->w(P.wo), m->w(P.bo), O, H), 1, s), "oproj");
+    SL(sgemm(lin(m->ws(P.Cx), M, D, m->w(P.wo), m->w(P.bo), O, H), 1, s, sk), "oproj");
     add_ln_f32_kernel<<<M, rt, lnsm, s>>>(O, X, H, m->w(P.g1), m->w(P.b1), c.ln_eps, m->ws(P.Y1), m->ws(P.XH1),
                                           m->ws(P.R1));
     SL(cudaGetLastError(), "ln1");
-    SL(sgemm(lin(m->ws(P.Y1), M, H, m->w(P.w1), m->w(P.bi1), m->ws(P.U), F), 1, s), "ffn1");
+    SL(sgemm(lin(m->ws(P.Y1), M, H, m->w(P.w1), m->w(P.bi1), m->ws(P.U), F), 1, s, sk), "ffn1");
     act_fwd_kernel<<<1184, 256, 0, s>>>(m->ws(P.U), m->ws(P.Act), (size_t)M * F, c.act);
     SL(cudaGetLastError(), "act");
-    SL(sgemm(lin(m->ws(P.Act), M, F, m->w(P.w2), m->w(P.bi2), O, H), 1, s), "ffn2");
+    SL(sgemm(lin(m->ws(P.Act), M, F, m->w(P.w2), m->w(P.bi2), O, H), 1, s, sk), "ffn2");
     float* Xn = l + 1 < c.num_layers ? m->ws(m->L[l + 1].X) : m->ws(m->Xout);
     add_ln_f32_kernel<<<M, rt, lnsm, s>>>(O, m->ws(P.Y1), H, m->w(P.g2), m->w(P.b2), c.ln_eps, Xn, m->ws(P.XH2),
                                           m->ws(P.R2));
@@ -742,18 +746,18 @@ ff_status score_batch(ff_scorer* m, const int* ids, const int* mask, const int* 
     float* dAm = m->ws(m->dAm);
     ln_bwd_kernel<<<M, rt, 32 * 4, s>>>(dX, m->w(P.g2), m->ws(P.XH2), m->ws(P.R2), H, dZ);  // d(o2 + y1)
     SL(cudaGetLastError(), "ln2 bwd");
-    SL(sgemm(lin_back(dZ, M, H, m->w(P.w2), F, dAm, false), 1, s), "ffn2 bwd");  // d(act * nu)
+    SL(sgemm(lin_back(dZ, M, H, m->w(P.w2), F, dAm, false), 1, s, sk), "ffn2 bwd");  // d(act * nu)
     colprod_kernel<<<dim3((F + 31) / 32, kRowChunks), 256, 0, s>>>(m->ws(P.Act), dAm, M, F, F, m->ws(m->colg));
     group_abs_add_kernel<<<(F + 127) / 128, 128, 0, s>>>(m->ws(m->colg), F, F, 1, fsc + (size_t)l * m->Fmax);
     act_bwd_kernel<<<1184, 256, 0, s>>>(m->ws(P.U), dAm, (size_t)M * F, c.act);
     copy_kernel<<<1184, 256, 0, s>>>(dZ, dY1, (size_t)M * H);
-    SL(sgemm(lin_back(dAm, M, F, m->w(P.w1), H, dY1, true), 1, s), "ffn1 bwd");
+    SL(sgemm(lin_back(dAm, M, F, m->w(P.w1), H, dY1, true), 1, s, sk), "ffn1 bwd");
     ln_bwd_kernel<<<M, rt, 32 * 4, s>>>(dY1, m->w(P.g1), m->ws(P.XH1), m->ws(P.R1), H, dZ);  // d(o + x)
     SL(cudaGetLastError(), "ln1 bwd");
     float* dC = m->ws(m->dC);
-    SL(sgemm(lin_back(dZ, M, H, m->w(P.wo), D, dC, false), 1, s), "oproj bwd");
+    SL(sgemm(lin_back(dZ, M, H, m->w(P.wo), D, dC, false), 1, s, sk), "oproj bwd");
     colprod_kernel<<<dim3((D + 31) / 32, kRowChunks), 256, 0, s>>>(m->ws(P.Cx), dC, M, D, D, m->ws(m->colg));
-    group_abs_add_kernel<<<1, 128, 0, s>>>(m->ws(m->colg), D, A, d, hsc + (size_t)l * sc_ld);
+    group_abs_add_kernel<<<(A + 127) / 128, 128, 0, s>>>(m->ws(m->colg), D, A, d, hsc + (size_t)l * sc_ld);
     // attention backward per (b, h)
     float* QKV = m->ws(P.QKV);
     float* dQKV = m->ws(m->dQKV);
@@ -787,7 +791,7 @@ ff_status score_batch(ff_scorer* m, const int* ids, const int* mask, const int* 
     SL(sgemm(g, B * A, s), "dK");
     if (l > 0) {  // gradient w.r.t. the layer input (residual + QKV path)
       copy_kernel<<<1184, 256, 0, s>>>(dZ, dX, (size_t)M * H);
-      SL(sgemm(lin_back(dQKV, M, 3 * D, m->w(P.wqkv), H, dX, true), 1, s), "qkv bwd");
+      SL(sgemm(lin_back(dQKV, M, 3 * D, m->w(P.wqkv), H, dX, true), 1, s, sk), "qkv bwd");
     }
   }
   return FF_OK;
@@ -864,12 +868,20 @@ ff_status ff_scorer_load_weights(ff_scorer* m, const char* name, const float* ho
   const ff_config& c = m->cfg;
   if (n == "embeddings.word_embeddings.weight") { m->top_loaded |= 1; return put(m->tok, (size_t)c.vocab_size * H); }
   if (n == "embeddings.position_embeddings.weight") {
-    if (shape[0] < c.max_positions) return sfail(FF_E_SHAPE, "position table shorter than max_positions");
+    // only the first max_positions rows are copied: the table must be 2-D [>= max_positions, hidden]
+    if (rank != 2 || shape[1] != H || shape[0] < c.max_positions)
+      return sfail(FF_E_SHAPE, "position table must be [>= max_positions, hidden]");
     numel = (size_t)c.max_positions * H;
     m->top_loaded |= 2;
     return put(m->pos, numel);
   }
-  if (n == "embeddings.token_type_embeddings.weight") { numel = H; m->top_loaded |= 4; return put(m->type0, H); }
+  if (n == "embeddings.token_type_embeddings.weight") {  // row 0 only (DESIGN R16)
+    if (rank != 2 || shape[1] != H || shape[0] < 1)
+      return sfail(FF_E_SHAPE, "token-type table must be [>= 1, hidden]");
+    numel = H;
+    m->top_loaded |= 4;
+    return put(m->type0, H);
+  }
   if (n == "embeddings.LayerNorm.weight") { m->top_loaded |= 8; return put(m->eg, H); }
   if (n == "embeddings.LayerNorm.bias") { m->top_loaded |= 16; return put(m->eb, H); }
   if (n == "pooler.dense.weight" || n == "classifier.dense.weight") { m->top_loaded |= 32; return put(m->pw, (size_t)H * H); }

@@ -25,19 +25,15 @@ FF_OPT_ATTN_TC = 3
 FF_OPT_FUSED_EPILOGUES = 4
 FF_OPT_PDL = 5
 FF_OPT_ACT_QUANT = 6
-FF_OPT_GEMM_MC = 7
 FF_OPT_FUSED_MASK = 8
 FF_OPT_PDL_RR = 9
-FF_OPT_GEMM_BALANCE = 10
-FF_OPT_PDL_KINDS = 11
-FF_OPT_ATTN_SPLIT = 12
 KERNEL_KINDS = ["embed_ln", "gemm_f16", "gemm_i8", "attention", "quant_rows", "add_ln", "head", "gemm_rr_f16",
                 "gemm_rr_i8"]
 STATUS_NAMES = ["FF_OK", "FF_E_INVALID", "FF_E_SHAPE", "FF_E_STATE", "FF_E_CUDA", "FF_E_INPUT", "FF_E_UNSUPPORTED",
                 "FF_E_NOMEM"]
 
 EXPORTED = ["ff_abi_version", "ff_last_error", "ff_model_create", "ff_model_memory", "ff_bind_memory",
-            "ff_load_weights", "ff_finalize", "ff_encode", "ff_encode_host", "ff_encode_host_async", "ff_check", "ff_set_option",
+            "ff_load_weights", "ff_finalize", "ff_encode", "ff_encode_host", "ff_encode_host_async", "ff_check", "ff_set_option", "ff_get_option",
             "ff_model_destroy", "ff_launch_count", "ff_profile", "ff_encode_trace", "ff_debug_gemm", "ff_debug_quant_rows",
             "ff_debug_attention", "ff_debug_attention_q8", "ff_debug_set_trace",
             "ff_scorer_last_error", "ff_scorer_create", "ff_scorer_memory", "ff_scorer_bind_memory",
@@ -81,6 +77,7 @@ def lib():
         L.ff_encode_host_async.argtypes = [vp, vp, vp, i32, i32, vp, vp]
         L.ff_check.argtypes = [vp, vp]
         L.ff_set_option.argtypes = [vp, i32, ctypes.c_int64]
+        L.ff_get_option.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_int64)]
         L.ff_model_destroy.argtypes = [vp]
         L.ff_model_destroy.restype = None
         L.ff_launch_count.argtypes = [vp, i32, i32, ctypes.POINTER(i32)]
@@ -114,10 +111,21 @@ def check(status: int):
         raise FFError(status, lib().ff_last_error().decode(errors="replace"))
 
 
-def _stream_ptr(stream=None):
+def _stream_ptr(stream=None, device=None):
     import torch
-    s = stream if stream is not None else torch.cuda.current_stream()
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check_tensor(t, dtype, device, what):
+    """Argument marshalling guard: the C ABI reads raw pointers, so a wrong
+    dtype / layout / device would be silently misread."""
+    assert t.dtype == dtype, f"{what}: expected {dtype}, got {t.dtype}"
+    assert t.is_contiguous(), f"{what} must be contiguous"
+    if device is not None:
+        assert t.device == device, f"{what} must be on {device}, is on {t.device}"
+    else:
+        assert t.device.type == "cpu", f"{what} must be a host tensor"
 
 
 def _ptr(t):
@@ -175,6 +183,15 @@ class Encoder:
         if not cta_pairs:
             check(L.ff_set_option(self.h, FF_OPT_CTA_PAIRS, 0))
 
+    def get_option(self, option: int) -> int:
+        v = ctypes.c_int64()
+        check(lib().ff_get_option(self.h, option, ctypes.byref(v)))
+        return v.value
+
+    def fused_mask(self) -> int:
+        """FF_OPT_FUSED_MASK in effect."""
+        return self.get_option(FF_OPT_FUSED_MASK)
+
     def set_fused(self, mask: int):
         """FF_OPT_FUSED_MASK: bit 0 out-proj+LN1, bit 1 FFN1+requant, bit 2 FFN2+LN2."""
         check(lib().ff_set_option(self.h, FF_OPT_FUSED_MASK, int(mask)))
@@ -187,13 +204,17 @@ class Encoder:
             self.h = None
 
     def encode(self, ids, mask, logits=None, stream=None):
-        """ids, mask: int32 [B, S] CUDA tensors -> logits fp32 [B, C] (async on the stream)."""
+        """ids, mask: int32 [B, S] CUDA tensors -> logits fp32 [B, C] (async on the stream;
+        default: the current stream of the model's device)."""
         import torch
         B, S = ids.shape
-        assert ids.dtype == torch.int32 and mask.dtype == torch.int32 and ids.is_contiguous() and mask.is_contiguous()
+        _check_tensor(ids, torch.int32, self.device, "ids")
+        _check_tensor(mask, torch.int32, self.device, "mask")
         if logits is None:
             logits = torch.empty((B, self.cfg.num_classes), dtype=torch.float32, device=ids.device)
-        check(lib().ff_encode(self.h, _ptr(ids), _ptr(mask), B, S, _ptr(logits), _stream_ptr(stream)))
+        _check_tensor(logits, torch.float32, self.device, "logits")
+        assert tuple(logits.shape) == (B, self.cfg.num_classes), "logits must be [B, num_classes]"
+        check(lib().ff_encode(self.h, _ptr(ids), _ptr(mask), B, S, _ptr(logits), _stream_ptr(stream, self.device)))
         return logits
 
     def encode_host(self, ids, mask, logits=None, stream=None):
@@ -202,14 +223,20 @@ class Encoder:
         B, S = ids.shape
         if logits is None:
             logits = torch.empty((B, self.cfg.num_classes), dtype=torch.float32).pin_memory()
-        check(lib().ff_encode_host(self.h, _ptr(ids), _ptr(mask), B, S, _ptr(logits), _stream_ptr(stream)))
+        for t, dt, n in ((ids, torch.int32, "ids"), (mask, torch.int32, "mask"), (logits, torch.float32, "logits")):
+            _check_tensor(t, dt, None, n)
+        check(lib().ff_encode_host(self.h, _ptr(ids), _ptr(mask), B, S, _ptr(logits), _stream_ptr(stream, self.device)))
         return logits
 
     def encode_host_async(self, ids, mask, logits, stream=None):
         """ff_encode_host_async: pinned host ids / mask -> pinned host logits, enqueued
         without synchronizing (read `logits` only after the stream is synchronized)."""
+        import torch
         B, S = ids.shape
-        check(lib().ff_encode_host_async(self.h, _ptr(ids), _ptr(mask), B, S, _ptr(logits), _stream_ptr(stream)))
+        for t, dt, n in ((ids, torch.int32, "ids"), (mask, torch.int32, "mask"), (logits, torch.float32, "logits")):
+            _check_tensor(t, dt, None, n)
+        check(lib().ff_encode_host_async(self.h, _ptr(ids), _ptr(mask), B, S, _ptr(logits),
+                                         _stream_ptr(stream, self.device)))
         return logits
 
     def check_inputs(self, stream=None):
@@ -254,22 +281,6 @@ class Encoder:
 
 
 # ------------------------------------------------------------ debug entry points
-def set_gemm_mc(on: bool):
-    """FF_OPT_GEMM_MC (process-wide): CTA-pair GEMMs in clusters of two pairs
-    sharing W k-blocks by TMA multicast."""
-    check(lib().ff_set_option(None, FF_OPT_GEMM_MC, 1 if on else 0))
-
-
-def set_gemm_balance(on: bool):
-    """FF_OPT_GEMM_BALANCE (process-wide): split the last partial wave of CTA-pair tiles."""
-    check(lib().ff_set_option(None, FF_OPT_GEMM_BALANCE, 1 if on else 0))
-
-
-def set_attn_split(on: bool):
-    """FF_OPT_ATTN_SPLIT (process-wide): clusters may split a sequence's heads in the tcgen05 attention."""
-    check(lib().ff_set_option(None, FF_OPT_ATTN_SPLIT, 1 if on else 0))
-
-
 def gemm(A, W, out_mode=0, bias=None, sx=None, sw=None, act=-1, out=None, cta_pair=None):
     """C = A W^T through the production tcgen05 kernel.  A [M,K], W [N,K]: both
     int8 (kind::i8) or both fp16 (kind::f16) CUDA tensors with 16-byte aligned rows."""
@@ -389,11 +400,19 @@ class Scorer:
         self.ffn_scores.zero_()
 
     def score(self, ids, mask, labels, logits=None, stream=None):
+        """ids, mask [B, S], labels [B]: int32 tensors on the scorer's device."""
+        import torch
         B, S = ids.shape
+        for t, n in ((ids, "ids"), (mask, "mask"), (labels, "labels")):
+            _check_tensor(t, torch.int32, self.device, n)
+        assert labels.shape == (B,), "labels must be [B]"
+        if logits is not None:
+            _check_tensor(logits, torch.float32, self.device, "logits")
         nul = ctypes.c_void_p(None)
         _scheck(lib().ff_score_batch(self.h, _ptr(ids), _ptr(mask), _ptr(labels), B, S, _ptr(self.head_scores),
                                      _ptr(self.ffn_scores), _ptr(self.loss),
-                                     _ptr(logits) if logits is not None else nul, _stream_ptr(stream)))
+                                     _ptr(logits) if logits is not None else nul,
+                                     _stream_ptr(stream, self.device)))
         return self.loss
 
     def check_inputs(self, stream=None):

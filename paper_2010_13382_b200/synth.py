@@ -78,6 +78,10 @@ def config(name: str) -> ModelConfig:
     if name == "c2":  # configs[1]: TinyBERT 4L/312, 12 heads (d=26), FFN 1200, B64 S128
         return ModelConfig("c2", 4, 312, 26, _uniform(4, 12), _uniform(4, 1200), _uniform(4, I8), 30522, 512, 2,
                            1e-12, batch=64, seq=128, cls_id=101)
+    if name in ("c2_9_900", "c2_8_600"):  # Table 3 pruned TinyBERT students (DESIGN R20)
+        A, F = (9, 900) if name == "c2_9_900" else (8, 600)
+        return ModelConfig(name, 4, 312, 26, _uniform(4, A), _uniform(4, F), _uniform(4, I8), 30522, 512, 2,
+                           1e-12, batch=64, seq=128, cls_id=101)
     if name == "c3":  # configs[2]: distilroberta 6L/768, heads 12->8, FFN 3072->1536, int8, B256 S128
         return ModelConfig("c3", 6, 768, 64, _uniform(6, 8), _uniform(6, 1536), _uniform(6, I8), 50265, 514, 2,
                            1e-5, batch=256, seq=128, cls_id=0)

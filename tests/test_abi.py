@@ -96,17 +96,12 @@ def test_null_model_calls_are_rejected(built):
     assert built.ff_finalize(None, None) == ffb.FF_E_INVALID
 
 
-def test_process_wide_options_without_a_model(built):
-    """FF_OPT_PDL / GEMM_MC / PDL_RR / GEMM_BALANCE / PDL_KINDS are process-wide
-    and accept m = NULL (no device work); model options need a model."""
-    for opt, on, off in ((ffb.FF_OPT_GEMM_MC, 1, 0), (ffb.FF_OPT_PDL_RR, 1, 0), (ffb.FF_OPT_GEMM_BALANCE, 1, 0),
-                         (ffb.FF_OPT_PDL_KINDS, 0x3, 0xFFFFFFFF), (ffb.FF_OPT_PDL, 0, 1)):
-        assert built.ff_set_option(None, opt, on) == ffb.FF_OK
-        assert built.ff_set_option(None, opt, off) == ffb.FF_OK
-    assert built.ff_set_option(None, ffb.FF_OPT_PDL_RR, 0) == ffb.FF_OK  # restore the default
-    assert built.ff_set_option(None, ffb.FF_OPT_FUSED_MASK, 2) == ffb.FF_E_INVALID
-    assert built.ff_set_option(None, ffb.FF_OPT_GRAPHS, 1) == ffb.FF_E_INVALID
-    assert built.ff_set_option(None, 999, 1) == ffb.FF_E_INVALID
+def test_options_are_per_model(built):
+    """Every option is per model (no process-wide state on the launch path):
+    m = NULL is rejected, and the removed round-1 experiment ids (7, 10, 11,
+    12) are unknown."""
+    for opt in (ffb.FF_OPT_PDL, ffb.FF_OPT_PDL_RR, ffb.FF_OPT_FUSED_MASK, ffb.FF_OPT_GRAPHS, 7, 10, 11, 12, 999):
+        assert built.ff_set_option(None, opt, 1) == ffb.FF_E_INVALID
 
 
 def test_scorer_config_validation_before_device(built):

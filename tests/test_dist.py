@@ -1,6 +1,8 @@
 """Multi-process (world_size 2, gloo, CPU) tests of the data-parallel path:
 contiguous sharding, logits gather to rank 0, and sharded == single-process
-results (the oracle stands in for the per-GPU encoder)."""
+results (the oracle stands in for the per-GPU encoder), including empty
+shards (B < world) and several batches in flight on the double-buffered
+gather."""
 import os
 import socket
 
@@ -33,7 +35,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, B, out_path):
+def _worker(rank, world, port, Bs, out_path):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -42,27 +44,43 @@ def _worker(rank, world, port, B, out_path):
     cfg = synth.config("c1")
     w = synth.make_weights(cfg)
     orc = oracle.Oracle(cfg, w)
-    ids, mask = synth.make_inputs(cfg, B=B, ragged=True, seed=3)
 
-    def encode(i, m):
-        return torch.from_numpy(orc.encode(i.numpy(), m.numpy()))
+    def encode(i, m, out):
+        out.copy_(torch.from_numpy(orc.encode(i.numpy(), m.numpy())))
 
-    got = ShardedEncoder(encode).encode_global(torch.from_numpy(ids), torch.from_numpy(mask))
+    sh = ShardedEncoder(encode, cfg.num_classes, max(Bs))
+    # several global batches submitted back to back (depth-2 buffer reuse),
+    # results read in order after all were submitted
+    batches = [synth.make_inputs(cfg, B=B, ragged=True, seed=3 + k) for k, B in enumerate(Bs)]
+    outs = []
+    pend = []
+    for ids, mask in batches:
+        pend.append(sh.submit(torch.from_numpy(ids), torch.from_numpy(mask)))
+        if len(pend) == sh.depth:  # the oldest slot is reused by the next submit: read it now
+            r = pend.pop(0).result()
+            outs.append(None if r is None else r.clone())
+    for p in pend:
+        r = p.result()
+        outs.append(None if r is None else r.clone())
     if rank == 0:
-        np.save(out_path, got.numpy())
+        np.savez(out_path, *[o.numpy() for o in outs])
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("B", [4, 5])
-def test_sharded_equals_single_process_gloo(tmp_path, B):
-    out = str(tmp_path / "logits.npy")
-    mp.spawn(_worker, args=(2, _free_port(), B, out), nprocs=2, join=True)
+@pytest.mark.parametrize("Bs", [(4,), (5,), (1,), (3, 1, 4, 2)])
+def test_sharded_equals_single_process_gloo(tmp_path, Bs):
+    """B = 1 with world 2 gives rank 1 an empty shard (it still joins the gather)."""
+    out = str(tmp_path / "logits.npz")
+    mp.spawn(_worker, args=(2, _free_port(), Bs, out), nprocs=2, join=True)
     got = np.load(out)
     import oracle
     from paper_2010_13382_b200 import synth
     cfg = synth.config("c1")
-    ids, mask = synth.make_inputs(cfg, B=B, ragged=True, seed=3)
-    ref = oracle.Oracle(cfg, synth.make_weights(cfg)).encode(ids, mask)
-    assert got.shape == ref.shape
-    assert np.array_equal(got, ref)  # batch invariance makes sharding exact
+    orc = oracle.Oracle(cfg, synth.make_weights(cfg))
+    for k, B in enumerate(Bs):
+        ids, mask = synth.make_inputs(cfg, B=B, ragged=True, seed=3 + k)
+        ref = orc.encode(ids, mask)
+        g = got[f"arr_{k}"]
+        assert g.shape == ref.shape
+        assert np.array_equal(g, ref)  # batch invariance makes sharding exact

@@ -88,76 +88,6 @@ def test_gemm_epilogues(act, pair):
     assert np.all(np.abs(got - ref) <= np.abs(ref) * 2.0 ** -10 + 2.0 ** -24 * 4), np.abs(got - ref).max()
 
 
-@pytest.mark.parametrize("i8", [True, False])
-@pytest.mark.parametrize("M,N,K", [(32768, 1536, 768), (32768, 768, 1536), (19000, 768, 512), (9000, 1200, 312),
-                                   (40000, 1536, 768), (23000, 3072, 768)])
-def test_gemm_w_multicast_identical(M, N, K, i8):
-    """FF_OPT_GEMM_MC (clusters of two CTA pairs sharing W by TMA multicast,
-    odd / ragged row-tile counts included) gives the same accumulators and
-    the same fp16 epilogue output as independent pairs; int8 accumulators
-    also equal an independent int8 GEMM (cuBLASLt) bit for bit."""
-    rng = np.random.default_rng(M + N + K)
-    if i8:
-        A = _pitched(rng.integers(-127, 128, (M, K), dtype=np.int8), torch.int8, 16)
-        W = _pitched(rng.integers(-127, 128, (N, K), dtype=np.int8), torch.int8, 16)
-    else:
-        A = _pitched(np.float16(rng.standard_normal((M, K))), torch.float16, 8)
-        W = _pitched(np.float16(rng.standard_normal((N, K)) * 0.05), torch.float16, 8)
-    b = torch.from_numpy((rng.standard_normal(N) * 0.1).astype(np.float32)).cuda()
-    sx = torch.from_numpy((rng.random(M) * 0.01 + 1e-3).astype(np.float32)).cuda() if i8 else None
-    sw = torch.from_numpy((rng.random(N) * 0.001 + 1e-4).astype(np.float32)).cuda() if i8 else None
-    outs = {}
-    try:
-        for mc in (False, True):
-            ffb.set_gemm_mc(mc)
-            raw = ffb.gemm(A, W, out_mode=0, cta_pair=True)
-            y = ffb.gemm(A, W, out_mode=1, bias=b, sx=sx, sw=sw, act=0, cta_pair=True)
-            torch.cuda.synchronize()
-            outs[mc] = (raw.cpu(), y.cpu())
-    finally:
-        ffb.set_gemm_mc(False)
-    assert torch.equal(outs[True][0], outs[False][0])
-    assert torch.equal(outs[True][1], outs[False][1])
-    if i8 and K % 8 == 0 and N % 8 == 0:
-        ref = torch._int_mm(A.contiguous(), W.contiguous().t().contiguous()).cpu()
-        assert torch.equal(outs[True][0], ref)
-
-
-@pytest.mark.parametrize("i8", [True, False])
-@pytest.mark.parametrize("M,N,K", [(32768, 768, 1536), (32768, 1536, 768), (19000, 768, 512), (9000, 1200, 312),
-                                   (5000, 640, 320), (32768, 768, 512)])
-def test_gemm_tail_balancing_identical(M, N, K, i8):
-    """FF_OPT_GEMM_BALANCE (the last partial wave of CTA-pair tiles split into
-    half-width tiles: N = BN/2 MMAs, BN/4-row W boxes, 32 columns per epilogue warp)
-    gives the same accumulators and fp16 epilogue output as whole tiles; the
-    int8 accumulators also equal an independent int8 GEMM (cuBLASLt)."""
-    rng = np.random.default_rng(M + 3 * N + K)
-    if i8:
-        A = _pitched(rng.integers(-127, 128, (M, K), dtype=np.int8), torch.int8, 16)
-        W = _pitched(rng.integers(-127, 128, (N, K), dtype=np.int8), torch.int8, 16)
-    else:
-        A = _pitched(np.float16(rng.standard_normal((M, K))), torch.float16, 8)
-        W = _pitched(np.float16(rng.standard_normal((N, K)) * 0.05), torch.float16, 8)
-    b = torch.from_numpy((rng.standard_normal(N) * 0.1).astype(np.float32)).cuda()
-    sx = torch.from_numpy((rng.random(M) * 0.01 + 1e-3).astype(np.float32)).cuda() if i8 else None
-    sw = torch.from_numpy((rng.random(N) * 0.001 + 1e-4).astype(np.float32)).cuda() if i8 else None
-    outs = {}
-    try:
-        for bal in (False, True):
-            ffb.set_gemm_balance(bal)
-            raw = ffb.gemm(A, W, out_mode=0, cta_pair=True)
-            y = ffb.gemm(A, W, out_mode=1, bias=b, sx=sx, sw=sw, act=0, cta_pair=True)
-            torch.cuda.synchronize()
-            outs[bal] = (raw.cpu(), y.cpu())
-    finally:
-        ffb.set_gemm_balance(False)
-    assert torch.equal(outs[True][0], outs[False][0])
-    assert torch.equal(outs[True][1], outs[False][1])
-    if i8 and K % 8 == 0 and N % 8 == 0:
-        ref = torch._int_mm(A.contiguous(), W.contiguous().t().contiguous()).cpu()
-        assert torch.equal(outs[True][0], ref)
-
-
 def test_quant_rows_bit_exact_vs_oracle():
     rng = np.random.default_rng(11)
     for M, K in [(64, 312), (33, 1536), (5, 4096), (7, 234)]:

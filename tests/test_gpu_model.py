@@ -121,6 +121,31 @@ def test_stage_lockstep(name, fused):
                 assert_close16(got, ref, f"{name} layer {l} {key} fused={fused}")
 
 
+@pytest.mark.parametrize("name", ["c2_i8", "c3_i8"])
+def test_gelu_epilogue_follows_oracle_rounding(name):
+    """DESIGN R2: in int8 layers the FFN1 dequant is bit-exact, so the stored
+    fp16 intermediate differs from the oracle's RN16(RN32(GELU_fp64(y))) only
+    where the degree-11 GELU's fp32 error crosses an fp16 rounding midpoint:
+    <= 2e-4 of the elements (measured 6.6e-5 on the device, 2^28 points,
+    tools/micro/exp_accuracy.cu; the round-1 degree-6 fit flipped 0.2-0.4%),
+    and never by more than one fp16 ulp."""
+    cfg, w, ids, mask = build_case(name)
+    enc = Encoder(cfg, w)
+    orc = Oracle(cfg, w)
+    B, S = ids.shape
+    nd = tot = 0
+    for l in range(cfg.num_layers):
+        t = {k: f32(v) for k, v in enc.trace(dev(ids), dev(mask), l).items()}
+        ref = orc.stage(l, oracle.ST_FFN1, t["h1"], None, mask=mask, B=B, S=S)
+        got = t["i"]
+        diff = got != ref
+        ulp = np.spacing(np.abs(ref).astype(np.float16)).astype(np.float64)
+        assert np.all(np.abs(got - ref)[diff] <= ulp[diff] * 1.0001 + 2.0 ** -24), f"layer {l}: > 1 ulp"
+        nd += int(diff.sum())
+        tot += diff.size
+    assert nd <= 2e-4 * tot, f"{nd} of {tot} GELU outputs differ from the oracle's rounding"
+
+
 @pytest.mark.parametrize("name", ["c1_i8", "c3_i8", "c3_f16"])
 def test_fused_epilogues_match_unfused(name):
     """Same layer input -> the fused cluster epilogues reproduce the unfused
@@ -211,7 +236,7 @@ def test_end_to_end_deep_calibrated(name, B):
         assert np.abs(got - ref).max() <= 1e-2
     else:
         drift = np.abs(orc.encode(ids, mask, acc32=True) - ref).max()
-        bound = max(3 * drift, 1e-3 * np.abs(ref).max())
+        bound = max(2 * drift, 1e-3 * np.abs(ref).max())
         assert np.abs(got - ref).max() <= bound, (np.abs(got - ref).max(), drift)
     assert _margin_ok(ref, got, 2e-2) >= 0.999
 
@@ -308,10 +333,10 @@ def test_full_size_c3_sampled_rows_vs_oracle():
     ref = _oracle_rows_parallel(orc, ids, mask, rows)
     drift = np.abs(_oracle_rows_parallel(orc, ids, mask, rows, acc32=True) - ref).max()
     err = np.abs(got[rows] - ref).max()
-    # DESIGN "Tolerances": 6 int8 layers amplify rounding-boundary flips; the
-    # GPU differs from the oracle in more reduction orders (LN, softmax, GELU)
-    # than the oracle's own fp32-vs-fp64 drift, hence the factor 3.
-    bound = max(3 * drift, 1e-3 * np.abs(ref).max())
+    # DESIGN "Tolerances": 6 int8 layers amplify
+    # rounding-boundary flips, so the bound is 2 x the oracle's own
+    # fp32-vs-fp64 accumulation drift on the same rows.
+    bound = max(2 * drift, 1e-3 * np.abs(ref).max())
     assert err <= bound, (err, drift, np.abs(ref).max())
     assert _margin_ok(ref, got[rows], 2e-2) == 1.0
 
@@ -386,7 +411,7 @@ def test_full_size_sampled_rows_vs_oracle(name, rows):
         assert err <= 1e-2, err
     else:
         drift = np.abs(_oracle_rows_parallel(orc, ids, mask, rows, acc32=True) - ref).max()
-        assert err <= max(3 * drift, 1e-3 * np.abs(ref).max()), (err, drift)
+        assert err <= max(2 * drift, 1e-3 * np.abs(ref).max()), (err, drift)
     assert _margin_ok(ref, got[rows], 2e-2) == 1.0
 
 
@@ -401,7 +426,7 @@ def test_full_size_c3_fused_epilogues_sampled_rows():
     rows = [0, 100, 200, 255]
     ref = _oracle_rows_parallel(orc, ids, mask, rows)
     drift = np.abs(_oracle_rows_parallel(orc, ids, mask, rows, acc32=True) - ref).max()
-    assert np.abs(got[rows] - ref).max() <= max(3 * drift, 1e-3 * np.abs(ref).max())
+    assert np.abs(got[rows] - ref).max() <= max(2 * drift, 1e-3 * np.abs(ref).max())
     assert _margin_ok(ref, got[rows], 2e-2) == 1.0
 
 
@@ -420,7 +445,7 @@ def test_per_tensor_u8_activations_vs_oracle(name, B, S):
     ref = orc.encode(ids, mask)
     drift = np.abs(orc.encode(ids, mask, acc32=True) - ref).max()
     err = np.abs(got - ref).max()
-    assert err <= max(3 * drift, 1e-3 * np.abs(ref).max()), (err, drift)
+    assert err <= max(2 * drift, 1e-3 * np.abs(ref).max()), (err, drift)
     assert _margin_ok(ref, got, 2e-2) >= 0.999
     # a genuinely different quantizer from the per-row default
     row = f32(Encoder(cfg, w).encode(dev(ids), dev(mask)))
@@ -482,25 +507,6 @@ def test_encode_host_async_matches_sync():
         assert torch.equal(o, enc.encode_host(i, m))
 
 
-@pytest.mark.parametrize("name,B,S", [("c1", 4, 32), ("c3", 256, 128), ("c3", 37, 96)])
-@pytest.mark.parametrize("dt", [1, 0])
-def test_attention_cluster_head_split_identical(name, B, S, dt):
-    """FF_OPT_ATTN_SPLIT: clusters of CTAs splitting each sequence's heads (the
-    fused int8 requant's row amax exchanged through DSMEM) give bit-identical
-    logits to one CTA per sequence."""
-    cfg = synth.config(name).with_dtype(dt).with_batch(B, S)
-    w = synth.make_weights(cfg)
-    ids, mask = synth.make_inputs(cfg, B=B, S=S, ragged=True, seed=91)
-    out = {}
-    try:
-        for split in (False, True):
-            ffb.set_attn_split(split)
-            out[split] = Encoder(cfg, w).encode(dev(ids), dev(mask)).cpu()
-    finally:
-        ffb.set_attn_split(False)
-    assert torch.equal(out[True], out[False])
-
-
 @pytest.mark.parametrize("mask_bits", [1, 3, 4, 5, 6, 7])
 def test_every_fusion_mask_within_drift_bound(mask_bits):
     """FF_OPT_FUSED_MASK combinations with a LayerNorm fusion (the LN sums run in
@@ -514,5 +520,5 @@ def test_every_fusion_mask_within_drift_bound(mask_bits):
     rows = [0, 5, 15]
     ref = orc.encode(ids[rows], mask[rows])
     drift = np.abs(orc.encode(ids[rows], mask[rows], acc32=True) - ref).max()
-    assert np.abs(got[rows] - ref).max() <= max(3 * drift, 1e-3 * np.abs(ref).max())
+    assert np.abs(got[rows] - ref).max() <= max(2 * drift, 1e-3 * np.abs(ref).max())
     assert (got[rows].argmax(1) == ref.argmax(1)).all() or _margin_ok(ref, got[rows], 2e-2) == 1.0

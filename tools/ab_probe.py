@@ -1,8 +1,8 @@
-"""A/B probe of a process-wide kernel option on the C3 forward: device time per
+"""A/B probe of a per-model kernel option on the C3 forward: device time per
 step (graph replay, L2 flushed before each step, median of 30) and the
 per-launch GEMM times of one profiled forward (first layer's four GEMMs).
 
-python tools/ab_probe.py [option_name] [dtype i8|f16]   (default gemm_mc i8)
+python tools/ab_probe.py [option_name] [dtype i8|f16]   (default fused7 i8)
 """
 import sys
 
@@ -12,14 +12,14 @@ sys.path.insert(0, ".")
 from paper_2010_13382_b200 import synth  # noqa: E402
 from paper_2010_13382_b200 import fastformers as ffb  # noqa: E402
 
-OPTS = {"gemm_mc": lambda enc, on: ffb.set_gemm_mc(on),
-        "gemm_balance": lambda enc, on: ffb.set_gemm_balance(on)}
+OPTS = {"pdl": lambda enc, on: ffb.check(ffb.lib().ff_set_option(enc.h, ffb.FF_OPT_PDL, 1 if on else 0)),
+        "pdl_rr": lambda enc, on: ffb.check(ffb.lib().ff_set_option(enc.h, ffb.FF_OPT_PDL_RR, 1 if on else 0))}
 for _m in range(1, 8):  # FF_OPT_FUSED_MASK bits: 1 out-proj+LN1, 2 FFN1+requant, 4 FFN2+LN2
     OPTS[f"fused{_m}"] = (lambda m: lambda enc, on: enc.set_fused(m if on else 0))(_m)
 
 
 def main():
-    opt = sys.argv[1] if len(sys.argv) > 1 else "gemm_mc"
+    opt = sys.argv[1] if len(sys.argv) > 1 else "fused7"
     dtype = 1 if (sys.argv[2] if len(sys.argv) > 2 else "i8") == "i8" else 0
     cfg = synth.config("c3").with_dtype(dtype)
     w = synth.make_weights(cfg)
