@@ -29,17 +29,46 @@ def f32(t):
     return t.float().cpu().numpy()
 
 
-def assert_close16(got, ref, what, frac=1e-4):
+def assert_close16(got, ref, what, frac=1e-4, slack=0.0):
     """fp16 stage tolerance (DESIGN "Tolerances"): elements differing by more
     than 2 fp16 ulps (2^-10 relative, floor 2^-14 = smallest normal fp16, which
-    covers fp32 accumulation-order noise near zero) are <= 1e-4 of the tensor,
-    no element is off by more than 8 ulps of max|ref|, rel. Frobenius <= 1e-3."""
+    covers fp32 accumulation-order noise near zero) -- plus a per-element
+    `slack` where an unobservable intermediate may round either way -- are
+    <= 1e-4 of the tensor, no element is off by more than 8 ulps of max|ref|,
+    rel. Frobenius <= 1e-3."""
     d = np.abs(got.astype(np.float64) - ref.astype(np.float64))
-    big = d > np.abs(ref) * 2.0 ** -10 + 2.0 ** -14
+    big = d > np.abs(ref) * 2.0 ** -10 + 2.0 ** -14 + slack
     rel = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
     assert big.mean() <= frac, f"{what}: {int(big.sum())} elements beyond 2 ulp (max abs {d.max():.3e})"
     assert d.max() <= 8 * 2.0 ** -10 * max(np.abs(ref).max(), 2.0 ** -4), f"{what}: max abs {d.max():.3e}"
     assert rel <= 1e-3, f"{what}: rel {rel:.3e}"
+
+
+def _ln_slack_of_fp16_gemm(a16, W, b, res, gamma, eps):
+    """Per-element bound on how much LN(R16(a16 W16^T + b) + res) can move
+    when R16 of the fp16 GEMM output is taken from any fp32 accumulation order:
+    an output o_j is ambiguous when the fp32 accumulation error bound
+    K 2^-24 sum_k |a_k w_k| (fp64 sums) reaches an fp16 rounding midpoint; then
+    it may differ by one fp16 ulp u_j.  To first order, with x = o + res,
+    r = 1/sqrt(var + eps):  |dy_i| <= |g_i| r (|do_i| + sum|do| / H
+    + r^2 |x_i - mu| sum(|x - mu| |do|) / H)."""
+    W16 = W.astype(np.float16).astype(np.float64)
+    a = a16.astype(np.float64)
+    acc = a @ W16.T
+    K = a.shape[1]
+    err = K * 2.0 ** -24 * (np.abs(a) @ np.abs(W16).T)
+    lo = np.float16((acc - err).astype(np.float32) + b.astype(np.float32))
+    hi = np.float16((acc + err).astype(np.float32) + b.astype(np.float32))
+    o = np.float16(acc.astype(np.float32) + b.astype(np.float32)).astype(np.float64)
+    do = np.where(lo != hi, np.spacing(np.abs(o).astype(np.float16)).astype(np.float64), 0.0)
+    x = o + res.astype(np.float64)
+    H = x.shape[1]
+    mu = x.mean(1, keepdims=True)
+    r = 1.0 / np.sqrt(((x - mu) ** 2).mean(1, keepdims=True) + eps)
+    g = np.abs(gamma.astype(np.float64))[None, :]
+    dmu = do.sum(1, keepdims=True) / H
+    dvar = (np.abs(x - mu) * do).sum(1, keepdims=True) / H
+    return 1.01 * g * r * (do + dmu + r * r * np.abs(x - mu) * dvar)
 
 
 def small(cfg, B, S):
@@ -113,10 +142,16 @@ def test_stage_lockstep(name, fused):
                 nbad = int((got != ref).sum())
                 assert nbad == 0, f"{name} layer {l} {key}: {nbad} elements differ (int8 stage must be bit-exact)"
             elif fused and not i8 and key in ("h1", "x_out"):
-                # two composed stages: the GPU's internal R16(O) / R16(Y) of an
-                # fp16 GEMM differs from the oracle's by one ulp on ~1% of the
-                # elements (fp32 summation order), and LN carries that flip
-                assert_close16(got, ref, f"{name} layer {l} {key} fused", frac=1e-3)
+                # two composed stages whose intermediate R16(O) / R16(Y) (an
+                # fp16 GEMM with fp32 accumulation) never reaches memory: the
+                # LN check allows, per element, what a legitimately different
+                # rounding of that intermediate can move it
+                pre = "attention.output" if key == "h1" else "output"
+                a_in, res = (t["ctx"], t["x_in"]) if key == "h1" else (t["i"], t["h1"])
+                slack = _ln_slack_of_fp16_gemm(a_in, w[f"encoder.layer.{l}.{pre}.dense.weight"],
+                                               w[f"encoder.layer.{l}.{pre}.dense.bias"], res,
+                                               w[f"encoder.layer.{l}.{pre}.LayerNorm.weight"], cfg.ln_eps)
+                assert_close16(got, ref, f"{name} layer {l} {key} fused", slack=slack)
             else:
                 assert_close16(got, ref, f"{name} layer {l} {key} fused={fused}")
 
