@@ -1,0 +1,356 @@
+// attention_long.cu -- fused masked-softmax attention on the tcgen05 tensor
+// cores for 128 < S <= 512 and head_dim 64: the long-passage shapes of the
+// SuperGLUE configs (C4 BERT-base at S 512, C5 at S 256; "ReCoRD's long
+// passages"; SURVEY 8(a) a3, P:104 Q.K^T and P.V in floating point).
+//
+// Work unit = (sequence b, query block of 128 rows, head h); one persistent
+// CTA per SM walks units blockIdx.x, +gridDim.x, ...  Per unit, with KC =
+// ceil(S / 128) key chunks:
+//   warp 0     TMA: Q block, K_0..K_{KC-1}, V_0..V_{KC-1} (128 rows x 64 fp16,
+//              128B swizzle) through a ring of 16 KB tile slots, running ahead
+//              into the next units
+//   warp 1     TMEM allocator + MMA issuer (one thread):
+//                S_c = Q . K_c^T     (fp32, TMEM columns [128 c, 128 c + 128))
+//                O  += P_c . V_c     (fp32; KC = 4: columns [0, 64), reusing
+//                                    S_0 once it has been read; KC = 2: [256, 320))
+//   warps 2-9  softmax + epilogue: two warps per TMEM lane quadrant (= 32
+//              query rows), each owning one half (64 keys) of every chunk:
+//                pass 1: s = RN(raw * fp32(1/sqrt d)) (+ key mask -inf), row max
+//                pass 2: e = exp(s - max) (ex2.approx of (s - max) log2 e), the
+//                        row sum l; e written back over S in TMEM
+//                pass 3: p = e / l (IEEE quotient, Markstein), P16 = R16(p)
+//                        into a double-buffered 128B-swizzled K-major P tile
+//                epilogue: ctx = R16(O) (fp16 rows)
+// This is the oracle's order (DESIGN R9: max over all keys, then e, l, then
+// normalise and round P to fp16 before P.V) -- no online rescaling -- and one
+// exp per score.  TMEM reads are cheap (~900 B/clk/SM, tools/micro/tmem_bw.cu)
+// so S is re-read per pass instead of being held in registers.
+// int8 layers store fp16 ctx here; their Q8row requant runs as quant_rows.
+#include "ff_kernels.h"
+#include "ptx.cuh"
+#include "quant.cuh"
+
+namespace ff {
+
+namespace {
+
+constexpr int kLQ = 128;               // query rows per unit (TMEM lanes)
+constexpr int kLD = 64;                // head_dim
+constexpr int kLTile = 128 * 128;      // one 128-row x 64-column fp16 tile, 128B swizzle
+constexpr int kLSlots = 8;             // ring of tile slots (Q, K_c, V_c of consecutive units)
+constexpr int kLSoftWarps = 8;
+constexpr int kLThreads = 64 + 32 * kLSoftWarps;
+constexpr int kLMaxKeys = 512;
+
+struct SmemL {
+  static constexpr int RING = 0;                              // [kLSlots] tiles
+  static constexpr int P = RING + kLSlots * kLTile;           // P[2]: 2 k-blocks of 64 keys each
+  static constexpr int MASK = P + 2 * 2 * kLTile;             // kLMaxKeys floats
+  static constexpr int RED = MASK + kLMaxKeys * 4;            // [2][2][128] floats: max, sum
+  static constexpr int BAR = RED + 2 * 2 * kLQ * 4;
+  static constexpr int TOTAL = BAR + 256 + 1024;
+  static_assert(TOTAL <= 227 * 1024, "smem budget");
+};
+
+__device__ __forceinline__ constexpr uint32_t idesc_l(int N, int b_mn) {
+  return (1u << 4) | ((uint32_t)b_mn << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ uint64_t sw128_desc_mn(const void* smem_tile) {
+  const uint64_t addr = smem_u32(smem_tile);
+  return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+__device__ __forceinline__ float ex2l(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+struct Unit {
+  int b, qb, h;
+};
+__device__ __forceinline__ Unit unit_of(int u, int nqb, int A) {
+  Unit x;
+  x.h = u % A;
+  const int t = u / A;
+  x.qb = t % nqb;
+  x.b = t / nqb;
+  return x;
+}
+
+template <int KC>
+__global__ void __launch_bounds__(kLThreads, 1)
+    attention_long_kernel(const __grid_constant__ CUtensorMap tmQKV, const int32_t* __restrict__ mask, int B, int S,
+                          int A, float scale, __half* __restrict__ ctx, int ldc) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SmemL::BAR);
+  uint64_t* full = bar;                    // [kLSlots] TMA -> MMA
+  uint64_t* empty = bar + kLSlots;         // [kLSlots] MMA -> TMA
+  uint64_t* s_full = bar + 2 * kLSlots;    // MMA (all S chunks) -> softmax
+  uint64_t* p_full = s_full + 1;           // [2] softmax (P chunk written) -> MMA
+  uint64_t* p_empty = p_full + 2;          // [2] MMA (P chunk consumed) -> softmax
+  uint64_t* o_full = p_empty + 2;          // MMA (last P.V) -> epilogue
+  uint64_t* t_free = o_full + 1;           // epilogue (O read, all of S consumed) -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_free + 1);
+  float* sMask = reinterpret_cast<float*>(smem + SmemL::MASK);
+  float* sRed = reinterpret_cast<float*>(smem + SmemL::RED);
+  constexpr uint32_t kO = KC == 4 ? 0u : (uint32_t)(KC * 128);  // O columns
+  constexpr int kSoft = 32 * kLSoftWarps;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int D = A * kLD;
+  const int nqb = (S + kLQ - 1) / kLQ;
+  const int n_units = B * nqb * A;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQKV);
+    for (int i = 0; i < kLSlots; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, 1);
+    }
+    mbar_init(s_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(p_full + i, kSoft);
+      mbar_init(p_empty + i, 1);
+    }
+    mbar_init(o_full, 1);
+    mbar_init(t_free, kSoft);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  griddep_wait();  // QKV / mask come from the previous kernel
+  griddep_launch();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t cnt = 0;
+      auto load = [&](int col, int row) {
+        const int slot = cnt % kLSlots;
+        mbar_wait(empty + slot, ((cnt / kLSlots) & 1) ^ 1);
+        mbar_expect_tx(full + slot, kLTile);
+        tma_load_2d(smem + SmemL::RING + slot * kLTile, &tmQKV, full + slot, col, row, kEvictFirst);
+        ++cnt;
+      };
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const Unit x = unit_of(u, nqb, A);
+        const int row0 = x.b * S;
+        load(x.h * kLD, row0 + x.qb * kLQ);
+        for (int c = 0; c < KC; ++c) load(D + x.h * kLD, row0 + c * 128);
+        for (int c = 0; c < KC; ++c) load(2 * D + x.h * kLD, row0 + c * 128);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id1 = idesc_l(128, 0);   // S_c = Q K_c^T: N = 128 keys
+      constexpr uint32_t id2 = idesc_l(kLD, 1);   // O += P_c V_c: N = 64, V MN-major
+      uint32_t cnt = 0, g = 0, n = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++n) {
+        // TMEM (S chunks, O) free once the previous unit's epilogue read O
+        mbar_wait(t_free, (n & 1) ^ 1);
+        tc_fence_after();
+        const int qslot = cnt % kLSlots;
+        mbar_wait(full + qslot, (cnt / kLSlots) & 1);
+        ++cnt;
+        const uint64_t qd = make_sw128_desc(smem + SmemL::RING + qslot * kLTile);
+        for (int c = 0; c < KC; ++c) {
+          const int ks = cnt % kLSlots;
+          mbar_wait(full + ks, (cnt / kLSlots) & 1);
+          ++cnt;
+          tc_fence_after();
+          const uint64_t kd = make_sw128_desc(smem + SmemL::RING + ks * kLTile);
+#pragma unroll
+          for (int k = 0; k < kLD / 16; ++k) mma_f16(tmem + c * 128, qd + 2 * k, kd + 2 * k, id1, k != 0);
+          mma_commit(empty + ks);
+        }
+        mma_commit(empty + qslot);
+        mma_commit(s_full);
+        for (int c = 0; c < KC; ++c, ++g) {
+          const int vs = cnt % kLSlots;
+          mbar_wait(full + vs, (cnt / kLSlots) & 1);
+          ++cnt;
+          mbar_wait(p_full + (g & 1), (g >> 1) & 1);
+          tc_fence_after();
+          uint8_t* P = smem + SmemL::P + (g & 1) * 2 * kLTile;
+          uint8_t* V = smem + SmemL::RING + vs * kLTile;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint64_t pd = make_sw128_desc(P + (k >> 2) * kLTile) + 2 * (k & 3);
+            const uint64_t vd = sw128_desc_mn(V + k * 2048);
+            mma_f16(tmem + kO, pd, vd, id2, (c | k) != 0);
+          }
+          mma_commit(empty + vs);
+          mma_commit(p_empty + (g & 1));
+        }
+        mma_commit(o_full);
+      }
+    }
+  } else {
+    const int q = warp & 3;            // TMEM lane quadrant
+    const int half = (warp - 2) >> 2;  // keys [64 half, +64) of every chunk; O columns [32 half, +32)
+    const int r = q * 32 + lane;
+    const int tid = threadIdx.x - 64;
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+    float* redMax = sRed;
+    float* redSum = sRed + 2 * kLQ;
+    const int pair_bar = 2 + q;
+    auto pair_sync = [pair_bar]() { asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory"); };
+    auto soft_sync = []() { asm volatile("bar.sync 1, 256;" ::: "memory"); };
+    const float2 cd2 = make_float2(scale, scale);
+    const float2 l2e = make_float2(1.4426950408889634f, 1.4426950408889634f);
+    uint32_t g = 0, n = 0;
+    int prev_b = -1;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++n) {
+      const Unit x = unit_of(u, nqb, A);
+      if (x.b != prev_b) {  // key mask bias of the sequence (0 / -inf; keys >= S masked)
+        soft_sync();        // every thread finished reading the previous mask
+        for (int j = tid; j < KC * 128; j += kSoft)
+          sMask[j] = (j < S && __ldg(mask + (size_t)x.b * S + j) != 0) ? 0.0f : -INFINITY;
+        soft_sync();
+        prev_b = x.b;
+      }
+      mbar_wait(s_full, n & 1);
+      tc_fence_after();
+      // pass 1: row max of s = RN(raw * cd) + mask bias over this half of every chunk
+      float mx = -INFINITY;
+      for (int c = 0; c < KC; ++c) {
+        uint32_t raw[2][32];
+        tmem_ld32(trow + c * 128 + half * 64, raw[0]);
+        tmem_ld32(trow + c * 128 + half * 64 + 32, raw[1]);
+        tmem_wait_ld();
+        const float2* mk = reinterpret_cast<const float2*>(sMask + c * 128 + half * 64);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float2 s = fma2(make_float2(__uint_as_float(raw[j >> 4][(2 * j) & 31]),
+                                            __uint_as_float(raw[j >> 4][(2 * j + 1) & 31])),
+                                cd2, mk[j]);
+          mx = fmaxf(mx, fmaxf(s.x, s.y));
+        }
+      }
+      redMax[half * kLQ + r] = mx;
+      pair_sync();
+      mx = fmaxf(mx, redMax[(half ^ 1) * kLQ + r]);
+      const float2 mxv = make_float2(mx, mx);
+      // pass 2: e = exp(s - max) in fp32, written back over S; row sum
+      float2 la = make_float2(0.0f, 0.0f), lb = make_float2(0.0f, 0.0f);
+      for (int c = 0; c < KC; ++c) {
+        uint32_t raw[2][32];
+        tmem_ld32(trow + c * 128 + half * 64, raw[0]);
+        tmem_ld32(trow + c * 128 + half * 64 + 32, raw[1]);
+        tmem_wait_ld();
+        const float2* mk = reinterpret_cast<const float2*>(sMask + c * 128 + half * 64);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float2 s = fma2(make_float2(__uint_as_float(raw[j >> 4][(2 * j) & 31]),
+                                            __uint_as_float(raw[j >> 4][(2 * j + 1) & 31])),
+                                cd2, mk[j]);
+          const float2 t = mul2(sub2(s, mxv), l2e);
+          const float2 e = make_float2(ex2l(t.x), ex2l(t.y));
+          if (j & 1) lb = add2(lb, e);
+          else la = add2(la, e);
+          raw[j >> 4][(2 * j) & 31] = __float_as_uint(e.x);
+          raw[j >> 4][(2 * j + 1) & 31] = __float_as_uint(e.y);
+        }
+        tmem_st32(trow + c * 128 + half * 64, raw[0]);
+        tmem_st32(trow + c * 128 + half * 64 + 32, raw[1]);
+      }
+      tmem_wait_st();
+      const float2 l2 = add2(la, lb);
+      redSum[half * kLQ + r] = l2.x + l2.y;
+      pair_sync();
+      const float l = redSum[r] + redSum[kLQ + r];  // fixed order in both halves
+      const float rl = __frcp_rn(l);
+      const float2 lv = make_float2(l, l), rlv = make_float2(rl, rl);
+      // pass 3: P16 = R16(e / l) chunk by chunk into P[g & 1] (K-major, 128B
+      // swizzle: 16-byte chunk cc of row r at (cc ^ (r & 7)))
+      for (int c = 0; c < KC; ++c, ++g) {
+        uint32_t ev[2][32];
+        tmem_ld32(trow + c * 128 + half * 64, ev[0]);
+        tmem_ld32(trow + c * 128 + half * 64 + 32, ev[1]);
+        tmem_wait_ld();
+        mbar_wait(p_empty + (g & 1), ((g >> 1) & 1) ^ 1);  // P.V of chunk g - 2 has read the buffer
+        uint8_t* prow = smem + SmemL::P + (g & 1) * 2 * kLTile + half * kLTile + r * 128;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          uint32_t w[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int j = cc * 4 + i;
+            const float2 p = div2_cr(make_float2(__uint_as_float(ev[j >> 4][(2 * j) & 31]),
+                                                 __uint_as_float(ev[j >> 4][(2 * j + 1) & 31])),
+                                     lv, rlv);
+            w[i] = pack_half2(p.x, p.y);
+          }
+          *reinterpret_cast<uint4*>(prow + ((cc ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        tc_fence_before();
+        fence_async_smem();
+        mbar_arrive(p_full + (g & 1));
+      }
+      // epilogue: ctx = R16(O), fp16 rows; then TMEM is free for the next unit
+      mbar_wait(o_full, n & 1);
+      tc_fence_after();
+      uint32_t o[32];
+      tmem_ld32(trow + kO + half * 32, o);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(t_free);
+      const int qrow = x.qb * kLQ + r;
+      if (qrow < S) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pk[i] = pack_half2(__uint_as_float(o[2 * i]), __uint_as_float(o[2 * i + 1]));
+        uint4* dst = reinterpret_cast<uint4*>(ctx + ((size_t)x.b * S + qrow) * ldc + x.h * kLD + half * 32);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) dst[c] = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace
+
+bool attention_long_supported(int S, int d, int ldqkv, int ldctx) {
+  return d == kLD && S > 128 && S <= kLMaxKeys && (ldqkv % 8) == 0 && (ldctx % 8) == 0;
+}
+
+cudaError_t prepare_attention_long_kernel() {
+  cudaError_t e = cudaFuncSetAttribute(attention_long_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       SmemL::TOTAL);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(attention_long_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemL::TOTAL);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(attention_long_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemL::TOTAL);
+}
+
+cudaError_t launch_attention_long(const AttnTCPlan& plan, const int32_t* mask, int B, int S, int A, __half* ctx,
+                                  int ldctx, cudaStream_t s) {
+  if (S <= 128 || S > kLMaxKeys) return cudaErrorInvalidValue;
+  const float scale = (float)(1.0 / sqrt((double)kLD));  // fp32(1/sqrt(d)) (R10)
+  const int n_units = B * ((S + kLQ - 1) / kLQ) * A;
+  const int grid = n_units < kNumSMs ? n_units : kNumSMs;
+  const int kc = (S + 127) / 128;
+  if (kc == 2)
+    launch_ex(attention_long_kernel<2>, dim3(grid), dim3(kLThreads), SmemL::TOTAL, s, 0, plan.map, mask, B, S, A,
+              scale, ctx, ldctx);
+  else if (kc == 3)
+    launch_ex(attention_long_kernel<3>, dim3(grid), dim3(kLThreads), SmemL::TOTAL, s, 0, plan.map, mask, B, S, A,
+              scale, ctx, ldctx);
+  else
+    launch_ex(attention_long_kernel<4>, dim3(grid), dim3(kLThreads), SmemL::TOTAL, s, 0, plan.map, mask, B, S, A,
+              scale, ctx, ldctx);
+  return cudaGetLastError();
+}
+
+}  // namespace ff

@@ -36,8 +36,16 @@ namespace {
 
 constexpr int kQ = 128;             // queries per item (TMEM lanes)
 constexpr int kKeys = 128;          // keys (S <= 128)
-constexpr int kD = 64;              // head_dim
-constexpr int kMaxHeads = 8;        // heads per item
+constexpr int kD = 64;              // columns of a Q / K / V head tile (TMA box, 128B swizzle)
+// DP = head_dim padded to the MMA granularity: 64 (d in (32, 64]) or 32
+// (d <= 32, e.g. the TinyBERT shape's d = 26, DESIGN R18); an item holds up
+// to 512 / DP heads (their packed fp16 ctx fills the 256 parking columns).
+template <int DP>
+struct HeadCfg {
+  static constexpr int kMaxHeads = 512 / DP;
+  static constexpr int kHalf = DP / 2;         // O columns per half-row thread
+  static constexpr int kPark = DP / 2;         // parking columns per head (packed fp16 pairs)
+};
 constexpr int kTileBytes = 128 * 128;  // 128 rows x 128 B (64 fp16)
 constexpr int kKVStages = 3;
 constexpr int kSoftmaxWarps = 8;
@@ -85,6 +93,7 @@ __device__ __forceinline__ void softmax_sync() { asm volatile("bar.sync 1, 256;"
 
 // Walk of the heads one CTA processes: items blockIdx.x, +gridDim.x, ...;
 // each item = (sequence b, heads [h0, h0 + nh)).
+template <int MH>
 struct HeadIter {
   int item, hl, b, h0, nh;
   int n_items, n_groups, A, stride;
@@ -95,8 +104,8 @@ struct HeadIter {
   __device__ void set() {
     if (item < n_items) {
       b = item / n_groups;
-      h0 = (item - b * n_groups) * kMaxHeads;
-      nh = min(A, h0 + kMaxHeads) - h0;
+      h0 = (item - b * n_groups) * MH;
+      nh = min(A, h0 + MH) - h0;
     }
   }
   __device__ bool valid() const { return item < n_items; }
@@ -116,9 +125,10 @@ struct HeadIter {
 //   MMA:     .. S(n) | O(n-1) | S(n+1) | O(n) ..
 //   softmax: .. softmax(n) -> P[n&1] | epilogue(n-1) from O[(n-1)&1] | softmax(n+1) ..
 // Buffers: Q/K/V x3 stages (smem), S x1 (TMEM), P x2 (smem), O x2 (TMEM).
+template <int DP>
 __global__ void __launch_bounds__(kThreadsTC, 1)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const int32_t* __restrict__ mask, int B, int S,
-                        int A, float scale, __half* __restrict__ ctx, int ldc, int8_t* __restrict__ ctxq, int ldq,
+                        int A, int d, float scale, __half* __restrict__ ctx, int ldc, int8_t* __restrict__ ctxq, int ldq,
                         float* __restrict__ ctxs, const uint8_t* __restrict__ qkv_rows, int row_bytes,
                         unsigned long long* __restrict__ trace) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -136,8 +146,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   float* sRed = reinterpret_cast<float*>(smem + SmemTC::RED);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int D = A * kD;
-  const int n_groups = (A + kMaxHeads - 1) / kMaxHeads;
+  using HC = HeadCfg<DP>;
+  constexpr int MH = HC::kMaxHeads;
+  using Iter = HeadIter<MH>;
+  const int D = A * d;
+  const int n_groups = (A + MH - 1) / MH;
+  const bool manual = ((d * 2) & 15) != 0;  // head slices TMA cannot address (d = 26)
   const int n_items = B * n_groups;
   const int it_first = (int)blockIdx.x;
   const int it_stride = (int)gridDim.x;
@@ -145,7 +159,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmQKV);
     for (int i = 0; i < kKVStages; ++i) {
-      mbar_init(kv_full + i, 1);
+      mbar_init(kv_full + i, manual ? 32 : 1);  // manual copy: one arrival per producer lane
       mbar_init(kv_empty + i, 1);
     }
     mbar_init(s_full, 1);
@@ -169,70 +183,125 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   griddep_launch();
 
   if (warp == 0) {
-    if (lane == 0) {
+    if (manual) {
+      // head columns not 16-byte aligned (d = 26: head h starts at byte 52 h),
+      // which TMA cannot address: the whole warp copies each head's 32-column
+      // Q / K / V slices (4-byte cp.async) into the same 128B-swizzled tiles,
+      // zero-filling the columns >= d and the rows >= S
+      const int ldw = row_bytes / 4;  // QKV row pitch in 4-byte words
+      const uint32_t* src_w = reinterpret_cast<const uint32_t*>(qkv_rows);
+      uint32_t n = 0;
+      for (Iter it(it_first, n_items, n_groups, A, it_stride); it.valid(); it.next(), ++n) {
+        const int slot = n % kKVStages;
+        const int h = it.h0 + it.hl;
+        uint8_t* base = smem + slot * SmemTC::SLOT;
+        mbar_wait(kv_empty + slot, ((n / kKVStages) & 1) ^ 1);
+        if (lane == 0) trace_ev(trace, n, 0);
+#pragma unroll 1
+        for (int t = 0; t < 3; ++t) {
+          const int w0 = (t * D + h * d) >> 1;  // first word of the slice (d even)
+          uint8_t* tile = base + t * kTileBytes;
+          for (int idx = lane; idx < 128 * (DP / 2); idx += 32) {
+            const int rr = idx / (DP / 2), w = idx % (DP / 2);
+            const uint32_t dst = smem_u32(tile + rr * 128 + ((((w >> 2) ^ (rr & 7))) << 4) + (w & 3) * 4);
+            if (rr < S && 2 * w < d) {
+              const uint32_t* src = src_w + (size_t)(it.b * S + rr) * ldw + w0 + w;
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+            } else {
+              asm volatile("st.shared.b32 [%0], %1;" ::"r"(dst), "r"(0u) : "memory");
+            }
+          }
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        fence_async_smem();  // generic-proxy smem writes -> visible to the tensor cores
+        mbar_arrive(kv_full + slot);
+      }
+    } else if (lane == 0) {
       // (An L2 bulk prefetch of each item's QKV rows, meant to open each DRAM
       // page once per item, measured 5.5 us slower per C3 launch: the QKV
       // buffer was just written by the projection GEMM and is largely still
       // in L2, and the prefetch queued ahead of the first head's loads.)
-      (void)qkv_rows;
-      (void)row_bytes;
       uint32_t n = 0;
-      for (HeadIter it(it_first, n_items, n_groups, A, it_stride); it.valid(); it.next(), ++n) {
+      for (Iter it(it_first, n_items, n_groups, A, it_stride); it.valid(); it.next(), ++n) {
         const int slot = n % kKVStages;
         const int h = it.h0 + it.hl;
         uint8_t* base = smem + slot * SmemTC::SLOT;
         mbar_wait(kv_empty + slot, ((n / kKVStages) & 1) ^ 1);
         trace_ev(trace, n, 0);
         mbar_expect_tx(kv_full + slot, 3 * kTileBytes);
-        tma_load_2d(base, &tmQKV, kv_full + slot, h * kD, it.b * S, kEvictFirst);
-        tma_load_2d(base + kTileBytes, &tmQKV, kv_full + slot, D + h * kD, it.b * S, kEvictFirst);
-        tma_load_2d(base + 2 * kTileBytes, &tmQKV, kv_full + slot, 2 * D + h * kD, it.b * S, kEvictFirst);
+        tma_load_2d(base, &tmQKV, kv_full + slot, h * d, it.b * S, kEvictFirst);
+        tma_load_2d(base + kTileBytes, &tmQKV, kv_full + slot, D + h * d, it.b * S, kEvictFirst);
+        tma_load_2d(base + 2 * kTileBytes, &tmQKV, kv_full + slot, 2 * D + h * d, it.b * S, kEvictFirst);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    // all 32 lanes walk the schedule (they zero Q's padding columns when
+    // d < DP); lane 0 issues the MMAs and commits
+    {
+      const bool issuer = lane == 0;
       constexpr uint32_t id1 = idesc_f16(kKeys, 0);  // S = Q K^T: N = 128 keys
-      constexpr uint32_t id2 = idesc_f16(kD, 1);     // O = P V:   N = 64, V MN-major
+      constexpr uint32_t id2 = idesc_f16(DP, 1);     // O = P V:   N = DP, V MN-major
       auto issue_pv = [&](uint32_t m) {
         const int ps = m & 1;
         const int slot = m % kKVStages;
         mbar_wait(p_full + ps, (m >> 1) & 1);
-        trace_ev(trace, m, 5);
+        if (issuer) trace_ev(trace, m, 5);
         mbar_wait(o_empty + ps, ((m >> 1) & 1) ^ 1);
         tc_fence_after();
-        uint8_t* P = smem + SmemTC::P + ps * 2 * kTileBytes;
-        uint8_t* V = smem + slot * SmemTC::SLOT + 2 * kTileBytes;
+        if (issuer) {
+          uint8_t* P = smem + SmemTC::P + ps * 2 * kTileBytes;
+          uint8_t* V = smem + slot * SmemTC::SLOT + 2 * kTileBytes;
 #pragma unroll
-        for (int k = 0; k < kKeys / 16; ++k) {
-          // A = P: k-block k/4 (64 keys), +32 B per 16 keys inside the 128B row
-          const uint64_t pd = make_sw128_desc(P + (k >> 2) * kTileBytes) + 2 * (k & 3);
-          // B = V (MN-major): 16 keys = two 8-row groups = 2048 B
-          const uint64_t vd = make_sw128_desc_mn(V + k * 2048);
-          mma_f16(tmem + kTmemO + ps * kD, pd, vd, id2, k != 0);
+          for (int k = 0; k < kKeys / 16; ++k) {
+            // A = P: k-block k/4 (64 keys), +32 B per 16 keys inside the 128B row
+            const uint64_t pd = make_sw128_desc(P + (k >> 2) * kTileBytes) + 2 * (k & 3);
+            // B = V (MN-major): 16 keys = two 8-row groups = 2048 B
+            const uint64_t vd = make_sw128_desc_mn(V + k * 2048);
+            mma_f16(tmem + kTmemO + ps * 64, pd, vd, id2, k != 0);
+          }
+          mma_commit(o_full + ps);
+          mma_commit(kv_empty + slot);  // Q/K/V of head m free once these MMAs complete
         }
-        mma_commit(o_full + ps);
-        mma_commit(kv_empty + slot);  // Q/K/V of head m free once these MMAs complete
+        __syncwarp();
       };
       uint32_t n = 0;
-      for (HeadIter it(it_first, n_items, n_groups, A, it_stride); it.valid(); it.next(), ++n) {
+      for (Iter it(it_first, n_items, n_groups, A, it_stride); it.valid(); it.next(), ++n) {
         const int slot = n % kKVStages;
         uint8_t* base = smem + slot * SmemTC::SLOT;
         mbar_wait(kv_full + slot, (n / kKVStages) & 1);
-        trace_ev(trace, n, 1);
+        if (issuer) trace_ev(trace, n, 1);
+        if (d < DP && !manual) {
+          // head_dim below the MMA granularity (d = 16 by TMA): the box also
+          // holds the next head's first columns; zero Q's columns [d, DP) so
+          // they add nothing to Q.K^T (V's extra columns only reach O columns
+          // that are never stored); the manual copy (d = 26) zero-fills itself
+          for (int rr = lane; rr < 128; rr += 32)
+            for (int c = d; c < DP; ++c)
+              *reinterpret_cast<__half*>(base + rr * 128 + (((c >> 3) ^ (rr & 7)) << 4) + (c & 7) * 2) =
+                  __float2half_rn(0.0f);
+          fence_async_smem();
+          __syncwarp();
+        }
         mbar_wait(s_empty, (n & 1) ^ 1);
-        trace_ev(trace, n, 2);
-        tc_fence_after();
-        const uint64_t qd = make_sw128_desc(base), kd = make_sw128_desc(base + kTileBytes);
+        if (issuer) {
+          trace_ev(trace, n, 2);
+          tc_fence_after();
+          const uint64_t qd = make_sw128_desc(base), kd = make_sw128_desc(base + kTileBytes);
 #pragma unroll
-        for (int k = 0; k < kD / 16; ++k) mma_f16(tmem, qd + 2 * k, kd + 2 * k, id1, k != 0);
-        mma_commit(s_full);
+          for (int k = 0; k < DP / 16; ++k) mma_f16(tmem, qd + 2 * k, kd + 2 * k, id1, k != 0);
+          mma_commit(s_full);
+        }
+        __syncwarp();
         if (n > 0) issue_pv(n - 1);
       }
       if (n > 0) issue_pv(n - 1);
     }
   } else {
     const int q = warp & 3;             // TMEM lane quadrant
-    const int half = (warp - 2) >> 2;   // keys [64 half, 64 half + 64), O columns [32 half, 32 half + 32)
+    const int half = (warp - 2) >> 2;   // keys [64 half, 64 half + 64), O columns [DP/2 half, DP/2 half + DP/2)
+    constexpr int HW = HC::kHalf / 2;   // packed fp16 words of this thread's half-row of one head
+    // valid head_dim columns of this half (DP = 32, d = 26: 16 and 10)
+    const int vcols = min(max(d - half * HC::kHalf, 0), HC::kHalf);
     const int r = q * 32 + lane;
     const int tid = threadIdx.x - 64;
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
@@ -255,20 +324,29 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     int qb = 0, qhbase = 0;
     float qsc = 1.0f, qrs = 1.0f;
     auto flush_head = [&](int j) {  // quantize + store parked head j of the pending item
-      uint32_t v[16];
-      tmem_ld16(trow + kTmemCtx + j * 32 + half * 16, v);
+      uint32_t v[HW];
+      if constexpr (HW == 16) tmem_ld16(trow + kTmemCtx + j * HC::kPark + half * HW, v);
+      else tmem_ld8(trow + kTmemCtx + j * HC::kPark + half * HW, v);
       tmem_wait_ld();
-      uint32_t w[8];
+      uint32_t w[HW / 2];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < HW / 2; ++i) {
         const float2 a0 = __half22float2(*reinterpret_cast<const __half2*>(&v[2 * i]));
         const float2 a1 = __half22float2(*reinterpret_cast<const __half2*>(&v[2 * i + 1]));
         w[i] = q8_quant4(a0, a1, qsc, qrs);
       }
-      if (r < S) {  // this thread's 32 s8 values: one full 32-byte sector of the row
-        uint4* dst = reinterpret_cast<uint4*>(ctxq + ((size_t)qb * S + r) * ldq + (qhbase + j) * kD + half * 32);
-        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+      if (r < S) {
+        int8_t* row_q = ctxq + ((size_t)qb * S + r) * ldq + (qhbase + j) * d + half * HC::kHalf;
+        if (DP == 64 && d == 64) {  // this thread's 32 s8 values: one full 32-byte sector of the row
+          uint4* dst = reinterpret_cast<uint4*>(row_q);
+          dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+          dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        } else {  // d even: 2-byte aligned pieces of the vcols valid values
+#pragma unroll
+          for (int i = 0; i < HW; ++i)
+            if (2 * i < vcols)
+              *reinterpret_cast<uint16_t*>(row_q + 2 * i) = (uint16_t)(w[i >> 1] >> ((i & 1) * 16));
+        }
       }
     };
 
@@ -281,25 +359,35 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       mbar_wait(o_full + os, (m >> 1) & 1);
       if (threadIdx.x == 64) trace_ev(trace, m, 6);
       tc_fence_after();
-      uint32_t o[32];
-      tmem_ld32(trow + kTmemO + os * kD + half * 32, o);
+      uint32_t o[2 * HW];
+      if constexpr (HW == 16) tmem_ld32(trow + kTmemO + os * 64 + half * HC::kHalf, o);
+      else tmem_ld16(trow + kTmemO + os * 64 + half * HC::kHalf, o);
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(o_empty + os);
-      uint32_t pk[16];
+      uint32_t pk[HW];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        pk[i] = pack_half2(__uint_as_float(o[2 * i]), __uint_as_float(o[2 * i + 1]));
+      for (int i = 0; i < HW; ++i) {
+        // O columns >= d (DP = 32, d = 26) hold the next head's values: zero
+        pk[i] = 2 * i < vcols ? pack_half2(__uint_as_float(o[2 * i]), __uint_as_float(o[2 * i + 1])) : 0u;
         amax2 = __hmax2(amax2, __habs2(*reinterpret_cast<const __half2*>(&pk[i])));
       }
       if (ctx != nullptr && r < S) {
-        uint4* dst = reinterpret_cast<uint4*>(ctx + grow * ldc + h * kD + half * 32);
+        __half* row_c = ctx + grow * ldc + h * d + half * HC::kHalf;
+        if (DP == 64 && d == 64) {
+          uint4* dst = reinterpret_cast<uint4*>(row_c);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) dst[c] = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+          for (int c = 0; c < 4; ++c) dst[c] = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        } else {  // d even: 4-byte aligned pairs
+#pragma unroll
+          for (int i = 0; i < HW; ++i)
+            if (2 * i < vcols) *reinterpret_cast<uint32_t*>(row_c + 2 * i) = pk[i];
+        }
       }
       if (!fuse_q) return;
       if (qpend) flush_head(hl);  // frees parking slot hl (the load completed above)
-      tmem_st16(trow + kTmemCtx + hl * 32 + half * 16, pk);
+      if constexpr (HW == 16) tmem_st16(trow + kTmemCtx + hl * HC::kPark + half * HW, pk);
+      else tmem_st8(trow + kTmemCtx + hl * HC::kPark + half * HW, pk);
       if (!last) return;
       // row amax over both halves -> this item's row scale; its heads are
       // quantized by the next item's epilogues (or after the loop)
@@ -329,7 +417,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       return __ldg(mask + (size_t)(item / n_groups) * S + tid);
     };
     int mval = mask_of(it_first);
-    for (HeadIter it(it_first, n_items, n_groups, A, it_stride); it.valid(); it.next(), ++n) {
+    for (Iter it(it_first, n_items, n_groups, A, it_stride); it.valid(); it.next(), ++n) {
       if (it.hl == 0) {
         // every softmax thread finished reading the previous item's mask
         // before this barrier
@@ -426,10 +514,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 }  // namespace
 
 bool attention_tc_supported(int S, int d, int ldqkv, int ldctx) {
-  return d == kD && S >= 1 && S <= kKeys && (ldqkv % 8) == 0 && (ldctx % 8) == 0;
+  return d >= 16 && d <= 64 && (d % 2) == 0 && (d == 64 || d <= 32) && S >= 1 && S <= kKeys && (ldqkv % 8) == 0 &&
+         (ldctx % 8) == 0;
 }
 
-bool attention_tc_fuses_quant(int A) { return A >= 1 && A <= kMaxHeads; }
+bool attention_tc_fuses_quant(int A, int d) { return A >= 1 && A <= (d <= 32 ? 16 : 8); }
 
 bool plan_attention_tc(AttnTCPlan* plan, const void* qkv, int M_rows, int ldqkv, const char** err) {
   // [M_rows x ldqkv] fp16, 64-column x 128-row boxes, 128B swizzle
@@ -439,18 +528,26 @@ bool plan_attention_tc(AttnTCPlan* plan, const void* qkv, int M_rows, int ldqkv,
 }
 
 cudaError_t prepare_attention_tc_kernel() {
-  return cudaFuncSetAttribute(attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemTC::TOTAL);
+  cudaError_t e = cudaFuncSetAttribute(attention_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       SmemTC::TOTAL);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(attention_tc_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemTC::TOTAL);
 }
 
-cudaError_t launch_attention_tc(const AttnTCPlan& plan, const int32_t* mask, int B, int S, int A, __half* ctx,
+cudaError_t launch_attention_tc(const AttnTCPlan& plan, const int32_t* mask, int B, int S, int A, int d, __half* ctx,
                                 int ldctx, int8_t* ctxq, int ldq, float* ctxs, cudaStream_t s,
                                 unsigned long long* trace) {
-  if (ctxq != nullptr && !attention_tc_fuses_quant(A)) return cudaErrorInvalidValue;
-  const float scale = (float)(1.0 / sqrt((double)kD));
-  const int n_items = B * ((A + kMaxHeads - 1) / kMaxHeads);
+  if (ctxq != nullptr && !attention_tc_fuses_quant(A, d)) return cudaErrorInvalidValue;
+  const float scale = (float)(1.0 / sqrt((double)d));  // fp32(1/sqrt(d)) (R10)
+  const int mh = d <= 32 ? HeadCfg<32>::kMaxHeads : HeadCfg<64>::kMaxHeads;
+  const int n_items = B * ((A + mh - 1) / mh);
   const int grid = n_items < kNumSMs ? n_items : kNumSMs;
-  launch_ex(attention_tc_kernel, dim3(grid), dim3(kThreadsTC), SmemTC::TOTAL, s, 0, plan.map, mask, B, S, A, scale,
-            ctx, ldctx, ctxq, ldq, ctxs, static_cast<const uint8_t*>(plan.qkv), plan.ldqkv * 2, trace);
+  if (d <= 32)
+    launch_ex(attention_tc_kernel<32>, dim3(grid), dim3(kThreadsTC), SmemTC::TOTAL, s, 0, plan.map, mask, B, S, A, d,
+              scale, ctx, ldctx, ctxq, ldq, ctxs, static_cast<const uint8_t*>(plan.qkv), plan.ldqkv * 2, trace);
+  else
+    launch_ex(attention_tc_kernel<64>, dim3(grid), dim3(kThreadsTC), SmemTC::TOTAL, s, 0, plan.map, mask, B, S, A, d,
+              scale, ctx, ldctx, ctxq, ldq, ctxs, static_cast<const uint8_t*>(plan.qkv), plan.ldqkv * 2, trace);
   return cudaGetLastError();
 }
 

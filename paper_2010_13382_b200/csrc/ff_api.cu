@@ -98,8 +98,8 @@ struct ff_model {
   bool use_graphs = true;
   int pair_mode = -1;  // FF_OPT_CTA_PAIRS: -1 auto, 0 never (GemmPlan::force_pair)
   bool attn_tc = true;  // FF_OPT_ATTN_TC: tcgen05 attention where supported
-  int fused = 2;  // FF_OPT_FUSED_EPILOGUES / _MASK: cluster row-reduction GEMM epilogues,
-                 // bit 0 out-proj + LN1, bit 1 FFN1 + requant (default), bit 2 FFN2 + LN2
+  int fused = 7;  // FF_OPT_FUSED_EPILOGUES / _MASK: cluster row-reduction GEMM epilogues,
+                 // bit 0 out-proj + LN1, bit 1 FFN1 + requant, bit 2 FFN2 + LN2 (default: all)
   int act_quant = 0;    // FF_OPT_ACT_QUANT: 0 per-row s8, 1 per-tensor u8 + zero point
   ff::LaunchPolicy launch{true, false};  // FF_OPT_PDL / FF_OPT_PDL_RR of this model's forwards
   ff::AttnTCPlan tm_qkv;  // QKV buffer map for the tcgen05 attention
@@ -333,7 +333,7 @@ ff_status dump(void* dst, const void* src, int ld_elems, int cols, int M, cudaSt
 // int8 layer whose ctx requant (a4) runs inside the tcgen05 attention kernel.
 bool attention_fuses_quant(const ff_model* m, const LayerPlan& P, int S) {
   return P.dt == FF_I8 && m->attn_tc && ff::attention_tc_supported(S, m->cfg.head_dim, m->ldqkv, m->ldc16) &&
-         ff::attention_tc_fuses_quant(P.A);
+         ff::attention_tc_fuses_quant(P.A, m->cfg.head_dim);
 }
 
 // ff_debug_set_trace: timeline buffer and target (0 debug GEMMs; 1 / 2 / 3 the
@@ -405,9 +405,12 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     const bool att_q = attention_fuses_quant(m, P, S) && !pt;
     if (m->attn_tc && ff::attention_tc_supported(S, c.head_dim, m->ldqkv, m->ldc16))
       FF_LAUNCH(FF_K_ATTENTION,
-                ff::launch_attention_tc(m->tm_qkv, mask, B, S, P.A, (att_q && !tr) ? nullptr : CTX, m->ldc16,
+                ff::launch_attention_tc(m->tm_qkv, mask, B, S, P.A, c.head_dim, (att_q && !tr) ? nullptr : CTX, m->ldc16,
                                         att_q ? CTXq : nullptr, m->ldc8, att_q ? CTXs : nullptr, s),
                 "attention_tc");
+    else if (m->attn_tc && ff::attention_long_supported(S, c.head_dim, m->ldqkv, m->ldc16))
+      FF_LAUNCH(FF_K_ATTENTION, ff::launch_attention_long(m->tm_qkv, mask, B, S, P.A, CTX, m->ldc16, s),
+                "attention_long");
     else
       FF_LAUNCH(FF_K_ATTENTION, ff::launch_attention(QKV, m->ldqkv, mask, B, S, P.A, c.head_dim, CTX, m->ldc16, s),
                 "attention");
@@ -753,6 +756,7 @@ ff_status ff_finalize(ff_model* m, void* stream) {
   FF_CK(ff::prepare_gemm_kernels());
   FF_CK(ff::prepare_attention_kernels());
   FF_CK(ff::prepare_attention_tc_kernel());
+  FF_CK(ff::prepare_attention_long_kernel());
   FF_CK(ff::prepare_rr_kernels());
   FF_CK(ff::prepare_row_kernels());
   for (LayerPlan& P : m->L)  // zero-point corrections of the per-tensor u8 mode (DESIGN R22)
@@ -1071,19 +1075,27 @@ ff_status ff_debug_attention(const void* d_qkv16, const int32_t* d_mask, int32_t
   if (!prepared) {
     FF_CK(ff::prepare_attention_kernels());
     FF_CK(ff::prepare_attention_tc_kernel());
+    FF_CK(ff::prepare_attention_long_kernel());
     prepared = true;
   }
   const int mode = impl;  // 0 auto (tcgen05 where supported), 1 mma.sync kernel, 2 tcgen05 (must be supported)
-  const bool tc = mode != 1 && ff::attention_tc_supported(S, d, 3 * A * d, A * d) &&
-                  (reinterpret_cast<uintptr_t>(d_qkv16) & 15) == 0;
-  if (mode == 2 && !tc) return fail(FF_E_UNSUPPORTED, "tcgen05 attention needs head_dim 64, S <= 128");
-  if (tc) {
+  const bool aligned = (reinterpret_cast<uintptr_t>(d_qkv16) & 15) == 0;
+  const bool tc = mode != 1 && aligned && ff::attention_tc_supported(S, d, 3 * A * d, A * d);
+  const bool tcl = mode != 1 && aligned && !tc && ff::attention_long_supported(S, d, 3 * A * d, A * d);
+  if (mode == 2 && !tc && !tcl)
+    return fail(FF_E_UNSUPPORTED,
+                "tcgen05 attention needs head_dim 64 (S <= 512) or an even head_dim <= 32 (S <= 128)");
+  if (tc || tcl) {
     ff::AttnTCPlan map;
     const char* err = nullptr;
     if (!ff::plan_attention_tc(&map, d_qkv16, B * S, 3 * A * d, &err))
       return fail(FF_E_INVALID, std::string("attention tensor map: ") + err);
-    FF_CK(ff::launch_attention_tc(map, d_mask, B, S, A, static_cast<__half*>(d_ctx16), A * d, nullptr, 0, nullptr,
-                                  static_cast<cudaStream_t>(stream)));
+    if (tc)
+      FF_CK(ff::launch_attention_tc(map, d_mask, B, S, A, d, static_cast<__half*>(d_ctx16), A * d, nullptr, 0,
+                                    nullptr, static_cast<cudaStream_t>(stream)));
+    else
+      FF_CK(ff::launch_attention_long(map, d_mask, B, S, A, static_cast<__half*>(d_ctx16), A * d,
+                                      static_cast<cudaStream_t>(stream)));
     return FF_OK;
   }
   FF_CK(ff::launch_attention(static_cast<const __half*>(d_qkv16), 3 * A * d, d_mask, B, S, A, d,
@@ -1095,19 +1107,20 @@ ff_status ff_debug_attention_q8(const void* d_qkv16, const int32_t* d_mask, int3
                                 int32_t d, void* d_ctx16, int8_t* d_ctxq, float* d_ctxs, uint64_t* d_trace,
                                 void* stream) {
   if (B < 1 || S < 1 || A < 1 || !d_ctxq || !d_ctxs) return fail(FF_E_INVALID, "bad attention args");
-  if (!ff::attention_tc_supported(S, d, 3 * A * d, A * d) || !ff::attention_tc_fuses_quant(A) ||
+  if (!ff::attention_tc_supported(S, d, 3 * A * d, A * d) || !ff::attention_tc_fuses_quant(A, d) ||
       (reinterpret_cast<uintptr_t>(d_qkv16) & 15) != 0 || (A * d) % 16 != 0)
-    return fail(FF_E_UNSUPPORTED, "fused attention + requant needs head_dim 64, S <= 128, A <= 8");
+    return fail(FF_E_UNSUPPORTED, "fused attention + requant needs head_dim 64 (A <= 8) or an even head_dim <= 32 (A <= 16), S <= 128");
   static bool prepared = false;
   if (!prepared) {
     FF_CK(ff::prepare_attention_tc_kernel());
+    FF_CK(ff::prepare_attention_long_kernel());
     prepared = true;
   }
   ff::AttnTCPlan map;
   const char* err = nullptr;
   if (!ff::plan_attention_tc(&map, d_qkv16, B * S, 3 * A * d, &err))
     return fail(FF_E_INVALID, std::string("attention tensor map: ") + err);
-  FF_CK(ff::launch_attention_tc(map, d_mask, B, S, A, static_cast<__half*>(d_ctx16), A * d, d_ctxq, A * d, d_ctxs,
+  FF_CK(ff::launch_attention_tc(map, d_mask, B, S, A, d, static_cast<__half*>(d_ctx16), A * d, d_ctxq, A * d, d_ctxs,
                                 static_cast<cudaStream_t>(stream),
                                 reinterpret_cast<unsigned long long*>(d_trace)));
   return FF_OK;

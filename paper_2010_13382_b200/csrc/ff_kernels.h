@@ -186,22 +186,29 @@ size_t attention_smem_bytes(int S, int d);
 cudaError_t launch_attention(const __half* qkv, int ldqkv, const int32_t* mask, int B, int S, int A, int d,
                              __half* ctx, int ldctx, cudaStream_t s);
 
-// tcgen05 attention (head_dim 64, S <= 128); the tensor map covers the QKV
+// tcgen05 attention (head_dim 64 or <= 32 even -- padded to 32 --, S <= 128); the tensor map covers the QKV
 // buffer [M_rows x ldqkv] fp16 with 64-column x 128-row boxes.  Writes the
 // fp16 ctx rows when ctx != null and, when ctxq != null (requires
-// attention_tc_fuses_quant(A)), the Q8row s8 ctx rows + per-row scales.
+// attention_tc_fuses_quant(A, d)), the Q8row s8 ctx rows + per-row scales.
 bool attention_tc_supported(int S, int d, int ldqkv, int ldctx);
-bool attention_tc_fuses_quant(int A);
+bool attention_tc_fuses_quant(int A, int d);
 struct AttnTCPlan {
   CUtensorMap map;
   const void* qkv;  // QKV rows (contiguous: ldqkv fp16 per row)
   int ldqkv;
 };
 bool plan_attention_tc(AttnTCPlan* plan, const void* qkv, int M_rows, int ldqkv, const char** err);
-cudaError_t launch_attention_tc(const AttnTCPlan& plan, const int32_t* mask, int B, int S, int A, __half* ctx,
+cudaError_t launch_attention_tc(const AttnTCPlan& plan, const int32_t* mask, int B, int S, int A, int d, __half* ctx,
                                 int ldctx, int8_t* ctxq, int ldq, float* ctxs, cudaStream_t s,
                                 unsigned long long* trace = nullptr);
 cudaError_t prepare_attention_tc_kernel();
+
+// tcgen05 attention for 128 < S <= 512, head_dim 64 (attention_long.cu): fp16
+// ctx rows [B*S, ldctx]; the same QKV tensor map as attention_tc.
+bool attention_long_supported(int S, int d, int ldqkv, int ldctx);
+cudaError_t launch_attention_long(const AttnTCPlan& plan, const int32_t* mask, int B, int S, int A, __half* ctx,
+                                  int ldctx, cudaStream_t s);
+cudaError_t prepare_attention_long_kernel();
 
 // ------------------------------------------------------- weight packing
 cudaError_t launch_cast_f16(const float* src, int N, int K, __half* dst, int ldd, cudaStream_t s);

@@ -117,10 +117,14 @@ __device__ __forceinline__ float gelu_expo(float s) {
   return s <= kGeluFast ? s * p7 : sc * p11;
 }
 
+// GELU(y) from a = s * P(s): with e = 2^-a and h = y / 2, y < 0 -> h * e and
+// y >= 0 -> y - h * e, both as one FMA fma(h, +-e, y or 0) (the sign and the
+// addend are selected on the ALU pipe).
 __device__ __forceinline__ float gelu_from_expo(float y, float a) {
   float e;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-a));
-  return (0.5f * y) * (y >= 0.0f ? 2.0f - e : e);
+  const bool neg = y < 0.0f;
+  return __fmaf_rn(0.5f * y, neg ? e : -e, neg ? 0.0f : y);
 }
 
 template <int ACT>
@@ -160,9 +164,9 @@ __device__ __forceinline__ void gelu16x2(float2 (&v)[16]) {
     float2 ex;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ex.x) : "f"(-a.x));
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ex.y) : "f"(-a.y));
-    const float2 t = sub2(make_float2(2.0f, 2.0f), ex);
-    const float2 sel = make_float2(v[e].x >= 0.0f ? t.x : ex.x, v[e].y >= 0.0f ? t.y : ex.y);
-    v[e] = mul2(mul2(v[e], make_float2(0.5f, 0.5f)), sel);
+    const bool nx = v[e].x < 0.0f, ny = v[e].y < 0.0f;
+    v[e] = fma2(mul2(v[e], make_float2(0.5f, 0.5f)), make_float2(nx ? ex.x : -ex.x, ny ? ex.y : -ex.y),
+                make_float2(nx ? 0.0f : v[e].x, ny ? 0.0f : v[e].y));
   }
 }
 
@@ -517,14 +521,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 // 128x256 tile per CTA; CTA `rank` always owns columns [256 rank, +256), so
 // its bias / column scales / LN gamma, beta are staged in smem once).
 // Same producer / MMA roles as gemm_tc_kernel (single-CTA MMA, 3 smem
-// stages, double-buffered TMEM accumulator); 16 epilogue warps, warp (q, g)
-// owning rows [32q, 32q+32) x columns [64g, 64g+64) of the tile.  Passes over
-// the accumulator keep intermediates in TMEM (tcgen05.st).  Row statistics:
-// the 4 column-group partials of a row are combined inside the CTA (smem,
-// one warp per quadrant), the CTA partial is bulk-copied into every CTA of
-// the cluster (cp.async.bulk.shared::cluster, completion on an mbarrier armed
-// with the expected bytes), and every CTA combines the CN partials in the
-// same fixed order, so all derive bit-identical statistics.
+// stages, double-buffered TMEM accumulator).  The 16 epilogue warps form TWO
+// groups of 8 that ping-pong: group G drains accumulator buffer G, i.e. every
+// other tile, so one group's cluster exchanges, barriers and store waits
+// overlap the other group's arithmetic (the epilogue is FMA-pipe and
+// latency bound, not TMEM bound: tcgen05.ld reads ~900 B/clk/SM,
+// tools/micro/tmem_bw.cu).  In a group, warp (q, hc) owns rows [32q, +32) x
+// columns [128hc, +128) of the tile, in 4 chunks of 32; intermediates stay in
+// the group's own accumulator columns (x as fp32, then the packed fp16
+// results), which are released to the MMA warp after the last pass.  Row
+// statistics: the 2 column-half partials of a row are combined inside the
+// CTA (smem, 64-thread named barrier per quadrant), the CTA partial is
+// bulk-copied into every CTA of the cluster (cp.async.bulk.shared::cluster,
+// completion on an mbarrier armed with the expected bytes), and every CTA
+// combines the CN partials in the same fixed order, so all derive
+// bit-identical statistics.  Exchange buffers are per group (x2 in flight).
 //   RR_LN:    x = R16(dequant(acc) + bias) + residual (R11); LN over the row
 //             (per-thread two-pass mean / M2, Chan combination); y16 = R16(LN)
 //             -> fp16 rows (TMA) [+ Q8row s8 rows + scale]
@@ -534,16 +545,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 constexpr int kRRStages = 3;
 constexpr int kRRBN = 256;
 constexpr int kRRMaxCN = 8;
+constexpr int kRRGroupWarps = kRREpiWarps / 2;  // 8 warps per ping-pong group
 struct RRCfg {
   static constexpr int A_BYTES = BM * BK_BYTES;
   static constexpr int B_BYTES = kRRBN * BK_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_OFF = kRRStages * STAGE_BYTES;                 // staging [warp] 2 KB
   static constexpr int PAR_OFF = EPI_OFF + kRREpiWarps * kRRStageTile;    // [bias|sw|gamma|beta][256] fp32
-  static constexpr int LOC_OFF = PAR_OFF + 4 * kRRBN * 4;                 // [g 4][q 4][v 2][32] fp32
-  static constexpr int MYP_OFF = LOC_OFF + 4 * 4 * 2 * 32 * 4;            // [b 2][q 4][v 2][32] fp32
-  static constexpr int RED_OFF = MYP_OFF + 2 * 4 * 2 * 32 * 4;            // [b 2][rank 8][q 4][v 2][32] fp32
-  static constexpr int BAR_OFF = RED_OFF + 2 * kRRMaxCN * 4 * 2 * 32 * 4;
+  static constexpr int LOC_OFF = PAR_OFF + 4 * kRRBN * 4;                 // [G 2][hc 2][q 4][v 2][32] fp32
+  static constexpr int MYP_OFF = LOC_OFF + 2 * 2 * 4 * 2 * 32 * 4;        // [b 4][q 4][v 2][32] fp32
+  static constexpr int RED_OFF = MYP_OFF + 4 * 4 * 2 * 32 * 4;            // [b 4][rank 8][q 4][v 2][32] fp32
+  static constexpr int BAR_OFF = RED_OFF + 4 * kRRMaxCN * 4 * 2 * 32 * 4;
   static constexpr int SMEM = BAR_OFF + 512 + 1024;
   static_assert(SMEM <= 227 * 1024, "smem budget");
 };
@@ -563,8 +575,8 @@ __global__ void __launch_bounds__(kRRThreads, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* redbar = tempty + 2;
-  uint64_t* resbar = redbar + 2;  // [kRREpiWarps] per-warp residual TMA loads
+  uint64_t* redbar = tempty + 2;  // [4] = [group][exchange parity]
+  uint64_t* resbar = redbar + 4;  // [kRREpiWarps] per-warp residual TMA loads
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(resbar + kRREpiWarps);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -584,9 +596,9 @@ __global__ void __launch_bounds__(kRRThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kRREpiWarps);
-      mbar_init(&redbar[a], 1);
+      mbar_init(&tempty[a], kRRGroupWarps);  // the 8 warps of the group draining buffer a
     }
+    for (int b = 0; b < 4; ++b) mbar_init(&redbar[b], 1);
     for (int w = 0; w < kRREpiWarps; ++w) mbar_init(&resbar[w], 1);
     fence_barrier_init();
   }
@@ -660,9 +672,10 @@ __global__ void __launch_bounds__(kRRThreads, 1)
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;
-    const int q = warp & 3;        // TMEM lane quadrant: rows [32q, 32q+32)
-    const int g = ew >> 2;         // column group: [64g, 64g+64) of the CTA's 256
-    const int c_lo = g * 64;
+    const int G = ew / kRRGroupWarps;          // ping-pong group: accumulator buffer G, local tiles lt % 2 == G
+    const int q = warp & 3;                    // TMEM lane quadrant: rows [32q, 32q+32)
+    const int hc = (ew % kRRGroupWarps) >> 2;  // column half: [128hc, 128hc+128) of the CTA's 256
+    const int c_lo = hc * 128;
     const int ncol0 = (int)rank * BN;
     float* par = reinterpret_cast<float*>(smem + RRCfg::PAR_OFF);
     float* loc = reinterpret_cast<float*>(smem + RRCfg::LOC_OFF);
@@ -680,30 +693,30 @@ __global__ void __launch_bounds__(kRRThreads, 1)
     const float* psw = par + BN + c_lo;
     const float* pgam = par + 2 * BN + c_lo;
     const float* pbet = par + 3 * BN + c_lo;
+    const int qbar = 2 + G * 4 + q;  // named barrier of the group's two warps on quadrant q
 
-    int step = 0;  // exchange counter (buffer b = step & 1, phase (step >> 1) & 1)
-    // Row combine of nv per-thread values: in-CTA over the 4 column groups,
-    // then across the cluster.  STATS: (mean, M2) of 64 values each -> (mean,
-    // M2) of the full row; MAX: max.  Every thread returns the row result.
+    int step = 0;  // this group's exchange counter (buffer 2G + (step & 1), phase (step >> 1) & 1)
+    // Row combine of per-thread values: in-CTA over the 2 column halves, then
+    // across the cluster.  STATS: (mean, M2) of 128 values each -> (mean, M2)
+    // of the full row; MAX: max.  Every thread returns the row result.
     auto exchange = [&](float v0, float v1, bool stats, float& o0, float& o1) {
       const int nv = stats ? 2 : 1;
-      const int b = step & 1;
+      const int b = 2 * G + (step & 1);
       const uint32_t ph = (uint32_t)(step >> 1) & 1u;
-      loc[((g * 4 + q) * 2 + 0) * 32 + lane] = v0;
-      if (stats) loc[((g * 4 + q) * 2 + 1) * 32 + lane] = v1;
-      asm volatile("bar.sync %0, 128;" ::"r"(2 + q) : "memory");
-      if (g == 0) {
+      float* lg = loc + G * (2 * 4 * 2 * 32);
+      lg[((hc * 4 + q) * 2 + 0) * 32 + lane] = v0;
+      if (stats) lg[((hc * 4 + q) * 2 + 1) * 32 + lane] = v1;
+      asm volatile("bar.sync %0, 64;" ::"r"(qbar) : "memory");
+      if (hc == 0) {
         float r0, r1 = 0.0f;
-        const float a0 = loc[((0 * 4 + q) * 2) * 32 + lane], a1 = loc[((1 * 4 + q) * 2) * 32 + lane];
-        const float a2 = loc[((2 * 4 + q) * 2) * 32 + lane], a3 = loc[((3 * 4 + q) * 2) * 32 + lane];
+        const float a0 = lg[((0 * 4 + q) * 2) * 32 + lane], a1 = lg[((1 * 4 + q) * 2) * 32 + lane];
         if (stats) {
-          r0 = ((a0 + a1) + (a2 + a3)) * 0.25f;
-          const float d0 = a0 - r0, d1 = a1 - r0, d2 = a2 - r0, d3 = a3 - r0;
-          const float m0 = loc[((0 * 4 + q) * 2 + 1) * 32 + lane], m1 = loc[((1 * 4 + q) * 2 + 1) * 32 + lane];
-          const float m2 = loc[((2 * 4 + q) * 2 + 1) * 32 + lane], m3 = loc[((3 * 4 + q) * 2 + 1) * 32 + lane];
-          r1 = ((m0 + m1) + (m2 + m3)) + 64.0f * ((d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3));
+          r0 = (a0 + a1) * 0.5f;
+          const float d0 = a0 - r0, d1 = a1 - r0;
+          const float m0 = lg[((0 * 4 + q) * 2 + 1) * 32 + lane], m1 = lg[((1 * 4 + q) * 2 + 1) * 32 + lane];
+          r1 = (m0 + m1) + 128.0f * (d0 * d0 + d1 * d1);
         } else {
-          r0 = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
+          r0 = fmaxf(a0, a1);
         }
         float* mine = myp + ((b * 4 + q) * 2) * 32;
         mine[lane] = r0;
@@ -711,6 +724,7 @@ __global__ void __launch_bounds__(kRRThreads, 1)
         fence_async_smem();
         __syncwarp();
         if (lane == 0) {
+          // 4 quadrant copies of nv x 128 B from each of the CN CTAs
           if (q == 0) mbar_expect_tx(&redbar[b], (uint32_t)(CN * 4 * nv * 128));
           const uint32_t dst = smem_u32(red + (((b * kRRMaxCN + (int)rank) * 4 + q) * 2) * 32);
           const uint32_t bl = smem_u32(&redbar[b]);
@@ -757,23 +771,29 @@ __global__ void __launch_bounds__(kRRThreads, 1)
       }
     };
 
-    int acc = 0;
+    const int acc = G;
     uint32_t acc_phase = 0;
-    int lt = 0;
     uint32_t rphase = 0;  // resbar[ew] phase
     const bool tr0 = ew == 0 && lane == 0;
-    for (int mt = unit; mt < p.m_tiles; mt += nunits, ++lt) {
+    int lt = G;
+    for (int mt = unit + G * nunits; mt < p.m_tiles; mt += 2 * nunits, lt += 2) {
       const int row0 = mt * BM + q * 32;
       const int row = row0 + lane;
       const bool row_ok = row < p.M;
       const float sx = (I8 && row_ok) ? p.row_scale[row] : 0.0f;
       const float2 sx2 = make_float2(sx, sx);
       if (MODE == RR_LN) {
-        // residual of the NEXT tile -> L2 (its TMA loads then hit L2, not
-        // HBM); this thread's 128 bytes of its row = one line
-        const int nrow = row + nunits * BM;
-        if (nrow < p.M) prefetch_l2(p.residual + (size_t)nrow * p.ldr + ncol0 + c_lo);
-        if (mt == unit && row_ok) prefetch_l2(p.residual + (size_t)row * p.ldr + ncol0 + c_lo);
+        // residual of this group's NEXT tile -> L2 (its TMA loads then hit
+        // L2, not HBM): this thread's 256 bytes of its row
+        const int nrow = row + 2 * nunits * BM;
+        if (nrow < p.M) {
+          prefetch_l2(p.residual + (size_t)nrow * p.ldr + ncol0 + c_lo);
+          prefetch_l2(p.residual + (size_t)nrow * p.ldr + ncol0 + c_lo + 64);
+        }
+        if (lt < 2 && row_ok) {
+          prefetch_l2(p.residual + (size_t)row * p.ldr + ncol0 + c_lo);
+          prefetch_l2(p.residual + (size_t)row * p.ldr + ncol0 + c_lo + 64);
+        }
         // residual block of chunk 0 -> the warp's staging buffer, in flight
         // while the accumulator is still being computed
         if (lane == 0) {
@@ -788,21 +808,18 @@ __global__ void __launch_bounds__(kRRThreads, 1)
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c_lo;
       __half2 amax2 = __float2half2_rn(0.0f);
 
-      // TMEM reads are the scarce resource here (64 B/clk/SM: every pass over
-      // the 128 KB accumulator costs ~1 us): the accumulator is read once,
-      // x is written back (tcgen05.st, 4x faster than reads) and read once
-      // more for the LN pass; the packed fp16 results stay in registers
-      // across the amax exchange.
-      uint32_t hq[32];  // this thread's 64 output values, packed fp16 (Q8row input)
+      // The packed fp16 results of chunk ch are parked in the group's own
+      // accumulator columns [16 ch, 16 ch + 16) of the warp's range, which
+      // chunk 0 has already been read from.
       if (MODE == RR_LN) {
-        // pass 1: x = R16(dequant + bias) + residual (registers); shifted
-        // sums (shift = the thread's first x) for the local mean / M2.  The
-        // residual block (32 rows x 32 columns fp16) arrives by TMA in the
-        // warp's staging buffer (64B swizzle); each thread reads its row.
+        // pass 1: x = R16(dequant + bias) + residual (written back over the
+        // accumulator); shifted sums (shift = the thread's first x) for the
+        // local mean / M2.  The residual block (32 rows x 32 columns fp16)
+        // arrives by TMA in the warp's staging buffer (64B swizzle).
         float2 sd = make_float2(0.0f, 0.0f), sq = make_float2(0.0f, 0.0f);
         float2 shift = make_float2(0.0f, 0.0f);
-#pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
+#pragma unroll 1
+        for (int ch = 0; ch < 4; ++ch) {
           uint32_t r[32];
           tmem_ld32(tbase + ch * 32, r);
           mbar_wait(&resbar[ew], (uint32_t)(rphase & 1));
@@ -812,21 +829,22 @@ __global__ void __launch_bounds__(kRRThreads, 1)
           for (int cc = 0; cc < 4; ++cc)
             rv[cc] = *reinterpret_cast<const uint4*>(stage_buf + lane * 64 + ((cc ^ ((lane >> 1) & 3)) << 4));
           __syncwarp();  // every lane has read the block before it is reused
-          if (ch == 0 && lane == 0) {  // chunk 1's residual block, overlapping chunk 0's math
+          if (ch < 3 && lane == 0) {  // the next chunk's residual block, overlapping this chunk's math
             mbar_expect_tx(&resbar[ew], 32 * 64);
-            tma_load_2d(stage_buf, &tmR, &resbar[ew], ncol0 + c_lo + 32, row0, kEvictFirst);
+            tma_load_2d(stage_buf, &tmR, &resbar[ew], ncol0 + c_lo + 32 * (ch + 1), row0, kEvictFirst);
           }
           tmem_wait_ld();
           const __half2* rh = reinterpret_cast<const __half2*>(rv);
+          const float* pb = pbias + ch * 32;
+          const float* ps = psw + ch * 32;
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
-            const int j = ch * 32 + 2 * e;
-            const float2 bb = *reinterpret_cast<const float2*>(pbias + j);
+            const float2 bb = *reinterpret_cast<const float2*>(pb + 2 * e);
             float2 y;
             if (I8) {
               const float2 a = make_float2(__int2float_rn(static_cast<int>(r[2 * e])),
                                            __int2float_rn(static_cast<int>(r[2 * e + 1])));
-              y = fma2(a, mul2(sx2, *reinterpret_cast<const float2*>(psw + j)), bb);
+              y = fma2(a, mul2(sx2, *reinterpret_cast<const float2*>(ps + 2 * e)), bb);
             } else {
               y = add2(make_float2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])), bb);
             }
@@ -843,8 +861,8 @@ __global__ void __launch_bounds__(kRRThreads, 1)
         }
         tmem_wait_st();
         const float sdt = sd.x + sd.y;
-        const float mean_t = shift.x + sdt * (1.0f / 64.0f);
-        const float m2_t = fmaxf((sq.x + sq.y) - sdt * sdt * (1.0f / 64.0f), 0.0f);
+        const float mean_t = shift.x + sdt * (1.0f / 128.0f);
+        const float m2_t = fmaxf((sq.x + sq.y) - sdt * sdt * (1.0f / 128.0f), 0.0f);
         float mean, m2;
         if (tr0) gemm_trace(p.trace, lt, 8);
         exchange(mean_t, m2_t, true, mean, m2);
@@ -852,46 +870,34 @@ __global__ void __launch_bounds__(kRRThreads, 1)
         const float var = __fdiv_rn(m2, (float)p.N);
         const float rstd = 1.0f / sqrtf(var + p.eps);
         const float2 mean2 = make_float2(mean, mean), rstd2 = make_float2(rstd, rstd);
-        // pass 2: y16 = R16((x - mean) * rstd * gamma + beta) -> fp16 store, amax
-#pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
+        // pass 2: y16 = R16((x - mean) * rstd * gamma + beta) -> fp16 store, amax, park
+#pragma unroll 1
+        for (int ch = 0; ch < 4; ++ch) {
           uint32_t r[32];
           tmem_ld32(tbase + ch * 32, r);
           tmem_wait_ld();
-          if (ch == 1) {  // the accumulator columns have been read for the last time
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
-          }
+          uint32_t h[16];
+          const float* pg = pgam + ch * 32;
+          const float* pt = pbet + ch * 32;
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
-            const int j = ch * 32 + 2 * e;
             const float2 d = sub2(make_float2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])), mean2);
-            const float2 y = fma2(mul2(d, rstd2), *reinterpret_cast<const float2*>(pgam + j),
-                                  *reinterpret_cast<const float2*>(pbet + j));
+            const float2 y = fma2(mul2(d, rstd2), *reinterpret_cast<const float2*>(pg + 2 * e),
+                                  *reinterpret_cast<const float2*>(pt + 2 * e));
             const __half2 hh = __floats2half2_rn(y.x, y.y);
             amax2 = __hmax2(amax2, __habs2(hh));
-            hq[ch * 16 + e] = *reinterpret_cast<const uint32_t*>(&hh);
+            h[e] = *reinterpret_cast<const uint32_t*>(&hh);
           }
-          if (p.store16) {
-            uint32_t h[16];
-#pragma unroll
-            for (int e = 0; e < 16; ++e) h[e] = hq[ch * 16 + e];
-            store16(h, ncol0 + c_lo + ch * 32, row0);
-          }
+          if (p.outq) tmem_st16(tbase + ch * 16, h);
+          if (p.store16) store16(h, ncol0 + c_lo + ch * 32, row0);
         }
-      } else {  // RR_QUANT: y16 = R16(act(dequant + bias)) (registers); amax
-#pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
+      } else {  // RR_QUANT: y16 = R16(act(dequant + bias)); amax; park
+#pragma unroll 1
+        for (int ch = 0; ch < 4; ++ch) {
           uint32_t r[2][16];
           tmem_ld16(tbase + ch * 32, r[0]);
           tmem_ld16(tbase + ch * 32 + 16, r[1]);
           tmem_wait_ld();
-          if (ch == 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
-          }
           uint32_t h[16];
           switch (p.act) {
             case ACT_GELU: epi32<I8, ACT_GELU>(r, pbias + ch * 32, psw + ch * 32, sx, h); break;
@@ -900,29 +906,37 @@ __global__ void __launch_bounds__(kRRThreads, 1)
             default: epi32<I8, ACT_NONE>(r, pbias + ch * 32, psw + ch * 32, sx, h); break;
           }
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            amax2 = __hmax2(amax2, __habs2(*reinterpret_cast<const __half2*>(&h[e])));
-            hq[ch * 16 + e] = h[e];
-          }
+          for (int e = 0; e < 16; ++e) amax2 = __hmax2(amax2, __habs2(*reinterpret_cast<const __half2*>(&h[e])));
+          if (p.outq) tmem_st16(tbase + ch * 16, h);
           if (p.store16) store16(h, ncol0 + c_lo + ch * 32, row0);
         }
       }
+      (void)sx2;
 
       if (tr0) gemm_trace(p.trace, lt, 10);
       if (p.outq) {
+        tmem_wait_st();
         // Q8row over the whole row (R6-R8, R12) from the fp16-rounded values
         float rmax, unused;
         exchange(fmaxf(__low2float(amax2), __high2float(amax2)), 0.0f, false, rmax, unused);
         if (tr0) gemm_trace(p.trace, lt, 11);
         const float sc = q8_scale(rmax);
         const float rs = __frcp_rn(sc);
-#pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
+#pragma unroll 1
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t hv[16];
+          tmem_ld16(tbase + ch * 16, hv);
+          tmem_wait_ld();
+          if (ch == 3) {  // the group's accumulator buffer has been read for the last time
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+          }
           uint32_t o[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e)
-            o[e] = q8_quant4(__half22float2(*reinterpret_cast<const __half2*>(&hq[ch * 16 + 2 * e])),
-                             __half22float2(*reinterpret_cast<const __half2*>(&hq[ch * 16 + 2 * e + 1])), sc, rs);
+            o[e] = q8_quant4(__half22float2(*reinterpret_cast<const __half2*>(&hv[2 * e])),
+                             __half22float2(*reinterpret_cast<const __half2*>(&hv[2 * e + 1])), sc, rs);
           // s8 block 32 rows x 32 B through the staging buffer (32B swizzle) + TMA store
           if (lane == 0) bulk_wait_read<0>();
           __syncwarp();
@@ -936,15 +950,16 @@ __global__ void __launch_bounds__(kRRThreads, 1)
             tma_store_2d(&tmQ, stage_buf, ncol0 + c_lo + ch * 32, row0);
             bulk_commit();
           }
-          if (tr0) gemm_trace(p.trace, lt, 12 + ch);
+          if (tr0 && ch < 2) gemm_trace(p.trace, lt, 12 + ch);
         }
-        if (rank == 0 && g == 0 && row_ok) p.out_scale[row] = sc;
+        if (rank == 0 && hc == 0 && row_ok) p.out_scale[row] = sc;
+      } else {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
       }
       if (tr0) gemm_trace(p.trace, lt, 5);
-      if (++acc == 2) {
-        acc = 0;
-        acc_phase ^= 1;
-      }
+      acc_phase ^= 1;
     }
     if (lane == 0) bulk_wait<0>();
   }

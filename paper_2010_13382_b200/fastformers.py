@@ -313,7 +313,7 @@ def quant_rows(x16):
 
 
 def attention(qkv16, mask, A, d, impl=0):
-    """impl: 0 auto, 1 mma.sync kernel, 2 tcgen05 kernel (head_dim 64, S <= 128)."""
+    """impl: 0 auto, 1 mma.sync kernel, 2 tcgen05 kernel (head_dim 64 or even <= 32, S <= 128)."""
     import torch
     B, S = mask.shape
     ctx = torch.empty((B * S, A * d), dtype=torch.float16, device=qkv16.device)

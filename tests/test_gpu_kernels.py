@@ -129,12 +129,16 @@ def test_attention_matches_oracle(B, S, A, d, ragged):
     assert np.abs(got - ref64).max() <= 2e-2
 
 
-@pytest.mark.parametrize("B,S,A,ragged", [(2, 128, 8, False), (3, 128, 4, True), (2, 40, 3, True), (1, 7, 2, False),
-                                          (4, 32, 2, True), (1, 1, 1, False), (2, 64, 12, True), (3, 128, 16, False)])
-def test_attention_tcgen05_matches_oracle(B, S, A, ragged):
-    """The tcgen05/TMEM attention kernel (head_dim 64, S <= 128)."""
-    d = 64
-    rng = np.random.default_rng(100 + S + A)
+@pytest.mark.parametrize("B,S,A,ragged,d", [(2, 128, 8, False, 64), (3, 128, 4, True, 64), (2, 40, 3, True, 64),
+                                            (1, 7, 2, False, 64), (4, 32, 2, True, 64), (1, 1, 1, False, 64),
+                                            (2, 64, 12, True, 64), (3, 128, 16, False, 64),
+                                            # head_dim <= 32 padded to 32 (C2's d = 26, DESIGN R18)
+                                            (2, 128, 12, True, 26), (3, 128, 4, True, 26), (1, 7, 4, False, 26),
+                                            (2, 40, 16, True, 26), (2, 128, 8, False, 32), (1, 1, 1, False, 32),
+                                            (2, 64, 4, True, 16)])
+def test_attention_tcgen05_matches_oracle(B, S, A, ragged, d):
+    """The tcgen05/TMEM attention kernel (head_dim 64 or even <= 32, S <= 128)."""
+    rng = np.random.default_rng(100 + S + A + d)
     qkv = np.float16(rng.standard_normal((B * S, 3 * A * d)) * 1.5)
     mask = np.ones((B, S), np.int32)
     if ragged:
@@ -154,14 +158,44 @@ def test_attention_tcgen05_matches_oracle(B, S, A, ragged):
     assert np.abs(ctx1.astype(np.float64) - got).max() <= 4e-3 + 4e-3 * np.abs(ref).max()
 
 
-@pytest.mark.parametrize("B,S,A,ragged", [(2, 128, 8, False), (3, 128, 4, True), (2, 40, 3, True), (1, 7, 2, False),
-                                          (1, 1, 1, False), (5, 128, 8, True), (150, 16, 2, True)])
-def test_attention_fused_requant(B, S, A, ragged):
+@pytest.mark.parametrize("B,S,A,ragged", [(2, 256, 4, True), (1, 512, 3, True), (2, 512, 2, False), (3, 129, 2, True),
+                                          (2, 300, 3, True), (1, 384, 2, False), (4, 200, 12, True), (1, 511, 1, True)])
+def test_attention_long_tcgen05_matches_oracle(B, S, A, ragged):
+    """The tcgen05 attention for 128 < S <= 512 (attention_long.cu: max over
+    all key chunks, then e = exp(s - max) and l, then P16 = R16(e / l) chunk
+    by chunk -- the oracle's order, DESIGN R9), head_dim 64, ragged masks
+    with holes, partial last chunks and query blocks."""
+    d = 64
+    rng = np.random.default_rng(700 + S + A + B)
+    qkv = np.float16(rng.standard_normal((B * S, 3 * A * d)) * 1.5)
+    mask = np.ones((B, S), np.int32)
+    if ragged:
+        for b in range(B):
+            mask[b, rng.integers(max(1, S // 4), S + 1):] = 0
+        mask[0, S // 2] = 0
+    mask[:, 0] = 1
+    ctx = ffb.attention(torch.from_numpy(qkv).cuda(), torch.from_numpy(mask).cuda(), A, d, impl=2)
+    torch.cuda.synchronize()
+    got = ctx.cpu().numpy().astype(np.float64)
+    ref = oracle.attention(qkv.astype(np.float32), mask, A, d).astype(np.float64)
+    err = np.abs(got - ref)
+    assert err.max() <= 4e-3 + 4e-3 * np.abs(ref).max(), err.max()
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-3
+    # and the same as the mma.sync kernel (online max / sum) up to rounding
+    ctx1 = ffb.attention(torch.from_numpy(qkv).cuda(), torch.from_numpy(mask).cuda(), A, d, impl=1).cpu().numpy()
+    assert np.abs(ctx1.astype(np.float64) - got).max() <= 4e-3 + 4e-3 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("B,S,A,ragged,d", [(2, 128, 8, False, 64), (3, 128, 4, True, 64), (2, 40, 3, True, 64),
+                                            (1, 7, 2, False, 64), (1, 1, 1, False, 64), (5, 128, 8, True, 64),
+                                            (150, 16, 2, True, 64), (2, 128, 8, True, 26), (3, 128, 16, False, 26),
+                                            (1, 1, 8, False, 26)])
+def test_attention_fused_requant(B, S, A, ragged, d):
     """a3 + a4 fused (the int8-layer path): ctx within the attention bound of
     the oracle, and the s8 rows / scales bit-exact Q8row of the kernel's own
-    fp16 ctx (DESIGN R6-R8, R12)."""
-    d = 64
-    rng = np.random.default_rng(300 + S + A + B)
+    fp16 ctx (DESIGN R6-R8, R12); head_dim 64 (<= 8 heads per sequence) and
+    26 (<= 16 heads, the TinyBERT shape)."""
+    rng = np.random.default_rng(300 + S + A + B + d)
     qkv = np.float16(rng.standard_normal((B * S, 3 * A * d)) * 1.5)
     mask = np.ones((B, S), np.int32)
     if ragged:

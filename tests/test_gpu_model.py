@@ -364,7 +364,11 @@ def test_full_size_c3_sampled_rows_vs_oracle():
     got = f32(enc.encode(dev(ids), dev(mask)))
     assert np.isfinite(got).all()
     orc = Oracle(cfg, w)
-    rows = [0, 31, 64, 97, 128, 161, 200, 255]
+    # 32 rows: both maxima of the 2x-drift comparison are taken over enough
+    # rows to be stable (with 4-8 rows the GPU / drift ratio of the maxima
+    # exceeds 2 for ~1-2% of row sets although the per-row error
+    # distributions agree, tools/drift_ratio.py)
+    rows = list(range(0, 256, 8))
     ref = _oracle_rows_parallel(orc, ids, mask, rows)
     drift = np.abs(_oracle_rows_parallel(orc, ids, mask, rows, acc32=True) - ref).max()
     err = np.abs(got[rows] - ref).max()
@@ -424,7 +428,7 @@ def _oracle_rows_parallel(orc, ids, mask, rows, **kw):
     return np.concatenate(outs, 0)
 
 
-@pytest.mark.parametrize("name,rows", [("c2_i8", [0, 21, 42, 63]), ("c2_f16", [0, 21, 42, 63]),
+@pytest.mark.parametrize("name,rows", [("c2_i8", list(range(0, 64, 4))), ("c2_f16", [0, 21, 42, 63]),
                                        ("c3_f16", [0, 85, 170, 255]), ("c4_f16", [0, 127]), ("c5_f16", [0, 63])])
 def test_full_size_sampled_rows_vs_oracle(name, rows):
     """BASELINE configs[1], [2] (fp16 variant), [3], [4] at their full sizes in
@@ -450,15 +454,16 @@ def test_full_size_sampled_rows_vs_oracle(name, rows):
     assert _margin_ok(ref, got[rows], 2e-2) == 1.0
 
 
-def test_full_size_c3_fused_epilogues_sampled_rows():
-    """The opt-in fused row-reduction epilogues at the bench size: sampled rows
-    within the same bound as the default path."""
+def test_full_size_c3_ffn1_only_fusion_sampled_rows():
+    """FF_OPT_FUSED_MASK 2 (separate add_ln kernels, the LN order of the
+    oracle-shaped two-pass kernel) at the bench size: sampled rows within the
+    same bound as the default (all-fused) path."""
     cfg = synth.config("c3")
     w = synth.make_weights(cfg)
     ids, mask = synth.make_inputs(cfg, seed=1000)
-    got = f32(Encoder(cfg, w, fused=True).encode(dev(ids), dev(mask)))
+    got = f32(Encoder(cfg, w, fused=2).encode(dev(ids), dev(mask)))
     orc = Oracle(cfg, w)
-    rows = [0, 100, 200, 255]
+    rows = list(range(4, 256, 16))
     ref = _oracle_rows_parallel(orc, ids, mask, rows)
     drift = np.abs(_oracle_rows_parallel(orc, ids, mask, rows, acc32=True) - ref).max()
     assert np.abs(got[rows] - ref).max() <= max(2 * drift, 1e-3 * np.abs(ref).max())
@@ -509,15 +514,15 @@ def test_per_tensor_quantizer_kernel_bit_exact():
 
 
 @pytest.mark.parametrize("name,B,S", [("c1", 4, 32), ("c2", 16, 128), ("c3", 256, 128)])
-def test_default_ffn1_fusion_bit_identical_to_separate_kernels(name, B, S):
-    """The default FF_OPT_FUSED_MASK = 2 (FFN1 + GELU + per-row requant in one
+def test_ffn1_fusion_bit_identical_to_separate_kernels(name, B, S):
+    """FF_OPT_FUSED_MASK = 2 (FFN1 + GELU + per-row requant in one
     cluster row-reduction GEMM) computes Q8row from the same R16 values as the
     separate quant_rows kernel (R12), so the logits are bit-identical to the
     fully unfused path (mask 0), which the lockstep tests check stage by stage."""
     cfg = synth.config(name).with_dtype(1).with_batch(B, S)
     w = synth.make_weights(cfg)
     ids, mask = synth.make_inputs(cfg, B=B, S=S, ragged=True, seed=77)
-    fused = Encoder(cfg, w)
+    fused = Encoder(cfg, w, fused=2)
     n_fused, n_sep = fused.launch_count(B, S), Encoder(cfg, w, fused=False).launch_count(B, S)
     fusable = cfg.ffn_dim[0] % 256 == 0  # row = 256 x 1..8 columns (C2's F' = 1200 is not)
     assert (n_fused < n_sep) if fusable else (n_fused == n_sep)
@@ -552,8 +557,8 @@ def test_every_fusion_mask_within_drift_bound(mask_bits):
     ids, mask = synth.make_inputs(cfg, B=16, S=128, ragged=True, seed=55)
     got = f32(Encoder(cfg, w, fused=mask_bits).encode(dev(ids), dev(mask)))
     orc = Oracle(cfg, w)
-    rows = [0, 5, 15]
-    ref = orc.encode(ids[rows], mask[rows])
-    drift = np.abs(orc.encode(ids[rows], mask[rows], acc32=True) - ref).max()
+    rows = list(range(16))
+    ref = _oracle_rows_parallel(orc, ids, mask, rows)
+    drift = np.abs(_oracle_rows_parallel(orc, ids, mask, rows, acc32=True) - ref).max()
     assert np.abs(got[rows] - ref).max() <= max(2 * drift, 1e-3 * np.abs(ref).max())
     assert (got[rows].argmax(1) == ref.argmax(1)).all() or _margin_ok(ref, got[rows], 2e-2) == 1.0
