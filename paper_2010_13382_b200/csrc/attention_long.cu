@@ -13,8 +13,9 @@
 //                S_c = Q . K_c^T     (fp32, TMEM columns [128 c, 128 c + 128))
 //                O  += P_c . V_c     (fp32; KC = 4: columns [0, 64), reusing
 //                                    S_0 once it has been read; KC = 2: [256, 320))
-//   warps 2-9  softmax + epilogue: two warps per TMEM lane quadrant (= 32
-//              query rows), each owning one half (64 keys) of every chunk:
+//   warps 2-17 softmax + epilogue: four warps per TMEM lane quadrant (= 32
+//              query rows), each owning one quarter (32 keys) of every chunk
+//              (16 warps hide the MUFU / TMEM latencies of the serial passes):
 //                pass 1: s = RN(raw * fp32(1/sqrt d)) (+ key mask -inf), row max
 //                pass 2: e = exp(s - max) (ex2.approx of (s - max) log2 e), the
 //                        row sum l; e written back over S in TMEM
@@ -38,7 +39,7 @@ constexpr int kLQ = 128;               // query rows per unit (TMEM lanes)
 constexpr int kLD = 64;                // head_dim
 constexpr int kLTile = 128 * 128;      // one 128-row x 64-column fp16 tile, 128B swizzle
 constexpr int kLSlots = 8;             // ring of tile slots (Q, K_c, V_c of consecutive units)
-constexpr int kLSoftWarps = 8;
+constexpr int kLSoftWarps = 16;
 constexpr int kLThreads = 64 + 32 * kLSoftWarps;
 constexpr int kLMaxKeys = 512;
 
@@ -46,8 +47,8 @@ struct SmemL {
   static constexpr int RING = 0;                              // [kLSlots] tiles
   static constexpr int P = RING + kLSlots * kLTile;           // P[2]: 2 k-blocks of 64 keys each
   static constexpr int MASK = P + 2 * 2 * kLTile;             // kLMaxKeys floats
-  static constexpr int RED = MASK + kLMaxKeys * 4;            // [2][2][128] floats: max, sum
-  static constexpr int BAR = RED + 2 * 2 * kLQ * 4;
+  static constexpr int RED = MASK + kLMaxKeys * 4;            // [2][4][128] floats: max, sum per quarter
+  static constexpr int BAR = RED + 2 * 4 * kLQ * 4;
   static constexpr int TOTAL = BAR + 256 + 1024;
   static_assert(TOTAL <= 227 * 1024, "smem budget");
 };
@@ -191,16 +192,16 @@ __global__ void __launch_bounds__(kLThreads, 1)
       }
     }
   } else {
-    const int q = warp & 3;            // TMEM lane quadrant
-    const int half = (warp - 2) >> 2;  // keys [64 half, +64) of every chunk; O columns [32 half, +32)
+    const int q = warp & 3;              // TMEM lane quadrant
+    const int qt = (warp - 2) >> 2;      // keys [32 qt, +32) of every chunk; O columns [16 qt, +16)
     const int r = q * 32 + lane;
     const int tid = threadIdx.x - 64;
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
     float* redMax = sRed;
-    float* redSum = sRed + 2 * kLQ;
-    const int pair_bar = 2 + q;
-    auto pair_sync = [pair_bar]() { asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory"); };
-    auto soft_sync = []() { asm volatile("bar.sync 1, 256;" ::: "memory"); };
+    float* redSum = sRed + 4 * kLQ;
+    const int quad_bar = 2 + q;  // the four warps sharing TMEM lane quadrant q
+    auto quad_sync = [quad_bar]() { asm volatile("bar.sync %0, 128;" ::"r"(quad_bar) : "memory"); };
+    auto soft_sync = []() { asm volatile("bar.sync 1, %0;" ::"n"(kSoft) : "memory"); };
     const float2 cd2 = make_float2(scale, scale);
     const float2 l2e = make_float2(1.4426950408889634f, 1.4426950408889634f);
     uint32_t g = 0, n = 0;
@@ -216,77 +217,70 @@ __global__ void __launch_bounds__(kLThreads, 1)
       }
       mbar_wait(s_full, n & 1);
       tc_fence_after();
-      // pass 1: row max of s = RN(raw * cd) + mask bias over this half of every chunk
+      // pass 1: row max of s = RN(raw * cd) + mask bias over this quarter of every chunk
       float mx = -INFINITY;
       for (int c = 0; c < KC; ++c) {
-        uint32_t raw[2][32];
-        tmem_ld32(trow + c * 128 + half * 64, raw[0]);
-        tmem_ld32(trow + c * 128 + half * 64 + 32, raw[1]);
+        uint32_t raw[32];
+        tmem_ld32(trow + c * 128 + qt * 32, raw);
         tmem_wait_ld();
-        const float2* mk = reinterpret_cast<const float2*>(sMask + c * 128 + half * 64);
+        const float2* mk = reinterpret_cast<const float2*>(sMask + c * 128 + qt * 32);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float2 s = fma2(make_float2(__uint_as_float(raw[j >> 4][(2 * j) & 31]),
-                                            __uint_as_float(raw[j >> 4][(2 * j + 1) & 31])),
-                                cd2, mk[j]);
+        for (int j = 0; j < 16; ++j) {
+          const float2 s = fma2(make_float2(__uint_as_float(raw[2 * j]), __uint_as_float(raw[2 * j + 1])), cd2, mk[j]);
           mx = fmaxf(mx, fmaxf(s.x, s.y));
         }
       }
-      redMax[half * kLQ + r] = mx;
-      pair_sync();
-      mx = fmaxf(mx, redMax[(half ^ 1) * kLQ + r]);
+      redMax[qt * kLQ + r] = mx;
+      quad_sync();
+      mx = fmaxf(fmaxf(redMax[r], redMax[kLQ + r]), fmaxf(redMax[2 * kLQ + r], redMax[3 * kLQ + r]));
       const float2 mxv = make_float2(mx, mx);
       // pass 2: e = exp(s - max) in fp32, written back over S; row sum
       float2 la = make_float2(0.0f, 0.0f), lb = make_float2(0.0f, 0.0f);
       for (int c = 0; c < KC; ++c) {
-        uint32_t raw[2][32];
-        tmem_ld32(trow + c * 128 + half * 64, raw[0]);
-        tmem_ld32(trow + c * 128 + half * 64 + 32, raw[1]);
+        uint32_t raw[32];
+        tmem_ld32(trow + c * 128 + qt * 32, raw);
         tmem_wait_ld();
-        const float2* mk = reinterpret_cast<const float2*>(sMask + c * 128 + half * 64);
+        const float2* mk = reinterpret_cast<const float2*>(sMask + c * 128 + qt * 32);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float2 s = fma2(make_float2(__uint_as_float(raw[j >> 4][(2 * j) & 31]),
-                                            __uint_as_float(raw[j >> 4][(2 * j + 1) & 31])),
-                                cd2, mk[j]);
+        for (int j = 0; j < 16; ++j) {
+          const float2 s = fma2(make_float2(__uint_as_float(raw[2 * j]), __uint_as_float(raw[2 * j + 1])), cd2, mk[j]);
           const float2 t = mul2(sub2(s, mxv), l2e);
           const float2 e = make_float2(ex2l(t.x), ex2l(t.y));
           if (j & 1) lb = add2(lb, e);
           else la = add2(la, e);
-          raw[j >> 4][(2 * j) & 31] = __float_as_uint(e.x);
-          raw[j >> 4][(2 * j + 1) & 31] = __float_as_uint(e.y);
+          raw[2 * j] = __float_as_uint(e.x);
+          raw[2 * j + 1] = __float_as_uint(e.y);
         }
-        tmem_st32(trow + c * 128 + half * 64, raw[0]);
-        tmem_st32(trow + c * 128 + half * 64 + 32, raw[1]);
+        tmem_st32(trow + c * 128 + qt * 32, raw);
       }
       tmem_wait_st();
       const float2 l2 = add2(la, lb);
-      redSum[half * kLQ + r] = l2.x + l2.y;
-      pair_sync();
-      const float l = redSum[r] + redSum[kLQ + r];  // fixed order in both halves
+      redSum[qt * kLQ + r] = l2.x + l2.y;
+      quad_sync();
+      const float l = (redSum[r] + redSum[kLQ + r]) + (redSum[2 * kLQ + r] + redSum[3 * kLQ + r]);  // fixed order
+      quad_sync();  // every quarter read redMax / redSum before the next unit's writes
       const float rl = __frcp_rn(l);
       const float2 lv = make_float2(l, l), rlv = make_float2(rl, rl);
       // pass 3: P16 = R16(e / l) chunk by chunk into P[g & 1] (K-major, 128B
-      // swizzle: 16-byte chunk cc of row r at (cc ^ (r & 7)))
+      // swizzle: 16-byte chunk cc of row r at (cc ^ (r & 7)); this quarter's
+      // 32 keys = chunks 4 (qt & 1) .. + 3 of k-block qt >> 1)
       for (int c = 0; c < KC; ++c, ++g) {
-        uint32_t ev[2][32];
-        tmem_ld32(trow + c * 128 + half * 64, ev[0]);
-        tmem_ld32(trow + c * 128 + half * 64 + 32, ev[1]);
+        uint32_t ev[32];
+        tmem_ld32(trow + c * 128 + qt * 32, ev);
         tmem_wait_ld();
         mbar_wait(p_empty + (g & 1), ((g >> 1) & 1) ^ 1);  // P.V of chunk g - 2 has read the buffer
-        uint8_t* prow = smem + SmemL::P + (g & 1) * 2 * kLTile + half * kLTile + r * 128;
+        uint8_t* prow = smem + SmemL::P + (g & 1) * 2 * kLTile + (qt >> 1) * kLTile + r * 128;
 #pragma unroll
-        for (int cc = 0; cc < 8; ++cc) {
+        for (int cc = 0; cc < 4; ++cc) {
           uint32_t w[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int j = cc * 4 + i;
-            const float2 p = div2_cr(make_float2(__uint_as_float(ev[j >> 4][(2 * j) & 31]),
-                                                 __uint_as_float(ev[j >> 4][(2 * j + 1) & 31])),
-                                     lv, rlv);
+            const float2 p = div2_cr(make_float2(__uint_as_float(ev[2 * j]), __uint_as_float(ev[2 * j + 1])), lv, rlv);
             w[i] = pack_half2(p.x, p.y);
           }
-          *reinterpret_cast<uint4*>(prow + ((cc ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+          const int pc = (qt & 1) * 4 + cc;
+          *reinterpret_cast<uint4*>(prow + ((pc ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
         }
         tc_fence_before();
         fence_async_smem();
@@ -295,19 +289,19 @@ __global__ void __launch_bounds__(kLThreads, 1)
       // epilogue: ctx = R16(O), fp16 rows; then TMEM is free for the next unit
       mbar_wait(o_full, n & 1);
       tc_fence_after();
-      uint32_t o[32];
-      tmem_ld32(trow + kO + half * 32, o);
+      uint32_t o[16];
+      tmem_ld16(trow + kO + qt * 16, o);
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(t_free);
       const int qrow = x.qb * kLQ + r;
       if (qrow < S) {
-        uint32_t pk[16];
+        uint32_t pk[8];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) pk[i] = pack_half2(__uint_as_float(o[2 * i]), __uint_as_float(o[2 * i + 1]));
-        uint4* dst = reinterpret_cast<uint4*>(ctx + ((size_t)x.b * S + qrow) * ldc + x.h * kLD + half * 32);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) dst[c] = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        for (int i = 0; i < 8; ++i) pk[i] = pack_half2(__uint_as_float(o[2 * i]), __uint_as_float(o[2 * i + 1]));
+        uint4* dst = reinterpret_cast<uint4*>(ctx + ((size_t)x.b * S + qrow) * ldc + x.h * kLD + qt * 16);
+        dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
       }
     }
   }

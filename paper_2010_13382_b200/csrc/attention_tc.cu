@@ -128,7 +128,7 @@ struct HeadIter {
 template <int DP>
 __global__ void __launch_bounds__(kThreadsTC, 1)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const int32_t* __restrict__ mask, int B, int S,
-                        int A, int d, float scale, __half* __restrict__ ctx, int ldc, int8_t* __restrict__ ctxq, int ldq,
+                        int A, int d, int hs, float scale, __half* __restrict__ ctx, int ldc, int8_t* __restrict__ ctxq, int ldq,
                         float* __restrict__ ctxs, const uint8_t* __restrict__ qkv_rows, int row_bytes,
                         unsigned long long* __restrict__ trace) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -149,9 +149,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   using HC = HeadCfg<DP>;
   constexpr int MH = HC::kMaxHeads;
   using Iter = HeadIter<MH>;
-  const int D = A * d;
+  const int D = A * hs;  // QKV section width (head stride hs >= d; hs > d: zero-padded heads)
   const int n_groups = (A + MH - 1) / MH;
-  const bool manual = ((d * 2) & 15) != 0;  // head slices TMA cannot address (d = 26)
   const int n_items = B * n_groups;
   const int it_first = (int)blockIdx.x;
   const int it_stride = (int)gridDim.x;
@@ -159,7 +158,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmQKV);
     for (int i = 0; i < kKVStages; ++i) {
-      mbar_init(kv_full + i, manual ? 32 : 1);  // manual copy: one arrival per producer lane
+      mbar_init(kv_full + i, 1);
       mbar_init(kv_empty + i, 1);
     }
     mbar_init(s_full, 1);
@@ -183,44 +182,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   griddep_launch();
 
   if (warp == 0) {
-    if (manual) {
-      // head columns not 16-byte aligned (d = 26: head h starts at byte 52 h),
-      // which TMA cannot address: the whole warp copies each head's 32-column
-      // Q / K / V slices (4-byte cp.async) into the same 128B-swizzled tiles,
-      // zero-filling the columns >= d and the rows >= S
-      const int ldw = row_bytes / 4;  // QKV row pitch in 4-byte words
-      const uint32_t* src_w = reinterpret_cast<const uint32_t*>(qkv_rows);
-      uint32_t n = 0;
-      for (Iter it(it_first, n_items, n_groups, A, it_stride); it.valid(); it.next(), ++n) {
-        const int slot = n % kKVStages;
-        const int h = it.h0 + it.hl;
-        uint8_t* base = smem + slot * SmemTC::SLOT;
-        mbar_wait(kv_empty + slot, ((n / kKVStages) & 1) ^ 1);
-        if (lane == 0) trace_ev(trace, n, 0);
-#pragma unroll 1
-        for (int t = 0; t < 3; ++t) {
-          const int w0 = (t * D + h * d) >> 1;  // first word of the slice (d even)
-          uint8_t* tile = base + t * kTileBytes;
-          for (int idx = lane; idx < 128 * (DP / 2); idx += 32) {
-            const int rr = idx / (DP / 2), w = idx % (DP / 2);
-            const uint32_t dst = smem_u32(tile + rr * 128 + ((((w >> 2) ^ (rr & 7))) << 4) + (w & 3) * 4);
-            if (rr < S && 2 * w < d) {
-              const uint32_t* src = src_w + (size_t)(it.b * S + rr) * ldw + w0 + w;
-              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
-            } else {
-              asm volatile("st.shared.b32 [%0], %1;" ::"r"(dst), "r"(0u) : "memory");
-            }
-          }
-        }
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        fence_async_smem();  // generic-proxy smem writes -> visible to the tensor cores
-        mbar_arrive(kv_full + slot);
-      }
-    } else if (lane == 0) {
+    if (lane == 0) {
       // (An L2 bulk prefetch of each item's QKV rows, meant to open each DRAM
       // page once per item, measured 5.5 us slower per C3 launch: the QKV
       // buffer was just written by the projection GEMM and is largely still
       // in L2, and the prefetch queued ahead of the first head's loads.)
+      (void)qkv_rows;
+      (void)row_bytes;
       uint32_t n = 0;
       for (Iter it(it_first, n_items, n_groups, A, it_stride); it.valid(); it.next(), ++n) {
         const int slot = n % kKVStages;
@@ -229,9 +197,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         mbar_wait(kv_empty + slot, ((n / kKVStages) & 1) ^ 1);
         trace_ev(trace, n, 0);
         mbar_expect_tx(kv_full + slot, 3 * kTileBytes);
-        tma_load_2d(base, &tmQKV, kv_full + slot, h * d, it.b * S, kEvictFirst);
-        tma_load_2d(base + kTileBytes, &tmQKV, kv_full + slot, D + h * d, it.b * S, kEvictFirst);
-        tma_load_2d(base + 2 * kTileBytes, &tmQKV, kv_full + slot, 2 * D + h * d, it.b * S, kEvictFirst);
+        tma_load_2d(base, &tmQKV, kv_full + slot, h * hs, it.b * S, kEvictFirst);
+        tma_load_2d(base + kTileBytes, &tmQKV, kv_full + slot, D + h * hs, it.b * S, kEvictFirst);
+        tma_load_2d(base + 2 * kTileBytes, &tmQKV, kv_full + slot, 2 * D + h * hs, it.b * S, kEvictFirst);
       }
     }
   } else if (warp == 1) {
@@ -270,13 +238,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         uint8_t* base = smem + slot * SmemTC::SLOT;
         mbar_wait(kv_full + slot, (n / kKVStages) & 1);
         if (issuer) trace_ev(trace, n, 1);
-        if (d < DP && !manual) {
-          // head_dim below the MMA granularity (d = 16 by TMA): the box also
-          // holds the next head's first columns; zero Q's columns [d, DP) so
-          // they add nothing to Q.K^T (V's extra columns only reach O columns
-          // that are never stored); the manual copy (d = 26) zero-fills itself
+        if (hs < DP) {
+          // head stride below the MMA granularity (d = 16 unpadded): the box
+          // also holds the next head's first columns; zero Q's columns
+          // [hs, DP) so they add nothing to Q.K^T (V's extra columns only
+          // reach O columns that are never stored).  Padded heads (hs = DP >
+          // d, e.g. d = 26) carry exact zeros in [d, hs) from the QKV GEMM.
           for (int rr = lane; rr < 128; rr += 32)
-            for (int c = d; c < DP; ++c)
+            for (int c = hs; c < DP; ++c)
               *reinterpret_cast<__half*>(base + rr * 128 + (((c >> 3) ^ (rr & 7)) << 4) + (c & 7) * 2) =
                   __float2half_rn(0.0f);
           fence_async_smem();
@@ -513,9 +482,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 
 }  // namespace
 
-bool attention_tc_supported(int S, int d, int ldqkv, int ldctx) {
-  return d >= 16 && d <= 64 && (d % 2) == 0 && (d == 64 || d <= 32) && S >= 1 && S <= kKeys && (ldqkv % 8) == 0 &&
-         (ldctx % 8) == 0;
+// TMA addresses a head slice only when it starts on a 16-byte boundary
+// (2 hs % 16 == 0).  TinyBERT's d = 26 is therefore stored with head stride
+// hs = 32 (the QKV GEMM writes zero-padded heads, ff_api.cu); unpadded, it
+// would start at byte 52 h (a 4-byte cp.async producer for that layout
+// measured 99 us per C2 launch, 2.4x the mma.sync kernel).
+bool attention_tc_supported(int S, int d, int hs, int ldqkv, int ldctx) {
+  const bool shape = (d == 64 && hs == 64) || (d >= 2 && d % 2 == 0 && d <= hs && hs <= 32 && (2 * hs) % 16 == 0);
+  return shape && S >= 1 && S <= kKeys && (ldqkv % 8) == 0 && (ldctx % 2) == 0;
 }
 
 bool attention_tc_fuses_quant(int A, int d) { return A >= 1 && A <= (d <= 32 ? 16 : 8); }
@@ -534,8 +508,8 @@ cudaError_t prepare_attention_tc_kernel() {
   return cudaFuncSetAttribute(attention_tc_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemTC::TOTAL);
 }
 
-cudaError_t launch_attention_tc(const AttnTCPlan& plan, const int32_t* mask, int B, int S, int A, int d, __half* ctx,
-                                int ldctx, int8_t* ctxq, int ldq, float* ctxs, cudaStream_t s,
+cudaError_t launch_attention_tc(const AttnTCPlan& plan, const int32_t* mask, int B, int S, int A, int d, int hs,
+                                __half* ctx, int ldctx, int8_t* ctxq, int ldq, float* ctxs, cudaStream_t s,
                                 unsigned long long* trace) {
   if (ctxq != nullptr && !attention_tc_fuses_quant(A, d)) return cudaErrorInvalidValue;
   const float scale = (float)(1.0 / sqrt((double)d));  // fp32(1/sqrt(d)) (R10)
@@ -544,10 +518,10 @@ cudaError_t launch_attention_tc(const AttnTCPlan& plan, const int32_t* mask, int
   const int grid = n_items < kNumSMs ? n_items : kNumSMs;
   if (d <= 32)
     launch_ex(attention_tc_kernel<32>, dim3(grid), dim3(kThreadsTC), SmemTC::TOTAL, s, 0, plan.map, mask, B, S, A, d,
-              scale, ctx, ldctx, ctxq, ldq, ctxs, static_cast<const uint8_t*>(plan.qkv), plan.ldqkv * 2, trace);
+              hs, scale, ctx, ldctx, ctxq, ldq, ctxs, static_cast<const uint8_t*>(plan.qkv), plan.ldqkv * 2, trace);
   else
     launch_ex(attention_tc_kernel<64>, dim3(grid), dim3(kThreadsTC), SmemTC::TOTAL, s, 0, plan.map, mask, B, S, A, d,
-              scale, ctx, ldctx, ctxq, ldq, ctxs, static_cast<const uint8_t*>(plan.qkv), plan.ldqkv * 2, trace);
+              hs, scale, ctx, ldctx, ctxq, ldq, ctxs, static_cast<const uint8_t*>(plan.qkv), plan.ldqkv * 2, trace);
   return cudaGetLastError();
 }
 

@@ -60,6 +60,7 @@ const char* kTopKeys[9] = {"embeddings.word_embeddings.weight", "embeddings.posi
 
 struct LayerPlan {
   int A, F, dt, D;
+  int Dq;  // QKV section width A * hs (hs = the model's QKV head stride)
   int N[4], K[4], ldw[4];  // GEMM shapes; ldw = packed row pitch in elements
   size_t w[4], sw[4], bias[4], cs[4];  // cs: int32 weight column sums (int8 layers)
   size_t ln1g, ln1b, ln2g, ln2b;
@@ -81,7 +82,11 @@ struct ff_model {
   size_t emb_tok, emb_pos, emb_type, emb_g, emb_b, pool_w, pool_b, cls_w, cls_b;
   uint32_t top_loaded = 0;
   size_t wbytes = 0;
-  int Dmax = 0, Fmax = 0;
+  int Dmax = 0, Fmax = 0, Dqmax = 0;
+  // QKV head stride: head_dim rounded up to 8 elements, so every head slice
+  // of the QKV buffer starts on a 16-byte boundary (TMA); for head_dim 26
+  // (TinyBERT) the fused QKV GEMM writes zero-padded 32-column heads
+  int hs = 0;
   bool any_i8 = false;
   // workspace pitches (elements) and offsets
   int ldx16, ldx8, ldqkv, ldc16, ldc8, ldi16, ldi8;
@@ -155,6 +160,7 @@ void plan_memory(ff_model* m) {
   m->emb_type = wa.take((size_t)H * 4);
   m->emb_g = wa.take((size_t)H * 4);
   m->emb_b = wa.take((size_t)H * 4);
+  m->hs = round_up(c.head_dim, 8);
   m->L.resize(c.num_layers);
   for (int l = 0; l < c.num_layers; ++l) {
     LayerPlan& P = m->L[l];
@@ -162,7 +168,8 @@ void plan_memory(ff_model* m) {
     P.F = m->ffn[l];
     P.dt = m->dtype[l];
     P.D = P.A * c.head_dim;
-    const int Ns[4] = {3 * P.D, H, P.F, H}, Ks[4] = {H, P.D, H, P.F};
+    P.Dq = P.A * m->hs;
+    const int Ns[4] = {3 * P.Dq, H, P.F, H}, Ks[4] = {H, P.D, H, P.F};
     const int eb = P.dt == FF_I8 ? 1 : 2;
     for (int i = 0; i < 4; ++i) {
       P.N[i] = Ns[i];
@@ -178,6 +185,7 @@ void plan_memory(ff_model* m) {
     P.ln2g = wa.take((size_t)H * 4);
     P.ln2b = wa.take((size_t)H * 4);
     m->Dmax = std::max(m->Dmax, P.D);
+    m->Dqmax = std::max(m->Dqmax, P.Dq);
     m->Fmax = std::max(m->Fmax, P.F);
     m->any_i8 = m->any_i8 || P.dt == FF_I8;
   }
@@ -190,7 +198,7 @@ void plan_memory(ff_model* m) {
   const size_t M = (size_t)c.max_tokens;
   m->ldx16 = round_up(H, 8);
   m->ldx8 = round_up(H, 16);
-  m->ldqkv = round_up(3 * m->Dmax, 8);
+  m->ldqkv = round_up(3 * m->Dqmax, 8);
   m->ldc16 = round_up(m->Dmax, 8);
   m->ldc8 = round_up(m->Dmax, 16);
   m->ldi16 = round_up(m->Fmax, 8);
@@ -332,7 +340,7 @@ ff_status dump(void* dst, const void* src, int ld_elems, int cols, int M, cudaSt
 
 // int8 layer whose ctx requant (a4) runs inside the tcgen05 attention kernel.
 bool attention_fuses_quant(const ff_model* m, const LayerPlan& P, int S) {
-  return P.dt == FF_I8 && m->attn_tc && ff::attention_tc_supported(S, m->cfg.head_dim, m->ldqkv, m->ldc16) &&
+  return P.dt == FF_I8 && m->attn_tc && ff::attention_tc_supported(S, m->cfg.head_dim, m->hs, m->ldqkv, m->ldc16) &&
          ff::attention_tc_fuses_quant(P.A, m->cfg.head_dim);
 }
 
@@ -399,20 +407,32 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     g.p.act = ff::ACT_NONE;
     if (q && pt && tensor_quant(X16, m->ldx16, H, Xq, m->ldx8, g, P, W_QKV) != FF_OK) return FF_E_CUDA;
     FF_LAUNCH(q ? FF_K_GEMM_I8 : FF_K_GEMM_F16, ff::launch_gemm(g, s), "gemm qkv");
-    if (tr && dump(d_dump[1], QKV, m->ldqkv, 3 * P.D, M, s) != FF_OK) return FF_E_CUDA;
+    if (tr) {  // the trace holds the unpadded [M, 3 D] Q | K | V rows
+      if (m->hs == c.head_dim) {
+        if (dump(d_dump[1], QKV, m->ldqkv, 3 * P.D, M, s) != FF_OK) return FF_E_CUDA;
+      } else if (d_dump[1]) {
+        for (int t = 0; t < 3; ++t)
+          for (int h = 0; h < P.A; ++h)
+            FF_CK(cudaMemcpy2DAsync(static_cast<__half*>(d_dump[1]) + t * P.D + h * c.head_dim, (size_t)3 * P.D * 2,
+                                    QKV + t * P.Dq + h * m->hs, (size_t)m->ldqkv * 2, (size_t)c.head_dim * 2, M,
+                                    cudaMemcpyDeviceToDevice, s));
+      }
+    }
     // a3: fused masked-softmax attention over this layer's A'_l heads
     // (int8 layers: a4, the ctx requant, fused into the tcgen05 attention)
     const bool att_q = attention_fuses_quant(m, P, S) && !pt;
-    if (m->attn_tc && ff::attention_tc_supported(S, c.head_dim, m->ldqkv, m->ldc16))
+    if (m->attn_tc && ff::attention_tc_supported(S, c.head_dim, m->hs, m->ldqkv, m->ldc16))
       FF_LAUNCH(FF_K_ATTENTION,
-                ff::launch_attention_tc(m->tm_qkv, mask, B, S, P.A, c.head_dim, (att_q && !tr) ? nullptr : CTX, m->ldc16,
+                ff::launch_attention_tc(m->tm_qkv, mask, B, S, P.A, c.head_dim, m->hs, (att_q && !tr) ? nullptr : CTX,
+                                        m->ldc16,
                                         att_q ? CTXq : nullptr, m->ldc8, att_q ? CTXs : nullptr, s),
                 "attention_tc");
-    else if (m->attn_tc && ff::attention_long_supported(S, c.head_dim, m->ldqkv, m->ldc16))
+    else if (m->attn_tc && m->hs == c.head_dim && ff::attention_long_supported(S, c.head_dim, m->ldqkv, m->ldc16))
       FF_LAUNCH(FF_K_ATTENTION, ff::launch_attention_long(m->tm_qkv, mask, B, S, P.A, CTX, m->ldc16, s),
                 "attention_long");
     else
-      FF_LAUNCH(FF_K_ATTENTION, ff::launch_attention(QKV, m->ldqkv, mask, B, S, P.A, c.head_dim, CTX, m->ldc16, s),
+      FF_LAUNCH(FF_K_ATTENTION,
+                ff::launch_attention(QKV, m->ldqkv, mask, B, S, P.A, c.head_dim, m->hs, CTX, m->ldc16, s),
                 "attention");
     if (tr && dump(d_dump[2], CTX, m->ldc16, P.D, M, s) != FF_OK) return FF_E_CUDA;
     // a4 + a5: requant (int8 layers) and out-projection
@@ -713,13 +733,31 @@ ff_status ff_load_weights(ff_model* m, const char* cname, const float* h_data, c
   };
   ff_status st = FF_OK;
   switch (ki) {
-    case 0: case 1: case 2:  // query / key / value weight -> rows [ki*D, (ki+1)*D) of fused QKV
+    case 0: case 1: case 2:  // query / key / value weight -> section ki of the fused QKV
       if (!shape_is({D, H})) return bad_shape();
-      st = pack_weight(W_QKV, ki * D, D, H);
+      if (m->hs == c.head_dim) {
+        st = pack_weight(W_QKV, ki * D, D, H);
+      } else {  // head h -> rows [ki Dq + h hs, + d); rows up to + hs stay zero (bind memset)
+        const float* all = h_data;
+        for (int h = 0; h < P.A && st == FF_OK; ++h) {
+          h_data = all + (size_t)h * c.head_dim * H;
+          st = pack_weight(W_QKV, ki * P.Dq + h * m->hs, c.head_dim, H);
+        }
+        h_data = all;
+      }
       break;
     case 3: case 4: case 5:
       if (!shape_is({D})) return bad_shape();
-      st = copy_f32(P.bias[W_QKV] + (size_t)(ki - 3) * D * 4, D);
+      if (m->hs == c.head_dim) {
+        st = copy_f32(P.bias[W_QKV] + (size_t)(ki - 3) * D * 4, D);
+      } else {
+        const float* all = h_data;
+        for (int h = 0; h < P.A && st == FF_OK; ++h) {
+          h_data = all + (size_t)h * c.head_dim;
+          st = copy_f32(P.bias[W_QKV] + ((size_t)(ki - 3) * P.Dq + (size_t)h * m->hs) * 4, c.head_dim);
+        }
+        h_data = all;
+      }
       break;
     case 6: if (!shape_is({H, D})) return bad_shape(); st = pack_weight(W_O, 0, H, D); break;
     case 7: if (!shape_is({H})) return bad_shape(); st = copy_f32(P.bias[W_O], H); break;
@@ -1080,7 +1118,7 @@ ff_status ff_debug_attention(const void* d_qkv16, const int32_t* d_mask, int32_t
   }
   const int mode = impl;  // 0 auto (tcgen05 where supported), 1 mma.sync kernel, 2 tcgen05 (must be supported)
   const bool aligned = (reinterpret_cast<uintptr_t>(d_qkv16) & 15) == 0;
-  const bool tc = mode != 1 && aligned && ff::attention_tc_supported(S, d, 3 * A * d, A * d);
+  const bool tc = mode != 1 && aligned && ff::attention_tc_supported(S, d, d, 3 * A * d, A * d);
   const bool tcl = mode != 1 && aligned && !tc && ff::attention_long_supported(S, d, 3 * A * d, A * d);
   if (mode == 2 && !tc && !tcl)
     return fail(FF_E_UNSUPPORTED,
@@ -1091,14 +1129,14 @@ ff_status ff_debug_attention(const void* d_qkv16, const int32_t* d_mask, int32_t
     if (!ff::plan_attention_tc(&map, d_qkv16, B * S, 3 * A * d, &err))
       return fail(FF_E_INVALID, std::string("attention tensor map: ") + err);
     if (tc)
-      FF_CK(ff::launch_attention_tc(map, d_mask, B, S, A, d, static_cast<__half*>(d_ctx16), A * d, nullptr, 0,
+      FF_CK(ff::launch_attention_tc(map, d_mask, B, S, A, d, d, static_cast<__half*>(d_ctx16), A * d, nullptr, 0,
                                     nullptr, static_cast<cudaStream_t>(stream)));
     else
       FF_CK(ff::launch_attention_long(map, d_mask, B, S, A, static_cast<__half*>(d_ctx16), A * d,
                                       static_cast<cudaStream_t>(stream)));
     return FF_OK;
   }
-  FF_CK(ff::launch_attention(static_cast<const __half*>(d_qkv16), 3 * A * d, d_mask, B, S, A, d,
+  FF_CK(ff::launch_attention(static_cast<const __half*>(d_qkv16), 3 * A * d, d_mask, B, S, A, d, d,
                              static_cast<__half*>(d_ctx16), A * d, static_cast<cudaStream_t>(stream)));
   return FF_OK;
 }
@@ -1107,7 +1145,7 @@ ff_status ff_debug_attention_q8(const void* d_qkv16, const int32_t* d_mask, int3
                                 int32_t d, void* d_ctx16, int8_t* d_ctxq, float* d_ctxs, uint64_t* d_trace,
                                 void* stream) {
   if (B < 1 || S < 1 || A < 1 || !d_ctxq || !d_ctxs) return fail(FF_E_INVALID, "bad attention args");
-  if (!ff::attention_tc_supported(S, d, 3 * A * d, A * d) || !ff::attention_tc_fuses_quant(A, d) ||
+  if (!ff::attention_tc_supported(S, d, d, 3 * A * d, A * d) || !ff::attention_tc_fuses_quant(A, d) ||
       (reinterpret_cast<uintptr_t>(d_qkv16) & 15) != 0 || (A * d) % 16 != 0)
     return fail(FF_E_UNSUPPORTED, "fused attention + requant needs head_dim 64 (A <= 8) or an even head_dim <= 32 (A <= 16), S <= 128");
   static bool prepared = false;
@@ -1120,7 +1158,7 @@ ff_status ff_debug_attention_q8(const void* d_qkv16, const int32_t* d_mask, int3
   const char* err = nullptr;
   if (!ff::plan_attention_tc(&map, d_qkv16, B * S, 3 * A * d, &err))
     return fail(FF_E_INVALID, std::string("attention tensor map: ") + err);
-  FF_CK(ff::launch_attention_tc(map, d_mask, B, S, A, d, static_cast<__half*>(d_ctx16), A * d, d_ctxq, A * d, d_ctxs,
+  FF_CK(ff::launch_attention_tc(map, d_mask, B, S, A, d, d, static_cast<__half*>(d_ctx16), A * d, d_ctxq, A * d, d_ctxs,
                                 static_cast<cudaStream_t>(stream),
                                 reinterpret_cast<unsigned long long*>(d_trace)));
   return FF_OK;

@@ -183,14 +183,17 @@ cudaError_t launch_head(const __half* x16, int ldx, int B, int S, int H, int C, 
 
 // ------------------------------------------------------------- attention
 size_t attention_smem_bytes(int S, int d);
-cudaError_t launch_attention(const __half* qkv, int ldqkv, const int32_t* mask, int B, int S, int A, int d,
+// mma.sync attention: QKV sections of A heads at head stride hs >= d (hs > d:
+// zero-padded head columns), ctx rows unpadded [B*S, ldctx] (head h at h * d).
+cudaError_t launch_attention(const __half* qkv, int ldqkv, const int32_t* mask, int B, int S, int A, int d, int hs,
                              __half* ctx, int ldctx, cudaStream_t s);
 
 // tcgen05 attention (head_dim 64 or <= 32 even -- padded to 32 --, S <= 128); the tensor map covers the QKV
 // buffer [M_rows x ldqkv] fp16 with 64-column x 128-row boxes.  Writes the
 // fp16 ctx rows when ctx != null and, when ctxq != null (requires
 // attention_tc_fuses_quant(A, d)), the Q8row s8 ctx rows + per-row scales.
-bool attention_tc_supported(int S, int d, int ldqkv, int ldctx);
+// hs: head stride of the QKV buffer (>= d; TMA needs 2 hs % 16 == 0).
+bool attention_tc_supported(int S, int d, int hs, int ldqkv, int ldctx);
 bool attention_tc_fuses_quant(int A, int d);
 struct AttnTCPlan {
   CUtensorMap map;
@@ -198,7 +201,8 @@ struct AttnTCPlan {
   int ldqkv;
 };
 bool plan_attention_tc(AttnTCPlan* plan, const void* qkv, int M_rows, int ldqkv, const char** err);
-cudaError_t launch_attention_tc(const AttnTCPlan& plan, const int32_t* mask, int B, int S, int A, int d, __half* ctx,
+cudaError_t launch_attention_tc(const AttnTCPlan& plan, const int32_t* mask, int B, int S, int A, int d, int hs,
+                                __half* ctx,
                                 int ldctx, int8_t* ctxq, int ldq, float* ctxs, cudaStream_t s,
                                 unsigned long long* trace = nullptr);
 cudaError_t prepare_attention_tc_kernel();

@@ -132,10 +132,9 @@ def test_attention_matches_oracle(B, S, A, d, ragged):
 @pytest.mark.parametrize("B,S,A,ragged,d", [(2, 128, 8, False, 64), (3, 128, 4, True, 64), (2, 40, 3, True, 64),
                                             (1, 7, 2, False, 64), (4, 32, 2, True, 64), (1, 1, 1, False, 64),
                                             (2, 64, 12, True, 64), (3, 128, 16, False, 64),
-                                            # head_dim <= 32 padded to 32 (C2's d = 26, DESIGN R18)
-                                            (2, 128, 12, True, 26), (3, 128, 4, True, 26), (1, 7, 4, False, 26),
-                                            (2, 40, 16, True, 26), (2, 128, 8, False, 32), (1, 1, 1, False, 32),
-                                            (2, 64, 4, True, 16)])
+                                            # head_dim <= 32 padded to 32 (TMA-aligned head slices)
+                                            (2, 128, 8, False, 32), (1, 1, 1, False, 32), (3, 128, 12, True, 32),
+                                            (2, 64, 4, True, 16), (2, 40, 6, True, 24)])
 def test_attention_tcgen05_matches_oracle(B, S, A, ragged, d):
     """The tcgen05/TMEM attention kernel (head_dim 64 or even <= 32, S <= 128)."""
     rng = np.random.default_rng(100 + S + A + d)
@@ -188,13 +187,13 @@ def test_attention_long_tcgen05_matches_oracle(B, S, A, ragged):
 
 @pytest.mark.parametrize("B,S,A,ragged,d", [(2, 128, 8, False, 64), (3, 128, 4, True, 64), (2, 40, 3, True, 64),
                                             (1, 7, 2, False, 64), (1, 1, 1, False, 64), (5, 128, 8, True, 64),
-                                            (150, 16, 2, True, 64), (2, 128, 8, True, 26), (3, 128, 16, False, 26),
-                                            (1, 1, 8, False, 26)])
+                                            (150, 16, 2, True, 64), (2, 128, 8, True, 32), (3, 128, 16, False, 32),
+                                            (1, 1, 8, False, 32)])
 def test_attention_fused_requant(B, S, A, ragged, d):
     """a3 + a4 fused (the int8-layer path): ctx within the attention bound of
     the oracle, and the s8 rows / scales bit-exact Q8row of the kernel's own
     fp16 ctx (DESIGN R6-R8, R12); head_dim 64 (<= 8 heads per sequence) and
-    26 (<= 16 heads, the TinyBERT shape)."""
+    32 (<= 16 heads)."""
     rng = np.random.default_rng(300 + S + A + B + d)
     qkv = np.float16(rng.standard_normal((B * S, 3 * A * d)) * 1.5)
     mask = np.ones((B, S), np.int32)
