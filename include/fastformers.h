@@ -168,7 +168,7 @@ FF_API ff_status ff_check(ff_model *m, void *stream);
  * fuse residual + LayerNorm (+ s8 requant) into the out-proj / FFN2 GEMM
  * epilogues and the FFN-intermediate requant into FFN1, using clusters that
  * span the row; 0: separate add_ln / quant_rows kernels everywhere; the
- * default is 1, i.e. FF_OPT_FUSED_MASK = 7).  With 1, ff_encode_trace does not fill the O16 / Y16 dumps (never
+ * default is FF_OPT_FUSED_MASK = -1, auto).  With 1, ff_encode_trace does not fill the O16 / Y16 dumps (never
  * materialised). */
 #define FF_OPT_FUSED_EPILOGUES 4
 /* FF_OPT_PDL (1 = default: launch every forward kernel of this model with
@@ -184,11 +184,13 @@ FF_API ff_status ff_check(ff_model *m, void *stream);
 #define FF_OPT_ACT_QUANT 6
 /* FF_OPT_FUSED_MASK: per-fusion control of FF_OPT_FUSED_EPILOGUES (which sets
  * 0 or 7): bit 0 out-proj + residual + LN1, bit 1 FFN1 + activation + requant
- * (int8 layers), bit 2 FFN2 + residual + LN2.  Value 0..7; default 7 (the
- * fastest measured; the LN fusions combine the LN statistics across the
- * cluster in another order than add_ln, so their logits agree with the
- * unfused path within the DESIGN §3 bounds, not bit for bit; mask 2 is
- * bit-identical to the unfused path). */
+ * (int8 layers), bit 2 FFN2 + residual + LN2.  Value 0..7, or -1 = auto (the
+ * default): FFN1 + requant always, and each LN fusion where the GEMM's K row
+ * is at most 2 KB (with longer rows the row-reduction kernel's single-CTA
+ * tiles lose to the CTA-pair GEMM + add_ln).  The LN fusions combine
+ * the LN statistics across the cluster in another order than add_ln, so their
+ * logits agree with the unfused path within the DESIGN §3 bounds, not bit for
+ * bit; mask 2 is bit-identical to the unfused path. */
 #define FF_OPT_FUSED_MASK 8
 /* FF_OPT_PDL_RR (per model): 1 = the LN-mode row-reduction GEMMs
  * (FF_OPT_FUSED_MASK bits 0 / 2) also launch with PDL; default 0 (with PDL

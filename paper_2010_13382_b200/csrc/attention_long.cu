@@ -4,7 +4,9 @@
 // passages"; SURVEY 8(a) a3, P:104 Q.K^T and P.V in floating point).
 //
 // Work unit = (sequence b, query block of 128 rows, head h); one persistent
-// CTA per SM walks units blockIdx.x, +gridDim.x, ...  Per unit, with KC =
+// CTA per SM takes a contiguous range of units (heads fastest, so its units
+// share the sequence's key mask and the K / V tiles of a head stay in L2
+// across the query blocks).  Per unit, with KC =
 // ceil(S / 128) key chunks:
 //   warp 0     TMA: Q block, K_0..K_{KC-1}, V_0..V_{KC-1} (128 rows x 64 fp16,
 //              128B swizzle) through a ring of 16 KB tile slots, running ahead
@@ -102,6 +104,8 @@ __global__ void __launch_bounds__(kLThreads, 1)
   const int D = A * kLD;
   const int nqb = (S + kLQ - 1) / kLQ;
   const int n_units = B * nqb * A;
+  const int per = (n_units + gridDim.x - 1) / gridDim.x;  // contiguous units of this CTA
+  const int u_begin = min(n_units, (int)blockIdx.x * per), u_end = min(n_units, u_begin + per);
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmQKV);
     for (int i = 0; i < kLSlots; ++i) {
@@ -138,7 +142,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
         tma_load_2d(smem + SmemL::RING + slot * kLTile, &tmQKV, full + slot, col, row, kEvictFirst);
         ++cnt;
       };
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      for (int u = u_begin; u < u_end; ++u) {
         const Unit x = unit_of(u, nqb, A);
         const int row0 = x.b * S;
         load(x.h * kLD, row0 + x.qb * kLQ);
@@ -151,7 +155,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
       constexpr uint32_t id1 = idesc_l(128, 0);   // S_c = Q K_c^T: N = 128 keys
       constexpr uint32_t id2 = idesc_l(kLD, 1);   // O += P_c V_c: N = 64, V MN-major
       uint32_t cnt = 0, g = 0, n = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++n) {
+      for (int u = u_begin; u < u_end; ++u, ++n) {
         // TMEM (S chunks, O) free once the previous unit's epilogue read O
         mbar_wait(t_free, (n & 1) ^ 1);
         tc_fence_after();
@@ -206,7 +210,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
     const float2 l2e = make_float2(1.4426950408889634f, 1.4426950408889634f);
     uint32_t g = 0, n = 0;
     int prev_b = -1;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++n) {
+    for (int u = u_begin; u < u_end; ++u, ++n) {
       const Unit x = unit_of(u, nqb, A);
       if (x.b != prev_b) {  // key mask bias of the sequence (0 / -inf; keys >= S masked)
         soft_sync();        // every thread finished reading the previous mask

@@ -93,19 +93,18 @@ __device__ __forceinline__ void softmax_sync() { asm volatile("bar.sync 1, 256;"
 
 // Walk of the heads one CTA processes: items blockIdx.x, +gridDim.x, ...;
 // each item = (sequence b, heads [h0, h0 + nh)).
-template <int MH>
 struct HeadIter {
   int item, hl, b, h0, nh;
-  int n_items, n_groups, A, stride;
-  __device__ HeadIter(int first, int n_items_, int n_groups_, int A_, int stride_)
-      : item(first), hl(0), n_items(n_items_), n_groups(n_groups_), A(A_), stride(stride_) {
+  int n_items, n_groups, A, stride, mh;
+  __device__ HeadIter(int first, int n_items_, int n_groups_, int A_, int stride_, int mh_)
+      : item(first), hl(0), n_items(n_items_), n_groups(n_groups_), A(A_), stride(stride_), mh(mh_) {
     set();
   }
   __device__ void set() {
     if (item < n_items) {
       b = item / n_groups;
-      h0 = (item - b * n_groups) * MH;
-      nh = min(A, h0 + MH) - h0;
+      h0 = (item - b * n_groups) * mh;
+      nh = min(A, h0 + mh) - h0;
     }
   }
   __device__ bool valid() const { return item < n_items; }
@@ -128,7 +127,7 @@ struct HeadIter {
 template <int DP>
 __global__ void __launch_bounds__(kThreadsTC, 1)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const int32_t* __restrict__ mask, int B, int S,
-                        int A, int d, int hs, float scale, __half* __restrict__ ctx, int ldc, int8_t* __restrict__ ctxq, int ldq,
+                        int A, int d, int hs, int mh, float scale, __half* __restrict__ ctx, int ldc, int8_t* __restrict__ ctxq, int ldq,
                         float* __restrict__ ctxs, const uint8_t* __restrict__ qkv_rows, int row_bytes,
                         unsigned long long* __restrict__ trace) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -147,10 +146,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   using HC = HeadCfg<DP>;
-  constexpr int MH = HC::kMaxHeads;
-  using Iter = HeadIter<MH>;
+  using Iter = HeadIter;
   const int D = A * hs;  // QKV section width (head stride hs >= d; hs > d: zero-padded heads)
-  const int n_groups = (A + MH - 1) / MH;
+  const int n_groups = (A + mh - 1) / mh;  // items per sequence (mh heads each, mh <= 512 / DP)
   const int n_items = B * n_groups;
   const int it_first = (int)blockIdx.x;
   const int it_stride = (int)gridDim.x;
@@ -190,7 +188,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       (void)qkv_rows;
       (void)row_bytes;
       uint32_t n = 0;
-      for (Iter it(it_first, n_items, n_groups, A, it_stride); it.valid(); it.next(), ++n) {
+      for (Iter it(it_first, n_items, n_groups, A, it_stride, mh); it.valid(); it.next(), ++n) {
         const int slot = n % kKVStages;
         const int h = it.h0 + it.hl;
         uint8_t* base = smem + slot * SmemTC::SLOT;
@@ -233,7 +231,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         __syncwarp();
       };
       uint32_t n = 0;
-      for (Iter it(it_first, n_items, n_groups, A, it_stride); it.valid(); it.next(), ++n) {
+      for (Iter it(it_first, n_items, n_groups, A, it_stride, mh); it.valid(); it.next(), ++n) {
         const int slot = n % kKVStages;
         uint8_t* base = smem + slot * SmemTC::SLOT;
         mbar_wait(kv_full + slot, (n / kKVStages) & 1);
@@ -386,7 +384,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       return __ldg(mask + (size_t)(item / n_groups) * S + tid);
     };
     int mval = mask_of(it_first);
-    for (Iter it(it_first, n_items, n_groups, A, it_stride); it.valid(); it.next(), ++n) {
+    for (Iter it(it_first, n_items, n_groups, A, it_stride, mh); it.valid(); it.next(), ++n) {
       if (it.hl == 0) {
         // every softmax thread finished reading the previous item's mask
         // before this barrier
@@ -508,20 +506,42 @@ cudaError_t prepare_attention_tc_kernel() {
   return cudaFuncSetAttribute(attention_tc_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemTC::TOTAL);
 }
 
+// Heads per work item: the whole row (A heads) when the ctx requant is fused
+// (its row amax needs every head); otherwise the item size that minimises the
+// heads on the busiest CTA (ties: larger items, fewer item switches), so small
+// batches still spread over all SMs (C2: 64 sequences x 12 heads).
+static int heads_per_item(int B, int A, int max_heads, bool fused) {
+  if (fused) return A;
+  int best = max_heads < A ? max_heads : A;
+  long long best_cost = -1;
+  for (int mh = best; mh >= 1; --mh) {
+    const long long items = (long long)B * ((A + mh - 1) / mh);
+    const long long cost = ((items + kNumSMs - 1) / kNumSMs) * mh;
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = mh;
+    }
+  }
+  return best;
+}
+
 cudaError_t launch_attention_tc(const AttnTCPlan& plan, const int32_t* mask, int B, int S, int A, int d, int hs,
                                 __half* ctx, int ldctx, int8_t* ctxq, int ldq, float* ctxs, cudaStream_t s,
                                 unsigned long long* trace) {
   if (ctxq != nullptr && !attention_tc_fuses_quant(A, d)) return cudaErrorInvalidValue;
   const float scale = (float)(1.0 / sqrt((double)d));  // fp32(1/sqrt(d)) (R10)
-  const int mh = d <= 32 ? HeadCfg<32>::kMaxHeads : HeadCfg<64>::kMaxHeads;
+  const int max_heads = d <= 32 ? HeadCfg<32>::kMaxHeads : HeadCfg<64>::kMaxHeads;
+  const int mh = heads_per_item(B, A, max_heads, ctxq != nullptr);
   const int n_items = B * ((A + mh - 1) / mh);
   const int grid = n_items < kNumSMs ? n_items : kNumSMs;
   if (d <= 32)
     launch_ex(attention_tc_kernel<32>, dim3(grid), dim3(kThreadsTC), SmemTC::TOTAL, s, 0, plan.map, mask, B, S, A, d,
-              hs, scale, ctx, ldctx, ctxq, ldq, ctxs, static_cast<const uint8_t*>(plan.qkv), plan.ldqkv * 2, trace);
+              hs, mh, scale, ctx, ldctx, ctxq, ldq, ctxs, static_cast<const uint8_t*>(plan.qkv), plan.ldqkv * 2,
+              trace);
   else
     launch_ex(attention_tc_kernel<64>, dim3(grid), dim3(kThreadsTC), SmemTC::TOTAL, s, 0, plan.map, mask, B, S, A, d,
-              hs, scale, ctx, ldctx, ctxq, ldq, ctxs, static_cast<const uint8_t*>(plan.qkv), plan.ldqkv * 2, trace);
+              hs, mh, scale, ctx, ldctx, ctxq, ldq, ctxs, static_cast<const uint8_t*>(plan.qkv), plan.ldqkv * 2,
+              trace);
   return cudaGetLastError();
 }
 

@@ -103,8 +103,8 @@ struct ff_model {
   bool use_graphs = true;
   int pair_mode = -1;  // FF_OPT_CTA_PAIRS: -1 auto, 0 never (GemmPlan::force_pair)
   bool attn_tc = true;  // FF_OPT_ATTN_TC: tcgen05 attention where supported
-  int fused = 7;  // FF_OPT_FUSED_EPILOGUES / _MASK: cluster row-reduction GEMM epilogues,
-                 // bit 0 out-proj + LN1, bit 1 FFN1 + requant, bit 2 FFN2 + LN2 (default: all)
+  int fused = -1;  // FF_OPT_FUSED_EPILOGUES / _MASK: cluster row-reduction GEMM epilogues,
+                  // bit 0 out-proj + LN1, bit 1 FFN1 + requant, bit 2 FFN2 + LN2; -1 = auto
   int act_quant = 0;    // FF_OPT_ACT_QUANT: 0 per-row s8, 1 per-tensor u8 + zero point
   ff::LaunchPolicy launch{true, false};  // FF_OPT_PDL / FF_OPT_PDL_RR of this model's forwards
   ff::AttnTCPlan tm_qkv;  // QKV buffer map for the tcgen05 attention
@@ -125,6 +125,18 @@ struct ff_model {
 };
 
 namespace {
+
+// Fusions of one layer: an explicit FF_OPT_FUSED_MASK as given; auto (-1,
+// the default) fuses the FFN1 requant always and residual + LN into a GEMM
+// whose K row is at most 2 KB -- with longer K rows the single-CTA 128-row
+// tiles of the row-reduction kernel feed the tensor cores worse than the
+// CTA-pair GEMM + add_ln (measured: C4 fp16 FFN2 K = 3072 fused 337 us vs 220 +
+// 59 us; C3 int8 FFN2 K = 1536 B fused 67 us vs 41 + 35 us).
+int fused_mask(const ff_model* m, const LayerPlan& P) {
+  if (m->fused >= 0) return m->fused;
+  const int eb = P.dt == FF_I8 ? 1 : 2;
+  return 2 | (P.K[1] * eb <= 2048 ? 1 : 0) | (P.K[3] * eb <= 2048 ? 4 : 0);
+}
 
 void drop_graphs(ff_model* m) {
   for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second.exec);
@@ -338,9 +350,13 @@ ff_status dump(void* dst, const void* src, int ld_elems, int cols, int M, cudaSt
   return FF_OK;
 }
 
-// int8 layer whose ctx requant (a4) runs inside the tcgen05 attention kernel.
-bool attention_fuses_quant(const ff_model* m, const LayerPlan& P, int S) {
-  return P.dt == FF_I8 && m->attn_tc && ff::attention_tc_supported(S, m->cfg.head_dim, m->hs, m->ldqkv, m->ldc16) &&
+// int8 layer whose ctx requant (a4) runs inside the tcgen05 attention kernel:
+// the fused kernel needs a whole sequence per work item, so it is used only
+// when the batch alone fills the SMs (C3: B = 256); smaller batches (C2: 64)
+// spread heads over all SMs and requantize with quant_rows.
+bool attention_fuses_quant(const ff_model* m, const LayerPlan& P, int B, int S) {
+  return P.dt == FF_I8 && m->attn_tc && B >= ff::kNumSMs &&
+         ff::attention_tc_supported(S, m->cfg.head_dim, m->hs, m->ldqkv, m->ldc16) &&
          ff::attention_tc_fuses_quant(P.A, m->cfg.head_dim);
 }
 
@@ -420,7 +436,7 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     }
     // a3: fused masked-softmax attention over this layer's A'_l heads
     // (int8 layers: a4, the ctx requant, fused into the tcgen05 attention)
-    const bool att_q = attention_fuses_quant(m, P, S) && !pt;
+    const bool att_q = attention_fuses_quant(m, P, B, S) && !pt;
     if (m->attn_tc && ff::attention_tc_supported(S, c.head_dim, m->hs, m->ldqkv, m->ldc16))
       FF_LAUNCH(FF_K_ATTENTION,
                 ff::launch_attention_tc(m->tm_qkv, mask, B, S, P.A, c.head_dim, m->hs, (att_q && !tr) ? nullptr : CTX,
@@ -438,9 +454,10 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     // a4 + a5: requant (int8 layers) and out-projection
     if (q && !att_q && !pt)
       FF_LAUNCH(FF_K_QUANT, ff::launch_quant_rows(CTX, m->ldc16, M, P.D, CTXq, m->ldc8, CTXs, s), "quant ctx");
-    const bool fuse_ln = (m->fused & 1) && !pt && P.rr_ok[0];
-    const bool fuse_q = (m->fused & 2) && !pt && q && P.rr_ok[1];
-    const bool fuse_ln2 = (m->fused & 4) && !pt && P.rr_ok[0];
+    const int fm = fused_mask(m, P);
+    const bool fuse_ln = (fm & 1) && !pt && P.rr_ok[0];
+    const bool fuse_q = (fm & 2) && !pt && q && P.rr_ok[1];
+    const bool fuse_ln2 = (fm & 4) && !pt && P.rr_ok[0];
     if (fuse_ln) {
       // a5 + a6 fused: H1 = LN1(R16(O) + X16) (+ s8 rows) in the out-proj epilogue
       ff::RRPlan r = P.rp[0];
@@ -954,7 +971,7 @@ ff_status ff_set_option(ff_model* m, int32_t option, int64_t value) {
     return FF_OK;
   }
   if (option == FF_OPT_FUSED_MASK) {
-    if (value < 0 || value > 7) return fail(FF_E_INVALID, "FF_OPT_FUSED_MASK must be in 0..7");
+    if (value < -1 || value > 7) return fail(FF_E_INVALID, "FF_OPT_FUSED_MASK must be -1 (auto) or 0..7");
     m->fused = (int)value;
     drop_graphs(m);
     return FF_OK;
@@ -978,7 +995,7 @@ ff_status ff_get_option(const ff_model* m, int32_t option, int64_t* value) {
     case FF_OPT_GRAPHS: *value = m->use_graphs ? 1 : 0; return FF_OK;
     case FF_OPT_CTA_PAIRS: *value = m->pair_mode == 0 ? 0 : 1; return FF_OK;
     case FF_OPT_ATTN_TC: *value = m->attn_tc ? 1 : 0; return FF_OK;
-    case FF_OPT_FUSED_EPILOGUES: *value = m->fused == 7 ? 1 : 0; return FF_OK;
+    case FF_OPT_FUSED_EPILOGUES: *value = m->fused != 0 ? 1 : 0; return FF_OK;
     case FF_OPT_PDL: *value = m->launch.pdl ? 1 : 0; return FF_OK;
     case FF_OPT_ACT_QUANT: *value = m->act_quant; return FF_OK;
     case FF_OPT_FUSED_MASK: *value = m->fused; return FF_OK;
@@ -1003,7 +1020,6 @@ void ff_model_destroy(ff_model* m) {
 
 ff_status ff_launch_count(const ff_model* m, int32_t batch, int32_t seq, int32_t* count) {
   if (!m || !count) return fail(FF_E_INVALID, "null argument");
-  (void)batch;
   int n = 3;  // embed_ln + pooler + classifier
   for (const LayerPlan& P : m->L) {
     const bool q = P.dt == FF_I8;
@@ -1011,10 +1027,11 @@ ff_status ff_launch_count(const ff_model* m, int32_t batch, int32_t seq, int32_t
       n += 7 + (q ? 8 : 0);
       continue;
     }
-    const bool fln = (m->fused & 1) && P.rr_ok[0], fq = (m->fused & 2) && q && P.rr_ok[1];
-    const bool fln2 = (m->fused & 4) && P.rr_ok[0];
+    const int fm = fused_mask(m, P);
+    const bool fln = (fm & 1) && P.rr_ok[0], fq = (fm & 2) && q && P.rr_ok[1];
+    const bool fln2 = (fm & 4) && P.rr_ok[0];
     n += 2;                              // QKV GEMM + attention
-    n += (q && !attention_fuses_quant(m, P, seq)) ? 1 : 0;  // ctx requant
+    n += (q && !attention_fuses_quant(m, P, batch, seq)) ? 1 : 0;  // ctx requant
     n += fln ? 1 : 2;                    // out-proj (+ add_ln1)
     n += fq ? 1 : (q ? 2 : 1);           // FFN1 (+ requant)
     n += fln2 ? 1 : 2;                   // FFN2 (+ add_ln2)
