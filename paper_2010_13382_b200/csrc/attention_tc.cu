@@ -43,22 +43,20 @@ constexpr int kD = 64;              // columns of a Q / K / V head tile (TMA box
 template <int DP>
 struct HeadCfg {
   static constexpr int kMaxHeads = 512 / DP;
-  static constexpr int kHalf = DP / 2;         // O columns per half-row thread
   static constexpr int kPark = DP / 2;         // parking columns per head (packed fp16 pairs)
 };
 constexpr int kTileBytes = 128 * 128;  // 128 rows x 128 B (64 fp16)
 constexpr int kKVStages = 3;
 constexpr int kSoftmaxWarps = 8;
 constexpr int kThreadsTC = 64 + 32 * kSoftmaxWarps;
-constexpr uint32_t kTmemO = 128;    // O[2]: columns [128, 192), [192, 256)
 constexpr uint32_t kTmemCtx = 256;  // packed ctx [256, 256 + 32 * heads)
 
 struct SmemTC {
   static constexpr int SLOT = 3 * kTileBytes;                // Q, K, V of one head
   static constexpr int P = kKVStages * SLOT;                 // P[2]: 2 k-blocks of 64 keys, 128B-swizzled
-  static constexpr int MASK = P + 2 * 2 * kTileBytes;        // kKeys floats
-  static constexpr int RED = MASK + kKeys * 4;               // [3][2][128] floats: max, sum, amax
-  static constexpr int BAR = RED + 3 * 2 * kQ * 4;
+  static constexpr int MASK = P + 2 * 2 * kTileBytes;        // [2][kKeys] floats (per group)
+  static constexpr int RED = MASK + 2 * kKeys * 4;           // [2][128] floats: per-group row amax
+  static constexpr int BAR = RED + 2 * kQ * 4;
   static constexpr int TOTAL = BAR + 256 + 1024;             // barriers + alignment slack
   static_assert(TOTAL <= 227 * 1024, "smem budget");
 };
@@ -89,7 +87,6 @@ __device__ __forceinline__ void trace_ev(unsigned long long* trace, uint32_t n, 
     trace[((size_t)blockIdx.x * kTraceHeads + n) * 8 + e] = t;
   }
 }
-__device__ __forceinline__ void softmax_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 // Walk of the heads one CTA processes: items blockIdx.x, +gridDim.x, ...;
 // each item = (sequence b, heads [h0, h0 + nh)).
@@ -118,58 +115,61 @@ struct HeadIter {
 };
 
 // Per-head schedule (n = this CTA's head counter; every role walks the same
-// sequence).  The MMA thread issues S(n) = Q K^T before O(n-1) = P V, and the
-// softmax warps run the ctx epilogue of head n-1 after publishing P(n), so the
-// softmax of one head overlaps the P.V MMA of the previous one:
-//   MMA:     .. S(n) | O(n-1) | S(n+1) | O(n) ..
-//   softmax: .. softmax(n) -> P[n&1] | epilogue(n-1) from O[(n-1)&1] | softmax(n+1) ..
-// Buffers: Q/K/V x3 stages (smem), S x1 (TMEM), P x2 (smem), O x2 (TMEM).
+// sequence).  The 8 softmax warps form two groups of 4 (one warp per TMEM lane
+// quadrant, a thread owns a whole query row) that take alternate heads:
+// group G = n & 1 owns TMEM columns [128 G, 128 G + 128), where the MMA
+// computes S(n) and later, once the group has turned S into P, O(n) = P V
+// (first DP columns).  The MMA thread issues S(n) as soon as group G has read
+// O(n - 2), then O(n - 1) of the other group, so one group's softmax overlaps
+// the other's exp / P-store / epilogue and the MMAs:
+//   MMA:      .. S(n) | O(n-1) | S(n+1) | O(n) ..
+//   group G:  .. softmax(n) -> P[G] | epilogue(n) (O(n) from its S columns) ..
+// Buffers: Q/K/V x3 stages (smem), S/O x2 (TMEM, one per group), P x2 (smem),
+// parked int8 ctx [256, 512).
 template <int DP>
 __global__ void __launch_bounds__(kThreadsTC, 1)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const int32_t* __restrict__ mask, int B, int S,
-                        int A, int d, int hs, int mh, float scale, __half* __restrict__ ctx, int ldc, int8_t* __restrict__ ctxq, int ldq,
-                        float* __restrict__ ctxs, const uint8_t* __restrict__ qkv_rows, int row_bytes,
-                        unsigned long long* __restrict__ trace) {
+                        int A, int d, int hs, int mh, float scale, __half* __restrict__ ctx, int ldc,
+                        int8_t* __restrict__ ctxq, int ldq, float* __restrict__ ctxs,
+                        const uint8_t* __restrict__ qkv_rows, int row_bytes, unsigned long long* __restrict__ trace) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SmemTC::BAR);
   uint64_t* kv_full = bar + 0;    // [3] TMA -> MMA
   uint64_t* kv_empty = bar + 3;   // [3] MMA (after P.V) -> TMA
-  uint64_t* s_full = bar + 6;     // MMA1 -> softmax
-  uint64_t* s_empty = bar + 7;    // softmax (S read) -> MMA1
-  uint64_t* p_full = bar + 8;     // [2] softmax (P written) -> MMA2
-  uint64_t* o_full = bar + 10;    // [2] MMA2 -> epilogue
-  uint64_t* o_empty = bar + 12;   // [2] epilogue (O read) -> MMA2
+  uint64_t* s_full = bar + 6;     // [2] MMA (S in group G's columns) -> group G
+  uint64_t* p_full = bar + 8;     // [2] group G (P written, S consumed) -> MMA
+  uint64_t* o_full = bar + 10;    // [2] MMA (O in group G's columns) -> group G
+  uint64_t* t_free = bar + 12;    // [2] group G (O read) -> MMA: columns free for S(n + 2)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
-  float* sMask = reinterpret_cast<float*>(smem + SmemTC::MASK);
-  float* sRed = reinterpret_cast<float*>(smem + SmemTC::RED);
+  float* sMask = reinterpret_cast<float*>(smem + SmemTC::MASK);  // [2][kKeys]: per group
+  float* sRed = reinterpret_cast<float*>(smem + SmemTC::RED);    // [2][kQ]: per-group row amax
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   using HC = HeadCfg<DP>;
   using Iter = HeadIter;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int D = A * hs;  // QKV section width (head stride hs >= d; hs > d: zero-padded heads)
   const int n_groups = (A + mh - 1) / mh;  // items per sequence (mh heads each, mh <= 512 / DP)
   const int n_items = B * n_groups;
   const int it_first = (int)blockIdx.x;
   const int it_stride = (int)gridDim.x;
-  constexpr int kSoftmaxThreads = 32 * kSoftmaxWarps;
+  constexpr int kGroupThreads = 128;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmQKV);
     for (int i = 0; i < kKVStages; ++i) {
       mbar_init(kv_full + i, 1);
       mbar_init(kv_empty + i, 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(s_empty, kSoftmaxThreads);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(p_full + i, kSoftmaxThreads);
-      mbar_init(o_full + i, 1);
-      mbar_init(o_empty + i, kSoftmaxThreads);
+    for (int g = 0; g < 2; ++g) {
+      mbar_init(s_full + g, 1);
+      mbar_init(p_full + g, kGroupThreads);
+      mbar_init(o_full + g, 1);
+      mbar_init(t_free + g, kGroupThreads);
     }
     fence_barrier_init();
   }
   if (warp == 1) {
-    tmem_alloc(tmem_slot, 512);  // S [0,128), O[2] [128,256), packed ctx [256, 512)
+    tmem_alloc(tmem_slot, 512);  // S/O of group 0 [0,128), group 1 [128,256), packed ctx [256, 512)
     tmem_relinquish();
   }
   tc_fence_before();
@@ -202,98 +202,93 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     }
   } else if (warp == 1) {
     // all 32 lanes walk the schedule (they zero Q's padding columns when
-    // d < DP); lane 0 issues the MMAs and commits
-    {
-      const bool issuer = lane == 0;
-      constexpr uint32_t id1 = idesc_f16(kKeys, 0);  // S = Q K^T: N = 128 keys
-      constexpr uint32_t id2 = idesc_f16(DP, 1);     // O = P V:   N = DP, V MN-major
-      auto issue_pv = [&](uint32_t m) {
-        const int ps = m & 1;
-        const int slot = m % kKVStages;
-        mbar_wait(p_full + ps, (m >> 1) & 1);
-        if (issuer) trace_ev(trace, m, 5);
-        mbar_wait(o_empty + ps, ((m >> 1) & 1) ^ 1);
+    // hs < DP); lane 0 issues the MMAs and commits
+    const bool issuer = lane == 0;
+    constexpr uint32_t id1 = idesc_f16(kKeys, 0);  // S = Q K^T: N = 128 keys
+    constexpr uint32_t id2 = idesc_f16(DP, 1);     // O = P V:   N = DP, V MN-major
+    auto issue_pv = [&](uint32_t m) {
+      const int g = m & 1;
+      const int slot = m % kKVStages;
+      mbar_wait(p_full + g, (m >> 1) & 1);  // group g has written P(m) and read all of S(m)
+      if (issuer) {
+        trace_ev(trace, m, 5);
         tc_fence_after();
-        if (issuer) {
-          uint8_t* P = smem + SmemTC::P + ps * 2 * kTileBytes;
-          uint8_t* V = smem + slot * SmemTC::SLOT + 2 * kTileBytes;
+        uint8_t* P = smem + SmemTC::P + g * 2 * kTileBytes;
+        uint8_t* V = smem + slot * SmemTC::SLOT + 2 * kTileBytes;
 #pragma unroll
-          for (int k = 0; k < kKeys / 16; ++k) {
-            // A = P: k-block k/4 (64 keys), +32 B per 16 keys inside the 128B row
-            const uint64_t pd = make_sw128_desc(P + (k >> 2) * kTileBytes) + 2 * (k & 3);
-            // B = V (MN-major): 16 keys = two 8-row groups = 2048 B
-            const uint64_t vd = make_sw128_desc_mn(V + k * 2048);
-            mma_f16(tmem + kTmemO + ps * 64, pd, vd, id2, k != 0);
-          }
-          mma_commit(o_full + ps);
-          mma_commit(kv_empty + slot);  // Q/K/V of head m free once these MMAs complete
+        for (int k = 0; k < kKeys / 16; ++k) {
+          // A = P: k-block k/4 (64 keys), +32 B per 16 keys inside the 128B row
+          const uint64_t pd = make_sw128_desc(P + (k >> 2) * kTileBytes) + 2 * (k & 3);
+          // B = V (MN-major): 16 keys = two 8-row groups = 2048 B
+          const uint64_t vd = make_sw128_desc_mn(V + k * 2048);
+          mma_f16(tmem + g * 128, pd, vd, id2, k != 0);
         }
-        __syncwarp();
-      };
-      uint32_t n = 0;
-      for (Iter it(it_first, n_items, n_groups, A, it_stride, mh); it.valid(); it.next(), ++n) {
-        const int slot = n % kKVStages;
-        uint8_t* base = smem + slot * SmemTC::SLOT;
-        mbar_wait(kv_full + slot, (n / kKVStages) & 1);
-        if (issuer) trace_ev(trace, n, 1);
-        if (hs < DP) {
-          // head stride below the MMA granularity (d = 16 unpadded): the box
-          // also holds the next head's first columns; zero Q's columns
-          // [hs, DP) so they add nothing to Q.K^T (V's extra columns only
-          // reach O columns that are never stored).  Padded heads (hs = DP >
-          // d, e.g. d = 26) carry exact zeros in [d, hs) from the QKV GEMM.
-          for (int rr = lane; rr < 128; rr += 32)
-            for (int c = hs; c < DP; ++c)
-              *reinterpret_cast<__half*>(base + rr * 128 + (((c >> 3) ^ (rr & 7)) << 4) + (c & 7) * 2) =
-                  __float2half_rn(0.0f);
-          fence_async_smem();
-          __syncwarp();
-        }
-        mbar_wait(s_empty, (n & 1) ^ 1);
-        if (issuer) {
-          trace_ev(trace, n, 2);
-          tc_fence_after();
-          const uint64_t qd = make_sw128_desc(base), kd = make_sw128_desc(base + kTileBytes);
-#pragma unroll
-          for (int k = 0; k < DP / 16; ++k) mma_f16(tmem, qd + 2 * k, kd + 2 * k, id1, k != 0);
-          mma_commit(s_full);
-        }
-        __syncwarp();
-        if (n > 0) issue_pv(n - 1);
+        mma_commit(o_full + g);
+        mma_commit(kv_empty + slot);  // Q/K/V of head m free once these MMAs complete
       }
+      __syncwarp();
+    };
+    uint32_t n = 0;
+    for (Iter it(it_first, n_items, n_groups, A, it_stride, mh); it.valid(); it.next(), ++n) {
+      const int slot = n % kKVStages;
+      const int g = n & 1;
+      uint8_t* base = smem + slot * SmemTC::SLOT;
+      mbar_wait(kv_full + slot, (n / kKVStages) & 1);
+      if (issuer) trace_ev(trace, n, 1);
+      if (hs < DP) {
+        // head stride below the MMA granularity (d = 16 unpadded): the box
+        // also holds the next head's first columns; zero Q's columns
+        // [hs, DP) so they add nothing to Q.K^T (V's extra columns only
+        // reach O columns that are never stored).  Padded heads (hs = DP >
+        // d, e.g. d = 26) carry exact zeros in [d, hs) from the QKV GEMM.
+        for (int rr = lane; rr < 128; rr += 32)
+          for (int c = hs; c < DP; ++c)
+            *reinterpret_cast<__half*>(base + rr * 128 + (((c >> 3) ^ (rr & 7)) << 4) + (c & 7) * 2) =
+                __float2half_rn(0.0f);
+        fence_async_smem();
+        __syncwarp();
+      }
+      mbar_wait(t_free + g, ((n >> 1) & 1) ^ 1);  // group g has read O(n - 2) out of its columns
+      if (issuer) {
+        trace_ev(trace, n, 2);
+        tc_fence_after();
+        const uint64_t qd = make_sw128_desc(base), kd = make_sw128_desc(base + kTileBytes);
+#pragma unroll
+        for (int k = 0; k < DP / 16; ++k) mma_f16(tmem + g * 128, qd + 2 * k, kd + 2 * k, id1, k != 0);
+        mma_commit(s_full + g);
+      }
+      __syncwarp();
       if (n > 0) issue_pv(n - 1);
     }
+    if (n > 0) issue_pv(n - 1);
   } else {
-    const int q = warp & 3;             // TMEM lane quadrant
-    const int half = (warp - 2) >> 2;   // keys [64 half, 64 half + 64), O columns [DP/2 half, DP/2 half + DP/2)
-    constexpr int HW = HC::kHalf / 2;   // packed fp16 words of this thread's half-row of one head
-    // valid head_dim columns of this half (DP = 32, d = 26: 16 and 10)
-    const int vcols = min(max(d - half * HC::kHalf, 0), HC::kHalf);
+    const int G = (warp - 2) >> 2;  // ping-pong group: heads n with n & 1 == G
+    const int q = warp & 3;         // TMEM lane quadrant = rows [32 q, 32 q + 32)
     const int r = q * 32 + lane;
-    const int tid = threadIdx.x - 64;
+    const int gtid = threadIdx.x - 64 - kGroupThreads * G;  // 0..127 within the group
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-    float* redMax = sRed;
-    float* redSum = sRed + 2 * kQ;
-    float* redAmax = sRed + 4 * kQ;
+    const uint32_t treg = trow + G * 128;  // this group's S / O columns
+    float* gMask = sMask + G * kKeys;
     const bool fuse_q = ctxq != nullptr;
-    // the two warps sharing TMEM lane quadrant q (same rows, other key half)
-    const int pair_bar = 2 + q;
-    auto pair_sync = [pair_bar]() { asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory"); };
-    __half2 amax2 = __float2half2_rn(0.0f);  // |ctx| max of the row over the heads epilogued so far
+    auto both_sync = []() { asm volatile("bar.sync 2, 256;" ::: "memory"); };  // both groups (item end)
+    auto group_sync = [G]() { asm volatile("bar.sync %0, 128;" ::"r"(3 + G) : "memory"); };
+    const float2 cd2 = make_float2(scale, scale);
+    const float2 l2e = make_float2(1.4426950408889634f, 1.4426950408889634f);
+    constexpr int HW = DP / 2;  // packed fp16 words of one head's row
+    __half2 amax2 = __float2half2_rn(0.0f);  // |ctx| max of the row over this group's heads of the item
 
-    // Q8row of a finished item (R6-R8) is applied lazily: its packed fp16 ctx
-    // stays parked in TMEM and head j of it is quantized and stored by the
-    // epilogue of head j of the CTA's NEXT item, right before that head parks
-    // its own ctx in the same columns (all fused items have nh = A <= 8 heads),
-    // so no epilogue stalls on a whole item's requant; the CTA's last item is
-    // flushed after the loop.  Per row: its scale (sc, rs), sequence and head base.
+    // Q8row of a finished item (R6-R8): its packed fp16 ctx stays parked in
+    // TMEM; head j of it is quantized and stored by whichever group runs head
+    // j of the CTA's NEXT item, right before that head parks its own ctx in the
+    // same columns (fused items hold all A heads); the last item is flushed
+    // after the loop.  Both groups derive the same scale at the item end.
     bool qpend = false;
-    int qb = 0, qhbase = 0;
+    int qb = 0, qhbase = 0, qnh = 0;
     float qsc = 1.0f, qrs = 1.0f;
     auto flush_head = [&](int j) {  // quantize + store parked head j of the pending item
       uint32_t v[HW];
-      if constexpr (HW == 16) tmem_ld16(trow + kTmemCtx + j * HC::kPark + half * HW, v);
-      else tmem_ld8(trow + kTmemCtx + j * HC::kPark + half * HW, v);
+      if constexpr (HW == 32) tmem_ld32(trow + kTmemCtx + j * HC::kPark, v);
+      else tmem_ld16(trow + kTmemCtx + j * HC::kPark, v);
       tmem_wait_ld();
       uint32_t w[HW / 2];
 #pragma unroll
@@ -303,172 +298,177 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         w[i] = q8_quant4(a0, a1, qsc, qrs);
       }
       if (r < S) {
-        int8_t* row_q = ctxq + ((size_t)qb * S + r) * ldq + (qhbase + j) * d + half * HC::kHalf;
-        if (DP == 64 && d == 64) {  // this thread's 32 s8 values: one full 32-byte sector of the row
+        int8_t* row_q = ctxq + ((size_t)qb * S + r) * ldq + (qhbase + j) * d;
+        if (DP == 64 && d == 64) {  // the row's 64 s8 values: two 32-byte sectors
           uint4* dst = reinterpret_cast<uint4*>(row_q);
-          dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-          dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
-        } else {  // d even: 2-byte aligned pieces of the vcols valid values
+#pragma unroll
+          for (int c = 0; c < 4; ++c) dst[c] = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+        } else {  // d even: 2-byte aligned pieces of the d valid values
 #pragma unroll
           for (int i = 0; i < HW; ++i)
-            if (2 * i < vcols)
-              *reinterpret_cast<uint16_t*>(row_q + 2 * i) = (uint16_t)(w[i >> 1] >> ((i & 1) * 16));
+            if (2 * i < d) *reinterpret_cast<uint16_t*>(row_q + 2 * i) = (uint16_t)(w[i >> 1] >> ((i & 1) * 16));
         }
       }
-    };
-
-    // ctx epilogue of head m = head h of sequence b (local index hl): R16(O),
-    // fp16 store and/or parking in TMEM; after the item's last head, its row
-    // scale (the row amax over all heads).
-    auto epilogue = [&](uint32_t m, int b, int h, int hl, bool last, int nh) {
-      const int os = m & 1;
-      const size_t grow = (size_t)b * S + r;
-      mbar_wait(o_full + os, (m >> 1) & 1);
-      if (threadIdx.x == 64) trace_ev(trace, m, 6);
-      tc_fence_after();
-      uint32_t o[2 * HW];
-      if constexpr (HW == 16) tmem_ld32(trow + kTmemO + os * 64 + half * HC::kHalf, o);
-      else tmem_ld16(trow + kTmemO + os * 64 + half * HC::kHalf, o);
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(o_empty + os);
-      uint32_t pk[HW];
-#pragma unroll
-      for (int i = 0; i < HW; ++i) {
-        // O columns >= d (DP = 32, d = 26) hold the next head's values: zero
-        pk[i] = 2 * i < vcols ? pack_half2(__uint_as_float(o[2 * i]), __uint_as_float(o[2 * i + 1])) : 0u;
-        amax2 = __hmax2(amax2, __habs2(*reinterpret_cast<const __half2*>(&pk[i])));
-      }
-      if (ctx != nullptr && r < S) {
-        __half* row_c = ctx + grow * ldc + h * d + half * HC::kHalf;
-        if (DP == 64 && d == 64) {
-          uint4* dst = reinterpret_cast<uint4*>(row_c);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) dst[c] = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-        } else {  // d even: 4-byte aligned pairs
-#pragma unroll
-          for (int i = 0; i < HW; ++i)
-            if (2 * i < vcols) *reinterpret_cast<uint32_t*>(row_c + 2 * i) = pk[i];
-        }
-      }
-      if (!fuse_q) return;
-      if (qpend) flush_head(hl);  // frees parking slot hl (the load completed above)
-      if constexpr (HW == 16) tmem_st16(trow + kTmemCtx + hl * HC::kPark + half * HW, pk);
-      else tmem_st8(trow + kTmemCtx + hl * HC::kPark + half * HW, pk);
-      if (!last) return;
-      // row amax over both halves -> this item's row scale; its heads are
-      // quantized by the next item's epilogues (or after the loop)
-      tmem_wait_st();
-      redAmax[half * kQ + r] = fmaxf(__low2float(amax2), __high2float(amax2));
-      pair_sync();
-      const float am = fmaxf(redAmax[r], redAmax[kQ + r]);
-      pair_sync();  // both partners read redAmax before the next item's writes
-      amax2 = __float2half2_rn(0.0f);
-      qb = b;
-      qhbase = h - hl;
-      qpend = true;
-      (void)nh;
-      qsc = q8_scale(am);
-      qrs = __frcp_rn(qsc);
-      if (half == 0 && r < S) ctxs[grow] = qsc;
-      if (threadIdx.x == 64) trace_ev(trace, m, 7);
     };
 
     uint32_t n = 0;
-    bool pend = false;  // epilogue of head n-1 outstanding
-    int pb = 0, ph_ = 0, phl = 0, pnh = 0;
-    bool plast = false;
-    // key mask of an item's sequence (keys >= S masked), fetched one item ahead
-    auto mask_of = [&](int item) -> int {
-      if (item >= n_items || tid >= S) return 0;
-      return __ldg(mask + (size_t)(item / n_groups) * S + tid);
-    };
-    int mval = mask_of(it_first);
+    int mask_item = -1;
     for (Iter it(it_first, n_items, n_groups, A, it_stride, mh); it.valid(); it.next(), ++n) {
-      if (it.hl == 0) {
-        // every softmax thread finished reading the previous item's mask
-        // before this barrier
-        softmax_sync();
-        if (tid < kKeys) sMask[tid] = mval != 0 ? 0.0f : -INFINITY;
-        softmax_sync();
-        mval = mask_of(it.item + it.stride);
-      }
-      mbar_wait(s_full, n & 1);
-      if (threadIdx.x == 64) trace_ev(trace, n, 3);
-      tc_fence_after();
-      uint32_t raw[2][32];
-      tmem_ld32(trow + half * 64, raw[0]);
-      tmem_ld32(trow + half * 64 + 32, raw[1]);
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(s_empty);
-      // s = RN(raw * fp32(1/sqrt d)) (+ mask bias 0 / -inf in the same FFMA),
-      // the row max, x = s - max and e = exp2(x * log2 e): the oracle's
-      // rounding points (R9, R10; the exp itself is ex2.approx); packed fp32
-      // pairs throughout
-      const float2 cd2 = make_float2(scale, scale);
-      float2 s2[32];
-      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-      const float4* mk4 = reinterpret_cast<const float4*>(sMask) + half * 16;
-#pragma unroll
-      for (int j = 0; j < 64; j += 4) {
-        const float4 mk = mk4[j >> 2];
-        const uint32_t* rw = &raw[j >> 5][j & 31];
-        s2[j / 2] = fma2(make_float2(__uint_as_float(rw[0]), __uint_as_float(rw[1])), cd2, make_float2(mk.x, mk.y));
-        s2[j / 2 + 1] =
-            fma2(make_float2(__uint_as_float(rw[2]), __uint_as_float(rw[3])), cd2, make_float2(mk.z, mk.w));
-        m4[0] = fmaxf(m4[0], s2[j / 2].x);
-        m4[1] = fmaxf(m4[1], s2[j / 2].y);
-        m4[2] = fmaxf(m4[2], s2[j / 2 + 1].x);
-        m4[3] = fmaxf(m4[3], s2[j / 2 + 1].y);
-      }
-      float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-      redMax[half * kQ + r] = mx;
-      pair_sync();
-      mx = fmaxf(mx, redMax[(half ^ 1) * kQ + r]);
-      const float2 l2e = make_float2(1.4426950408889634f, 1.4426950408889634f), mxv = make_float2(mx, mx);
-      float2 l2a = make_float2(0.0f, 0.0f), l2b = make_float2(0.0f, 0.0f);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float2 e = mul2(sub2(s2[j], mxv), l2e);
-        s2[j] = make_float2(ex2f(e.x), ex2f(e.y));
-        if (j & 1) l2b = add2(l2b, s2[j]); else l2a = add2(l2a, s2[j]);
-      }
-      const float2 l2 = add2(l2a, l2b);
-      float l = l2.x + l2.y;
-      redSum[half * kQ + r] = l;
-      pair_sync();
-      l = redSum[r] + redSum[kQ + r];  // fixed order in both halves
-      const float inv = __frcp_rn(l);
-      const float2 inv2 = make_float2(inv, inv), lv2 = make_float2(l, l);
-      // P16 = R16(p) into k-block `half` of the K-major 128B-swizzled tile
-      // P[n&1]: 16B chunk c of row r at (c ^ (r & 7)).  P[n&1] was last read
-      // by O(n-2), complete since epilogue(n-2) passed o_full.
-      uint8_t* prow = smem + SmemTC::P + (n & 1) * 2 * kTileBytes + half * kTileBytes + r * 128;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        uint32_t w[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float2 pn = div2_cr(s2[c * 4 + i], lv2, inv2);  // IEEE e / l (R9)
-          w[i] = pack_half2(pn.x, pn.y);
+      const bool mine = (int)(n & 1) == G;
+      const bool item_last = it.hl == it.nh - 1;
+      if (mine) {
+        const uint32_t k = n >> 1;  // this group's head counter
+        const int h = it.h0 + it.hl;
+        if (it.item != mask_item) {  // key mask of the item's sequence (keys >= S masked)
+          group_sync();              // every group thread finished reading the previous mask
+          for (int j = gtid; j < kKeys; j += kGroupThreads)
+            gMask[j] = (j < S && __ldg(mask + (size_t)it.b * S + j) != 0) ? 0.0f : -INFINITY;
+          group_sync();
+          mask_item = it.item;
         }
-        *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+        mbar_wait(s_full + G, k & 1);
+        if (threadIdx.x == 64) trace_ev(trace, n, 3);
+        tc_fence_after();
+        // pass 1: s = RN(raw * fp32(1/sqrt d)) + mask bias (0 / -inf) in one
+        // FFMA2 per pair (R10), the row max over the 128 keys
+        float mx = -INFINITY;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t raw[32];
+          tmem_ld32(treg + c * 32, raw);
+          tmem_wait_ld();
+          const float2* mk = reinterpret_cast<const float2*>(gMask + c * 32);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float2 sv =
+                fma2(make_float2(__uint_as_float(raw[2 * j]), __uint_as_float(raw[2 * j + 1])), cd2, mk[j]);
+            mx = fmaxf(mx, fmaxf(sv.x, sv.y));
+          }
+        }
+        const float2 mxv = make_float2(mx, mx);
+        // pass 2: e = exp2((s - max) log2 e) in fp32 (R9), written back over S; row sum
+        float2 la = make_float2(0.0f, 0.0f), lb = make_float2(0.0f, 0.0f);
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t raw[32];
+          tmem_ld32(treg + c * 32, raw);
+          tmem_wait_ld();
+          const float2* mk = reinterpret_cast<const float2*>(gMask + c * 32);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float2 sv =
+                fma2(make_float2(__uint_as_float(raw[2 * j]), __uint_as_float(raw[2 * j + 1])), cd2, mk[j]);
+            const float2 t = mul2(sub2(sv, mxv), l2e);
+            const float2 e = make_float2(ex2f(t.x), ex2f(t.y));
+            if (j & 1) lb = add2(lb, e);
+            else la = add2(la, e);
+            raw[2 * j] = __float_as_uint(e.x);
+            raw[2 * j + 1] = __float_as_uint(e.y);
+          }
+          tmem_st32(treg + c * 32, raw);
+        }
+        tmem_wait_st();
+        const float2 l2 = add2(la, lb);
+        const float l = l2.x + l2.y;
+        const float rl = __frcp_rn(l);
+        const float2 lv = make_float2(l, l), rlv = make_float2(rl, rl);
+        // pass 3: P16 = R16(e / l) (IEEE quotient, R9) into the group's K-major
+        // 128B-swizzled P tile: key chunk c = 16-byte chunks 4 (c & 1) .. + 3 of
+        // k-block c >> 1, chunk cc of row r at (cc ^ (r & 7))
+        uint8_t* prow = smem + SmemTC::P + G * 2 * kTileBytes + r * 128;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t ev[32];
+          tmem_ld32(treg + c * 32, ev);
+          tmem_wait_ld();
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            uint32_t w[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int j = cc * 4 + i;
+              const float2 pv =
+                  div2_cr(make_float2(__uint_as_float(ev[2 * j]), __uint_as_float(ev[2 * j + 1])), lv, rlv);
+              w[i] = pack_half2(pv.x, pv.y);
+            }
+            const int pc = (c & 1) * 4 + cc;
+            *reinterpret_cast<uint4*>(prow + (c >> 1) * kTileBytes + ((pc ^ (r & 7)) << 4)) =
+                make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+        tc_fence_before();
+        fence_async_smem();
+        mbar_arrive(p_full + G);
+        if (threadIdx.x == 64) trace_ev(trace, n, 4);
+        // epilogue of this head: ctx = R16(O), O in the group's first DP columns
+        mbar_wait(o_full + G, k & 1);
+        if (threadIdx.x == 64) trace_ev(trace, n, 6);
+        tc_fence_after();
+        uint32_t o[DP];
+        if constexpr (DP == 64) {
+          tmem_ld32(treg, *reinterpret_cast<uint32_t(*)[32]>(o));
+          tmem_ld32(treg + 32, *reinterpret_cast<uint32_t(*)[32]>(o + 32));
+        } else {
+          tmem_ld32(treg, *reinterpret_cast<uint32_t(*)[32]>(o));
+        }
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(t_free + G);
+        uint32_t pk[HW];
+#pragma unroll
+        for (int i = 0; i < HW; ++i) {
+          // O columns >= d (padded or neighbouring head columns): zero
+          pk[i] = 2 * i < d ? pack_half2(__uint_as_float(o[2 * i]), __uint_as_float(o[2 * i + 1])) : 0u;
+          amax2 = __hmax2(amax2, __habs2(*reinterpret_cast<const __half2*>(&pk[i])));
+        }
+        if (ctx != nullptr && r < S) {
+          __half* row_c = ctx + ((size_t)it.b * S + r) * ldc + h * d;
+          if (DP == 64 && d == 64) {
+            uint4* dst = reinterpret_cast<uint4*>(row_c);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) dst[c] = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+          } else {  // d even: 4-byte aligned pairs
+#pragma unroll
+            for (int i = 0; i < HW; ++i)
+              if (2 * i < d) *reinterpret_cast<uint32_t*>(row_c + 2 * i) = pk[i];
+          }
+        }
+        if (fuse_q) {
+          if (qpend && it.hl < qnh) flush_head(it.hl);  // frees parking slot hl (its load completed)
+          if constexpr (HW == 32) tmem_st32(trow + kTmemCtx + it.hl * HC::kPark, *reinterpret_cast<uint32_t(*)[32]>(pk));
+          else tmem_st16(trow + kTmemCtx + it.hl * HC::kPark, *reinterpret_cast<uint32_t(*)[16]>(pk));
+          tmem_wait_st();
+        }
+        if (threadIdx.x == 64) trace_ev(trace, n, 7);
       }
-      fence_async_smem();
-      mbar_arrive(p_full + (n & 1));
-      if (threadIdx.x == 64) trace_ev(trace, n, 4);
-      if (pend) epilogue(n - 1, pb, ph_, phl, plast, pnh);
-      pend = true;
-      pb = it.b;
-      ph_ = it.h0 + it.hl;
-      phl = it.hl;
-      pnh = it.nh;
-      plast = it.hl == it.nh - 1;
+      if (fuse_q && item_last) {
+        // both groups: the row amax over all heads of the item -> its scale;
+        // the previous item's parked heads this group did not flush (the item
+        // had more heads than this one's flushing heads covered) are flushed
+        // first, so the parking columns are free for the next item
+        if (qpend) {
+          for (int j = it.nh; j < qnh; ++j)
+            if ((j & 1) == G) flush_head(j);
+        }
+        sRed[G * kQ + r] = fmaxf(__low2float(amax2), __high2float(amax2));
+        tc_fence_before();  // parked TMEM stores ordered before the other group's later reads
+        both_sync();
+        tc_fence_after();
+        const float am = fmaxf(sRed[r], sRed[kQ + r]);
+        both_sync();  // both groups read sRed before the next item's writes
+        amax2 = __float2half2_rn(0.0f);
+        qb = it.b;
+        qhbase = it.h0;
+        qnh = it.nh;
+        qpend = true;
+        qsc = q8_scale(am);
+        qrs = __frcp_rn(qsc);
+        if (G == 0 && r < S) ctxs[(size_t)it.b * S + r] = qsc;
+      }
     }
-    if (pend) epilogue(n - 1, pb, ph_, phl, plast, pnh);
-    if (qpend)
-      for (int j = 0; j < pnh; ++j) flush_head(j);
+    if (fuse_q && qpend)
+      for (int j = 0; j < qnh; ++j)
+        if ((j & 1) == G) flush_head(j);
   }
   tc_fence_before();
   __syncthreads();

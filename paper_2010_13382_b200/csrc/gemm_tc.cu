@@ -550,8 +550,8 @@ struct RRCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_OFF = kRRStages * STAGE_BYTES;                 // staging [warp] 2 KB
   static constexpr int PAR_OFF = EPI_OFF + kRREpiWarps * kRRStageTile;    // [bias|sw|gamma|beta][256] fp32
-  static constexpr int LOC_OFF = PAR_OFF + 4 * kRRBN * 4;                 // [G 2][hc 2][q 4][v 2][32] fp32
-  static constexpr int MYP_OFF = LOC_OFF + 2 * 2 * 4 * 2 * 32 * 4;        // [b 4][q 4][v 2][32] fp32
+  static constexpr int LOC_OFF = PAR_OFF + 4 * kRRBN * 4;                 // [G 2][par 2][hc 2][q 4][v 2][32] fp32
+  static constexpr int MYP_OFF = LOC_OFF + 2 * 2 * 2 * 4 * 2 * 32 * 4;    // [b 4][q 4][v 2][32] fp32
   static constexpr int RED_OFF = MYP_OFF + 4 * 4 * 2 * 32 * 4;            // [b 4][rank 8][q 4][v 2][32] fp32
   static constexpr int BAR_OFF = RED_OFF + 4 * kRRMaxCN * 4 * 2 * 32 * 4;
   static constexpr int SMEM = BAR_OFF + 512 + 1024;
@@ -701,7 +701,9 @@ __global__ void __launch_bounds__(kRRThreads, 1)
       const int nv = stats ? 2 : 1;
       const int b = 2 * G + (step & 1);
       const uint32_t ph = (uint32_t)(step >> 1) & 1u;
-      float* lg = loc + G * (2 * 4 * 2 * 32);
+      // in-CTA partials, double-buffered by exchange parity so that the next
+      // exchange's writes never alias the combining warp's reads
+      float* lg = loc + (2 * G + (step & 1)) * (2 * 4 * 2 * 32);
       lg[((hc * 4 + q) * 2 + 0) * 32 + lane] = v0;
       if (stats) lg[((hc * 4 + q) * 2 + 1) * 32 + lane] = v1;
       asm volatile("bar.sync %0, 64;" ::"r"(qbar) : "memory");
@@ -716,20 +718,27 @@ __global__ void __launch_bounds__(kRRThreads, 1)
         } else {
           r0 = fmaxf(a0, a1);
         }
-        float* mine = myp + ((b * 4 + q) * 2) * 32;
-        mine[lane] = r0;
-        if (stats) mine[32 + lane] = r1;
-        fence_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          // 4 quadrant copies of nv x 128 B from each of the CN CTAs
-          if (q == 0) mbar_expect_tx(&redbar[b], (uint32_t)(CN * 4 * nv * 128));
-          const uint32_t dst = smem_u32(red + (((b * kRRMaxCN + (int)rank) * 4 + q) * 2) * 32);
-          const uint32_t bl = smem_u32(&redbar[b]);
-          for (int c = 0; c < CN; ++c) bulk_copy_s2c(mapa_shared(dst, c), mine, nv * 128, mapa_shared(bl, c));
+        if (CN == 1) {  // a one-CTA cluster: the CTA partial is the row result
+          float* slot = red + (((b * kRRMaxCN) * 4 + q) * 2) * 32;
+          slot[lane] = r0;
+          if (stats) slot[32 + lane] = r1;
+        } else {
+          float* mine = myp + ((b * 4 + q) * 2) * 32;
+          mine[lane] = r0;
+          if (stats) mine[32 + lane] = r1;
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            // 4 quadrant copies of nv x 128 B from each of the CN CTAs
+            if (q == 0) mbar_expect_tx(&redbar[b], (uint32_t)(CN * 4 * nv * 128));
+            const uint32_t dst = smem_u32(red + (((b * kRRMaxCN + (int)rank) * 4 + q) * 2) * 32);
+            const uint32_t bl = smem_u32(&redbar[b]);
+            for (int c = 0; c < CN; ++c) bulk_copy_s2c(mapa_shared(dst, c), mine, nv * 128, mapa_shared(bl, c));
+          }
         }
       }
-      mbar_wait(&redbar[b], ph);
+      if (CN == 1) asm volatile("bar.sync %0, 64;" ::"r"(qbar) : "memory");
+      else mbar_wait(&redbar[b], ph);
       ++step;
       if (stats) {
         float msum = 0.0f;
