@@ -127,7 +127,7 @@ struct HeadIter {
 // Buffers: Q/K/V x3 stages (smem), S/O x2 (TMEM, one per group), P x2 (smem),
 // parked int8 ctx [256, 512).
 template <int DP>
-__global__ void __launch_bounds__(kThreadsTC, 1)
+__global__ void __maxnreg__(200)  // 320 threads, one CTA per SM: a thread holds a whole S row
     attention_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const int32_t* __restrict__ mask, int B, int S,
                         int A, int d, int hs, int mh, float scale, __half* __restrict__ ctx, int ldc,
                         int8_t* __restrict__ ctxq, int ldq, float* __restrict__ ctxs,
@@ -329,66 +329,54 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         mbar_wait(s_full + G, k & 1);
         if (threadIdx.x == 64) trace_ev(trace, n, 3);
         tc_fence_after();
-        // pass 1: s = RN(raw * fp32(1/sqrt d)) + mask bias (0 / -inf) in one
-        // FFMA2 per pair (R10), the row max over the 128 keys
-        float mx = -INFINITY;
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t raw[32];
-          tmem_ld32(treg + c * 32, raw);
-          tmem_wait_ld();
-          const float2* mk = reinterpret_cast<const float2*>(gMask + c * 32);
+        // the whole row of S in registers (4 loads, one wait): s = RN(raw *
+        // fp32(1/sqrt d)) + mask bias (0 / -inf) in one FFMA2 per pair (R10),
+        // the row max, e = exp2((s - max) log2 e) (R9) and the row sum in place
+        uint32_t v[128];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float2 sv =
-                fma2(make_float2(__uint_as_float(raw[2 * j]), __uint_as_float(raw[2 * j + 1])), cd2, mk[j]);
-            mx = fmaxf(mx, fmaxf(sv.x, sv.y));
-          }
+        for (int c = 0; c < 4; ++c) tmem_ld32(treg + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
+        tmem_wait_ld();
+        tc_fence_before();  // (S is read; the MMA overwrites these columns with O after p_full)
+        const float2* mk = reinterpret_cast<const float2*>(gMask);
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int j = 0; j < 64; ++j) {
+          const float2 sv = fma2(make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1])), cd2, mk[j]);
+          v[2 * j] = __float_as_uint(sv.x);
+          v[2 * j + 1] = __float_as_uint(sv.y);
+          m4[j & 1] = fmaxf(m4[j & 1], sv.x);
+          m4[2 + (j & 1)] = fmaxf(m4[2 + (j & 1)], sv.y);
         }
+        const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
         const float2 mxv = make_float2(mx, mx);
-        // pass 2: e = exp2((s - max) log2 e) in fp32 (R9), written back over S; row sum
         float2 la = make_float2(0.0f, 0.0f), lb = make_float2(0.0f, 0.0f);
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t raw[32];
-          tmem_ld32(treg + c * 32, raw);
-          tmem_wait_ld();
-          const float2* mk = reinterpret_cast<const float2*>(gMask + c * 32);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float2 sv =
-                fma2(make_float2(__uint_as_float(raw[2 * j]), __uint_as_float(raw[2 * j + 1])), cd2, mk[j]);
-            const float2 t = mul2(sub2(sv, mxv), l2e);
-            const float2 e = make_float2(ex2f(t.x), ex2f(t.y));
-            if (j & 1) lb = add2(lb, e);
-            else la = add2(la, e);
-            raw[2 * j] = __float_as_uint(e.x);
-            raw[2 * j + 1] = __float_as_uint(e.y);
-          }
-          tmem_st32(treg + c * 32, raw);
+        for (int j = 0; j < 64; ++j) {
+          const float2 t = mul2(sub2(make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1])), mxv), l2e);
+          const float2 e = make_float2(ex2f(t.x), ex2f(t.y));
+          if (j & 1) lb = add2(lb, e);
+          else la = add2(la, e);
+          v[2 * j] = __float_as_uint(e.x);
+          v[2 * j + 1] = __float_as_uint(e.y);
         }
-        tmem_wait_st();
         const float2 l2 = add2(la, lb);
         const float l = l2.x + l2.y;
         const float rl = __frcp_rn(l);
         const float2 lv = make_float2(l, l), rlv = make_float2(rl, rl);
-        // pass 3: P16 = R16(e / l) (IEEE quotient, R9) into the group's K-major
-        // 128B-swizzled P tile: key chunk c = 16-byte chunks 4 (c & 1) .. + 3 of
-        // k-block c >> 1, chunk cc of row r at (cc ^ (r & 7))
+        // P16 = R16(e / l) (IEEE quotient, R9) into the group's K-major
+        // 128B-swizzled P tile: keys [32 c, 32 c + 32) = 16-byte chunks
+        // 4 (c & 1) .. + 3 of k-block c >> 1, chunk cc of row r at (cc ^ (r & 7))
         uint8_t* prow = smem + SmemTC::P + G * 2 * kTileBytes + r * 128;
-#pragma unroll 1
+#pragma unroll
         for (int c = 0; c < 4; ++c) {
-          uint32_t ev[32];
-          tmem_ld32(treg + c * 32, ev);
-          tmem_wait_ld();
 #pragma unroll
           for (int cc = 0; cc < 4; ++cc) {
             uint32_t w[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              const int j = cc * 4 + i;
+              const int j = c * 16 + cc * 4 + i;
               const float2 pv =
-                  div2_cr(make_float2(__uint_as_float(ev[2 * j]), __uint_as_float(ev[2 * j + 1])), lv, rlv);
+                  div2_cr(make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1])), lv, rlv);
               w[i] = pack_half2(pv.x, pv.y);
             }
             const int pc = (c & 1) * 4 + cc;
