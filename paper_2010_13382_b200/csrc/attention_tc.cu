@@ -127,7 +127,7 @@ struct HeadIter {
 // Buffers: Q/K/V x3 stages (smem), S/O x2 (TMEM, one per group), P x2 (smem),
 // parked int8 ctx [256, 512).
 template <int DP>
-__global__ void __maxnreg__(192)  // 320 threads, one CTA per SM: a thread holds a whole S row
+__global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds a whole S row (a few spilled registers)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const int32_t* __restrict__ mask, int B, int S,
                         int A, int d, int hs, int mh, float scale, __half* __restrict__ ctx, int ldc,
                         int8_t* __restrict__ ctxq, int ldq, float* __restrict__ ctxs,
