@@ -528,8 +528,9 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
-        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines (rank / nranks) in the log
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines (rank / nranks) in the log,
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")  # on stderr: stdout carries only the JSON line
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = workload(args)
     # weak scaling: every rank owns B sequences per step (global batch world x B);

@@ -86,8 +86,8 @@ __device__ __forceinline__ void load_tile_async(__half* dst, const __half* src, 
 template <int DP>
 __global__ void __launch_bounds__(256, 1) attention_kernel(const __half* __restrict__ qkv, int ld,
                                                           const int32_t* __restrict__ mask, int B, int S, int A,
-                                                          int d, int hs, float scale, __half* __restrict__ ctx,
-                                                          int ldc, int nbuf) {
+                                                          int d, int hs, int hm_rows, float scale,
+                                                          __half* __restrict__ ctx, int ldc, int nbuf) {
   constexpr int LDS = DP + 8;
   constexpr int NT = KC / 8;  // n-tiles per chunk
   extern __shared__ __align__(16) uint8_t smem[];
@@ -98,7 +98,10 @@ __global__ void __launch_bounds__(256, 1) attention_kernel(const __half* __restr
   const size_t buf_bytes = buf_halves * 2 + (size_t)S16 * 4;
   // QKV sections of A heads of stride hs >= d (hs > d: zero-padded heads,
   // loaded whole so 16-byte copies apply); ctx rows are unpadded (h * d)
-  const int D = A * hs;
+  // head slice (t, h) of token r: row-major qkv + r * ld + t * A * hs + h * hs;
+  // head-major (hm_rows > 0, ld = 64) qkv + ((t * A + h) * hm_rows + r) * 64
+  const size_t sec = hm_rows > 0 ? (size_t)A * hm_rows * 64 : (size_t)A * hs;
+  const size_t hst = hm_rows > 0 ? (size_t)hm_rows * 64 : (size_t)hs;
   const int nqt = (S + QT - 1) / QT;
   const int n_items = B * A * nqt;
   const int dl = hs > d ? hs : d;  // columns copied per head (the rest of DP zero-filled)
@@ -113,9 +116,9 @@ __global__ void __launch_bounds__(256, 1) attention_kernel(const __half* __restr
     float* sMask = reinterpret_cast<float*>(base + buf_halves * 2);
     const size_t tok0 = (size_t)it.b * S;
     const int q0 = it.qt * QT;
-    load_tile_async<DP, LDS>(sQ, qkv + (tok0 + q0) * ld + it.h * hs, ld, min(QT, S - q0), QT, dl, vec);
-    load_tile_async<DP, LDS>(sK, qkv + tok0 * ld + D + it.h * hs, ld, S, S16, dl, vec);
-    load_tile_async<DP, LDS>(sV, qkv + tok0 * ld + 2 * D + it.h * hs, ld, S, S16, dl, vec);
+    load_tile_async<DP, LDS>(sQ, qkv + (tok0 + q0) * ld + it.h * hst, ld, min(QT, S - q0), QT, dl, vec);
+    load_tile_async<DP, LDS>(sK, qkv + tok0 * ld + sec + it.h * hst, ld, S, S16, dl, vec);
+    load_tile_async<DP, LDS>(sV, qkv + tok0 * ld + 2 * sec + it.h * hst, ld, S, S16, dl, vec);
     for (int i = threadIdx.x; i < S16; i += blockDim.x)
       sMask[i] = (i < S && __ldg(mask + tok0 + i) != 0) ? 0.0f : -INFINITY;
   };
@@ -296,8 +299,8 @@ size_t attn_buf_bytes(int S) {
 constexpr size_t kSmemMax = 227 * 1024;
 
 template <int DP>
-cudaError_t launch_dp(const __half* qkv, int ld, const int32_t* mask, int B, int S, int A, int d, int hs, __half* ctx,
-                      int ldc, cudaStream_t s) {
+cudaError_t launch_dp(const __half* qkv, int ld, const int32_t* mask, int B, int S, int A, int d, int hs,
+                      int hm_rows, __half* ctx, int ldc, cudaStream_t s) {
   const size_t one = attn_buf_bytes<DP>(S);
   if (one > kSmemMax) return cudaErrorInvalidValue;
   const int nbuf = 2 * one <= kSmemMax ? 2 : 1;
@@ -305,7 +308,8 @@ cudaError_t launch_dp(const __half* qkv, int ld, const int32_t* mask, int B, int
   const int n_items = B * A * ((S + QT - 1) / QT);
   const int per_sm = 1;  // ~240 registers x 256 threads: one resident CTA per SM
   const int grid = n_items < kNumSMs * per_sm ? n_items : kNumSMs * per_sm;
-  launch_ex(attention_kernel<DP>, dim3(grid), dim3(256), nbuf * one, s, 0, qkv, ld, mask, B, S, A, d, hs, scale, ctx, ldc,
+  launch_ex(attention_kernel<DP>, dim3(grid), dim3(256), nbuf * one, s, 0, qkv, ld, mask, B, S, A, d, hs, hm_rows, scale,
+            ctx, ldc,
             nbuf);
   return cudaGetLastError();
 }
@@ -326,11 +330,11 @@ size_t attention_smem_bytes(int S, int d) {
 }
 
 cudaError_t launch_attention(const __half* qkv, int ldqkv, const int32_t* mask, int B, int S, int A, int d, int hs,
-                             __half* ctx, int ldctx, cudaStream_t s) {
+                             int hm_rows, __half* ctx, int ldctx, cudaStream_t s) {
   const int w = hs > d ? hs : d;
-  if (w <= 32) return launch_dp<32>(qkv, ldqkv, mask, B, S, A, d, hs, ctx, ldctx, s);
-  if (w <= 64) return launch_dp<64>(qkv, ldqkv, mask, B, S, A, d, hs, ctx, ldctx, s);
-  return launch_dp<128>(qkv, ldqkv, mask, B, S, A, d, hs, ctx, ldctx, s);
+  if (w <= 32) return launch_dp<32>(qkv, ldqkv, mask, B, S, A, d, hs, hm_rows, ctx, ldctx, s);
+  if (w <= 64) return launch_dp<64>(qkv, ldqkv, mask, B, S, A, d, hs, hm_rows, ctx, ldctx, s);
+  return launch_dp<128>(qkv, ldqkv, mask, B, S, A, d, hs, hm_rows, ctx, ldctx, s);
 }
 
 }  // namespace ff

@@ -83,7 +83,7 @@ __device__ __forceinline__ Unit unit_of(int u, int nqb, int A) {
 template <int KC>
 __global__ void __launch_bounds__(kLThreads, 1)
     attention_long_kernel(const __grid_constant__ CUtensorMap tmQKV, const int32_t* __restrict__ mask, int B, int S,
-                          int A, float scale, __half* __restrict__ ctx, int ldc) {
+                          int A, int hm_rows, float scale, __half* __restrict__ ctx, int ldc) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SmemL::BAR);
@@ -145,9 +145,15 @@ __global__ void __launch_bounds__(kLThreads, 1)
       for (int u = u_begin; u < u_end; ++u) {
         const Unit x = unit_of(u, nqb, A);
         const int row0 = x.b * S;
-        load(x.h * kLD, row0 + x.qb * kLQ);
-        for (int c = 0; c < KC; ++c) load(D + x.h * kLD, row0 + c * 128);
-        for (int c = 0; c < KC; ++c) load(2 * D + x.h * kLD, row0 + c * 128);
+        if (hm_rows > 0) {  // head-major QKV: contiguous 128 x 64 blocks
+          load(0, x.h * hm_rows + row0 + x.qb * kLQ);
+          for (int c = 0; c < KC; ++c) load(0, (A + x.h) * hm_rows + row0 + c * 128);
+          for (int c = 0; c < KC; ++c) load(0, (2 * A + x.h) * hm_rows + row0 + c * 128);
+        } else {
+          load(x.h * kLD, row0 + x.qb * kLQ);
+          for (int c = 0; c < KC; ++c) load(D + x.h * kLD, row0 + c * 128);
+          for (int c = 0; c < KC; ++c) load(2 * D + x.h * kLD, row0 + c * 128);
+        }
       }
     }
   } else if (warp == 1) {
@@ -341,13 +347,13 @@ cudaError_t launch_attention_long(const AttnTCPlan& plan, const int32_t* mask, i
   const int kc = (S + 127) / 128;
   if (kc == 2)
     launch_ex(attention_long_kernel<2>, dim3(grid), dim3(kLThreads), SmemL::TOTAL, s, 0, plan.map, mask, B, S, A,
-              scale, ctx, ldctx);
+              plan.hm_rows, scale, ctx, ldctx);
   else if (kc == 3)
     launch_ex(attention_long_kernel<3>, dim3(grid), dim3(kLThreads), SmemL::TOTAL, s, 0, plan.map, mask, B, S, A,
-              scale, ctx, ldctx);
+              plan.hm_rows, scale, ctx, ldctx);
   else
     launch_ex(attention_long_kernel<4>, dim3(grid), dim3(kLThreads), SmemL::TOTAL, s, 0, plan.map, mask, B, S, A,
-              scale, ctx, ldctx);
+              plan.hm_rows, scale, ctx, ldctx);
   return cudaGetLastError();
 }
 

@@ -129,7 +129,7 @@ struct HeadIter {
 template <int DP>
 __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds a whole S row (a few spilled registers)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const int32_t* __restrict__ mask, int B, int S,
-                        int A, int d, int hs, int mh, float scale, __half* __restrict__ ctx, int ldc,
+                        int A, int d, int hs, int mh, int hm_rows, float scale, __half* __restrict__ ctx, int ldc,
                         int8_t* __restrict__ ctxq, int ldq, float* __restrict__ ctxs,
                         const uint8_t* __restrict__ qkv_rows, int row_bytes, unsigned long long* __restrict__ trace) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -195,9 +195,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds a whole S ro
         mbar_wait(kv_empty + slot, ((n / kKVStages) & 1) ^ 1);
         trace_ev(trace, n, 0);
         mbar_expect_tx(kv_full + slot, 3 * kTileBytes);
-        tma_load_2d(base, &tmQKV, kv_full + slot, h * hs, it.b * S, kEvictFirst);
-        tma_load_2d(base + kTileBytes, &tmQKV, kv_full + slot, D + h * hs, it.b * S, kEvictFirst);
-        tma_load_2d(base + 2 * kTileBytes, &tmQKV, kv_full + slot, 2 * D + h * hs, it.b * S, kEvictFirst);
+        if (hm_rows > 0) {  // head-major QKV: each slice is a contiguous 128 x 64 block
+          tma_load_2d(base, &tmQKV, kv_full + slot, 0, h * hm_rows + it.b * S, kEvictFirst);
+          tma_load_2d(base + kTileBytes, &tmQKV, kv_full + slot, 0, (A + h) * hm_rows + it.b * S, kEvictFirst);
+          tma_load_2d(base + 2 * kTileBytes, &tmQKV, kv_full + slot, 0, (2 * A + h) * hm_rows + it.b * S,
+                      kEvictFirst);
+        } else {
+          tma_load_2d(base, &tmQKV, kv_full + slot, h * hs, it.b * S, kEvictFirst);
+          tma_load_2d(base + kTileBytes, &tmQKV, kv_full + slot, D + h * hs, it.b * S, kEvictFirst);
+          tma_load_2d(base + 2 * kTileBytes, &tmQKV, kv_full + slot, 2 * D + h * hs, it.b * S, kEvictFirst);
+        }
       }
     }
   } else if (warp == 1) {
@@ -484,7 +491,16 @@ bool plan_attention_tc(AttnTCPlan* plan, const void* qkv, int M_rows, int ldqkv,
   // [M_rows x ldqkv] fp16, 64-column x 128-row boxes, 128B swizzle
   plan->qkv = qkv;
   plan->ldqkv = ldqkv;
+  plan->hm_rows = 0;
   return make_operand_map(&plan->map, qkv, M_rows, ldqkv, 2, (size_t)ldqkv * 2, 128, err);
+}
+
+bool plan_attention_tc_hm(AttnTCPlan* plan, const void* qkv, int n_blocks, int hm_rows, const char** err) {
+  // [n_blocks * hm_rows x 64] fp16 (128-byte rows), 128-row boxes, 128B swizzle
+  plan->qkv = qkv;
+  plan->ldqkv = 64;
+  plan->hm_rows = hm_rows;
+  return make_operand_map(&plan->map, qkv, n_blocks * hm_rows, 64, 2, 128, 128, err);
 }
 
 cudaError_t prepare_attention_tc_kernel() {
@@ -524,12 +540,12 @@ cudaError_t launch_attention_tc(const AttnTCPlan& plan, const int32_t* mask, int
   const int grid = n_items < kNumSMs ? n_items : kNumSMs;
   if (d <= 32)
     launch_ex(attention_tc_kernel<32>, dim3(grid), dim3(kThreadsTC), SmemTC::TOTAL, s, 0, plan.map, mask, B, S, A, d,
-              hs, mh, scale, ctx, ldctx, ctxq, ldq, ctxs, static_cast<const uint8_t*>(plan.qkv), plan.ldqkv * 2,
-              trace);
+              hs, mh, plan.hm_rows, scale, ctx, ldctx, ctxq, ldq, ctxs, static_cast<const uint8_t*>(plan.qkv),
+              plan.ldqkv * 2, trace);
   else
     launch_ex(attention_tc_kernel<64>, dim3(grid), dim3(kThreadsTC), SmemTC::TOTAL, s, 0, plan.map, mask, B, S, A, d,
-              hs, mh, scale, ctx, ldctx, ctxq, ldq, ctxs, static_cast<const uint8_t*>(plan.qkv), plan.ldqkv * 2,
-              trace);
+              hs, mh, plan.hm_rows, scale, ctx, ldctx, ctxq, ldq, ctxs, static_cast<const uint8_t*>(plan.qkv),
+              plan.ldqkv * 2, trace);
   return cudaGetLastError();
 }
 

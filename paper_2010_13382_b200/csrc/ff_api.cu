@@ -87,6 +87,11 @@ struct ff_model {
   // of the QKV buffer starts on a 16-byte boundary (TMA); for head_dim 26
   // (TinyBERT) the fused QKV GEMM writes zero-padded 32-column heads
   int hs = 0;
+  // head-major QKV buffer (hs = 64): [3 A heads x hm_rows, 64], every (section,
+  // head) slice of a sequence one contiguous block, so the attention's TMA tiles
+  // are contiguous 16 KB (the row-major layout reads 128 B from each of 128
+  // rows 3 KB apart); hm_rows = max_tokens rounded up to 256 (0: row-major)
+  int hm_rows = 0;
   bool any_i8 = false;
   // workspace pitches (elements) and offsets
   int ldx16, ldx8, ldqkv, ldc16, ldc8, ldi16, ldi8;
@@ -220,7 +225,8 @@ void plan_memory(ff_model* m) {
   m->ws_x16 = a.take(M * m->ldx16 * 2);
   m->ws_xq = q ? a.take(M * m->ldx8) : 0;
   m->ws_xs = q ? a.take(M * 4) : 0;
-  m->ws_qkv = a.take(M * m->ldqkv * 2);
+  m->hm_rows = m->hs == 64 ? round_up((int)M, 256) : 0;
+  m->ws_qkv = m->hm_rows > 0 ? a.take((size_t)3 * (m->Dqmax / 64) * m->hm_rows * 64 * 2) : a.take(M * m->ldqkv * 2);
   m->ws_ctx = a.take(M * m->ldc16 * 2);
   m->ws_ctxq = q ? a.take(M * m->ldc8) : 0;
   m->ws_ctxs = q ? a.take(M * 4) : 0;
@@ -272,8 +278,9 @@ ff_status build_gemm_plans(ff_model* m) {
         case W_FFN1: out = m->dWS + m->ws_i; ldo = m->ldi16; break;
         default: out = m->dWS + m->ws_o; ldo = m->ldx16; break;
       }
-      if (!ff::plan_gemm_output(&P.gp[i], out, ldo, &err))
-        return fail(FF_E_CUDA, std::string("output tensor map: ") + err);
+      const bool ok = (i == W_QKV && m->hm_rows > 0) ? ff::plan_gemm_output_hm(&P.gp[i], out, m->hm_rows, &err)
+                                                     : ff::plan_gemm_output(&P.gp[i], out, ldo, &err);
+      if (!ok) return fail(FF_E_CUDA, std::string("output tensor map: ") + err);
     }
     // fused row-reduction epilogues where the output row fits a cluster (N = 256 x 1..8)
     const bool q = P.dt == FF_I8;
@@ -416,22 +423,25 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     g.force_pair = m->pair_mode;
     ff::plan_gemm_set_m(&g, M);
     g.p.out = QKV;
-    g.p.ldo = m->ldqkv;
+    g.p.ldo = m->hm_rows > 0 ? 64 : m->ldqkv;
     g.p.bias = m->w<float>(P.bias[W_QKV]);
     g.p.row_scale = q ? Xs : nullptr;
     g.p.col_scale = q ? m->w<float>(P.sw[W_QKV]) : nullptr;
     g.p.act = ff::ACT_NONE;
     if (q && pt && tensor_quant(X16, m->ldx16, H, Xq, m->ldx8, g, P, W_QKV) != FF_OK) return FF_E_CUDA;
     FF_LAUNCH(q ? FF_K_GEMM_I8 : FF_K_GEMM_F16, ff::launch_gemm(g, s), "gemm qkv");
-    if (tr) {  // the trace holds the unpadded [M, 3 D] Q | K | V rows
-      if (m->hs == c.head_dim) {
+    if (tr) {  // the trace holds the unpadded row-major [M, 3 D] Q | K | V rows
+      if (m->hm_rows == 0 && m->hs == c.head_dim) {
         if (dump(d_dump[1], QKV, m->ldqkv, 3 * P.D, M, s) != FF_OK) return FF_E_CUDA;
       } else if (d_dump[1]) {
         for (int t = 0; t < 3; ++t)
-          for (int h = 0; h < P.A; ++h)
+          for (int h = 0; h < P.A; ++h) {
+            const __half* src = m->hm_rows > 0 ? QKV + (size_t)(t * P.A + h) * m->hm_rows * 64
+                                               : QKV + t * P.Dq + h * m->hs;
+            const size_t spitch = m->hm_rows > 0 ? 128 : (size_t)m->ldqkv * 2;
             FF_CK(cudaMemcpy2DAsync(static_cast<__half*>(d_dump[1]) + t * P.D + h * c.head_dim, (size_t)3 * P.D * 2,
-                                    QKV + t * P.Dq + h * m->hs, (size_t)m->ldqkv * 2, (size_t)c.head_dim * 2, M,
-                                    cudaMemcpyDeviceToDevice, s));
+                                    src, spitch, (size_t)c.head_dim * 2, M, cudaMemcpyDeviceToDevice, s));
+          }
       }
     }
     // a3: fused masked-softmax attention over this layer's A'_l heads
@@ -448,7 +458,8 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
                 "attention_long");
     else
       FF_LAUNCH(FF_K_ATTENTION,
-                ff::launch_attention(QKV, m->ldqkv, mask, B, S, P.A, c.head_dim, m->hs, CTX, m->ldc16, s),
+                ff::launch_attention(QKV, m->hm_rows > 0 ? 64 : m->ldqkv, mask, B, S, P.A, c.head_dim, m->hs,
+                                     m->hm_rows, CTX, m->ldc16, s),
                 "attention");
     if (tr && dump(d_dump[2], CTX, m->ldc16, P.D, M, s) != FF_OK) return FF_E_CUDA;
     // a4 + a5: requant (int8 layers) and out-projection
@@ -822,7 +833,10 @@ ff_status ff_finalize(ff_model* m, void* stream) {
   FF_CK(cudaStreamSynchronize(s));
   {
     const char* err = nullptr;
-    if (!ff::plan_attention_tc(&m->tm_qkv, m->dWS + m->ws_qkv, m->cfg.max_tokens, m->ldqkv, &err))
+    const bool ok = m->hm_rows > 0
+                        ? ff::plan_attention_tc_hm(&m->tm_qkv, m->dWS + m->ws_qkv, 3 * (m->Dqmax / 64), m->hm_rows, &err)
+                        : ff::plan_attention_tc(&m->tm_qkv, m->dWS + m->ws_qkv, m->cfg.max_tokens, m->ldqkv, &err);
+    if (!ok)
       return fail(FF_E_CUDA, std::string("attention tensor map: ") + err);
   }
   ff_status st = build_gemm_plans(m);
@@ -1153,7 +1167,7 @@ ff_status ff_debug_attention(const void* d_qkv16, const int32_t* d_mask, int32_t
                                       static_cast<cudaStream_t>(stream)));
     return FF_OK;
   }
-  FF_CK(ff::launch_attention(static_cast<const __half*>(d_qkv16), 3 * A * d, d_mask, B, S, A, d, d,
+  FF_CK(ff::launch_attention(static_cast<const __half*>(d_qkv16), 3 * A * d, d_mask, B, S, A, d, d, 0,
                              static_cast<__half*>(d_ctx16), A * d, static_cast<cudaStream_t>(stream)));
   return FF_OK;
 }

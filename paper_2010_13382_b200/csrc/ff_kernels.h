@@ -84,6 +84,10 @@ struct GemmParams {
   const float* tensor_qp;
   const int* colsum;
   int dbg_noload;  // debug MMA-rate probe: skip the operand loads (ff_debug_gemm bit 6; 0 in production)
+  // head-major output (the fused QKV projection, hs = 64): output column n goes
+  // to row (n / 64) * hm_rows + m, column n % 64 of a [heads * hm_rows, 64]
+  // buffer, so every (section, head) slice is one contiguous block; 0 = row-major
+  int hm_rows;
 };
 
 struct GemmPlan {
@@ -109,6 +113,9 @@ bool plan_gemm(GemmPlan* g, bool i8, const void* A, int M_rows, int lda, const v
                const char** err);
 // Bind the fp16 output buffer [M_rows x N] (pitch ldo elements) of a plan.
 bool plan_gemm_output(GemmPlan* g, void* out, int ldo, const char** err);
+// Bind a head-major fp16 output (see GemmParams::hm_rows): N / 64 blocks of
+// hm_rows x 64 (hm_rows >= M_rows, a multiple of 256 so no tile straddles two heads).
+bool plan_gemm_output_hm(GemmPlan* g, void* out, int hm_rows, const char** err);
 // Update the per-call fields (M) of a plan.
 void plan_gemm_set_m(GemmPlan* g, int M);
 cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t s);
@@ -186,7 +193,7 @@ size_t attention_smem_bytes(int S, int d);
 // mma.sync attention: QKV sections of A heads at head stride hs >= d (hs > d:
 // zero-padded head columns), ctx rows unpadded [B*S, ldctx] (head h at h * d).
 cudaError_t launch_attention(const __half* qkv, int ldqkv, const int32_t* mask, int B, int S, int A, int d, int hs,
-                             __half* ctx, int ldctx, cudaStream_t s);
+                             int hm_rows, __half* ctx, int ldctx, cudaStream_t s);
 
 // tcgen05 attention (head_dim 64 or <= 32 even -- padded to 32 --, S <= 128); the tensor map covers the QKV
 // buffer [M_rows x ldqkv] fp16 with 64-column x 128-row boxes.  Writes the
@@ -199,8 +206,14 @@ struct AttnTCPlan {
   CUtensorMap map;
   const void* qkv;  // QKV rows (contiguous: ldqkv fp16 per row)
   int ldqkv;
+  // 0: row-major [tokens, ldqkv] QKV; > 0: head-major [3 A heads x hm_rows, 64]
+  // (the map then has 64 columns and the head slice (t, h) of token r is row
+  // (t A + h) hm_rows + r)
+  int hm_rows;
 };
 bool plan_attention_tc(AttnTCPlan* plan, const void* qkv, int M_rows, int ldqkv, const char** err);
+// Head-major QKV buffer of n_blocks = 3 * Amax blocks of hm_rows x 64 fp16.
+bool plan_attention_tc_hm(AttnTCPlan* plan, const void* qkv, int n_blocks, int hm_rows, const char** err);
 cudaError_t launch_attention_tc(const AttnTCPlan& plan, const int32_t* mask, int B, int S, int A, int d, int hs,
                                 __half* ctx,
                                 int ldctx, int8_t* ctxq, int ldq, float* ctxs, cudaStream_t s,

@@ -488,7 +488,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             fence_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(&tmC, buf, n0, row0);
+              if (p.hm_rows > 0) tma_store_2d(&tmC, buf, n0 & 63, (n0 >> 6) * p.hm_rows + row0);
+              else tma_store_2d(&tmC, buf, n0, row0);
               bulk_commit();
             }
             if (tr0 && ci < 4) gemm_trace(p.trace, lt, 10 + 3 * ci);
@@ -1060,13 +1061,28 @@ bool plan_gemm(GemmPlan* g, bool i8, const void* A, int M_rows, int lda, const v
   g->p.trace = nullptr;
   g->p.tensor_qp = nullptr;
   g->p.colsum = nullptr;
+  g->p.hm_rows = 0;
   plan_gemm_set_m(g, M_rows);
   return true;
+}
+
+bool plan_gemm_output_hm(GemmPlan* g, void* out, int hm_rows, const char** err) {
+  if (hm_rows % 256 != 0 || hm_rows < g->M_rows || g->p.N % 64 != 0) {
+    *err = "head-major output needs N % 64 == 0 and hm_rows a multiple of 256 >= M_rows";
+    return false;
+  }
+  g->p.out = out;
+  g->p.ldo = 64;
+  g->p.hm_rows = hm_rows;
+  g->has_out_map = true;
+  return encode_2d(&g->tmC, out, (g->p.N / 64) * hm_rows, 64, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, 128, kEpiCols, 32,
+                   CU_TENSOR_MAP_SWIZZLE_64B, err);
 }
 
 bool plan_gemm_output(GemmPlan* g, void* out, int ldo, const char** err) {
   g->p.out = out;
   g->p.ldo = ldo;
+  g->p.hm_rows = 0;
   g->has_out_map = true;
   return encode_2d(&g->tmC, out, g->M_rows, g->p.N, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (size_t)ldo * 2, kEpiCols,
                    32, CU_TENSOR_MAP_SWIZZLE_64B, err);

@@ -3,7 +3,7 @@
 python tools/att_trace.py [B] [S] [A]
 Events: 0 load issued, 1 kv_full seen (MMA), 2 S MMA issued, 3 s_full seen
 (softmax), 4 P published, 5 p_full seen (MMA), 6 o_full seen (epilogue),
-7 epilogue done.  Prints per-head intervals (us) for a few CTAs and medians.
+7 epilogue done (events 3, 4, 6, 7 of softmax group 0 only: even heads).  Prints per-head intervals (us) for a few CTAs and medians.
 """
 import os
 import sys
@@ -25,10 +25,19 @@ grid = min(B, 148)
 trace = torch.zeros(grid, 32, 8, dtype=torch.int64, device="cuda")
 for _ in range(3):
     ffb.attention_q8(qkv, mask, A, d, with_ctx16=False)
-# flush L2 so QKV comes from HBM like in the forward
+# flush L2 so QKV comes from HBM (ATT_NOFLUSH=1: leave it warm)
 junk = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-junk.fill_(1)
+if not os.environ.get("ATT_NOFLUSH"):
+    junk.fill_(1)
 torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+ffb.attention_q8(qkv, mask, A, d, with_ctx16=False)
+e1.record()
+torch.cuda.synchronize()
+print("untraced launch %.1f us" % (e0.elapsed_time(e1) * 1e3))
+if not os.environ.get("ATT_NOFLUSH"):
+    junk.fill_(1)
 ffb.attention_q8(qkv, mask, A, d, with_ctx16=False, trace=trace)
 torch.cuda.synchronize()
 t = trace.cpu().numpy().astype(np.int64)
