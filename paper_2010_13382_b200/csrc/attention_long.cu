@@ -227,17 +227,28 @@ __global__ void __launch_bounds__(kLThreads, 1)
       }
       mbar_wait(s_full, n & 1);
       tc_fence_after();
-      // pass 1: row max of s = RN(raw * cd) + mask bias over this quarter of every chunk
+      // The three passes walk this quarter's keys in 16-column slices; the
+      // TMEM load of slice i + 1 is issued right after the wait for slice i,
+      // so it lands while slice i is processed (tcgen05.wait::ld waits for all
+      // outstanding loads, hence two alternating register buffers).
+      constexpr int NSL = 2 * KC;
+      auto col_of = [&](int sl) { return (uint32_t)((sl >> 1) * 128 + qt * 32 + (sl & 1) * 16); };
+      // pass 1: row max of s = RN(raw * cd) + mask bias
       float mx = -INFINITY;
-      for (int c = 0; c < KC; ++c) {
-        uint32_t raw[32];
-        tmem_ld32(trow + c * 128 + qt * 32, raw);
-        tmem_wait_ld();
-        const float2* mk = reinterpret_cast<const float2*>(sMask + c * 128 + qt * 32);
+      {
+        uint32_t buf[2][16];
+        tmem_ld16(trow + col_of(0), buf[0]);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float2 s = fma2(make_float2(__uint_as_float(raw[2 * j]), __uint_as_float(raw[2 * j + 1])), cd2, mk[j]);
-          mx = fmaxf(mx, fmaxf(s.x, s.y));
+        for (int sl = 0; sl < NSL; ++sl) {
+          tmem_wait_ld();
+          if (sl + 1 < NSL) tmem_ld16(trow + col_of(sl + 1), buf[(sl + 1) & 1]);
+          const float2* mk = reinterpret_cast<const float2*>(sMask + col_of(sl));
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float2 sv = fma2(make_float2(__uint_as_float(buf[sl & 1][2 * j]), __uint_as_float(buf[sl & 1][2 * j + 1])),
+                                   cd2, mk[j]);
+            mx = fmaxf(mx, fmaxf(sv.x, sv.y));
+          }
         }
       }
       redMax[qt * kLQ + r] = mx;
@@ -246,22 +257,27 @@ __global__ void __launch_bounds__(kLThreads, 1)
       const float2 mxv = make_float2(mx, mx);
       // pass 2: e = exp(s - max) in fp32, written back over S; row sum
       float2 la = make_float2(0.0f, 0.0f), lb = make_float2(0.0f, 0.0f);
-      for (int c = 0; c < KC; ++c) {
-        uint32_t raw[32];
-        tmem_ld32(trow + c * 128 + qt * 32, raw);
-        tmem_wait_ld();
-        const float2* mk = reinterpret_cast<const float2*>(sMask + c * 128 + qt * 32);
+      {
+        uint32_t buf[2][16];
+        tmem_ld16(trow + col_of(0), buf[0]);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float2 s = fma2(make_float2(__uint_as_float(raw[2 * j]), __uint_as_float(raw[2 * j + 1])), cd2, mk[j]);
-          const float2 t = mul2(sub2(s, mxv), l2e);
-          const float2 e = make_float2(ex2l(t.x), ex2l(t.y));
-          if (j & 1) lb = add2(lb, e);
-          else la = add2(la, e);
-          raw[2 * j] = __float_as_uint(e.x);
-          raw[2 * j + 1] = __float_as_uint(e.y);
+        for (int sl = 0; sl < NSL; ++sl) {
+          tmem_wait_ld();
+          if (sl + 1 < NSL) tmem_ld16(trow + col_of(sl + 1), buf[(sl + 1) & 1]);
+          const float2* mk = reinterpret_cast<const float2*>(sMask + col_of(sl));
+          uint32_t* v = buf[sl & 1];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float2 sv = fma2(make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1])), cd2, mk[j]);
+            const float2 t = mul2(sub2(sv, mxv), l2e);
+            const float2 e = make_float2(ex2l(t.x), ex2l(t.y));
+            if (j & 1) lb = add2(lb, e);
+            else la = add2(la, e);
+            v[2 * j] = __float_as_uint(e.x);
+            v[2 * j + 1] = __float_as_uint(e.y);
+          }
+          tmem_st16(trow + col_of(sl), *reinterpret_cast<uint32_t(*)[16]>(v));
         }
-        tmem_st32(trow + c * 128 + qt * 32, raw);
       }
       tmem_wait_st();
       const float2 l2 = add2(la, lb);
@@ -274,27 +290,36 @@ __global__ void __launch_bounds__(kLThreads, 1)
       // pass 3: P16 = R16(e / l) chunk by chunk into P[g & 1] (K-major, 128B
       // swizzle: 16-byte chunk cc of row r at (cc ^ (r & 7)); this quarter's
       // 32 keys = chunks 4 (qt & 1) .. + 3 of k-block qt >> 1)
-      for (int c = 0; c < KC; ++c, ++g) {
-        uint32_t ev[32];
-        tmem_ld32(trow + c * 128 + qt * 32, ev);
-        tmem_wait_ld();
-        mbar_wait(p_empty + (g & 1), ((g >> 1) & 1) ^ 1);  // P.V of chunk g - 2 has read the buffer
-        uint8_t* prow = smem + SmemL::P + (g & 1) * 2 * kLTile + (qt >> 1) * kLTile + r * 128;
+      {
+        uint32_t buf[2][16];
+        tmem_ld16(trow + col_of(0), buf[0]);
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          uint32_t w[4];
+        for (int sl = 0; sl < NSL; ++sl) {
+          tmem_wait_ld();
+          if (sl + 1 < NSL) tmem_ld16(trow + col_of(sl + 1), buf[(sl + 1) & 1]);
+          const uint32_t gg = g + (sl >> 1);  // P buffer of chunk sl / 2
+          if ((sl & 1) == 0) mbar_wait(p_empty + (gg & 1), ((gg >> 1) & 1) ^ 1);  // P.V of chunk gg - 2 done
+          uint8_t* prow = smem + SmemL::P + (gg & 1) * 2 * kLTile + (qt >> 1) * kLTile + r * 128;
+          const uint32_t* v = buf[sl & 1];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int j = cc * 4 + i;
-            const float2 p = div2_cr(make_float2(__uint_as_float(ev[2 * j]), __uint_as_float(ev[2 * j + 1])), lv, rlv);
-            w[i] = pack_half2(p.x, p.y);
+          for (int cc = 0; cc < 2; ++cc) {
+            uint32_t w[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int j = cc * 4 + i;
+              const float2 pv = div2_cr(make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1])), lv, rlv);
+              w[i] = pack_half2(pv.x, pv.y);
+            }
+            const int pc = (qt & 1) * 4 + (sl & 1) * 2 + cc;
+            *reinterpret_cast<uint4*>(prow + ((pc ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
           }
-          const int pc = (qt & 1) * 4 + cc;
-          *reinterpret_cast<uint4*>(prow + ((pc ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+          if (sl & 1) {
+            tc_fence_before();
+            fence_async_smem();
+            mbar_arrive(p_full + (gg & 1));
+          }
         }
-        tc_fence_before();
-        fence_async_smem();
-        mbar_arrive(p_full + (g & 1));
+        g += KC;
       }
       // epilogue: ctx = R16(O), fp16 rows; then TMEM is free for the next unit
       mbar_wait(o_full, n & 1);
