@@ -46,15 +46,17 @@ struct HeadCfg {
   static constexpr int kPark = DP / 2;         // parking columns per head (packed fp16 pairs)
 };
 constexpr int kTileBytes = 128 * 128;  // 128 rows x 128 B (64 fp16)
-constexpr int kKVStages = 3;
+// Q/K/V ring depth: P(n) is written over the dead Q and K tiles of head n's
+// own slot (S(n) has consumed them), so no separate P buffers are needed and a
+// 4th head fits in flight (192 KB of loads in flight per SM instead of 144 KB)
+constexpr int kKVStages = 4;
 constexpr int kSoftmaxWarps = 8;
 constexpr int kThreadsTC = 64 + 32 * kSoftmaxWarps;
 constexpr uint32_t kTmemCtx = 256;  // packed ctx [256, 256 + 32 * heads)
 
 struct SmemTC {
-  static constexpr int SLOT = 3 * kTileBytes;                // Q, K, V of one head
-  static constexpr int P = kKVStages * SLOT;                 // P[2]: 2 k-blocks of 64 keys, 128B-swizzled
-  static constexpr int MASK = P + 2 * 2 * kTileBytes;        // [2][kKeys] floats (per group)
+  static constexpr int SLOT = 3 * kTileBytes;                // Q, K, V of one head (P(n) over Q, K)
+  static constexpr int MASK = kKVStages * SLOT;              // [2][kKeys] floats (per group)
   static constexpr int RED = MASK + 2 * kKeys * 4;           // [2][128] floats: per-group row amax
   static constexpr int BAR = RED + 2 * kQ * 4;
   static constexpr int TOTAL = BAR + 256 + 1024;             // barriers + alignment slack
@@ -124,8 +126,8 @@ struct HeadIter {
 // the other's exp / P-store / epilogue and the MMAs:
 //   MMA:      .. S(n) | O(n-1) | S(n+1) | O(n) ..
 //   group G:  .. softmax(n) -> P[G] | epilogue(n) (O(n) from its S columns) ..
-// Buffers: Q/K/V x3 stages (smem), S/O x2 (TMEM, one per group), P x2 (smem),
-// parked int8 ctx [256, 512).
+// Buffers: Q/K/V x4 stages (smem; P(n) is written over head n's Q and K
+// tiles), S/O x2 (TMEM, one per group), parked int8 ctx [256, 512).
 template <int DP>
 __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds a whole S row (a few spilled registers)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const int32_t* __restrict__ mask, int B, int S,
@@ -135,13 +137,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds a whole S ro
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SmemTC::BAR);
-  uint64_t* kv_full = bar + 0;    // [3] TMA -> MMA
-  uint64_t* kv_empty = bar + 3;   // [3] MMA (after P.V) -> TMA
-  uint64_t* s_full = bar + 6;     // [2] MMA (S in group G's columns) -> group G
-  uint64_t* p_full = bar + 8;     // [2] group G (P written, S consumed) -> MMA
-  uint64_t* o_full = bar + 10;    // [2] MMA (O in group G's columns) -> group G
-  uint64_t* t_free = bar + 12;    // [2] group G (O read) -> MMA: columns free for S(n + 2)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+  uint64_t* kv_full = bar + 0;                 // [kKVStages] TMA -> MMA
+  uint64_t* kv_empty = bar + kKVStages;        // [kKVStages] MMA (after P.V) -> TMA
+  uint64_t* s_full = bar + 2 * kKVStages;      // [2] MMA (S in group G's columns) -> group G
+  uint64_t* p_full = s_full + 2;               // [2] group G (P written, S consumed) -> MMA
+  uint64_t* o_full = p_full + 2;               // [2] MMA (O in group G's columns) -> group G
+  uint64_t* t_free = o_full + 2;               // [2] group G (O read) -> MMA: columns free for S(n + 2)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_free + 2);
   float* sMask = reinterpret_cast<float*>(smem + SmemTC::MASK);  // [2][kKeys]: per group
   float* sRed = reinterpret_cast<float*>(smem + SmemTC::RED);    // [2][kQ]: per-group row amax
 
@@ -220,7 +222,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds a whole S ro
       if (issuer) {
         trace_ev(trace, m, 5);
         tc_fence_after();
-        uint8_t* P = smem + SmemTC::P + g * 2 * kTileBytes;
+        uint8_t* P = smem + slot * SmemTC::SLOT;  // P(m) over the Q, K tiles of m's slot
         uint8_t* V = smem + slot * SmemTC::SLOT + 2 * kTileBytes;
 #pragma unroll
         for (int k = 0; k < kKeys / 16; ++k) {
@@ -370,10 +372,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds a whole S ro
         const float l = l2.x + l2.y;
         const float rl = __frcp_rn(l);
         const float2 lv = make_float2(l, l), rlv = make_float2(rl, rl);
-        // P16 = R16(e / l) (IEEE quotient, R9) into the group's K-major
-        // 128B-swizzled P tile: keys [32 c, 32 c + 32) = 16-byte chunks
+        // P16 = R16(e / l) (IEEE quotient, R9) into a K-major 128B-swizzled
+        // P tile over this head's Q / K tiles: keys [32 c, 32 c + 32) = 16-byte chunks
         // 4 (c & 1) .. + 3 of k-block c >> 1, chunk cc of row r at (cc ^ (r & 7))
-        uint8_t* prow = smem + SmemTC::P + G * 2 * kTileBytes + r * 128;
+        // (over the Q and K tiles of this head's slot: S(n) has consumed them)
+        uint8_t* prow = smem + (n % kKVStages) * SmemTC::SLOT + r * 128;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
 #pragma unroll
