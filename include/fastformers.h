@@ -266,7 +266,9 @@ FF_API ff_status ff_debug_attention(const void *d_qkv16, const int32_t *d_mask, 
  * %globaltimer stamps (events documented in csrc/gemm_tc.cu); the buffer must
  * be zeroed by the caller.  which = 0: subsequent ff_debug_gemm launches;
  * 1 / 2 / 3: the layer-0 fused out-proj+LN / FFN1+requant / FFN2+LN GEMM of
- * subsequent forwards (FF_OPT_FUSED_EPILOGUES). */
+ * subsequent forwards (FF_OPT_FUSED_EPILOGUES); 4: the S > 128 attention of
+ * subsequent ff_debug_attention calls (uint64 [grid x 32 x 8], events in
+ * csrc/attention_long.cu). */
 FF_API ff_status ff_debug_set_trace(uint64_t *d_trace, int32_t which);
 
 /* The tcgen05 attention with the int8 ctx requant fused (a3 + a4; the path

@@ -68,6 +68,18 @@ __device__ __forceinline__ float ex2l(float x) {
   return y;
 }
 
+// Debug timeline (ff_debug_set_trace which = 4): %globaltimer of event e for
+// the CTA's unit k at trace[(cta * 32 + k) * 8 + e]: 0 Q load issued, 1 MMA saw
+// t_free, 2 S committed, 3 softmax saw s_full, 4 pass 1 done, 5 pass 2 done,
+// 6 last P chunk published, 7 O read (epilogue).
+__device__ __forceinline__ void ltrace(unsigned long long* tr, uint32_t k, int e) {
+  if (tr != nullptr && k < 32) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    tr[((size_t)blockIdx.x * 32 + k) * 8 + e] = t;
+  }
+}
+
 struct Unit {
   int b, qb, h;
 };
@@ -83,7 +95,8 @@ __device__ __forceinline__ Unit unit_of(int u, int nqb, int A) {
 template <int KC>
 __global__ void __launch_bounds__(kLThreads, 1)
     attention_long_kernel(const __grid_constant__ CUtensorMap tmQKV, const int32_t* __restrict__ mask, int B, int S,
-                          int A, int hm_rows, float scale, __half* __restrict__ ctx, int ldc) {
+                          int A, int hm_rows, float scale, __half* __restrict__ ctx, int ldc,
+                          unsigned long long* __restrict__ trace) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SmemL::BAR);
@@ -145,6 +158,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
       for (int u = u_begin; u < u_end; ++u) {
         const Unit x = unit_of(u, nqb, A);
         const int row0 = x.b * S;
+        ltrace(trace, (uint32_t)(u - u_begin), 0);
         if (hm_rows > 0) {  // head-major QKV: contiguous 128 x 64 blocks
           load(0, x.h * hm_rows + row0 + x.qb * kLQ);
           for (int c = 0; c < KC; ++c) load(0, (A + x.h) * hm_rows + row0 + c * 128);
@@ -164,6 +178,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
       for (int u = u_begin; u < u_end; ++u, ++n) {
         // TMEM (S chunks, O) free once the previous unit's epilogue read O
         mbar_wait(t_free, (n & 1) ^ 1);
+        ltrace(trace, n, 1);
         tc_fence_after();
         const int qslot = cnt % kLSlots;
         mbar_wait(full + qslot, (cnt / kLSlots) & 1);
@@ -181,6 +196,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
         }
         mma_commit(empty + qslot);
         mma_commit(s_full);
+        ltrace(trace, n, 2);
         for (int c = 0; c < KC; ++c, ++g) {
           const int vs = cnt % kLSlots;
           mbar_wait(full + vs, (cnt / kLSlots) & 1);
@@ -226,6 +242,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
         prev_b = x.b;
       }
       mbar_wait(s_full, n & 1);
+      if (threadIdx.x == 64) ltrace(trace, n, 3);
       tc_fence_after();
       // The three passes walk this quarter's keys in 16-column slices; the
       // TMEM load of slice i + 1 is issued right after the wait for slice i,
@@ -251,6 +268,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
           }
         }
       }
+      if (threadIdx.x == 64) ltrace(trace, n, 4);
       redMax[qt * kLQ + r] = mx;
       quad_sync();
       mx = fmaxf(fmaxf(redMax[r], redMax[kLQ + r]), fmaxf(redMax[2 * kLQ + r], redMax[3 * kLQ + r]));
@@ -280,6 +298,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
         }
       }
       tmem_wait_st();
+      if (threadIdx.x == 64) ltrace(trace, n, 5);
       const float2 l2 = add2(la, lb);
       redSum[qt * kLQ + r] = l2.x + l2.y;
       quad_sync();
@@ -321,6 +340,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
         }
         g += KC;
       }
+      if (threadIdx.x == 64) ltrace(trace, n, 6);
       // epilogue: ctx = R16(O), fp16 rows; then TMEM is free for the next unit
       mbar_wait(o_full, n & 1);
       tc_fence_after();
@@ -329,6 +349,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(t_free);
+      if (threadIdx.x == 64) ltrace(trace, n, 7);
       const int qrow = x.qb * kLQ + r;
       if (qrow < S) {
         uint32_t pk[8];
@@ -364,7 +385,7 @@ cudaError_t prepare_attention_long_kernel() {
 }
 
 cudaError_t launch_attention_long(const AttnTCPlan& plan, const int32_t* mask, int B, int S, int A, __half* ctx,
-                                  int ldctx, cudaStream_t s) {
+                                  int ldctx, cudaStream_t s, unsigned long long* trace) {
   if (S <= 128 || S > kLMaxKeys) return cudaErrorInvalidValue;
   const float scale = (float)(1.0 / sqrt((double)kLD));  // fp32(1/sqrt(d)) (R10)
   const int n_units = B * ((S + kLQ - 1) / kLQ) * A;
@@ -372,13 +393,13 @@ cudaError_t launch_attention_long(const AttnTCPlan& plan, const int32_t* mask, i
   const int kc = (S + 127) / 128;
   if (kc == 2)
     launch_ex(attention_long_kernel<2>, dim3(grid), dim3(kLThreads), SmemL::TOTAL, s, 0, plan.map, mask, B, S, A,
-              plan.hm_rows, scale, ctx, ldctx);
+              plan.hm_rows, scale, ctx, ldctx, trace);
   else if (kc == 3)
     launch_ex(attention_long_kernel<3>, dim3(grid), dim3(kLThreads), SmemL::TOTAL, s, 0, plan.map, mask, B, S, A,
-              plan.hm_rows, scale, ctx, ldctx);
+              plan.hm_rows, scale, ctx, ldctx, trace);
   else
     launch_ex(attention_long_kernel<4>, dim3(grid), dim3(kLThreads), SmemL::TOTAL, s, 0, plan.map, mask, B, S, A,
-              plan.hm_rows, scale, ctx, ldctx);
+              plan.hm_rows, scale, ctx, ldctx, trace);
   return cudaGetLastError();
 }
 

@@ -1164,7 +1164,8 @@ ff_status ff_debug_attention(const void* d_qkv16, const int32_t* d_mask, int32_t
                                     nullptr, static_cast<cudaStream_t>(stream)));
     else
       FF_CK(ff::launch_attention_long(map, d_mask, B, S, A, static_cast<__half*>(d_ctx16), A * d,
-                                      static_cast<cudaStream_t>(stream)));
+                                      static_cast<cudaStream_t>(stream),
+                                      g_debug_trace_which == 4 ? g_debug_trace : nullptr));
     return FF_OK;
   }
   FF_CK(ff::launch_attention(static_cast<const __half*>(d_qkv16), 3 * A * d, d_mask, B, S, A, d, d, 0,

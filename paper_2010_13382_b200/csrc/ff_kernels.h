@@ -224,7 +224,7 @@ cudaError_t prepare_attention_tc_kernel();
 // ctx rows [B*S, ldctx]; the same QKV tensor map as attention_tc.
 bool attention_long_supported(int S, int d, int ldqkv, int ldctx);
 cudaError_t launch_attention_long(const AttnTCPlan& plan, const int32_t* mask, int B, int S, int A, __half* ctx,
-                                  int ldctx, cudaStream_t s);
+                                  int ldctx, cudaStream_t s, unsigned long long* trace = nullptr);
 cudaError_t prepare_attention_long_kernel();
 
 // ------------------------------------------------------- weight packing
