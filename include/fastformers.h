@@ -298,7 +298,9 @@ FF_API ff_status ff_debug_attention_q8(const void *d_qkv16, const int32_t *d_mas
  * Errors: ff_scorer_last_error() (thread-local).  Same call order as the
  * model: create -> memory -> bind -> load_weights x N -> finalize -> score*.
  * cfg: as for ff_model_create (dtype ignored: fp32 throughout; C <= 64);
- * workspace grows with max_tokens * (layers x (12 H + 4 D + 2 F + A * max_positions)). */
+ * workspace grows with max_tokens * (layers x (12 H + 4 D + 2 F + A * max_positions));
+ * the weight arena holds the fp32 weights plus four TF32 split copies of each
+ * linear's weight (about 5x the linears' fp32 bytes). */
 typedef struct ff_scorer ff_scorer;
 FF_API const char *ff_scorer_last_error(void);
 FF_API ff_status ff_scorer_create(const ff_config *cfg, int32_t cuda_device, ff_scorer **out);
@@ -311,7 +313,10 @@ FF_API ff_status ff_scorer_bind_memory(ff_scorer *s, void *d_weights, size_t wei
  * return); FF_E_SHAPE for an unknown name or a wrong shape. */
 FF_API ff_status ff_scorer_load_weights(ff_scorer *s, const char *name, const float *h_data, const int64_t *shape,
                                         int32_t rank, void *stream);
-/* FF_E_STATE unless every tensor was loaded. */
+/* FF_E_STATE unless every tensor was loaded.  Derives the TF32 hi / lo splits
+ * of the linears' weights (and their transposes) inside the weight arena;
+ * synchronizes `stream`.  Loading a tensor after finalize requires finalizing
+ * again (ff_score_batch returns FF_E_STATE until then). */
 FF_API ff_status ff_scorer_finalize(ff_scorer *s, void *stream);
 /* One batch (device buffers, async on `stream`): d_ids / d_mask int32 [B, S]
  * (mask[b][0] must be 1), d_labels int32 [B] in [0, C).  Accumulates into
@@ -328,6 +333,15 @@ FF_API ff_status ff_score_batch(ff_scorer *s, const int32_t *d_ids, const int32_
  * mask[b][0] != 1, or a label outside [0, C) (such inputs are read as 0, never
  * out of bounds, and that batch's scores are not meaningful), else FF_OK. */
 FF_API ff_status ff_scorer_check(ff_scorer *s, void *stream);
+/* Scorer options (any time after create; apply to later ff_score_batch calls).
+ * FF_SCORER_OPT_TC_LINEARS (default 1): the eight linears per layer (QKV,
+ *   out-proj, FFN1, FFN2 and their input gradients) run on the tcgen05 tensor
+ *   cores as 3xTF32 (hi / lo TF32 splits, fp32 accumulation: fp32-level error,
+ *   DESIGN §6 "importance scorer"); 0 = the SIMT fp32 SGEMM.  The per-head
+ *   attention products always use the SIMT SGEMM.
+ * FF_E_INVALID for an unknown option or value. */
+#define FF_SCORER_OPT_TC_LINEARS 1
+FF_API ff_status ff_scorer_set_option(ff_scorer *s, int32_t option, int32_t value);
 /* Frees host state only (the arenas belong to the caller). */
 FF_API void ff_scorer_destroy(ff_scorer *s);
 

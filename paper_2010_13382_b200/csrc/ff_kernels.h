@@ -103,7 +103,7 @@ struct GemmPlan {
 };
 
 // Encode a 2-D K-major tensor map for a GEMM operand: rows x cols elements of
-// `elem_bytes` (2 fp16 / 1 int8), row pitch in bytes, box = box_rows x 128 B,
+// `elem_bytes` (4 fp32 / 2 fp16 / 1 int8), row pitch in bytes, box = box_rows x 128 B,
 // 128-byte swizzle, zero fill out of bounds.
 bool make_operand_map(CUtensorMap* map, const void* base, int rows, int cols, int elem_bytes, size_t pitch_bytes,
                       int box_rows, const char** err);
@@ -237,5 +237,17 @@ cudaError_t launch_add_row(const float* src, int N, int K, const float* row, flo
 cudaError_t prepare_gemm_kernels();
 cudaError_t prepare_attention_kernels();
 cudaError_t prepare_row_kernels();
+
+// ---- importance scorer: 3xTF32 tcgen05 GEMM (gemm_x3.cu)
+// C[M x N] (+)= A[M x K] B[N x K]^T (+ bias[N]) with A = Ah + Al and B = Bh + Bl
+// given as TF32 hi / lo splits (row pitch lda / ldb floats, multiples of 4,
+// zero-padded beyond K); C has row pitch ldc.  *err set on a setup failure.
+cudaError_t launch_gemm_x3(const float* Ah, const float* Al, int lda, const float* Bh, const float* Bl, int ldb,
+                           int M, int N, int K, const float* bias, float* C, int ldc, bool accumulate, cudaStream_t s,
+                           const char** err);
+// hi / lo split of X [M x K] (pitch ldx) into [M x ldo] buffers (ldo % 4 == 0, >= K; zero-padded).
+cudaError_t launch_split_tf32(const float* X, int M, int K, int ldx, float* hi, float* lo, int ldo, cudaStream_t s);
+// hi / lo split of W^T for W [N x K] (pitch K): outputs [K x ldo] (ldo % 4 == 0, >= N; zero-padded).
+cudaError_t launch_split_tf32_t(const float* W, int N, int K, float* hi, float* lo, int ldo, cudaStream_t s);
 
 }  // namespace ff

@@ -1025,7 +1025,10 @@ static bool encode_2d(CUtensorMap* map, const void* base, int rows, int cols, CU
 bool make_operand_map(CUtensorMap* map, const void* base, int rows, int cols, int elem_bytes, size_t pitch_bytes,
                       int box_rows, const char** err) {
   return encode_2d(map, base, rows, cols,
-                   elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, elem_bytes,
+                   elem_bytes == 4   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                   : elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                     : CU_TENSOR_MAP_DATA_TYPE_UINT8,
+                   elem_bytes,
                    pitch_bytes, 128 / elem_bytes, box_rows, CU_TENSOR_MAP_SWIZZLE_128B, err);
 }
 

@@ -538,10 +538,20 @@ const char* kSLayer[16] = {
     "attention.output.LayerNorm.bias", "intermediate.dense.weight", "intermediate.dense.bias",
     "output.dense.weight", "output.dense.bias", "output.LayerNorm.weight", "output.LayerNorm.bias"};
 
+struct XSplit {
+  size_t h = 0, l = 0;  // hi / lo offsets in the weight arena
+  int ld = 0;           // row pitch (floats, multiple of 4)
+};
+inline int round4(int x) { return (x + 3) & ~3; }
+
 struct SLayer {
   int A, D, F;
   size_t wqkv, bqkv, wo, bo, g1, b1, w1, bi1, w2, bi2, g2, b2;  // weight offsets
   size_t X, QKV, P, Cx, Y1, XH1, R1, U, Act, XH2, R2;          // saved activations (workspace)
+  // TF32 hi / lo splits of the linears' weights for the tcgen05 path (weight
+  // arena, written by ff_scorer_finalize): W [N x K] as [N x round4(K)] (forward
+  // B operand) and W^T as [K x round4(N)] (input-gradient B operand).
+  XSplit qkv, qkvT, o, oT, f1, f1T, f2, f2T;
   uint32_t loaded = 0;
 };
 
@@ -556,7 +566,9 @@ struct ff_scorer {
   uint32_t top_loaded = 0;
   size_t wbytes = 0, wsbytes = 0;
   size_t Xout, dX, dZ, dY1, dAm, dC, dP, dQKV, colg, lossb, errf, skws, headws, ids, mask, labels;
-  int Dmax = 0, Fmax = 0, Amax = 0;
+  size_t xh = 0, xl = 0;  // TF32 hi / lo split of the current linear's input [M x round4(Kmax)]
+  int Dmax = 0, Fmax = 0, Amax = 0, Kmax = 0;
+  int tc_linears = 1;     // FF_SCORER_OPT_TC_LINEARS
   uint8_t* dW = nullptr;
   uint8_t* dWS = nullptr;
   float* w(size_t o) const { return reinterpret_cast<float*>(dW + o); }
@@ -601,6 +613,24 @@ void plan_scorer(ff_scorer* m) {
     P.g2 = take(H);
     P.b2 = take(H);
   }
+  // TF32 hi / lo splits of the four linears' weights and of their transposes
+  auto split = [&](XSplit& x, size_t rows, int cols) {
+    x.ld = round4(cols);
+    x.h = take(rows * x.ld);
+    x.l = take(rows * x.ld);
+  };
+  for (int l = 0; l < c.num_layers; ++l) {
+    SLayer& P = m->L[l];
+    split(P.qkv, 3 * (size_t)P.D, (int)H);
+    split(P.qkvT, H, 3 * P.D);
+    split(P.o, H, P.D);
+    split(P.oT, P.D, (int)H);
+    split(P.f1, P.F, (int)H);
+    split(P.f1T, H, P.F);
+    split(P.f2, H, P.F);
+    split(P.f2T, P.F, (int)H);
+    m->Kmax = std::max(m->Kmax, std::max((int)H, std::max(3 * P.D, P.F)));
+  }
   m->pw = take(H * H);
   m->pb = take(H);
   m->cw = take((size_t)c.num_classes * H);
@@ -634,6 +664,8 @@ void plan_scorer(ff_scorer* m) {
   m->skws = take(4 * M * std::max((size_t)H, (size_t)m->Dmax));  // split-K partials
   m->headws = take(2 * M * H);                                     // head: pool, dpre [B x H] each
   m->lossb = take(M);
+  m->xh = take(M * round4(m->Kmax));
+  m->xl = take(M * round4(m->Kmax));
   m->errf = take(64);
   m->wsbytes = o;
 }
@@ -669,6 +701,32 @@ ff_status launch_ck(cudaError_t e, const char* what) {
 
 int rows_threads(int H) { return H >= 512 ? 256 : 128; }
 
+// One linear of the scorer, Y[M x N] (+)= X[M x K] B^T (+ bias) with B the
+// TF32-split weight operand w ([N x K]: W for Y = X W^T, W^T for dX = dY W):
+// split X, then the 3xTF32 tcgen05 GEMM (gemm_x3.cu).  With
+// FF_SCORER_OPT_TC_LINEARS = 0 the SIMT SGEMM `g` (same contraction) runs instead.
+ff_status linear(ff_scorer* m, const SG& g, const XSplit& w, const SplitKScratch& sk, cudaStream_t s,
+                 const char* what) {
+  if (!m->tc_linears) {
+    SL(sgemm(g, 1, s, sk), what);
+    return FF_OK;
+  }
+  const int K = g.K, kp = round4(K);
+  float* xh = m->ws(m->xh);
+  float* xl = m->ws(m->xl);
+  SL(ff::launch_split_tf32(g.A, g.M, K, (int)g.sAm, xh, xl, kp, s), what);
+  const char* err = nullptr;
+  const cudaError_t e = ff::launch_gemm_x3(xh, xl, kp, m->w(w.h), m->w(w.l), w.ld, g.M, g.N, K, g.bias, g.C, (int)g.sCm,
+                                       g.accumulate != 0, s, &err);
+  if (e != cudaSuccess) return sfail(FF_E_CUDA, std::string(what) + ": " + (err ? err : cudaGetErrorString(e)));
+  return FF_OK;
+}
+#define LIN(g, w, what)                               \
+  do {                                                \
+    ff_status s_ = linear(m, (g), (w), sk, s, what);  \
+    if (s_ != FF_OK) return s_;                       \
+  } while (0)
+
 ff_status score_batch(ff_scorer* m, const int* ids, const int* mask, const int* labels, int B, int S, double* hsc,
                       double* fsc, float* loss, float* logits, cudaStream_t s) {
   const ff_config& c = m->cfg;
@@ -689,7 +747,7 @@ ff_status score_batch(ff_scorer* m, const int* ids, const int* mask, const int* 
     const int A = P.A, D = P.D, F = P.F;
     float* X = m->ws(P.X);
     float* QKV = m->ws(P.QKV);
-    SL(sgemm(lin(X, M, H, m->w(P.wqkv), m->w(P.bqkv), QKV, 3 * D), 1, s, sk), "qkv");
+    LIN(lin(X, M, H, m->w(P.wqkv), m->w(P.bqkv), QKV, 3 * D), P.qkv, "qkv");
     // S = Q K^T per (b, h) into P, then softmax in place
     SG g{};
     g.A = QKV; g.sAb = (long long)S * 3 * D; g.sAh = d; g.sAm = 3 * D; g.sAk = 1;
@@ -707,14 +765,14 @@ ff_status score_batch(ff_scorer* m, const int* ids, const int* mask, const int* 
     g.M = S; g.N = d; g.K = S; g.nh = A; g.alpha = 1.0f;
     SL(sgemm(g, B * A, s), "pv");
     float* O = m->ws(m->dZ);  // scratch for the projection outputs
-    SL(sgemm(lin(m->ws(P.Cx), M, D, m->w(P.wo), m->w(P.bo), O, H), 1, s, sk), "oproj");
+    LIN(lin(m->ws(P.Cx), M, D, m->w(P.wo), m->w(P.bo), O, H), P.o, "oproj");
     add_ln_f32_kernel<<<M, rt, lnsm, s>>>(O, X, H, m->w(P.g1), m->w(P.b1), c.ln_eps, m->ws(P.Y1), m->ws(P.XH1),
                                           m->ws(P.R1));
     SL(cudaGetLastError(), "ln1");
-    SL(sgemm(lin(m->ws(P.Y1), M, H, m->w(P.w1), m->w(P.bi1), m->ws(P.U), F), 1, s, sk), "ffn1");
+    LIN(lin(m->ws(P.Y1), M, H, m->w(P.w1), m->w(P.bi1), m->ws(P.U), F), P.f1, "ffn1");
     act_fwd_kernel<<<1184, 256, 0, s>>>(m->ws(P.U), m->ws(P.Act), (size_t)M * F, c.act);
     SL(cudaGetLastError(), "act");
-    SL(sgemm(lin(m->ws(P.Act), M, F, m->w(P.w2), m->w(P.bi2), O, H), 1, s, sk), "ffn2");
+    LIN(lin(m->ws(P.Act), M, F, m->w(P.w2), m->w(P.bi2), O, H), P.f2, "ffn2");
     float* Xn = l + 1 < c.num_layers ? m->ws(m->L[l + 1].X) : m->ws(m->Xout);
     add_ln_f32_kernel<<<M, rt, lnsm, s>>>(O, m->ws(P.Y1), H, m->w(P.g2), m->w(P.b2), c.ln_eps, Xn, m->ws(P.XH2),
                                           m->ws(P.R2));
@@ -746,16 +804,16 @@ ff_status score_batch(ff_scorer* m, const int* ids, const int* mask, const int* 
     float* dAm = m->ws(m->dAm);
     ln_bwd_kernel<<<M, rt, 32 * 4, s>>>(dX, m->w(P.g2), m->ws(P.XH2), m->ws(P.R2), H, dZ);  // d(o2 + y1)
     SL(cudaGetLastError(), "ln2 bwd");
-    SL(sgemm(lin_back(dZ, M, H, m->w(P.w2), F, dAm, false), 1, s, sk), "ffn2 bwd");  // d(act * nu)
+    LIN(lin_back(dZ, M, H, m->w(P.w2), F, dAm, false), P.f2T, "ffn2 bwd");  // d(act * nu)
     colprod_kernel<<<dim3((F + 31) / 32, kRowChunks), 256, 0, s>>>(m->ws(P.Act), dAm, M, F, F, m->ws(m->colg));
     group_abs_add_kernel<<<(F + 127) / 128, 128, 0, s>>>(m->ws(m->colg), F, F, 1, fsc + (size_t)l * m->Fmax);
     act_bwd_kernel<<<1184, 256, 0, s>>>(m->ws(P.U), dAm, (size_t)M * F, c.act);
     copy_kernel<<<1184, 256, 0, s>>>(dZ, dY1, (size_t)M * H);
-    SL(sgemm(lin_back(dAm, M, F, m->w(P.w1), H, dY1, true), 1, s, sk), "ffn1 bwd");
+    LIN(lin_back(dAm, M, F, m->w(P.w1), H, dY1, true), P.f1T, "ffn1 bwd");
     ln_bwd_kernel<<<M, rt, 32 * 4, s>>>(dY1, m->w(P.g1), m->ws(P.XH1), m->ws(P.R1), H, dZ);  // d(o + x)
     SL(cudaGetLastError(), "ln1 bwd");
     float* dC = m->ws(m->dC);
-    SL(sgemm(lin_back(dZ, M, H, m->w(P.wo), D, dC, false), 1, s, sk), "oproj bwd");
+    LIN(lin_back(dZ, M, H, m->w(P.wo), D, dC, false), P.oT, "oproj bwd");
     colprod_kernel<<<dim3((D + 31) / 32, kRowChunks), 256, 0, s>>>(m->ws(P.Cx), dC, M, D, D, m->ws(m->colg));
     group_abs_add_kernel<<<(A + 127) / 128, 128, 0, s>>>(m->ws(m->colg), D, A, d, hsc + (size_t)l * sc_ld);
     // attention backward per (b, h)
@@ -791,7 +849,7 @@ ff_status score_batch(ff_scorer* m, const int* ids, const int* mask, const int* 
     SL(sgemm(g, B * A, s), "dK");
     if (l > 0) {  // gradient w.r.t. the layer input (residual + QKV path)
       copy_kernel<<<1184, 256, 0, s>>>(dZ, dX, (size_t)M * H);
-      SL(sgemm(lin_back(dQKV, M, 3 * D, m->w(P.wqkv), H, dX, true), 1, s, sk), "qkv bwd");
+      LIN(lin_back(dQKV, M, 3 * D, m->w(P.wqkv), H, dX, true), P.qkvT, "qkv bwd");
     }
   }
   return FF_OK;
@@ -863,6 +921,7 @@ ff_status ff_scorer_load_weights(ff_scorer* m, const char* name, const float* ho
     SDev dg_(m->device);
     SC_CK(cudaMemcpyAsync(m->dW + off, host, numel * 4, cudaMemcpyHostToDevice, s));
     SC_CK(cudaStreamSynchronize(s));  // host buffer may be freed after return
+    if (m->state == 2) m->state = 1;  // derived TF32 splits are stale: finalize again
     return FF_OK;
   };
   const ff_config& c = m->cfg;
@@ -922,7 +981,25 @@ ff_status ff_scorer_finalize(ff_scorer* m, void* stream) {
   if (m->top_loaded != 511u) return sfail(FF_E_STATE, "missing embedding / pooler / classifier tensors");
   for (auto& P : m->L)
     if (P.loaded != 0xFFFFu) return sfail(FF_E_STATE, "missing layer tensors");
-  (void)stream;
+  // TF32 hi / lo splits of every linear's weight and its transpose (the B
+  // operands of the tcgen05 linears), from the loaded fp32 weights
+  SDev dg_(m->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int H = m->cfg.hidden;
+  for (auto& P : m->L) {
+    const int D = P.D, F = P.F;
+    struct {
+      size_t w;
+      int n, k;
+      XSplit *fwd, *bwd;
+    } ws[4] = {{P.wqkv, 3 * D, H, &P.qkv, &P.qkvT}, {P.wo, H, D, &P.o, &P.oT}, {P.w1, F, H, &P.f1, &P.f1T},
+               {P.w2, H, F, &P.f2, &P.f2T}};
+    for (auto& x : ws) {
+      SC_CK(ff::launch_split_tf32(m->w(x.w), x.n, x.k, x.k, m->w(x.fwd->h), m->w(x.fwd->l), x.fwd->ld, s));
+      SC_CK(ff::launch_split_tf32_t(m->w(x.w), x.n, x.k, m->w(x.bwd->h), m->w(x.bwd->l), x.bwd->ld, s));
+    }
+  }
+  SC_CK(cudaStreamSynchronize(s));
   m->state = 2;
   return FF_OK;
 }
@@ -956,6 +1033,16 @@ ff_status ff_scorer_check(ff_scorer* m, void* stream) {
     return sfail(FF_E_INPUT, "input error:" + why);
   }
   return FF_OK;
+}
+
+ff_status ff_scorer_set_option(ff_scorer* m, int32_t option, int32_t value) {
+  if (!m) return sfail(FF_E_INVALID, "null argument");
+  if (option == FF_SCORER_OPT_TC_LINEARS) {
+    if (value != 0 && value != 1) return sfail(FF_E_INVALID, "FF_SCORER_OPT_TC_LINEARS takes 0 or 1");
+    m->tc_linears = value;
+    return FF_OK;
+  }
+  return sfail(FF_E_INVALID, "unknown scorer option");
 }
 
 void ff_scorer_destroy(ff_scorer* m) { delete m; }

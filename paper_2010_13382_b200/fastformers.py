@@ -27,6 +27,7 @@ FF_OPT_PDL = 5
 FF_OPT_ACT_QUANT = 6
 FF_OPT_FUSED_MASK = 8
 FF_OPT_PDL_RR = 9
+FF_SCORER_OPT_TC_LINEARS = 1  # ff_scorer_set_option
 KERNEL_KINDS = ["embed_ln", "gemm_f16", "gemm_i8", "attention", "quant_rows", "add_ln", "head", "gemm_rr_f16",
                 "gemm_rr_i8"]
 STATUS_NAMES = ["FF_OK", "FF_E_INVALID", "FF_E_SHAPE", "FF_E_STATE", "FF_E_CUDA", "FF_E_INPUT", "FF_E_UNSUPPORTED",
@@ -37,7 +38,8 @@ EXPORTED = ["ff_abi_version", "ff_last_error", "ff_model_create", "ff_model_memo
             "ff_model_destroy", "ff_launch_count", "ff_profile", "ff_encode_trace", "ff_debug_gemm", "ff_debug_quant_rows",
             "ff_debug_attention", "ff_debug_attention_q8", "ff_debug_set_trace",
             "ff_scorer_last_error", "ff_scorer_create", "ff_scorer_memory", "ff_scorer_bind_memory",
-            "ff_scorer_load_weights", "ff_scorer_finalize", "ff_score_batch", "ff_scorer_check", "ff_scorer_destroy"]
+            "ff_scorer_load_weights", "ff_scorer_finalize", "ff_score_batch", "ff_scorer_check", "ff_scorer_set_option",
+            "ff_scorer_destroy"]
 
 
 class FFError(RuntimeError):
@@ -96,6 +98,7 @@ def lib():
         L.ff_scorer_finalize.argtypes = [vp, vp]
         L.ff_score_batch.argtypes = [vp, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp]
         L.ff_scorer_check.argtypes = [vp, vp]
+        L.ff_scorer_set_option.argtypes = [vp, i32, i32]
         L.ff_scorer_destroy.argtypes = [vp]
         L.ff_scorer_destroy.restype = None
         for name in EXPORTED:
@@ -355,7 +358,8 @@ class Scorer:
     to ``head_scores`` [L, max heads] / ``ffn_scores`` [L, max ffn] (fp64,
     device) and returns the batch's mean cross-entropy (device scalar)."""
 
-    def __init__(self, cfg, weights: Dict[str, np.ndarray], max_tokens: Optional[int] = None, device: int = 0):
+    def __init__(self, cfg, weights: Dict[str, np.ndarray], max_tokens: Optional[int] = None, device: int = 0,
+                 tc_linears: bool = True):
         import torch
         L = lib()
         self.cfg = cfg
@@ -370,6 +374,7 @@ class Scorer:
         h = ctypes.c_void_p()
         _scheck(L.ff_scorer_create(ctypes.byref(c), device, ctypes.byref(h)))
         self.h = h
+        self.set_tc_linears(tc_linears)
         wb, wsb = ctypes.c_size_t(), ctypes.c_size_t()
         _scheck(L.ff_scorer_memory(self.h, ctypes.byref(wb), ctypes.byref(wsb)))
         with torch.cuda.device(self.device):
@@ -394,6 +399,10 @@ class Scorer:
         h = getattr(self, "h", None)
         if h is not None and _lib is not None:
             _lib.ff_scorer_destroy(h)
+
+    def set_tc_linears(self, on: bool):
+        """FF_SCORER_OPT_TC_LINEARS: 3xTF32 tcgen05 linears (default) or the SIMT SGEMM."""
+        _scheck(lib().ff_scorer_set_option(self.h, FF_SCORER_OPT_TC_LINEARS, 1 if on else 0))
 
     def reset(self):
         self.head_scores.zero_()

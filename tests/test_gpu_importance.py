@@ -6,7 +6,10 @@ B*S tokens of products of forward activations and back-propagated gradients,
 so its fp32-vs-fp64 error is relative to the layer's score scale, not to the
 (possibly cancelling) score itself: |gpu - ref| <= 1e-4 |ref| + 2e-5 max_l(ref)
 (measured, tools/importance_err.py: <= 2.2e-6 of the layer max on all three
-configs, so the bound has ~10x headroom)."""
+configs with the SIMT linears, so the bound has ~10x headroom).  The default
+linears are 3xTF32 on tcgen05 (gemm_x3.cu: hi / lo TF32 splits, per-product
+error <= ~2^-21 relative, fp32 accumulation in TMEM); every parity test runs
+both paths against the same oracle and the same bound."""
 import numpy as np
 import pytest
 
@@ -53,12 +56,13 @@ CONFIGS = [
 ]
 
 
+@pytest.mark.parametrize("tc", [True, False], ids=["tc_x3", "simt"])
 @pytest.mark.parametrize("name,mk,B,S,std", CONFIGS)
-def test_scores_match_oracle(name, mk, B, S, std):
+def test_scores_match_oracle(name, mk, B, S, std, tc):
     cfg = mk()
     w = synth.make_weights(cfg, std=std)
     batches = [_batch(cfg, B, S, 100 + i) for i in range(2)]
-    sc = ffb.Scorer(cfg, w, max_tokens=B * S)
+    sc = ffb.Scorer(cfg, w, max_tokens=B * S, tc_linears=tc)
     losses = []
     for ids, mask, labels in batches:
         lg = torch.empty((B, cfg.num_classes), dtype=torch.float32, device="cuda")
@@ -159,3 +163,57 @@ def test_scorer_flags_invalid_inputs_without_faulting():
             sc.check_inputs()
         assert e.value.status == ffb.FF_E_INPUT
         sc.check_inputs()  # the flag was cleared
+
+
+def test_tc_linears_match_simt_linears_on_ragged_tails():
+    """The 3xTF32 tcgen05 linears against the SIMT fp32 SGEMM on a shape with
+    ragged M / N / K tails in every linear (H = 50: K not a multiple of 4;
+    D = 3 x 12, F = 70 / 130: N tails; M = 5 x 29 = 145 rows: an M tail), two
+    batches accumulating: scores, loss and logits agree at fp32 level."""
+    cfg = synth.ModelConfig("tails", 2, 50, 12, [3, 5], [70, 130], [0, 0], 61, 40, 3, 1e-12, batch=5, seq=29,
+                            cls_id=1)
+    w = synth.make_weights(cfg, std=0.1)
+    batches = [_batch(cfg, 5, 29, 40 + i) for i in range(2)]
+    out = []
+    for tc in (True, False):
+        sc = ffb.Scorer(cfg, w, max_tokens=5 * 29, tc_linears=tc)
+        lg = torch.empty((5, cfg.num_classes), dtype=torch.float32, device="cuda")
+        losses = [float(sc.score(*_cuda(*b), logits=lg).item()) for b in batches]
+        out.append((sc.scores(), losses, lg.cpu().numpy()))
+    (hs_t, fs_t), loss_t, lg_t = out[0]
+    (hs_s, fs_s), loss_s, lg_s = out[1]
+    np.testing.assert_allclose(loss_t, loss_s, rtol=1e-5)
+    np.testing.assert_allclose(lg_t, lg_s, rtol=0, atol=1e-5)
+    _close(hs_t, hs_s)
+    _close(fs_t, fs_s)
+    rh, rf, _ = imp.compute_importance(cfg, w, batches)
+    _close(hs_t, rh)
+    _close(fs_t, rf)
+
+
+def test_reload_after_finalize_requires_finalize():
+    """Loading a tensor after ff_scorer_finalize invalidates the TF32 splits:
+    ff_score_batch refuses (FF_E_STATE) until finalize runs again."""
+    import ctypes
+    cfg = _tiny()
+    w = synth.make_weights(cfg)
+    sc = ffb.Scorer(cfg, w, max_tokens=3 * 7)
+    L = ffb.lib()
+    name = "encoder.layer.0.intermediate.dense.weight"
+    a = np.ascontiguousarray(w[name] * 2, dtype=np.float32)
+    shape = (ctypes.c_int64 * 2)(*a.shape)
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert L.ff_scorer_load_weights(sc.h, name.encode(), ctypes.c_void_p(a.ctypes.data), shape, 2, st) == 0
+    ids, mask, labels = _cuda(*_batch(cfg, 3, 7, 5))
+    with pytest.raises(ffb.FFError, match="FF_E_STATE"):
+        sc.score(ids, mask, labels)
+    assert L.ff_scorer_finalize(sc.h, st) == 0
+    sc.score(ids, mask, labels)
+    w2 = dict(w)
+    w2[name] = a
+    ref = ffb.Scorer(cfg, w2, max_tokens=3 * 7)
+    ref.score(ids, mask, labels)
+    torch.cuda.synchronize()
+    for g, r in zip(sc.scores(), ref.scores()):
+        for x, y in zip(g, r):
+            np.testing.assert_array_equal(x, y)
