@@ -341,6 +341,16 @@ FF_API ff_status ff_scorer_check(ff_scorer *s, void *stream);
  *   attention products always use the SIMT SGEMM.
  * FF_E_INVALID for an unknown option or value. */
 #define FF_SCORER_OPT_TC_LINEARS 1
+/* Test hook: one 3xTF32 tcgen05 GEMM as the scorer's linears run it,
+ * d_C[M x N] (+)= d_A[M x K] d_B[N x K]^T (+ d_bias[N], optional), fp32 device
+ * buffers with row pitches lda, ldb, ldc (elements); kc = k-blocks of 32 per
+ * TMEM accumulation chunk (the scorer uses 4).  Split-K is chosen as in the
+ * scorer (workspace for up to 4 partial sums).  Split buffers are allocated
+ * stream-ordered (cudaMallocAsync) and freed before return.  Errors via
+ * ff_scorer_last_error(). */
+FF_API ff_status ff_debug_gemm_x3(const float *d_A, int32_t lda, const float *d_B, int32_t ldb, int32_t M, int32_t N,
+                                  int32_t K, const float *d_bias, float *d_C, int32_t ldc, int32_t accumulate,
+                                  int32_t kc, void *stream);
 FF_API ff_status ff_scorer_set_option(ff_scorer *s, int32_t option, int32_t value);
 /* Frees host state only (the arenas belong to the caller). */
 FF_API void ff_scorer_destroy(ff_scorer *s);

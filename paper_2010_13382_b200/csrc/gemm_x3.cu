@@ -7,9 +7,16 @@
 // is split into two TF32 numbers, x = hi + lo with hi = RN_tf32(x) and
 // lo = RN_tf32(x - hi) (|x - hi - lo| <= 2^-22 |x|), and the product is
 //   A B^T ~= Ah Bh^T + Ah Bl^T + Al Bh^T        ("3xTF32"; Al Bl^T ~ 2^-22 dropped)
-// accumulated in fp32 in TMEM by kind::tf32 MMAs.  Both halves are exact TF32
+// accumulated in fp32 by kind::tf32 MMAs.  Both halves are exact TF32
 // values, so the tensor core's treatment of the 13 low mantissa bits of an
 // operand (ignored) does not matter.
+//
+// The tensor core's fp32 accumulation is not IEEE round-to-nearest (measured:
+// one TMEM accumulator over K = 3072, i.e. 1152 MMA accumulations, leaves
+// errors ~20x the SIMT SGEMM's), so the K loop is cut into chunks of `kc`
+// k-blocks (default 4 = 128 of K): each chunk accumulates into its own TMEM
+// slot (4-slot ring, 128 columns each), and the epilogue warps add the chunk
+// results in registers with IEEE fp32 adds.
 //
 // Operands: A [M x K] and B [N x K], both K-major (row pitch a multiple of 4
 // floats: the split buffers are padded with zeros to K rounded up to 4).  The
@@ -19,9 +26,10 @@
 // Kernel: persistent, one CTA per SM, 128 x 128 output tiles; warp 0 issues
 // the TMA loads of the four 16 KB operand tiles of a 32-float k-block (3-stage
 // ring, 192 KB), warp 1 issues 12 MMAs per k-block (4 k-steps x 3 products)
-// into one of two 128-column TMEM accumulators, warps 4-7 drain the other
-// accumulator (tcgen05.ld -> +bias (+C) -> coalesced row stores through a
-// 32 x 33 smem transpose per warp).
+// into the next free TMEM slot, warps 4-7 add each finished slot into their
+// rows' fp32 sums (thread = row, 128 registers) and, after the last chunk of a
+// tile, store sum + bias (+ C) with coalesced row stores through a 32 x 33
+// smem transpose per warp.
 #include <algorithm>
 
 #include "ff_kernels.h"
@@ -68,7 +76,28 @@ struct X3Params {
   const float* bias;
   int M, N, ldc, accumulate;
   int m_tiles, n_tiles, k_blocks;
+  int kc;  // k-blocks per TMEM accumulation chunk
+  // split-K (wave quantization of few-tile shapes): unit u = (ks, tile) covers
+  // k-blocks [ks * kbps, (ks + 1) * kbps); with splits > 1 each unit writes its
+  // plain partial sum to ws[ks] ([M x N]) and x3_splitk_reduce adds them.
+  int splits, kbps;
+  float* ws;
 };
+struct X3Unit {
+  int mt, nt, ks, kb0, kb1;
+};
+__device__ __forceinline__ X3Unit x3_unit(const X3Params& p, int u) {
+  X3Unit w;
+  const int tiles = p.m_tiles * p.n_tiles;
+  w.ks = u / tiles;
+  const int t = u - w.ks * tiles;
+  w.mt = t / p.n_tiles;
+  w.nt = t - w.mt * p.n_tiles;
+  w.kb0 = w.ks * p.kbps;
+  w.kb1 = min(p.k_blocks, w.kb0 + p.kbps);
+  return w;
+}
+constexpr int X3_SLOTS = 4;  // TMEM accumulator ring: 4 x 128 columns = all 512
 
 __global__ void __launch_bounds__(X3_THREADS, 1)
     gemm_x3_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
@@ -78,8 +107,8 @@ __global__ void __launch_bounds__(X3_THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + X3_BAR_OFF);
   uint64_t* empty = full + X3_STAGES;
   uint64_t* tfull = empty + X3_STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tempty = tfull + X3_SLOTS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + X3_SLOTS);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmAh);
@@ -90,29 +119,30 @@ __global__ void __launch_bounds__(X3_THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < X3_SLOTS; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4);
     }
     fence_barrier_init();
   }
   if (warp == 2) {
-    tmem_alloc(tmem_slot, 2 * X3_TN);
+    tmem_alloc(tmem_slot, X3_SLOTS * X3_TN);
     tmem_relinquish();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int num_tiles = p.m_tiles * p.n_tiles;
+  const int num_units = p.m_tiles * p.n_tiles * p.splits;
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+        const X3Unit w = x3_unit(p, u);
+        const int mt = w.mt, nt = w.nt;
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * X3_STAGE;
           mbar_expect_tx(&full[stage], X3_STAGE);
@@ -132,11 +162,16 @@ __global__ void __launch_bounds__(X3_THREADS, 1)
       constexpr uint32_t idesc = x3_idesc();
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * X3_TN;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+        const X3Unit w = x3_unit(p, u);
+        uint32_t d_tmem = 0;
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
+          const int kin = (kb - w.kb0) % p.kc;  // k-block index inside its chunk
+          if (kin == 0) {             // a new chunk: next TMEM slot
+            mbar_wait(&tempty[acc], acc_phase ^ 1);
+            tc_fence_after();
+            d_tmem = tmem_base + acc * X3_TN;
+          }
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           uint8_t* st = smem + stage * X3_STAGE;
@@ -146,7 +181,7 @@ __global__ void __launch_bounds__(X3_THREADS, 1)
           for (int k = 0; k < 4; ++k) {  // 4 x 8 fp32 (32 B) of K; +2 = +32 B in the >>4 address field
             // small products first: the larger Ah Bh^T term then adds to an accumulator already
             // holding the corrections of this k-step
-            mma_tf32(d_tmem, al + 2 * k, bh + 2 * k, idesc, (kb | k) != 0);
+            mma_tf32(d_tmem, al + 2 * k, bh + 2 * k, idesc, (kin | k) != 0);
             mma_tf32(d_tmem, ah + 2 * k, bl + 2 * k, idesc, 1);
             mma_tf32(d_tmem, ah + 2 * k, bh + 2 * k, idesc, 1);
           }
@@ -155,11 +190,13 @@ __global__ void __launch_bounds__(X3_THREADS, 1)
             stage = 0;
             phase ^= 1;
           }
-        }
-        mma_commit(&tfull[acc]);
-        if (++acc == 2) {
-          acc = 0;
-          acc_phase ^= 1;
+          if (kin == p.kc - 1 || kb == w.kb1 - 1) {  // chunk complete
+            mma_commit(&tfull[acc]);
+            if (++acc == X3_SLOTS) {
+              acc = 0;
+              acc_phase ^= 1;
+            }
+          }
         }
       }
     }
@@ -168,44 +205,65 @@ __global__ void __launch_bounds__(X3_THREADS, 1)
     float* buf = reinterpret_cast<float*>(smem + X3_EPI_OFF + (warp - 4) * X3_EPI_WARP);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+    const bool part = p.splits > 1;
+    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+      const X3Unit w = x3_unit(p, u);
+      const int nchunks = (w.kb1 - w.kb0 + p.kc - 1) / p.kc;
+      const int mt = w.mt, nt = w.nt;
       const int row0 = mt * X3_TM + q * 32;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * X3_TN;
-#pragma unroll 1
-      for (int c = 0; c < X3_TN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tbase + c * 32, r);
-        tmem_wait_ld();
-        if (c == X3_TN / 32 - 1) {  // accumulator drained: hand it back to the MMA warp
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
-        }
+      // partial sums (split-K) go to ws[ks] without bias / accumulate
+      float* const out = part ? p.ws + (size_t)w.ks * p.M * p.N : p.C;
+      const int ldo = part ? p.N : p.ldc;
+      float sum[X3_TN];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = __uint_as_float(r[j]);
+      for (int j = 0; j < X3_TN; ++j) sum[j] = 0.0f;
+      for (int ch = 0; ch < nchunks; ++ch) {
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * X3_TN;
+#pragma unroll
+        for (int c = 0; c < X3_TN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tbase + c * 32, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sum[c * 32 + j] += __uint_as_float(r[j]);
+        }
+        tc_fence_before();  // slot drained: hand it back to the MMA warp
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (++acc == X3_SLOTS) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < X3_TN / 32; ++c) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = sum[c * 32 + j];
         __syncwarp();
         const int col = nt * X3_TN + c * 32 + lane;
         const bool cok = col < p.N;
-        const float b = (p.bias != nullptr && cok) ? __ldg(p.bias + col) : 0.0f;
-#pragma unroll 4
-        for (int rr = 0; rr < 32; ++rr) {
-          const int row = row0 + rr;
-          if (row >= p.M) break;
-          if (cok) {
-            float v = buf[rr * 33 + lane] + b;
-            float* dst = p.C + (size_t)row * p.ldc + col;
-            if (p.accumulate) v += *dst;
-            *dst = v;
+        const float b = (!part && p.bias != nullptr && cok) ? __ldg(p.bias + col) : 0.0f;
+        float* dst = out + (size_t)row0 * ldo + col;
+        const int nrows = min(32, p.M - row0);
+        if (p.accumulate && !part) {  // 16 loads of C in flight before the stores
+#pragma unroll
+          for (int h = 0; h < 32; h += 16) {
+            float cv[16];
+#pragma unroll
+            for (int rr = 0; rr < 16; ++rr)
+              cv[rr] = (cok && h + rr < nrows) ? dst[(size_t)(h + rr) * ldo] : 0.0f;
+#pragma unroll
+            for (int rr = 0; rr < 16; ++rr)
+              if (cok && h + rr < nrows) dst[(size_t)(h + rr) * ldo] = buf[(h + rr) * 33 + lane] + b + cv[rr];
           }
+        } else {
+#pragma unroll
+          for (int rr = 0; rr < 32; ++rr)
+            if (cok && rr < nrows) dst[(size_t)rr * ldo] = buf[rr * 33 + lane] + b;
         }
         __syncwarp();
-      }
-      if (++acc == 2) {
-        acc = 0;
-        acc_phase ^= 1;
       }
     }
   }
@@ -213,7 +271,7 @@ __global__ void __launch_bounds__(X3_THREADS, 1)
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 2 * X3_TN);
+    tmem_dealloc(tmem_base, X3_SLOTS * X3_TN);
   }
 }
 
@@ -259,24 +317,85 @@ __global__ void split_tf32_t_kernel(const float* __restrict__ W, int N, int K, f
   }
 }
 
-bool encode_f32(CUtensorMap* map, const float* base, int rows, int ld, const char** err) {
-  return make_operand_map(map, base, rows, ld, 4, (size_t)ld * 4, 128, err);
+// C = sum_ks ws[ks] + bias (+ C), partials added in ks order (deterministic).
+// One thread per 4 consecutive columns (N % 4 == 0 and ldc % 4 == 0: float4
+// accesses; the launcher checks alignment), else one per element.
+template <bool V4>
+__global__ void x3_splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N,
+                                        const float* __restrict__ bias, float* C, int ldc, int accumulate) {
+  constexpr int W = V4 ? 4 : 1;
+  const int nq = N / W;
+  const size_t n = (size_t)M * nq, plane = (size_t)M * N, stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int r = (int)(i / nq), c = (int)(i - (size_t)r * nq) * W;
+    const size_t o = (size_t)r * N + c;
+    float* dst = C + (size_t)r * ldc + c;
+    if constexpr (V4) {
+      float4 v = *reinterpret_cast<const float4*>(ws + o);
+      for (int k = 1; k < splits; ++k) {
+        const float4 w = *reinterpret_cast<const float4*>(ws + (size_t)k * plane + o);
+        v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
+      }
+      if (bias != nullptr) {
+        const float4 b = *reinterpret_cast<const float4*>(bias + c);
+        v.x += b.x; v.y += b.y; v.z += b.z; v.w += b.w;
+      }
+      if (accumulate) {
+        const float4 d = *reinterpret_cast<const float4*>(dst);
+        v.x += d.x; v.y += d.y; v.z += d.z; v.w += d.w;
+      }
+      *reinterpret_cast<float4*>(dst) = v;
+    } else {
+      float v = ws[o];
+      for (int k = 1; k < splits; ++k) v += ws[(size_t)k * plane + o];
+      if (bias != nullptr) v += __ldg(bias + c);
+      if (accumulate) v += *dst;
+      *dst = v;
+    }
+  }
+}
+
+// Split count for the K loop: the wave makespan of 148 persistent CTAs, in
+// k-block times, plus ~3 k-blocks of fill / drain per unit and the partial-sum
+// traffic of the reduction (S + 2 passes over M x N fp32 at ~5 TB/s against
+// ~0.75 us per k-block); at most `cap` partial buffers fit the workspace.
+int pick_splits(int tiles, int k_blocks, size_t MN, int cap) {
+  int best = 1;
+  double best_cost = 1e30;
+  for (int S = 1; S <= std::min(4, cap); ++S) {
+    if (S > 1 && k_blocks / S < 4) break;
+    const int kbps = (k_blocks + S - 1) / S;
+    const int waves = (tiles * S + kNumSMs - 1) / kNumSMs;
+    double cost = (double)waves * (kbps + 3);
+    if (S > 1) cost += (double)(S + 2) * MN * 4 / 5e12 / 0.75e-6;
+    if (cost < best_cost * 0.97) {
+      best_cost = cost;
+      best = S;
+    }
+  }
+  return best;
 }
 
 }  // namespace
 
 cudaError_t launch_gemm_x3(const float* Ah, const float* Al, int lda, const float* Bh, const float* Bl, int ldb,
                            int M, int N, int K, const float* bias, float* C, int ldc, bool accumulate, cudaStream_t s,
-                           const char** err) {
+                           const char** err, int kc, float* ws, size_t ws_floats) {
   if (M <= 0 || N <= 0) return cudaSuccess;
+  if (kc < 1) {
+    *err = "gemm_x3: kc must be >= 1";
+    return cudaErrorInvalidValue;
+  }
   if ((lda & 3) || (ldb & 3) || K > lda || K > ldb) {
     *err = "gemm_x3: operand pitch must be a multiple of 4 floats and >= K";
     return cudaErrorInvalidValue;
   }
-  CUtensorMap ah, al, bh, bl;
   // the maps cover the K-padded width (zeros), so K rounds up to whole k-blocks
-  if (!encode_f32(&ah, Ah, M, lda, err) || !encode_f32(&al, Al, M, lda, err) || !encode_f32(&bh, Bh, N, ldb, err) ||
-      !encode_f32(&bl, Bl, N, ldb, err))
+  CUtensorMap ah, al, bh, bl;
+  if (!make_operand_map(&ah, Ah, M, lda, 4, (size_t)lda * 4, 128, err) ||
+      !make_operand_map(&al, Al, M, lda, 4, (size_t)lda * 4, 128, err) ||
+      !make_operand_map(&bh, Bh, N, ldb, 4, (size_t)ldb * 4, 128, err) ||
+      !make_operand_map(&bl, Bl, N, ldb, 4, (size_t)ldb * 4, 128, err))
     return cudaErrorInvalidValue;
   static bool attr_set = false;  // per process; all devices are B200s
   if (!attr_set) {
@@ -293,9 +412,25 @@ cudaError_t launch_gemm_x3(const float* Ah, const float* Al, int lda, const floa
   p.accumulate = accumulate ? 1 : 0;
   p.m_tiles = (M + X3_TM - 1) / X3_TM;
   p.n_tiles = (N + X3_TN - 1) / X3_TN;
-  p.k_blocks = (K + X3_KE - 1) / X3_KE;
+  p.k_blocks = std::max(1, (K + X3_KE - 1) / X3_KE);
+  p.kc = kc;
   const int tiles = p.m_tiles * p.n_tiles;
-  gemm_x3_kernel<<<std::min(tiles, kNumSMs), X3_THREADS, X3_SMEM, s>>>(ah, al, bh, bl, p);
+  const size_t MN = (size_t)M * N;
+  const int cap = ws != nullptr ? (int)std::min<size_t>(4, ws_floats / MN) : 1;
+  p.splits = pick_splits(tiles, p.k_blocks, MN, std::max(1, cap));
+  p.kbps = (p.k_blocks + p.splits - 1) / p.splits;
+  p.splits = (p.k_blocks + p.kbps - 1) / p.kbps;  // no empty split
+  p.ws = ws;
+  const int units = tiles * p.splits;
+  gemm_x3_kernel<<<std::min(units, kNumSMs), X3_THREADS, X3_SMEM, s>>>(ah, al, bh, bl, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || p.splits == 1) return e;
+  const bool v4 = (N % 4) == 0 && (ldc % 4) == 0 && ((reinterpret_cast<uintptr_t>(C) | reinterpret_cast<uintptr_t>(ws) |
+                                                      reinterpret_cast<uintptr_t>(bias)) & 15) == 0;
+  const size_t work = v4 ? MN / 4 : MN;
+  const int blocks = (int)std::min<size_t>((work + 255) / 256, (size_t)kNumSMs * 8);
+  if (v4) x3_splitk_reduce_kernel<true><<<blocks, 256, 0, s>>>(ws, p.splits, M, N, bias, C, ldc, accumulate ? 1 : 0);
+  else x3_splitk_reduce_kernel<false><<<blocks, 256, 0, s>>>(ws, p.splits, M, N, bias, C, ldc, accumulate ? 1 : 0);
   return cudaGetLastError();
 }
 

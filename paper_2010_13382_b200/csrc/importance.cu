@@ -515,13 +515,20 @@ __global__ void colprod_kernel(const float* X, const float* dX, int M, int ncols
   }
 }
 // scores[u] += | sum_{c in [u*group, +group)} sum_chunks colg[chunk][c] |
+// One warp per unit: strided fp64 partial sums, then a fixed xor-shuffle tree
+// (deterministic).
 __global__ void group_abs_add_kernel(const float* colg, int ncols, int units, int group, double* scores) {
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int u = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (u >= units) return;
   double s = 0.0;
-  for (int ch = 0; ch < kRowChunks; ++ch)
-    for (int i = 0; i < group; ++i) s += (double)colg[(size_t)ch * ncols + u * group + i];
-  scores[u] += fabs(s);
+  const int n = kRowChunks * group;
+  for (int i = lane; i < n; i += 32) {
+    const int ch = i / group, j = i - ch * group;
+    s += (double)colg[(size_t)ch * ncols + (size_t)u * group + j];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) scores[u] += fabs(s);
 }
 
 __global__ void copy_kernel(const float* a, float* b, size_t n) {
@@ -716,8 +723,8 @@ ff_status linear(ff_scorer* m, const SG& g, const XSplit& w, const SplitKScratch
   float* xl = m->ws(m->xl);
   SL(ff::launch_split_tf32(g.A, g.M, K, (int)g.sAm, xh, xl, kp, s), what);
   const char* err = nullptr;
-  const cudaError_t e = ff::launch_gemm_x3(xh, xl, kp, m->w(w.h), m->w(w.l), w.ld, g.M, g.N, K, g.bias, g.C, (int)g.sCm,
-                                       g.accumulate != 0, s, &err);
+  const cudaError_t e = ff::launch_gemm_x3(xh, xl, kp, m->w(w.h), m->w(w.l), w.ld, g.M, g.N, K, g.bias, g.C,
+                                           (int)g.sCm, g.accumulate != 0, s, &err, 4, sk.ws, sk.cap);
   if (e != cudaSuccess) return sfail(FF_E_CUDA, std::string(what) + ": " + (err ? err : cudaGetErrorString(e)));
   return FF_OK;
 }
@@ -806,7 +813,7 @@ ff_status score_batch(ff_scorer* m, const int* ids, const int* mask, const int* 
     SL(cudaGetLastError(), "ln2 bwd");
     LIN(lin_back(dZ, M, H, m->w(P.w2), F, dAm, false), P.f2T, "ffn2 bwd");  // d(act * nu)
     colprod_kernel<<<dim3((F + 31) / 32, kRowChunks), 256, 0, s>>>(m->ws(P.Act), dAm, M, F, F, m->ws(m->colg));
-    group_abs_add_kernel<<<(F + 127) / 128, 128, 0, s>>>(m->ws(m->colg), F, F, 1, fsc + (size_t)l * m->Fmax);
+    group_abs_add_kernel<<<(F + 3) / 4, 128, 0, s>>>(m->ws(m->colg), F, F, 1, fsc + (size_t)l * m->Fmax);
     act_bwd_kernel<<<1184, 256, 0, s>>>(m->ws(P.U), dAm, (size_t)M * F, c.act);
     copy_kernel<<<1184, 256, 0, s>>>(dZ, dY1, (size_t)M * H);
     LIN(lin_back(dAm, M, F, m->w(P.w1), H, dY1, true), P.f1T, "ffn1 bwd");
@@ -815,7 +822,7 @@ ff_status score_batch(ff_scorer* m, const int* ids, const int* mask, const int* 
     float* dC = m->ws(m->dC);
     LIN(lin_back(dZ, M, H, m->w(P.wo), D, dC, false), P.oT, "oproj bwd");
     colprod_kernel<<<dim3((D + 31) / 32, kRowChunks), 256, 0, s>>>(m->ws(P.Cx), dC, M, D, D, m->ws(m->colg));
-    group_abs_add_kernel<<<(A + 127) / 128, 128, 0, s>>>(m->ws(m->colg), D, A, d, hsc + (size_t)l * sc_ld);
+    group_abs_add_kernel<<<(A + 3) / 4, 128, 0, s>>>(m->ws(m->colg), D, A, d, hsc + (size_t)l * sc_ld);
     // attention backward per (b, h)
     float* QKV = m->ws(P.QKV);
     float* dQKV = m->ws(m->dQKV);
@@ -1032,6 +1039,33 @@ ff_status ff_scorer_check(ff_scorer* m, void* stream) {
     if (flag & 4) why += " label outside [0, num_classes)";
     return sfail(FF_E_INPUT, "input error:" + why);
   }
+  return FF_OK;
+}
+
+ff_status ff_debug_gemm_x3(const float* d_A, int32_t lda, const float* d_B, int32_t ldb, int32_t M, int32_t N,
+                           int32_t K, const float* d_bias, float* d_C, int32_t ldc, int32_t accumulate, int32_t kc,
+                           void* stream) {
+  if (!d_A || !d_B || !d_C) return sfail(FF_E_INVALID, "null argument");
+  if (M < 1 || N < 1 || K < 1 || lda < K || ldb < K || ldc < N || kc < 1) return sfail(FF_E_SHAPE, "bad GEMM shape");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int kp = round4(K);
+  float *ah = nullptr, *bh = nullptr;
+  SC_CK(cudaMallocAsync(reinterpret_cast<void**>(&ah), (size_t)2 * M * kp * 4, s));
+  SC_CK(cudaMallocAsync(reinterpret_cast<void**>(&bh), (size_t)2 * N * kp * 4, s));
+  float* ws = nullptr;  // split-K partials, as the scorer provides
+  SC_CK(cudaMallocAsync(reinterpret_cast<void**>(&ws), (size_t)4 * M * N * 4, s));
+  float* al = ah + (size_t)M * kp;
+  float* bl = bh + (size_t)N * kp;
+  cudaError_t e = ff::launch_split_tf32(d_A, M, K, lda, ah, al, kp, s);
+  if (e == cudaSuccess) e = ff::launch_split_tf32(d_B, N, K, ldb, bh, bl, kp, s);
+  const char* err = nullptr;
+  if (e == cudaSuccess)
+    e = ff::launch_gemm_x3(ah, al, kp, bh, bl, kp, M, N, K, d_bias, d_C, ldc, accumulate != 0, s, &err, kc, ws,
+                           (size_t)4 * M * N);
+  cudaFreeAsync(ah, s);
+  cudaFreeAsync(bh, s);
+  cudaFreeAsync(ws, s);
+  if (e != cudaSuccess) return sfail(FF_E_CUDA, err ? err : cudaGetErrorString(e));
   return FF_OK;
 }
 

@@ -38,7 +38,7 @@ EXPORTED = ["ff_abi_version", "ff_last_error", "ff_model_create", "ff_model_memo
             "ff_model_destroy", "ff_launch_count", "ff_profile", "ff_encode_trace", "ff_debug_gemm", "ff_debug_quant_rows",
             "ff_debug_attention", "ff_debug_attention_q8", "ff_debug_set_trace",
             "ff_scorer_last_error", "ff_scorer_create", "ff_scorer_memory", "ff_scorer_bind_memory",
-            "ff_scorer_load_weights", "ff_scorer_finalize", "ff_score_batch", "ff_scorer_check", "ff_scorer_set_option",
+            "ff_scorer_load_weights", "ff_scorer_finalize", "ff_score_batch", "ff_scorer_check", "ff_scorer_set_option", "ff_debug_gemm_x3",
             "ff_scorer_destroy"]
 
 
@@ -99,6 +99,7 @@ def lib():
         L.ff_score_batch.argtypes = [vp, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp]
         L.ff_scorer_check.argtypes = [vp, vp]
         L.ff_scorer_set_option.argtypes = [vp, i32, i32]
+        L.ff_debug_gemm_x3.argtypes = [vp, i32, vp, i32, i32, i32, i32, vp, vp, i32, i32, i32, vp]
         L.ff_scorer_destroy.argtypes = [vp]
         L.ff_scorer_destroy.restype = None
         for name in EXPORTED:
@@ -349,6 +350,21 @@ def set_gemm_trace(trace=None, which=0):
 def _scheck(status: int):
     if status != FF_OK:
         raise FFError(status, lib().ff_scorer_last_error().decode(errors="replace"))
+
+
+def gemm_x3(A, B, bias=None, out=None, accumulate=False, kc=4):
+    """ff_debug_gemm_x3: C (+)= A B^T (+ bias) on the scorer's 3xTF32 tcgen05
+    GEMM; A [M, K], B [N, K] fp32 CUDA tensors (unit column stride)."""
+    import torch
+    M, K = A.shape
+    N = B.shape[0]
+    if out is None:
+        out = torch.zeros((M, N), dtype=torch.float32, device=A.device)
+    nul = ctypes.c_void_p(None)
+    _scheck(lib().ff_debug_gemm_x3(_ptr(A), A.stride(0), _ptr(B), B.stride(0), M, N, K,
+                                   _ptr(bias) if bias is not None else nul, _ptr(out), out.stride(0),
+                                   1 if accumulate else 0, kc, _stream_ptr()))
+    return out
 
 
 class Scorer:

@@ -217,3 +217,49 @@ def test_reload_after_finalize_requires_finalize():
     for g, r in zip(sc.scores(), ref.scores()):
         for x, y in zip(g, r):
             np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 128, 32), (300, 200, 100), (1, 5, 3), (257, 130, 3072), (4096, 768, 3072)])
+def test_gemm_x3_against_fp64(M, N, K):
+    """The scorer's 3xTF32 tcgen05 GEMM (ff_debug_gemm_x3) against an fp64
+    matmul of the same fp32 inputs: the error is bounded by fp32-level terms,
+    |err| <= 2^-20 * sum_k |a_ik b_jk| + 2^-24 |c| (3 TF32 products ~2^-21
+    relative each, chunked IEEE accumulation), and within 16x the error of a
+    plain fp32 torch matmul (TF32 disabled) on the same inputs."""
+    g = torch.Generator().manual_seed(M * 7 + N * 3 + K)
+    A = torch.randn(M, K, generator=g, dtype=torch.float64)
+    B = torch.randn(N, K, generator=g, dtype=torch.float64) * 0.05
+    bias = torch.randn(N, generator=g, dtype=torch.float64)
+    ref = A @ B.T + bias
+    A32, B32, b32 = (t.float().cuda() for t in (A, B, bias))
+    got = ffb.gemm_x3(A32, B32, bias=b32).double().cpu()
+    bound = 2.0 ** -20 * (A.abs() @ B.abs().T) + 2.0 ** -24 * ref.abs()
+    err = (got - ref).abs()
+    assert (err <= bound).all(), float((err / bound).max())
+    torch.backends.cuda.matmul.allow_tf32 = False
+    fp32 = (A32 @ B32.T + b32).double().cpu()
+    e32 = (fp32 - ref).abs()
+    print("max abs err x3 %.3e fp32 %.3e" % (float(err.max()), float(e32.max())))
+    assert err.max() <= 16 * e32.max() + 1e-12, (float(err.max()), float(e32.max()))
+    # accumulate: C += A B^T
+    c0 = torch.randn(M, N, generator=g, dtype=torch.float64)
+    out = c0.float().cuda()
+    ffb.gemm_x3(A32, B32, out=out, accumulate=True)
+    ref2 = c0.float().double() + A @ B.T
+    assert ((out.double().cpu() - ref2).abs() <= bound + 2.0 ** -23 * ref2.abs()).all()
+
+
+def test_gemm_x3_chunking_reduces_error():
+    """One TMEM accumulator over the whole K (kc = K / 32) is less accurate
+    than the default 128-wide chunks summed with IEEE adds (the design reason
+    for chunking, gemm_x3.cu); both stay within the fp32-level bound's 4x."""
+    g = torch.Generator().manual_seed(5)
+    M, N, K = 512, 256, 3072
+    A = torch.randn(M, K, generator=g, dtype=torch.float64).abs()  # same-sign terms: biased rounding shows
+    B = torch.randn(N, K, generator=g, dtype=torch.float64).abs() * 0.05
+    ref = A @ B.T
+    A32, B32 = A.float().cuda(), B.float().cuda()
+    e_chunk = (ffb.gemm_x3(A32, B32, kc=4).double().cpu() - ref).abs().max()
+    e_whole = (ffb.gemm_x3(A32, B32, kc=K // 32).double().cpu() - ref).abs().max()
+    print("max abs err chunked %.3e whole-K %.3e" % (e_chunk, e_whole))
+    assert e_chunk <= e_whole
