@@ -234,9 +234,9 @@ def importance_variant(stream, flush, B=32, S=128, n=10):
     att = sum(2.0 * 2 * A * S * S * d for A in cfg.heads) * B
     flops = fwd + lin + 2 * att
     peaks, src = load_peaks()
-    # the linears (all but the per-head attention products) run as 3xTF32 on
-    # tcgen05: three TF32 MMAs per product, TF32 = 1/2 of the bf16 rate (nominal)
-    peak = peaks["bf16_tflops"] / 2 / 3
+    # the linears (all but the per-head attention products) run as 3xFP16 on
+    # tcgen05: three fp16 MMAs per product at the (measured) bf16 = fp16 rate
+    peak = peaks["bf16_tflops"] / 3
     peak_simt = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
     ach = flops / (ms / 1e3) / 1e12
     from oracle import importance as imp
@@ -247,7 +247,7 @@ def importance_variant(stream, flush, B=32, S=128, n=10):
     return {"workload": f"c3_unpruned (6L H768 12 heads FFN 3072, P:97) importance scoring, batch {B} x seq {S}",
             "value": B / (ms / 1e3), "unit": "sequences/s", "ms_per_batch": ms,
             "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                         "peak_source": f"{src}: bf16_tflops (burst) / 2 (nominal tf32 / bf16) / 3 (3xTF32 products)",
+                         "peak_source": f"{src}: bf16_tflops (burst) / 3 (3xFP16 products)",
                          "algorithmic": f"{flops / 1e9:.1f} GFLOP per batch (fwd + input-gradient bwd; the "
                                         "per-head attention products, ~{:.0f}%, stay on the SIMT SGEMM)".format(
                                             100 * 3 * att / flops)},

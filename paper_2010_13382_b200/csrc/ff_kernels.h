@@ -238,19 +238,23 @@ cudaError_t prepare_gemm_kernels();
 cudaError_t prepare_attention_kernels();
 cudaError_t prepare_row_kernels();
 
-// ---- importance scorer: 3xTF32 tcgen05 GEMM (gemm_x3.cu)
-// C[M x N] (+)= A[M x K] B[N x K]^T (+ bias[N]) with A = Ah + Al and B = Bh + Bl
-// given as TF32 hi / lo splits (row pitch lda / ldb floats, multiples of 4,
-// zero-padded beyond K); C has row pitch ldc.  kc = k-blocks (32 of K) per
-// TMEM accumulation chunk (chunks are summed with IEEE fp32 adds).  ws (optional,
-// ws_floats floats): split-K partial sums for shapes with too few tiles to fill
-// the SMs (up to 4 x M x N).  *err set on a setup failure.
-cudaError_t launch_gemm_x3(const float* Ah, const float* Al, int lda, const float* Bh, const float* Bl, int ldb,
-                           int M, int N, int K, const float* bias, float* C, int ldc, bool accumulate, cudaStream_t s,
-                           const char** err, int kc = 4, float* ws = nullptr, size_t ws_floats = 0);
-// hi / lo split of X [M x K] (pitch ldx) into [M x ldo] buffers (ldo % 4 == 0, >= K; zero-padded).
-cudaError_t launch_split_tf32(const float* X, int M, int K, int ldx, float* hi, float* lo, int ldo, cudaStream_t s);
-// hi / lo split of W^T for W [N x K] (pitch K): outputs [K x ldo] (ldo % 4 == 0, >= N; zero-padded).
-cudaError_t launch_split_tf32_t(const float* W, int N, int K, float* hi, float* lo, int ldo, cudaStream_t s);
+// ---- importance scorer: 3xFP16 tcgen05 GEMM (gemm_x3.cu)
+// C[M x N] (+)= A[M x K] B[N x K]^T (+ bias[N]) with A row m = sa[m] (Ah + Al)
+// and B row n = sb[n] (Bh + Bl) given as row-scaled fp16 hi / lo splits (row
+// pitch lda / ldb halves, multiples of 8, zero-padded beyond K); C has row
+// pitch ldc.  kc = k-blocks (64 of K) per TMEM accumulation chunk (chunks are
+// summed with IEEE fp32 adds).  ws (optional, ws_floats floats): split-K
+// partial sums for shapes with too few tiles to fill the SMs (up to 4 x M x N).
+// *err set on a setup failure.
+cudaError_t launch_gemm_x3(const __half* Ah, const __half* Al, const float* sa, int lda, const __half* Bh,
+                           const __half* Bl, const float* sb, int ldb, int M, int N, int K, const float* bias, float* C,
+                           int ldc, bool accumulate, cudaStream_t s, const char** err, int kc = 2,
+                           float* ws = nullptr, size_t ws_floats = 0);
+// Row-scaled hi / lo fp16 split of X [M x K] (pitch ldx) into [M x ldo]
+// buffers (ldo % 8 == 0, >= K; zero-padded) and the row scales scale[M] (2^e).
+cudaError_t launch_split_x3(const float* X, int M, int K, int ldx, __half* hi, __half* lo, int ldo, float* scale,
+                            cudaStream_t s);
+// WT [K x N] = W^T for W [N x K] (fp32, dense).
+cudaError_t launch_transpose_f32(const float* W, int N, int K, float* WT, cudaStream_t s);
 
 }  // namespace ff

@@ -2,34 +2,38 @@
 // SURVEY 8(f) NEXT-3) on the tcgen05 tensor cores.
 //
 // The scorer must keep fp32 accuracy (its scores are compared with the fp64
-// oracle at 1e-4 of a score + 2e-5 of the layer maximum), so a
-// single TF32 product (10-bit mantissa operands) is not enough.  Each operand
-// is split into two TF32 numbers, x = hi + lo with hi = RN_tf32(x) and
-// lo = RN_tf32(x - hi) (|x - hi - lo| <= 2^-22 |x|), and the product is
-//   A B^T ~= Ah Bh^T + Ah Bl^T + Al Bh^T        ("3xTF32"; Al Bl^T ~ 2^-22 dropped)
-// accumulated in fp32 by kind::tf32 MMAs.  Both halves are exact TF32
-// values, so the tensor core's treatment of the 13 low mantissa bits of an
-// operand (ignored) does not matter.
+// oracle at 1e-4 of a score + 2e-5 of the layer maximum), so one
+// low-precision product is not enough.  Each operand row r is scaled by a
+// power of two 2^-e_r (its largest magnitude maps below 2^14, exact) and split
+// into two fp16 numbers, y = x 2^-e_r = hi + lo with hi = RN_fp16(y) and
+// lo = RN_fp16(y - hi): 22 significant bits for every element within 2^-17 of
+// the row's maximum (smaller ones keep an absolute error <= 2^-39 of it).  The
+// product is
+//   A B^T ~= 2^(e_a + e_b) (Ah Bh^T + Ah Bl^T + Al Bh^T)     ("3xFP16"; Al Bl^T ~ 2^-22 dropped)
+// with fp32 accumulation by kind::f16 MMAs (11-bit x 11-bit products are exact
+// in fp32).  Same precision as a hi / lo TF32 split (3xTF32), at half the
+// operand bytes and twice the MMA rate (measured: the 3xTF32 form of this
+// kernel ran at 0.44 of its peak, bound by operand feed).
 //
-// The tensor core's fp32 accumulation is not IEEE round-to-nearest (measured:
-// one TMEM accumulator over K = 3072, i.e. 1152 MMA accumulations, leaves
-// errors ~20x the SIMT SGEMM's), so the K loop is cut into chunks of `kc`
-// k-blocks (default 4 = 128 of K): each chunk accumulates into its own TMEM
-// slot (4-slot ring, 128 columns each), and the epilogue warps add the chunk
-// results in registers with IEEE fp32 adds.
+// The tensor core's fp32 accumulation is not IEEE round-to-nearest (measured
+// with 3xTF32: one TMEM accumulator over K = 3072 left errors ~20x the SIMT
+// SGEMM's), so the K loop is cut into chunks of `kc` k-blocks (default 2 =
+// 128 of K): each chunk accumulates into its own TMEM slot (4-slot ring, 128
+// columns each), and the epilogue warps add the chunk results in registers
+// with IEEE fp32 adds.
 //
-// Operands: A [M x K] and B [N x K], both K-major (row pitch a multiple of 4
-// floats: the split buffers are padded with zeros to K rounded up to 4).  The
-// forward linear Y = X W^T takes B = W; the input-gradient dX = dY W takes
-// B = W^T, split once when the scorer is finalized.
+// Operands: A [M x K] and B [N x K] fp16 hi / lo, both K-major (row pitch a
+// multiple of 8 halves, zero-padded beyond K), with per-row fp32 scales
+// 2^e.  The forward linear Y = X W^T takes B = W; the input-gradient
+// dX = dY W takes B = W^T, both split once when the scorer is finalized.
 //
 // Kernel: persistent, one CTA per SM, 128 x 128 output tiles; warp 0 issues
-// the TMA loads of the four 16 KB operand tiles of a 32-float k-block (3-stage
-// ring, 192 KB), warp 1 issues 12 MMAs per k-block (4 k-steps x 3 products)
-// into the next free TMEM slot, warps 4-7 add each finished slot into their
-// rows' fp32 sums (thread = row, 128 registers) and, after the last chunk of a
-// tile, store sum + bias (+ C) with coalesced row stores through a 32 x 33
-// smem transpose per warp.
+// the TMA loads of the four 16 KB operand tiles of a 64-element k-block
+// (3-stage ring, 192 KB), warp 1 issues 12 MMAs per k-block (4 k-steps x 3
+// products) into the next free TMEM slot, warps 4-7 add each finished slot
+// into their rows' fp32 sums (thread = row, 128 registers) and, after the last
+// chunk of a tile, store sum * 2^(e_a + e_b) + bias (+ C) with coalesced row
+// stores through a 32 x 33 smem transpose per warp.
 #include <algorithm>
 
 #include "ff_kernels.h"
@@ -40,7 +44,7 @@ namespace ff {
 namespace {
 
 constexpr int X3_TM = 128, X3_TN = 128;
-constexpr int X3_KE = 32;                 // fp32 elements per k-block (128 B rows)
+constexpr int X3_KE = 64;                 // fp16 elements per k-block (128 B rows)
 constexpr int X3_STAGES = 3;
 constexpr int X3_TILE = 128 * 128;        // bytes of one 128-row x 128 B operand tile
 constexpr int X3_STAGE = 4 * X3_TILE;     // Ah, Al, Bh, Bl
@@ -50,30 +54,17 @@ constexpr int X3_BAR_OFF = X3_EPI_OFF + 4 * X3_EPI_WARP;
 constexpr int X3_SMEM = X3_BAR_OFF + 128 + 1024;  // + barriers + 1024-B alignment slack
 constexpr int X3_THREADS = 256;
 
-// kind::tf32 instruction descriptor: D f32 (bits 4-5 = 1), A / B TF32 (bits
-// 7-9, 10-12 = 2), both K-major, N >> 3 at bit 17, M >> 4 at bit 24.
+// kind::f16 instruction descriptor: D f32 (bits 4-5 = 1), A / B fp16 (bits
+// 7-9, 10-12 = 0), both K-major, N >> 3 at bit 17, M >> 4 at bit 24.
 __host__ __device__ constexpr uint32_t x3_idesc() {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(X3_TN >> 3) << 17) | ((uint32_t)(X3_TM >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
-__device__ __forceinline__ float rna_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  return (1u << 4) | ((uint32_t)(X3_TN >> 3) << 17) | ((uint32_t)(X3_TM >> 4) << 24);
 }
 
 struct X3Params {
   float* C;
   const float* bias;
+  const float* sa;  // per-row scales 2^e of A [M] and of B [N]
+  const float* sb;
   int M, N, ldc, accumulate;
   int m_tiles, n_tiles, k_blocks;
   int kc;  // k-blocks per TMEM accumulation chunk
@@ -178,12 +169,12 @@ __global__ void __launch_bounds__(X3_THREADS, 1)
           const uint64_t ah = make_sw128_desc(st), al = make_sw128_desc(st + X3_TILE);
           const uint64_t bh = make_sw128_desc(st + 2 * X3_TILE), bl = make_sw128_desc(st + 3 * X3_TILE);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {  // 4 x 8 fp32 (32 B) of K; +2 = +32 B in the >>4 address field
+          for (int k = 0; k < 4; ++k) {  // 4 x 16 fp16 (32 B) of K; +2 = +32 B in the >>4 address field
             // small products first: the larger Ah Bh^T term then adds to an accumulator already
             // holding the corrections of this k-step
-            mma_tf32(d_tmem, al + 2 * k, bh + 2 * k, idesc, (kin | k) != 0);
-            mma_tf32(d_tmem, ah + 2 * k, bl + 2 * k, idesc, 1);
-            mma_tf32(d_tmem, ah + 2 * k, bh + 2 * k, idesc, 1);
+            mma_f16(d_tmem, al + 2 * k, bh + 2 * k, idesc, (kin | k) != 0);
+            mma_f16(d_tmem, ah + 2 * k, bl + 2 * k, idesc, 1);
+            mma_f16(d_tmem, ah + 2 * k, bh + 2 * k, idesc, 1);
           }
           mma_commit(&empty[stage]);
           if (++stage == X3_STAGES) {
@@ -237,14 +228,17 @@ __global__ void __launch_bounds__(X3_THREADS, 1)
           acc_phase ^= 1;
         }
       }
+      // undo the operand scaling: this thread's row scale now, the column's at the store
+      const float srow = row0 + lane < p.M ? __ldg(p.sa + row0 + lane) : 0.0f;
 #pragma unroll
       for (int c = 0; c < X3_TN / 32; ++c) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = sum[c * 32 + j];
+        for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = sum[c * 32 + j] * srow;
         __syncwarp();
         const int col = nt * X3_TN + c * 32 + lane;
         const bool cok = col < p.N;
         const float b = (!part && p.bias != nullptr && cok) ? __ldg(p.bias + col) : 0.0f;
+        const float scol = cok ? __ldg(p.sb + col) : 0.0f;
         float* dst = out + (size_t)row0 * ldo + col;
         const int nrows = min(32, p.M - row0);
         if (p.accumulate && !part) {  // 16 loads of C in flight before the stores
@@ -256,12 +250,12 @@ __global__ void __launch_bounds__(X3_THREADS, 1)
               cv[rr] = (cok && h + rr < nrows) ? dst[(size_t)(h + rr) * ldo] : 0.0f;
 #pragma unroll
             for (int rr = 0; rr < 16; ++rr)
-              if (cok && h + rr < nrows) dst[(size_t)(h + rr) * ldo] = buf[(h + rr) * 33 + lane] + b + cv[rr];
+              if (cok && h + rr < nrows) dst[(size_t)(h + rr) * ldo] = buf[(h + rr) * 33 + lane] * scol + b + cv[rr];
           }
         } else {
 #pragma unroll
           for (int rr = 0; rr < 32; ++rr)
-            if (cok && rr < nrows) dst[(size_t)rr * ldo] = buf[rr * 33 + lane] + b;
+            if (cok && rr < nrows) dst[(size_t)rr * ldo] = buf[rr * 33 + lane] * scol + b;
         }
         __syncwarp();
       }
@@ -275,30 +269,39 @@ __global__ void __launch_bounds__(X3_THREADS, 1)
   }
 }
 
-// hi / lo TF32 split of X [M x K] (pitch ldx) into [M x ldo] (ldo >= K, the
-// columns [K, ldo) zero-filled).  One thread per 4 output columns.
-__global__ void split_tf32_kernel(const float* __restrict__ X, int M, int K, int ldx, float* __restrict__ hi,
-                                  float* __restrict__ lo, int ldo) {
-  const int q4 = ldo >> 2;
-  const size_t n = (size_t)M * q4;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    const int r = (int)(i / q4), k0 = (int)(i - (size_t)r * q4) * 4;
-    float x[4], h[4], l[4];
+// Row-scaled fp16 hi / lo split of X [M x K] (pitch ldx) into [M x ldo]
+// (ldo even, >= K; columns [K, ldo) zero): one warp per row finds max |x|,
+// picks 2^-e with max |x| 2^-e < 2^14 (e = 0 for an all-zero row), then
+// writes hi = RN_fp16(y), lo = RN_fp16(y - hi) of y = x 2^-e and scale[r] = 2^e.
+__global__ void split_x3_kernel(const float* __restrict__ X, int M, int K, int ldx, __half* __restrict__ hi,
+                                __half* __restrict__ lo, int ldo, float* __restrict__ scale) {
+  const int r = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (r >= M) return;
+  const float* x = X + (size_t)r * ldx;
+  float mx = 0.0f;
+  for (int k = lane; k < K; k += 32) mx = fmaxf(mx, fabsf(x[k]));
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      x[j] = k0 + j < K ? X[(size_t)r * ldx + k0 + j] : 0.0f;
-      h[j] = rna_tf32(x[j]);
-      l[j] = rna_tf32(x[j] - h[j]);
-    }
-    *reinterpret_cast<float4*>(hi + (size_t)r * ldo + k0) = make_float4(h[0], h[1], h[2], h[3]);
-    *reinterpret_cast<float4*>(lo + (size_t)r * ldo + k0) = make_float4(l[0], l[1], l[2], l[3]);
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  int e = 14;  // all-zero row: scale 1
+  if (mx > 0.0f) {
+    frexpf(mx, &e);  // mx < 2^e
+    e = max(e, -100);  // keeps 2^(14 - e) finite; such rows are ~0 anyway
+  }
+  const float inv = ldexpf(1.0f, 14 - e);
+  if (lane == 0) scale[r] = ldexpf(1.0f, e - 14);
+  __half2* h2 = reinterpret_cast<__half2*>(hi + (size_t)r * ldo);
+  __half2* l2 = reinterpret_cast<__half2*>(lo + (size_t)r * ldo);
+  for (int k = 2 * lane; k < ldo; k += 64) {
+    const float y0 = k < K ? x[k] * inv : 0.0f, y1 = k + 1 < K ? x[k + 1] * inv : 0.0f;
+    const __half2 h = __floats2half2_rn(y0, y1);
+    const float2 f = __half22float2(h);
+    h2[k >> 1] = h;
+    l2[k >> 1] = __floats2half2_rn(y0 - f.x, y1 - f.y);
   }
 }
 
-// Transposed split: W [N x K] (pitch K) -> hi / lo [K x ldo] holding W^T
-// (ldo >= N, columns [N, ldo) zero).  32 x 32 smem tiles.
-__global__ void split_tf32_t_kernel(const float* __restrict__ W, int N, int K, float* __restrict__ hi,
-                                    float* __restrict__ lo, int ldo) {
+// W [N x K] (pitch K) -> WT [K x N] (pitch N), 32 x 32 smem tiles.
+__global__ void transpose_f32_kernel(const float* __restrict__ W, int N, int K, float* __restrict__ WT) {
   __shared__ float t[32][33];
   const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -308,12 +311,7 @@ __global__ void split_tf32_t_kernel(const float* __restrict__ W, int N, int K, f
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int k = k0 + i, n = n0 + threadIdx.x;
-    if (k < K && n < ldo) {
-      const float x = t[threadIdx.x][i];
-      const float h = rna_tf32(x);
-      hi[(size_t)k * ldo + n] = h;
-      lo[(size_t)k * ldo + n] = rna_tf32(x - h);
-    }
+    if (k < K && n < N) WT[(size_t)k * N + n] = t[threadIdx.x][i];
   }
 }
 
@@ -378,24 +376,25 @@ int pick_splits(int tiles, int k_blocks, size_t MN, int cap) {
 
 }  // namespace
 
-cudaError_t launch_gemm_x3(const float* Ah, const float* Al, int lda, const float* Bh, const float* Bl, int ldb,
-                           int M, int N, int K, const float* bias, float* C, int ldc, bool accumulate, cudaStream_t s,
-                           const char** err, int kc, float* ws, size_t ws_floats) {
+cudaError_t launch_gemm_x3(const __half* Ah, const __half* Al, const float* sa, int lda, const __half* Bh,
+                           const __half* Bl, const float* sb, int ldb, int M, int N, int K, const float* bias, float* C,
+                           int ldc, bool accumulate, cudaStream_t s, const char** err, int kc, float* ws,
+                           size_t ws_floats) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   if (kc < 1) {
     *err = "gemm_x3: kc must be >= 1";
     return cudaErrorInvalidValue;
   }
-  if ((lda & 3) || (ldb & 3) || K > lda || K > ldb) {
-    *err = "gemm_x3: operand pitch must be a multiple of 4 floats and >= K";
+  if ((lda & 7) || (ldb & 7) || K > lda || K > ldb) {
+    *err = "gemm_x3: operand pitch must be a multiple of 8 halves and >= K";
     return cudaErrorInvalidValue;
   }
   // the maps cover the K-padded width (zeros), so K rounds up to whole k-blocks
   CUtensorMap ah, al, bh, bl;
-  if (!make_operand_map(&ah, Ah, M, lda, 4, (size_t)lda * 4, 128, err) ||
-      !make_operand_map(&al, Al, M, lda, 4, (size_t)lda * 4, 128, err) ||
-      !make_operand_map(&bh, Bh, N, ldb, 4, (size_t)ldb * 4, 128, err) ||
-      !make_operand_map(&bl, Bl, N, ldb, 4, (size_t)ldb * 4, 128, err))
+  if (!make_operand_map(&ah, Ah, M, lda, 2, (size_t)lda * 2, 128, err) ||
+      !make_operand_map(&al, Al, M, lda, 2, (size_t)lda * 2, 128, err) ||
+      !make_operand_map(&bh, Bh, N, ldb, 2, (size_t)ldb * 2, 128, err) ||
+      !make_operand_map(&bl, Bl, N, ldb, 2, (size_t)ldb * 2, 128, err))
     return cudaErrorInvalidValue;
   static bool attr_set = false;  // per process; all devices are B200s
   if (!attr_set) {
@@ -406,6 +405,8 @@ cudaError_t launch_gemm_x3(const float* Ah, const float* Al, int lda, const floa
   X3Params p{};
   p.C = C;
   p.bias = bias;
+  p.sa = sa;
+  p.sb = sb;
   p.M = M;
   p.N = N;
   p.ldc = ldc;
@@ -434,17 +435,16 @@ cudaError_t launch_gemm_x3(const float* Ah, const float* Al, int lda, const floa
   return cudaGetLastError();
 }
 
-cudaError_t launch_split_tf32(const float* X, int M, int K, int ldx, float* hi, float* lo, int ldo, cudaStream_t s) {
+cudaError_t launch_split_x3(const float* X, int M, int K, int ldx, __half* hi, __half* lo, int ldo, float* scale,
+                            cudaStream_t s) {
   if (M <= 0) return cudaSuccess;
-  const size_t n = (size_t)M * (ldo >> 2);
-  const int blocks = (int)std::min<size_t>((n + 255) / 256, (size_t)kNumSMs * 8);
-  split_tf32_kernel<<<blocks, 256, 0, s>>>(X, M, K, ldx, hi, lo, ldo);
+  split_x3_kernel<<<(M + 7) / 8, 256, 0, s>>>(X, M, K, ldx, hi, lo, ldo, scale);
   return cudaGetLastError();
 }
 
-cudaError_t launch_split_tf32_t(const float* W, int N, int K, float* hi, float* lo, int ldo, cudaStream_t s) {
-  dim3 grid((ldo + 31) / 32, (K + 31) / 32);
-  split_tf32_t_kernel<<<grid, dim3(32, 8), 0, s>>>(W, N, K, hi, lo, ldo);
+cudaError_t launch_transpose_f32(const float* W, int N, int K, float* WT, cudaStream_t s) {
+  if (N <= 0 || K <= 0) return cudaSuccess;
+  transpose_f32_kernel<<<dim3((N + 31) / 32, (K + 31) / 32), dim3(32, 8), 0, s>>>(W, N, K, WT);
   return cudaGetLastError();
 }
 

@@ -546,18 +546,20 @@ const char* kSLayer[16] = {
     "output.dense.weight", "output.dense.bias", "output.LayerNorm.weight", "output.LayerNorm.bias"};
 
 struct XSplit {
-  size_t h = 0, l = 0;  // hi / lo offsets in the weight arena
-  int ld = 0;           // row pitch (floats, multiple of 4)
+  size_t h = 0, l = 0;  // fp16 hi / lo offsets in the weight arena
+  size_t s = 0;         // per-row scales (fp32, 2^e)
+  int ld = 0;           // row pitch (halves, multiple of 8)
 };
-inline int round4(int x) { return (x + 3) & ~3; }
+inline int round8(int x) { return (x + 7) & ~7; }
 
 struct SLayer {
   int A, D, F;
   size_t wqkv, bqkv, wo, bo, g1, b1, w1, bi1, w2, bi2, g2, b2;  // weight offsets
   size_t X, QKV, P, Cx, Y1, XH1, R1, U, Act, XH2, R2;          // saved activations (workspace)
-  // TF32 hi / lo splits of the linears' weights for the tcgen05 path (weight
-  // arena, written by ff_scorer_finalize): W [N x K] as [N x round4(K)] (forward
-  // B operand) and W^T as [K x round4(N)] (input-gradient B operand).
+  // Row-scaled fp16 hi / lo splits of the linears' weights for the tcgen05
+  // path (weight arena, written by ff_scorer_finalize): W [N x K] as
+  // [N x round8(K)] (forward B operand) and W^T as [K x round8(N)]
+  // (input-gradient B operand).
   XSplit qkv, qkvT, o, oT, f1, f1T, f2, f2T;
   uint32_t loaded = 0;
 };
@@ -573,13 +575,16 @@ struct ff_scorer {
   uint32_t top_loaded = 0;
   size_t wbytes = 0, wsbytes = 0;
   size_t Xout, dX, dZ, dY1, dAm, dC, dP, dQKV, colg, lossb, errf, skws, headws, ids, mask, labels;
-  size_t xh = 0, xl = 0;  // TF32 hi / lo split of the current linear's input [M x round4(Kmax)]
+  size_t xh = 0, xl = 0, xs = 0;  // fp16 hi / lo split of the current linear's input [M x round8(Kmax)], row scales
+  size_t tws = 0, tws_floats = 0;  // finalize-time transpose scratch (the split-K region, free then)
   int Dmax = 0, Fmax = 0, Amax = 0, Kmax = 0;
   int tc_linears = 1;     // FF_SCORER_OPT_TC_LINEARS
   uint8_t* dW = nullptr;
   uint8_t* dWS = nullptr;
   float* w(size_t o) const { return reinterpret_cast<float*>(dW + o); }
   float* ws(size_t o) const { return reinterpret_cast<float*>(dWS + o); }
+  __half* hw(size_t o) const { return reinterpret_cast<__half*>(dW + o); }
+  __half* hws(size_t o) const { return reinterpret_cast<__half*>(dWS + o); }
 };
 
 namespace {
@@ -620,11 +625,12 @@ void plan_scorer(ff_scorer* m) {
     P.g2 = take(H);
     P.b2 = take(H);
   }
-  // TF32 hi / lo splits of the four linears' weights and of their transposes
+  // fp16 hi / lo splits of the four linears' weights and of their transposes
   auto split = [&](XSplit& x, size_t rows, int cols) {
-    x.ld = round4(cols);
-    x.h = take(rows * x.ld);
-    x.l = take(rows * x.ld);
+    x.ld = round8(cols);
+    x.h = take((rows * x.ld + 1) / 2);
+    x.l = take((rows * x.ld + 1) / 2);
+    x.s = take(rows);
   };
   for (int l = 0; l < c.num_layers; ++l) {
     SLayer& P = m->L[l];
@@ -668,11 +674,17 @@ void plan_scorer(ff_scorer* m) {
   m->dP = take(M * m->Amax * Sm);
   m->dQKV = take(M * 3 * m->Dmax);
   m->colg = take((size_t)kRowChunks * std::max(m->Fmax, m->Dmax));
-  m->skws = take(4 * M * std::max((size_t)H, (size_t)m->Dmax));  // split-K partials
+  {  // split-K partials; at finalize, the fp32 transpose of one weight (the largest fits)
+    size_t wmax = 0;
+    for (const SLayer& P : m->L) wmax = std::max(wmax, std::max((size_t)3 * P.D * H, (size_t)P.F * H));
+    m->tws_floats = std::max(4 * M * std::max((size_t)H, (size_t)m->Dmax), wmax);
+    m->skws = m->tws = take(m->tws_floats);
+  }
   m->headws = take(2 * M * H);                                     // head: pool, dpre [B x H] each
   m->lossb = take(M);
-  m->xh = take(M * round4(m->Kmax));
-  m->xl = take(M * round4(m->Kmax));
+  m->xh = take((M * round8(m->Kmax) + 1) / 2);
+  m->xl = take((M * round8(m->Kmax) + 1) / 2);
+  m->xs = take(M);
   m->errf = take(64);
   m->wsbytes = o;
 }
@@ -709,8 +721,8 @@ ff_status launch_ck(cudaError_t e, const char* what) {
 int rows_threads(int H) { return H >= 512 ? 256 : 128; }
 
 // One linear of the scorer, Y[M x N] (+)= X[M x K] B^T (+ bias) with B the
-// TF32-split weight operand w ([N x K]: W for Y = X W^T, W^T for dX = dY W):
-// split X, then the 3xTF32 tcgen05 GEMM (gemm_x3.cu).  With
+// split weight operand w ([N x K]: W for Y = X W^T, W^T for dX = dY W): split
+// X (row-scaled fp16 hi / lo), then the 3xFP16 tcgen05 GEMM (gemm_x3.cu).  With
 // FF_SCORER_OPT_TC_LINEARS = 0 the SIMT SGEMM `g` (same contraction) runs instead.
 ff_status linear(ff_scorer* m, const SG& g, const XSplit& w, const SplitKScratch& sk, cudaStream_t s,
                  const char* what) {
@@ -718,13 +730,14 @@ ff_status linear(ff_scorer* m, const SG& g, const XSplit& w, const SplitKScratch
     SL(sgemm(g, 1, s, sk), what);
     return FF_OK;
   }
-  const int K = g.K, kp = round4(K);
-  float* xh = m->ws(m->xh);
-  float* xl = m->ws(m->xl);
-  SL(ff::launch_split_tf32(g.A, g.M, K, (int)g.sAm, xh, xl, kp, s), what);
+  const int K = g.K, kp = round8(K);
+  __half* xh = m->hws(m->xh);
+  __half* xl = m->hws(m->xl);
+  float* xs = m->ws(m->xs);
+  SL(ff::launch_split_x3(g.A, g.M, K, (int)g.sAm, xh, xl, kp, xs, s), what);
   const char* err = nullptr;
-  const cudaError_t e = ff::launch_gemm_x3(xh, xl, kp, m->w(w.h), m->w(w.l), w.ld, g.M, g.N, K, g.bias, g.C,
-                                           (int)g.sCm, g.accumulate != 0, s, &err, 4, sk.ws, sk.cap);
+  const cudaError_t e = ff::launch_gemm_x3(xh, xl, xs, kp, m->hw(w.h), m->hw(w.l), m->w(w.s), w.ld, g.M, g.N, K,
+                                           g.bias, g.C, (int)g.sCm, g.accumulate != 0, s, &err, 2, sk.ws, sk.cap);
   if (e != cudaSuccess) return sfail(FF_E_CUDA, std::string(what) + ": " + (err ? err : cudaGetErrorString(e)));
   return FF_OK;
 }
@@ -743,7 +756,7 @@ ff_status score_batch(ff_scorer* m, const int* ids, const int* mask, const int* 
   const size_t lnsm = (size_t)(H + 32) * 4;
   SplitKScratch sk;  // split-K scratch of this scorer (stream-ordered use)
   sk.ws = m->ws(m->skws);
-  sk.cap = 4 * (size_t)c.max_tokens * (size_t)std::max(H, m->Dmax);
+  sk.cap = m->tws_floats;
   // ---- forward, keeping what the backward needs
   int* errf = reinterpret_cast<int*>(m->dWS + m->errf);
   embed_ln_f32_kernel<<<M, rt, lnsm, s>>>(ids, mask, S, H, c.vocab_size, m->w(m->tok), m->w(m->pos), m->w(m->type0),
@@ -988,8 +1001,9 @@ ff_status ff_scorer_finalize(ff_scorer* m, void* stream) {
   if (m->top_loaded != 511u) return sfail(FF_E_STATE, "missing embedding / pooler / classifier tensors");
   for (auto& P : m->L)
     if (P.loaded != 0xFFFFu) return sfail(FF_E_STATE, "missing layer tensors");
-  // TF32 hi / lo splits of every linear's weight and its transpose (the B
-  // operands of the tcgen05 linears), from the loaded fp32 weights
+  // row-scaled fp16 hi / lo splits of every linear's weight and of its
+  // transpose (the B operands of the tcgen05 linears), from the loaded fp32
+  // weights; W^T goes through the split-K scratch of the workspace
   SDev dg_(m->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int H = m->cfg.hidden;
@@ -1002,8 +1016,12 @@ ff_status ff_scorer_finalize(ff_scorer* m, void* stream) {
     } ws[4] = {{P.wqkv, 3 * D, H, &P.qkv, &P.qkvT}, {P.wo, H, D, &P.o, &P.oT}, {P.w1, F, H, &P.f1, &P.f1T},
                {P.w2, H, F, &P.f2, &P.f2T}};
     for (auto& x : ws) {
-      SC_CK(ff::launch_split_tf32(m->w(x.w), x.n, x.k, x.k, m->w(x.fwd->h), m->w(x.fwd->l), x.fwd->ld, s));
-      SC_CK(ff::launch_split_tf32_t(m->w(x.w), x.n, x.k, m->w(x.bwd->h), m->w(x.bwd->l), x.bwd->ld, s));
+      SC_CK(ff::launch_split_x3(m->w(x.w), x.n, x.k, x.k, m->hw(x.fwd->h), m->hw(x.fwd->l), x.fwd->ld,
+                                m->w(x.fwd->s), s));
+      if ((size_t)x.n * x.k > m->tws_floats) return sfail(FF_E_STATE, "transpose scratch too small");
+      float* wt = m->ws(m->tws);
+      SC_CK(ff::launch_transpose_f32(m->w(x.w), x.n, x.k, wt, s));
+      SC_CK(ff::launch_split_x3(wt, x.k, x.n, x.n, m->hw(x.bwd->h), m->hw(x.bwd->l), x.bwd->ld, m->w(x.bwd->s), s));
     }
   }
   SC_CK(cudaStreamSynchronize(s));
@@ -1048,22 +1066,25 @@ ff_status ff_debug_gemm_x3(const float* d_A, int32_t lda, const float* d_B, int3
   if (!d_A || !d_B || !d_C) return sfail(FF_E_INVALID, "null argument");
   if (M < 1 || N < 1 || K < 1 || lda < K || ldb < K || ldc < N || kc < 1) return sfail(FF_E_SHAPE, "bad GEMM shape");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int kp = round4(K);
-  float *ah = nullptr, *bh = nullptr;
-  SC_CK(cudaMallocAsync(reinterpret_cast<void**>(&ah), (size_t)2 * M * kp * 4, s));
-  SC_CK(cudaMallocAsync(reinterpret_cast<void**>(&bh), (size_t)2 * N * kp * 4, s));
-  float* ws = nullptr;  // split-K partials, as the scorer provides
+  const int kp = round8(K);
+  __half *ah = nullptr, *bh = nullptr;
+  float *sa = nullptr, *ws = nullptr;  // row scales; split-K partials, as the scorer provides
+  SC_CK(cudaMallocAsync(reinterpret_cast<void**>(&ah), (size_t)2 * M * kp * 2, s));
+  SC_CK(cudaMallocAsync(reinterpret_cast<void**>(&bh), (size_t)2 * N * kp * 2, s));
+  SC_CK(cudaMallocAsync(reinterpret_cast<void**>(&sa), (size_t)(M + N) * 4, s));
   SC_CK(cudaMallocAsync(reinterpret_cast<void**>(&ws), (size_t)4 * M * N * 4, s));
-  float* al = ah + (size_t)M * kp;
-  float* bl = bh + (size_t)N * kp;
-  cudaError_t e = ff::launch_split_tf32(d_A, M, K, lda, ah, al, kp, s);
-  if (e == cudaSuccess) e = ff::launch_split_tf32(d_B, N, K, ldb, bh, bl, kp, s);
+  __half* al = ah + (size_t)M * kp;
+  __half* bl = bh + (size_t)N * kp;
+  float* sb = sa + M;
+  cudaError_t e = ff::launch_split_x3(d_A, M, K, lda, ah, al, kp, sa, s);
+  if (e == cudaSuccess) e = ff::launch_split_x3(d_B, N, K, ldb, bh, bl, kp, sb, s);
   const char* err = nullptr;
   if (e == cudaSuccess)
-    e = ff::launch_gemm_x3(ah, al, kp, bh, bl, kp, M, N, K, d_bias, d_C, ldc, accumulate != 0, s, &err, kc, ws,
-                           (size_t)4 * M * N);
+    e = ff::launch_gemm_x3(ah, al, sa, kp, bh, bl, sb, kp, M, N, K, d_bias, d_C, ldc, accumulate != 0, s, &err, kc,
+                           ws, (size_t)4 * M * N);
   cudaFreeAsync(ah, s);
   cudaFreeAsync(bh, s);
+  cudaFreeAsync(sa, s);
   cudaFreeAsync(ws, s);
   if (e != cudaSuccess) return sfail(FF_E_CUDA, err ? err : cudaGetErrorString(e));
   return FF_OK;

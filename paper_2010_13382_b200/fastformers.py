@@ -352,8 +352,8 @@ def _scheck(status: int):
         raise FFError(status, lib().ff_scorer_last_error().decode(errors="replace"))
 
 
-def gemm_x3(A, B, bias=None, out=None, accumulate=False, kc=4):
-    """ff_debug_gemm_x3: C (+)= A B^T (+ bias) on the scorer's 3xTF32 tcgen05
+def gemm_x3(A, B, bias=None, out=None, accumulate=False, kc=2):
+    """ff_debug_gemm_x3: C (+)= A B^T (+ bias) on the scorer's 3xFP16 tcgen05
     GEMM; A [M, K], B [N, K] fp32 CUDA tensors (unit column stride)."""
     import torch
     M, K = A.shape

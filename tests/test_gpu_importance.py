@@ -7,9 +7,10 @@ so its fp32-vs-fp64 error is relative to the layer's score scale, not to the
 (possibly cancelling) score itself: |gpu - ref| <= 1e-4 |ref| + 2e-5 max_l(ref)
 (measured, tools/importance_err.py: <= 2.2e-6 of the layer max on all three
 configs with the SIMT linears, so the bound has ~10x headroom).  The default
-linears are 3xTF32 on tcgen05 (gemm_x3.cu: hi / lo TF32 splits, per-product
-error <= ~2^-21 relative, fp32 accumulation in TMEM); every parity test runs
-both paths against the same oracle and the same bound."""
+linears are 3xFP16 on tcgen05 (gemm_x3.cu: row-scaled fp16 hi / lo splits,
+per-product error <= ~2^-21 relative, fp32 accumulation in TMEM in 128-wide
+K chunks summed with IEEE adds); every parity test runs both paths against the
+same oracle and the same bound."""
 import numpy as np
 import pytest
 
@@ -166,7 +167,7 @@ def test_scorer_flags_invalid_inputs_without_faulting():
 
 
 def test_tc_linears_match_simt_linears_on_ragged_tails():
-    """The 3xTF32 tcgen05 linears against the SIMT fp32 SGEMM on a shape with
+    """The 3xFP16 tcgen05 linears against the SIMT fp32 SGEMM on a shape with
     ragged M / N / K tails in every linear (H = 50: K not a multiple of 4;
     D = 3 x 12, F = 70 / 130: N tails; M = 5 x 29 = 145 rows: an M tail), two
     batches accumulating: scores, loss and logits agree at fp32 level."""
@@ -192,7 +193,7 @@ def test_tc_linears_match_simt_linears_on_ragged_tails():
 
 
 def test_reload_after_finalize_requires_finalize():
-    """Loading a tensor after ff_scorer_finalize invalidates the TF32 splits:
+    """Loading a tensor after ff_scorer_finalize invalidates the weight splits:
     ff_score_batch refuses (FF_E_STATE) until finalize runs again."""
     import ctypes
     cfg = _tiny()
@@ -221,10 +222,10 @@ def test_reload_after_finalize_requires_finalize():
 
 @pytest.mark.parametrize("M,N,K", [(128, 128, 32), (300, 200, 100), (1, 5, 3), (257, 130, 3072), (4096, 768, 3072)])
 def test_gemm_x3_against_fp64(M, N, K):
-    """The scorer's 3xTF32 tcgen05 GEMM (ff_debug_gemm_x3) against an fp64
+    """The scorer's 3xFP16 tcgen05 GEMM (ff_debug_gemm_x3) against an fp64
     matmul of the same fp32 inputs: the error is bounded by fp32-level terms,
-    |err| <= 2^-20 * sum_k |a_ik b_jk| + 2^-24 |c| (3 TF32 products ~2^-21
-    relative each, chunked IEEE accumulation), and within 16x the error of a
+    |err| <= 2^-20 * sum_k |a_ik b_jk| + 2^-24 |c| (3 products of 11-bit
+    halves, ~2^-21 relative each; chunked IEEE accumulation), and within 16x the error of a
     plain fp32 torch matmul (TF32 disabled) on the same inputs."""
     g = torch.Generator().manual_seed(M * 7 + N * 3 + K)
     A = torch.randn(M, K, generator=g, dtype=torch.float64)
@@ -250,7 +251,7 @@ def test_gemm_x3_against_fp64(M, N, K):
 
 
 def test_gemm_x3_chunking_reduces_error():
-    """One TMEM accumulator over the whole K (kc = K / 32) is less accurate
+    """One TMEM accumulator over the whole K (kc = K / 64) is less accurate
     than the default 128-wide chunks summed with IEEE adds (the design reason
     for chunking, gemm_x3.cu); both stay within the fp32-level bound's 4x."""
     g = torch.Generator().manual_seed(5)
@@ -259,7 +260,25 @@ def test_gemm_x3_chunking_reduces_error():
     B = torch.randn(N, K, generator=g, dtype=torch.float64).abs() * 0.05
     ref = A @ B.T
     A32, B32 = A.float().cuda(), B.float().cuda()
-    e_chunk = (ffb.gemm_x3(A32, B32, kc=4).double().cpu() - ref).abs().max()
-    e_whole = (ffb.gemm_x3(A32, B32, kc=K // 32).double().cpu() - ref).abs().max()
+    e_chunk = (ffb.gemm_x3(A32, B32, kc=2).double().cpu() - ref).abs().max()
+    e_whole = (ffb.gemm_x3(A32, B32, kc=K // 64).double().cpu() - ref).abs().max()
     print("max abs err chunked %.3e whole-K %.3e" % (e_chunk, e_whole))
     assert e_chunk <= e_whole
+
+
+def test_gemm_x3_row_scaling_handles_wide_dynamic_range():
+    """Rows of very different magnitude (1e-30 .. 1e30, and an all-zero row)
+    keep fp32-level relative accuracy: each operand row is scaled by its own
+    power of two before the fp16 split (gemm_x3.cu)."""
+    g = torch.Generator().manual_seed(11)
+    M, N, K = 130, 70, 200
+    A = torch.randn(M, K, generator=g, dtype=torch.float64)
+    A *= torch.logspace(-30, 30, M, dtype=torch.float64)[:, None]
+    A[7] = 0.0
+    B = torch.randn(N, K, generator=g, dtype=torch.float64) * torch.logspace(-5, 5, N, dtype=torch.float64)[:, None]
+    A32, B32 = A.float(), B.float()
+    ref = A32.double() @ B32.double().T
+    got = ffb.gemm_x3(A32.cuda(), B32.cuda()).double().cpu()
+    bound = 2.0 ** -20 * (A32.double().abs() @ B32.double().abs().T)
+    assert ((got - ref).abs() <= bound).all()
+    assert (got[7] == 0).all()
