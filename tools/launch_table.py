@@ -16,7 +16,7 @@ for r in rows[hi + 1:]:
         continue
     name = r[ki].split("(")[0].replace("void ", "")
     t = float(r[vi].replace(",", ""))
-    unit = 1e-3 if "nsecond" in r[h.index("Metric Unit")] else 1.0
+    unit = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}[r[h.index("Metric Unit")]]
     tot[name] += t * unit
     cnt[name] += 1
 T = sum(tot.values())
