@@ -22,6 +22,7 @@ import json
 import os
 import statistics
 import sys
+import subprocess
 import threading
 import time
 
@@ -259,16 +260,37 @@ def importance_variant(stream, flush, B=32, S=128, n=10):
                            "sample": "1 sequence, numpy fp64 forward + backward"}}
 
 
+def physical_cores():
+    """Physical cores of the host (lscpu CORE,SOCKET pairs), for the record."""
+    try:
+        out = subprocess.run(["lscpu", "-p=CORE,SOCKET"], capture_output=True, text=True, timeout=10).stdout
+        return len({l for l in out.splitlines() if l and not l.startswith("#")}) or None
+    except (OSError, subprocess.SubprocessError):
+        return None
+
+
 def cpu_baseline(cfg, weights, ids, mask, per_core=8):
-    """The oracle as it stands, multi-instance on the host cores (one
-    single-threaded instance per core, whole sequences): `per_core`
-    sequences per core, ~10 s of wall time on C3 (~160 core-seconds)."""
+    """The oracle as it stands, multi-instance on the host cores (P:114, P:150:
+    one single-threaded instance per core, whole sequences): `per_core`
+    sequences per core, each worker thread pinned to its own core
+    (os.sched_setaffinity on the calling thread; the oracle is a C library
+    called without the GIL), ~10 s of wall time on C3.  Also records the
+    single-core rate and, as context, PyTorch's own FBGEMM int8 path
+    (fbgemm_context)."""
     import oracle
-    cores = len(os.sched_getaffinity(0))
+    cpus = sorted(os.sched_getaffinity(0))
+    cores = len(cpus)
     n = per_core * cores
     orc = oracle.Oracle(cfg, weights)
+    t0 = time.perf_counter()
+    orc.encode(ids[:1], mask[:1])
+    single = 1.0 / (time.perf_counter() - t0)
 
     def work(i):
+        try:
+            os.sched_setaffinity(0, {cpus[i]})  # this thread only
+        except OSError:
+            pass
         for r in range(per_core):
             j = (i * per_core + r) % ids.shape[0]
             orc.encode(ids[j:j + 1], mask[j:j + 1])
@@ -280,9 +302,95 @@ def cpu_baseline(cfg, weights, ids, mask, per_core=8):
     for t in ths:
         t.join()
     wall = time.perf_counter() - t0
-    return {"value": n / wall, "unit": "sequences/s", "cores": cores, "kind": "oracle",
-            "sample": f"{n} sequences of {cfg.name} (S={ids.shape[1]}, {'int8' if cfg.dtype[0] else 'fp16'} emulation),"
-                      f" {per_core} per core on {cores} threads (one oracle call per sequence), wall {wall:.1f} s"}
+    out = {"value": n / wall, "unit": "sequences/s", "cores": cores, "kind": "oracle",
+           "sample": f"{n} sequences of {cfg.name} (S={ids.shape[1]}, {'int8' if cfg.dtype[0] else 'fp16'} emulation),"
+                     f" {per_core} per core on {cores} pinned threads (one oracle call per sequence), wall {wall:.1f} s",
+           "single_core": single, "physical_cores": physical_cores()}
+    try:
+        out["fbgemm_context"] = fbgemm_context(cfg, weights, ids, mask, cores)
+    except Exception as e:  # context only: never fail the bench line on it
+        out["fbgemm_context"] = {"unavailable": str(e)[:200]}
+    return out
+
+
+def fbgemm_context(cfg, weights, ids, mask, cores, seconds=6.0):
+    """Context for the CPU side: the same encoder shapes in plain
+    PyTorch on the host cores with torch.ao.quantization.quantize_dynamic
+    (int8 nn.Linear on FBGEMM, fp32 attention / LN / GELU) -- the CPU int8
+    path the paper's comparison uses (P:104 onnxruntime dynamic int8 plays the
+    same role).  Not the oracle and not a parity reference: a throughput line."""
+    import numpy as np
+    import torch
+    import torch.nn.functional as Fn
+
+    torch.backends.quantized.engine = "fbgemm"
+    H, d = cfg.hidden, cfg.head_dim
+
+    def lin(name, fin, fout):
+        m = torch.nn.Linear(fin, fout)
+        m.weight.data = torch.from_numpy(np.ascontiguousarray(weights[name + ".weight"], np.float32))
+        m.bias.data = torch.from_numpy(np.ascontiguousarray(weights[name + ".bias"], np.float32))
+        return m
+
+    class Enc(torch.nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.layers = torch.nn.ModuleList()
+            for l in range(cfg.num_layers):
+                A, F, pre = cfg.heads[l], cfg.ffn_dim[l], f"encoder.layer.{l}."
+                m = torch.nn.Module()
+                m.A = A
+                m.q = lin(pre + "attention.self.query", H, A * d)
+                m.k = lin(pre + "attention.self.key", H, A * d)
+                m.v = lin(pre + "attention.self.value", H, A * d)
+                m.o = lin(pre + "attention.output.dense", A * d, H)
+                m.f1 = lin(pre + "intermediate.dense", H, F)
+                m.f2 = lin(pre + "output.dense", F, H)
+                m.g1 = torch.from_numpy(weights[pre + "attention.output.LayerNorm.weight"].astype(np.float32))
+                m.b1 = torch.from_numpy(weights[pre + "attention.output.LayerNorm.bias"].astype(np.float32))
+                m.g2 = torch.from_numpy(weights[pre + "output.LayerNorm.weight"].astype(np.float32))
+                m.b2 = torch.from_numpy(weights[pre + "output.LayerNorm.bias"].astype(np.float32))
+                self.layers.append(m)
+            self.pool = lin("pooler.dense", H, H)
+            self.cls = lin("classifier", H, cfg.num_classes)
+            w = lambda k: torch.from_numpy(np.ascontiguousarray(weights[k], np.float32))
+            self.tok, self.pos, self.typ = w("embeddings.word_embeddings.weight"), \
+                w("embeddings.position_embeddings.weight"), w("embeddings.token_type_embeddings.weight")[0]
+            self.eg, self.eb = w("embeddings.LayerNorm.weight"), w("embeddings.LayerNorm.bias")
+
+        def forward(self, ids, mask):
+            B, S = ids.shape
+            x = Fn.layer_norm(self.tok[ids] + self.pos[:S] + self.typ, (H,), self.eg, self.eb, cfg.ln_eps)
+            bias = (1.0 - mask[:, None, None, :].float()) * -1e30
+            for m in self.layers:
+                sh = lambda t: t.view(B, S, m.A, d).transpose(1, 2)
+                p = torch.softmax(sh(m.q(x)) @ sh(m.k(x)).transpose(-1, -2) / d ** 0.5 + bias, -1)
+                ctx = (p @ sh(m.v(x))).transpose(1, 2).reshape(B, S, m.A * d)
+                x = Fn.layer_norm(x + m.o(ctx), (H,), m.g1, m.b1, cfg.ln_eps)
+                x = Fn.layer_norm(x + m.f2(Fn.gelu(m.f1(x))), (H,), m.g2, m.b2, cfg.ln_eps)
+            return self.cls(torch.tanh(self.pool(x[:, 0])))
+
+    model = torch.ao.quantization.quantize_dynamic(Enc().eval(), {torch.nn.Linear}, dtype=torch.qint8)
+    ti, tm = torch.from_numpy(ids.astype(np.int64)), torch.from_numpy(mask.astype(np.int64))
+    prev = torch.get_num_threads()
+    res = {}
+    try:
+        for label, nthr, bsz in (("all_cores", cores, 16), ("single_thread", 1, 1)):
+            torch.set_num_threads(nthr)
+            with torch.inference_mode():
+                model(ti[:bsz], tm[:bsz])
+                n, t0 = 0, time.perf_counter()
+                while time.perf_counter() - t0 < seconds / 2:
+                    model(ti[n % ti.shape[0]:n % ti.shape[0] + bsz], tm[n % ti.shape[0]:n % ti.shape[0] + bsz])
+                    n += bsz
+                res[label] = n / (time.perf_counter() - t0)
+    finally:
+        torch.set_num_threads(prev)
+    return {"value": res["all_cores"], "unit": "sequences/s", "threads": cores,
+            "single_thread": res["single_thread"],
+            "what": f"PyTorch quantize_dynamic (FBGEMM int8 linears, fp32 attention / LN / GELU) on the same "
+                    f"{cfg.name} shapes, batches of 16 on {cores} intra-op threads (and batch 1 on one thread); "
+                    f"context only, not the oracle"}
 
 
 def run_reference(args):
@@ -304,11 +412,20 @@ def run_reference(args):
     warm = min(args.warmup, 1)
     steps = max(1, min(args.steps, int(170.0 / max(t1, 1e-3)) - warm))
 
+    cpus = sorted(os.sched_getaffinity(0))
+
+    def pinned(i, j):  # one single-threaded instance per core
+        try:
+            os.sched_setaffinity(0, {cpus[i]})
+        except OSError:
+            pass
+        orc.encode(ids[j:j + 1], mask[j:j + 1])
+
     def one_step(k):
         ths = []
         for i in range(cores):
             j = (k * cores + i) % cfg.batch
-            ths.append(threading.Thread(target=orc.encode, args=(ids[j:j + 1], mask[j:j + 1])))
+            ths.append(threading.Thread(target=pinned, args=(i, j)))
         for t in ths:
             t.start()
         for t in ths:
