@@ -522,6 +522,13 @@ __global__ void __launch_bounds__(256) tensor_quant_kernel(const __half* __restr
     qp[0] = sc;
     qp[1] = zp;
   }
+  // x / sc as the correctly rounded quotient without a division per element
+  // (Markstein's correction with rs = RN(1 / sc), as q8_quant4 / div2_cr),
+  // RNE via the 1.5 * 2^23 magic add (|x / sc| <= 255): bit-identical to
+  // rintf(__fdiv_rn(x, sc)).
+  const float rs = __frcp_rn(sc);
+  const float2 rs2 = make_float2(rs, rs), nsc2 = make_float2(-sc, -sc);
+  const float2 kMagic = make_float2(12582912.0f, 12582912.0f);
   const int kc = K / 8;
   const size_t n = (size_t)M * kc;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
@@ -530,7 +537,14 @@ __global__ void __launch_bounds__(256) tensor_quant_kernel(const __half* __restr
     unpack8(__ldg(reinterpret_cast<const uint4*>(x + r * ldx + c * 8)), f);
     uint32_t b[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) b[j] = (uint32_t)fminf(fmaxf(rintf(__fdiv_rn(f[j], sc)) + zp, 0.0f), 255.0f);
+    for (int j = 0; j < 8; j += 2) {
+      const float2 xv = make_float2(f[j], f[j + 1]);
+      const float2 t = mul2(xv, rs2);
+      const float2 qv = fma2(fma2(t, nsc2, xv), rs2, t);
+      const float2 rn = sub2(add2(qv, kMagic), kMagic);  // RNE(q), exact for |q| < 2^22
+      b[j] = (uint32_t)fminf(fmaxf(rn.x + zp, 0.0f), 255.0f);
+      b[j + 1] = (uint32_t)fminf(fmaxf(rn.y + zp, 0.0f), 255.0f);
+    }
     *reinterpret_cast<uint2*>(q + r * ldq + c * 8) =
         make_uint2(b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24), b[4] | (b[5] << 8) | (b[6] << 16) | (b[7] << 24));
   }
