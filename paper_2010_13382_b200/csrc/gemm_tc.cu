@@ -117,10 +117,14 @@ __device__ __forceinline__ float gelu_expo(float s) {
   return s <= kGeluFast ? s * p7 : sc * p11;
 }
 
+// GELU(y) = y/2 (2 - e) for y >= 0, y/2 e for y < 0, written without a
+// select as 0.5 * fma(-|y|, e, y + |y|) (y + |y| is 2y or 0, exact; one
+// rounding for y >= 0, the same value as (0.5 y) e for y < 0).
 __device__ __forceinline__ float gelu_from_expo(float y, float a) {
   float e;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-a));
-  return (0.5f * y) * (y >= 0.0f ? 2.0f - e : e);
+  const float s = fabsf(y);
+  return 0.5f * __fmaf_rn(-s, e, y + s);
 }
 
 template <int ACT>
@@ -160,11 +164,9 @@ __device__ __forceinline__ void gelu16x2(float2 (&v)[16]) {
     float2 ex;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ex.x) : "f"(-a.x));
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ex.y) : "f"(-a.y));
-    // (a one-FMA tail fma(y / 2, +-e, y or 0) measured 20% slower in the
-    // fp16 FFN1 GEMM epilogue: more ALU-pipe selects / negations)
-    const float2 t = sub2(make_float2(2.0f, 2.0f), ex);
-    const float2 sel = make_float2(v[e].x >= 0.0f ? t.x : ex.x, v[e].y >= 0.0f ? t.y : ex.y);
-    v[e] = mul2(mul2(v[e], make_float2(0.5f, 0.5f)), sel);
+    // select-free tail (gelu_from_expo): 0.5 * fma(-s, e, y + s)
+    const float2 h = add2(v[e], s);
+    v[e] = mul2(fma2(make_float2(-s.x, -s.y), ex, h), make_float2(0.5f, 0.5f));
   }
 }
 

@@ -279,6 +279,20 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// 16-byte global store (row-contiguous epilogue output written from registers).
+__device__ __forceinline__ void st_global_v4(void* ptr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(ptr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+// Per-warpgroup register budgets (all 128 threads of the warpgroup execute
+// it): the light producer / MMA warpgroup hands registers to the epilogue.
+template <uint32_t N>
+__device__ __forceinline__ void regs_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N>
+__device__ __forceinline__ void regs_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
 // Bulk smem -> peer-smem copy (16B-aligned, size multiple of 16) that signals
 // its bytes on an mbarrier of the destination CTA.
 __device__ __forceinline__ void bulk_copy_s2c(uint32_t dst_cluster, const void* src, uint32_t bytes,
