@@ -947,17 +947,24 @@ __global__ void __launch_bounds__(kRRThreads, 1)
           for (int e = 0; e < 8; ++e)
             o[e] = q8_quant4(__half22float2(*reinterpret_cast<const __half2*>(&hv[2 * e])),
                              __half22float2(*reinterpret_cast<const __half2*>(&hv[2 * e + 1])), sc, rs);
-          // s8 block 32 rows x 32 B through the staging buffer (32B swizzle) + TMA store
-          if (lane == 0) bulk_wait_read<0>();
+          // s8 block 32 rows x 32 B (1 KB, 32B swizzle) + TMA store, double
+          // buffered in the two halves of the warp's staging buffer: chunk ch
+          // only waits for the store that last read its half (ch 0: for every
+          // earlier store, which may have used the whole buffer)
+          uint8_t* qbuf = stage_buf + (ch & 1) * 1024;
+          if (lane == 0) {
+            if (ch == 0) bulk_wait_read<0>();
+            else bulk_wait_read<1>();
+          }
           __syncwarp();
 #pragma unroll
           for (int cc = 0; cc < 2; ++cc)
-            *reinterpret_cast<uint4*>(stage_buf + lane * 32 + ((cc ^ ((lane >> 2) & 1)) << 4)) =
+            *reinterpret_cast<uint4*>(qbuf + lane * 32 + ((cc ^ ((lane >> 2) & 1)) << 4)) =
                 make_uint4(o[4 * cc], o[4 * cc + 1], o[4 * cc + 2], o[4 * cc + 3]);
           fence_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmQ, stage_buf, ncol0 + c_lo + ch * 32, row0);
+            tma_store_2d(&tmQ, qbuf, ncol0 + c_lo + ch * 32, row0);
             bulk_commit();
           }
           if (tr0 && ch < 2) gemm_trace(p.trace, lt, 12 + ch);
