@@ -726,17 +726,17 @@ __global__ void __launch_bounds__(kRRThreads, 1)
           slot[lane] = r0;
           if (stats) slot[32 + lane] = r1;
         } else {
-          float* mine = myp + ((b * 4 + q) * 2) * 32;
-          mine[lane] = r0;
-          if (stats) mine[32 + lane] = r1;
-          fence_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            // 4 quadrant copies of nv x 128 B from each of the CN CTAs
-            if (q == 0) mbar_expect_tx(&redbar[b], (uint32_t)(CN * 4 * nv * 128));
-            const uint32_t dst = smem_u32(red + (((b * kRRMaxCN + (int)rank) * 4 + q) * 2) * 32);
-            const uint32_t bl = smem_u32(&redbar[b]);
-            for (int c = 0; c < CN; ++c) bulk_copy_s2c(mapa_shared(dst, c), mine, nv * 128, mapa_shared(bl, c));
+          // every lane stores its row's partial into slot `rank` of every
+          // CTA of the cluster (st.async: remote smem stores counted on the
+          // destination's mbarrier; no trip through the bulk-copy engine,
+          // which queues behind the mainloop's operand loads)
+          if (lane == 0 && q == 0) mbar_expect_tx(&redbar[b], (uint32_t)(CN * 4 * nv * 128));
+          const uint32_t dst = smem_u32(red + (((b * kRRMaxCN + (int)rank) * 4 + q) * 2) * 32 + lane);
+          const uint32_t bl = smem_u32(&redbar[b]);
+          for (int c = 0; c < CN; ++c) {
+            const uint32_t rb = mapa_shared(bl, c), rd = mapa_shared(dst, c);
+            st_async_f32(rd, r0, rb);
+            if (stats) st_async_f32(rd + 128, r1, rb);
           }
         }
       }

@@ -21,6 +21,7 @@ for block in out.split('"File Path",')[1:]:
     h = rows[0]
     iss = h.index("Warp Stall Sampling (All Samples)")
     iex = h.index("Instructions Executed")
+    ist = [(i, c[6:]) for i, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]
     agg = {}
     cur = None
     for r in rows[1:]:
@@ -32,10 +33,14 @@ for block in out.split('"File Path",')[1:]:
             continue
         s = int(r[iss]) if r[iss].isdigit() else 0
         e = int(r[iex]) if r[iex].isdigit() else 0
-        a = agg.setdefault(cur, [0, 0])
+        a = agg.setdefault(cur, [0, 0, {}])
         a[0] += s
         a[1] += e
+        for i, c in ist:
+            if len(r) > i and r[i].isdigit():
+                a[2][c] = a[2].get(c, 0) + int(r[i])
     tot = sum(v[0] for v in agg.values()) or 1
     print(f"== {fname[:60]} {func[:100]} samples {tot}")
     for k, v in sorted(agg.items(), key=lambda kv: -kv[1][0])[:n]:
-        print(f"  {v[0] / tot:6.1%} {v[1]:>10d}  L{k[0]}: {k[1]}")
+        why = ",".join(f"{c}:{n}" for c, n in sorted(v[2].items(), key=lambda x: -x[1])[:3] if n)
+        print(f"  {v[0] / tot:6.1%} {v[1]:>10d}  L{k[0]}: {k[1][:60]:60s} {why}")
