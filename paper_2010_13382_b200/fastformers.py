@@ -15,7 +15,8 @@ from typing import Dict, Optional
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libfastformers.so")
+# FF_LIB_PATH: load another build of the library (A/B experiments, tools/ab_lib.py)
+LIB_PATH = os.environ.get("FF_LIB_PATH") or os.path.join(_PKG, "libfastformers.so")
 
 FF_OK, FF_E_INVALID, FF_E_SHAPE, FF_E_STATE, FF_E_CUDA, FF_E_INPUT, FF_E_UNSUPPORTED, FF_E_NOMEM = range(8)
 FF_F16, FF_I8 = 0, 1
