@@ -50,15 +50,16 @@ constexpr int kTileBytes = 128 * 128;  // 128 rows x 128 B (64 fp16)
 // own slot (S(n) has consumed them), so no separate P buffers are needed and a
 // 4th head fits in flight (192 KB of loads in flight per SM instead of 144 KB)
 constexpr int kKVStages = 4;
-constexpr int kSoftmaxWarps = 8;
+constexpr int kSoftmaxWarps = 16;  // 2 groups x 4 quadrants x 2 key halves
 constexpr int kThreadsTC = 64 + 32 * kSoftmaxWarps;
 constexpr uint32_t kTmemCtx = 256;  // packed ctx [256, 256 + 32 * heads)
 
 struct SmemTC {
   static constexpr int SLOT = 3 * kTileBytes;                // Q, K, V of one head (P(n) over Q, K)
   static constexpr int MASK = kKVStages * SLOT;              // [2][kKeys] floats (per group)
-  static constexpr int RED = MASK + 2 * kKeys * 4;           // [2][128] floats: per-group row amax
-  static constexpr int BAR = RED + 2 * kQ * 4;
+  static constexpr int RED = MASK + 2 * kKeys * 4;           // [2 G][2 half][128] floats: row amax partials
+  static constexpr int XCH = RED + 4 * kQ * 4;               // [2 max|sum][2 G][2 half][128] floats
+  static constexpr int BAR = XCH + 8 * kQ * 4;
   static constexpr int TOTAL = BAR + 256 + 1024;             // barriers + alignment slack
   static_assert(TOTAL <= 227 * 1024, "smem budget");
 };
@@ -129,7 +130,7 @@ struct HeadIter {
 // Buffers: Q/K/V x4 stages (smem; P(n) is written over head n's Q and K
 // tiles), S/O x2 (TMEM, one per group), parked int8 ctx [256, 512).
 template <int DP>
-__global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds a whole S row (a few spilled registers)
+__global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds half an S row
     attention_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const int32_t* __restrict__ mask, int B, int S,
                         int A, int d, int hs, int mh, int hm_rows, float scale, __half* __restrict__ ctx, int ldc,
                         int8_t* __restrict__ ctxq, int ldq, float* __restrict__ ctxs,
@@ -145,7 +146,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds a whole S ro
   uint64_t* t_free = o_full + 2;               // [2] group G (O read) -> MMA: columns free for S(n + 2)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_free + 2);
   float* sMask = reinterpret_cast<float*>(smem + SmemTC::MASK);  // [2][kKeys]: per group
-  float* sRed = reinterpret_cast<float*>(smem + SmemTC::RED);    // [2][kQ]: per-group row amax
+  float* sRed = reinterpret_cast<float*>(smem + SmemTC::RED);    // [2 G][2 half][kQ]: row amax partials
+  float* sXch = reinterpret_cast<float*>(smem + SmemTC::XCH);    // [max|sum][G][half][kQ]: half-row stats
 
   using HC = HeadCfg<DP>;
   using Iter = HeadIter;
@@ -155,7 +157,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds a whole S ro
   const int n_items = B * n_groups;
   const int it_first = (int)blockIdx.x;
   const int it_stride = (int)gridDim.x;
-  constexpr int kGroupThreads = 128;
+  constexpr int kGroupThreads = 256;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmQKV);
     for (int i = 0; i < kKVStages; ++i) {
@@ -271,16 +273,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds a whole S ro
     }
     if (n > 0) issue_pv(n - 1);
   } else {
-    const int G = (warp - 2) >> 2;  // ping-pong group: heads n with n & 1 == G
-    const int q = warp & 3;         // TMEM lane quadrant = rows [32 q, 32 q + 32)
+    const int G = (warp - 2) >> 3;        // ping-pong group: heads n with n & 1 == G
+    const int hf = ((warp - 2) >> 2) & 1;  // key half [64 hf, 64 hf + 64) of S, O columns half hf
+    const int q = warp & 3;               // TMEM lane quadrant = rows [32 q, 32 q + 32)
     const int r = q * 32 + lane;
-    const int gtid = threadIdx.x - 64 - kGroupThreads * G;  // 0..127 within the group
+    const int gtid = threadIdx.x - 64 - kGroupThreads * G;  // 0..255 within the group
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
     const uint32_t treg = trow + G * 128;  // this group's S / O columns
     float* gMask = sMask + G * kKeys;
     const bool fuse_q = ctxq != nullptr;
-    auto both_sync = []() { asm volatile("bar.sync 2, 256;" ::: "memory"); };  // both groups (item end)
-    auto group_sync = [G]() { asm volatile("bar.sync %0, 128;" ::"r"(3 + G) : "memory"); };
+    auto both_sync = []() { asm volatile("bar.sync 2, 512;" ::: "memory"); };  // both groups (item end)
+    auto group_sync = [G]() { asm volatile("bar.sync %0, 256;" ::"r"(3 + G) : "memory"); };
+    // the two half-row warps of (group, quadrant): row max / sum exchange
+    auto pair_sync = [G, q]() { asm volatile("bar.sync %0, 64;" ::"r"(5 + 4 * G + q) : "memory"); };
+    float* xmax = sXch + ((0 * 2 + G) * 2) * kQ;  // [half][kQ]
+    float* xsum = sXch + ((1 * 2 + G) * 2) * kQ;
     const float2 cd2 = make_float2(scale, scale);
     const float2 l2e = make_float2(1.4426950408889634f, 1.4426950408889634f);
     constexpr int HW = DP / 2;  // packed fp16 words of one head's row
@@ -294,28 +301,30 @@ __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds a whole S ro
     bool qpend = false;
     int qb = 0, qhbase = 0, qnh = 0;
     float qsc = 1.0f, qrs = 1.0f;
-    auto flush_head = [&](int j) {  // quantize + store parked head j of the pending item
-      uint32_t v[HW];
-      if constexpr (HW == 32) tmem_ld32(trow + kTmemCtx + j * HC::kPark, v);
-      else tmem_ld16(trow + kTmemCtx + j * HC::kPark, v);
+    constexpr int HH = HW / 2;       // packed words of this thread's half of a head row
+    const int c0 = hf * (DP / 2);    // first head column of this thread's half
+    auto flush_head = [&](int j) {  // quantize + store this thread's half of parked head j of the pending item
+      uint32_t v[HH];
+      if constexpr (HH == 16) tmem_ld16(trow + kTmemCtx + j * HC::kPark + hf * HH, v);
+      else tmem_ld8(trow + kTmemCtx + j * HC::kPark + hf * HH, v);
       tmem_wait_ld();
-      uint32_t w[HW / 2];
+      uint32_t w[HH / 2];
 #pragma unroll
-      for (int i = 0; i < HW / 2; ++i) {
+      for (int i = 0; i < HH / 2; ++i) {
         const float2 a0 = __half22float2(*reinterpret_cast<const __half2*>(&v[2 * i]));
         const float2 a1 = __half22float2(*reinterpret_cast<const __half2*>(&v[2 * i + 1]));
         w[i] = q8_quant4(a0, a1, qsc, qrs);
       }
       if (r < S) {
-        int8_t* row_q = ctxq + ((size_t)qb * S + r) * ldq + (qhbase + j) * d;
-        if (DP == 64 && d == 64) {  // the row's 64 s8 values: two 32-byte sectors
+        int8_t* row_q = ctxq + ((size_t)qb * S + r) * ldq + (qhbase + j) * d + c0;
+        if (DP == 64 && d == 64) {  // the half row's 32 s8 values: one 32-byte sector
           uint4* dst = reinterpret_cast<uint4*>(row_q);
 #pragma unroll
-          for (int c = 0; c < 4; ++c) dst[c] = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
-        } else {  // d even: 2-byte aligned pieces of the d valid values
+          for (int c = 0; c < 2; ++c) dst[c] = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+        } else {  // d even: 2-byte aligned pieces of the valid values
 #pragma unroll
-          for (int i = 0; i < HW; ++i)
-            if (2 * i < d) *reinterpret_cast<uint16_t*>(row_q + 2 * i) = (uint16_t)(w[i >> 1] >> ((i & 1) * 16));
+          for (int i = 0; i < HH; ++i)
+            if (c0 + 2 * i < d) *reinterpret_cast<uint16_t*>(row_q + 2 * i) = (uint16_t)(w[i >> 1] >> ((i & 1) * 16));
         }
       }
     };
@@ -338,29 +347,33 @@ __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds a whole S ro
         mbar_wait(s_full + G, k & 1);
         if (threadIdx.x == 64) trace_ev(trace, n, 3);
         tc_fence_after();
-        // the whole row of S in registers (4 loads, one wait): s = RN(raw *
-        // fp32(1/sqrt d)) + mask bias (0 / -inf) in one FFMA2 per pair (R10),
-        // the row max, e = exp2((s - max) log2 e) (R9) and the row sum in place
-        uint32_t v[128];
+        // half an S row in registers (keys [64 hf, 64 hf + 64); 2 loads, one
+        // wait): s = RN(raw * fp32(1/sqrt d)) + mask bias (0 / -inf) in one
+        // FFMA2 per pair (R10), the row max (the two halves combined through
+        // smem), e = exp2((s - max) log2 e) (R9) and the row sum in place
+        uint32_t v[64];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld32(treg + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
+        for (int c = 0; c < 2; ++c) tmem_ld32(treg + hf * 64 + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
         tmem_wait_ld();
         tc_fence_before();  // (S is read; the MMA overwrites these columns with O after p_full)
-        const float2* mk = reinterpret_cast<const float2*>(gMask);
+        const float2* mk = reinterpret_cast<const float2*>(gMask + hf * 64);
         float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-        for (int j = 0; j < 64; ++j) {
+        for (int j = 0; j < 32; ++j) {
           const float2 sv = fma2(make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1])), cd2, mk[j]);
           v[2 * j] = __float_as_uint(sv.x);
           v[2 * j + 1] = __float_as_uint(sv.y);
           m4[j & 1] = fmaxf(m4[j & 1], sv.x);
           m4[2 + (j & 1)] = fmaxf(m4[2 + (j & 1)], sv.y);
         }
-        const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+        float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+        xmax[hf * kQ + r] = mx;
+        pair_sync();
+        mx = fmaxf(mx, xmax[(hf ^ 1) * kQ + r]);
         const float2 mxv = make_float2(mx, mx);
         float2 la = make_float2(0.0f, 0.0f), lb = make_float2(0.0f, 0.0f);
 #pragma unroll
-        for (int j = 0; j < 64; ++j) {
+        for (int j = 0; j < 32; ++j) {
           const float2 t = mul2(sub2(make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1])), mxv), l2e);
           const float2 e = make_float2(ex2f(t.x), ex2f(t.y));
           if (j & 1) lb = add2(lb, e);
@@ -369,16 +382,20 @@ __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds a whole S ro
           v[2 * j + 1] = __float_as_uint(e.y);
         }
         const float2 l2 = add2(la, lb);
-        const float l = l2.x + l2.y;
+        const float lh = l2.x + l2.y;
+        xsum[hf * kQ + r] = lh;
+        pair_sync();
+        const float l = lh + xsum[(hf ^ 1) * kQ + r];  // half 0 + half 1 (commutative: same on both)
         const float rl = __frcp_rn(l);
         const float2 lv = make_float2(l, l), rlv = make_float2(rl, rl);
         // P16 = R16(e / l) (IEEE quotient, R9) into a K-major 128B-swizzled
         // P tile over this head's Q / K tiles: keys [32 c, 32 c + 32) = 16-byte chunks
         // 4 (c & 1) .. + 3 of k-block c >> 1, chunk cc of row r at (cc ^ (r & 7))
         // (over the Q and K tiles of this head's slot: S(n) has consumed them)
-        uint8_t* prow = smem + (n % kKVStages) * SmemTC::SLOT + r * 128;
+        // (this thread's half: keys [64 hf, +64) = k-block hf)
+        uint8_t* prow = smem + (n % kKVStages) * SmemTC::SLOT + r * 128 + hf * kTileBytes;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 2; ++c) {
 #pragma unroll
           for (int cc = 0; cc < 4; ++cc) {
             uint32_t w[4];
@@ -389,9 +406,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds a whole S ro
                   div2_cr(make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1])), lv, rlv);
               w[i] = pack_half2(pv.x, pv.y);
             }
-            const int pc = (c & 1) * 4 + cc;
-            *reinterpret_cast<uint4*>(prow + (c >> 1) * kTileBytes + ((pc ^ (r & 7)) << 4)) =
-                make_uint4(w[0], w[1], w[2], w[3]);
+            const int pc = c * 4 + cc;
+            *reinterpret_cast<uint4*>(prow + ((pc ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
           }
         }
         tc_fence_before();
@@ -402,39 +418,38 @@ __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds a whole S ro
         mbar_wait(o_full + G, k & 1);
         if (threadIdx.x == 64) trace_ev(trace, n, 6);
         tc_fence_after();
-        uint32_t o[DP];
-        if constexpr (DP == 64) {
-          tmem_ld32(treg, *reinterpret_cast<uint32_t(*)[32]>(o));
-          tmem_ld32(treg + 32, *reinterpret_cast<uint32_t(*)[32]>(o + 32));
-        } else {
-          tmem_ld32(treg, *reinterpret_cast<uint32_t(*)[32]>(o));
-        }
+        // this thread's half of O: columns [c0, c0 + DP / 2)
+        uint32_t o[DP / 2];
+        if constexpr (DP == 64) tmem_ld32(treg + c0, *reinterpret_cast<uint32_t(*)[32]>(o));
+        else tmem_ld16(treg + c0, *reinterpret_cast<uint32_t(*)[16]>(o));
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(t_free + G);
-        uint32_t pk[HW];
+        uint32_t pk[HH];
 #pragma unroll
-        for (int i = 0; i < HW; ++i) {
+        for (int i = 0; i < HH; ++i) {
           // O columns >= d (padded or neighbouring head columns): zero
-          pk[i] = 2 * i < d ? pack_half2(__uint_as_float(o[2 * i]), __uint_as_float(o[2 * i + 1])) : 0u;
+          pk[i] = c0 + 2 * i < d ? pack_half2(__uint_as_float(o[2 * i]), __uint_as_float(o[2 * i + 1])) : 0u;
           amax2 = __hmax2(amax2, __habs2(*reinterpret_cast<const __half2*>(&pk[i])));
         }
         if (ctx != nullptr && r < S) {
-          __half* row_c = ctx + ((size_t)it.b * S + r) * ldc + h * d;
+          __half* row_c = ctx + ((size_t)it.b * S + r) * ldc + h * d + c0;
           if (DP == 64 && d == 64) {
             uint4* dst = reinterpret_cast<uint4*>(row_c);
 #pragma unroll
-            for (int c = 0; c < 8; ++c) dst[c] = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+            for (int c = 0; c < 4; ++c) dst[c] = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
           } else {  // d even: 4-byte aligned pairs
 #pragma unroll
-            for (int i = 0; i < HW; ++i)
-              if (2 * i < d) *reinterpret_cast<uint32_t*>(row_c + 2 * i) = pk[i];
+            for (int i = 0; i < HH; ++i)
+              if (c0 + 2 * i < d) *reinterpret_cast<uint32_t*>(row_c + 2 * i) = pk[i];
           }
         }
         if (fuse_q) {
           if (qpend && it.hl < qnh) flush_head(it.hl);  // frees parking slot hl (its load completed)
-          if constexpr (HW == 32) tmem_st32(trow + kTmemCtx + it.hl * HC::kPark, *reinterpret_cast<uint32_t(*)[32]>(pk));
-          else tmem_st16(trow + kTmemCtx + it.hl * HC::kPark, *reinterpret_cast<uint32_t(*)[16]>(pk));
+          if constexpr (HH == 16)
+            tmem_st16(trow + kTmemCtx + it.hl * HC::kPark + hf * HH, *reinterpret_cast<uint32_t(*)[16]>(pk));
+          else
+            tmem_st8(trow + kTmemCtx + it.hl * HC::kPark + hf * HH, *reinterpret_cast<uint32_t(*)[8]>(pk));
           tmem_wait_st();
         }
         if (threadIdx.x == 64) trace_ev(trace, n, 7);
@@ -448,11 +463,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds a whole S ro
           for (int j = it.nh; j < qnh; ++j)
             if ((j & 1) == G) flush_head(j);
         }
-        sRed[G * kQ + r] = fmaxf(__low2float(amax2), __high2float(amax2));
+        sRed[(2 * G + hf) * kQ + r] = fmaxf(__low2float(amax2), __high2float(amax2));
         tc_fence_before();  // parked TMEM stores ordered before the other group's later reads
         both_sync();
         tc_fence_after();
-        const float am = fmaxf(sRed[r], sRed[kQ + r]);
+        const float am = fmaxf(fmaxf(sRed[r], sRed[kQ + r]), fmaxf(sRed[2 * kQ + r], sRed[3 * kQ + r]));
         both_sync();  // both groups read sRed before the next item's writes
         amax2 = __float2half2_rn(0.0f);
         qb = it.b;
@@ -461,7 +476,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds a whole S ro
         qpend = true;
         qsc = q8_scale(am);
         qrs = __frcp_rn(qsc);
-        if (G == 0 && r < S) ctxs[(size_t)it.b * S + r] = qsc;
+        if (G == 0 && hf == 0 && r < S) ctxs[(size_t)it.b * S + r] = qsc;
       }
     }
     if (fuse_q && qpend)
