@@ -331,6 +331,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds half an S ro
 
     uint32_t n = 0;
     int mask_item = -1;
+    // key mask words of the next item, loaded one item ahead (thread gtid < kKeys
+    // holds key gtid) so the load latency is not exposed at the item switch
+    auto load_mask = [&](int item) -> int {
+      if (gtid >= kKeys || gtid >= S || item >= n_items) return 0;
+      return __ldg(mask + (size_t)(item / n_groups) * S + gtid);
+    };
+    int mask_next = load_mask(it_first);
     for (Iter it(it_first, n_items, n_groups, A, it_stride, mh); it.valid(); it.next(), ++n) {
       const bool mine = (int)(n & 1) == G;
       const bool item_last = it.hl == it.nh - 1;
@@ -339,8 +346,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds half an S ro
         const int h = it.h0 + it.hl;
         if (it.item != mask_item) {  // key mask of the item's sequence (keys >= S masked)
           group_sync();              // every group thread finished reading the previous mask
-          for (int j = gtid; j < kKeys; j += kGroupThreads)
-            gMask[j] = (j < S && __ldg(mask + (size_t)it.b * S + j) != 0) ? 0.0f : -INFINITY;
+          if (gtid < kKeys) gMask[gtid] = (gtid < S && mask_next != 0) ? 0.0f : -INFINITY;
+          mask_next = load_mask(it.item + it_stride);
           group_sync();
           mask_item = it.item;
         }
