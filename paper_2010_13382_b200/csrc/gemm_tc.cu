@@ -926,17 +926,20 @@ __global__ void __launch_bounds__(kRRThreads, 1)
       if (tr0) gemm_trace(p.trace, lt, 10);
       if (p.outq) {
         tmem_wait_st();
+        // the parked values of chunk 0 are read while the row amax is exchanged
+        // (they do not depend on it); chunk ch + 1 is read during chunk ch
+        uint32_t hv[2][16];
+        tmem_ld16(tbase, hv[0]);
         // Q8row over the whole row (R6-R8, R12) from the fp16-rounded values
         float rmax, unused;
         exchange(fmaxf(__low2float(amax2), __high2float(amax2)), 0.0f, false, rmax, unused);
         if (tr0) gemm_trace(p.trace, lt, 11);
         const float sc = q8_scale(rmax);
         const float rs = __frcp_rn(sc);
-#pragma unroll 1
+#pragma unroll
         for (int ch = 0; ch < 4; ++ch) {
-          uint32_t hv[16];
-          tmem_ld16(tbase + ch * 16, hv);
           tmem_wait_ld();
+          if (ch < 3) tmem_ld16(tbase + (ch + 1) * 16, hv[(ch + 1) & 1]);
           if (ch == 3) {  // the group's accumulator buffer has been read for the last time
             tc_fence_before();
             __syncwarp();
@@ -945,8 +948,8 @@ __global__ void __launch_bounds__(kRRThreads, 1)
           uint32_t o[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e)
-            o[e] = q8_quant4(__half22float2(*reinterpret_cast<const __half2*>(&hv[2 * e])),
-                             __half22float2(*reinterpret_cast<const __half2*>(&hv[2 * e + 1])), sc, rs);
+            o[e] = q8_quant4(__half22float2(*reinterpret_cast<const __half2*>(&hv[ch & 1][2 * e])),
+                             __half22float2(*reinterpret_cast<const __half2*>(&hv[ch & 1][2 * e + 1])), sc, rs);
           // s8 block 32 rows x 32 B (1 KB, 32B swizzle) + TMA store, double
           // buffered in the two halves of the warp's staging buffer: chunk ch
           // only waits for the store that last read its half (ch 0: for every
