@@ -328,6 +328,27 @@ def test_graphs_host_path_and_repeatability():
     assert np.array_equal(a, a2) and np.array_equal(a, b) and np.array_equal(a, h)
 
 
+@pytest.mark.parametrize("name", ["c3_i8", "c2_i8", "c3_f16"])
+def test_full_size_forward_deterministic_under_repetition(name):
+    """Stress for the hand-rolled pipelines (mbarrier rings, cluster st.async
+    row exchanges, TMEM hand-offs, the attention's half-row max / sum
+    exchange): 30 back-to-back full-size forwards, with the L2 scrubbed in
+    between to vary timing, must all give the same logits bit for bit (a race
+    shows up as a run-to-run difference; compute-sanitizer is not available on
+    the GPU pool)."""
+    cfg = synth.config(name.split("_")[0]).with_dtype(1 if name.endswith("i8") else 0)
+    w = synth.make_weights(cfg)
+    ids, mask = synth.make_inputs(cfg, seed=11)
+    enc = Encoder(cfg, w)
+    ref = f32(enc.encode(dev(ids), dev(mask)))
+    junk = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    for k in range(30):
+        if k % 3 == 0:
+            junk.fill_(k)
+        got = f32(enc.encode(dev(ids), dev(mask)))
+        assert np.array_equal(got, ref), (k, float(np.abs(got - ref).max()))
+
+
 def test_input_errors_are_reported():
     cfg, w, ids, mask = build_case("c1_i8")
     enc = Encoder(cfg, w)
