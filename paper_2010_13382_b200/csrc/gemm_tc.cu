@@ -544,6 +544,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 //             rows + scale (the FFN-intermediate requant)
 // ========================================================================
 constexpr int kRRStages = 3;
+#ifndef FF_RR_SLEEP_NS
+#define FF_RR_SLEEP_NS 128
+#endif
+constexpr uint32_t kRRSleepNs = FF_RR_SLEEP_NS;  // epilogue group's probe interval while its accumulator is computed
 constexpr int kRRBN = 256;
 constexpr int kRRMaxCN = 8;
 constexpr int kRRGroupWarps = kRREpiWarps / 2;  // 8 warps per ping-pong group
@@ -812,7 +816,7 @@ __global__ void __launch_bounds__(kRRThreads, 1)
           tma_load_2d(stage_buf, &tmR, &resbar[ew], ncol0 + c_lo, row0, kEvictFirst);
         }
       }
-      mbar_wait(&tfull[acc], acc_phase);
+      mbar_wait_sleep(&tfull[acc], acc_phase, kRRSleepNs);
       if (tr0) gemm_trace(p.trace, lt, 3);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c_lo;
