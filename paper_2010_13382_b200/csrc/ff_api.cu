@@ -133,14 +133,16 @@ namespace {
 
 // Fusions of one layer: an explicit FF_OPT_FUSED_MASK as given; auto (-1,
 // the default) fuses the FFN1 requant always and residual + LN into a GEMM
-// whose K row is at most 2 KB -- with longer K rows the single-CTA 128-row
+// whose K row is at most 3 KB -- with longer K rows the single-CTA 128-row
 // tiles of the row-reduction kernel feed the tensor cores worse than the
-// CTA-pair GEMM + add_ln (measured: C4 fp16 FFN2 K = 3072 fused 337 us vs 220 +
-// 59 us; C3 int8 FFN2 K = 1536 B fused 67 us vs 41 + 35 us).
+// CTA-pair GEMM + add_ln (measured, whole step: C3 fp16 FFN2 3 KB rows fused
+// +1.9%, C4 int8 FFN2 3 KB +1.7%, C5 int8 FFN2 4 KB -0.3%, C5 fp16 8 KB -1.1%,
+// C4 fp16 FFN2 6 KB fused 337 us vs 220 + 59 us).
+constexpr int kFuseMaxKRowBytes = 3072;
 int fused_mask(const ff_model* m, const LayerPlan& P) {
   if (m->fused >= 0) return m->fused;
   const int eb = P.dt == FF_I8 ? 1 : 2;
-  return 2 | (P.K[1] * eb <= 2048 ? 1 : 0) | (P.K[3] * eb <= 2048 ? 4 : 0);
+  return 2 | (P.K[1] * eb <= kFuseMaxKRowBytes ? 1 : 0) | (P.K[3] * eb <= kFuseMaxKRowBytes ? 4 : 0);
 }
 
 void drop_graphs(ff_model* m) {

@@ -60,6 +60,12 @@ ok = (v >= 0).all(axis=2)
 def med(a, b):
     x = (v[:, :, b] - v[:, :, a]); x = x[(v[:, :, a] >= 0) & (v[:, :, b] >= 0)]
     return np.median(x), np.percentile(x, 90)
+import os as _os
+if _os.environ.get("ATT_SUB"):
+    for name, a, b in [("S seen -> S in regs 3->0", 3, 0), ("mask/max + pair 0->1", 0, 1), ("exp/sum + pair 1->2", 1, 2),
+                       ("normalize + P store 2->4", 2, 4)]:
+        m, p9 = med(a, b)
+        print(f"{name:28s} median {m:7.3f} us  p90 {p9:7.3f}")
 for name, a, b in [("load latency 0->1", 0, 1), ("S wait 1->2", 1, 2), ("S ready->seen 2->3", 2, 3),
                    ("softmax 3->4", 3, 4), ("P->MMA seen 4->5", 4, 5), ("P->O seen 4->6", 4, 6),
                    ("epilogue 6->7", 6, 7)]:
