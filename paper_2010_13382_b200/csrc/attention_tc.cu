@@ -102,8 +102,12 @@ struct HeadIter {
   }
   __device__ void set() {
     if (item < n_items) {
-      b = item / n_groups;
-      h0 = (item - b * n_groups) * mh;
+      // items are walked from the last sequence to the first: the QKV GEMM
+      // writes its row tiles in increasing order, so the most recently
+      // written (most likely still L2-resident) sequences are read first
+      const int rev = n_items - 1 - item;
+      b = rev / n_groups;
+      h0 = (rev - b * n_groups) * mh;
       nh = min(A, h0 + mh) - h0;
     }
   }
@@ -335,7 +339,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds half an S ro
     // holds key gtid) so the load latency is not exposed at the item switch
     auto load_mask = [&](int item) -> int {
       if (gtid >= kKeys || gtid >= S || item >= n_items) return 0;
-      return __ldg(mask + (size_t)(item / n_groups) * S + gtid);
+      return __ldg(mask + (size_t)((n_items - 1 - item) / n_groups) * S + gtid);
     };
     int mask_next = load_mask(it_first);
     for (Iter it(it_first, n_items, n_groups, A, it_stride, mh); it.valid(); it.next(), ++n) {
