@@ -95,19 +95,18 @@ __device__ __forceinline__ void trace_ev(unsigned long long* trace, uint32_t n, 
 // each item = (sequence b, heads [h0, h0 + nh)).
 struct HeadIter {
   int item, hl, b, h0, nh;
-  int n_items, n_groups, A, stride, mh;
-  __device__ HeadIter(int first, int n_items_, int n_groups_, int A_, int stride_, int mh_)
-      : item(first), hl(0), n_items(n_items_), n_groups(n_groups_), A(A_), stride(stride_), mh(mh_) {
+  int n_items, n_groups, A, stride, mh, rev;
+  __device__ HeadIter(int first, int n_items_, int n_groups_, int A_, int stride_, int mh_, int rev_)
+      : item(first), hl(0), n_items(n_items_), n_groups(n_groups_), A(A_), stride(stride_), mh(mh_), rev(rev_) {
     set();
   }
   __device__ void set() {
     if (item < n_items) {
-      // items are walked from the last sequence to the first: the QKV GEMM
-      // writes its row tiles in increasing order, so the most recently
-      // written (most likely still L2-resident) sequences are read first
-      const int rev = n_items - 1 - item;
-      b = rev / n_groups;
-      h0 = (rev - b * n_groups) * mh;
+      // rev: items walked from the last sequence to the first, so that the
+      // rows the QKV GEMM wrote last (most likely still in L2) are read first
+      const int ri = rev ? n_items - 1 - item : item;
+      b = ri / n_groups;
+      h0 = (ri - b * n_groups) * mh;
       nh = min(A, h0 + mh) - h0;
     }
   }
@@ -138,7 +137,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds half an S ro
     attention_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const int32_t* __restrict__ mask, int B, int S,
                         int A, int d, int hs, int mh, int hm_rows, float scale, __half* __restrict__ ctx, int ldc,
                         int8_t* __restrict__ ctxq, int ldq, float* __restrict__ ctxs,
-                        const uint8_t* __restrict__ qkv_rows, int row_bytes, unsigned long long* __restrict__ trace) {
+                        const uint8_t* __restrict__ qkv_rows, int row_bytes, unsigned long long* __restrict__ trace,
+                        int rev) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SmemTC::BAR);
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds half an S ro
       (void)qkv_rows;
       (void)row_bytes;
       uint32_t n = 0;
-      for (Iter it(it_first, n_items, n_groups, A, it_stride, mh); it.valid(); it.next(), ++n) {
+      for (Iter it(it_first, n_items, n_groups, A, it_stride, mh, rev); it.valid(); it.next(), ++n) {
         const int slot = n % kKVStages;
         const int h = it.h0 + it.hl;
         uint8_t* base = smem + slot * SmemTC::SLOT;
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds half an S ro
       __syncwarp();
     };
     uint32_t n = 0;
-    for (Iter it(it_first, n_items, n_groups, A, it_stride, mh); it.valid(); it.next(), ++n) {
+    for (Iter it(it_first, n_items, n_groups, A, it_stride, mh, rev); it.valid(); it.next(), ++n) {
       const int slot = n % kKVStages;
       const int g = n & 1;
       uint8_t* base = smem + slot * SmemTC::SLOT;
@@ -339,10 +339,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)  // a thread holds half an S ro
     // holds key gtid) so the load latency is not exposed at the item switch
     auto load_mask = [&](int item) -> int {
       if (gtid >= kKeys || gtid >= S || item >= n_items) return 0;
-      return __ldg(mask + (size_t)((n_items - 1 - item) / n_groups) * S + gtid);
+      return __ldg(mask + (size_t)((rev ? n_items - 1 - item : item) / n_groups) * S + gtid);
     };
     int mask_next = load_mask(it_first);
-    for (Iter it(it_first, n_items, n_groups, A, it_stride, mh); it.valid(); it.next(), ++n) {
+    for (Iter it(it_first, n_items, n_groups, A, it_stride, mh, rev); it.valid(); it.next(), ++n) {
       const bool mine = (int)(n & 1) == G;
       const bool item_last = it.hl == it.nh - 1;
       if (mine) {
@@ -560,7 +560,7 @@ static int heads_per_item(int B, int A, int max_heads, bool fused) {
 
 cudaError_t launch_attention_tc(const AttnTCPlan& plan, const int32_t* mask, int B, int S, int A, int d, int hs,
                                 __half* ctx, int ldctx, int8_t* ctxq, int ldq, float* ctxs, cudaStream_t s,
-                                unsigned long long* trace) {
+                                unsigned long long* trace, int rev) {
   if (ctxq != nullptr && !attention_tc_fuses_quant(A, d)) return cudaErrorInvalidValue;
   const float scale = (float)(1.0 / sqrt((double)d));  // fp32(1/sqrt(d)) (R10)
   const int max_heads = d <= 32 ? HeadCfg<32>::kMaxHeads : HeadCfg<64>::kMaxHeads;
@@ -570,11 +570,11 @@ cudaError_t launch_attention_tc(const AttnTCPlan& plan, const int32_t* mask, int
   if (d <= 32)
     launch_ex(attention_tc_kernel<32>, dim3(grid), dim3(kThreadsTC), SmemTC::TOTAL, s, 0, plan.map, mask, B, S, A, d,
               hs, mh, plan.hm_rows, scale, ctx, ldctx, ctxq, ldq, ctxs, static_cast<const uint8_t*>(plan.qkv),
-              plan.ldqkv * 2, trace);
+              plan.ldqkv * 2, trace, rev);
   else
     launch_ex(attention_tc_kernel<64>, dim3(grid), dim3(kThreadsTC), SmemTC::TOTAL, s, 0, plan.map, mask, B, S, A, d,
               hs, mh, plan.hm_rows, scale, ctx, ldctx, ctxq, ldq, ctxs, static_cast<const uint8_t*>(plan.qkv),
-              plan.ldqkv * 2, trace);
+              plan.ldqkv * 2, trace, rev);
   return cudaGetLastError();
 }
 

@@ -88,6 +88,10 @@ struct GemmParams {
   // to row (n / 64) * hm_rows + m, column n % 64 of a [heads * hm_rows, 64]
   // buffer, so every (section, head) slice is one contiguous block; 0 = row-major
   int hm_rows;
+  // 1: walk the row tiles from the last to the first (the launch order
+  // alternates so a kernel first reads the rows its producer wrote last,
+  // i.e. the ones most likely still in L2)
+  int rev;
 };
 
 struct GemmPlan {
@@ -146,6 +150,7 @@ struct RRParams {
   int ldq;
   float* out_scale;        // [M] or null
   unsigned long long* trace;  // debug timeline (ff_debug_set_trace), null in production
+  int rev;                    // 1: row tiles walked last to first (see GemmParams::rev)
 };
 struct RRPlan {
   CUtensorMap tmA, tmB, tmC;
@@ -217,7 +222,7 @@ bool plan_attention_tc_hm(AttnTCPlan* plan, const void* qkv, int n_blocks, int h
 cudaError_t launch_attention_tc(const AttnTCPlan& plan, const int32_t* mask, int B, int S, int A, int d, int hs,
                                 __half* ctx,
                                 int ldctx, int8_t* ctxq, int ldq, float* ctxs, cudaStream_t s,
-                                unsigned long long* trace = nullptr);
+                                unsigned long long* trace = nullptr, int rev = 1);
 cudaError_t prepare_attention_tc_kernel();
 
 // tcgen05 attention for 128 < S <= 512, head_dim 64 (attention_long.cu): fp16

@@ -295,7 +295,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int lt = 0;
       for (int tile = unit; tile < num_tiles; tile += nunits, ++lt) {
-        const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+        const int mt0 = tile / p.n_tiles, nt = tile - mt0 * p.n_tiles;
+        const int mt = p.rev ? p.m_tiles - 1 - mt0 : mt0;
         const int arow = mt * TM + (int)rank * BM;
         const int brow = nt * BN + (PAIR ? (int)rank * (BN / 2) : 0);
         for (int kb = 0; kb < p.k_blocks; ++kb) {
@@ -384,7 +385,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* sPar = reinterpret_cast<float*>(smem + Cfg::PAR_OFF);
     const int et = ew * 32 + lane;  // 0 .. 511
     for (int tile = unit; tile < num_tiles; tile += nunits, ++lt) {
-      const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+      const int mt0 = tile / p.n_tiles, nt = tile - mt0 * p.n_tiles;
+        const int mt = p.rev ? p.m_tiles - 1 - mt0 : mt0;
       const int nb = nt * BN;  // first output column of this tile
       constexpr int wcols = WCOLS;
       const int c_lo = (ew >> 2) * wcols;  // this warp's column group of the tile
@@ -628,7 +630,7 @@ __global__ void __launch_bounds__(kRRThreads, 1)
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], RRCfg::STAGE_BYTES);
-          tma_load_2d(sA + stage * RRCfg::A_BYTES, &tmA, &full[stage], kb * KE, mt * BM, kEvictNormal);
+          tma_load_2d(sA + stage * RRCfg::A_BYTES, &tmA, &full[stage], kb * KE, (p.rev ? p.m_tiles - 1 - mt : mt) * BM, kEvictNormal);
           tma_load_2d(sB + stage * RRCfg::B_BYTES, &tmB, &full[stage], kb * KE, (int)rank * BN, kEvictLast);
           if (++stage == STAGES) {
             stage = 0;
@@ -791,7 +793,7 @@ __global__ void __launch_bounds__(kRRThreads, 1)
     const bool tr0 = ew == 0 && lane == 0;
     int lt = G;
     for (int mt = unit + G * nunits; mt < p.m_tiles; mt += 2 * nunits, lt += 2) {
-      const int row0 = mt * BM + q * 32;
+      const int row0 = (p.rev ? p.m_tiles - 1 - mt : mt) * BM + q * 32;
       const int row = row0 + lane;
       const bool row_ok = row < p.M;
       const float sx = (I8 && row_ok) ? p.row_scale[row] : 0.0f;
@@ -799,8 +801,8 @@ __global__ void __launch_bounds__(kRRThreads, 1)
       if (MODE == RR_LN) {
         // residual of this group's NEXT tile -> L2 (its TMA loads then hit
         // L2, not HBM): this thread's 256 bytes of its row
-        const int nrow = row + 2 * nunits * BM;
-        if (nrow < p.M) {
+        const int nrow = p.rev ? row - 2 * nunits * BM : row + 2 * nunits * BM;
+        if (nrow >= 0 && nrow < p.M) {
           prefetch_l2(p.residual + (size_t)nrow * p.ldr + ncol0 + c_lo);
           prefetch_l2(p.residual + (size_t)nrow * p.ldr + ncol0 + c_lo + 64);
         }
@@ -1081,6 +1083,7 @@ bool plan_gemm(GemmPlan* g, bool i8, const void* A, int M_rows, int lda, const v
   g->p.tensor_qp = nullptr;
   g->p.colsum = nullptr;
   g->p.hm_rows = 0;
+  g->p.rev = 0;
   plan_gemm_set_m(g, M_rows);
   return true;
 }
@@ -1102,6 +1105,7 @@ bool plan_gemm_output(GemmPlan* g, void* out, int ldo, const char** err) {
   g->p.out = out;
   g->p.ldo = ldo;
   g->p.hm_rows = 0;
+  g->p.rev = 0;
   g->has_out_map = true;
   return encode_2d(&g->tmC, out, g->M_rows, g->p.N, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (size_t)ldo * 2, kEpiCols,
                    32, CU_TENSOR_MAP_SWIZZLE_64B, err);
