@@ -409,7 +409,8 @@ def run_reference(args):
     t0 = time.perf_counter()
     orc.encode(ids[:1], mask[:1])
     t1 = time.perf_counter() - t0
-    warm = min(args.warmup, 1)
+    # the requested warm-up steps (each one bounded sample, like a timed step)
+    warm = max(args.warmup, 0)
     steps = max(1, min(args.steps, int(170.0 / max(t1, 1e-3)) - warm))
 
     cpus = sorted(os.sched_getaffinity(0))
