@@ -844,6 +844,21 @@ def run_ours(args):
             variants["int8_per_tensor_u8"] = {"value": B / (mspt / 1e3), "unit": "sequences/s", "ms_per_step": mspt,
                                               "what": "per-tensor u8 activations + zero point (P:104, DESIGN R22)"}
             del encpt
+        # FF_OPT_CLS_LAST_LAYER (opt-in serving option): the last layer's
+        # row-local steps on the first-token rows only; bit-identical logits
+        enccl = Encoder(cfg, w, max_tokens=B * S, device=local, cls_last=True, **enc_kw)
+        ref_l = torch.empty_like(logits)
+        enc.encode(dids[0], dmask[0], ref_l)
+        enccl.encode(dids[0], dmask[0], logits)
+        torch.cuda.synchronize()
+        assert torch.equal(ref_l, logits), "FF_OPT_CLS_LAST_LAYER logits differ"
+        mscl = time_forward(enccl, dids, dmask, logits, stream, flush, 50)
+        variants["cls_last_layer"] = {
+            "value": B / (mscl / 1e3), "unit": "sequences/s", "ms_per_step": mscl,
+            "what": "FF_OPT_CLS_LAST_LAYER: the last layer's out-proj / LN / FFN on the B first-token rows the "
+                    "classifier reads (QKV and attention on every token); logits bit-identical to the headline "
+                    "path (checked here and in tests); opt-in, not the headline"}
+        del enccl
         torch.cuda.empty_cache()
         if not args.no_configs:
             cv = {}

@@ -186,7 +186,7 @@ FF_API ff_status ff_check(ff_model *m, void *stream);
  * 0 or 7): bit 0 out-proj + residual + LN1, bit 1 FFN1 + activation + requant
  * (int8 layers), bit 2 FFN2 + residual + LN2.  Value 0..7, or -1 = auto (the
  * default): FFN1 + requant always, and each LN fusion where the GEMM's K row
- * is at most 2 KB (with longer rows the row-reduction kernel's single-CTA
+ * is at most 3 KB (with longer rows the row-reduction kernel's single-CTA
  * tiles lose to the CTA-pair GEMM + add_ln).  The LN fusions combine
  * the LN statistics across the cluster in another order than add_ln, so their
  * logits agree with the unfused path within the DESIGN §3 bounds, not bit for
@@ -196,6 +196,17 @@ FF_API ff_status ff_check(ff_model *m, void *stream);
  * (FF_OPT_FUSED_MASK bits 0 / 2) also launch with PDL; default 0 (with PDL
  * they slowed the step by 5-10%). */
 #define FF_OPT_PDL_RR 9
+/* FF_OPT_CLS_LAST_LAYER (per model, default 0): the pooler reads only the first
+ * token of each sequence (a11; "pooler = tanh of first-token
+ * projection") and every step of a layer after the attention (out-projection,
+ * residual + LN1, FFN, residual + LN2, the per-row requants) is row-local, so
+ * with 1 the LAST layer runs those steps on the B first-token rows only (its
+ * QKV projection and attention still see every token).  The logits are
+ * bit-identical to the default path (tests/test_gpu_model.py); hidden states of
+ * the last layer other than the first tokens are not computed (ff_encode_trace
+ * of the last layer disables it).  Off by default: the bench's headline runs
+ * every row of every layer; this is reported as a variant. */
+#define FF_OPT_CLS_LAST_LAYER 13
 /* Set `option` to `value` on model m (invalidates its captured graphs).  Every
  * option is per model: the library holds no process-wide mutable state on the
  * launch path, so models may be driven from different host threads (one

@@ -111,6 +111,7 @@ struct ff_model {
   int fused = -1;  // FF_OPT_FUSED_EPILOGUES / _MASK: cluster row-reduction GEMM epilogues,
                   // bit 0 out-proj + LN1, bit 1 FFN1 + requant, bit 2 FFN2 + LN2; -1 = auto
   int act_quant = 0;    // FF_OPT_ACT_QUANT: 0 per-row s8, 1 per-tensor u8 + zero point
+  bool cls_last = false;  // FF_OPT_CLS_LAST_LAYER: last layer's row-local steps on the B first-token rows only
   ff::LaunchPolicy launch{true, false};  // FF_OPT_PDL / FF_OPT_PDL_RR of this model's forwards
   ff::AttnTCPlan tm_qkv;  // QKV buffer map for the tcgen05 attention
   // CUDA-graph cache of ff_encode, keyed by (batch, seq, ids, mask, logits);
@@ -484,6 +485,15 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     // a4 + a5: requant (int8 layers) and out-projection
     if (q && !att_q && !pt)
       FF_LAUNCH(FF_K_QUANT, ff::launch_quant_rows(CTX, m->ldc16, M, P.D, CTXq, m->ldc8, CTXs, s), "quant ctx");
+    // FF_OPT_CLS_LAST_LAYER: the classifier reads only the first token of each
+    // sequence (a11), and a5-a10 are row-local, so in the last layer they run
+    // on the B rows b*S (read with an S-row pitch) and write compact rows
+    // [0, B); the logits are bit-identical (tests/test_gpu_model.py)
+    const bool cls = m->cls_last && l + 1 == c.num_layers && !pt && !tr;
+    const int Mr = cls ? B : M;
+    const char* rerr = nullptr;
+    const int lda_o = q ? m->ldc8 : m->ldc16;
+    const void* A_o = q ? static_cast<const void*>(CTXq) : static_cast<const void*>(CTX);
     const int fm = fused_mask(m, P);
     const bool fuse_ln = (fm & 1) && !pt && P.rr_ok[0];
     const bool fuse_q = (fm & 2) && !pt && q && P.rr_ok[1];
@@ -491,12 +501,17 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     if (fuse_ln) {
       // a5 + a6 fused: H1 = LN1(R16(O) + X16) (+ s8 rows) in the out-proj epilogue
       ff::RRPlan r = P.rp[0];
-      ff::plan_rr_set_m(&r, M);
+      if (cls) {
+        if (!ff::rebind_rr_rows(&r, A_o, lda_o * S, X16, m->ldx16 * S, B, &rerr))
+          return fail(FF_E_CUDA, std::string("rr tensor map: ") + rerr);
+        r.p.rs_stride = S;
+      }
+      ff::plan_rr_set_m(&r, Mr);
       r.p.bias = m->w<float>(P.bias[W_O]);
       r.p.row_scale = q ? CTXs : nullptr;
       r.p.col_scale = q ? m->w<float>(P.sw[W_O]) : nullptr;
       r.p.residual = X16;
-      r.p.ldr = m->ldx16;
+      r.p.ldr = cls ? m->ldx16 * S : m->ldx16;
       r.p.gamma = m->w<float>(P.ln1g);
       r.p.beta = m->w<float>(P.ln1b);
       r.p.eps = c.ln_eps;
@@ -510,7 +525,11 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     } else {
     g = P.gp[W_O];
     g.force_pair = m->pair_mode;
-    ff::plan_gemm_set_m(&g, M);
+    if (cls) {
+      if (!ff::rebind_gemm_rows(&g, A_o, lda_o * S, B, &rerr)) return fail(FF_E_CUDA, std::string("tensor map: ") + rerr);
+      g.p.rs_stride = S;
+    }
+    ff::plan_gemm_set_m(&g, Mr);
     g.p.out = O16;
     g.p.ldo = m->ldx16;
     g.p.bias = m->w<float>(P.bias[W_O]);
@@ -522,7 +541,7 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     FF_LAUNCH(q ? FF_K_GEMM_I8 : FF_K_GEMM_F16, ff::launch_gemm(g, s), "gemm o");
     if (tr && dump(d_dump[3], O16, m->ldx16, H, M, s) != FF_OK) return FF_E_CUDA;
     // a6: residual + LN1 (+ s8 rows for FFN1)
-    FF_LAUNCH(FF_K_ADD_LN, ff::launch_add_ln(O16, m->ldx16, X16, m->ldx16, M, H, m->w<float>(P.ln1g), m->w<float>(P.ln1b),
+    FF_LAUNCH(FF_K_ADD_LN, ff::launch_add_ln(O16, m->ldx16, X16, cls ? m->ldx16 * S : m->ldx16, Mr, H, m->w<float>(P.ln1g), m->w<float>(P.ln1b),
                                 c.ln_eps, H1, m->ldx16, (q && !pt) ? H1q : nullptr, m->ldx8,
                                 (q && !pt) ? H1s : nullptr, s),
               "add_ln1");
@@ -535,7 +554,7 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
       // a7 + a8 fused: Iq, Is = Q8row(R16(act(FFN1))) in the FFN1 epilogue; the
       // fp16 copy of I is only materialised when a trace asks for it
       ff::RRPlan r = P.rp[1];
-      ff::plan_rr_set_m(&r, M);
+      ff::plan_rr_set_m(&r, Mr);
       r.p.bias = m->w<float>(P.bias[W_FFN1]);
       r.p.row_scale = H1s;
       r.p.col_scale = m->w<float>(P.sw[W_FFN1]);
@@ -551,7 +570,7 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     } else {
     g = P.gp[W_FFN1];
     g.force_pair = m->pair_mode;
-    ff::plan_gemm_set_m(&g, M);
+    ff::plan_gemm_set_m(&g, Mr);
     g.p.out = I16;
     g.p.ldo = m->ldi16;
     g.p.bias = m->w<float>(P.bias[W_FFN1]);
@@ -563,7 +582,7 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     FF_LAUNCH(q ? FF_K_GEMM_I8 : FF_K_GEMM_F16, ff::launch_gemm(g, s), "gemm ffn1");
     if (tr && dump(d_dump[5], I16, m->ldi16, P.F, M, s) != FF_OK) return FF_E_CUDA;
     // a8 + a9: requant and FFN2
-    if (q && !pt) FF_LAUNCH(FF_K_QUANT, ff::launch_quant_rows(I16, m->ldi16, M, P.F, Iq, m->ldi8, Is, s), "quant ffn");
+    if (q && !pt) FF_LAUNCH(FF_K_QUANT, ff::launch_quant_rows(I16, m->ldi16, Mr, P.F, Iq, m->ldi8, Is, s), "quant ffn");
     }
     role = (role + 1) % 5;
     rdir = (rmask >> (4 - role)) & 1;
@@ -571,7 +590,7 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     if (fuse_ln2) {
       // a9 + a10 fused: X16 = LN2(R16(Y) + H1) (+ s8 rows for the next int8 layer)
       ff::RRPlan r = P.rp[2];
-      ff::plan_rr_set_m(&r, M);
+      ff::plan_rr_set_m(&r, Mr);
       r.p.bias = m->w<float>(P.bias[W_FFN2]);
       r.p.row_scale = q ? Is : nullptr;
       r.p.col_scale = q ? m->w<float>(P.sw[W_FFN2]) : nullptr;
@@ -590,7 +609,7 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     } else {
     g = P.gp[W_FFN2];
     g.force_pair = m->pair_mode;
-    ff::plan_gemm_set_m(&g, M);
+    ff::plan_gemm_set_m(&g, Mr);
     g.p.out = O16;
     g.p.ldo = m->ldx16;
     g.p.bias = m->w<float>(P.bias[W_FFN2]);
@@ -602,7 +621,7 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     FF_LAUNCH(q ? FF_K_GEMM_I8 : FF_K_GEMM_F16, ff::launch_gemm(g, s), "gemm ffn2");
     if (tr && dump(d_dump[6], O16, m->ldx16, H, M, s) != FF_OK) return FF_E_CUDA;
     // a10: residual + LN2 (+ s8 rows when the next layer is int8)
-    FF_LAUNCH(FF_K_ADD_LN, ff::launch_add_ln(O16, m->ldx16, H1, m->ldx16, M, H, m->w<float>(P.ln2g), m->w<float>(P.ln2b),
+    FF_LAUNCH(FF_K_ADD_LN, ff::launch_add_ln(O16, m->ldx16, H1, m->ldx16, Mr, H, m->w<float>(P.ln2g), m->w<float>(P.ln2b),
                                 c.ln_eps, X16, m->ldx16, nq ? Xq : nullptr, m->ldx8, nq ? Xs : nullptr, s),
               "add_ln2");
     }
@@ -611,8 +630,10 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
     if (tr && dump(d_dump[7], X16, m->ldx16, H, M, s) != FF_OK) return FF_E_CUDA;
   }
   // a11: pooler + classifier
+  // (with FF_OPT_CLS_LAST_LAYER the first-token rows are compact rows [0, B))
+  const bool cls_out = m->cls_last && !pt && trace_layer != c.num_layers - 1;
   FF_LAUNCH(FF_K_HEAD, ff::launch_head(X16, m->ldx16, B, S, H, c.num_classes, m->w<float>(m->pool_w), m->w<float>(m->pool_b),
-                            m->w<float>(m->cls_w), m->w<float>(m->cls_b), m->ws<float>(m->ws_pooled), logits, s),
+                            m->w<float>(m->cls_w), m->w<float>(m->cls_b), m->ws<float>(m->ws_pooled), logits, s, cls_out ? 1 : S),
             "head");
   return FF_OK;
 }
@@ -1031,6 +1052,11 @@ ff_status ff_set_option(ff_model* m, int32_t option, int64_t value) {
     drop_graphs(m);  // captured launch configs change
     return FF_OK;
   }
+  if (option == FF_OPT_CLS_LAST_LAYER) {
+    m->cls_last = value != 0;
+    drop_graphs(m);
+    return FF_OK;
+  }
   return fail(FF_E_INVALID, "unknown option");
 }
 
@@ -1045,6 +1071,7 @@ ff_status ff_get_option(const ff_model* m, int32_t option, int64_t* value) {
     case FF_OPT_ACT_QUANT: *value = m->act_quant; return FF_OK;
     case FF_OPT_FUSED_MASK: *value = m->fused; return FF_OK;
     case FF_OPT_PDL_RR: *value = m->launch.pdl_rr ? 1 : 0; return FF_OK;
+    case FF_OPT_CLS_LAST_LAYER: *value = m->cls_last ? 1 : 0; return FF_OK;
     default: return fail(FF_E_INVALID, "unknown option");
   }
 }

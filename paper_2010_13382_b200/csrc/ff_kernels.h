@@ -92,6 +92,7 @@ struct GemmParams {
   // alternates so a kernel first reads the rows its producer wrote last,
   // i.e. the ones most likely still in L2)
   int rev;
+  int rs_stride;  // row_scale[m * rs_stride] (1; S when A holds every S-th token row)
 };
 
 struct GemmPlan {
@@ -151,6 +152,7 @@ struct RRParams {
   float* out_scale;        // [M] or null
   unsigned long long* trace;  // debug timeline (ff_debug_set_trace), null in production
   int rev;                    // 1: row tiles walked last to first (see GemmParams::rev)
+  int rs_stride;              // row_scale[m * rs_stride]
 };
 struct RRPlan {
   CUtensorMap tmA, tmB, tmC;
@@ -165,6 +167,11 @@ bool plan_rr(RRPlan* g, bool i8, const void* A, int M_rows, int lda, const void*
 void plan_rr_set_m(RRPlan* g, int M);
 // Bind the residual (RR_LN) and s8 output buffers (either may be null) of a plan.
 bool plan_rr_io(RRPlan* g, const void* residual, int ldr, void* outq, int ldq, const char** err);
+// Re-encode the row-indexed input maps of a plan for M_rows rows at pitch lda
+// (elements) -- e.g. the first token of each sequence (lda = S x the row
+// pitch); the residual map of an RR_LN plan too when residual != null.
+bool rebind_gemm_rows(GemmPlan* g, const void* A, int lda, int M_rows, const char** err);
+bool rebind_rr_rows(RRPlan* g, const void* A, int lda, const void* residual, int ldr, int M_rows, const char** err);
 cudaError_t launch_rr(const RRPlan& g, cudaStream_t s);
 cudaError_t prepare_rr_kernels();
 
@@ -191,7 +198,8 @@ cudaError_t launch_quant_rows(const __half* x, int ldx, int M, int K, int8_t* q,
 // pooled = tanh(Wp x0 + bp); logits = Wc pooled + bc, x0 = row b*S of x16.
 // part: fp32 scratch of at least B x S x H floats (split-K partials).
 cudaError_t launch_head(const __half* x16, int ldx, int B, int S, int H, int C, const float* Wp, const float* bp,
-                        const float* Wc, const float* bc, float* part, float* logits, cudaStream_t s);
+                        const float* Wc, const float* bc, float* part, float* logits, cudaStream_t s,
+                        int seq_stride = -1);
 
 // ------------------------------------------------------------- attention
 size_t attention_smem_bytes(int S, int d);

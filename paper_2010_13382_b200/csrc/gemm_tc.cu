@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row0 = mt * TM + (int)rank * BM + q * 32;
       const int row = row0 + lane;
       float sx = 0.0f;
-      if (I8 && p.out_mode == 1 && row < p.M) sx = PT ? p.tensor_qp[0] : p.row_scale[row];
+      if (I8 && p.out_mode == 1 && row < p.M) sx = PT ? p.tensor_qp[0] : p.row_scale[(size_t)row * p.rs_stride];
       const int zp = (PT && p.out_mode == 1) ? (int)p.tensor_qp[1] : 0;
       // this tile's bias / column scales -> smem (double-buffered by acc; the
       // barrier of tile t+1 orders every warp's reads of tile t before the
@@ -796,7 +796,7 @@ __global__ void __launch_bounds__(kRRThreads, 1)
       const int row0 = (p.rev ? p.m_tiles - 1 - mt : mt) * BM + q * 32;
       const int row = row0 + lane;
       const bool row_ok = row < p.M;
-      const float sx = (I8 && row_ok) ? p.row_scale[row] : 0.0f;
+      const float sx = (I8 && row_ok) ? p.row_scale[(size_t)row * p.rs_stride] : 0.0f;
       const float2 sx2 = make_float2(sx, sx);
       if (MODE == RR_LN) {
         // residual of this group's NEXT tile -> L2 (its TMA loads then hit
@@ -1084,6 +1084,7 @@ bool plan_gemm(GemmPlan* g, bool i8, const void* A, int M_rows, int lda, const v
   g->p.colsum = nullptr;
   g->p.hm_rows = 0;
   g->p.rev = 0;
+  g->p.rs_stride = 1;
   plan_gemm_set_m(g, M_rows);
   return true;
 }
@@ -1106,6 +1107,7 @@ bool plan_gemm_output(GemmPlan* g, void* out, int ldo, const char** err) {
   g->p.ldo = ldo;
   g->p.hm_rows = 0;
   g->p.rev = 0;
+  g->p.rs_stride = 1;
   g->has_out_map = true;
   return encode_2d(&g->tmC, out, g->M_rows, g->p.N, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (size_t)ldo * 2, kEpiCols,
                    32, CU_TENSOR_MAP_SWIZZLE_64B, err);
@@ -1191,11 +1193,30 @@ bool plan_rr(RRPlan* g, bool i8, const void* A, int M_rows, int lda, const void*
     return false;
   RRParams& p = g->p;
   p = RRParams{};
+  p.rs_stride = 1;
   p.N = N;
   p.K = K;
   p.k_blocks = (K * eb + BK_BYTES - 1) / BK_BYTES;
   p.act = ACT_NONE;
   plan_rr_set_m(g, M_rows);
+  return true;
+}
+
+bool rebind_gemm_rows(GemmPlan* g, const void* A, int lda, int M_rows, const char** err) {
+  const int eb = g->i8 ? 1 : 2;
+  if (!make_operand_map(&g->tmA, A, M_rows, g->p.K, eb, (size_t)lda * eb, BM, err)) return false;
+  g->M_rows = M_rows;
+  return true;
+}
+
+bool rebind_rr_rows(RRPlan* g, const void* A, int lda, const void* residual, int ldr, int M_rows, const char** err) {
+  const int eb = g->i8 ? 1 : 2;
+  if (!make_operand_map(&g->tmA, A, M_rows, g->p.K, eb, (size_t)lda * eb, BM, err)) return false;
+  if (residual != nullptr &&
+      !encode_2d(&g->tmR, const_cast<void*>(residual), M_rows, g->p.N, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                 (size_t)ldr * 2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B, err))
+    return false;
+  g->M_rows = M_rows;
   return true;
 }
 

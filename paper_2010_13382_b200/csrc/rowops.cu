@@ -604,14 +604,19 @@ cudaError_t launch_quant_rows(const __half* x, int ldx, int M, int K, int8_t* q,
 }
 
 cudaError_t launch_head(const __half* x16, int ldx, int B, int S, int H, int C, const float* Wp, const float* bp,
-                        const float* Wc, const float* bc, float* part, float* logits, cudaStream_t s) {
+                        const float* Wc, const float* bc, float* part, float* logits, cudaStream_t s,
+                        int seq_stride) {
+  // seq_stride: rows between consecutive sequences' first tokens (S; 1 when
+  // they are compact, FF_OPT_CLS_LAST_LAYER); the split-K geometry depends on
+  // S only, so both layouts sum in the same order
   // nks K slices of cps kPoolK-column chunks; part holds nks x B x H floats,
   // within the caller's B x S x H scratch (nks <= S)
   const int chunks = (H + kPoolK - 1) / kPoolK;
   const int cps = (chunks + min(chunks, S) - 1) / min(chunks, S);
   const int nks = (chunks + cps - 1) / cps;
   dim3 grid((H + kPoolT - 1) / kPoolT, (B + kPoolT - 1) / kPoolT, nks);
-  launch_ex(pooler_kernel, grid, dim3(256), kPoolSmem, s, 0, x16, ldx, B, S, H, Wp, cps, part);
+  launch_ex(pooler_kernel, grid, dim3(256), kPoolSmem, s, 0, x16, ldx, B, seq_stride < 0 ? S : seq_stride, H, Wp, cps,
+            part);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   launch_ex(head_kernel, dim3(B), dim3(kHeadThreads), 0, s, 0, (const float*)part, nks, B, H, C, bp, Wc, bc, logits);

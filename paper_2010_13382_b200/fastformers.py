@@ -28,6 +28,7 @@ FF_OPT_PDL = 5
 FF_OPT_ACT_QUANT = 6
 FF_OPT_FUSED_MASK = 8
 FF_OPT_PDL_RR = 9
+FF_OPT_CLS_LAST_LAYER = 13
 FF_SCORER_OPT_TC_LINEARS = 1  # ff_scorer_set_option
 KERNEL_KINDS = ["embed_ln", "gemm_f16", "gemm_i8", "attention", "quant_rows", "add_ln", "head", "gemm_rr_f16",
                 "gemm_rr_i8"]
@@ -142,7 +143,7 @@ class Encoder:
 
     def __init__(self, cfg, weights: Dict[str, np.ndarray], max_tokens: Optional[int] = None, device: int = 0,
                  use_graphs: bool = True, cta_pairs: bool = True, attn_tc: bool = True, fused=None,
-                 act_quant: int = 0):
+                 act_quant: int = 0, cls_last: bool = False):
         import torch
         L = lib()
         self.cfg = cfg
@@ -187,6 +188,9 @@ class Encoder:
         self.act_quant = act_quant
         if not cta_pairs:
             check(L.ff_set_option(self.h, FF_OPT_CTA_PAIRS, 0))
+        # FF_OPT_CLS_LAST_LAYER: last layer's row-local steps on the first tokens only
+        if cls_last:
+            check(L.ff_set_option(self.h, FF_OPT_CLS_LAST_LAYER, 1))
 
     def get_option(self, option: int) -> int:
         v = ctypes.c_int64()

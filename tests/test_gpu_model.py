@@ -349,6 +349,29 @@ def test_full_size_forward_deterministic_under_repetition(name):
         assert np.array_equal(got, ref), (k, float(np.abs(got - ref).max()))
 
 
+@pytest.mark.parametrize("name,fused", [("c1_i8", None), ("c1_i8", 0), ("c1_f16", None), ("c1_mixed", 7),
+                                        ("c3_i8", None), ("c3_f16", None), ("c3_i8", 0), ("c2_i8", None),
+                                        ("c4_f16", None), ("c3_full", None)])
+def test_cls_last_layer_logits_bit_identical(name, fused):
+    """FF_OPT_CLS_LAST_LAYER: the last layer's out-projection / LN / FFN run on
+    the first-token rows only (strided A / residual / row scales, compact
+    outputs); every step is row-local and the pooler reads only those rows, so
+    the logits must equal the default path bit for bit (ragged masks)."""
+    if name == "c3_full":  # BASELINE configs[2] at full size (B 256 x S 128)
+        cfg = synth.config("c3").with_dtype(1)
+        w = synth.make_weights(cfg)
+        ids, mask = synth.make_inputs(cfg, seed=5)
+    else:
+        cfg, w, ids, mask = build_case(name)
+    kw = {} if fused is None else {"fused": fused}
+    ref = f32(Encoder(cfg, w, **kw).encode(dev(ids), dev(mask)))
+    enc = Encoder(cfg, w, cls_last=True, **kw)
+    got = f32(enc.encode(dev(ids), dev(mask)))
+    assert np.array_equal(got, ref), float(np.abs(got - ref).max())
+    got2 = f32(enc.encode(dev(ids), dev(mask)))  # graph replay
+    assert np.array_equal(got2, ref)
+
+
 def test_input_errors_are_reported():
     cfg, w, ids, mask = build_case("c1_i8")
     enc = Encoder(cfg, w)
