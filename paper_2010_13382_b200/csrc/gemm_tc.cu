@@ -106,10 +106,13 @@ constexpr float kGeluClamp = 6.5f;
 
 // s * P(s) for one value: P7 when s <= 2.5, else P11 of min(s, 6.5).
 __device__ __forceinline__ float gelu_expo(float s) {
+  // (Horner starts from the leading coefficient: fma(0, s, c) is not folded
+  // by the compiler -- 0 * inf -- and would cost an instruction per value)
   float p7 = 0.0f, p11 = 0.0f;
+  bool f7 = true, f11 = true;
   const float sc = fminf(s, kGeluClamp);
-#define FF_H7(c) p7 = __fmaf_rn(p7, s, c);
-#define FF_H11(c) p11 = __fmaf_rn(p11, sc, c);
+#define FF_H7(c) p7 = f7 ? (c) : __fmaf_rn(p7, s, c); f7 = false;
+#define FF_H11(c) p11 = f11 ? (c) : __fmaf_rn(p11, sc, c); f11 = false;
   FF_GELU_P7(FF_H7)
   FF_GELU_P11(FF_H11)
 #undef FF_H7
@@ -157,7 +160,8 @@ __device__ __forceinline__ void gelu16x2(float2 (&v)[16]) {
   for (int e = 0; e < 16; ++e) {
     const float2 s = make_float2(fabsf(v[e].x), fabsf(v[e].y));
     float2 p = make_float2(0.0f, 0.0f);
-#define FF_H2(c) p = fma2(p, s, make_float2(c, c));
+    bool first = true;  // Horner from the leading coefficient (see gelu_expo)
+#define FF_H2(c) p = first ? make_float2(c, c) : fma2(p, s, make_float2(c, c)); first = false;
     FF_GELU_P7(FF_H2)
 #undef FF_H2
     const float2 a = mul2(s, p);
