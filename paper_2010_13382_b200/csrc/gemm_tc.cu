@@ -868,8 +868,8 @@ __global__ void __launch_bounds__(kRRThreads, 1)
             } else {
               y = add2(make_float2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])), bb);
             }
-            const float2 y16 = __half22float2(__floats2half2_rn(y.x, y.y));
-            const float2 x = add2(y16, __half22float2(rh[e]));
+            // x = R16(y) + residual: the fp16-rounded y added as fp16 (FHADD)
+            const float2 x = add_h2f(pack_half2(y.x, y.y), __half22float2(rh[e]));
             if (ch == 0 && e == 0) shift = make_float2(x.x, x.x);
             const float2 d = sub2(x, shift);
             sd = add2(sd, d);

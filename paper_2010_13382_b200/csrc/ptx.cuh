@@ -369,6 +369,17 @@ __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// float(lo / hi half of h2) + c.x / c.y in one mixed-precision add each (sm_100
+// add.rn.f32.f16 -> FHADD, the half selected in the operand): exact
+// conversion, one rounding -- the same value as FADD of the unpacked halves.
+__device__ __forceinline__ float2 add_h2f(uint32_t h2, float2 c) {
+  float2 d;
+  asm("{.reg .f16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\tadd.rn.f32.f16 %0, lo, %3;\n\tadd.rn.f32.f16 %1, hi, %4;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "r"(h2), "f"(c.x), "f"(c.y));
+  return d;
+}
+
 // Packed fp32 pair arithmetic (sm_100: FFMA2 / FADD2 / FMUL2, one issue slot
 // for two IEEE round-to-nearest operations).
 __device__ __forceinline__ uint64_t f2_bits(float2 a) { return *reinterpret_cast<const uint64_t*>(&a); }
