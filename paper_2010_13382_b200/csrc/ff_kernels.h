@@ -96,7 +96,7 @@ struct GemmParams {
 };
 
 struct GemmPlan {
-  CUtensorMap tmA, tmB, tmB2, tmC;  // A, W (BN / BN/2-row boxes, 128B swizzle); fp16 output (64B swizzle)
+  CUtensorMap tmA, tmB, tmB2, tmB3, tmC;  // A, W (256 / 128 / 64-row boxes, 128B swizzle); fp16 output
   GemmParams p;
   int bn;       // N tile (128 or 256)
   int i8;       // 1 = kind::i8

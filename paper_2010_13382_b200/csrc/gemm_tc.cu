@@ -1071,9 +1071,11 @@ bool plan_gemm(GemmPlan* g, bool i8, const void* A, int M_rows, int lda, const v
   g->has_out_map = false;
   g->force_pair = -1;
   if (!make_operand_map(&g->tmA, A, M_rows, K, eb, (size_t)lda * eb, BM, err)) return false;
-  // W boxes cover BN rows (single CTA) or BN/2 rows (each CTA of a pair): two maps.
-  if (!make_operand_map(&g->tmB, W, N, K, eb, (size_t)ldw * eb, g->bn, err)) return false;
-  if (!make_operand_map(&g->tmB2, W, N, K, eb, (size_t)ldw * eb, g->bn / 2, err)) return false;
+  // W boxes cover BN rows (single CTA) or BN/2 rows (each CTA of a pair), BN
+  // 256 or 128 chosen per M (plan_gemm_set_m): 256-, 128- and 64-row maps.
+  if (!make_operand_map(&g->tmB, W, N, K, eb, (size_t)ldw * eb, 256, err)) return false;
+  if (!make_operand_map(&g->tmB2, W, N, K, eb, (size_t)ldw * eb, 128, err)) return false;
+  if (!make_operand_map(&g->tmB3, W, N, K, eb, (size_t)ldw * eb, 64, err)) return false;
   g->p.N = N;
   g->p.K = K;
   g->p.n_tiles = (N + g->bn - 1) / g->bn;
@@ -1117,11 +1119,34 @@ bool plan_gemm_output(GemmPlan* g, void* out, int ldo, const char** err) {
                    32, CU_TENSOR_MAP_SWIZZLE_64B, err);
 }
 
+// Pair decision for a tile width: CTA pairs (256-row tiles) when there are
+// enough of them to fill the GPU.
+static bool use_pairs(const GemmPlan* g, int M, int bn) {
+  const int pair_tiles = ((M + 255) / 256) * ((g->p.N + bn - 1) / bn);
+  return g->force_pair == 1 || (g->force_pair < 0 && pair_tiles >= kNumSMs / 2);
+}
+
 void plan_gemm_set_m(GemmPlan* g, int M) {
   g->p.M = M;
-  // CTA pairs (M = 256 tiles) when there are enough tiles to fill the GPU.
-  const int pair_tiles = ((M + 255) / 256) * g->p.n_tiles;
-  g->pair = g->force_pair == 1 || (g->force_pair < 0 && pair_tiles >= kNumSMs / 2);
+  // Tile width: the fewer wasted columns (pick_bn), unless 128-column tiles
+  // give a shorter makespan for this M: rounds of the tile grid over the
+  // persistent CTAs (or pairs) x tile width, 128-column tiles charged 10% extra (their
+  // per-column cost measured 6-15% higher on C3).  Small batches (C2: M = 8192,
+  // N = 1200: 3 rounds of 256-column pair tiles vs 5 of 128) take the
+  // narrower tiles; the large shapes keep 256.
+  int bn = pick_bn(g->p.N);
+  if (bn == 256 && g->p.hm_rows == 0) {
+    auto cost = [&](int w) {
+      const bool pr = use_pairs(g, M, w);
+      const long tiles = (long)((M + (pr ? 255 : 127)) / (pr ? 256 : 128)) * ((g->p.N + w - 1) / w);
+      const long units = pr ? kNumSMs / 2 : kNumSMs;
+      return (double)((tiles + units - 1) / units) * w * (w == 128 ? 1.1 : 1.0);  // per-SM work per round: 128 x w
+    };
+    if (cost(128) < cost(256)) bn = 128;
+  }
+  g->bn = bn;
+  g->p.n_tiles = (g->p.N + bn - 1) / bn;
+  g->pair = use_pairs(g, M, bn);
   const int tm = g->pair ? 256 : BM;
   g->p.m_tiles = (M + tm - 1) / tm;
   const int tiles = g->p.m_tiles * g->p.n_tiles;
@@ -1156,14 +1181,21 @@ cudaError_t prepare_gemm_kernels() {
   return set_attr<128, false, true>();
 }
 
+// W map whose box is the rows one CTA loads per k-block: BN, or BN / 2 in a pair
+template <int BN, bool PAIR>
+static const CUtensorMap& wmap(const GemmPlan& g) {
+  constexpr int rows = PAIR ? BN / 2 : BN;
+  return rows == 256 ? g.tmB : rows == 128 ? g.tmB2 : g.tmB3;
+}
+
 template <int BN, bool I8, bool PAIR>
 static cudaError_t launch_t(const GemmPlan& g, cudaStream_t s) {
   if (g.grid <= 0) return cudaSuccess;
   if (I8 && g.p.tensor_qp != nullptr)
     return launch_ex(gemm_tc_kernel<BN, I8, PAIR, I8>, dim3(g.grid), dim3(kThreads), GemmCfg<BN, PAIR>::SMEM, s,
-                     PAIR ? 2 : 0, g.tmA, PAIR ? g.tmB2 : g.tmB, g.tmC, g.p);
+                     PAIR ? 2 : 0, g.tmA, wmap<BN, PAIR>(g), g.tmC, g.p);
   return launch_ex(gemm_tc_kernel<BN, I8, PAIR, false>, dim3(g.grid), dim3(kThreads), GemmCfg<BN, PAIR>::SMEM, s,
-                   PAIR ? 2 : 0, g.tmA, PAIR ? g.tmB2 : g.tmB, g.tmC, g.p);
+                   PAIR ? 2 : 0, g.tmA, wmap<BN, PAIR>(g), g.tmC, g.p);
 }
 
 cudaError_t launch_gemm(const GemmPlan& g, cudaStream_t s) {
