@@ -207,6 +207,14 @@ FF_API ff_status ff_check(ff_model *m, void *stream);
  * of the last layer disables it).  Off by default: the bench's headline runs
  * every row of every layer; this is reported as a variant. */
 #define FF_OPT_CLS_LAST_LAYER 13
+/* FF_OPT_ROW_DIRS (per model): row-tile walking direction per launch role,
+ * bits high to low QKV, attention, out-projection, FFN1, FFN2 (1 = last row
+ * tile first).  Results do not depend on it (every step is row-local; tested);
+ * it only decides which rows a kernel reads first -- a consumer walking
+ * opposite to its producer first reads the rows written last, the most likely
+ * to still be in L2.  Default 0b01010 (attention and FFN1 reversed; measured,
+ * DESIGN §6).  Value 0..31, else FF_E_INVALID. */
+#define FF_OPT_ROW_DIRS 14
 /* Set `option` to `value` on model m (invalidates its captured graphs).  Every
  * option is per model: the library holds no process-wide mutable state on the
  * launch path, so models may be driven from different host threads (one

@@ -112,6 +112,7 @@ struct ff_model {
                   // bit 0 out-proj + LN1, bit 1 FFN1 + requant, bit 2 FFN2 + LN2; -1 = auto
   int act_quant = 0;    // FF_OPT_ACT_QUANT: 0 per-row s8, 1 per-tensor u8 + zero point
   bool cls_last = false;  // FF_OPT_CLS_LAST_LAYER: last layer's row-local steps on the B first-token rows only
+  int row_dirs = 0b01010;  // FF_OPT_ROW_DIRS: row-tile direction per launch role (run_forward)
   ff::LaunchPolicy launch{true, false};  // FF_OPT_PDL / FF_OPT_PDL_RR of this model's forwards
   ff::AttnTCPlan tm_qkv;  // QKV buffer map for the tcgen05 attention
   // CUDA-graph cache of ff_encode, keyed by (batch, seq, ids, mask, logits);
@@ -425,7 +426,7 @@ ff_status run_forward(ff_model* m, const int32_t* ids, const int32_t* mask, int 
   // decreasing order.  Measured on C3 int8 (same-box A/B, every mask):
   // 0b01010 +1.1% over all-forward; 0b01000 +0.7%; alternating every launch
   // +0.3%.
-  constexpr int rmask = 0b01010;
+  const int rmask = m->row_dirs;
   int role = 0;
   int rdir = (rmask >> 4) & 1;
   for (int l = 0; l < c.num_layers; ++l) {
@@ -1057,6 +1058,12 @@ ff_status ff_set_option(ff_model* m, int32_t option, int64_t value) {
     drop_graphs(m);
     return FF_OK;
   }
+  if (option == FF_OPT_ROW_DIRS) {
+    if (value < 0 || value > 31) return fail(FF_E_INVALID, "FF_OPT_ROW_DIRS must be 0..31");
+    m->row_dirs = (int)value;
+    drop_graphs(m);
+    return FF_OK;
+  }
   return fail(FF_E_INVALID, "unknown option");
 }
 
@@ -1072,6 +1079,7 @@ ff_status ff_get_option(const ff_model* m, int32_t option, int64_t* value) {
     case FF_OPT_FUSED_MASK: *value = m->fused; return FF_OK;
     case FF_OPT_PDL_RR: *value = m->launch.pdl_rr ? 1 : 0; return FF_OK;
     case FF_OPT_CLS_LAST_LAYER: *value = m->cls_last ? 1 : 0; return FF_OK;
+    case FF_OPT_ROW_DIRS: *value = m->row_dirs; return FF_OK;
     default: return fail(FF_E_INVALID, "unknown option");
   }
 }

@@ -29,6 +29,7 @@ FF_OPT_ACT_QUANT = 6
 FF_OPT_FUSED_MASK = 8
 FF_OPT_PDL_RR = 9
 FF_OPT_CLS_LAST_LAYER = 13
+FF_OPT_ROW_DIRS = 14
 FF_SCORER_OPT_TC_LINEARS = 1  # ff_scorer_set_option
 KERNEL_KINDS = ["embed_ln", "gemm_f16", "gemm_i8", "attention", "quant_rows", "add_ln", "head", "gemm_rr_f16",
                 "gemm_rr_i8"]

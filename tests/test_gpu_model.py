@@ -372,6 +372,27 @@ def test_cls_last_layer_logits_bit_identical(name, fused):
     assert np.array_equal(got2, ref)
 
 
+@pytest.mark.parametrize("name", ["c1_i8", "c3_full", "c3_f16"])
+def test_row_tile_directions_do_not_change_results(name):
+    """FF_OPT_ROW_DIRS only changes the order in which the GEMM / attention
+    kernels walk their row tiles (L2 locality): every direction mask gives the
+    same logits bit for bit (both directions of every kernel role run)."""
+    if name == "c3_full":
+        cfg = synth.config("c3").with_dtype(1)
+        w = synth.make_weights(cfg)
+        ids, mask = synth.make_inputs(cfg, seed=9)
+    else:
+        cfg, w, ids, mask = build_case(name)
+    enc = Encoder(cfg, w)
+    assert enc.get_option(ffb.FF_OPT_ROW_DIRS) == 0b01010
+    ref = f32(enc.encode(dev(ids), dev(mask)))
+    for dirs in (0, 31, 0b10101, 0b01010):
+        ffb.check(ffb.lib().ff_set_option(enc.h, ffb.FF_OPT_ROW_DIRS, dirs))
+        got = f32(enc.encode(dev(ids), dev(mask)))
+        assert np.array_equal(got, ref), (dirs, float(np.abs(got - ref).max()))
+    assert ffb.lib().ff_set_option(enc.h, ffb.FF_OPT_ROW_DIRS, 32) != ffb.FF_OK
+
+
 def test_input_errors_are_reported():
     cfg, w, ids, mask = build_case("c1_i8")
     enc = Encoder(cfg, w)
