@@ -555,6 +555,13 @@ constexpr int kRRStages = 3;
 #endif
 constexpr uint32_t kRRSleepNs = FF_RR_SLEEP_NS;  // epilogue group's probe interval while its accumulator is computed
 constexpr int kRRBN = 256;
+// PARK (RR_LN): the LN output row is parked in registers instead of TMEM, so
+// the accumulator returns to the MMA warp before the amax exchange and the
+// requant; warpgroup 0 hands registers to the epilogue (setmaxnreg).
+constexpr uint32_t kRRRegsCtl = 40;
+constexpr uint32_t kRRRegsEpi = 104;  // 128 x 40 + 512 x 104 <= 640 x 96
+static_assert(128 * kRRRegsCtl + 32 * kRREpiWarps * kRRRegsEpi <= kRRThreads * 96, "register pool");
+constexpr int kRRParkKBlocks = 8;
 constexpr int kRRMaxCN = 8;
 constexpr int kRRGroupWarps = kRREpiWarps / 2;  // 8 warps per ping-pong group
 struct RRCfg {
@@ -571,7 +578,7 @@ struct RRCfg {
   static_assert(SMEM <= 227 * 1024, "smem budget");
 };
 
-template <bool I8, int MODE>
+template <bool I8, int MODE, bool PARK = false>
 __global__ void __launch_bounds__(kRRThreads, 1)
     gemm_rr_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmR,
@@ -626,7 +633,9 @@ __global__ void __launch_bounds__(kRRThreads, 1)
   griddep_launch();
   constexpr int KE = I8 ? 128 : 64;
 
-  if (warp == 0) {
+  if (warp < 4) {
+    if constexpr (PARK) regs_dec<kRRRegsCtl>();
+    if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
@@ -643,7 +652,7 @@ __global__ void __launch_bounds__(kRRThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
+    } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = make_idesc<I8, BM, BN>();
       int stage = 0;
@@ -681,7 +690,9 @@ __global__ void __launch_bounds__(kRRThreads, 1)
         }
       }
     }
-  } else if (warp >= 4) {
+    }
+  } else {
+    if constexpr (PARK) regs_inc<kRRRegsEpi>();
     const int ew = warp - 4;
     const int G = ew / kRRGroupWarps;          // ping-pong group: accumulator buffer G, local tiles lt % 2 == G
     const int q = warp & 3;                    // TMEM lane quadrant: rows [32q, 32q+32)
@@ -831,6 +842,7 @@ __global__ void __launch_bounds__(kRRThreads, 1)
       // The packed fp16 results of chunk ch are parked in the group's own
       // accumulator columns [16 ch, 16 ch + 16) of the warp's range, which
       // chunk 0 has already been read from.
+      uint32_t hp[PARK ? 4 : 1][16];  // PARK: the LN output row (fp16 pairs)
       if (MODE == RR_LN) {
         // pass 1: x = R16(dequant + bias) + residual (written back over the
         // accumulator); shifted sums (shift = the thread's first x) for the
@@ -891,6 +903,30 @@ __global__ void __launch_bounds__(kRRThreads, 1)
         const float rstd = 1.0f / sqrtf(var + p.eps);
         const float2 mean2 = make_float2(mean, mean), rstd2 = make_float2(rstd, rstd);
         // pass 2: y16 = R16((x - mean) * rstd * gamma + beta) -> fp16 store, amax, park
+        if constexpr (PARK) {
+#pragma unroll
+          for (int hh = 0; hh < 8; ++hh) {  // 16-column pieces (register budget)
+            uint32_t r[16];
+            tmem_ld16(tbase + hh * 16, r);
+            tmem_wait_ld();
+            const float* pg = pgam + hh * 16;
+            const float* pt = pbet + hh * 16;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float2 d = sub2(make_float2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])), mean2);
+              const float2 y = fma2(mul2(d, rstd2), *reinterpret_cast<const float2*>(pg + 2 * e),
+                                    *reinterpret_cast<const float2*>(pt + 2 * e));
+              const __half2 hh2 = __floats2half2_rn(y.x, y.y);
+              amax2 = __hmax2(amax2, __habs2(hh2));
+              hp[hh >> 1][(hh & 1) * 8 + e] = *reinterpret_cast<const uint32_t*>(&hh2);
+            }
+            if ((hh & 1) && p.store16) store16(hp[hh >> 1], ncol0 + c_lo + (hh >> 1) * 32, row0);
+          }
+          // every TMEM read of this tile is complete: release the accumulator
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        } else {
 #pragma unroll 1
         for (int ch = 0; ch < 4; ++ch) {
           uint32_t r[32];
@@ -910,6 +946,7 @@ __global__ void __launch_bounds__(kRRThreads, 1)
           }
           if (p.outq) tmem_st16(tbase + ch * 16, h);
           if (p.store16) store16(h, ncol0 + c_lo + ch * 32, row0);
+        }
         }
       } else {  // RR_QUANT: y16 = R16(act(dequant + bias)); amax; park
 #pragma unroll 1
@@ -935,11 +972,11 @@ __global__ void __launch_bounds__(kRRThreads, 1)
 
       if (tr0) gemm_trace(p.trace, lt, 10);
       if (p.outq) {
-        tmem_wait_st();
+        if constexpr (!PARK) tmem_wait_st();
         // the parked values of chunk 0 are read while the row amax is exchanged
         // (they do not depend on it); chunk ch + 1 is read during chunk ch
         uint32_t hv[2][16];
-        tmem_ld16(tbase, hv[0]);
+        if constexpr (!PARK) tmem_ld16(tbase, hv[0]);
         // Q8row over the whole row (R6-R8, R12) from the fp16-rounded values
         float rmax, unused;
         exchange(fmaxf(__low2float(amax2), __high2float(amax2)), 0.0f, false, rmax, unused);
@@ -948,12 +985,17 @@ __global__ void __launch_bounds__(kRRThreads, 1)
         const float rs = __frcp_rn(sc);
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) {
-          tmem_wait_ld();
-          if (ch < 3) tmem_ld16(tbase + (ch + 1) * 16, hv[(ch + 1) & 1]);
-          if (ch == 3) {  // the group's accumulator buffer has been read for the last time
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+          if constexpr (PARK) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) hv[ch & 1][e] = hp[ch][e];
+          } else {
+            tmem_wait_ld();
+            if (ch < 3) tmem_ld16(tbase + (ch + 1) * 16, hv[(ch + 1) & 1]);
+            if (ch == 3) {  // the group's accumulator buffer has been read for the last time
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&tempty[acc]);
+            }
           }
           uint32_t o[8];
 #pragma unroll
@@ -983,7 +1025,7 @@ __global__ void __launch_bounds__(kRRThreads, 1)
           if (tr0 && ch < 2) gemm_trace(p.trace, lt, 12 + ch);
         }
         if (rank == 0 && hc == 0 && row_ok) p.out_scale[row] = sc;
-      } else {
+      } else if (!PARK || MODE != RR_LN) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -1309,30 +1351,42 @@ void plan_rr_set_m(RRPlan* g, int M) {
   g->grid = nc * g->cn;
 }
 
-template <bool I8, int MODE>
+template <bool I8, int MODE, bool PARK = false>
 static cudaError_t launch_rr_t(const RRPlan& g, cudaStream_t s) {
   // LN-mode row-reduction GEMMs launch without PDL unless FF_OPT_PDL_RR (measured)
   const bool pdl = tl_launch.pdl && (MODE != RR_LN || tl_launch.pdl_rr);
-  return launch_ex_pdl(pdl, gemm_rr_kernel<I8, MODE>, dim3(g.grid), dim3(kRRThreads), RRCfg::SMEM, s, g.cn, g.tmA,
-                       g.tmB, g.tmC, g.tmR, g.tmQ, g.p);
+  return launch_ex_pdl(pdl, gemm_rr_kernel<I8, MODE, PARK>, dim3(g.grid), dim3(kRRThreads), RRCfg::SMEM, s, g.cn,
+                       g.tmA, g.tmB, g.tmC, g.tmR, g.tmQ, g.p);
 }
 
-template <bool I8, int MODE>
+template <bool I8, int MODE, bool PARK = false>
 static cudaError_t set_rr_attr() {
-  return cudaFuncSetAttribute(gemm_rr_kernel<I8, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, RRCfg::SMEM);
+  return cudaFuncSetAttribute(gemm_rr_kernel<I8, MODE, PARK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              RRCfg::SMEM);
 }
 
 cudaError_t prepare_rr_kernels() {
   cudaError_t e;
   if ((e = set_rr_attr<true, RR_LN>()) != cudaSuccess) return e;
   if ((e = set_rr_attr<false, RR_LN>()) != cudaSuccess) return e;
+  if ((e = set_rr_attr<true, RR_LN, true>()) != cudaSuccess) return e;
+  if ((e = set_rr_attr<false, RR_LN, true>()) != cudaSuccess) return e;
   if ((e = set_rr_attr<true, RR_QUANT>()) != cudaSuccess) return e;
   return set_rr_attr<false, RR_QUANT>();
 }
 
 cudaError_t launch_rr(const RRPlan& g, cudaStream_t s) {
   if (g.grid <= 0) return cudaSuccess;
-  if (g.p.mode == RR_LN) return g.i8 ? launch_rr_t<true, RR_LN>(g, s) : launch_rr_t<false, RR_LN>(g, s);
+  // LN launches with long K rows (>= kRRParkKBlocks k-blocks: FFN2) take the
+  // register-parked variant -- their MMA would otherwise wait for the whole
+  // epilogue of the tile holding its accumulator; the short-K out-projection
+  // is bound by epilogue throughput and keeps TMEM parking (same-box A/B:
+  // FFN2 parked +0.9% on the C3 step, out-proj parked -1.2%)
+  if (g.p.mode == RR_LN) {
+    if (g.p.k_blocks >= kRRParkKBlocks)
+      return g.i8 ? launch_rr_t<true, RR_LN, true>(g, s) : launch_rr_t<false, RR_LN, true>(g, s);
+    return g.i8 ? launch_rr_t<true, RR_LN>(g, s) : launch_rr_t<false, RR_LN>(g, s);
+  }
   return g.i8 ? launch_rr_t<true, RR_QUANT>(g, s) : launch_rr_t<false, RR_QUANT>(g, s);
 }
 
