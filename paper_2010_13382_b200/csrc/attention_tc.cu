@@ -36,7 +36,6 @@ namespace {
 
 constexpr int kQ = 128;             // queries per item (TMEM lanes)
 constexpr int kKeys = 128;          // keys (S <= 128)
-constexpr int kD = 64;              // columns of a Q / K / V head tile (TMA box, 128B swizzle)
 // DP = head_dim padded to the MMA granularity: 64 (d in (32, 64]) or 32
 // (d <= 32, e.g. the TinyBERT shape's d = 26, DESIGN R18); an item holds up
 // to 512 / DP heads (their packed fp16 ctx fills the 256 parking columns).

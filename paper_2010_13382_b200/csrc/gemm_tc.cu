@@ -571,8 +571,7 @@ struct RRCfg {
   static constexpr int EPI_OFF = kRRStages * STAGE_BYTES;                 // staging [warp] 2 KB
   static constexpr int PAR_OFF = EPI_OFF + kRREpiWarps * kRRStageTile;    // [bias|sw|gamma|beta][256] fp32
   static constexpr int LOC_OFF = PAR_OFF + 4 * kRRBN * 4;                 // [G 2][par 2][hc 2][q 4][v 2][32] fp32
-  static constexpr int MYP_OFF = LOC_OFF + 2 * 2 * 2 * 4 * 2 * 32 * 4;    // [b 4][q 4][v 2][32] fp32
-  static constexpr int RED_OFF = MYP_OFF + 4 * 4 * 2 * 32 * 4;            // [b 4][rank 8][q 4][v 2][32] fp32
+  static constexpr int RED_OFF = LOC_OFF + 2 * 2 * 2 * 4 * 2 * 32 * 4;    // [b 4][rank 8][q 4][v 2][32] fp32
   static constexpr int BAR_OFF = RED_OFF + 4 * kRRMaxCN * 4 * 2 * 32 * 4;
   static constexpr int SMEM = BAR_OFF + 512 + 1024;
   static_assert(SMEM <= 227 * 1024, "smem budget");
@@ -701,7 +700,6 @@ __global__ void __launch_bounds__(kRRThreads, 1)
     const int ncol0 = (int)rank * BN;
     float* par = reinterpret_cast<float*>(smem + RRCfg::PAR_OFF);
     float* loc = reinterpret_cast<float*>(smem + RRCfg::LOC_OFF);
-    float* myp = reinterpret_cast<float*>(smem + RRCfg::MYP_OFF);
     float* red = reinterpret_cast<float*>(smem + RRCfg::RED_OFF);
     uint8_t* stage_buf = smem + RRCfg::EPI_OFF + ew * kRRStageTile;
     // this CTA's column parameters, once: bias, column scale, gamma, beta
